@@ -1,0 +1,232 @@
+// K1 preprocess_fwd: one thread per Gaussian.
+// activate_scales/opacity, rotation_from_quaternion (:59-67),
+// build_covariance3d (:69-77), project_mean (:132-140), project_covariance
+// (:142-150), invert_cov2d (:152-160), eval_sh (:79-87), bound_rect (:214-222)
+// and the exact-cull COUNT pass (:224-232).  HBM-bound: reads 44 B + 12*D B of
+// parameters, writes a 48 B splat row + 8 B rect + 4 B count + 4 B depth key.
+#include "ts_internal.cuh"
+#include "ts_math.cuh"
+
+namespace ts {
+namespace {
+
+constexpr int kBlock = 128;
+
+__global__ void __launch_bounds__(kBlock) preprocess_kernel(
+    const float* __restrict__ P, int64_t N, DevCam cam, ts_render_config cfg, float4* __restrict__ splat,
+    uint2* __restrict__ rect, uint32_t* __restrict__ tcount, uint32_t* __restrict__ dkey,
+    uint32_t* __restrict__ dperm, uint32_t* __restrict__ vis_counter) {
+    using namespace tsx;
+    __shared__ float sh_rest[kBlock * 45];
+    const Off off(N);
+    const int64_t g0 = int64_t(blockIdx.x) * kBlock;
+    const int64_t g = g0 + threadIdx.x;
+    const int deg = cfg.sh_degree;
+    const int nb = (deg + 1) * (deg + 1);
+    const int nrest = 3 * (nb - 1);
+    // cooperative, coalesced staging of the used SH prefix of each 45-float row
+    if (nrest > 0) {
+        const int64_t rows = tmin<int64_t>(kBlock, N - g0);
+        const float* src = P + off.rest + g0 * 45;
+        for (int i = threadIdx.x; i < rows * nrest; i += kBlock) {
+            int r = i / nrest, cc = i - r * nrest;
+            sh_rest[r * 45 + cc] = __ldg(src + int64_t(r) * 45 + cc);
+        }
+    }
+    __syncthreads();
+    if (g >= N) return;
+
+    float4 s0 = make_float4(0.f, 0.f, 0.f, 0.f), s1 = s0, s2 = s0;
+    uint32_t cnt = 0;
+    uint2 rc = make_uint2(1u, 1u);  // empty: tx0=1 > tx1=0
+    bool ok = false;
+    float zh = 0.f;
+    do {
+        const float* W = cam.W;
+        const float m0 = P[off.means + 3 * g], m1 = P[off.means + 3 * g + 1], m2 = P[off.means + 3 * g + 2];
+        // project_mean, fixed order (depth feeds the sort key)
+        const float xh = add(add(add(mul(W[0], m0), mul(W[1], m1)), mul(W[2], m2)), W[3]);
+        const float yh = add(add(add(mul(W[4], m0), mul(W[5], m1)), mul(W[6], m2)), W[7]);
+        zh = add(add(add(mul(W[8], m0), mul(W[9], m1)), mul(W[10], m2)), W[11]);
+        if (!(zh > cam.nearp)) break;
+        const float4 qv = make_float4(P[off.q + 4 * g], P[off.q + 4 * g + 1], P[off.q + 4 * g + 2], P[off.q + 4 * g + 3]);
+        const float qq = add(add(add(mul(qv.x, qv.x), mul(qv.y, qv.y)), mul(qv.z, qv.z)), mul(qv.w, qv.w));
+        const float qn = sqrt_(qq);
+        if (!(qn >= 1e-4f)) break;
+        const float w = div(qv.x, qn), x = div(qv.y, qn), y = div(qv.z, qn), z = div(qv.w, qn);
+        float R[9];
+        {
+            const float xx = mul(x, x), yy = mul(y, y), zz = mul(z, z), xy = mul(x, y), xz = mul(x, z),
+                        yz = mul(y, z), wx = mul(w, x), wy = mul(w, y), wz = mul(w, z);
+            R[0] = sub(1.f, mul(2.f, add(yy, zz)));
+            R[1] = mul(2.f, sub(xy, wz));
+            R[2] = mul(2.f, add(xz, wy));
+            R[3] = mul(2.f, add(xy, wz));
+            R[4] = sub(1.f, mul(2.f, add(xx, zz)));
+            R[5] = mul(2.f, sub(yz, wx));
+            R[6] = mul(2.f, sub(xz, wy));
+            R[7] = mul(2.f, add(yz, wx));
+            R[8] = sub(1.f, mul(2.f, add(xx, yy)));
+        }
+        float sc[3];
+        sc[0] = expf_det(P[off.ls + 3 * g]);
+        sc[1] = expf_det(P[off.ls + 3 * g + 1]);
+        sc[2] = expf_det(P[off.ls + 3 * g + 2]);
+        float Mm[9];
+#pragma unroll
+        for (int i = 0; i < 3; ++i)
+#pragma unroll
+            for (int k = 0; k < 3; ++k) Mm[3 * i + k] = mul(R[3 * i + k], sc[k]);
+        auto sdot = [&](int i, int j) {
+            return add(add(mul(Mm[3 * i], Mm[3 * j]), mul(Mm[3 * i + 1], Mm[3 * j + 1])),
+                       mul(Mm[3 * i + 2], Mm[3 * j + 2]));
+        };
+        const float S00 = sdot(0, 0), S01 = sdot(0, 1), S02 = sdot(0, 2), S11 = sdot(1, 1), S12 = sdot(1, 2),
+                    S22 = sdot(2, 2);
+        // project_covariance with clamped ratios
+        const float limx = mul(1.3f, div(mul(0.5f, float(cam.w)), cam.fx));
+        const float limy = mul(1.3f, div(mul(0.5f, float(cam.h)), cam.fy));
+        const float txz = div(xh, zh), tyz = div(yh, zh);
+        const float ux = txz < -limx ? -limx : (txz > limx ? limx : txz);
+        const float uy = tyz < -limy ? -limy : (tyz > limy ? limy : tyz);
+        const float tx = mul(ux, zh), ty = mul(uy, zh);
+        const float zz2 = mul(zh, zh);
+        const float J00 = div(cam.fx, zh), J02 = div(-mul(cam.fx, tx), zz2);
+        const float J11 = div(cam.fy, zh), J12 = div(-mul(cam.fy, ty), zz2);
+        float Tm[6];
+#pragma unroll
+        for (int j = 0; j < 3; ++j) {
+            Tm[j] = add(mul(J00, W[j]), mul(J02, W[8 + j]));
+            Tm[3 + j] = add(mul(J11, W[4 + j]), mul(J12, W[8 + j]));
+        }
+        const float Sf[9] = {S00, S01, S02, S01, S11, S12, S02, S12, S22};
+        float U[6];
+#pragma unroll
+        for (int i = 0; i < 2; ++i)
+#pragma unroll
+            for (int j = 0; j < 3; ++j)
+                U[3 * i + j] =
+                    add(add(mul(Tm[3 * i], Sf[j]), mul(Tm[3 * i + 1], Sf[3 + j])), mul(Tm[3 * i + 2], Sf[6 + j]));
+        float a = add(add(mul(U[0], Tm[0]), mul(U[1], Tm[1])), mul(U[2], Tm[2]));
+        const float b = add(add(mul(U[0], Tm[3]), mul(U[1], Tm[4])), mul(U[2], Tm[5]));
+        float c = add(add(mul(U[3], Tm[3]), mul(U[4], Tm[4])), mul(U[5], Tm[5]));
+        // invert_cov2d with dilation
+        a = add(a, cfg.dilation);
+        c = add(c, cfg.dilation);
+        const float det = sub(mul(a, c), mul(b, b));
+        if (!(det >= 1e-6f)) break;
+        const float A = div(c, det), B = div(-b, det), C = div(a, det);
+        const float mx = add(mul(cam.fx, txz), cam.cx), my = add(mul(cam.fy, tyz), cam.cy);
+        // activate_opacity; alpha level set Q <= k2  <=>  o exp(-Q/2) >= tau
+        const float logit = P[off.op + g];
+        const float o = div(1.f, add(1.f, expf_det(-logit)));
+        const float tau = cfg.tau_alpha;
+        const bool has_bound = o > tau;
+        const float k2 = has_bound ? mul(-2.f, logf_det(div(tau, o))) : 0.f;
+        ok = true;
+
+        // ---- eval_sh (colour tolerance path: contraction allowed) ----
+        const float cpx = -((W[0] * W[3] + W[4] * W[7]) + W[8] * W[11]);
+        const float cpy = -((W[1] * W[3] + W[5] * W[7]) + W[9] * W[11]);
+        const float cpz = -((W[2] * W[3] + W[6] * W[7]) + W[10] * W[11]);
+        float d0 = m0 - cpx, d1 = m1 - cpy, d2 = m2 - cpz;
+        const float il = rsqrtf(d0 * d0 + d1 * d1 + d2 * d2);
+        d0 *= il;
+        d1 *= il;
+        d2 *= il;
+        float Y[16];
+        Y[0] = TS_SH_C0;
+        if (deg >= 1) {
+            Y[1] = -TS_SH_C1 * d1;
+            Y[2] = TS_SH_C1 * d2;
+            Y[3] = -TS_SH_C1 * d0;
+        }
+        if (deg >= 2) {
+            const float xx = d0 * d0, yy = d1 * d1, zz = d2 * d2;
+            Y[4] = TS_SH_C2_0 * d0 * d1;
+            Y[5] = TS_SH_C2_1 * d1 * d2;
+            Y[6] = TS_SH_C2_2 * (2.f * zz - xx - yy);
+            Y[7] = TS_SH_C2_3 * d0 * d2;
+            Y[8] = TS_SH_C2_4 * (xx - yy);
+            if (deg >= 3) {
+                Y[9] = TS_SH_C3_0 * d1 * (3.f * xx - yy);
+                Y[10] = TS_SH_C3_1 * d0 * d1 * d2;
+                Y[11] = TS_SH_C3_2 * d1 * (4.f * zz - xx - yy);
+                Y[12] = TS_SH_C3_3 * d2 * (2.f * zz - 3.f * xx - 3.f * yy);
+                Y[13] = TS_SH_C3_4 * d0 * (4.f * zz - xx - yy);
+                Y[14] = TS_SH_C3_5 * d2 * (xx - yy);
+                Y[15] = TS_SH_C3_6 * d0 * (xx - 3.f * yy);
+            }
+        }
+        float rgb[3];
+        const float* rs = sh_rest + threadIdx.x * 45;
+#pragma unroll
+        for (int ch = 0; ch < 3; ++ch) {
+            float acc = Y[0] * P[off.dc + 3 * g + ch];
+            for (int k = 1; k < nb; ++k) acc += Y[k] * rs[3 * (k - 1) + ch];
+            acc += 0.5f;
+            rgb[ch] = acc < 0.f ? 0.f : acc;
+        }
+        s0 = make_float4(mx, my, k2, o);
+        s1 = make_float4(A, B, C, zh);
+        s2 = make_float4(rgb[0], rgb[1], rgb[2], det);
+        if (!has_bound) break;
+
+        // ---- bound (opacity-aware rect / rect / square) -> inclusive tile rect ----
+        float rx, ry;
+        if (cfg.bound_mode == 0) {
+            const float mid = mul(0.5f, add(a, c));
+            const float disc = sub(mul(mid, mid), det);
+            const float lam = add(mid, sqrt_(disc > 0.f ? disc : 0.f));
+            rx = ry = mul(3.f, sqrt_(lam));
+        } else {
+            const float kk = sqrt_(cfg.bound_mode == 1 ? mul(-2.f, logf_det(tau)) : k2);
+            rx = mul(kk, sqrt_(a));
+            ry = mul(kk, sqrt_(c));
+        }
+        const float wm1 = float(cam.w - 1), hm1 = float(cam.h - 1);
+        float lox = sub(mx, rx), hix = add(mx, rx), loy = sub(my, ry), hiy = add(my, ry);
+        lox = lox < 0.f ? 0.f : lox;
+        hix = hix > wm1 ? wm1 : hix;
+        loy = loy < 0.f ? 0.f : loy;
+        hiy = hiy > hm1 ? hm1 : hiy;
+        if (!(lox <= hix) || !(loy <= hiy)) break;
+        const int px0 = int(ceilf(lox)), px1 = int(floorf(hix));
+        const int py0 = int(ceilf(loy)), py1 = int(floorf(hiy));
+        if (px0 > px1 || py0 > py1) break;
+        const int tx0 = px0 >> 4, tx1 = px1 >> 4, ty0 = py0 >> 4, ty1 = py1 >> 4;
+        rc = make_uint2(uint32_t(tx0) | (uint32_t(tx1) << 16), uint32_t(ty0) | (uint32_t(ty1) << 16));
+        if (cfg.cull_mode == 0) {
+            cnt = uint32_t((tx1 - tx0 + 1) * (ty1 - ty0 + 1));
+        } else {
+            for (int tyy = ty0; tyy <= ty1; ++tyy)
+                for (int txx = tx0; txx <= tx1; ++txx)
+                    cnt += tile_keep(mx, my, A, B, C, k2, txx, tyy, cam.w, cam.h) ? 1u : 0u;
+        }
+    } while (false);
+    (void)ok;
+    splat[3 * g] = s0;
+    splat[3 * g + 1] = s1;
+    splat[3 * g + 2] = s2;
+    rect[g] = rc;
+    tcount[g] = cnt;
+    dkey[g] = cnt ? (__float_as_uint(zh) ^ 0x80000000u) : 0xFFFFFFFFu;
+    dperm[g] = uint32_t(g);
+    // warp-aggregated visible counter (bench V)
+    const unsigned am = __activemask();
+    const unsigned vis = __ballot_sync(am, cnt != 0);
+    if ((threadIdx.x & 31) == __ffs(am) - 1 && vis) atomicAdd(vis_counter, __popc(vis));
+}
+
+}  // namespace
+
+void launch_preprocess(Context& c, const DevCam& cam, const ts_render_config& cfg) {
+    if (c.N == 0) return;
+    const int64_t blocks = (c.N + kBlock - 1) / kBlock;
+    preprocess_kernel<<<unsigned(blocks), kBlock, 0, c.stream>>>(c.params.p, c.N, cam, cfg, c.splat.p, c.rect.p,
+                                                                  c.tcount.p, c.dkey[0].p, c.dperm[0].p,
+                                                                  c.counters.p + 1);
+    TS_LAUNCHED(c);
+}
+
+}  // namespace ts

@@ -1,0 +1,750 @@
+// ts_capi.cu — C-ABI entry points (include/tilesplat_c.h) and the host runtime:
+// context, grow-only device buffers, the per-view pipeline and stage timing.
+// Every entry point is noexcept-by-construction (no C++ exceptions cross the
+// ABI) and maps CUDA failures to TS_ERR_CUDA with ts_last_error() text.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <vector>
+
+#include "ts_internal.cuh"
+
+using namespace ts;
+
+struct ts_ctx {
+    Context c;
+};
+
+namespace ts {
+
+template <class T>
+bool ensure(Context& c, DevBuf<T>& b, size_t n, bool keep) {
+    if (n <= b.cap && b.p) return true;
+    size_t cap = std::max<size_t>(n, 1);
+    T* p = nullptr;
+    if (cudaMalloc(&p, cap * sizeof(T)) != cudaSuccess) {
+        cudaGetLastError();
+        c.err = "cudaMalloc failed (" + std::to_string(cap * sizeof(T)) + " bytes)";
+        return false;
+    }
+    if (keep && b.p && b.cap) cudaMemcpyAsync(p, b.p, b.cap * sizeof(T), cudaMemcpyDeviceToDevice, c.stream);
+    if (b.p) {
+        cudaStreamSynchronize(c.stream);
+        cudaFree(b.p);
+    }
+    b.p = p;
+    b.cap = cap;
+    return true;
+}
+
+template bool ensure<float>(Context&, DevBuf<float>&, size_t, bool);
+template bool ensure<float4>(Context&, DevBuf<float4>&, size_t, bool);
+template bool ensure<uint2>(Context&, DevBuf<uint2>&, size_t, bool);
+template bool ensure<uint8_t>(Context&, DevBuf<uint8_t>&, size_t, bool);
+template bool ensure<uint16_t>(Context&, DevBuf<uint16_t>&, size_t, bool);
+template bool ensure<uint32_t>(Context&, DevBuf<uint32_t>&, size_t, bool);
+template bool ensure<double>(Context&, DevBuf<double>&, size_t, bool);
+template bool ensure<unsigned long long>(Context&, DevBuf<unsigned long long>&, size_t, bool);
+
+}  // namespace ts
+
+namespace {
+
+template <class T>
+void release(DevBuf<T>& b) {
+    if (b.p) cudaFree(b.p);
+    b.p = nullptr;
+    b.cap = 0;
+}
+
+#define TS_CHECK_CTX(ctx)                          \
+    do {                                           \
+        if (!(ctx)) return TS_ERR_VALIDATION;      \
+    } while (0)
+
+ts_status cuda_fail(Context& c, cudaError_t e, const char* where) {
+    c.err = std::string(where) + ": " + cudaGetErrorString(e);
+    return TS_ERR_CUDA;
+}
+
+#define CK(expr)                                              \
+    do {                                                      \
+        cudaError_t _e = (expr);                              \
+        if (_e != cudaSuccess) return cuda_fail(c, _e, #expr); \
+    } while (0)
+
+ts_status last_launch(Context& c, const char* where) {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(c, e, where);
+    return TS_OK;
+}
+
+ts_status validation(Context& c, const char* msg) {
+    c.err = msg;
+    return TS_ERR_VALIDATION;
+}
+
+ts_status oom(Context& c) { return TS_ERR_OOM; }
+
+void stage_begin(Context& c, int k) {
+    if (!c.profiling) return;
+    cudaEventRecord(c.ev_b[k], c.stream);
+}
+void stage_end(Context& c, int k) {
+    if (!c.profiling) return;
+    cudaEventRecord(c.ev_e[k], c.stream);
+    c.ev_rec[k] = true;
+}
+
+bool valid_camera(const ts_camera* cam, std::string* why) {
+    if (!cam) return *why = "camera is NULL", false;
+    if (cam->width < 6 || cam->height < 6) return *why = "image must be at least 6x6", false;
+    if (!(cam->fx > 0.f) || !(cam->fy > 0.f)) return *why = "fx, fy must be > 0", false;
+    int64_t tn = int64_t((cam->width + 15) / 16) * ((cam->height + 15) / 16);
+    if (tn > 65535) return *why = "more than 65535 tiles (16-bit tile keys, ~16 MP)", false;
+    return true;
+}
+
+bool valid_config(const ts_render_config* cfg, std::string* why) {
+    if (!cfg) return *why = "render config is NULL", false;
+    if (cfg->sh_degree < 0 || cfg->sh_degree > 3) return *why = "sh_degree must be 0..3", false;
+    if (cfg->bound_mode < 0 || cfg->bound_mode > 2) return *why = "bound_mode must be 0..2", false;
+    if (cfg->cull_mode < 0 || cfg->cull_mode > 1) return *why = "cull_mode must be 0..1", false;
+    if (cfg->truncation != 0) return *why = "only classic truncation (0) is supported", false;
+    if (cfg->backward_mode != 0) return *why = "only the per-pixel backward (0) is implemented on device", false;
+    if (!(cfg->tau_alpha > 0.f && cfg->tau_alpha < 1.f)) return *why = "tau_alpha must be in (0,1)", false;
+    if (!(cfg->dilation >= 0.f)) return *why = "dilation must be >= 0", false;
+    return true;
+}
+
+DevCam make_devcam(const ts_camera& cam) {
+    DevCam d;
+    for (int i = 0; i < 16; ++i) d.W[i] = cam.W[i];
+    d.fx = cam.fx;
+    d.fy = cam.fy;
+    d.cx = cam.cx;
+    d.cy = cam.cy;
+    d.nearp = cam.near_plane;
+    d.w = cam.width;
+    d.h = cam.height;
+    d.tiles_x = (cam.width + 15) / 16;
+    d.tiles_y = (cam.height + 15) / 16;
+    return d;
+}
+
+ts_status ensure_gaussian_buffers(Context& c, int64_t n) {
+    const size_t N = size_t(std::max<int64_t>(n, 1));
+    bool ok = ensure(c, c.params, 59 * N) && ensure(c, c.grads, 59 * N) && ensure(c, c.m, 59 * N) &&
+              ensure(c, c.v, 59 * N) && ensure(c, c.accum, N) && ensure(c, c.vcount, N) &&
+              ensure(c, c.splat, 3 * N) && ensure(c, c.rect, N) && ensure(c, c.tcount, N) &&
+              ensure(c, c.dkey[0], N) && ensure(c, c.dkey[1], N) && ensure(c, c.dperm[0], N) &&
+              ensure(c, c.dperm[1], N) && ensure(c, c.offsets, N + 1) && ensure(c, c.g2d, 3 * N) &&
+              ensure(c, c.vis, N);
+    return ok ? TS_OK : TS_ERR_OOM;
+}
+
+ts_status zero_state(Context& c) {
+    const size_t N = size_t(c.N);
+    if (N == 0) return TS_OK;
+    CK(cudaMemsetAsync(c.grads.p, 0, 59 * N * 4, c.stream));
+    CK(cudaMemsetAsync(c.m.p, 0, 59 * N * 4, c.stream));
+    CK(cudaMemsetAsync(c.v.p, 0, 59 * N * 4, c.stream));
+    CK(cudaMemsetAsync(c.accum.p, 0, N * 4, c.stream));
+    CK(cudaMemsetAsync(c.vcount.p, 0, N * 4, c.stream));
+    CK(cudaMemsetAsync(c.g2d.p, 0, 3 * N * 16, c.stream));
+    CK(cudaMemsetAsync(c.vis.p, 0, N, c.stream));
+    return TS_OK;
+}
+
+ts_status ensure_frame(Context& c, int w, int h) {
+    const size_t P = size_t(w) * h;
+    bool ok = ensure(c, c.rgb, 3 * P) && ensure(c, c.Tfin, P) && ensure(c, c.pcount, P) && ensure(c, c.dLdC, 3 * P) &&
+              ensure(c, c.hwc_stage, 3 * P) && ensure(c, c.tgt, 3 * P);
+    c.fw = w;
+    c.fh = h;
+    return ok ? TS_OK : TS_ERR_OOM;
+}
+
+int tile_bits_for(int tn) {
+    int b = 1;
+    while ((1 << b) < tn) ++b;
+    return b;
+}
+
+// the forward pipeline of one view
+ts_status run_forward(Context& c, const ts_camera& cam, const ts_render_config& cfg) {
+    DevCam dc = make_devcam(cam);
+    const int Tn = dc.tiles_x * dc.tiles_y;
+    if (ensure_frame(c, cam.width, cam.height) != TS_OK) return TS_ERR_OOM;
+    if (!ensure(c, c.starts, size_t(Tn) + 1)) return TS_ERR_OOM;
+    CK(cudaMemsetAsync(c.counters.p + 1, 0, 2 * sizeof(uint32_t), c.stream));
+    stage_begin(c, 0);
+    launch_preprocess(c, dc, cfg);
+    stage_end(c, 0);
+    stage_begin(c, 1);
+    launch_depth_sort(c);
+    stage_end(c, 1);
+    stage_begin(c, 2);
+    const int64_t I = launch_scan_counts(c);
+    stage_end(c, 2);
+    if (ts_status s = last_launch(c, "preprocess/sort/scan"); s != TS_OK) return s;
+    if (I > int64_t(0xFFFFFFF0u)) return validation(c, "instance count exceeds 2^32");
+    const size_t capI = size_t(I) + size_t(I) / 4 + 1024;
+    if (c.tkey[0].cap < size_t(I) || c.tkey[1].cap < size_t(I) || c.ival[0].cap < size_t(I) ||
+        c.ival[1].cap < size_t(I)) {
+        for (int k = 0; k < 2; ++k) {
+            release(c.tkey[k]);
+            release(c.ival[k]);
+            if (!ensure(c, c.tkey[k], capI) || !ensure(c, c.ival[k], capI)) return TS_ERR_OOM;
+        }
+    }
+    c.I = I;
+    stage_begin(c, 3);
+    launch_duplicate(c, dc, cfg);
+    stage_end(c, 3);
+    stage_begin(c, 4);
+    launch_tile_sort(c, tile_bits_for(Tn));
+    stage_end(c, 4);
+    stage_begin(c, 5);
+    launch_ranges(c, Tn);
+    stage_end(c, 5);
+    stage_begin(c, 6);
+    launch_blend_fwd(c, dc, cfg);
+    stage_end(c, 6);
+    if (ts_status s = last_launch(c, "forward"); s != TS_OK) return s;
+    c.cam = cam;
+    c.cfg = cfg;
+    c.view_valid = true;
+    c.loss_valid = false;
+    return TS_OK;
+}
+
+ts_status upload_image_chw(Context& c, const float* hwc, float* dst_chw) {
+    const size_t P = size_t(c.fw) * c.fh;
+    CK(cudaMemcpyAsync(c.hwc_stage.p, hwc, 3 * P * 4, cudaMemcpyHostToDevice, c.stream));
+    launch_hwc_to_chw(c, c.hwc_stage.p, dst_chw, int(P));
+    return last_launch(c, "hwc_to_chw");
+}
+
+ts_status run_loss(Context& c, const float* target_hwc, int32_t slot, float* out_loss) {
+    if (!c.view_valid) return validation(c, "ts_loss needs a preceding ts_forward");
+    const size_t P = size_t(c.fw) * c.fh;
+    const float* tgt = nullptr;
+    if (target_hwc) {
+        if (ts_status s = upload_image_chw(c, target_hwc, c.tgt.p); s != TS_OK) return s;
+        tgt = c.tgt.p;
+    } else {
+        if (slot < 0 || slot >= c.n_target_slots) return validation(c, "target slot out of range");
+        if (c.target_w != c.fw || c.target_h != c.fh) return validation(c, "target slot size != view size");
+        tgt = c.targets.p + size_t(slot) * 3 * P;
+    }
+    if (!ensure(c, c.loss_tmp, 3 * 11 * P)) return TS_ERR_OOM;
+    stage_begin(c, 7);
+    launch_loss(c, tgt);
+    stage_end(c, 7);
+    if (ts_status s = last_launch(c, "loss"); s != TS_OK) return s;
+    c.loss_valid = true;
+    if (out_loss) {
+        double acc[2];
+        CK(cudaMemcpyAsync(acc, c.loss_acc.p, sizeof(acc), cudaMemcpyDeviceToHost, c.stream));
+        CK(cudaStreamSynchronize(c.stream));
+        const double M = 3.0 * double(P);
+        *out_loss = float(0.8 * acc[0] / M + 0.2 * (1.0 - acc[1] / M));
+    }
+    return TS_OK;
+}
+
+ts_status run_backward(Context& c, const float* dLdC_hwc) {
+    if (!c.view_valid) return validation(c, "ts_backward needs a preceding ts_forward");
+    if (dLdC_hwc) {
+        if (ts_status s = upload_image_chw(c, dLdC_hwc, c.dLdC.p); s != TS_OK) return s;
+    } else if (!c.loss_valid) {
+        return validation(c, "ts_backward(NULL) needs a preceding ts_loss");
+    }
+    DevCam dc = make_devcam(c.cam);
+    stage_begin(c, 8);
+    launch_blend_bwd(c, dc, c.cfg);
+    stage_end(c, 8);
+    stage_begin(c, 9);
+    launch_project_bwd(c, dc, c.cfg);
+    stage_end(c, 9);
+    return last_launch(c, "backward");
+}
+
+ts_status run_adam(Context& c, const ts_adam_config& a, int64_t begin, int64_t end) {
+    if (!(a.bc1 > 0.f) || !(a.bc2 > 0.f)) return validation(c, "bias corrections must be > 0 (step >= 1)");
+    if (a.mode < 0 || a.mode > 2) return validation(c, "adam mode must be 0..2");
+    stage_begin(c, 10);
+    launch_adam(c, a, begin, end);
+    stage_end(c, 10);
+    CK(cudaMemsetAsync(c.vis.p, 0, size_t(std::max<int64_t>(c.N, 1)), c.stream));
+    c.view_valid = false;
+    c.loss_valid = false;
+    return last_launch(c, "adam");
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ts_version(void) { return "tilesplat-b200 0.1 (sm_100a)"; }
+
+ts_status ts_create(int32_t device, void* stream, ts_ctx** out) {
+    if (!out) return TS_ERR_VALIDATION;
+    *out = nullptr;
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+        cudaGetLastError();
+        return TS_ERR_CUDA;
+    }
+    if (device < 0 || device >= ndev) return TS_ERR_VALIDATION;
+    cudaDeviceProp prop;
+    if (cudaGetDeviceProperties(&prop, device) != cudaSuccess) return TS_ERR_CUDA;
+    if (prop.major < 10) return TS_ERR_CUDA;  // built for sm_100a only; no fallback
+    ts_ctx* x = new (std::nothrow) ts_ctx();
+    if (!x) return TS_ERR_OOM;
+    Context& c = x->c;
+    c.device = device;
+    c.sm_count = prop.multiProcessorCount;
+    if (cudaSetDevice(device) != cudaSuccess) {
+        delete x;
+        return TS_ERR_CUDA;
+    }
+    if (stream) {
+        c.stream = static_cast<cudaStream_t>(stream);
+    } else {
+        if (cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking) != cudaSuccess) {
+            delete x;
+            return TS_ERR_CUDA;
+        }
+        c.own_stream = true;
+    }
+    if (!ensure(c, c.counters, 16) || !ensure(c, c.loss_acc, 2)) {
+        delete x;
+        return TS_ERR_OOM;
+    }
+    cudaMemsetAsync(c.counters.p, 0, 16 * 4, c.stream);
+    for (int k = 0; k < kNumStages; ++k) {
+        cudaEventCreate(&c.ev_b[k]);
+        cudaEventCreate(&c.ev_e[k]);
+    }
+    c.ev_init = true;
+    if (ensure_gaussian_buffers(c, 1) != TS_OK) {
+        delete x;
+        return TS_ERR_OOM;
+    }
+    if (cudaStreamSynchronize(c.stream) != cudaSuccess) {
+        delete x;
+        return TS_ERR_CUDA;
+    }
+    *out = x;
+    return TS_OK;
+}
+
+ts_status ts_destroy(ts_ctx* x) {
+    TS_CHECK_CTX(x);
+    Context& c = x->c;
+    cudaSetDevice(c.device);
+    cudaStreamSynchronize(c.stream);
+    release(c.params), release(c.grads), release(c.m), release(c.v), release(c.accum), release(c.vcount);
+    release(c.splat), release(c.rect), release(c.tcount), release(c.offsets), release(c.g2d), release(c.vis);
+    for (int k = 0; k < 2; ++k) {
+        release(c.dkey[k]), release(c.dperm[k]), release(c.tkey[k]), release(c.ival[k]);
+    }
+    release(c.starts), release(c.rhist), release(c.scan_state), release(c.scan_tmp), release(c.counters);
+    release(c.rgb), release(c.Tfin), release(c.dLdC), release(c.hwc_stage), release(c.tgt), release(c.pcount);
+    release(c.loss_acc), release(c.loss_tmp), release(c.targets), release(c.dens);
+    if (c.ev_init)
+        for (int k = 0; k < kNumStages; ++k) {
+            cudaEventDestroy(c.ev_b[k]);
+            cudaEventDestroy(c.ev_e[k]);
+        }
+    if (c.own_stream) cudaStreamDestroy(c.stream);
+    delete x;
+    return TS_OK;
+}
+
+const char* ts_last_error(const ts_ctx* x) { return x ? x->c.err.c_str() : "null context"; }
+
+ts_status ts_synchronize(ts_ctx* x) {
+    TS_CHECK_CTX(x);
+    Context& c = x->c;
+    CK(cudaStreamSynchronize(c.stream));
+    return TS_OK;
+}
+
+ts_status ts_set_params_flat(ts_ctx* x, int64_t n, const float* flat) {
+    TS_CHECK_CTX(x);
+    Context& c = x->c;
+    if (n < 0 || (n > 0 && !flat)) return validation(c, "bad parameter array");
+    if (n >= (int64_t(1) << 31)) return validation(c, "N must be < 2^31");
+    CK(cudaSetDevice(c.device));
+    if (ensure_gaussian_buffers(c, n) != TS_OK) return TS_ERR_OOM;
+    c.N = n;
+    if (n) CK(cudaMemcpyAsync(c.params.p, flat, size_t(59) * n * 4, cudaMemcpyHostToDevice, c.stream));
+    if (ts_status s = zero_state(c); s != TS_OK) return s;
+    c.view_valid = c.loss_valid = false;
+    CK(cudaStreamSynchronize(c.stream));
+    return TS_OK;
+}
+
+ts_status ts_set_params(ts_ctx* x, int64_t n, const float* means, const float* ls, const float* q, const float* op,
+                        const float* dc, const float* rest) {
+    TS_CHECK_CTX(x);
+    Context& c = x->c;
+    if (n < 0) return validation(c, "n < 0");
+    if (n > 0 && (!means || !ls || !q || !op || !dc || !rest)) return validation(c, "NULL parameter array");
+    std::vector<float> flat(size_t(59) * n);
+    const Off o(n);
+    std::memcpy(flat.data() + o.means, means, size_t(3) * n * 4);
+    std::memcpy(flat.data() + o.ls, ls, size_t(3) * n * 4);
+    std::memcpy(flat.data() + o.q, q, size_t(4) * n * 4);
+    std::memcpy(flat.data() + o.op, op, size_t(1) * n * 4);
+    std::memcpy(flat.data() + o.dc, dc, size_t(3) * n * 4);
+    std::memcpy(flat.data() + o.rest, rest, size_t(45) * n * 4);
+    return ts_set_params_flat(x, n, flat.data());
+}
+
+ts_status ts_get_params_flat(ts_ctx* x, float* flat) {
+    TS_CHECK_CTX(x);
+    Context& c = x->c;
+    if (c.N && !flat) return validation(c, "NULL output");
+    CK(cudaSetDevice(c.device));
+    if (c.N) CK(cudaMemcpyAsync(flat, c.params.p, size_t(59) * c.N * 4, cudaMemcpyDeviceToHost, c.stream));
+    CK(cudaStreamSynchronize(c.stream));
+    return TS_OK;
+}
+
+ts_status ts_num_gaussians(const ts_ctx* x, int64_t* n) {
+    if (!x || !n) return TS_ERR_VALIDATION;
+    *n = x->c.N;
+    return TS_OK;
+}
+
+ts_status ts_forward(ts_ctx* x, const ts_camera* cam, const ts_render_config* cfg, float* out_rgb, float* out_T,
+                     uint32_t* out_count) {
+    TS_CHECK_CTX(x);
+    Context& c = x->c;
+    std::string why;
+    if (!valid_camera(cam, &why) || !valid_config(cfg, &why)) return validation(c, why.c_str());
+    CK(cudaSetDevice(c.device));
+    if (ts_status s = run_forward(c, *cam, *cfg); s != TS_OK) return s;
+    const size_t P = size_t(cam->width) * cam->height;
+    if (out_rgb) {
+        launch_chw_to_hwc(c, c.rgb.p, c.hwc_stage.p, int(P));
+        CK(cudaMemcpyAsync(out_rgb, c.hwc_stage.p, 3 * P * 4, cudaMemcpyDeviceToHost, c.stream));
+    }
+    if (out_T) CK(cudaMemcpyAsync(out_T, c.Tfin.p, P * 4, cudaMemcpyDeviceToHost, c.stream));
+    if (out_count) CK(cudaMemcpyAsync(out_count, c.pcount.p, P * 4, cudaMemcpyDeviceToHost, c.stream));
+    if (out_rgb || out_T || out_count) CK(cudaStreamSynchronize(c.stream));
+    return last_launch(c, "ts_forward");
+}
+
+ts_status ts_set_target(ts_ctx* x, int32_t slot, int32_t w, int32_t h, const float* hwc) {
+    TS_CHECK_CTX(x);
+    Context& c = x->c;
+    if (slot < 0 || slot > 4096 || w < 6 || h < 6 || !hwc) return validation(c, "bad target");
+    CK(cudaSetDevice(c.device));
+    const size_t P = size_t(w) * h;
+    if (c.target_w != w || c.target_h != h) {
+        release(c.targets);
+        c.n_target_slots = 0;
+        c.target_w = w;
+        c.target_h = h;
+    }
+    if (slot >= c.n_target_slots) {
+        if (!ensure(c, c.targets, size_t(slot + 1) * 3 * P, true)) return TS_ERR_OOM;
+        c.n_target_slots = slot + 1;
+    }
+    if (ensure_frame(c, std::max(c.fw, w), std::max(c.fh, h)) != TS_OK) return TS_ERR_OOM;
+    CK(cudaMemcpyAsync(c.hwc_stage.p, hwc, 3 * P * 4, cudaMemcpyHostToDevice, c.stream));
+    launch_hwc_to_chw(c, c.hwc_stage.p, c.targets.p + size_t(slot) * 3 * P, int(P));
+    CK(cudaStreamSynchronize(c.stream));
+    return last_launch(c, "ts_set_target");
+}
+
+ts_status ts_loss(ts_ctx* x, const float* target_hwc, int32_t slot, float* out_loss) {
+    TS_CHECK_CTX(x);
+    Context& c = x->c;
+    CK(cudaSetDevice(c.device));
+    return run_loss(c, target_hwc, slot, out_loss);
+}
+
+ts_status ts_backward(ts_ctx* x, const float* dLdC_hwc) {
+    TS_CHECK_CTX(x);
+    Context& c = x->c;
+    CK(cudaSetDevice(c.device));
+    return run_backward(c, dLdC_hwc);
+}
+
+ts_status ts_zero_grads(ts_ctx* x) {
+    TS_CHECK_CTX(x);
+    Context& c = x->c;
+    CK(cudaSetDevice(c.device));
+    if (c.N) CK(cudaMemsetAsync(c.grads.p, 0, size_t(59) * c.N * 4, c.stream));
+    return TS_OK;
+}
+
+ts_status ts_grad_buffer(ts_ctx* x, float** p, int64_t* n) {
+    TS_CHECK_CTX(x);
+    if (p) *p = x->c.grads.p;
+    if (n) *n = 59 * x->c.N;
+    return TS_OK;
+}
+
+ts_status ts_param_buffer(ts_ctx* x, float** p, int64_t* n) {
+    TS_CHECK_CTX(x);
+    if (p) *p = x->c.params.p;
+    if (n) *n = 59 * x->c.N;
+    return TS_OK;
+}
+
+ts_status ts_stats_buffer(ts_ctx* x, float** a, float** cnt) {
+    TS_CHECK_CTX(x);
+    if (a) *a = x->c.accum.p;
+    if (cnt) *cnt = x->c.vcount.p;
+    return TS_OK;
+}
+
+ts_status ts_adam_step(ts_ctx* x, const ts_adam_config* a) {
+    TS_CHECK_CTX(x);
+    Context& c = x->c;
+    if (!a) return validation(c, "adam config is NULL");
+    CK(cudaSetDevice(c.device));
+    return run_adam(c, *a, 0, 59 * c.N);
+}
+
+ts_status ts_adam_step_range(ts_ctx* x, const ts_adam_config* a, int64_t begin, int64_t end) {
+    TS_CHECK_CTX(x);
+    Context& c = x->c;
+    if (!a) return validation(c, "adam config is NULL");
+    if (begin < 0 || end > 59 * c.N || begin > end) return validation(c, "bad range");
+    CK(cudaSetDevice(c.device));
+    return run_adam(c, *a, begin, end);
+}
+
+ts_status ts_train_step(ts_ctx* x, const ts_camera* cam, const ts_render_config* cfg, const float* target_hwc,
+                        int32_t slot, const ts_adam_config* adam, float* out_loss) {
+    TS_CHECK_CTX(x);
+    Context& c = x->c;
+    std::string why;
+    if (!valid_camera(cam, &why) || !valid_config(cfg, &why)) return validation(c, why.c_str());
+    if (!adam) return validation(c, "adam config is NULL");
+    CK(cudaSetDevice(c.device));
+    if (ts_status s = run_forward(c, *cam, *cfg); s != TS_OK) return s;
+    if (ts_status s = run_loss(c, target_hwc, slot, nullptr); s != TS_OK) return s;
+    if (ts_status s = run_backward(c, nullptr); s != TS_OK) return s;
+    if (ts_status s = run_adam(c, *adam, 0, 59 * c.N); s != TS_OK) return s;
+    if (out_loss) {
+        double acc[2];
+        CK(cudaMemcpyAsync(acc, c.loss_acc.p, sizeof(acc), cudaMemcpyDeviceToHost, c.stream));
+        CK(cudaStreamSynchronize(c.stream));
+        const double M = 3.0 * double(cam->width) * cam->height;
+        *out_loss = float(0.8 * acc[0] / M + 0.2 * (1.0 - acc[1] / M));
+    }
+    return TS_OK;
+}
+
+ts_status ts_opacity_reset(ts_ctx* x) {
+    TS_CHECK_CTX(x);
+    Context& c = x->c;
+    CK(cudaSetDevice(c.device));
+    launch_opacity_reset(c, float(std::log(0.01 / 0.99)));
+    c.view_valid = c.loss_valid = false;
+    return last_launch(c, "opacity_reset");
+}
+
+ts_status ts_densify(ts_ctx* x, float grad_thresh, float extent, uint64_t seed, int64_t iter, int64_t* n_after,
+                     int64_t stats[3]) {
+    TS_CHECK_CTX(x);
+    Context& c = x->c;
+    if (!(extent > 0.f)) return validation(c, "extent must be > 0");
+    CK(cudaSetDevice(c.device));
+    int64_t st[3] = {0, 0, 0};
+    const float log_small = float(std::log(0.01 * double(extent)));
+    const float log_big = float(std::log(0.1 * double(extent)));
+    const float logit_min = float(std::log(0.05 / 0.95));
+    const int64_t na = launch_densify(c, grad_thresh, log_small, log_big, logit_min, seed, iter, st);
+    if (na < 0) return c.err.empty() ? TS_ERR_CUDA : TS_ERR_OOM;
+    if (n_after) *n_after = na;
+    if (stats) std::memcpy(stats, st, sizeof(st));
+    c.view_valid = c.loss_valid = false;
+    return last_launch(c, "densify");
+}
+
+ts_status ts_set_state(ts_ctx* x, const float* grads, const float* m, const float* v, const float* accum,
+                       const float* vcount) {
+    TS_CHECK_CTX(x);
+    Context& c = x->c;
+    CK(cudaSetDevice(c.device));
+    const size_t L = size_t(59) * c.N, N = size_t(c.N);
+    if (grads) CK(cudaMemcpyAsync(c.grads.p, grads, L * 4, cudaMemcpyHostToDevice, c.stream));
+    if (m) CK(cudaMemcpyAsync(c.m.p, m, L * 4, cudaMemcpyHostToDevice, c.stream));
+    if (v) CK(cudaMemcpyAsync(c.v.p, v, L * 4, cudaMemcpyHostToDevice, c.stream));
+    if (accum) CK(cudaMemcpyAsync(c.accum.p, accum, N * 4, cudaMemcpyHostToDevice, c.stream));
+    if (vcount) CK(cudaMemcpyAsync(c.vcount.p, vcount, N * 4, cudaMemcpyHostToDevice, c.stream));
+    CK(cudaStreamSynchronize(c.stream));
+    return TS_OK;
+}
+
+ts_status ts_get_state(ts_ctx* x, float* grads, float* m, float* v, float* accum, float* vcount) {
+    TS_CHECK_CTX(x);
+    Context& c = x->c;
+    CK(cudaSetDevice(c.device));
+    const size_t L = size_t(59) * c.N, N = size_t(c.N);
+    if (grads) CK(cudaMemcpyAsync(grads, c.grads.p, L * 4, cudaMemcpyDeviceToHost, c.stream));
+    if (m) CK(cudaMemcpyAsync(m, c.m.p, L * 4, cudaMemcpyDeviceToHost, c.stream));
+    if (v) CK(cudaMemcpyAsync(v, c.v.p, L * 4, cudaMemcpyDeviceToHost, c.stream));
+    if (accum) CK(cudaMemcpyAsync(accum, c.accum.p, N * 4, cudaMemcpyDeviceToHost, c.stream));
+    if (vcount) CK(cudaMemcpyAsync(vcount, c.vcount.p, N * 4, cudaMemcpyDeviceToHost, c.stream));
+    CK(cudaStreamSynchronize(c.stream));
+    return TS_OK;
+}
+
+ts_status ts_debug_preprocess(ts_ctx* x, float* splat12, int32_t* rect4, uint32_t* tile_count, uint32_t* depth_key) {
+    TS_CHECK_CTX(x);
+    Context& c = x->c;
+    if (!c.view_valid) return validation(c, "no forward state");
+    CK(cudaSetDevice(c.device));
+    const size_t N = size_t(c.N);
+    std::vector<float4> sp(3 * N);
+    std::vector<uint2> rc(N);
+    std::vector<uint32_t> cnt(N);
+    if (N) {
+        CK(cudaMemcpyAsync(sp.data(), c.splat.p, 3 * N * 16, cudaMemcpyDeviceToHost, c.stream));
+        CK(cudaMemcpyAsync(rc.data(), c.rect.p, N * 8, cudaMemcpyDeviceToHost, c.stream));
+        CK(cudaMemcpyAsync(cnt.data(), c.tcount.p, N * 4, cudaMemcpyDeviceToHost, c.stream));
+    }
+    CK(cudaStreamSynchronize(c.stream));
+    for (size_t g = 0; g < N; ++g) {
+        if (splat12) std::memcpy(splat12 + 12 * g, &sp[3 * g], 48);
+        if (rect4) {
+            rect4[4 * g] = int32_t(rc[g].x & 0xFFFF);
+            rect4[4 * g + 1] = int32_t(rc[g].y & 0xFFFF);
+            rect4[4 * g + 2] = int32_t(rc[g].x >> 16);
+            rect4[4 * g + 3] = int32_t(rc[g].y >> 16);
+        }
+        if (tile_count) tile_count[g] = cnt[g];
+        if (depth_key) {
+            uint32_t bits;
+            std::memcpy(&bits, &sp[3 * g + 1].w, 4);
+            depth_key[g] = cnt[g] ? (bits ^ 0x80000000u) : 0xFFFFFFFFu;
+        }
+    }
+    return TS_OK;
+}
+
+ts_status ts_debug_instances(ts_ctx* x, int64_t* n_inst, uint64_t* keys, uint32_t* vals, uint32_t* ranges) {
+    TS_CHECK_CTX(x);
+    Context& c = x->c;
+    if (!c.view_valid) return validation(c, "no forward state");
+    CK(cudaSetDevice(c.device));
+    if (n_inst) *n_inst = c.I;
+    if (!keys && !vals && !ranges) return TS_OK;
+    const size_t I = size_t(c.I), N = size_t(c.N);
+    const int Tn = ((c.cam.width + 15) / 16) * ((c.cam.height + 15) / 16);
+    std::vector<uint16_t> tk(I);
+    std::vector<uint32_t> iv(I), st(size_t(Tn) + 1);
+    std::vector<float4> sp(3 * N);
+    if (I) {
+        CK(cudaMemcpyAsync(tk.data(), c.tkey[0].p, I * 2, cudaMemcpyDeviceToHost, c.stream));
+        CK(cudaMemcpyAsync(iv.data(), c.ival[0].p, I * 4, cudaMemcpyDeviceToHost, c.stream));
+    }
+    if (N) CK(cudaMemcpyAsync(sp.data(), c.splat.p, 3 * N * 16, cudaMemcpyDeviceToHost, c.stream));
+    CK(cudaMemcpyAsync(st.data(), c.starts.p, (size_t(Tn) + 1) * 4, cudaMemcpyDeviceToHost, c.stream));
+    CK(cudaStreamSynchronize(c.stream));
+    for (size_t i = 0; i < I; ++i) {
+        if (vals) vals[i] = iv[i];
+        if (keys) {
+            uint32_t bits;
+            std::memcpy(&bits, &sp[3 * size_t(iv[i]) + 1].w, 4);
+            keys[i] = (uint64_t(tk[i]) << 32) | uint64_t(bits ^ 0x80000000u);
+        }
+    }
+    if (ranges)
+        for (int t = 0; t < Tn; ++t) {
+            ranges[2 * t] = st[t];
+            ranges[2 * t + 1] = st[t + 1];
+        }
+    return TS_OK;
+}
+
+ts_status ts_debug_grad2d(ts_ctx* x, const float* dLdC_hwc, float* g2d9) {
+    TS_CHECK_CTX(x);
+    Context& c = x->c;
+    if (!c.view_valid) return validation(c, "no forward state");
+    if (!dLdC_hwc || !g2d9) return validation(c, "NULL argument");
+    CK(cudaSetDevice(c.device));
+    const size_t N = size_t(c.N);
+    if (ts_status s = upload_image_chw(c, dLdC_hwc, c.dLdC.p); s != TS_OK) return s;
+    CK(cudaMemsetAsync(c.g2d.p, 0, 3 * N * 16, c.stream));
+    DevCam dc = make_devcam(c.cam);
+    launch_blend_bwd(c, dc, c.cfg);
+    std::vector<float4> g(3 * N);
+    if (N) CK(cudaMemcpyAsync(g.data(), c.g2d.p, 3 * N * 16, cudaMemcpyDeviceToHost, c.stream));
+    CK(cudaMemsetAsync(c.g2d.p, 0, 3 * N * 16, c.stream));
+    CK(cudaStreamSynchronize(c.stream));
+    for (size_t k = 0; k < N; ++k) {
+        const float* s = reinterpret_cast<const float*>(&g[3 * k]);
+        std::memcpy(g2d9 + 9 * k, s, 9 * 4);
+    }
+    return last_launch(c, "debug_grad2d");
+}
+
+ts_status ts_view_stats(ts_ctx* x, int64_t out[4]) {
+    TS_CHECK_CTX(x);
+    Context& c = x->c;
+    if (!out) return validation(c, "NULL output");
+    CK(cudaSetDevice(c.device));
+    uint32_t cnt[3];
+    CK(cudaMemcpyAsync(cnt, c.counters.p, sizeof(cnt), cudaMemcpyDeviceToHost, c.stream));
+    CK(cudaStreamSynchronize(c.stream));
+    out[0] = cnt[1];
+    out[1] = c.I;
+    out[2] = cnt[2];
+    out[3] = int64_t(c.cam.width) * c.cam.height;
+    return TS_OK;
+}
+
+ts_status ts_set_profiling(ts_ctx* x, int32_t on) {
+    TS_CHECK_CTX(x);
+    x->c.profiling = on != 0;
+    for (int k = 0; k < kNumStages; ++k) x->c.ev_rec[k] = false;
+    return TS_OK;
+}
+
+ts_status ts_stage_times(ts_ctx* x, float* ms, int32_t n) {
+    TS_CHECK_CTX(x);
+    Context& c = x->c;
+    if (!ms) return validation(c, "NULL output");
+    CK(cudaStreamSynchronize(c.stream));
+    for (int k = 0; k < n && k < kNumStages; ++k) {
+        ms[k] = 0.f;
+        if (c.ev_rec[k]) cudaEventElapsedTime(&ms[k], c.ev_b[k], c.ev_e[k]);
+    }
+    return TS_OK;
+}
+
+ts_status ts_launch_count(ts_ctx* x, int64_t* n) {
+    TS_CHECK_CTX(x);
+    if (n) *n = x->c.launches;
+    return TS_OK;
+}
+
+ts_status ts_host_alloc(size_t bytes, void** out) {
+    if (!out) return TS_ERR_VALIDATION;
+    if (cudaMallocHost(out, bytes) != cudaSuccess) {
+        cudaGetLastError();
+        *out = nullptr;
+        return TS_ERR_OOM;
+    }
+    return TS_OK;
+}
+
+ts_status ts_host_free(void* p) {
+    if (p) cudaFreeHost(p);
+    return TS_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,137 @@
+// ts_internal.cuh — device buffers, context and kernel launcher declarations.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+
+#include "../../include/tilesplat_c.h"
+
+namespace ts {
+
+constexpr int kTile = 16;
+constexpr int kParams = 59;
+constexpr int kG2D = 12;  // floats per Gaussian in the 2D-gradient accumulator (9 used, 16B aligned)
+constexpr int kNumStages = 11;
+
+// flat 59*N buffer block offsets
+struct Off {
+    int64_t means, ls, q, op, dc, rest;
+    __host__ __device__ explicit Off(int64_t n)
+        : means(0), ls(3 * n), q(6 * n), op(10 * n), dc(11 * n), rest(14 * n) {}
+};
+
+// Device-side camera with derived constants (computed in-kernel from ts_camera
+// fields so the float op sequence matches the oracle's Cam<float>).
+struct DevCam {
+    float W[16];
+    float fx, fy, cx, cy, nearp;
+    int w, h, tiles_x, tiles_y;
+};
+
+template <class T>
+struct DevBuf {
+    T* p = nullptr;
+    size_t cap = 0;  // elements
+};
+
+struct Context {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    std::string err;
+    int sm_count = 148;
+    int64_t launches = 0;
+
+    // ParameterStore + optimizer state + gradients (59*N each)
+    int64_t N = 0;
+    DevBuf<float> params, grads, m, v, accum, vcount;
+    int64_t step = 0;
+
+    // per-view (sized by N)
+    DevBuf<float4> splat;        // 3 float4 per Gaussian: (mx,my,k2,o) (A,B,C,depth) (r,g,b,det)
+    DevBuf<uint2> rect;          // packed tile rect
+    DevBuf<uint32_t> tcount;     // tiles per Gaussian
+    DevBuf<uint32_t> dkey[2];    // depth keys (radix double buffer)
+    DevBuf<uint32_t> dperm[2];   // gaussian indices (radix double buffer)
+    DevBuf<uint32_t> offsets;    // N+1 exclusive scan (depth-sorted order)
+    DevBuf<float4> g2d;          // 3 float4 per Gaussian, 2D grad accumulator
+    DevBuf<uint8_t> vis;         // visible in any view since the last optimizer step
+    // instances
+    int64_t I = 0;
+    DevBuf<uint16_t> tkey[2];
+    DevBuf<uint32_t> ival[2];
+    DevBuf<uint32_t> starts;     // Tn+1
+    // radix scratch
+    DevBuf<uint32_t> rhist;      // 256 * blocks
+    DevBuf<unsigned long long> scan_state;
+    DevBuf<uint32_t> scan_tmp;
+    DevBuf<uint32_t> counters;   // [0] scan tile ticket, [1] visible V, [2] Ip, [3..] spare
+    // frame (planar CHW)
+    int fw = 0, fh = 0;
+    DevBuf<float> rgb, Tfin, dLdC, hwc_stage, tgt;
+    DevBuf<uint32_t> pcount;
+    DevBuf<double> loss_acc;     // [0] L1 sum, [1] SSIM sum
+    DevBuf<float> loss_tmp;      // 13 planes of P for the SSIM passes
+    DevBuf<float> targets;       // target slots, CHW planar
+    int n_target_slots = 0, target_w = 0, target_h = 0;
+
+    // last view (forward -> backward contract)
+    bool view_valid = false;
+    bool loss_valid = false;
+    ts_camera cam{};
+    ts_render_config cfg{};
+    int64_t last_V = 0, last_Ip = 0;
+    bool stats_valid = false;
+
+    // profiling
+    bool profiling = false;
+    cudaEvent_t ev_b[kNumStages] = {}, ev_e[kNumStages] = {};
+    bool ev_rec[kNumStages] = {};
+    float stage_ms[kNumStages] = {};
+    bool ev_init = false;
+
+    DevBuf<uint32_t> dens;       // densify scratch
+};
+
+// ---- kernels / launchers (each returns cudaError_t of the launch) ----
+void launch_preprocess(Context& c, const DevCam& cam, const ts_render_config& cfg);
+void launch_depth_sort(Context& c);                 // sorts (dkey, perm) for N entries
+int64_t launch_scan_counts(Context& c);             // offsets in depth order; returns I (syncs)
+void launch_duplicate(Context& c, const DevCam& cam, const ts_render_config& cfg);
+void launch_tile_sort(Context& c, int tile_bits);
+void launch_ranges(Context& c, int n_tiles);
+void launch_blend_fwd(Context& c, const DevCam& cam, const ts_render_config& cfg);
+void launch_loss(Context& c, const float* target_chw);
+void launch_blend_bwd(Context& c, const DevCam& cam, const ts_render_config& cfg);
+void launch_project_bwd(Context& c, const DevCam& cam, const ts_render_config& cfg);
+void launch_adam(Context& c, const ts_adam_config& a, int64_t begin, int64_t end);
+void launch_hwc_to_chw(Context& c, const float* hwc, float* chw, int P);
+void launch_chw_to_hwc(Context& c, const float* chw, float* hwc, int P);
+void launch_opacity_reset(Context& c, float logit_max);
+int64_t launch_densify(Context& c, float grad_thresh, float log_small, float log_big, float logit_min,
+                       uint64_t seed, int64_t iter, int64_t stats[3]);
+
+// generic device-wide exclusive scan of u32 (decoupled look-back); in may be
+// gathered through perm (in[perm[i]]) when perm != nullptr.  out has n+1 entries.
+void launch_exclusive_scan(Context& c, const uint32_t* in, const uint32_t* perm, uint32_t* out, int64_t n);
+
+// radix sort one 8-bit digit pass (stable)
+template <class K>
+void radix_pass(Context& c, const K* kin, const uint32_t* vin, K* kout, uint32_t* vout, int64_t n, int shift);
+
+template <class T>
+bool ensure(Context& c, DevBuf<T>& b, size_t n, bool keep = false);
+
+#define TS_LAUNCHED(c) ((c).launches++)
+
+template <class T>
+__host__ __device__ __forceinline__ T tmin(T a, T b) {
+    return a < b ? a : b;
+}
+template <class T>
+__host__ __device__ __forceinline__ T tmax(T a, T b) {
+    return a < b ? b : a;
+}
+
+}  // namespace ts

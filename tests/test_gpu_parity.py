@@ -1,0 +1,254 @@
+"""CUDA path (libtilesplat_b200.so via the C-ABI) vs the CPU oracle on identical
+seeded scenes.  Tolerances are the north_star's: tile assignment, sorted keys
+and ranges bit-exact; images <= 1e-4 max abs per channel; gradients within
+1e-3 relative (>= 99% of coordinates per parameter class)."""
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from paper_2602_09999_b200 import scene, types as T
+
+pytestmark = pytest.mark.gpu
+
+IMG_TOL = 1e-4
+GRAD_RTOL = 1e-3
+
+
+def _scene(name):
+    if name == "c1":
+        w = scene.WORKLOADS["c1"]
+        p = scene.random_params(w.n, w.s0, w.m_o, w.seed)
+        cam = scene.workload_cameras(w)[0]
+        return p, w.n, cam, T.RenderConfig.make(sh_degree=0)
+    if name == "mid":  # SH3, odd image size (partial edge tiles), background colour
+        n = 40_000
+        p = scene.random_params(n, 0.015, 0.5, 11)
+        cam = scene.make_camera(637, 419, eye=(0.5, 0.9, -3.2))
+        return p, n, cam, T.RenderConfig.make(sh_degree=3, bg=(0.2, 0.1, 0.3))
+    if name == "dense":  # low opacity, long per-tile lists (c5-like)
+        n = 60_000
+        p = scene.random_params(n, 0.03, -2.0, 12)
+        cam = scene.make_camera(320, 240)
+        return p, n, cam, T.RenderConfig.make(sh_degree=2)
+    raise KeyError(name)
+
+
+SCENES = ["c1", "mid", "dense"]
+
+
+@pytest.fixture(scope="module", params=SCENES)
+def sc(request, engine):
+    p, n, cam, cfg = _scene(request.param)
+    engine.set_params(p, n)
+    out = engine.render(cam, cfg)
+    return dict(name=request.param, p=p, n=n, cam=cam, cfg=cfg, gpu=out)
+
+
+def test_preprocess_bit_exact(sc, engine):
+    engine.set_params(sc["p"], sc["n"])
+    engine.render(sc["cam"], sc["cfg"], outputs=False)
+    gs, gr, gc, gk = engine.debug_preprocess()
+    os_, or_, oc, ok = O.preprocess(sc["p"], sc["n"], sc["cam"], sc["cfg"])
+    assert np.array_equal(gc, oc), f"tile counts differ at {np.flatnonzero(gc != oc)[:10]}"
+    vis = oc > 0
+    assert np.array_equal(gr[vis], or_[vis])
+    assert np.array_equal(gk, ok)
+    # mean2d, k2, opacity, conic, depth, det are on the exact-op path: bitwise
+    exact_cols = [0, 1, 2, 3, 4, 5, 6, 7, 11]
+    assert np.array_equal(gs[vis][:, exact_cols].view(np.uint32), os_[vis][:, exact_cols].view(np.uint32))
+    # colour (SH) is on the tolerance path
+    assert np.abs(gs[vis][:, 8:11] - os_[vis][:, 8:11]).max() <= 1e-5
+
+
+def test_instances_sorted_keys_and_ranges_bit_exact(sc, engine):
+    engine.set_params(sc["p"], sc["n"])
+    engine.render(sc["cam"], sc["cfg"], outputs=False)
+    gk, gv, gr = engine.debug_instances()
+    ok, ov, orr, _ = O.instances(sc["p"], sc["n"], sc["cam"], sc["cfg"], sort="combined")
+    assert gk.shape == ok.shape
+    assert np.array_equal(gk, ok)
+    assert np.array_equal(gv, ov)
+    assert np.array_equal(gr, orr)
+
+
+def test_render_image_parity(sc):
+    rgb, Tf, cnt = sc["gpu"]
+    orgb, oT, ocnt, _ = O.render(sc["p"], sc["n"], sc["cam"], sc["cfg"])
+    err = np.abs(rgb - orgb).max()
+    assert err <= IMG_TOL, f"image max abs err {err}"
+    assert np.abs(Tf - oT).max() <= IMG_TOL
+    assert np.mean(cnt == ocnt) >= 0.999
+
+
+def _grad_check(g, o, name, rtol=GRAD_RTOL, frac=0.99):
+    """>= frac of coordinates within rtol relative, with an absolute floor of
+    rtol * RMS(class) for near-zero entries."""
+    o = o.astype(np.float64)
+    g = g.astype(np.float64)
+    rms = np.sqrt(np.mean(o * o)) + 1e-30
+    ok = np.abs(g - o) <= rtol * np.maximum(np.abs(o), rms)
+    f = ok.mean() if ok.size else 1.0
+    assert f >= frac, f"{name}: only {f:.5f} within {rtol} (max rel {np.max(np.abs(g-o)/np.maximum(np.abs(o), rms)):.3g})"
+
+
+def test_blend_backward_2d_grads(sc, engine):
+    rng = np.random.default_rng(3)
+    H, W = sc["cam"].height, sc["cam"].width
+    dl = rng.normal(0, 1e-3, (H, W, 3)).astype(np.float32)
+    engine.set_params(sc["p"], sc["n"])
+    engine.render(sc["cam"], sc["cfg"], outputs=False)
+    g2 = engine.debug_grad2d(dl)
+    _, o2, _, _ = O.backward(sc["p"], sc["n"], sc["cam"], sc["cfg"], dl)
+    for k, nm in enumerate(["dmx", "dmy", "dA", "dB", "dC", "do", "dr", "dg", "db"]):
+        _grad_check(g2[:, k], o2[:, k], nm)
+
+
+def test_parameter_grads_and_stats(sc, engine):
+    rng = np.random.default_rng(4)
+    H, W = sc["cam"].height, sc["cam"].width
+    dl = rng.normal(0, 1e-3, (H, W, 3)).astype(np.float32)
+    engine.set_params(sc["p"], sc["n"])
+    engine.render(sc["cam"], sc["cfg"], outputs=False)
+    engine.backward(dl)
+    G, _, _, acc, vc = engine.get_state()
+    oG, _, oacc, ovc = O.backward(sc["p"], sc["n"], sc["cam"], sc["cfg"], dl)
+    n = sc["n"]
+    for (a, b), nm in zip(T.group_slices(n), T.GROUPS):
+        if nm == "sh_rest" and sc["cfg"].sh_degree == 0:
+            assert np.all(G[a:b] == 0)
+            continue
+        _grad_check(G[a:b], oG[a:b], nm)
+    assert np.array_equal(vc, ovc)
+    _grad_check(acc, oacc, "densify accum")
+
+
+def test_loss_parity(sc, engine):
+    rng = np.random.default_rng(5)
+    rgb = sc["gpu"][0]
+    target = np.clip(rgb + rng.normal(0, 0.05, rgb.shape), 0, 1).astype(np.float32)
+    engine.set_params(sc["p"], sc["n"])
+    engine.render(sc["cam"], sc["cfg"], outputs=False)
+    loss = engine.training_loss(target)
+    ol, od = O.training_loss(rgb, target)
+    assert abs(loss - ol) <= 1e-5 * max(1.0, abs(ol))
+    # dL/dC: route through ts_backward's device buffer by comparing the resulting 2D grads
+    engine.backward(None)
+    G, _, _, _, _ = engine.get_state()
+    oG, _, _, _ = O.backward(sc["p"], sc["n"], sc["cam"], sc["cfg"], od)
+    a, b = T.group_slices(sc["n"])[0]
+    _grad_check(G[a:b], oG[a:b], "means via loss")
+
+
+def test_adam_bitwise(engine):
+    n = 5003  # odd N: unaligned group boundaries exercise the scalar paths
+    rng = np.random.default_rng(6)
+    p = scene.random_params(n, 0.02, 0.0, 9)
+    g = rng.normal(0, 1e-2, 59 * n).astype(np.float32)
+    m = rng.normal(0, 1e-3, 59 * n).astype(np.float32)
+    v = np.abs(rng.normal(0, 1e-4, 59 * n)).astype(np.float32)
+    engine.set_params(p, n)
+    engine.set_state(grads=g, m=m, v=v)
+    cfg = T.AdamConfig.make(step=7, extent=2.5, zero_grads=1)
+    engine.adam_step(cfg)
+    gp = engine.get_params()
+    gg, gm, gv, _, _ = engine.get_state()
+    op, om, ov = p.copy(), m.copy(), v.copy()
+    O.adam_step(op, g.copy(), om, ov, n, np.array(cfg.lr[:], np.float32), cfg.beta1, cfg.beta2, cfg.eps,
+                cfg.bc1, cfg.bc2, mode=1)
+    assert np.array_equal(gp.view(np.uint32), op.view(np.uint32))
+    assert np.array_equal(gm.view(np.uint32), om.view(np.uint32))
+    assert np.array_equal(gv.view(np.uint32), ov.view(np.uint32))
+    assert np.all(gg == 0)
+
+
+def test_adam_range_and_skip_invisible(engine):
+    w = scene.WORKLOADS["c1"]
+    p = scene.random_params(w.n, w.s0, w.m_o, w.seed)
+    cam = scene.workload_cameras(w)[0]
+    cfg = T.RenderConfig.make(sh_degree=0)
+    n = w.n
+    rng = np.random.default_rng(8)
+    dl = rng.normal(0, 1e-3, (cam.height, cam.width, 3)).astype(np.float32)
+    engine.set_params(p, n)
+    engine.render(cam, cfg, outputs=False)
+    engine.backward(dl)
+    _, _, _, _, vc = engine.get_state()
+    vis = vc > 0
+    engine.adam_step(T.AdamConfig.make(step=1, mode=T.ADAM_SKIP_INVISIBLE))
+    q = engine.get_params()
+    # invisible Gaussians untouched in every group
+    for (a, b), wd in zip(T.group_slices(n), T.GROUP_WIDTH):
+        blk_new = q[a:b].reshape(n, wd)
+        blk_old = p[a:b].reshape(n, wd)
+        assert np.array_equal(blk_new[~vis], blk_old[~vis])
+    # range update: only [begin, end) changes
+    engine.set_params(p, n)
+    engine.set_state(grads=np.ones(59 * n, np.float32))
+    engine.adam_step(T.AdamConfig.make(step=1), begin=100, end=1001)
+    q = engine.get_params()
+    changed = np.flatnonzero(q != p)
+    assert changed.min() >= 100 and changed.max() < 1001
+
+
+def test_densify_parity(engine):
+    n = 20_000
+    rng = np.random.default_rng(10)
+    p = scene.random_params(n, 0.02, 0.0, 13)
+    p[6 * n:10 * n][rng.random(4 * n) < 0.002] = 0.0   # a few degenerate quaternions
+    acc = np.abs(rng.normal(0, 4e-4, n)).astype(np.float32)
+    vc = rng.integers(0, 3, n).astype(np.float32)
+    m = rng.normal(0, 1e-3, 59 * n).astype(np.float32)
+    v = np.abs(rng.normal(0, 1e-4, 59 * n)).astype(np.float32)
+    extent = 2.0
+    engine.set_params(p, n)
+    engine.set_state(m=m, v=v, accum=acc, vcount=vc)
+    na, st = engine.densify_and_prune(2e-4, extent, 1234, 700)
+    gp = engine.get_params()
+    _, gm, gv, gacc, gvc = engine.get_state()
+    op, om, ov, ona, ost = O.densify(p, m, v, acc, vc, n, 2e-4, extent, 1234, 700)
+    assert na == ona and tuple(st) == tuple(ost)
+    assert np.array_equal(gm, om) and np.array_equal(gv, ov)
+    assert np.all(gacc == 0) and np.all(gvc == 0)
+    # everything but the sampled child positions is bit-exact
+    a, b = T.group_slices(na)[0]
+    assert np.array_equal(gp[b:], op[b:])
+    assert np.allclose(gp[a:b], op[a:b], rtol=0, atol=1e-5)
+
+
+def test_full_size_properties(engine):
+    """Headline size (3M Gaussians, SH3, 1080p): size-independent invariants."""
+    w = scene.WORKLOADS["H"]
+    p = scene.random_params(w.n, w.s0, w.m_o, w.seed)
+    cam = scene.workload_cameras(w)[0]
+    cfg = T.RenderConfig.make(sh_degree=3)
+    engine.set_params(p, w.n)
+    rgb, Tf, cnt = engine.render(cam, cfg)
+    keys, vals, ranges = engine.debug_instances()
+    st = engine.view_stats()
+    assert st["I"] == keys.size and st["P"] == cam.n_pixels
+    assert np.all(np.diff(keys.astype(np.uint64)) >= 0) or np.all(keys[1:] >= keys[:-1])
+    assert int(ranges[-1, 1]) == keys.size and np.all(ranges[1:, 0] == ranges[:-1, 1])
+    tiles = (keys >> np.uint64(32)).astype(np.int64)
+    for t in (0, cam.n_tiles // 2, cam.n_tiles - 1):
+        assert np.all(tiles[ranges[t, 0]:ranges[t, 1]] == t)
+    assert np.all(Tf >= 0) and np.all(Tf <= 1) and np.isfinite(rgb).all()
+    # per-tile slice of the image against the oracle on a crop is covered by the
+    # small scenes; here: every pixel's contributor count is within its tile list
+    tl = (ranges[:, 1] - ranges[:, 0]).reshape(cam.tiles_y, cam.tiles_x)
+    lim = np.kron(tl, np.ones((16, 16), np.int64))[:cam.height, :cam.width]
+    assert np.all(cnt <= lim)
+
+
+def test_train_steps_reduce_loss(engine):
+    w = scene.WORKLOADS["c1"]
+    gt = scene.random_params(w.n, w.s0, w.m_o, w.seed)
+    cam = scene.workload_cameras(w)[0]
+    cfg = T.RenderConfig.make(sh_degree=0)
+    engine.set_params(gt, w.n)
+    target, _, _ = engine.render(cam, cfg)
+    p0 = scene.perturb(gt, w.n, w.seed)
+    engine.set_params(p0, w.n)
+    engine.set_target(0, target)
+    losses = [engine.train_step(cam, cfg, T.AdamConfig.make(step=i + 1)) for i in range(30)]
+    assert losses[-1] < 0.7 * losses[0]
+    assert engine.launch_count() > 0

@@ -110,6 +110,9 @@ ts_status ts_zero_grads(ts_ctx* ctx);
 ts_status ts_grad_buffer(ts_ctx* ctx, float** dev_ptr, int64_t* count); /* 59*N device fp32 (for NCCL) */
 ts_status ts_param_buffer(ts_ctx* ctx, float** dev_ptr, int64_t* count);
 ts_status ts_stats_buffer(ts_ctx* ctx, float** dev_accum, float** dev_count);
+/* grow the parameter / gradient buffers to >= min_len floats (zero-filled pad
+ * beyond 59*N) so collectives can use equal-sized shards */
+ts_status ts_reserve_flat(ts_ctx* ctx, int64_t min_len);
 
 /* ---- optimizer ---- */
 ts_status ts_adam_step(ts_ctx* ctx, const ts_adam_config* cfg);
@@ -141,10 +144,12 @@ ts_status ts_debug_instances(ts_ctx* ctx, int64_t* n_inst, uint64_t* keys /* I *
 ts_status ts_debug_grad2d(ts_ctx* ctx, const float* dL_dC_hwc, float* g2d9 /* N*9 */);
 /* counters of the last view: {V visible, I instances, Ip processed instances, P pixels} */
 ts_status ts_view_stats(ts_ctx* ctx, int64_t out[4]);
-/* per-stage device times (ms) of the last forward/backward when profiling is on:
+/* per-stage device times: while profiling is on, every stage of every call is
+ * bracketed by CUDA events on the context stream; ts_stage_times returns the
+ * summed milliseconds and call counts per stage since ts_set_profiling(1):
  * {preprocess, depth_sort, scan, duplicate, tile_sort, ranges, blend, loss, blend_bwd, project_bwd, adam} */
 ts_status ts_set_profiling(ts_ctx* ctx, int32_t on);
-ts_status ts_stage_times(ts_ctx* ctx, float* ms, int32_t n);
+ts_status ts_stage_times(ts_ctx* ctx, float* ms, int32_t* counts /* may be NULL */, int32_t n);
 /* number of kernels this context has launched (evidence counter) */
 ts_status ts_launch_count(ts_ctx* ctx, int64_t* n);
 

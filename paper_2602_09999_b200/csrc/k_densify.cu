@@ -54,7 +54,9 @@ __global__ void densify_flags_kernel(const float* __restrict__ P, const float* _
     fA[g] = (!split && !prn) ? 1u : 0u;
     fB[g] = (sel && small && !prn) ? 1u : 0u;
     fC[g] = (split && !pchild) ? 2u : 0u;
+    // pruned rows of the post-densify set: the original, its clone, or both children
     uint32_t pruned = (!split && prn) ? 1u : 0u;
+    if (sel && small && prn) pruned += 1u;
     if (split && pchild) pruned += 2u;
     if (sel && small) atomicAdd(st + 0, 1u);
     if (split) atomicAdd(st + 1, 1u);

@@ -89,12 +89,22 @@ ts_status oom(Context& c) { return TS_ERR_OOM; }
 
 void stage_begin(Context& c, int k) {
     if (!c.profiling) return;
-    cudaEventRecord(c.ev_b[k], c.stream);
+    if (c.ev_cursor == c.ev_b.size()) {
+        cudaEvent_t b, e;
+        cudaEventCreate(&b);
+        cudaEventCreate(&e);
+        c.ev_b.push_back(b);
+        c.ev_e.push_back(e);
+        c.ev_stage.push_back(k);
+    }
+    c.ev_stage[c.ev_cursor] = k;
+    cudaEventRecord(c.ev_b[c.ev_cursor], c.stream);
 }
 void stage_end(Context& c, int k) {
     if (!c.profiling) return;
-    cudaEventRecord(c.ev_e[k], c.stream);
-    c.ev_rec[k] = true;
+    (void)k;
+    cudaEventRecord(c.ev_e[c.ev_cursor], c.stream);
+    ++c.ev_cursor;
 }
 
 bool valid_camera(const ts_camera* cam, std::string* why) {
@@ -325,11 +335,6 @@ ts_status ts_create(int32_t device, void* stream, ts_ctx** out) {
         return TS_ERR_OOM;
     }
     cudaMemsetAsync(c.counters.p, 0, 16 * 4, c.stream);
-    for (int k = 0; k < kNumStages; ++k) {
-        cudaEventCreate(&c.ev_b[k]);
-        cudaEventCreate(&c.ev_e[k]);
-    }
-    c.ev_init = true;
     if (ensure_gaussian_buffers(c, 1) != TS_OK) {
         delete x;
         return TS_ERR_OOM;
@@ -355,11 +360,10 @@ ts_status ts_destroy(ts_ctx* x) {
     release(c.starts), release(c.rhist), release(c.scan_state), release(c.scan_tmp), release(c.counters);
     release(c.rgb), release(c.Tfin), release(c.dLdC), release(c.hwc_stage), release(c.tgt), release(c.pcount);
     release(c.loss_acc), release(c.loss_tmp), release(c.targets), release(c.dens);
-    if (c.ev_init)
-        for (int k = 0; k < kNumStages; ++k) {
-            cudaEventDestroy(c.ev_b[k]);
-            cudaEventDestroy(c.ev_e[k]);
-        }
+    for (size_t k = 0; k < c.ev_b.size(); ++k) {
+        cudaEventDestroy(c.ev_b[k]);
+        cudaEventDestroy(c.ev_e[k]);
+    }
     if (c.own_stream) cudaStreamDestroy(c.stream);
     delete x;
     return TS_OK;
@@ -504,6 +508,22 @@ ts_status ts_stats_buffer(ts_ctx* x, float** a, float** cnt) {
     TS_CHECK_CTX(x);
     if (a) *a = x->c.accum.p;
     if (cnt) *cnt = x->c.vcount.p;
+    return TS_OK;
+}
+
+ts_status ts_reserve_flat(ts_ctx* x, int64_t min_len) {
+    TS_CHECK_CTX(x);
+    Context& c = x->c;
+    CK(cudaSetDevice(c.device));
+    const size_t L = size_t(59) * c.N;
+    if (min_len < 0) return validation(c, "min_len < 0");
+    if (size_t(min_len) > c.params.cap || size_t(min_len) > c.grads.cap) {
+        if (!ensure(c, c.params, size_t(min_len), true) || !ensure(c, c.grads, size_t(min_len), true))
+            return TS_ERR_OOM;
+    }
+    if (c.params.cap > L) CK(cudaMemsetAsync(c.params.p + L, 0, (c.params.cap - L) * 4, c.stream));
+    if (c.grads.cap > L) CK(cudaMemsetAsync(c.grads.p + L, 0, (c.grads.cap - L) * 4, c.stream));
+    CK(cudaStreamSynchronize(c.stream));
     return TS_OK;
 }
 
@@ -709,19 +729,29 @@ ts_status ts_view_stats(ts_ctx* x, int64_t out[4]) {
 
 ts_status ts_set_profiling(ts_ctx* x, int32_t on) {
     TS_CHECK_CTX(x);
-    x->c.profiling = on != 0;
-    for (int k = 0; k < kNumStages; ++k) x->c.ev_rec[k] = false;
+    Context& c = x->c;
+    if (c.profiling || on) cudaStreamSynchronize(c.stream);
+    c.profiling = on != 0;
+    if (on) c.ev_cursor = 0;
     return TS_OK;
 }
 
-ts_status ts_stage_times(ts_ctx* x, float* ms, int32_t n) {
+ts_status ts_stage_times(ts_ctx* x, float* ms, int32_t* counts, int32_t n) {
     TS_CHECK_CTX(x);
     Context& c = x->c;
     if (!ms) return validation(c, "NULL output");
     CK(cudaStreamSynchronize(c.stream));
-    for (int k = 0; k < n && k < kNumStages; ++k) {
+    for (int k = 0; k < n; ++k) {
         ms[k] = 0.f;
-        if (c.ev_rec[k]) cudaEventElapsedTime(&ms[k], c.ev_b[k], c.ev_e[k]);
+        if (counts) counts[k] = 0;
+    }
+    for (size_t i = 0; i < c.ev_cursor; ++i) {
+        const int k = c.ev_stage[i];
+        if (k >= n) continue;
+        float t = 0.f;
+        CK(cudaEventElapsedTime(&t, c.ev_b[i], c.ev_e[i]));
+        ms[k] += t;
+        if (counts) counts[k] += 1;
     }
     return TS_OK;
 }

@@ -4,6 +4,7 @@
 
 #include <cstdint>
 #include <string>
+#include <vector>
 
 #include "../../include/tilesplat_c.h"
 
@@ -86,10 +87,9 @@ struct Context {
 
     // profiling
     bool profiling = false;
-    cudaEvent_t ev_b[kNumStages] = {}, ev_e[kNumStages] = {};
-    bool ev_rec[kNumStages] = {};
-    float stage_ms[kNumStages] = {};
-    bool ev_init = false;
+    std::vector<cudaEvent_t> ev_b, ev_e;
+    std::vector<int> ev_stage;
+    size_t ev_cursor = 0;
 
     DevBuf<uint32_t> dens;       // densify scratch
 };

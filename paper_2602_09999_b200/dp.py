@@ -1,0 +1,99 @@
+"""Data-parallel training step over views.
+
+Gaussians, Adam moments and densification state are replicated on every rank;
+rank r renders its own slice of the view batch and accumulates gradients in
+its flat 59*N buffer; one collective over that buffer (NCCL over NVLink on the
+B200 nodes, gloo in the CPU tests) sums them (batch gradient = sum
+of per-view gradients), then every rank applies the same optimizer update, so
+parameters stay bitwise identical across ranks.
+
+Two exchange modes:
+  * "allreduce": all_reduce(grads) + replicated fused Adam (rung 1);
+  * "sharded":   all_reduce(grads) is replaced by reduce_scatter(grads) ->
+                 Adam on this rank's 1/G slice -> all_gather(params) (rung 2),
+                 so each rank runs 1/G of the 28 B/element Adam sweep.
+
+The engine is anything exposing the Engine surface used below (the CUDA
+Engine in production; the tests pass a CPU stand-in to exercise the
+collective logic with gloo).
+"""
+from __future__ import annotations
+
+import torch
+import torch.distributed as dist
+
+
+class _CudaArray:
+    """Zero-copy __cuda_array_interface__ view of a device fp32 buffer."""
+
+    def __init__(self, ptr: int, n: int):
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<f4", "data": (ptr, False), "version": 3,
+                                         "strides": None, "stream": None}
+
+
+def device_tensor(ptr: int, n: int, device: int) -> torch.Tensor:
+    with torch.cuda.device(device):
+        return torch.as_tensor(_CudaArray(ptr, n), device=f"cuda:{device}")
+
+
+def shard_bounds(length: int, world: int, rank: int, align: int = 4):
+    """[begin, end) of rank's slice of a flat buffer, 16-byte aligned slices."""
+    per = -(-length // world)
+    per = -(-per // align) * align
+    b = min(length, rank * per)
+    e = min(length, b + per)
+    return b, e, per
+
+
+class DataParallelStep:
+    def __init__(self, engine, mode: str = "allreduce", group=None):
+        assert mode in ("allreduce", "sharded")
+        self.e = engine
+        self.mode = mode
+        self.group = group
+        self.world = dist.get_world_size(group) if dist.is_available() and dist.is_initialized() else 1
+        self.rank = dist.get_rank(group) if self.world > 1 else 0
+
+    def my_views(self, n_views: int):
+        """Views {r, r+G, ...} of an n_views batch (disjoint slices)."""
+        return list(range(self.rank, n_views, self.world))
+
+    def accumulate(self, views):
+        """views: iterable of (camera, render_config, target_slot) rendered by THIS rank."""
+        for cam, cfg, slot in views:
+            self.e.render(cam, cfg, outputs=False)
+            self.e.training_loss(slot=slot, want_value=False)
+            self.e.backward(None)
+
+    def exchange_and_step(self, adam):
+        if self.world == 1:
+            self.e.adam_step(adam)
+            return
+        g = self.e.grad_tensor()
+        if self.mode == "allreduce":
+            dist.all_reduce(g, op=dist.ReduceOp.SUM, group=self.group)
+            self.e.adam_step(adam)
+            return
+        L = g.numel()
+        b, e, per = shard_bounds(L, self.world, self.rank)
+        padded = self.e.grad_tensor(padded_to=per * self.world)
+        out = torch.empty(per, dtype=padded.dtype, device=padded.device)
+        dist.reduce_scatter_tensor(out, padded, op=dist.ReduceOp.SUM, group=self.group)
+        padded[self.rank * per:(self.rank + 1) * per].copy_(out)
+        self.e.adam_step(adam, begin=b, end=e)
+        p = self.e.param_tensor(padded_to=per * self.world)
+        dist.all_gather_into_tensor(p, p[self.rank * per:(self.rank + 1) * per].clone(), group=self.group)
+        # slices of the other ranks' gradients were not consumed by this rank's Adam
+        self.e.zero_grads()
+
+    def step(self, views, adam):
+        self.accumulate(views)
+        self.exchange_and_step(adam)
+
+    def reduce_densify_stats(self):
+        """Sum (accum, count) across ranks before a densify event (replicas stay identical)."""
+        if self.world == 1:
+            return
+        a, c = self.e.stats_tensors()
+        dist.all_reduce(a, group=self.group)
+        dist.all_reduce(c, group=self.group)

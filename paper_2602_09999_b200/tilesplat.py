@@ -59,6 +59,7 @@ _SIGS = {
     "ts_grad_buffer": [_vp, ctypes.POINTER(_vp), ctypes.POINTER(_i64)],
     "ts_param_buffer": [_vp, ctypes.POINTER(_vp), ctypes.POINTER(_i64)],
     "ts_stats_buffer": [_vp, ctypes.POINTER(_vp), ctypes.POINTER(_vp)],
+    "ts_reserve_flat": [_vp, _i64],
     "ts_adam_step": [_vp, _vp],
     "ts_adam_step_range": [_vp, _vp, _i64, _i64],
     "ts_train_step": [_vp, _vp, _vp, _vp, _i32, _vp, _vp],
@@ -71,7 +72,7 @@ _SIGS = {
     "ts_debug_grad2d": [_vp, _vp, _vp],
     "ts_view_stats": [_vp, _vp],
     "ts_set_profiling": [_vp, _i32],
-    "ts_stage_times": [_vp, _vp, _i32],
+    "ts_stage_times": [_vp, _vp, _vp, _i32],
     "ts_launch_count": [_vp, ctypes.POINTER(_i64)],
     "ts_host_alloc": [ctypes.c_size_t, ctypes.POINTER(_vp)],
     "ts_host_free": [_vp],
@@ -267,6 +268,34 @@ class Engine:
         self._check(self._L.ts_stats_buffer(self._h, ctypes.byref(a), ctypes.byref(c)), "ts_stats_buffer")
         return int(a.value or 0), int(c.value or 0)
 
+    # ---- torch views for collectives (zero-copy, same device memory) ----
+    def reserve_flat(self, min_len: int):
+        self._check(self._L.ts_reserve_flat(self._h, int(min_len)), "ts_reserve_flat")
+
+    def grad_tensor(self, padded_to: int | None = None):
+        from .dp import device_tensor
+        p, n = self.grad_buffer()
+        if padded_to is not None and padded_to > n:
+            self.reserve_flat(padded_to)
+            p, n = self.grad_buffer()
+            n = padded_to
+        return device_tensor(p, n, self.device)
+
+    def param_tensor(self, padded_to: int | None = None):
+        from .dp import device_tensor
+        p, n = self.param_buffer()
+        if padded_to is not None and padded_to > n:
+            self.reserve_flat(padded_to)
+            p, n = self.param_buffer()
+            n = padded_to
+        return device_tensor(p, n, self.device)
+
+    def stats_tensors(self):
+        from .dp import device_tensor
+        a, c = self.stats_buffer()
+        n = self.num_gaussians()
+        return device_tensor(a, n, self.device), device_tensor(c, n, self.device)
+
     # ---- parity / debug ----
     def debug_preprocess(self):
         n = self.num_gaussians()
@@ -306,9 +335,11 @@ class Engine:
         self._check(self._L.ts_set_profiling(self._h, 1 if on else 0), "ts_set_profiling")
 
     def stage_times(self):
+        """{stage: (total_ms, calls)} summed since set_profiling(True)."""
         out = np.zeros(len(STAGES), np.float32)
-        self._check(self._L.ts_stage_times(self._h, _ptr(out), len(STAGES)), "ts_stage_times")
-        return dict(zip(STAGES, (float(x) for x in out)))
+        cnt = np.zeros(len(STAGES), np.int32)
+        self._check(self._L.ts_stage_times(self._h, _ptr(out), _ptr(cnt), len(STAGES)), "ts_stage_times")
+        return {k: (float(a), int(b)) for k, a, b in zip(STAGES, out, cnt)}
 
     def launch_count(self) -> int:
         n = ctypes.c_int64()

@@ -19,13 +19,10 @@ for i in range(5):
     e.train_step(cam, cfg, T.AdamConfig.make(step=i + 1), want_loss=False)
 e.synchronize()
 e.set_profiling(True)
-tot = {}
 K = 10
 for i in range(K):
     e.train_step(cam, cfg, T.AdamConfig.make(step=i + 6), want_loss=False)
-    st = e.stage_times()
-    for k, v in st.items():
-        tot[k] = tot.get(k, 0) + v / K
+tot = {k: v[0] / max(1, v[1]) for k, v in e.stage_times().items()}
 e.set_profiling(False)
 e.synchronize()
 t0 = time.perf_counter()

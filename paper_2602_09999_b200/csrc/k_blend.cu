@@ -1,99 +1,140 @@
 // K6 blend_fwd and K8 blend_bwd: one CTA per 16x16 tile, one thread per pixel.
 //
 // Forward (fragment_alpha SPEC.md:316-324, blend_tile :326-334): the tile's
-// depth-ordered instance list is staged 256 splats at a time into shared memory
-// (gathered by Gaussian index, 48 B rows), every pixel blends front to back,
-// "blend then stop" at T < 1e-4, and the CTA leaves as soon as all 256 pixels
-// are done (__syncthreads_count).  The keep decision Q <= k2 uses the exact-op
+// depth-ordered instance list is staged 128 splats at a time into shared memory
+// (gathered by Gaussian index, 48 B rows); each of 64 threads blends a 1x4 pixel
+// column front to back, "blend then stop" at T < 1e-4, and the CTA leaves as
+// soon as all 256 pixels are done (__syncthreads_count).  The keep decision Q <= k2 uses the exact-op
 // quadratic form (bit-identical to the oracle); alpha uses MUFU.EX2.
 //
 // Backward (backward_per_pixel SPEC.md:382-390): front-to-back replay with the
 // suffix-colour recurrence (no division by (1 - alpha) of T).
-// Per fragment, the 32 lanes of a warp (32 pixels) reduce their 9 partial
-// gradients with a transposed shuffle reduction (12 SHFL instead of 45), the 8
-// warps merge in shared memory, and each (Gaussian, tile) pair issues ONE set of
-// vector atomics (RED.F32x4) into the per-Gaussian 2D-gradient accumulator.
+// Each thread owns a 1x4 pixel column (64 threads per tile): per fragment it
+// sums its 4 pixels' 9 partial gradients, the warp (128 pixels) reduces them
+// with a transposed shuffle reduction (12 SHFL instead of 45), the 2 warps merge
+// in shared memory, and each (Gaussian, tile) pair issues ONE set of vector
+// atomics (RED.F32x4) into the per-Gaussian 2D-gradient accumulator.  A
+// conservative per-warp row cull skips splats whose alpha >= tau ellipse misses
+// the warp's 8 rows before any per-pixel work.
 #include "ts_internal.cuh"
 #include "ts_math.cuh"
 
 namespace ts {
 namespace {
 
-constexpr int kT = 256;
+constexpr int kT = 64;       // threads per tile CTA (2 warps)
+constexpr int kPPT = 4;      // pixels per thread (a 1x4 column)
+constexpr int kBatch = 128;  // splats staged per round
 constexpr float kNegHalfLog2e = -0.72134752044448170368f;  // -0.5 * log2(e)
 
+// conservative half-height of the alpha >= tau ellipse: max |dy| over Q <= k2
+// is sqrt(k2 * Sigma_yy), Sigma_yy = A / (A C - B^2); padded so the per-warp
+// row cull can never drop a fragment that the exact test would keep.
+__device__ __forceinline__ float ellipse_ry(float A, float B, float C, float k2) {
+    const float syy = A / (A * C - B * B);
+    return sqrtf(fmaxf(k2 * syy, 0.f)) * 1.001f + 0.05f;
+}
+
+// pixel rows of thread `tid` in a 16x16 tile: warp w owns rows [8w, 8w+8),
+// lanes 0-15 rows 8w..8w+3, lanes 16-31 rows 8w+4..8w+7; column = tid % 16.
+__device__ __forceinline__ int tile_row0(int tid) { return (tid >> 5) * 8 + ((tid >> 4) & 1) * 4; }
+
+template <bool kCompat>
 __global__ void __launch_bounds__(kT) blend_fwd_kernel(const uint32_t* __restrict__ starts,
                                                       const uint32_t* __restrict__ ival,
                                                       const float4* __restrict__ splat, DevCam cam,
                                                       ts_render_config cfg, float* __restrict__ rgb,
                                                       float* __restrict__ Tfin, uint32_t* __restrict__ pcount,
                                                       uint32_t* __restrict__ ip_counter) {
-    __shared__ float4 sA[kT];  // mx, my, k2, o
-    __shared__ float4 sB[kT];  // A, 2B, C
-    __shared__ float4 sC[kT];  // r, g, b
+    __shared__ float4 sA[kBatch];  // mx, my, k2, o
+    __shared__ float4 sB[kBatch];  // A, 2B, C, ry
+    __shared__ float4 sC[kBatch];  // r, g, b
     __shared__ uint32_t s_max;
     const int t = blockIdx.x;
     const int tx = t % cam.tiles_x, ty = t / cam.tiles_x;
-    const int px = tx * 16 + (threadIdx.x & 15), py = ty * 16 + (threadIdx.x >> 4);
-    const bool inside = px < cam.w && py < cam.h;
+    const int px = tx * 16 + (threadIdx.x & 15);
+    const int py0 = ty * 16 + tile_row0(threadIdx.x);
+    const float wy0 = float(ty * 16 + (threadIdx.x >> 5) * 8), wy1 = wy0 + 7.f;
     const uint32_t b = starts[t], e = starts[t + 1];
-    const float fpx = float(px), fpy = float(py);
-    float T = 1.f, C0 = 0.f, C1 = 0.f, C2 = 0.f;
-    uint32_t last = 0;
-    bool done = !inside;
-    const bool compat = cfg.early_stop_compat != 0;
+    const float fpx = float(px);
+    float T[kPPT], C0[kPPT], C1[kPPT], C2[kPPT];
+    uint32_t last[kPPT];
+    uint32_t done = 0;
+#pragma unroll
+    for (int k = 0; k < kPPT; ++k) {
+        T[k] = 1.f;
+        C0[k] = C1[k] = C2[k] = 0.f;
+        last[k] = 0;
+        if (px >= cam.w || py0 + k >= cam.h) done |= 1u << k;
+    }
     if (threadIdx.x == 0) s_max = 0;
-    for (uint32_t base = b; base < e; base += kT) {
-        if (__syncthreads_count(done) == kT) break;
-        const uint32_t i = base + threadIdx.x;
-        if (i < e) {
-            const uint32_t g = __ldg(ival + i);
-            const float4 s0 = __ldg(splat + 3 * g), s1 = __ldg(splat + 3 * g + 1), s2 = __ldg(splat + 3 * g + 2);
-            sA[threadIdx.x] = s0;
-            sB[threadIdx.x] = make_float4(s1.x, tsx::add(s1.y, s1.y), s1.z, 0.f);
-            sC[threadIdx.x] = s2;
+    for (uint32_t base = b; base < e; base += kBatch) {
+        if (__syncthreads_count(done == 0xFu) == kT) break;
+#pragma unroll
+        for (int u = 0; u < kBatch / kT; ++u) {
+            const uint32_t i = base + threadIdx.x + u * kT;
+            if (i < e) {
+                const uint32_t g = __ldg(ival + i);
+                const float4 s0 = __ldg(splat + 3 * g), s1 = __ldg(splat + 3 * g + 1), s2 = __ldg(splat + 3 * g + 2);
+                sA[threadIdx.x + u * kT] = s0;
+                sB[threadIdx.x + u * kT] = make_float4(s1.x, tsx::add(s1.y, s1.y), s1.z, ellipse_ry(s1.x, s1.y, s1.z, s0.z));
+                sC[threadIdx.x + u * kT] = s2;
+            }
         }
         __syncthreads();
-        const int n = int(tmin<uint32_t>(kT, e - base));
-        if (!done) {
+        const int n = int(tmin<uint32_t>(kBatch, e - base));
+        if (done != 0xFu) {
             for (int j = 0; j < n; ++j) {
-                const float4 a = sA[j];
                 const float4 q = sB[j];
-                const float dx = tsx::sub(fpx, a.x), dy = tsx::sub(fpy, a.y);
-                const float Q = tsx::conic_q(q.x, q.y, q.z, dx, dy);
-                if (!(Q <= a.z)) continue;
-                const float G = tsx::ex2_approx(Q * kNegHalfLog2e);
-                const float al = fminf(0.99f, a.w * G);
-                const float om = 1.f - al;
-                if (compat && T * om < 1e-4f) {
-                    done = true;
-                    break;
+                const float4 a = sA[j];
+                if (a.y + q.w < wy0 || a.y - q.w > wy1) continue;  // splat misses this warp's 8 rows
+                const float dx = tsx::sub(fpx, a.x);
+                const float adx = tsx::mul(q.x, dx);
+#pragma unroll
+                for (int k = 0; k < kPPT; ++k) {
+                    if (done & (1u << k)) continue;
+                    const float dy = tsx::sub(float(py0 + k), a.y);
+                    // Q = dx*(A*dx + 2B*dy) + dy*(C*dy), exact order (tsx::conic_q)
+                    const float Q = tsx::add(tsx::mul(dx, tsx::add(adx, tsx::mul(q.y, dy))),
+                                             tsx::mul(dy, tsx::mul(q.z, dy)));
+                    if (!(Q <= a.z)) continue;
+                    const float G = tsx::ex2_approx(Q * kNegHalfLog2e);
+                    const float al = fminf(0.99f, a.w * G);
+                    const float om = 1.f - al;
+                    if (kCompat && T[k] * om < 1e-4f) {
+                        done |= 1u << k;
+                        continue;
+                    }
+                    const float w = al * T[k];
+                    const float4 col = sC[j];
+                    C0[k] = fmaf(w, col.x, C0[k]);
+                    C1[k] = fmaf(w, col.y, C1[k]);
+                    C2[k] = fmaf(w, col.z, C2[k]);
+                    T[k] = T[k] * om;
+                    last[k] = base - b + uint32_t(j) + 1u;
+                    if (!kCompat && T[k] < 1e-4f) done |= 1u << k;
                 }
-                const float w = al * T;
-                const float4 col = sC[j];
-                C0 = fmaf(w, col.x, C0);
-                C1 = fmaf(w, col.y, C1);
-                C2 = fmaf(w, col.z, C2);
-                T = T * om;
-                last = base - b + uint32_t(j) + 1u;
-                if (!compat && T < 1e-4f) {
-                    done = true;
-                    break;
-                }
+                if (done == 0xFu) break;
             }
         }
     }
-    if (inside) {
-        const int P = cam.w * cam.h;
-        const int p = py * cam.w + px;
-        rgb[p] = C0 + T * cfg.bg[0];
-        rgb[P + p] = C1 + T * cfg.bg[1];
-        rgb[2 * P + p] = C2 + T * cfg.bg[2];
-        Tfin[p] = T;
-        pcount[p] = last;
+    const int P = cam.w * cam.h;
+    uint32_t mymax = 0;
+#pragma unroll
+    for (int k = 0; k < kPPT; ++k) {
+        const int py = py0 + k;
+        if (px < cam.w && py < cam.h) {
+            const int p = py * cam.w + px;
+            rgb[p] = C0[k] + T[k] * cfg.bg[0];
+            rgb[P + p] = C1[k] + T[k] * cfg.bg[1];
+            rgb[2 * P + p] = C2[k] + T[k] * cfg.bg[2];
+            Tfin[p] = T[k];
+            pcount[p] = last[k];
+        }
+        mymax = max(mymax, last[k]);
     }
     // processed list length of this tile (bench counter Ip)
-    const uint32_t wm = __reduce_max_sync(0xffffffffu, last);
+    const uint32_t wm = __reduce_max_sync(0xffffffffu, mymax);
     __syncthreads();
     if ((threadIdx.x & 31) == 0) atomicMax(&s_max, wm);
     __syncthreads();
@@ -155,122 +196,149 @@ __device__ __forceinline__ float red9(const float (&v)[9], int lane) {
 
 constexpr int kGS = 12;  // smem gradient row stride (floats)
 
+__device__ __forceinline__ float rcp_approx(float x) {
+    float y;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
 __global__ void __launch_bounds__(kT) blend_bwd_kernel(const uint32_t* __restrict__ starts,
                                                       const uint32_t* __restrict__ ival,
                                                       const float4* __restrict__ splat, DevCam cam,
                                                       const float* __restrict__ rgb, const uint32_t* __restrict__ pcount,
                                                       const float* __restrict__ dLdC, float4* __restrict__ g2d) {
-    __shared__ float4 sA[kT];  // mx, my, k2, o
-    __shared__ float4 sB[kT];  // A, 2B, C
-    __shared__ float4 sC[kT];  // r, g, b
-    __shared__ uint32_t sIdx[kT];
-    __shared__ float sG[kT * kGS];
+    __shared__ float4 sA[kBatch];  // mx, my, k2, o
+    __shared__ float4 sB[kBatch];  // A, 2B, C, ry
+    __shared__ float4 sC[kBatch];  // r, g, b
+    __shared__ uint32_t sIdx[kBatch];
+    __shared__ float sG[kBatch * kGS];
     __shared__ uint32_t s_max;
     const int lane = threadIdx.x & 31;
     const int t = blockIdx.x;
     const int tx = t % cam.tiles_x, ty = t / cam.tiles_x;
-    const int px = tx * 16 + (threadIdx.x & 15), py = ty * 16 + (threadIdx.x >> 4);
-    const bool inside = px < cam.w && py < cam.h;
+    const int px = tx * 16 + (threadIdx.x & 15);
+    const int py0 = ty * 16 + tile_row0(threadIdx.x);
+    const float wy0 = float(ty * 16 + (threadIdx.x >> 5) * 8), wy1 = wy0 + 7.f;
     const int P = cam.w * cam.h;
-    const int p = py * cam.w + px;
-    float g0 = 0.f, g1 = 0.f, g2 = 0.f, R0 = 0.f, R1 = 0.f, R2 = 0.f;
-    uint32_t cnt = 0;
-    if (inside) {
-        g0 = dLdC[p];
-        g1 = dLdC[P + p];
-        g2 = dLdC[2 * P + p];
-        R0 = rgb[p];
-        R1 = rgb[P + p];
-        R2 = rgb[2 * P + p];
-        cnt = pcount[p];
+    const float fpx = float(px);
+    // per pixel: upstream gradient g, suffix colour U = C_final - prefix (incl. background), T, count
+    float g0[kPPT], g1[kPPT], g2[kPPT], U0[kPPT], U1[kPPT], U2[kPPT], T[kPPT];
+    uint32_t cnt[kPPT];
+    uint32_t mymax = 0;
+#pragma unroll
+    for (int k = 0; k < kPPT; ++k) {
+        const int py = py0 + k;
+        T[k] = 1.f;
+        g0[k] = g1[k] = g2[k] = U0[k] = U1[k] = U2[k] = 0.f;
+        cnt[k] = 0;
+        if (px < cam.w && py < cam.h) {
+            const int p = py * cam.w + px;
+            g0[k] = dLdC[p];
+            g1[k] = dLdC[P + p];
+            g2[k] = dLdC[2 * P + p];
+            U0[k] = rgb[p];
+            U1[k] = rgb[P + p];
+            U2[k] = rgb[2 * P + p];
+            cnt[k] = pcount[p];
+        }
+        mymax = max(mymax, cnt[k]);
     }
     if (threadIdx.x == 0) s_max = 0;
     __syncthreads();
-    const uint32_t wm = __reduce_max_sync(0xffffffffu, cnt);
+    const uint32_t wm = __reduce_max_sync(0xffffffffu, mymax);
     if (lane == 0) atomicMax(&s_max, wm);
     __syncthreads();
     const uint32_t b = starts[t];
     const uint32_t e = min(starts[t + 1], b + s_max);
     const int slot = red9_slot(lane);
-    const float fpx = float(px), fpy = float(py);
-    float T = 1.f, P0 = 0.f, P1 = 0.f, P2 = 0.f;
-    for (uint32_t base = b; base < e; base += kT) {
-        const uint32_t i = base + threadIdx.x;
-        if (i < e) {
-            const uint32_t g = __ldg(ival + i);
-            const float4 s0 = __ldg(splat + 3 * g), s1 = __ldg(splat + 3 * g + 1), s2 = __ldg(splat + 3 * g + 2);
-            sA[threadIdx.x] = s0;
-            sB[threadIdx.x] = make_float4(s1.x, tsx::add(s1.y, s1.y), s1.z, 0.f);
-            sC[threadIdx.x] = s2;
-            sIdx[threadIdx.x] = g;
-        }
+    for (uint32_t base = b; base < e; base += kBatch) {
 #pragma unroll
-        for (int k = 0; k < kGS; ++k) sG[threadIdx.x * kGS + k] = 0.f;
+        for (int u = 0; u < kBatch / kT; ++u) {
+            const int r = threadIdx.x + u * kT;
+            const uint32_t i = base + r;
+            if (i < e) {
+                const uint32_t g = __ldg(ival + i);
+                const float4 s0 = __ldg(splat + 3 * g), s1 = __ldg(splat + 3 * g + 1), s2 = __ldg(splat + 3 * g + 2);
+                sA[r] = s0;
+                sB[r] = make_float4(s1.x, tsx::add(s1.y, s1.y), s1.z, ellipse_ry(s1.x, s1.y, s1.z, s0.z));
+                sC[r] = s2;
+                sIdx[r] = g;
+            }
+#pragma unroll
+            for (int k = 0; k < kGS; ++k) sG[r * kGS + k] = 0.f;
+        }
         __syncthreads();
-        const int n = int(tmin<uint32_t>(kT, e - base));
+        const int n = int(tmin<uint32_t>(kBatch, e - base));
         const uint32_t local0 = base - b;
         for (int j = 0; j < n; ++j) {
-            const float4 a = sA[j];
             const float4 q = sB[j];
+            const float4 a = sA[j];
+            if (a.y + q.w < wy0 || a.y - q.w > wy1) continue;  // warp-uniform row cull
+            const float dx = tsx::sub(fpx, a.x);
+            const float adx = tsx::mul(q.x, dx);
+            const float b2dx = q.y * dx;
+            const float4 col = sC[j];
             float v[9];
 #pragma unroll
             for (int k = 0; k < 9; ++k) v[k] = 0.f;
-            bool keep = false;
-            float dx = 0.f, dy = 0.f, Q = 0.f;
-            if (local0 + uint32_t(j) < cnt) {
-                dx = tsx::sub(fpx, a.x);
-                dy = tsx::sub(fpy, a.y);
-                Q = tsx::conic_q(q.x, q.y, q.z, dx, dy);
-                keep = Q <= a.z;
-            }
-            if (!__any_sync(0xffffffffu, keep)) continue;
-            if (keep) {
-                const float4 col = sC[j];
+            bool any = false;
+            const uint32_t li = local0 + uint32_t(j);
+#pragma unroll
+            for (int k = 0; k < kPPT; ++k) {
+                if (li >= cnt[k]) continue;
+                const float dy = tsx::sub(float(py0 + k), a.y);
+                const float b2dy = tsx::mul(q.y, dy);
+                const float cdy = tsx::mul(q.z, dy);
+                const float Q = tsx::add(tsx::mul(dx, tsx::add(adx, b2dy)), tsx::mul(dy, cdy));
+                if (!(Q <= a.z)) continue;
+                any = true;
                 const float G = tsx::ex2_approx(Q * kNegHalfLog2e);
                 const float og = a.w * G;
                 const bool clamped = og > 0.99f;
                 const float al = clamped ? 0.99f : og;
-                const float w = al * T;
+                const float w = al * T[k];
                 const float om = 1.f - al;
-                const float iom = __frcp_rn(om);
-                v[6] = w * g0;
-                v[7] = w * g1;
-                v[8] = w * g2;
-                const float af0 = R0 - P0 - w * col.x;
-                const float af1 = R1 - P1 - w * col.y;
-                const float af2 = R2 - P2 - w * col.z;
-                const float dal = g0 * (T * col.x - af0 * iom) + g1 * (T * col.y - af1 * iom) +
-                                  g2 * (T * col.z - af2 * iom);
+                const float gc = g0[k] * col.x + g1[k] * col.y + g2[k] * col.z;
+                const float gU = g0[k] * U0[k] + g1[k] * U1[k] + g2[k] * U2[k];
+                const float dal = T[k] * gc - (gU - w * gc) * rcp_approx(om);
+                v[6] = fmaf(w, g0[k], v[6]);
+                v[7] = fmaf(w, g1[k], v[7]);
+                v[8] = fmaf(w, g2[k], v[8]);
                 if (!clamped) {
-                    v[5] = G * dal;
-                    const float dQ = -0.5f * G * a.w * dal;
-                    v[0] = dQ * -(2.f * q.x * dx + q.y * dy);
-                    v[1] = dQ * -(q.y * dx + 2.f * q.z * dy);
-                    v[2] = dQ * dx * dx;
-                    v[3] = dQ * 2.f * dx * dy;
-                    v[4] = dQ * dy * dy;
+                    v[5] = fmaf(G, dal, v[5]);
+                    const float dQ = -0.5f * og * dal;
+                    v[0] = fmaf(dQ, -fmaf(2.f, adx, b2dy), v[0]);
+                    v[1] = fmaf(dQ, -fmaf(2.f, cdy, b2dx), v[1]);
+                    v[2] = fmaf(dQ, dx * dx, v[2]);
+                    v[3] = fmaf(dQ, 2.f * dx * dy, v[3]);
+                    v[4] = fmaf(dQ, dy * dy, v[4]);
                 }
-                P0 = fmaf(w, col.x, P0);
-                P1 = fmaf(w, col.y, P1);
-                P2 = fmaf(w, col.z, P2);
-                T = T * om;
+                U0[k] = fmaf(-w, col.x, U0[k]);
+                U1[k] = fmaf(-w, col.y, U1[k]);
+                U2[k] = fmaf(-w, col.z, U2[k]);
+                T[k] = T[k] * om;
             }
+            if (!__any_sync(0xffffffffu, any)) continue;
             const float r = red9(v, lane);
             if (slot >= 0) atomicAdd(&sG[j * kGS + slot], r);
         }
         __syncthreads();
-        if (int(threadIdx.x) < n) {
-            const float* gs = sG + threadIdx.x * kGS;
-            const float4 a0 = make_float4(gs[0], gs[1], gs[2], gs[3]);
-            const float4 a1 = make_float4(gs[4], gs[5], gs[6], gs[7]);
-            const float a2 = gs[8];
-            const bool any = (a0.x != 0.f) | (a0.y != 0.f) | (a0.z != 0.f) | (a0.w != 0.f) | (a1.x != 0.f) |
-                             (a1.y != 0.f) | (a1.z != 0.f) | (a1.w != 0.f) | (a2 != 0.f);
-            if (any) {
-                const uint32_t g = sIdx[threadIdx.x];
-                atomicAdd(g2d + 3 * g, a0);
-                atomicAdd(g2d + 3 * g + 1, a1);
-                atomicAdd(reinterpret_cast<float*>(g2d + 3 * g + 2), a2);
+#pragma unroll
+        for (int u = 0; u < kBatch / kT; ++u) {
+            const int r = threadIdx.x + u * kT;
+            if (r < n) {
+                const float* gs = sG + r * kGS;
+                const float4 a0 = make_float4(gs[0], gs[1], gs[2], gs[3]);
+                const float4 a1 = make_float4(gs[4], gs[5], gs[6], gs[7]);
+                const float a2 = gs[8];
+                const bool nz = (a0.x != 0.f) | (a0.y != 0.f) | (a0.z != 0.f) | (a0.w != 0.f) | (a1.x != 0.f) |
+                                (a1.y != 0.f) | (a1.z != 0.f) | (a1.w != 0.f) | (a2 != 0.f);
+                if (nz) {
+                    const uint32_t g = sIdx[r];
+                    atomicAdd(g2d + 3 * g, a0);
+                    atomicAdd(g2d + 3 * g + 1, a1);
+                    atomicAdd(reinterpret_cast<float*>(g2d + 3 * g + 2), a2);
+                }
             }
         }
         __syncthreads();
@@ -281,8 +349,12 @@ __global__ void __launch_bounds__(kT) blend_bwd_kernel(const uint32_t* __restric
 
 void launch_blend_fwd(Context& c, const DevCam& cam, const ts_render_config& cfg) {
     const int Tn = cam.tiles_x * cam.tiles_y;
-    blend_fwd_kernel<<<Tn, kT, 0, c.stream>>>(c.starts.p, c.ival[0].p, c.splat.p, cam, cfg, c.rgb.p, c.Tfin.p,
-                                              c.pcount.p, c.counters.p + 2);
+    if (cfg.early_stop_compat)
+        blend_fwd_kernel<true><<<Tn, kT, 0, c.stream>>>(c.starts.p, c.ival[0].p, c.splat.p, cam, cfg, c.rgb.p,
+                                                        c.Tfin.p, c.pcount.p, c.counters.p + 2);
+    else
+        blend_fwd_kernel<false><<<Tn, kT, 0, c.stream>>>(c.starts.p, c.ival[0].p, c.splat.p, cam, cfg, c.rgb.p,
+                                                         c.Tfin.p, c.pcount.p, c.counters.p + 2);
     TS_LAUNCHED(c);
 }
 

@@ -150,9 +150,11 @@ int64_t launch_densify(Context& c, float thresh, float log_small, float log_big,
     if (cudaStreamSynchronize(c.stream) != cudaSuccess) return -1;
     const int64_t nA = tot[0], nB = tot[1], nC = tot[2], NA = nA + nB + nC;
     DevBuf<float> np, nm, nv;
-    if (!ensure(c, np, size_t(59) * std::max<int64_t>(NA, 1)) || !ensure(c, nm, size_t(59) * std::max<int64_t>(NA, 1)) ||
-        !ensure(c, nv, size_t(59) * std::max<int64_t>(NA, 1)))
-        return -1;
+    const size_t L = (size_t(59) * std::max<int64_t>(NA, 1) + 7) & ~size_t(3);
+    if (!ensure(c, np, L) || !ensure(c, nm, L) || !ensure(c, nv, L)) return -1;
+    cudaMemsetAsync(np.p, 0, L * 4, c.stream);
+    cudaMemsetAsync(nm.p, 0, L * 4, c.stream);
+    cudaMemsetAsync(nv.p, 0, L * 4, c.stream);
     if (N) {
         densify_scatter_kernel<<<blocks, bs, 0, c.stream>>>(c.params.p, c.m.p, c.v.p, N, fA, fB, fC, oA, oB, oC, nA,
                                                            nB, NA, np.p, nm.p, nv.p, seed, iter);
@@ -168,13 +170,13 @@ int64_t launch_densify(Context& c, float thresh, float log_small, float log_big,
     c.N = NA;
     // resize the remaining per-Gaussian buffers and reset gradients / statistics
     const size_t n1 = size_t(std::max<int64_t>(NA, 1));
-    if (!ensure(c, c.grads, 59 * n1) || !ensure(c, c.accum, n1) || !ensure(c, c.vcount, n1) ||
+    if (!ensure(c, c.grads, L) || !ensure(c, c.accum, n1) || !ensure(c, c.vcount, n1) ||
         !ensure(c, c.splat, 3 * n1) || !ensure(c, c.rect, n1) || !ensure(c, c.tcount, n1) ||
         !ensure(c, c.dkey[0], n1) || !ensure(c, c.dkey[1], n1) || !ensure(c, c.dperm[0], n1) ||
         !ensure(c, c.dperm[1], n1) || !ensure(c, c.offsets, n1 + 1) || !ensure(c, c.g2d, 3 * n1) ||
         !ensure(c, c.vis, n1))
         return -1;
-    cudaMemsetAsync(c.grads.p, 0, 59 * n1 * 4, c.stream);
+    cudaMemsetAsync(c.grads.p, 0, c.grads.cap * 4, c.stream);
     cudaMemsetAsync(c.accum.p, 0, n1 * 4, c.stream);
     cudaMemsetAsync(c.vcount.p, 0, n1 * 4, c.stream);
     cudaMemsetAsync(c.g2d.p, 0, 3 * n1 * 16, c.stream);

@@ -31,55 +31,55 @@ __device__ __forceinline__ void adam_one(float& th, float& g, float& m, float& v
     th = sub(th, div(mul(lr, mh), den));
 }
 
-__device__ __forceinline__ int group_of(int64_t i, int64_t N, int64_t* gi) {
-    const int64_t b1 = 3 * N, b2 = 6 * N, b3 = 10 * N, b4 = 11 * N, b5 = 14 * N;
-    if (i < b1) { *gi = i / 3; return 0; }
-    if (i < b2) { *gi = (i - b1) / 3; return 1; }
-    if (i < b3) { *gi = (i - b2) / 4; return 2; }
-    if (i < b4) { *gi = i - b3; return 3; }
-    if (i < b5) { *gi = (i - b4) / 3; return 4; }
-    *gi = (i - b5) / 45;
-    return 5;
+// flat-buffer group boundaries (elements): means | scales | quats | opacity | sh_dc | sh_rest
+struct Bounds {
+    uint32_t b1, b2, b3, b4, b5;
+};
+
+template <int MODE>
+__device__ __forceinline__ bool visible_of(uint32_t i, const Bounds& b, const uint8_t* __restrict__ vis) {
+    if (MODE != 2) return true;
+    uint32_t gi;
+    if (i < b.b1) gi = i / 3u;
+    else if (i < b.b2) gi = (i - b.b1) / 3u;
+    else if (i < b.b3) gi = (i - b.b2) >> 2;
+    else if (i < b.b4) gi = i - b.b3;
+    else if (i < b.b5) gi = (i - b.b4) / 3u;
+    else gi = (i - b.b5) / 45u;
+    return vis[gi] != 0;
 }
 
-__global__ void adam_kernel(float* __restrict__ th, float* __restrict__ g, float* __restrict__ m,
-                            float* __restrict__ v, int64_t N, int64_t begin, int64_t end, AdamArgs a,
-                            const uint8_t* __restrict__ vis) {
-    // vectorized body over [vb, ve) (multiples of 4), scalar head/tail
-    const int64_t vb = (begin + 3) & ~int64_t(3);
-    const int64_t ve = max(vb, end & ~int64_t(3));
-    const int64_t stride = int64_t(gridDim.x) * blockDim.x;
-    const int64_t tid = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    for (int64_t q = vb / 4 + tid; q < ve / 4; q += stride) {
-        float4 t4 = reinterpret_cast<float4*>(th)[q];
-        float4 g4 = reinterpret_cast<float4*>(g)[q];
-        float4 m4 = reinterpret_cast<float4*>(m)[q];
-        float4 v4 = reinterpret_cast<float4*>(v)[q];
-        float* tp = &t4.x;
-        float* gp = &g4.x;
-        float* mp = &m4.x;
-        float* vp = &v4.x;
+// One float4 (4 consecutive elements) per thread; elements outside [begin, end)
+// are written back unchanged.  Buffers are padded to a multiple of 4 floats.
+template <int MODE, bool ZERO>
+__global__ void __launch_bounds__(256) adam_kernel(float4* __restrict__ th, float4* __restrict__ g,
+                                                   float4* __restrict__ m, float4* __restrict__ v, uint32_t q0,
+                                                   uint32_t q1, uint32_t begin, uint32_t end, Bounds bd, AdamArgs a,
+                                                   const uint8_t* __restrict__ vis) {
+    const uint32_t q = q0 + blockIdx.x * 256u + threadIdx.x;
+    if (q >= q1) return;
+    float4 t4 = th[q], g4 = g[q], m4 = m[q], v4 = v[q];
+    float* tp = &t4.x;
+    float* gp = &g4.x;
+    float* mp = &m4.x;
+    float* vp = &v4.x;
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            int64_t gi;
-            const int grp = group_of(4 * q + k, N, &gi);
-            if (a.mode == 2 && !vis[gi]) continue;
-            adam_one(tp[k], gp[k], mp[k], vp[k], a.lr[grp], a);
-        }
-        reinterpret_cast<float4*>(th)[q] = t4;
-        reinterpret_cast<float4*>(m)[q] = m4;
-        reinterpret_cast<float4*>(v)[q] = v4;
-        if (a.zero) reinterpret_cast<float4*>(g)[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int k = 0; k < 4; ++k) {
+        const uint32_t i = 4u * q + k;
+        if (i < begin || i >= end) continue;
+        const float lr = i < bd.b1 ? a.lr[0]
+                         : i < bd.b2 ? a.lr[1]
+                         : i < bd.b3 ? a.lr[2]
+                         : i < bd.b4 ? a.lr[3]
+                         : i < bd.b5 ? a.lr[4]
+                                     : a.lr[5];
+        if (visible_of<MODE>(i, bd, vis)) adam_one(tp[k], gp[k], mp[k], vp[k], lr, a);
+        if (ZERO) gp[k] = 0.f;
     }
-    // scalar head [begin, vb) and tail [ve, end)
-    for (int64_t i = tid; i < (vb - begin) + (end - ve); i += stride) {
-        const int64_t idx = i < (vb - begin) ? begin + i : ve + (i - (vb - begin));
-        if (idx >= end) continue;
-        int64_t gi;
-        const int grp = group_of(idx, N, &gi);
-        if (!(a.mode == 2 && !vis[gi])) adam_one(th[idx], g[idx], m[idx], v[idx], a.lr[grp], a);
-        if (a.zero) g[idx] = 0.f;
-    }
+    th[q] = t4;
+    m[q] = m4;
+    v[q] = v4;
+    if (ZERO) g[q] = g4;
 }
 
 __global__ void hwc_to_chw_kernel(const float* __restrict__ hwc, float* __restrict__ chw, int P) {
@@ -260,12 +260,26 @@ void launch_adam(Context& c, const ts_adam_config& a, int64_t begin, int64_t end
     x.bc2 = a.bc2;
     x.mode = a.mode;
     x.zero = a.zero_grads;
-    const int64_t n4 = (end - begin) / 4 + 1;
-    const int bs = 256;
-    const int64_t want = (n4 + bs - 1) / bs;
-    const int blocks = int(std::min<int64_t>(want, int64_t(c.sm_count) * 8));
-    adam_kernel<<<std::max(blocks, 1), bs, 0, c.stream>>>(c.params.p, c.grads.p, c.m.p, c.v.p, c.N, begin, end, x,
-                                                          c.vis.p);
+    const uint32_t N = uint32_t(c.N);
+    const Bounds bd{3u * N, 6u * N, 10u * N, 11u * N, 14u * N};
+    const uint32_t q0 = uint32_t(begin / 4), q1 = uint32_t((end + 3) / 4);
+    const unsigned blocks = (q1 - q0 + 255u) / 256u;
+    auto* th = reinterpret_cast<float4*>(c.params.p);
+    auto* g = reinterpret_cast<float4*>(c.grads.p);
+    auto* m = reinterpret_cast<float4*>(c.m.p);
+    auto* v = reinterpret_cast<float4*>(c.v.p);
+    const uint32_t b = uint32_t(begin), e = uint32_t(end);
+    if (a.mode == 2) {
+        if (a.zero_grads)
+            adam_kernel<2, true><<<blocks, 256, 0, c.stream>>>(th, g, m, v, q0, q1, b, e, bd, x, c.vis.p);
+        else
+            adam_kernel<2, false><<<blocks, 256, 0, c.stream>>>(th, g, m, v, q0, q1, b, e, bd, x, c.vis.p);
+    } else {
+        if (a.zero_grads)
+            adam_kernel<1, true><<<blocks, 256, 0, c.stream>>>(th, g, m, v, q0, q1, b, e, bd, x, c.vis.p);
+        else
+            adam_kernel<1, false><<<blocks, 256, 0, c.stream>>>(th, g, m, v, q0, q1, b, e, bd, x, c.vis.p);
+    }
     TS_LAUNCHED(c);
 }
 

@@ -6,32 +6,30 @@
 // parameters, writes a 48 B splat row + 8 B rect + 4 B count + 4 B depth key.
 #include "ts_internal.cuh"
 #include "ts_math.cuh"
+#include "ts_stage.cuh"
 
 namespace ts {
 namespace {
 
 constexpr int kBlock = 128;
 
+template <int DEG>
 __global__ void __launch_bounds__(kBlock) preprocess_kernel(
     const float* __restrict__ P, int64_t N, DevCam cam, ts_render_config cfg, float4* __restrict__ splat,
     uint2* __restrict__ rect, uint32_t* __restrict__ tcount, uint32_t* __restrict__ dkey,
     uint32_t* __restrict__ dperm, uint32_t* __restrict__ vis_counter) {
     using namespace tsx;
-    __shared__ float sh_rest[kBlock * 45];
+    __shared__ __align__(16) float sh_rest[kBlock * 45 + 4];
     const Off off(N);
     const int64_t g0 = int64_t(blockIdx.x) * kBlock;
     const int64_t g = g0 + threadIdx.x;
-    const int deg = cfg.sh_degree;
-    const int nb = (deg + 1) * (deg + 1);
-    const int nrest = 3 * (nb - 1);
-    // cooperative, coalesced staging of the used SH prefix of each 45-float row
-    if (nrest > 0) {
-        const int64_t rows = tmin<int64_t>(kBlock, N - g0);
-        const float* src = P + off.rest + g0 * 45;
-        for (int i = threadIdx.x; i < rows * nrest; i += kBlock) {
-            int r = i / nrest, cc = i - r * nrest;
-            sh_rest[r * 45 + cc] = __ldg(src + int64_t(r) * 45 + cc);
-        }
+    constexpr int deg = DEG;
+    constexpr int nb = (deg + 1) * (deg + 1);
+    constexpr int nrest = 3 * (nb - 1);
+    int sshift = 0;
+    if constexpr (nrest > 0) {
+        const int rows = int(tmin<int64_t>(kBlock, N - g0));
+        sshift = stage_span<kBlock>(sh_rest, P + off.rest + g0 * 45, rows * 45);
     }
     __syncthreads();
     if (g >= N) return;
@@ -159,11 +157,11 @@ __global__ void __launch_bounds__(kBlock) preprocess_kernel(
             }
         }
         float rgb[3];
-        const float* rs = sh_rest + threadIdx.x * 45;
+        const float* rs = sh_rest + sshift + threadIdx.x * 45;
 #pragma unroll
         for (int ch = 0; ch < 3; ++ch) {
             float acc = Y[0] * P[off.dc + 3 * g + ch];
-            for (int k = 1; k < nb; ++k) acc += Y[k] * rs[3 * (k - 1) + ch];
+            _Pragma("unroll") for (int k = 1; k < nb; ++k) acc += Y[k] * rs[3 * (k - 1) + ch];
             acc += 0.5f;
             rgb[ch] = acc < 0.f ? 0.f : acc;
         }
@@ -223,9 +221,17 @@ __global__ void __launch_bounds__(kBlock) preprocess_kernel(
 void launch_preprocess(Context& c, const DevCam& cam, const ts_render_config& cfg) {
     if (c.N == 0) return;
     const int64_t blocks = (c.N + kBlock - 1) / kBlock;
-    preprocess_kernel<<<unsigned(blocks), kBlock, 0, c.stream>>>(c.params.p, c.N, cam, cfg, c.splat.p, c.rect.p,
-                                                                  c.tcount.p, c.dkey[0].p, c.dperm[0].p,
-                                                                  c.counters.p + 1);
+#define TS_PRE(D)                                                                                      \
+    preprocess_kernel<D><<<unsigned(blocks), kBlock, 0, c.stream>>>(c.params.p, c.N, cam, cfg, c.splat.p, \
+                                                                     c.rect.p, c.tcount.p, c.dkey[0].p,   \
+                                                                     c.dperm[0].p, c.counters.p + 1)
+    switch (cfg.sh_degree) {
+        case 0: TS_PRE(0); break;
+        case 1: TS_PRE(1); break;
+        case 2: TS_PRE(2); break;
+        default: TS_PRE(3); break;
+    }
+#undef TS_PRE
     TS_LAUNCHED(c);
 }
 

@@ -8,41 +8,44 @@
 // memory so every global access is coalesced.
 #include "ts_internal.cuh"
 #include "ts_math.cuh"
+#include "ts_stage.cuh"
 
 namespace ts {
 namespace {
 
 constexpr int kBlock = 128;
 
+template <int DEG, bool ACCUM>
 __global__ void __launch_bounds__(kBlock) project_bwd_kernel(const float* __restrict__ P, float* __restrict__ G,
                                                              float4* __restrict__ g2d,
                                                              const uint32_t* __restrict__ tcount,
                                                              float* __restrict__ accum, float* __restrict__ vcount,
                                                              uint8_t* __restrict__ vis, int64_t N, DevCam cam,
                                                              ts_render_config cfg) {
-    __shared__ float s_par[kBlock * 45];
-    __shared__ float s_grd[kBlock * 45];
+    __shared__ __align__(16) float s_par[kBlock * 45 + 4];
+    __shared__ __align__(16) float s_grd[ACCUM ? kBlock * 45 + 4 : 4];
     const Off off(N);
     const int64_t g0 = int64_t(blockIdx.x) * kBlock;
     const int64_t g = g0 + threadIdx.x;
-    const int deg = cfg.sh_degree;
-    const int nb = (deg + 1) * (deg + 1);
-    const int nrest = 3 * (nb - 1);
-    const int64_t rows = tmin<int64_t>(kBlock, N - g0);
+    constexpr int deg = DEG;
+    constexpr int nb = (deg + 1) * (deg + 1);
+    constexpr int nrest = 3 * (nb - 1);
+    const int rows = int(tmin<int64_t>(kBlock, N - g0));
     const bool active = g < N && tcount[g] != 0;
     // does any Gaussian of this block need work?
     const int any = __syncthreads_or(active);
     if (!any) return;
-    if (nrest > 0) {
-        const float* sp = P + off.rest + g0 * 45;
-        const float* sg = G + off.rest + g0 * 45;
-        for (int i = threadIdx.x; i < rows * nrest; i += kBlock) {
-            const int r = i / nrest, cc = i - r * nrest;
-            s_par[r * 45 + cc] = __ldg(sp + int64_t(r) * 45 + cc);
-            s_grd[r * 45 + cc] = sg[int64_t(r) * 45 + cc];
-        }
+    int sp = 0, sg = 0;
+    if constexpr (nrest > 0) {
+        sp = stage_span<kBlock>(s_par, P + off.rest + g0 * 45, rows * 45);
+        if constexpr (ACCUM) sg = stage_span<kBlock>(s_grd, G + off.rest + g0 * 45, rows * 45);
     }
     __syncthreads();
+#define GW(idx, val)                          \
+    do {                                      \
+        if constexpr (ACCUM) G[idx] += (val); \
+        else G[idx] = (val);                  \
+    } while (0)
     if (active) {
         const float* W = cam.W;
         const float4 ga = g2d[3 * g], gb = g2d[3 * g + 1], gc = g2d[3 * g + 2];
@@ -112,8 +115,8 @@ __global__ void __launch_bounds__(kBlock) project_bwd_kernel(const float* __rest
         const float dl = sqrtf(e0 * e0 + e1 * e1 + e2 * e2);
         const float idl = 1.f / dl;
         const float d0 = e0 * idl, d1 = e1 * idl, d2 = e2 * idl;
-        const float* rs = s_par + threadIdx.x * 45;
-        float* rg = s_grd + threadIdx.x * 45;
+        float* rs = s_par + sp + threadIdx.x * 45;
+        float* rg = ACCUM ? s_grd + sg + threadIdx.x * 45 : rs;  // overwrite mode reuses the param row
         float Y[16];
         float dY[16][3];
         Y[0] = TS_SH_C0;
@@ -176,14 +179,15 @@ __global__ void __launch_bounds__(kBlock) project_bwd_kernel(const float* __rest
         float ddir0 = 0.f, ddir1 = 0.f, ddir2 = 0.f;
         for (int ch = 0; ch < 3; ++ch) {
             float raw = Y[0] * P[off.dc + 3 * g + ch];
-            for (int k = 1; k < nb; ++k) raw += Y[k] * rs[3 * (k - 1) + ch];
+            _Pragma("unroll") for (int k = 1; k < nb; ++k) raw += Y[k] * rs[3 * (k - 1) + ch];
             raw += 0.5f;
             if (raw < 0.f) drc[ch] = 0.f;
             const float d = drc[ch];
-            G[off.dc + 3 * g + ch] += Y[0] * d;
-            for (int k = 1; k < nb; ++k) {
-                rg[3 * (k - 1) + ch] += Y[k] * d;
+            GW(off.dc + 3 * g + ch, Y[0] * d);
+            _Pragma("unroll") for (int k = 1; k < nb; ++k) {
                 const float cf = rs[3 * (k - 1) + ch] * d;
+                if constexpr (ACCUM) rg[3 * (k - 1) + ch] += Y[k] * d;
+                else rg[3 * (k - 1) + ch] = Y[k] * d;
                 ddir0 += dY[k][0] * cf;
                 ddir1 += dY[k][1] * cf;
                 ddir2 += dY[k][2] * cf;
@@ -192,7 +196,7 @@ __global__ void __launch_bounds__(kBlock) project_bwd_kernel(const float* __rest
         const float nd = d0 * ddir0 + d1 * ddir1 + d2 * ddir2;
         float dmean0 = (ddir0 - d0 * nd) * idl, dmean1 = (ddir1 - d1 * nd) * idl, dmean2 = (ddir2 - d2 * nd) * idl;
         // ---- opacity ----
-        G[off.op + g] += dop * o * (1.f - o);
+        GW(off.op + g, dop * o * (1.f - o));
         // ---- conic -> dilated cov2d ----
         const float hb = 0.5f * dB;
         const float K00 = A * dA + B * hb, K01 = A * hb + B * dC;
@@ -233,9 +237,9 @@ __global__ void __launch_bounds__(kBlock) project_bwd_kernel(const float* __rest
         dmean0 += W[0] * dtx + W[4] * dty + W[8] * dtz;
         dmean1 += W[1] * dtx + W[5] * dty + W[9] * dtz;
         dmean2 += W[2] * dtx + W[6] * dty + W[10] * dtz;
-        G[off.means + 3 * g] += dmean0;
-        G[off.means + 3 * g + 1] += dmean1;
-        G[off.means + 3 * g + 2] += dmean2;
+        GW(off.means + 3 * g, dmean0);
+        GW(off.means + 3 * g + 1, dmean1);
+        GW(off.means + 3 * g + 2, dmean2);
         // ---- Sigma = M M^T, M = R diag(s) ----
         float dM[9];
         for (int i = 0; i < 3; ++i)
@@ -245,7 +249,7 @@ __global__ void __launch_bounds__(kBlock) project_bwd_kernel(const float* __rest
         for (int k = 0; k < 3; ++k) {
             const float ds = R[k] * dM[k] + R[3 + k] * dM[3 + k] + R[6 + k] * dM[6 + k];
             for (int i = 0; i < 3; ++i) dR[3 * i + k] = dM[3 * i + k] * s[k];
-            G[off.ls + 3 * g + k] += ds * s[k];
+            GW(off.ls + 3 * g + k, ds * s[k]);
         }
         const float dqw = 2.f * (-z * dR[1] + y * dR[2] + z * dR[3] - x * dR[5] - y * dR[6] + x * dR[7]);
         const float dqx = 2.f * (y * dR[1] + z * dR[2] + y * dR[3] - 2.f * x * dR[4] - w * dR[5] + z * dR[6] +
@@ -255,34 +259,52 @@ __global__ void __launch_bounds__(kBlock) project_bwd_kernel(const float* __rest
         const float dqz = 2.f * (-2.f * z * dR[0] - w * dR[1] + x * dR[2] + w * dR[3] - 2.f * z * dR[4] +
                                  y * dR[5] + x * dR[6] + y * dR[7]);
         const float dot = w * dqw + x * dqx + y * dqy + z * dqz;
-        G[off.q + 4 * g] += (dqw - w * dot) * iqn;
-        G[off.q + 4 * g + 1] += (dqx - x * dot) * iqn;
-        G[off.q + 4 * g + 2] += (dqy - y * dot) * iqn;
-        G[off.q + 4 * g + 3] += (dqz - z * dot) * iqn;
+        GW(off.q + 4 * g, (dqw - w * dot) * iqn);
+        GW(off.q + 4 * g + 1, (dqx - x * dot) * iqn);
+        GW(off.q + 4 * g + 2, (dqy - y * dot) * iqn);
+        GW(off.q + 4 * g + 3, (dqz - z * dot) * iqn);
         // ---- densification statistics ----
         accum[g] += sqrtf(dmx * dmx + dmy * dmy);
         vcount[g] += 1.f;
         vis[g] = 1;
     }
-    __syncthreads();
-    if (nrest > 0) {
-        float* dg = G + off.rest + g0 * 45;
-        for (int i = threadIdx.x; i < rows * nrest; i += kBlock) {
-            const int r = i / nrest, cc = i - r * nrest;
-            dg[int64_t(r) * 45 + cc] = s_grd[r * 45 + cc];
+#undef GW
+    if constexpr (!ACCUM && nrest > 0) {
+        // overwrite mode: rows of inactive Gaussians and inactive SH degrees carry zeros
+        if (int(threadIdx.x) < rows) {
+            float* row = s_par + sp + threadIdx.x * 45;
+            if (!active) {
+                for (int k = 0; k < 45; ++k) row[k] = 0.f;
+            } else {
+                for (int k = nrest; k < 45; ++k) row[k] = 0.f;
+            }
         }
+    }
+    __syncthreads();
+    if constexpr (nrest > 0) {
+        store_span<kBlock>(G + off.rest + g0 * 45, (ACCUM ? s_grd + sg : s_par + sp), rows * 45);
     }
 }
 
 }  // namespace
 
-void launch_project_bwd(Context& c, const DevCam& cam, const ts_render_config& cfg) {
+void launch_project_bwd(Context& c, const DevCam& cam, const ts_render_config& cfg, bool accumulate) {
     if (c.N == 0) return;
     const int64_t blocks = (c.N + kBlock - 1) / kBlock;
-    project_bwd_kernel<<<unsigned(blocks), kBlock, 0, c.stream>>>(c.params.p, c.grads.p, c.g2d.p, c.tcount.p,
-                                                                   c.accum.p, c.vcount.p,
-                                                                   c.vis.p, c.N, cam,
-                                                                   cfg);
+#define TS_PB(D)                                                                                       \
+    if (accumulate)                                                                                    \
+        project_bwd_kernel<D, true><<<unsigned(blocks), kBlock, 0, c.stream>>>(                        \
+            c.params.p, c.grads.p, c.g2d.p, c.tcount.p, c.accum.p, c.vcount.p, c.vis.p, c.N, cam, cfg); \
+    else                                                                                               \
+        project_bwd_kernel<D, false><<<unsigned(blocks), kBlock, 0, c.stream>>>(                       \
+            c.params.p, c.grads.p, c.g2d.p, c.tcount.p, c.accum.p, c.vcount.p, c.vis.p, c.N, cam, cfg)
+    switch (cfg.sh_degree) {
+        case 0: TS_PB(0); break;
+        case 1: TS_PB(1); break;
+        case 2: TS_PB(2); break;
+        default: TS_PB(3); break;
+    }
+#undef TS_PB
     TS_LAUNCHED(c);
 }
 

@@ -145,8 +145,9 @@ DevCam make_devcam(const ts_camera& cam) {
 
 ts_status ensure_gaussian_buffers(Context& c, int64_t n) {
     const size_t N = size_t(std::max<int64_t>(n, 1));
-    bool ok = ensure(c, c.params, 59 * N) && ensure(c, c.grads, 59 * N) && ensure(c, c.m, 59 * N) &&
-              ensure(c, c.v, 59 * N) && ensure(c, c.accum, N) && ensure(c, c.vcount, N) &&
+    const size_t L = (59 * N + 7) & ~size_t(3);  // float4 sweeps read whole quads
+    bool ok = ensure(c, c.params, L) && ensure(c, c.grads, L) && ensure(c, c.m, L) &&
+              ensure(c, c.v, L) && ensure(c, c.accum, N) && ensure(c, c.vcount, N) &&
               ensure(c, c.splat, 3 * N) && ensure(c, c.rect, N) && ensure(c, c.tcount, N) &&
               ensure(c, c.dkey[0], N) && ensure(c, c.dkey[1], N) && ensure(c, c.dperm[0], N) &&
               ensure(c, c.dperm[1], N) && ensure(c, c.offsets, N + 1) && ensure(c, c.g2d, 3 * N) &&
@@ -157,9 +158,9 @@ ts_status ensure_gaussian_buffers(Context& c, int64_t n) {
 ts_status zero_state(Context& c) {
     const size_t N = size_t(c.N);
     if (N == 0) return TS_OK;
-    CK(cudaMemsetAsync(c.grads.p, 0, 59 * N * 4, c.stream));
-    CK(cudaMemsetAsync(c.m.p, 0, 59 * N * 4, c.stream));
-    CK(cudaMemsetAsync(c.v.p, 0, 59 * N * 4, c.stream));
+    CK(cudaMemsetAsync(c.grads.p, 0, c.grads.cap * 4, c.stream));
+    CK(cudaMemsetAsync(c.m.p, 0, c.m.cap * 4, c.stream));
+    CK(cudaMemsetAsync(c.v.p, 0, c.v.cap * 4, c.stream));
     CK(cudaMemsetAsync(c.accum.p, 0, N * 4, c.stream));
     CK(cudaMemsetAsync(c.vcount.p, 0, N * 4, c.stream));
     CK(cudaMemsetAsync(c.g2d.p, 0, 3 * N * 16, c.stream));
@@ -277,7 +278,8 @@ ts_status run_backward(Context& c, const float* dLdC_hwc) {
     launch_blend_bwd(c, dc, c.cfg);
     stage_end(c, 8);
     stage_begin(c, 9);
-    launch_project_bwd(c, dc, c.cfg);
+    launch_project_bwd(c, dc, c.cfg, !c.grads_zero);
+    c.grads_zero = false;
     stage_end(c, 9);
     return last_launch(c, "backward");
 }
@@ -289,6 +291,7 @@ ts_status run_adam(Context& c, const ts_adam_config& a, int64_t begin, int64_t e
     launch_adam(c, a, begin, end);
     stage_end(c, 10);
     CK(cudaMemsetAsync(c.vis.p, 0, size_t(std::max<int64_t>(c.N, 1)), c.stream));
+    if (a.zero_grads && begin == 0 && end == 59 * c.N) c.grads_zero = true;
     c.view_valid = false;
     c.loss_valid = false;
     return last_launch(c, "adam");
@@ -388,6 +391,7 @@ ts_status ts_set_params_flat(ts_ctx* x, int64_t n, const float* flat) {
     c.N = n;
     if (n) CK(cudaMemcpyAsync(c.params.p, flat, size_t(59) * n * 4, cudaMemcpyHostToDevice, c.stream));
     if (ts_status s = zero_state(c); s != TS_OK) return s;
+    c.grads_zero = true;
     c.view_valid = c.loss_valid = false;
     CK(cudaStreamSynchronize(c.stream));
     return TS_OK;
@@ -487,6 +491,7 @@ ts_status ts_zero_grads(ts_ctx* x) {
     Context& c = x->c;
     CK(cudaSetDevice(c.device));
     if (c.N) CK(cudaMemsetAsync(c.grads.p, 0, size_t(59) * c.N * 4, c.stream));
+    c.grads_zero = true;
     return TS_OK;
 }
 
@@ -588,6 +593,7 @@ ts_status ts_densify(ts_ctx* x, float grad_thresh, float extent, uint64_t seed, 
     const int64_t na = launch_densify(c, grad_thresh, log_small, log_big, logit_min, seed, iter, st);
     if (na < 0) return c.err.empty() ? TS_ERR_CUDA : TS_ERR_OOM;
     if (n_after) *n_after = na;
+    c.grads_zero = true;
     if (stats) std::memcpy(stats, st, sizeof(st));
     c.view_valid = c.loss_valid = false;
     return last_launch(c, "densify");
@@ -599,7 +605,10 @@ ts_status ts_set_state(ts_ctx* x, const float* grads, const float* m, const floa
     Context& c = x->c;
     CK(cudaSetDevice(c.device));
     const size_t L = size_t(59) * c.N, N = size_t(c.N);
-    if (grads) CK(cudaMemcpyAsync(c.grads.p, grads, L * 4, cudaMemcpyHostToDevice, c.stream));
+    if (grads) {
+        CK(cudaMemcpyAsync(c.grads.p, grads, L * 4, cudaMemcpyHostToDevice, c.stream));
+        c.grads_zero = false;
+    }
     if (m) CK(cudaMemcpyAsync(c.m.p, m, L * 4, cudaMemcpyHostToDevice, c.stream));
     if (v) CK(cudaMemcpyAsync(c.v.p, v, L * 4, cudaMemcpyHostToDevice, c.stream));
     if (accum) CK(cudaMemcpyAsync(c.accum.p, accum, N * 4, cudaMemcpyHostToDevice, c.stream));

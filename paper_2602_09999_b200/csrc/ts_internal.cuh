@@ -48,6 +48,7 @@ struct Context {
     int64_t N = 0;
     DevBuf<float> params, grads, m, v, accum, vcount;
     int64_t step = 0;
+    bool grads_zero = true;  // gradient buffer known to be all zero (backward may overwrite)
 
     // per-view (sized by N)
     DevBuf<float4> splat;        // 3 float4 per Gaussian: (mx,my,k2,o) (A,B,C,depth) (r,g,b,det)
@@ -104,7 +105,7 @@ void launch_ranges(Context& c, int n_tiles);
 void launch_blend_fwd(Context& c, const DevCam& cam, const ts_render_config& cfg);
 void launch_loss(Context& c, const float* target_chw);
 void launch_blend_bwd(Context& c, const DevCam& cam, const ts_render_config& cfg);
-void launch_project_bwd(Context& c, const DevCam& cam, const ts_render_config& cfg);
+void launch_project_bwd(Context& c, const DevCam& cam, const ts_render_config& cfg, bool accumulate);
 void launch_adam(Context& c, const ts_adam_config& a, int64_t begin, int64_t end);
 void launch_hwc_to_chw(Context& c, const float* hwc, float* chw, int P);
 void launch_chw_to_hwc(Context& c, const float* chw, float* hwc, int P);

@@ -252,3 +252,28 @@ def test_train_steps_reduce_loss(engine):
     losses = [engine.train_step(cam, cfg, T.AdamConfig.make(step=i + 1)) for i in range(30)]
     assert losses[-1] < 0.7 * losses[0]
     assert engine.launch_count() > 0
+
+
+def test_multi_view_gradients_accumulate(engine):
+    """Batch gradient = sum of per-view gradients; exercises the
+    accumulate path of the project backward."""
+    n = 20_000
+    p = scene.random_params(n, 0.02, 0.0, 21)
+    cams = scene.fibonacci_cameras(2, 200, 150)
+    cfg = T.RenderConfig.make(sh_degree=3)
+    rng = np.random.default_rng(22)
+    dls = [rng.normal(0, 1e-3, (150, 200, 3)).astype(np.float32) for _ in cams]
+    engine.set_params(p, n)
+    for cam, dl in zip(cams, dls):
+        engine.render(cam, cfg, outputs=False)
+        engine.backward(dl)
+    G, _, _, acc, vc = engine.get_state()
+    oG = np.zeros_like(G)
+    ovc = np.zeros_like(vc)
+    for cam, dl in zip(cams, dls):
+        g_, _, _, c_ = O.backward(p, n, cam, cfg, dl)
+        oG += g_
+        ovc += c_
+    for (a, b), nm in zip(T.group_slices(n), T.GROUPS):
+        _grad_check(G[a:b], oG[a:b], nm)
+    assert np.array_equal(vc, ovc)

@@ -1098,6 +1098,7 @@ inline int group_of(int64_t idx, int64_t N, int64_t* gi) {
     return 5;
 }
 
+// adam_step_reference: the literal formula
 template <class T>
 inline void adam_elem(T& th, T g, T& m, T& v, T lr, T b1, T b2, T omb1, T omb2, T eps, T bc1, T bc2) {
     m = b1 * m + omb1 * g;
@@ -1106,6 +1107,17 @@ inline void adam_elem(T& th, T g, T& m, T& v, T lr, T b1, T b2, T omb1, T omb2, 
     T vh = v / bc2;
     T den = std::sqrt(vh) + eps;
     th = th - (lr * mh) / den;
+}
+
+// adam_step_fused: same contract, bias corrections folded
+// into per-step constants lr_eff = lr / bc1 and rsb2 = 1 / sqrt(bc2) computed in
+// double on the host -> one sqrt and one division per element.
+inline void adam_elem_fused(float& th, float g, float& m, float& v, float lr_eff, float b1, float b2, float omb1,
+                            float omb2, float eps, float rsb2) {
+    m = b1 * m + omb1 * g;
+    v = b2 * v + omb2 * g * g;
+    float den = std::sqrt(v) * rsb2 + eps;
+    th = th - (lr_eff * m) / den;
 }
 
 }  // namespace
@@ -1314,12 +1326,18 @@ void tso_adam_step(int64_t n, float* th, const float* g, float* m, float* v, con
                    float eps, float bc1, float bc2, int32_t mode, const uint8_t* visible) {
     int64_t L = 59 * n;
     float omb1 = 1.0f - b1, omb2 = 1.0f - b2;
+    float lr_eff[6];
+    for (int k = 0; k < 6; ++k) lr_eff[k] = float(double(lr[k]) / double(bc1));
+    const float rsb2 = float(1.0 / std::sqrt(double(bc2)));
     pfor(L, [&](int64_t b, int64_t e) {
         for (int64_t i = b; i < e; ++i) {
             int64_t gi;
             int grp = group_of(i, n, &gi);
             if (mode == 2 && visible && !visible[gi]) continue;
-            adam_elem<float>(th[i], g[i], m[i], v[i], lr[grp], b1, b2, omb1, omb2, eps, bc1, bc2);
+            if (mode == 0)
+                adam_elem<float>(th[i], g[i], m[i], v[i], lr[grp], b1, b2, omb1, omb2, eps, bc1, bc2);
+            else
+                adam_elem_fused(th[i], g[i], m[i], v[i], lr_eff[grp], b1, b2, omb1, omb2, eps, rsb2);
         }
     });
 }

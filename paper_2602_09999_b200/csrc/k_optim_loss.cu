@@ -1,14 +1,17 @@
 // K10 fused Adam, K7 training loss and
 // layout helpers.
 //
-// Adam: one linear float4 sweep over the flat 59*N buffer; per element the
-// SPEC's literal formula with explicit round-to-nearest ops in a fixed order,
-// so it is bitwise equal to the oracle's adam_step given the same gradient.
+// Adam: one linear float4 sweep over the flat 59*N buffer; per element a fixed
+// sequence of explicit round-to-nearest ops (reference = SPEC literal formula,
+// fused = bias corrections folded into host constants: one IEEE sqrt and one
+// IEEE division per element), bitwise equal to the oracle's restatement.
 // Reads theta, g, m, v and writes theta, m, v (28 B/element, HBM-bound); with
 // zero_grads the gradient is cleared in the same pass (+4 B).
 //
 // Loss: 0.8 L1 + 0.2 (1 - SSIM), 11x11 Gaussian window (sigma 1.5), reflect
 // padding; analytic dL/dC via the transposed (fold) separable filter.
+#include <cmath>
+
 #include "ts_internal.cuh"
 #include "ts_math.cuh"
 
@@ -16,19 +19,30 @@ namespace ts {
 namespace {
 
 struct AdamArgs {
-    float lr[6];
+    float lr[6];      // reference: lr ; fused: lr / (1 - b1^t) (host double -> float)
     float b1, b2, omb1, omb2, eps, bc1, bc2;
+    float rsb2;       // fused: 1 / sqrt(1 - b2^t) (host double -> float)
     int mode, zero;
 };
 
+// reference (SPEC.md:466 literal): theta -= lr * (m / bc1) / (sqrt(v / bc2) + eps)
+// fused:         theta -= (lr/bc1) * m / (sqrt(v) * (1/sqrt(bc2)) + eps)
+// Both fixed op sequences with explicit round-to-nearest ops; the oracle
+// restates each bit for bit.
+template <bool kFused>
 __device__ __forceinline__ void adam_one(float& th, float& g, float& m, float& v, float lr, const AdamArgs& a) {
     using namespace tsx;
     m = add(mul(a.b1, m), mul(a.omb1, g));
     v = add(mul(a.b2, v), mul(mul(a.omb2, g), g));
-    const float mh = div(m, a.bc1);
-    const float vh = div(v, a.bc2);
-    const float den = add(sqrt_(vh), a.eps);
-    th = sub(th, div(mul(lr, mh), den));
+    if (kFused) {
+        const float den = add(mul(sqrt_(v), a.rsb2), a.eps);
+        th = sub(th, div(mul(lr, m), den));
+    } else {
+        const float mh = div(m, a.bc1);
+        const float vh = div(v, a.bc2);
+        const float den = add(sqrt_(vh), a.eps);
+        th = sub(th, div(mul(lr, mh), den));
+    }
 }
 
 // flat-buffer group boundaries (elements): means | scales | quats | opacity | sh_dc | sh_rest
@@ -73,7 +87,7 @@ __global__ void __launch_bounds__(256) adam_kernel(float4* __restrict__ th, floa
                          : i < bd.b4 ? a.lr[3]
                          : i < bd.b5 ? a.lr[4]
                                      : a.lr[5];
-        if (visible_of<MODE>(i, bd, vis)) adam_one(tp[k], gp[k], mp[k], vp[k], lr, a);
+        if (visible_of<MODE>(i, bd, vis)) adam_one<MODE != 0>(tp[k], gp[k], mp[k], vp[k], lr, a);
         if (ZERO) gp[k] = 0.f;
     }
     th[q] = t4;
@@ -250,7 +264,8 @@ __global__ void loss_vt_kernel(const float* __restrict__ X, const float* __restr
 void launch_adam(Context& c, const ts_adam_config& a, int64_t begin, int64_t end) {
     if (end <= begin) return;
     AdamArgs x;
-    for (int k = 0; k < 6; ++k) x.lr[k] = a.lr[k];
+    const bool fused = a.mode != 0;
+    for (int k = 0; k < 6; ++k) x.lr[k] = fused ? float(double(a.lr[k]) / double(a.bc1)) : a.lr[k];
     x.b1 = a.beta1;
     x.b2 = a.beta2;
     x.omb1 = 1.0f - a.beta1;
@@ -258,6 +273,7 @@ void launch_adam(Context& c, const ts_adam_config& a, int64_t begin, int64_t end
     x.eps = a.eps;
     x.bc1 = a.bc1;
     x.bc2 = a.bc2;
+    x.rsb2 = float(1.0 / std::sqrt(double(a.bc2)));
     x.mode = a.mode;
     x.zero = a.zero_grads;
     const uint32_t N = uint32_t(c.N);
@@ -269,17 +285,18 @@ void launch_adam(Context& c, const ts_adam_config& a, int64_t begin, int64_t end
     auto* m = reinterpret_cast<float4*>(c.m.p);
     auto* v = reinterpret_cast<float4*>(c.v.p);
     const uint32_t b = uint32_t(begin), e = uint32_t(end);
+#define TS_ADAM(MODE, Z) adam_kernel<MODE, Z><<<blocks, 256, 0, c.stream>>>(th, g, m, v, q0, q1, b, e, bd, x, c.vis.p)
     if (a.mode == 2) {
-        if (a.zero_grads)
-            adam_kernel<2, true><<<blocks, 256, 0, c.stream>>>(th, g, m, v, q0, q1, b, e, bd, x, c.vis.p);
-        else
-            adam_kernel<2, false><<<blocks, 256, 0, c.stream>>>(th, g, m, v, q0, q1, b, e, bd, x, c.vis.p);
+        if (a.zero_grads) TS_ADAM(2, true);
+        else TS_ADAM(2, false);
+    } else if (a.mode == 1) {
+        if (a.zero_grads) TS_ADAM(1, true);
+        else TS_ADAM(1, false);
     } else {
-        if (a.zero_grads)
-            adam_kernel<1, true><<<blocks, 256, 0, c.stream>>>(th, g, m, v, q0, q1, b, e, bd, x, c.vis.p);
-        else
-            adam_kernel<1, false><<<blocks, 256, 0, c.stream>>>(th, g, m, v, q0, q1, b, e, bd, x, c.vis.p);
+        if (a.zero_grads) TS_ADAM(0, true);
+        else TS_ADAM(0, false);
     }
+#undef TS_ADAM
     TS_LAUNCHED(c);
 }
 

@@ -19,21 +19,37 @@ __global__ void __launch_bounds__(kBlock) preprocess_kernel(
     uint2* __restrict__ rect, uint32_t* __restrict__ tcount, uint32_t* __restrict__ dkey,
     uint32_t* __restrict__ dperm, uint32_t* __restrict__ vis_counter) {
     using namespace tsx;
-    __shared__ __align__(16) float sh_rest[kBlock * 45 + 4];
-    const Off off(N);
-    const int64_t g0 = int64_t(blockIdx.x) * kBlock;
-    const int64_t g = g0 + threadIdx.x;
+    // staged inputs of the CTA's 128 Gaussians (one pass of independent 16-byte loads)
+    constexpr int kMu = 0, kLs = kMu + 3 * kBlock + 4, kQ = kLs + 3 * kBlock + 4, kOp = kQ + 4 * kBlock + 4,
+                  kDc = kOp + kBlock + 4, kRest = kDc + 3 * kBlock + 4;
     constexpr int deg = DEG;
     constexpr int nb = (deg + 1) * (deg + 1);
     constexpr int nrest = 3 * (nb - 1);
-    int sshift = 0;
-    if constexpr (nrest > 0) {
-        const int rows = int(tmin<int64_t>(kBlock, N - g0));
-        sshift = stage_span<kBlock>(sh_rest, P + off.rest + g0 * 45, rows * 45);
+    __shared__ __align__(16) float sm[kRest + (nrest > 0 ? 45 * kBlock + 4 : 0)];
+    const Off off(N);
+    const int64_t g0 = int64_t(blockIdx.x) * kBlock;
+    const int64_t g = g0 + threadIdx.x;
+    const int rows = int(tmin<int64_t>(kBlock, N - g0));
+    int sh[6] = {0, 0, 0, 0, 0, 0};
+    {
+        const Span base[5] = {{sm + kMu, P + off.means + 3 * g0, 3 * rows},
+                              {sm + kLs, P + off.ls + 3 * g0, 3 * rows},
+                              {sm + kQ, P + off.q + 4 * g0, 4 * rows},
+                              {sm + kOp, P + off.op + g0, rows},
+                              {sm + kDc, P + off.dc + 3 * g0, 3 * rows}};
+        if constexpr (nrest > 0) {
+            const Span sp[6] = {base[0], base[1], base[2], base[3], base[4],
+                                {sm + kRest, P + off.rest + g0 * 45, 45 * rows}};
+            stage_spans<kBlock>(sp, sh);
+        } else {
+            int s5[5];
+            stage_spans<kBlock>(base, s5);
+            for (int k = 0; k < 5; ++k) sh[k] = s5[k];
+        }
     }
     __syncthreads();
     if (g >= N) return;
-
+    const int tid = threadIdx.x;
     float4 s0 = make_float4(0.f, 0.f, 0.f, 0.f), s1 = s0, s2 = s0;
     uint32_t cnt = 0;
     uint2 rc = make_uint2(1u, 1u);  // empty: tx0=1 > tx1=0
@@ -41,13 +57,15 @@ __global__ void __launch_bounds__(kBlock) preprocess_kernel(
     float zh = 0.f;
     do {
         const float* W = cam.W;
-        const float m0 = P[off.means + 3 * g], m1 = P[off.means + 3 * g + 1], m2 = P[off.means + 3 * g + 2];
+        const float* mus = sm + kMu + sh[0] + 3 * tid;
+        const float m0 = mus[0], m1 = mus[1], m2 = mus[2];
         // project_mean, fixed order (depth feeds the sort key)
         const float xh = add(add(add(mul(W[0], m0), mul(W[1], m1)), mul(W[2], m2)), W[3]);
         const float yh = add(add(add(mul(W[4], m0), mul(W[5], m1)), mul(W[6], m2)), W[7]);
         zh = add(add(add(mul(W[8], m0), mul(W[9], m1)), mul(W[10], m2)), W[11]);
         if (!(zh > cam.nearp)) break;
-        const float4 qv = make_float4(P[off.q + 4 * g], P[off.q + 4 * g + 1], P[off.q + 4 * g + 2], P[off.q + 4 * g + 3]);
+        const float* qs = sm + kQ + sh[2] + 4 * tid;
+        const float4 qv = make_float4(qs[0], qs[1], qs[2], qs[3]);
         const float qq = add(add(add(mul(qv.x, qv.x), mul(qv.y, qv.y)), mul(qv.z, qv.z)), mul(qv.w, qv.w));
         const float qn = sqrt_(qq);
         if (!(qn >= 1e-4f)) break;
@@ -67,9 +85,10 @@ __global__ void __launch_bounds__(kBlock) preprocess_kernel(
             R[8] = sub(1.f, mul(2.f, add(xx, yy)));
         }
         float sc[3];
-        sc[0] = expf_det(P[off.ls + 3 * g]);
-        sc[1] = expf_det(P[off.ls + 3 * g + 1]);
-        sc[2] = expf_det(P[off.ls + 3 * g + 2]);
+        const float* lss = sm + kLs + sh[1] + 3 * tid;
+        sc[0] = expf_det(lss[0]);
+        sc[1] = expf_det(lss[1]);
+        sc[2] = expf_det(lss[2]);
         float Mm[9];
 #pragma unroll
         for (int i = 0; i < 3; ++i)
@@ -116,7 +135,7 @@ __global__ void __launch_bounds__(kBlock) preprocess_kernel(
         const float A = div(c, det), B = div(-b, det), C = div(a, det);
         const float mx = add(mul(cam.fx, txz), cam.cx), my = add(mul(cam.fy, tyz), cam.cy);
         // activate_opacity; alpha level set Q <= k2  <=>  o exp(-Q/2) >= tau
-        const float logit = P[off.op + g];
+        const float logit = sm[kOp + sh[3] + tid];
         const float o = div(1.f, add(1.f, expf_det(-logit)));
         const float tau = cfg.tau_alpha;
         const bool has_bound = o > tau;
@@ -157,10 +176,10 @@ __global__ void __launch_bounds__(kBlock) preprocess_kernel(
             }
         }
         float rgb[3];
-        const float* rs = sh_rest + sshift + threadIdx.x * 45;
+        const float* rs = sm + kRest + sh[5] + tid * 45;
 #pragma unroll
         for (int ch = 0; ch < 3; ++ch) {
-            float acc = Y[0] * P[off.dc + 3 * g + ch];
+            float acc = Y[0] * sm[kDc + sh[4] + 3 * tid + ch];
             _Pragma("unroll") for (int k = 1; k < nb; ++k) acc += Y[k] * rs[3 * (k - 1) + ch];
             acc += 0.5f;
             rgb[ch] = acc < 0.f ? 0.f : acc;

@@ -4,8 +4,10 @@
 // accumulate_densify_stats: accum += |dL/dmean2d|, count += 1.
 // Gradients are ACCUMULATED into the flat 59*N buffer (multi-view batches sum,
 // SPEC.md:735); the per-Gaussian 2D accumulator is consumed and zeroed here.
-// HBM-bound: SH parameter rows and SH gradient rows are staged through shared
-// memory so every global access is coalesced.
+// HBM-bound: a CTA stages all inputs of its 128 Gaussians (6 attribute blocks,
+// SH rows, 2D gradients, statistics) with one pass of independent 16-byte
+// loads (stage_spans), computes from shared memory, and writes SH gradient
+// rows back through shared memory so every global access is coalesced.
 #include "ts_internal.cuh"
 #include "ts_math.cuh"
 #include "ts_stage.cuh"
@@ -15,6 +17,22 @@ namespace {
 
 constexpr int kBlock = 128;
 
+// shared-memory layout of one CTA (floats; every segment a multiple of 4)
+template <int DEG, bool ACCUM>
+struct PbLayout {
+    static constexpr int kMu = 0;
+    static constexpr int kLs = kMu + 3 * kBlock + 4;
+    static constexpr int kQ = kLs + 3 * kBlock + 4;
+    static constexpr int kOp = kQ + 4 * kBlock + 4;
+    static constexpr int kDc = kOp + kBlock + 4;
+    static constexpr int kG2 = kDc + 3 * kBlock + 4;
+    static constexpr int kAc = kG2 + 12 * kBlock + 4;
+    static constexpr int kVc = kAc + kBlock + 4;
+    static constexpr int kRest = kVc + kBlock + 4;
+    static constexpr int kGRest = kRest + (DEG > 0 ? 45 * kBlock + 4 : 0);
+    static constexpr int kTotal = kGRest + (DEG > 0 && ACCUM ? 45 * kBlock + 4 : 0);
+};
+
 template <int DEG, bool ACCUM>
 __global__ void __launch_bounds__(kBlock) project_bwd_kernel(const float* __restrict__ P, float* __restrict__ G,
                                                              float4* __restrict__ g2d,
@@ -22,8 +40,8 @@ __global__ void __launch_bounds__(kBlock) project_bwd_kernel(const float* __rest
                                                              float* __restrict__ accum, float* __restrict__ vcount,
                                                              uint8_t* __restrict__ vis, int64_t N, DevCam cam,
                                                              ts_render_config cfg) {
-    __shared__ __align__(16) float s_par[kBlock * 45 + 4];
-    __shared__ __align__(16) float s_grd[ACCUM ? kBlock * 45 + 4 : 4];
+    extern __shared__ __align__(16) float smem[];
+    using L = PbLayout<DEG, ACCUM>;
     const Off off(N);
     const int64_t g0 = int64_t(blockIdx.x) * kBlock;
     const int64_t g = g0 + threadIdx.x;
@@ -33,12 +51,34 @@ __global__ void __launch_bounds__(kBlock) project_bwd_kernel(const float* __rest
     const int rows = int(tmin<int64_t>(kBlock, N - g0));
     const bool active = g < N && tcount[g] != 0;
     // does any Gaussian of this block need work?
-    const int any = __syncthreads_or(active);
-    if (!any) return;
-    int sp = 0, sg = 0;
-    if constexpr (nrest > 0) {
-        sp = stage_span<kBlock>(s_par, P + off.rest + g0 * 45, rows * 45);
-        if constexpr (ACCUM) sg = stage_span<kBlock>(s_grd, G + off.rest + g0 * 45, rows * 45);
+    if (!__syncthreads_or(active)) return;
+    // ---- stage every per-Gaussian input of the CTA in one pass (max MLP) ----
+    int sh[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+    {
+        const Span base[8] = {{smem + L::kMu, P + off.means + 3 * g0, 3 * rows},
+                              {smem + L::kLs, P + off.ls + 3 * g0, 3 * rows},
+                              {smem + L::kQ, P + off.q + 4 * g0, 4 * rows},
+                              {smem + L::kOp, P + off.op + g0, rows},
+                              {smem + L::kDc, P + off.dc + 3 * g0, 3 * rows},
+                              {smem + L::kG2, reinterpret_cast<const float*>(g2d + 3 * g0), 12 * rows},
+                              {smem + L::kAc, accum + g0, rows},
+                              {smem + L::kVc, vcount + g0, rows}};
+        if constexpr (DEG == 0) {
+            int s8[8];
+            stage_spans<kBlock>(base, s8);
+            for (int k = 0; k < 8; ++k) sh[k] = s8[k];
+        } else if constexpr (!ACCUM) {
+            const Span sp[9] = {base[0], base[1], base[2], base[3], base[4], base[5], base[6], base[7],
+                                {smem + L::kRest, P + off.rest + g0 * 45, 45 * rows}};
+            int s9[9];
+            stage_spans<kBlock>(sp, s9);
+            for (int k = 0; k < 9; ++k) sh[k] = s9[k];
+        } else {
+            const Span sp[10] = {base[0], base[1], base[2], base[3], base[4], base[5], base[6], base[7],
+                                 {smem + L::kRest, P + off.rest + g0 * 45, 45 * rows},
+                                 {smem + L::kGRest, G + off.rest + g0 * 45, 45 * rows}};
+            stage_spans<kBlock>(sp, sh);
+        }
     }
     __syncthreads();
 #define GW(idx, val)                          \
@@ -46,21 +86,23 @@ __global__ void __launch_bounds__(kBlock) project_bwd_kernel(const float* __rest
         if constexpr (ACCUM) G[idx] += (val); \
         else G[idx] = (val);                  \
     } while (0)
+    const int tid = threadIdx.x;
     if (active) {
         const float* W = cam.W;
-        const float4 ga = g2d[3 * g], gb = g2d[3 * g + 1], gc = g2d[3 * g + 2];
-        g2d[3 * g] = make_float4(0.f, 0.f, 0.f, 0.f);
-        g2d[3 * g + 1] = make_float4(0.f, 0.f, 0.f, 0.f);
-        g2d[3 * g + 2] = make_float4(0.f, 0.f, 0.f, 0.f);
-        const float dmx = ga.x, dmy = ga.y, dA = ga.z, dB = ga.w, dC = gb.x, dop = gb.y;
-        float drc[3] = {gb.z, gb.w, gc.x};
-        // ---- recompute forward quantities ----
-        const float mu[3] = {P[off.means + 3 * g], P[off.means + 3 * g + 1], P[off.means + 3 * g + 2]};
+        const float* g2s = smem + L::kG2 + sh[5] + 12 * tid;
+        reinterpret_cast<float4*>(g2d)[3 * g] = make_float4(0.f, 0.f, 0.f, 0.f);
+        reinterpret_cast<float4*>(g2d)[3 * g + 1] = make_float4(0.f, 0.f, 0.f, 0.f);
+        reinterpret_cast<float4*>(g2d)[3 * g + 2] = make_float4(0.f, 0.f, 0.f, 0.f);
+        const float dmx = g2s[0], dmy = g2s[1], dA = g2s[2], dB = g2s[3], dC = g2s[4], dop = g2s[5];
+        float drc[3] = {g2s[6], g2s[7], g2s[8]};
+        // ---- recompute forward quantities (from the staged rows) ----
+        const float* mus = smem + L::kMu + sh[0] + 3 * tid;
+        const float mu[3] = {mus[0], mus[1], mus[2]};
         const float xh = W[0] * mu[0] + W[1] * mu[1] + W[2] * mu[2] + W[3];
         const float yh = W[4] * mu[0] + W[5] * mu[1] + W[6] * mu[2] + W[7];
         const float zh = W[8] * mu[0] + W[9] * mu[1] + W[10] * mu[2] + W[11];
-        const float q0 = P[off.q + 4 * g], q1 = P[off.q + 4 * g + 1], q2 = P[off.q + 4 * g + 2],
-                    q3 = P[off.q + 4 * g + 3];
+        const float* qs = smem + L::kQ + sh[2] + 4 * tid;
+        const float q0 = qs[0], q1 = qs[1], q2 = qs[2], q3 = qs[3];
         const float qn = sqrtf(q0 * q0 + q1 * q1 + q2 * q2 + q3 * q3);
         const float iqn = 1.f / qn;
         const float w = q0 * iqn, x = q1 * iqn, y = q2 * iqn, z = q3 * iqn;
@@ -74,8 +116,9 @@ __global__ void __launch_bounds__(kBlock) project_bwd_kernel(const float* __rest
         R[6] = 2.f * (x * z - w * y);
         R[7] = 2.f * (y * z + w * x);
         R[8] = 1.f - 2.f * (x * x + y * y);
+        const float* lss = smem + L::kLs + sh[1] + 3 * tid;
         float s[3];
-        for (int k = 0; k < 3; ++k) s[k] = __expf(P[off.ls + 3 * g + k]);
+        for (int k = 0; k < 3; ++k) s[k] = __expf(lss[k]);
         float Mm[9];
         for (int i = 0; i < 3; ++i)
             for (int k = 0; k < 3; ++k) Mm[3 * i + k] = R[3 * i + k] * s[k];
@@ -106,7 +149,8 @@ __global__ void __launch_bounds__(kBlock) project_bwd_kernel(const float* __rest
         const float c = TS[3] * Tm[3] + TS[4] * Tm[4] + TS[5] * Tm[5] + cfg.dilation;
         const float idet = 1.f / (a * c - bb * bb);
         const float A = c * idet, B = -bb * idet, C = a * idet;
-        const float o = 1.f / (1.f + __expf(-P[off.op + g]));
+        const float o = 1.f / (1.f + __expf(-smem[L::kOp + sh[3] + tid]));
+        const float* dcs = smem + L::kDc + sh[4] + 3 * tid;
         // ---- colour / SH ----
         const float cpx = -(W[0] * W[3] + W[4] * W[7] + W[8] * W[11]);
         const float cpy = -(W[1] * W[3] + W[5] * W[7] + W[9] * W[11]);
@@ -115,8 +159,8 @@ __global__ void __launch_bounds__(kBlock) project_bwd_kernel(const float* __rest
         const float dl = sqrtf(e0 * e0 + e1 * e1 + e2 * e2);
         const float idl = 1.f / dl;
         const float d0 = e0 * idl, d1 = e1 * idl, d2 = e2 * idl;
-        float* rs = s_par + sp + threadIdx.x * 45;
-        float* rg = ACCUM ? s_grd + sg + threadIdx.x * 45 : rs;  // overwrite mode reuses the param row
+        float* rs = smem + L::kRest + sh[8] + tid * 45;
+        float* rg = ACCUM ? smem + L::kGRest + sh[9] + tid * 45 : rs;  // overwrite mode reuses the param row
         float Y[16];
         float dY[16][3];
         Y[0] = TS_SH_C0;
@@ -178,7 +222,7 @@ __global__ void __launch_bounds__(kBlock) project_bwd_kernel(const float* __rest
         }
         float ddir0 = 0.f, ddir1 = 0.f, ddir2 = 0.f;
         for (int ch = 0; ch < 3; ++ch) {
-            float raw = Y[0] * P[off.dc + 3 * g + ch];
+            float raw = Y[0] * dcs[ch];
             _Pragma("unroll") for (int k = 1; k < nb; ++k) raw += Y[k] * rs[3 * (k - 1) + ch];
             raw += 0.5f;
             if (raw < 0.f) drc[ch] = 0.f;
@@ -264,15 +308,15 @@ __global__ void __launch_bounds__(kBlock) project_bwd_kernel(const float* __rest
         GW(off.q + 4 * g + 2, (dqy - y * dot) * iqn);
         GW(off.q + 4 * g + 3, (dqz - z * dot) * iqn);
         // ---- densification statistics ----
-        accum[g] += sqrtf(dmx * dmx + dmy * dmy);
-        vcount[g] += 1.f;
+        accum[g] = smem[L::kAc + sh[6] + tid] + sqrtf(dmx * dmx + dmy * dmy);
+        vcount[g] = smem[L::kVc + sh[7] + tid] + 1.f;
         vis[g] = 1;
     }
 #undef GW
     if constexpr (!ACCUM && nrest > 0) {
         // overwrite mode: rows of inactive Gaussians and inactive SH degrees carry zeros
         if (int(threadIdx.x) < rows) {
-            float* row = s_par + sp + threadIdx.x * 45;
+            float* row = smem + L::kRest + sh[8] + threadIdx.x * 45;
             if (!active) {
                 for (int k = 0; k < 45; ++k) row[k] = 0.f;
             } else {
@@ -282,7 +326,8 @@ __global__ void __launch_bounds__(kBlock) project_bwd_kernel(const float* __rest
     }
     __syncthreads();
     if constexpr (nrest > 0) {
-        store_span<kBlock>(G + off.rest + g0 * 45, (ACCUM ? s_grd + sg : s_par + sp), rows * 45);
+        store_span<kBlock>(G + off.rest + g0 * 45,
+                           (ACCUM ? smem + L::kGRest + sh[9] : smem + L::kRest + sh[8]), rows * 45);
     }
 }
 
@@ -291,13 +336,18 @@ __global__ void __launch_bounds__(kBlock) project_bwd_kernel(const float* __rest
 void launch_project_bwd(Context& c, const DevCam& cam, const ts_render_config& cfg, bool accumulate) {
     if (c.N == 0) return;
     const int64_t blocks = (c.N + kBlock - 1) / kBlock;
-#define TS_PB(D)                                                                                       \
-    if (accumulate)                                                                                    \
-        project_bwd_kernel<D, true><<<unsigned(blocks), kBlock, 0, c.stream>>>(                        \
+#define TS_PB(D)                                                                                      \
+    if (accumulate) {                                                                                 \
+        constexpr int sm = PbLayout<D, true>::kTotal * 4;                                             \
+        cudaFuncSetAttribute(project_bwd_kernel<D, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm); \
+        project_bwd_kernel<D, true><<<unsigned(blocks), kBlock, sm, c.stream>>>(                      \
             c.params.p, c.grads.p, c.g2d.p, c.tcount.p, c.accum.p, c.vcount.p, c.vis.p, c.N, cam, cfg); \
-    else                                                                                               \
-        project_bwd_kernel<D, false><<<unsigned(blocks), kBlock, 0, c.stream>>>(                       \
-            c.params.p, c.grads.p, c.g2d.p, c.tcount.p, c.accum.p, c.vcount.p, c.vis.p, c.N, cam, cfg)
+    } else {                                                                                          \
+        constexpr int sm = PbLayout<D, false>::kTotal * 4;                                            \
+        cudaFuncSetAttribute(project_bwd_kernel<D, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm); \
+        project_bwd_kernel<D, false><<<unsigned(blocks), kBlock, sm, c.stream>>>(                     \
+            c.params.p, c.grads.p, c.g2d.p, c.tcount.p, c.accum.p, c.vcount.p, c.vis.p, c.N, cam, cfg); \
+    }
     switch (cfg.sh_degree) {
         case 0: TS_PB(0); break;
         case 1: TS_PB(1); break;

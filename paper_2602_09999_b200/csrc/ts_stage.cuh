@@ -45,3 +45,61 @@ __device__ __forceinline__ void store_span(float* __restrict__ dst, const float*
 }
 
 }  // namespace ts
+
+namespace ts {
+
+// A contiguous run of 4-byte words to stage: src (global, 4-byte aligned) ->
+// dst (shared, 16-byte aligned, count + 4 words of room).
+struct Span {
+    float* dst;
+    const float* src;
+    int count;
+};
+
+// Stage NS spans with ONE barrier-free pass: every thread issues up to
+// kUnroll independent 16-byte loads across all spans before storing any of
+// them, so a CTA has its whole working set in flight at once (the per-Gaussian
+// attribute blocks of the flat 59*N layout are separate contiguous runs).
+// shift[s] locates element 0 of span s in its dst (see stage_span).
+template <int kThreads, int NS, int kUnroll = 8>
+__device__ __forceinline__ void stage_spans(const Span (&sp)[NS], int (&shift)[NS]) {
+    int start[NS + 1];
+    const float4* s4[NS];
+    start[0] = 0;
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+        const uintptr_t a = reinterpret_cast<uintptr_t>(sp[s].src);
+        shift[s] = int((a & 15u) >> 2);
+        s4[s] = reinterpret_cast<const float4*>(a - uintptr_t(shift[s]) * 4u);
+        const int n4 = sp[s].count > 0 ? (sp[s].count + shift[s] + 3) >> 2 : 0;
+        start[s + 1] = start[s] + n4;
+    }
+    const int total = start[NS];
+    for (int base = threadIdx.x; base < total; base += kUnroll * kThreads) {
+        float4 r[kUnroll];
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) {
+            const int i = base + u * kThreads;
+            if (i < total) {
+                const float4* p = s4[0] + i;
+#pragma unroll
+                for (int s = 1; s < NS; ++s)
+                    if (i >= start[s]) p = s4[s] + (i - start[s]);
+                r[u] = __ldg(p);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) {
+            const int i = base + u * kThreads;
+            if (i < total) {
+                float4* d = reinterpret_cast<float4*>(sp[0].dst) + i;
+#pragma unroll
+                for (int s = 1; s < NS; ++s)
+                    if (i >= start[s]) d = reinterpret_cast<float4*>(sp[s].dst) + (i - start[s]);
+                *d = r[u];
+            }
+        }
+    }
+}
+
+}  // namespace ts

@@ -139,7 +139,8 @@ def test_loss_parity(sc, engine):
     _grad_check(G[a:b], oG[a:b], "means via loss")
 
 
-def test_adam_bitwise(engine):
+@pytest.mark.parametrize("mode", [T.ADAM_REFERENCE, T.ADAM_FUSED])
+def test_adam_bitwise(engine, mode):
     n = 5003  # odd N: unaligned group boundaries exercise the scalar paths
     rng = np.random.default_rng(6)
     p = scene.random_params(n, 0.02, 0.0, 9)
@@ -148,13 +149,13 @@ def test_adam_bitwise(engine):
     v = np.abs(rng.normal(0, 1e-4, 59 * n)).astype(np.float32)
     engine.set_params(p, n)
     engine.set_state(grads=g, m=m, v=v)
-    cfg = T.AdamConfig.make(step=7, extent=2.5, zero_grads=1)
+    cfg = T.AdamConfig.make(step=7, extent=2.5, zero_grads=1, mode=mode)
     engine.adam_step(cfg)
     gp = engine.get_params()
     gg, gm, gv, _, _ = engine.get_state()
     op, om, ov = p.copy(), m.copy(), v.copy()
     O.adam_step(op, g.copy(), om, ov, n, np.array(cfg.lr[:], np.float32), cfg.beta1, cfg.beta2, cfg.eps,
-                cfg.bc1, cfg.bc2, mode=1)
+                cfg.bc1, cfg.bc2, mode=mode)
     assert np.array_equal(gp.view(np.uint32), op.view(np.uint32))
     assert np.array_equal(gm.view(np.uint32), om.view(np.uint32))
     assert np.array_equal(gv.view(np.uint32), ov.view(np.uint32))

@@ -472,29 +472,32 @@ Rect bound_tiles(const GFwd<T>& F, const Cam<T>& cam, const tso_render_config& c
 }
 
 // tile_cull_exact: max of the Gaussian over the tile's
-// sample rectangle; keep iff Q(p*) <= k2 (inclusive).
+// sample rectangle; keep iff Q(p*) <= k2 (inclusive).  With the
+// centre outside the rectangle the minimum of the convex Q lies on an edge
+// facing the centre (at most one vertical + one horizontal edge); on an edge
+// the 1D optimum t* = -(B/C) dx (resp. -(B/A) dy) is clamped to the edge.
 template <class T>
 bool tile_keep(T mx, T my, T A, T B, T C, T k2, int tx, int ty, const Cam<T>& cam) {
     T x0 = T(tx * TILE), y0 = T(ty * TILE);
     T x1 = T(std::min(tx * TILE + TILE - 1, cam.w - 1));
     T y1 = T(std::min(ty * TILE + TILE - 1, cam.h - 1));
-    if (mx >= x0 && mx <= x1 && my >= y0 && my <= y1) return true;
+    const bool inx = mx >= x0 && mx <= x1, iny = my >= y0 && my <= y1;
+    if (inx && iny) return true;
+    T nBA = (-B) / A, nBC = (-B) / C;
     T B2 = B + B;
     T best = T(INFINITY);
-    // vertical edges x = x0, x = x1
-    for (int e = 0; e < 2; ++e) {
-        T dx = (e == 0 ? x0 : x1) - mx;
+    if (!inx) {
+        T dx = (mx < x0 ? x0 : x1) - mx;
         T lo = y0 - my, hi = y1 - my;
-        T dy = (-(B * dx)) / C;
+        T dy = nBC * dx;
         dy = dy < lo ? lo : (dy > hi ? hi : dy);
         T qv = conic_q(A, B2, C, dx, dy);
         best = qv < best ? qv : best;
     }
-    // horizontal edges y = y0, y = y1
-    for (int e = 0; e < 2; ++e) {
-        T dy = (e == 0 ? y0 : y1) - my;
+    if (!iny) {
+        T dy = (my < y0 ? y0 : y1) - my;
         T lo = x0 - mx, hi = x1 - mx;
-        T dx = (-(B * dy)) / A;
+        T dx = nBA * dy;
         dx = dx < lo ? lo : (dx > hi ? hi : dx);
         T qv = conic_q(A, B2, C, dx, dy);
         best = qv < best ? qv : best;

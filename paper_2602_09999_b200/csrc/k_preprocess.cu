@@ -216,9 +216,10 @@ __global__ void __launch_bounds__(kBlock) preprocess_kernel(
         if (cfg.cull_mode == 0) {
             cnt = uint32_t((tx1 - tx0 + 1) * (ty1 - ty0 + 1));
         } else {
+            const float nBA = div(-B, A), nBC = div(-B, C);
             for (int tyy = ty0; tyy <= ty1; ++tyy)
                 for (int txx = tx0; txx <= tx1; ++txx)
-                    cnt += tile_keep(mx, my, A, B, C, k2, txx, tyy, cam.w, cam.h) ? 1u : 0u;
+                    cnt += tile_keep(mx, my, A, B, C, k2, nBA, nBC, txx, tyy, cam.w, cam.h) ? 1u : 0u;
         }
     } while (false);
     (void)ok;

@@ -113,63 +113,70 @@ __global__ void __launch_bounds__(kScanThreads) scan_kernel(const uint32_t* __re
 }
 
 // ----------------------------------------------------------------------------
-// radix pass: histogram + stable rank/scatter (8-bit digit)
+// Onesweep LSD radix sort (8-bit digits, stable):
+//   1. one read of the keys builds the global digit histogram of EVERY pass;
+//   2. per pass ONE kernel: each CTA takes the next tile (ticket), ranks its
+//      2048 keys stably in shared memory (warp match + per-warp counters),
+//      publishes its per-digit counts and resolves its global offsets by
+//      decoupled look-back over earlier tiles (one thread per digit), then
+//      writes digit-grouped runs (coalesced) from shared memory.
+// Per pass per element: one read and one write of (key, value).
 // ----------------------------------------------------------------------------
-constexpr int kRadixThreads = 256;
-constexpr int kRadixItems = 16;
-constexpr int kRadixTile = kRadixThreads * kRadixItems;  // 4096
-constexpr int kWarps = kRadixThreads / 32;
+constexpr int kRT = 256;             // threads per CTA
+constexpr int kRI = 8;               // keys per thread
+constexpr int kRTile = kRT * kRI;    // 2048 keys per tile
+constexpr int kRW = kRT / 32;        // warps
+constexpr uint32_t kFlagA = 1u << 30, kFlagP = 2u << 30, kValMask = (1u << 30) - 1u;
 
-template <class K>
-__global__ void __launch_bounds__(kRadixThreads) radix_hist_kernel(const K* __restrict__ keys, int64_t n, int shift,
-                                                                   uint32_t* __restrict__ hist, int nblocks) {
-    __shared__ uint32_t cnt[kWarps][256];
-    const int wid = threadIdx.x >> 5;
-    for (int i = threadIdx.x; i < kWarps * 256; i += kRadixThreads) (&cnt[0][0])[i] = 0;
+template <class K, int NPASS>
+__global__ void __launch_bounds__(256) radix_global_hist_kernel(const K* __restrict__ keys, int64_t n,
+                                                                uint32_t* __restrict__ ghist) {
+    __shared__ uint32_t h[NPASS * 256];
+    for (int i = threadIdx.x; i < NPASS * 256; i += blockDim.x) h[i] = 0;
     __syncthreads();
-    const int64_t base = int64_t(blockIdx.x) * kRadixTile;
-#pragma unroll 4
-    for (int k = 0; k < kRadixItems; ++k) {
-        const int64_t i = base + int64_t(k) * kRadixThreads + threadIdx.x;
-        if (i < n) atomicAdd(&cnt[wid][(uint32_t(keys[i]) >> shift) & 255u], 1u);
-    }
-    __syncthreads();
-    for (int d = threadIdx.x; d < 256; d += kRadixThreads) {
-        uint32_t s = 0;
+    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+        const uint32_t k = uint32_t(keys[i]);
 #pragma unroll
-        for (int w = 0; w < kWarps; ++w) s += cnt[w][d];
-        hist[int64_t(d) * nblocks + blockIdx.x] = s;
+        for (int p = 0; p < NPASS; ++p) atomicAdd(&h[p * 256 + ((k >> (8 * p)) & 255u)], 1u);
     }
+    __syncthreads();
+    for (int i = threadIdx.x; i < NPASS * 256; i += blockDim.x)
+        if (h[i]) atomicAdd(&ghist[i], h[i]);
 }
 
 template <class K>
-__global__ void __launch_bounds__(kRadixThreads) radix_scatter_kernel(const K* __restrict__ kin,
-                                                                      const uint32_t* __restrict__ vin,
-                                                                      K* __restrict__ kout,
-                                                                      uint32_t* __restrict__ vout, int64_t n,
-                                                                      int shift, const uint32_t* __restrict__ goff,
-                                                                      int nblocks) {
-    __shared__ uint32_t wcnt[kWarps][256];
-    __shared__ uint32_t bstart[256];
-    __shared__ uint32_t gstart[256];
+__global__ void __launch_bounds__(kRT) onesweep_kernel(const K* __restrict__ kin, const uint32_t* __restrict__ vin,
+                                                      K* __restrict__ kout, uint32_t* __restrict__ vout, int64_t n,
+                                                      int shift, const uint32_t* __restrict__ ghist,
+                                                      uint32_t* __restrict__ status, uint32_t* __restrict__ ticket) {
+    __shared__ uint32_t wcnt[kRW][256];
+    __shared__ uint32_t s_bstart[256];
+    __shared__ uint32_t s_goff[256];
     __shared__ uint32_t s_warp[33];
-    __shared__ K skey[kRadixTile];
-    __shared__ uint32_t sval[kRadixTile];
+    __shared__ K skey[kRTile];
+    __shared__ uint32_t sval[kRTile];
+    __shared__ uint32_t s_tile;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    for (int i = threadIdx.x; i < kWarps * 256; i += kRadixThreads) (&wcnt[0][0])[i] = 0;
+    if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1u);
+    for (int i = threadIdx.x; i < kRW * 256; i += kRT) (&wcnt[0][0])[i] = 0;
     __syncthreads();
-    const int64_t wbase = int64_t(blockIdx.x) * kRadixTile + int64_t(wid) * (kRadixItems * 32);
+    const uint32_t tile = s_tile;
+    const int64_t wbase = int64_t(tile) * kRTile + int64_t(wid) * (kRI * 32);
     const uint32_t lt = (1u << lane) - 1u;
-    K kk[kRadixItems];
-    uint32_t vv[kRadixItems];
-    uint32_t dr[kRadixItems];  // digit | rank << 8 ; digit 0x1FF = invalid
+    K kk[kRI];
+    uint32_t vv[kRI];
 #pragma unroll
-    for (int r = 0; r < kRadixItems; ++r) {
+    for (int r = 0; r < kRI; ++r) {
+        const int64_t i = wbase + r * 32 + lane;
+        kk[r] = i < n ? kin[i] : K(0);
+        vv[r] = i < n ? vin[i] : 0u;
+    }
+    uint32_t dr[kRI];  // digit | (rank within warp) << 9 ; digit 0x1FF = invalid
+#pragma unroll
+    for (int r = 0; r < kRI; ++r) {
         const int64_t i = wbase + r * 32 + lane;
         const bool valid = i < n;
-        K key = valid ? kin[i] : K(0);
-        uint32_t val = valid ? vin[i] : 0u;
-        uint32_t d = valid ? ((uint32_t(key) >> shift) & 255u) : 0x1FFu;
+        const uint32_t d = valid ? ((uint32_t(kk[r]) >> shift) & 255u) : 0x1FFu;
         const uint32_t peers = __match_any_sync(0xffffffffu, d);
         uint32_t rank = 0;
         if (valid) {
@@ -179,45 +186,58 @@ __global__ void __launch_bounds__(kRadixThreads) radix_scatter_kernel(const K* _
             if ((peers & lt) == 0) wcnt[wid][d] = pre + __popc(peers);
         }
         __syncwarp();
-        kk[r] = key;
-        vv[r] = val;
         dr[r] = d | (rank << 9);
     }
     __syncthreads();
-    // per digit: exclusive prefix over warps; block totals
+    // per digit (thread d): exclusive prefix over warps, block total
+    const int d = threadIdx.x;
     uint32_t tot = 0;
-    const int d = threadIdx.x;  // 256 threads == 256 digits
-    {
-        uint32_t run = 0;
 #pragma unroll
-        for (int w = 0; w < kWarps; ++w) {
-            uint32_t t = wcnt[w][d];
-            wcnt[w][d] = run;
-            run += t;
-        }
-        tot = run;
-        gstart[d] = goff[int64_t(d) * nblocks + blockIdx.x];
+    for (int w = 0; w < kRW; ++w) {
+        const uint32_t t = wcnt[w][d];
+        wcnt[w][d] = tot;
+        tot += t;
     }
+    // publish this tile's count, look back for the exclusive prefix of digit d
+    uint32_t excl = 0;
+    if (tile == 0) {
+        atomicExch(&status[d], kFlagP | tot);
+    } else {
+        atomicExch(&status[size_t(tile) * 256 + d], kFlagA | tot);
+        int64_t j = int64_t(tile) - 1;
+        while (j >= 0) {
+            uint32_t s;
+            do {
+                s = *reinterpret_cast<volatile uint32_t*>(&status[size_t(j) * 256 + d]);
+            } while ((s & ~kValMask) == 0);
+            excl += s & kValMask;
+            if ((s & ~kValMask) == kFlagP) break;
+            --j;
+        }
+        atomicExch(&status[size_t(tile) * 256 + d], kFlagP | (excl + tot));
+    }
+    // global start of digit d for this pass = exclusive scan of the global histogram
+    uint32_t gtot;
+    const uint32_t gstart = block_excl_scan(ghist[d], s_warp, &gtot);
+    s_goff[d] = gstart + excl;
     uint32_t btot;
-    const uint32_t bs = block_excl_scan(tot, s_warp, &btot);
-    bstart[d] = bs;
+    s_bstart[d] = block_excl_scan(tot, s_warp, &btot);
     __syncthreads();
-    // local stable placement
 #pragma unroll
-    for (int r = 0; r < kRadixItems; ++r) {
+    for (int r = 0; r < kRI; ++r) {
         const uint32_t dd = dr[r] & 0x1FFu;
         if (dd < 256u) {
-            const uint32_t lp = bstart[dd] + wcnt[wid][dd] + (dr[r] >> 9);
+            const uint32_t lp = s_bstart[dd] + wcnt[wid][dd] + (dr[r] >> 9);
             skey[lp] = kk[r];
             sval[lp] = vv[r];
         }
     }
     __syncthreads();
-    const int64_t tile_n = tmin<int64_t>(kRadixTile, n - int64_t(blockIdx.x) * kRadixTile);
-    for (int i = threadIdx.x; i < tile_n; i += kRadixThreads) {
+    const int64_t tile_n = tmin<int64_t>(kRTile, n - int64_t(tile) * kRTile);
+    for (int i = threadIdx.x; i < tile_n; i += kRT) {
         const K key = skey[i];
         const uint32_t dd = (uint32_t(key) >> shift) & 255u;
-        const uint32_t pos = gstart[dd] + (uint32_t(i) - bstart[dd]);
+        const uint32_t pos = s_goff[dd] + (uint32_t(i) - s_bstart[dd]);
         kout[pos] = key;
         vout[pos] = sval[i];
     }
@@ -239,9 +259,10 @@ __global__ void duplicate_kernel(const uint32_t* __restrict__ perm, const uint32
     const uint2 rc = rect[g];
     const int tx0 = rc.x & 0xFFFF, tx1 = rc.x >> 16, ty0 = rc.y & 0xFFFF, ty1 = rc.y >> 16;
     const float4 s0 = splat[3 * g], s1 = splat[3 * g + 1];
+    const float nBA = tsx::div(-s1.y, s1.x), nBC = tsx::div(-s1.y, s1.z);
     for (int ty = ty0; ty <= ty1; ++ty)
         for (int tx = tx0; tx <= tx1; ++tx) {
-            if (cull_mode == 0 || tsx::tile_keep(s0.x, s0.y, s1.x, s1.y, s1.z, s0.z, tx, ty, W, H)) {
+            if (cull_mode == 0 || tsx::tile_keep(s0.x, s0.y, s1.x, s1.y, s1.z, s0.z, nBA, nBC, tx, ty, W, H)) {
                 tkey[o] = uint16_t(ty * tiles_x + tx);
                 ival[o] = g;
                 ++o;
@@ -278,30 +299,36 @@ void launch_exclusive_scan(Context& c, const uint32_t* in, const uint32_t* perm,
     TS_LAUNCHED(c);
 }
 
-template <class K>
-void radix_pass(Context& c, const K* kin, const uint32_t* vin, K* kout, uint32_t* vout, int64_t n, int shift) {
+// Sorts (keys, vals) stably by the low 8*npass key bits, ping-ponging between
+// buffers 0 and 1 of the given pairs; the result ends in buffer (npass & 1).
+template <class K, int NPASS>
+void radix_sort(Context& c, K* k0, uint32_t* v0, K* k1, uint32_t* v1, int64_t n) {
     if (n == 0) return;
-    const int nblocks = int((n + kRadixTile - 1) / kRadixTile);
-    const size_t hn = size_t(nblocks) * 256;
-    ensure(c, c.rhist, 2 * hn + 1);
-    uint32_t* hist = c.rhist.p;
-    uint32_t* offs = c.rhist.p + hn;
-    radix_hist_kernel<K><<<nblocks, kRadixThreads, 0, c.stream>>>(kin, n, shift, hist, nblocks);
+    const int64_t tiles = (n + kRTile - 1) / kRTile;
+    // scratch: [NPASS*256 global hist][NPASS tickets][NPASS * tiles * 256 status]
+    const size_t words = size_t(NPASS) * 256 + 32 + size_t(NPASS) * size_t(tiles) * 256;
+    ensure(c, c.rhist, words);
+    uint32_t* ghist = c.rhist.p;
+    uint32_t* tickets = ghist + NPASS * 256;
+    uint32_t* status = tickets + 32;
+    cudaMemsetAsync(c.rhist.p, 0, words * 4, c.stream);
+    const int hb = int(std::min<int64_t>(int64_t(c.sm_count) * 4, (n + 255) / 256));
+    radix_global_hist_kernel<K, NPASS><<<hb, 256, 0, c.stream>>>(k0, n, ghist);
     TS_LAUNCHED(c);
-    launch_exclusive_scan(c, hist, nullptr, offs, int64_t(hn));
-    radix_scatter_kernel<K><<<nblocks, kRadixThreads, 0, c.stream>>>(kin, vin, kout, vout, n, shift, offs, nblocks);
-    TS_LAUNCHED(c);
+    K* ks[2] = {k0, k1};
+    uint32_t* vs[2] = {v0, v1};
+    for (int p = 0; p < NPASS; ++p) {
+        const int s = p & 1;
+        onesweep_kernel<K><<<unsigned(tiles), kRT, 0, c.stream>>>(ks[s], vs[s], ks[s ^ 1], vs[s ^ 1], n, 8 * p,
+                                                                   ghist + 256 * p, status + size_t(p) * tiles * 256,
+                                                                   tickets + p);
+        TS_LAUNCHED(c);
+    }
 }
-
-template void radix_pass<uint32_t>(Context&, const uint32_t*, const uint32_t*, uint32_t*, uint32_t*, int64_t, int);
-template void radix_pass<uint16_t>(Context&, const uint16_t*, const uint32_t*, uint16_t*, uint32_t*, int64_t, int);
 
 void launch_depth_sort(Context& c) {
     // stable LSD over 32-bit depth keys; 4 passes end in buffer 0
-    for (int p = 0; p < 4; ++p) {
-        const int s = p & 1;
-        radix_pass<uint32_t>(c, c.dkey[s].p, c.dperm[s].p, c.dkey[s ^ 1].p, c.dperm[s ^ 1].p, c.N, 8 * p);
-    }
+    radix_sort<uint32_t, 4>(c, c.dkey[0].p, c.dperm[0].p, c.dkey[1].p, c.dperm[1].p, c.N);
 }
 
 int64_t launch_scan_counts(Context& c) {
@@ -322,14 +349,12 @@ void launch_duplicate(Context& c, const DevCam& cam, const ts_render_config& cfg
 }
 
 void launch_tile_sort(Context& c, int tile_bits) {
-    const int passes = (tile_bits + 7) / 8;
-    for (int p = 0; p < passes; ++p) {
-        const int s = p & 1;
-        radix_pass<uint16_t>(c, c.tkey[s].p, c.ival[s].p, c.tkey[s ^ 1].p, c.ival[s ^ 1].p, c.I, 8 * p);
-    }
-    if (passes & 1) {  // keep the sorted list in buffer 0
-        std::swap(c.tkey[0], c.tkey[1]);
+    if (tile_bits <= 8) {
+        radix_sort<uint16_t, 1>(c, c.tkey[0].p, c.ival[0].p, c.tkey[1].p, c.ival[1].p, c.I);
+        std::swap(c.tkey[0], c.tkey[1]);  // keep the sorted list in buffer 0
         std::swap(c.ival[0], c.ival[1]);
+    } else {
+        radix_sort<uint16_t, 2>(c, c.tkey[0].p, c.ival[0].p, c.tkey[1].p, c.ival[1].p, c.I);
     }
 }
 

@@ -117,9 +117,6 @@ int64_t launch_densify(Context& c, float grad_thresh, float log_small, float log
 // gathered through perm (in[perm[i]]) when perm != nullptr.  out has n+1 entries.
 void launch_exclusive_scan(Context& c, const uint32_t* in, const uint32_t* perm, uint32_t* out, int64_t n);
 
-// radix sort one 8-bit digit pass (stable)
-template <class K>
-void radix_pass(Context& c, const K* kin, const uint32_t* vin, K* kout, uint32_t* vout, int64_t n, int shift);
 
 template <class T>
 bool ensure(Context& c, DevBuf<T>& b, size_t n, bool keep = false);

@@ -54,6 +54,8 @@ __device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* s_warp
     return r;
 }
 
+// in/out may be permuted: element i of the scanned sequence is in[perm[i]]
+// and its exclusive prefix is written to out[perm[i]] (out[n] = total).
 __global__ void __launch_bounds__(kScanThreads) scan_kernel(const uint32_t* __restrict__ in,
                                                             const uint32_t* __restrict__ perm,
                                                             uint32_t* __restrict__ out, int64_t n,
@@ -66,38 +68,55 @@ __global__ void __launch_bounds__(kScanThreads) scan_kernel(const uint32_t* __re
     __syncthreads();
     const uint32_t tile = s_tile;
     const int64_t base = int64_t(tile) * kScanTile + int64_t(threadIdx.x) * kScanItems;
-    uint32_t v[kScanItems];
+    uint32_t v[kScanItems], pi[kScanItems];
     uint32_t sum = 0;
 #pragma unroll
     for (int k = 0; k < kScanItems; ++k) {
         const int64_t i = base + k;
+        pi[k] = (perm && i < n) ? __ldg(perm + i) : uint32_t(i);
+    }
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) {
+        const int64_t i = base + k;
         uint32_t x = 0;
-        if (i < n) x = perm ? __ldg(in + __ldg(perm + i)) : __ldg(in + i);
+        if (i < n) x = __ldg(in + pi[k]);
         v[k] = x;
         sum += x;
     }
     uint32_t agg;
     uint32_t excl = block_excl_scan(sum, s_warp, &agg);
-    if (threadIdx.x == 0) {
+    // decoupled look-back by warp 0 over a window of 32 predecessors at a time
+    if (threadIdx.x < 32) {
         volatile unsigned long long* st = state;
+        const int lane = threadIdx.x;
         if (tile == 0) {
-            st[0] = (2ull << 32) | agg;
-            s_prefix = 0;
+            if (lane == 0) st[0] = (2ull << 32) | agg;
+            if (lane == 0) s_prefix = 0;
         } else {
-            st[tile] = (1ull << 32) | agg;
+            if (lane == 0) st[tile] = (1ull << 32) | agg;
             uint32_t prefix = 0;
-            int64_t j = int64_t(tile) - 1;
-            while (j >= 0) {
-                unsigned long long s;
-                do {
-                    s = st[j];
-                } while ((s >> 32) == 0);
-                prefix += uint32_t(s);
-                if ((s >> 32) == 2) break;
-                --j;
+            int64_t j0 = int64_t(tile) - 1;  // window: tiles j0, j0-1, ..., j0-31
+            while (true) {
+                const int64_t j = j0 - lane;
+                unsigned long long s = 2ull << 32;  // before tile 0: inclusive prefix 0
+                if (j >= 0) {
+                    do {
+                        s = st[j];
+                    } while ((s >> 32) == 0);
+                }
+                const unsigned pmask = __ballot_sync(0xffffffffu, (s >> 32) == 2);
+                const int first = pmask ? __ffs(pmask) - 1 : 32;  // closest inclusive prefix
+                uint32_t v = lane <= first ? uint32_t(s) : 0u;
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+                prefix += v;
+                if (pmask) break;
+                j0 -= 32;
             }
-            st[tile] = (2ull << 32) | (prefix + agg);
-            s_prefix = prefix;
+            if (lane == 0) {
+                st[tile] = (2ull << 32) | (prefix + agg);
+                s_prefix = prefix;
+            }
         }
     }
     __syncthreads();
@@ -105,7 +124,7 @@ __global__ void __launch_bounds__(kScanThreads) scan_kernel(const uint32_t* __re
 #pragma unroll
     for (int k = 0; k < kScanItems; ++k) {
         const int64_t i = base + k;
-        if (i < n) out[i] = run;
+        if (i < n) out[pi[k]] = run;
         run += v[k];
     }
     if (int64_t(tile) == (n - 1) / kScanTile && threadIdx.x == kScanThreads - 1) out[n] = s_prefix + agg;
@@ -113,56 +132,55 @@ __global__ void __launch_bounds__(kScanThreads) scan_kernel(const uint32_t* __re
 }
 
 // ----------------------------------------------------------------------------
-// Onesweep LSD radix sort (8-bit digits, stable):
-//   1. one read of the keys builds the global digit histogram of EVERY pass;
-//   2. per pass ONE kernel: each CTA takes the next tile (ticket), ranks its
-//      2048 keys stably in shared memory (warp match + per-warp counters),
-//      publishes its per-digit counts and resolves its global offsets by
-//      decoupled look-back over earlier tiles (one thread per digit), then
-//      writes digit-grouped runs (coalesced) from shared memory.
-// Per pass per element: one read and one write of (key, value).
+// LSD radix sort, 8-bit digits, stable.  Per pass: per-tile digit counts
+// (tile = 2048 keys) -> one exclusive scan over the digit-major count matrix
+// -> rank + scatter: each CTA loads its 2048 keys and values up front (16
+// independent loads per thread), ranks them stably in shared memory (warp
+// match + per-warp digit counters), and writes digit-grouped runs coalesced.
 // ----------------------------------------------------------------------------
 constexpr int kRT = 256;             // threads per CTA
 constexpr int kRI = 8;               // keys per thread
 constexpr int kRTile = kRT * kRI;    // 2048 keys per tile
 constexpr int kRW = kRT / 32;        // warps
-constexpr uint32_t kFlagA = 1u << 30, kFlagP = 2u << 30, kValMask = (1u << 30) - 1u;
 
-template <class K, int NPASS>
-__global__ void __launch_bounds__(256) radix_global_hist_kernel(const K* __restrict__ keys, int64_t n,
-                                                                uint32_t* __restrict__ ghist) {
-    __shared__ uint32_t h[NPASS * 256];
-    for (int i = threadIdx.x; i < NPASS * 256; i += blockDim.x) h[i] = 0;
+template <class K>
+__global__ void __launch_bounds__(kRT) radix_count_kernel(const K* __restrict__ keys, int64_t n, int shift,
+                                                          uint32_t* __restrict__ counts, int ntiles) {
+    __shared__ uint32_t h[kRW][256];
+    const int wid = threadIdx.x >> 5;
+    for (int i = threadIdx.x; i < kRW * 256; i += kRT) (&h[0][0])[i] = 0;
     __syncthreads();
-    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
-        const uint32_t k = uint32_t(keys[i]);
+    const int64_t base = int64_t(blockIdx.x) * kRTile;
+    uint32_t d[kRI];
 #pragma unroll
-        for (int p = 0; p < NPASS; ++p) atomicAdd(&h[p * 256 + ((k >> (8 * p)) & 255u)], 1u);
+    for (int r = 0; r < kRI; ++r) {
+        const int64_t i = base + int64_t(r) * kRT + threadIdx.x;
+        d[r] = i < n ? ((uint32_t(keys[i]) >> shift) & 255u) : 0x100u;
     }
+#pragma unroll
+    for (int r = 0; r < kRI; ++r)
+        if (d[r] < 256u) atomicAdd(&h[wid][d[r]], 1u);
     __syncthreads();
-    for (int i = threadIdx.x; i < NPASS * 256; i += blockDim.x)
-        if (h[i]) atomicAdd(&ghist[i], h[i]);
+    const int dd = threadIdx.x;
+    uint32_t s = 0;
+#pragma unroll
+    for (int w = 0; w < kRW; ++w) s += h[w][dd];
+    counts[int64_t(dd) * ntiles + blockIdx.x] = s;
 }
 
 template <class K>
-__global__ void __launch_bounds__(kRT) onesweep_kernel(const K* __restrict__ kin, const uint32_t* __restrict__ vin,
-                                                      K* __restrict__ kout, uint32_t* __restrict__ vout, int64_t n,
-                                                      int shift, const uint32_t* __restrict__ ghist,
-                                                      uint32_t* __restrict__ status, uint32_t* __restrict__ ticket) {
+__global__ void __launch_bounds__(kRT) radix_scatter_kernel(const K* __restrict__ kin,
+                                                           const uint32_t* __restrict__ vin, K* __restrict__ kout,
+                                                           uint32_t* __restrict__ vout, int64_t n, int shift,
+                                                           const uint32_t* __restrict__ goff, int ntiles) {
     __shared__ uint32_t wcnt[kRW][256];
     __shared__ uint32_t s_bstart[256];
     __shared__ uint32_t s_goff[256];
     __shared__ uint32_t s_warp[33];
     __shared__ K skey[kRTile];
     __shared__ uint32_t sval[kRTile];
-    __shared__ uint32_t s_tile;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1u);
-    for (int i = threadIdx.x; i < kRW * 256; i += kRT) (&wcnt[0][0])[i] = 0;
-    __syncthreads();
-    const uint32_t tile = s_tile;
-    const int64_t wbase = int64_t(tile) * kRTile + int64_t(wid) * (kRI * 32);
-    const uint32_t lt = (1u << lane) - 1u;
+    const int64_t wbase = int64_t(blockIdx.x) * kRTile + int64_t(wid) * (kRI * 32);
     K kk[kRI];
     uint32_t vv[kRI];
 #pragma unroll
@@ -171,6 +189,10 @@ __global__ void __launch_bounds__(kRT) onesweep_kernel(const K* __restrict__ kin
         kk[r] = i < n ? kin[i] : K(0);
         vv[r] = i < n ? vin[i] : 0u;
     }
+    for (int i = threadIdx.x; i < kRW * 256; i += kRT) (&wcnt[0][0])[i] = 0;
+    s_goff[threadIdx.x] = goff[int64_t(threadIdx.x) * ntiles + blockIdx.x];
+    __syncthreads();
+    const uint32_t lt = (1u << lane) - 1u;
     uint32_t dr[kRI];  // digit | (rank within warp) << 9 ; digit 0x1FF = invalid
 #pragma unroll
     for (int r = 0; r < kRI; ++r) {
@@ -178,18 +200,13 @@ __global__ void __launch_bounds__(kRT) onesweep_kernel(const K* __restrict__ kin
         const bool valid = i < n;
         const uint32_t d = valid ? ((uint32_t(kk[r]) >> shift) & 255u) : 0x1FFu;
         const uint32_t peers = __match_any_sync(0xffffffffu, d);
-        uint32_t rank = 0;
-        if (valid) {
-            const uint32_t pre = wcnt[wid][d];
-            rank = pre + __popc(peers & lt);
-            __syncwarp(peers);
-            if ((peers & lt) == 0) wcnt[wid][d] = pre + __popc(peers);
-        }
+        const uint32_t pre = valid ? wcnt[wid][d] : 0u;
         __syncwarp();
-        dr[r] = d | (rank << 9);
+        if (valid && (peers & lt) == 0) wcnt[wid][d] = pre + __popc(peers);
+        __syncwarp();
+        dr[r] = d | ((pre + __popc(peers & lt)) << 9);
     }
     __syncthreads();
-    // per digit (thread d): exclusive prefix over warps, block total
     const int d = threadIdx.x;
     uint32_t tot = 0;
 #pragma unroll
@@ -198,28 +215,6 @@ __global__ void __launch_bounds__(kRT) onesweep_kernel(const K* __restrict__ kin
         wcnt[w][d] = tot;
         tot += t;
     }
-    // publish this tile's count, look back for the exclusive prefix of digit d
-    uint32_t excl = 0;
-    if (tile == 0) {
-        atomicExch(&status[d], kFlagP | tot);
-    } else {
-        atomicExch(&status[size_t(tile) * 256 + d], kFlagA | tot);
-        int64_t j = int64_t(tile) - 1;
-        while (j >= 0) {
-            uint32_t s;
-            do {
-                s = *reinterpret_cast<volatile uint32_t*>(&status[size_t(j) * 256 + d]);
-            } while ((s & ~kValMask) == 0);
-            excl += s & kValMask;
-            if ((s & ~kValMask) == kFlagP) break;
-            --j;
-        }
-        atomicExch(&status[size_t(tile) * 256 + d], kFlagP | (excl + tot));
-    }
-    // global start of digit d for this pass = exclusive scan of the global histogram
-    uint32_t gtot;
-    const uint32_t gstart = block_excl_scan(ghist[d], s_warp, &gtot);
-    s_goff[d] = gstart + excl;
     uint32_t btot;
     s_bstart[d] = block_excl_scan(tot, s_warp, &btot);
     __syncthreads();
@@ -233,29 +228,36 @@ __global__ void __launch_bounds__(kRT) onesweep_kernel(const K* __restrict__ kin
         }
     }
     __syncthreads();
-    const int64_t tile_n = tmin<int64_t>(kRTile, n - int64_t(tile) * kRTile);
-    for (int i = threadIdx.x; i < tile_n; i += kRT) {
-        const K key = skey[i];
-        const uint32_t dd = (uint32_t(key) >> shift) & 255u;
-        const uint32_t pos = s_goff[dd] + (uint32_t(i) - s_bstart[dd]);
-        kout[pos] = key;
-        vout[pos] = sval[i];
+    const int tile_n = int(tmin<int64_t>(kRTile, n - int64_t(blockIdx.x) * kRTile));
+#pragma unroll
+    for (int r = 0; r < kRI; ++r) {
+        const int i = threadIdx.x + r * kRT;
+        if (i < tile_n) {
+            const K key = skey[i];
+            const uint32_t dd = (uint32_t(key) >> shift) & 255u;
+            const uint32_t pos = s_goff[dd] + (uint32_t(i) - s_bstart[dd]);
+            kout[pos] = key;
+            vout[pos] = sval[i];
+        }
     }
 }
 
 // ----------------------------------------------------------------------------
 // K3 duplicate (write pass of build_instances; per depth-sorted Gaussian)
 // ----------------------------------------------------------------------------
-__global__ void duplicate_kernel(const uint32_t* __restrict__ perm, const uint32_t* __restrict__ offsets,
-                                 const uint32_t* __restrict__ tcount, const uint2* __restrict__ rect,
-                                 const float4* __restrict__ splat, int64_t N, int W, int H, int tiles_x,
-                                 int cull_mode, uint16_t* __restrict__ tkey, uint32_t* __restrict__ ival) {
+// Iterates Gaussians in index order (coalesced reads); offsets[g] is the
+// exclusive prefix of tile counts in DEPTH order (scattered by the scan), so the
+// instance list comes out depth-major, Gaussian-major within equal depth.
+__global__ void duplicate_kernel(const uint32_t* __restrict__ offsets, const uint32_t* __restrict__ tcount,
+                                 const uint2* __restrict__ rect, const float4* __restrict__ splat, int64_t N, int W,
+                                 int H, int tiles_x, int cull_mode, uint16_t* __restrict__ tkey,
+                                 uint32_t* __restrict__ ival) {
     const int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (j >= N) return;
-    const uint32_t g = perm[j];
+    const uint32_t g = uint32_t(j);
     const uint32_t c = tcount[g];
     if (c == 0) return;
-    uint32_t o = offsets[j];
+    uint32_t o = offsets[g];
     const uint2 rc = rect[g];
     const int tx0 = rc.x & 0xFFFF, tx1 = rc.x >> 16, ty0 = rc.y & 0xFFFF, ty1 = rc.y >> 16;
     const float4 s0 = splat[3 * g], s1 = splat[3 * g + 1];
@@ -299,29 +301,25 @@ void launch_exclusive_scan(Context& c, const uint32_t* in, const uint32_t* perm,
     TS_LAUNCHED(c);
 }
 
-// Sorts (keys, vals) stably by the low 8*npass key bits, ping-ponging between
-// buffers 0 and 1 of the given pairs; the result ends in buffer (npass & 1).
+// Sorts (keys, vals) stably by the low 8*NPASS key bits, ping-ponging between
+// buffers 0 and 1 of the given pairs; the result ends in buffer (NPASS & 1).
 template <class K, int NPASS>
 void radix_sort(Context& c, K* k0, uint32_t* v0, K* k1, uint32_t* v1, int64_t n) {
     if (n == 0) return;
-    const int64_t tiles = (n + kRTile - 1) / kRTile;
-    // scratch: [NPASS*256 global hist][NPASS tickets][NPASS * tiles * 256 status]
-    const size_t words = size_t(NPASS) * 256 + 32 + size_t(NPASS) * size_t(tiles) * 256;
-    ensure(c, c.rhist, words);
-    uint32_t* ghist = c.rhist.p;
-    uint32_t* tickets = ghist + NPASS * 256;
-    uint32_t* status = tickets + 32;
-    cudaMemsetAsync(c.rhist.p, 0, words * 4, c.stream);
-    const int hb = int(std::min<int64_t>(int64_t(c.sm_count) * 4, (n + 255) / 256));
-    radix_global_hist_kernel<K, NPASS><<<hb, 256, 0, c.stream>>>(k0, n, ghist);
-    TS_LAUNCHED(c);
+    const int ntiles = int((n + kRTile - 1) / kRTile);
+    const size_t hn = size_t(ntiles) * 256;
+    ensure(c, c.rhist, 2 * hn + 1);
+    uint32_t* counts = c.rhist.p;
+    uint32_t* offs = c.rhist.p + hn;
     K* ks[2] = {k0, k1};
     uint32_t* vs[2] = {v0, v1};
     for (int p = 0; p < NPASS; ++p) {
         const int s = p & 1;
-        onesweep_kernel<K><<<unsigned(tiles), kRT, 0, c.stream>>>(ks[s], vs[s], ks[s ^ 1], vs[s ^ 1], n, 8 * p,
-                                                                   ghist + 256 * p, status + size_t(p) * tiles * 256,
-                                                                   tickets + p);
+        radix_count_kernel<K><<<ntiles, kRT, 0, c.stream>>>(ks[s], n, 8 * p, counts, ntiles);
+        TS_LAUNCHED(c);
+        launch_exclusive_scan(c, counts, nullptr, offs, int64_t(hn));
+        radix_scatter_kernel<K><<<ntiles, kRT, 0, c.stream>>>(ks[s], vs[s], ks[s ^ 1], vs[s ^ 1], n, 8 * p, offs,
+                                                              ntiles);
         TS_LAUNCHED(c);
     }
 }
@@ -343,8 +341,8 @@ void launch_duplicate(Context& c, const DevCam& cam, const ts_render_config& cfg
     if (c.N == 0 || c.I == 0) return;
     const int bs = 256;
     duplicate_kernel<<<unsigned((c.N + bs - 1) / bs), bs, 0, c.stream>>>(
-        c.dperm[0].p, c.offsets.p, c.tcount.p, c.rect.p, c.splat.p, c.N, cam.w, cam.h, cam.tiles_x,
-        cfg.cull_mode, c.tkey[0].p, c.ival[0].p);
+        c.offsets.p, c.tcount.p, c.rect.p, c.splat.p, c.N, cam.w, cam.h, cam.tiles_x, cfg.cull_mode, c.tkey[0].p,
+        c.ival[0].p);
     TS_LAUNCHED(c);
 }
 

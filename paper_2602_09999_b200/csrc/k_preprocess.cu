@@ -16,7 +16,7 @@ constexpr int kBlock = 128;
 template <int DEG>
 __global__ void __launch_bounds__(kBlock) preprocess_kernel(
     const float* __restrict__ P, int64_t N, DevCam cam, ts_render_config cfg, float4* __restrict__ splat,
-    uint2* __restrict__ rect, uint32_t* __restrict__ tcount, uint32_t* __restrict__ dkey,
+    uint4* __restrict__ rect, uint32_t* __restrict__ tcount, uint32_t* __restrict__ dkey,
     uint32_t* __restrict__ dperm, uint32_t* __restrict__ vis_counter) {
     using namespace tsx;
     // staged inputs of the CTA's 128 Gaussians (one pass of independent 16-byte loads)
@@ -52,7 +52,7 @@ __global__ void __launch_bounds__(kBlock) preprocess_kernel(
     const int tid = threadIdx.x;
     float4 s0 = make_float4(0.f, 0.f, 0.f, 0.f), s1 = s0, s2 = s0;
     uint32_t cnt = 0;
-    uint2 rc = make_uint2(1u, 1u);  // empty: tx0=1 > tx1=0
+    uint4 rc = make_uint4(1u, 1u, 0u, 0u);  // empty: tx0=1 > tx1=0
     bool ok = false;
     float zh = 0.f;
     do {
@@ -212,15 +212,26 @@ __global__ void __launch_bounds__(kBlock) preprocess_kernel(
         const int py0 = int(ceilf(loy)), py1 = int(floorf(hiy));
         if (px0 > px1 || py0 > py1) break;
         const int tx0 = px0 >> 4, tx1 = px1 >> 4, ty0 = py0 >> 4, ty1 = py1 >> 4;
-        rc = make_uint2(uint32_t(tx0) | (uint32_t(tx1) << 16), uint32_t(ty0) | (uint32_t(ty1) << 16));
+        const int ntl = (tx1 - tx0 + 1) * (ty1 - ty0 + 1);
+        const bool big = ntl > 64;
+        rc = make_uint4(uint32_t(tx0) | (uint32_t(tx1) << 16),
+                        uint32_t(ty0) | (uint32_t(ty1) << 16) | (big ? 0x80000000u : 0u), 0u, 0u);
+        uint64_t mask = 0;
         if (cfg.cull_mode == 0) {
-            cnt = uint32_t((tx1 - tx0 + 1) * (ty1 - ty0 + 1));
+            cnt = uint32_t(ntl);
+            if (!big) mask = ntl == 64 ? ~0ull : ((1ull << ntl) - 1ull);
         } else {
             const float nBA = div(-B, A), nBC = div(-B, C);
+            int bit = 0;
             for (int tyy = ty0; tyy <= ty1; ++tyy)
-                for (int txx = tx0; txx <= tx1; ++txx)
-                    cnt += tile_keep(mx, my, A, B, C, k2, nBA, nBC, txx, tyy, cam.w, cam.h) ? 1u : 0u;
+                for (int txx = tx0; txx <= tx1; ++txx, ++bit) {
+                    const bool keep = tile_keep(mx, my, A, B, C, k2, nBA, nBC, txx, tyy, cam.w, cam.h);
+                    cnt += keep ? 1u : 0u;
+                    if (keep && !big) mask |= 1ull << bit;
+                }
         }
+        rc.z = uint32_t(mask);
+        rc.w = uint32_t(mask >> 32);
     } while (false);
     (void)ok;
     splat[3 * g] = s0;

@@ -54,8 +54,8 @@ __device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* s_warp
     return r;
 }
 
-// in/out may be permuted: element i of the scanned sequence is in[perm[i]]
-// and its exclusive prefix is written to out[perm[i]] (out[n] = total).
+// element i of the scanned sequence is in[perm[i]] (or in[i]); its exclusive
+// prefix is written to out[i] and the total to out[n].
 __global__ void __launch_bounds__(kScanThreads) scan_kernel(const uint32_t* __restrict__ in,
                                                             const uint32_t* __restrict__ perm,
                                                             uint32_t* __restrict__ out, int64_t n,
@@ -124,7 +124,7 @@ __global__ void __launch_bounds__(kScanThreads) scan_kernel(const uint32_t* __re
 #pragma unroll
     for (int k = 0; k < kScanItems; ++k) {
         const int64_t i = base + k;
-        if (i < n) out[pi[k]] = run;
+        if (i < n) out[i] = run;
         run += v[k];
     }
     if (int64_t(tile) == (n - 1) / kScanTile && threadIdx.x == kScanThreads - 1) out[n] = s_prefix + agg;
@@ -245,21 +245,35 @@ __global__ void __launch_bounds__(kRT) radix_scatter_kernel(const K* __restrict_
 // ----------------------------------------------------------------------------
 // K3 duplicate (write pass of build_instances; per depth-sorted Gaussian)
 // ----------------------------------------------------------------------------
-// Iterates Gaussians in index order (coalesced reads); offsets[g] is the
-// exclusive prefix of tile counts in DEPTH order (scattered by the scan), so the
-// instance list comes out depth-major, Gaussian-major within equal depth.
-__global__ void duplicate_kernel(const uint32_t* __restrict__ offsets, const uint32_t* __restrict__ tcount,
-                                 const uint2* __restrict__ rect, const float4* __restrict__ splat, int64_t N, int W,
+// Iterates depth-sorted positions j (offsets[j] = exclusive prefix of tile
+// counts in depth order, so writes are contiguous across a warp); each
+// Gaussian's kept tiles come from the 64-bit mask K1 recorded over its tile
+// rect (bit = row-major position in the rect), so the exact-cull test is NOT
+// re-evaluated; rects of more than 64 tiles (flag bit) re-run it.
+__global__ void duplicate_kernel(const uint32_t* __restrict__ perm, const uint32_t* __restrict__ offsets,
+                                 const uint4* __restrict__ binrec, const float4* __restrict__ splat, int64_t N, int W,
                                  int H, int tiles_x, int cull_mode, uint16_t* __restrict__ tkey,
                                  uint32_t* __restrict__ ival) {
     const int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (j >= N) return;
-    const uint32_t g = uint32_t(j);
-    const uint32_t c = tcount[g];
-    if (c == 0) return;
-    uint32_t o = offsets[g];
-    const uint2 rc = rect[g];
-    const int tx0 = rc.x & 0xFFFF, tx1 = rc.x >> 16, ty0 = rc.y & 0xFFFF, ty1 = rc.y >> 16;
+    const uint32_t g = perm[j];
+    const uint4 rc = binrec[g];
+    const int tx0 = rc.x & 0xFFFF, tx1 = (rc.x >> 16) & 0x7FFF, ty0 = rc.y & 0xFFFF, ty1 = (rc.y >> 16) & 0x7FFF;
+    if (tx0 > tx1 || ty0 > ty1) return;
+    uint32_t o = offsets[j];
+    if (!(rc.y & 0x80000000u)) {
+        const int wdt = tx1 - tx0 + 1;
+        uint64_t m = (uint64_t(rc.w) << 32) | rc.z;
+        while (m) {
+            const int bit = __ffsll((long long)m) - 1;
+            m &= m - 1;
+            const int ty = ty0 + bit / wdt, tx = tx0 + bit % wdt;
+            tkey[o] = uint16_t(ty * tiles_x + tx);
+            ival[o] = g;
+            ++o;
+        }
+        return;
+    }
     const float4 s0 = splat[3 * g], s1 = splat[3 * g + 1];
     const float nBA = tsx::div(-s1.y, s1.x), nBC = tsx::div(-s1.y, s1.z);
     for (int ty = ty0; ty <= ty1; ++ty)
@@ -341,7 +355,7 @@ void launch_duplicate(Context& c, const DevCam& cam, const ts_render_config& cfg
     if (c.N == 0 || c.I == 0) return;
     const int bs = 256;
     duplicate_kernel<<<unsigned((c.N + bs - 1) / bs), bs, 0, c.stream>>>(
-        c.offsets.p, c.tcount.p, c.rect.p, c.splat.p, c.N, cam.w, cam.h, cam.tiles_x, cfg.cull_mode, c.tkey[0].p,
+        c.dperm[0].p, c.offsets.p, c.rect.p, c.splat.p, c.N, cam.w, cam.h, cam.tiles_x, cfg.cull_mode, c.tkey[0].p,
         c.ival[0].p);
     TS_LAUNCHED(c);
 }

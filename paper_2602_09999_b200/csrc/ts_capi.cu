@@ -41,6 +41,7 @@ bool ensure(Context& c, DevBuf<T>& b, size_t n, bool keep) {
 template bool ensure<float>(Context&, DevBuf<float>&, size_t, bool);
 template bool ensure<float4>(Context&, DevBuf<float4>&, size_t, bool);
 template bool ensure<uint2>(Context&, DevBuf<uint2>&, size_t, bool);
+template bool ensure<uint4>(Context&, DevBuf<uint4>&, size_t, bool);
 template bool ensure<uint8_t>(Context&, DevBuf<uint8_t>&, size_t, bool);
 template bool ensure<uint16_t>(Context&, DevBuf<uint16_t>&, size_t, bool);
 template bool ensure<uint32_t>(Context&, DevBuf<uint32_t>&, size_t, bool);
@@ -638,11 +639,11 @@ ts_status ts_debug_preprocess(ts_ctx* x, float* splat12, int32_t* rect4, uint32_
     CK(cudaSetDevice(c.device));
     const size_t N = size_t(c.N);
     std::vector<float4> sp(3 * N);
-    std::vector<uint2> rc(N);
+    std::vector<uint4> rc(N);
     std::vector<uint32_t> cnt(N);
     if (N) {
         CK(cudaMemcpyAsync(sp.data(), c.splat.p, 3 * N * 16, cudaMemcpyDeviceToHost, c.stream));
-        CK(cudaMemcpyAsync(rc.data(), c.rect.p, N * 8, cudaMemcpyDeviceToHost, c.stream));
+        CK(cudaMemcpyAsync(rc.data(), c.rect.p, N * 16, cudaMemcpyDeviceToHost, c.stream));
         CK(cudaMemcpyAsync(cnt.data(), c.tcount.p, N * 4, cudaMemcpyDeviceToHost, c.stream));
     }
     CK(cudaStreamSynchronize(c.stream));
@@ -651,8 +652,8 @@ ts_status ts_debug_preprocess(ts_ctx* x, float* splat12, int32_t* rect4, uint32_
         if (rect4) {
             rect4[4 * g] = int32_t(rc[g].x & 0xFFFF);
             rect4[4 * g + 1] = int32_t(rc[g].y & 0xFFFF);
-            rect4[4 * g + 2] = int32_t(rc[g].x >> 16);
-            rect4[4 * g + 3] = int32_t(rc[g].y >> 16);
+            rect4[4 * g + 2] = int32_t((rc[g].x >> 16) & 0x7FFF);
+            rect4[4 * g + 3] = int32_t((rc[g].y >> 16) & 0x7FFF);
         }
         if (tile_count) tile_count[g] = cnt[g];
         if (depth_key) {

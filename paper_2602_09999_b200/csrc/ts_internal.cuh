@@ -52,7 +52,7 @@ struct Context {
 
     // per-view (sized by N)
     DevBuf<float4> splat;        // 3 float4 per Gaussian: (mx,my,k2,o) (A,B,C,depth) (r,g,b,det)
-    DevBuf<uint2> rect;          // packed tile rect
+    DevBuf<uint4> rect;          // {tx0|tx1<<16, ty0|ty1<<16 (bit31: >64 tiles), kept-tile mask lo, hi}
     DevBuf<uint32_t> tcount;     // tiles per Gaussian
     DevBuf<uint32_t> dkey[2];    // depth keys (radix double buffer)
     DevBuf<uint32_t> dperm[2];   // gaussian indices (radix double buffer)

@@ -278,3 +278,17 @@ def test_multi_view_gradients_accumulate(engine):
     for (a, b), nm in zip(T.group_slices(n), T.GROUPS):
         _grad_check(G[a:b], oG[a:b], nm)
     assert np.array_equal(vc, ovc)
+
+
+def test_cpp_host_driver():
+    """The C++ API (include/tilesplat/tilesplat.hpp) trains through the C-ABI with
+    the full schedule (densify every 100 iterations)."""
+    import json
+    import os
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([os.path.join(root, "tools", "ts_train"), "20000", "300"], capture_output=True, text=True,
+                         timeout=300)
+    assert out.returncode == 0, out.stderr
+    r = json.loads(out.stdout.strip().splitlines()[-1])
+    assert r["loss_last"] < 0.8 * r["loss_first"]

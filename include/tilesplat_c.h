@@ -72,8 +72,9 @@ typedef struct {
 
 /* Adam: per-group lr (means, log_scales, quats, opacity,
  * sh_dc, sh_rest), betas, eps, host-computed bias corrections 1-b^t, mode
- * (0 reference, 1 fused, 2 skip-invisible), zero_grads (1: clear the gradient
- * buffer in the same sweep). */
+ * (0 reference, 1 fused, 2 skip-invisible, 3 fused_backward,
+ * 4 fused_backward_skip_invisible; modes 3/4 only in ts_backward_adam /
+ * ts_train_step), zero_grads (1: clear the gradient buffer in the same sweep). */
 typedef struct {
     float lr[6];
     float beta1, beta2, eps, bc1, bc2;
@@ -118,6 +119,13 @@ ts_status ts_reserve_flat(ts_ctx* ctx, int64_t min_len);
 ts_status ts_adam_step(ts_ctx* ctx, const ts_adam_config* cfg);
 /* Adam over [begin, end) of the flat buffer only (sharded optimizer for data parallel). */
 ts_status ts_adam_step_range(ts_ctx* ctx, const ts_adam_config* cfg, int64_t begin, int64_t end);
+
+/* fused_backward_update: backward of the last forward with the Adam
+ * update applied to each Gaussian's gradient row in place (modes 3/4); the end state
+ * equals ts_backward + ts_adam_step(mode 1/2) bitwise.  Only for single-view steps
+ * (the gradient buffer is neither read nor written). */
+ts_status ts_backward_adam(ts_ctx* ctx, const float* dL_dC_hwc /* or NULL: ts_loss result */,
+                           const ts_adam_config* adam);
 
 /* ---- one training step on one view: forward, loss, backward, Adam ---- */
 ts_status ts_train_step(ts_ctx* ctx, const ts_camera* cam, const ts_render_config* cfg,

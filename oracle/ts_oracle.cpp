@@ -1332,6 +1332,9 @@ void tso_adam_step(int64_t n, float* th, const float* g, float* m, float* v, con
     float lr_eff[6];
     for (int k = 0; k < 6; ++k) lr_eff[k] = float(double(lr[k]) / double(bc1));
     const float rsb2 = float(1.0 / std::sqrt(double(bc2)));
+    // fused_backward modes (3, 4) have the end state of fused (1) / skip-invisible (2)
+    if (mode == 3) mode = 1;
+    if (mode == 4) mode = 2;
     pfor(L, [&](int64_t b, int64_t e) {
         for (int64_t i = b; i < e; ++i) {
             int64_t gi;

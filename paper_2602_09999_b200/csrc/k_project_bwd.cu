@@ -1,13 +1,25 @@
-// K9 preprocess_bwd: one thread per Gaussian (visible ones do work).
+// K9 preprocess_bwd: one thread per Gaussian.
 // backward_project with the J clamp adjoint, the SH colour
 // clamp, sigmoid/exp activation adjoints, and
 // accumulate_densify_stats: accum += |dL/dmean2d|, count += 1.
-// Gradients are ACCUMULATED into the flat 59*N buffer (multi-view batches sum,
-// SPEC.md:735); the per-Gaussian 2D accumulator is consumed and zeroed here.
-// HBM-bound: a CTA stages all inputs of its 128 Gaussians (6 attribute blocks,
-// SH rows, 2D gradients, statistics) with one pass of independent 16-byte
-// loads (stage_spans), computes from shared memory, and writes SH gradient
-// rows back through shared memory so every global access is coalesced.
+//
+// Two kernels share the per-Gaussian adjoint (pb_grads):
+//  * project_bwd_kernel: gradients written (after a clear) or ACCUMULATED into
+//    the flat 59*N buffer (multi-view batches sum);
+//  * project_bwd_adam_kernel: fused_backward_update: each
+//    Gaussian's complete gradient row is consumed by the fused Adam update in
+//    place, and rows of invisible Gaussians get the zero-gradient update in
+//    the same sweep (or none in skip-invisible mode) -- the end state is bitwise
+//    that of backward + adam_step_fused, without writing or re-reading the
+//    gradient buffer.
+// Both are HBM-bound: a CTA stages all inputs of its Gaussians (attribute
+// blocks of the 59*N layout, SH rows, 2D gradients, statistics; for the fused
+// kernel also both Adam moments) with one pass of independent 16-byte loads
+// (stage_spans), computes from shared memory, and writes rows back through
+// shared memory so every global access is coalesced.  The per-Gaussian 2D
+// accumulator is consumed and zeroed.
+#include <cmath>
+
 #include "ts_internal.cuh"
 #include "ts_math.cuh"
 #include "ts_stage.cuh"
@@ -15,6 +27,254 @@
 namespace ts {
 namespace {
 
+// staged per-Gaussian rows of one Gaussian
+struct Rows {
+    const float* mu;   // 3
+    const float* ls;   // 3
+    const float* q;    // 4
+    float op;          // logit
+    const float* dc;   // 3
+    const float* rest; // 45 (only [0, nrest) read)
+    const float* g2;   // 12: dmx dmy dA dB dC do dr dg db
+};
+
+// Adjoint of one visible Gaussian.  gs[14] = d{means(3), log_scales(3),
+// quats(4), opacity_logit(1), sh_dc(3)}; SH-rest gradients [0, nrest) are
+// written to grest.  Returns |dL/dmean2d| for the densification statistics.
+template <int DEG>
+__device__ __forceinline__ float pb_grads(const Rows& r, float* grest, const DevCam& cam,
+                                          const ts_render_config& cfg, float (&gs)[14]) {
+    constexpr int nb = (DEG + 1) * (DEG + 1);
+    const float* W = cam.W;
+    const float dmx = r.g2[0], dmy = r.g2[1], dA = r.g2[2], dB = r.g2[3], dC = r.g2[4], dop = r.g2[5];
+    float drc[3] = {r.g2[6], r.g2[7], r.g2[8]};
+    // ---- recompute forward quantities ----
+    const float mu[3] = {r.mu[0], r.mu[1], r.mu[2]};
+    const float xh = W[0] * mu[0] + W[1] * mu[1] + W[2] * mu[2] + W[3];
+    const float yh = W[4] * mu[0] + W[5] * mu[1] + W[6] * mu[2] + W[7];
+    const float zh = W[8] * mu[0] + W[9] * mu[1] + W[10] * mu[2] + W[11];
+    const float q0 = r.q[0], q1 = r.q[1], q2 = r.q[2], q3 = r.q[3];
+    const float qn = sqrtf(q0 * q0 + q1 * q1 + q2 * q2 + q3 * q3);
+    const float iqn = 1.f / qn;
+    const float w = q0 * iqn, x = q1 * iqn, y = q2 * iqn, z = q3 * iqn;
+    float R[9];
+    R[0] = 1.f - 2.f * (y * y + z * z);
+    R[1] = 2.f * (x * y - w * z);
+    R[2] = 2.f * (x * z + w * y);
+    R[3] = 2.f * (x * y + w * z);
+    R[4] = 1.f - 2.f * (x * x + z * z);
+    R[5] = 2.f * (y * z - w * x);
+    R[6] = 2.f * (x * z - w * y);
+    R[7] = 2.f * (y * z + w * x);
+    R[8] = 1.f - 2.f * (x * x + y * y);
+    float s[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) s[k] = __expf(r.ls[k]);
+    float Mm[9];
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int k = 0; k < 3; ++k) Mm[3 * i + k] = R[3 * i + k] * s[k];
+    float Sf[9];
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j)
+            Sf[3 * i + j] = Mm[3 * i] * Mm[3 * j] + Mm[3 * i + 1] * Mm[3 * j + 1] + Mm[3 * i + 2] * Mm[3 * j + 2];
+    const float limx = 1.3f * (0.5f * float(cam.w) / cam.fx);
+    const float limy = 1.3f * (0.5f * float(cam.h) / cam.fy);
+    const float iz = 1.f / zh, iz2 = iz * iz, iz3 = iz2 * iz;
+    const float txz = xh * iz, tyz = yh * iz;
+    const bool clx = (txz < -limx) || (txz > limx);
+    const bool cly = (tyz < -limy) || (tyz > limy);
+    const float ux = fminf(limx, fmaxf(-limx, txz)), uy = fminf(limy, fmaxf(-limy, tyz));
+    const float J00 = cam.fx * iz, J02 = -cam.fx * ux * iz;
+    const float J11 = cam.fy * iz, J12 = -cam.fy * uy * iz;
+    float Tm[6];
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+        Tm[j] = J00 * W[j] + J02 * W[8 + j];
+        Tm[3 + j] = J11 * W[4 + j] + J12 * W[8 + j];
+    }
+    float TS[6];
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+        for (int j = 0; j < 3; ++j)
+            TS[3 * a + j] = Tm[3 * a] * Sf[j] + Tm[3 * a + 1] * Sf[3 + j] + Tm[3 * a + 2] * Sf[6 + j];
+    const float ca = TS[0] * Tm[0] + TS[1] * Tm[1] + TS[2] * Tm[2] + cfg.dilation;
+    const float cb = TS[0] * Tm[3] + TS[1] * Tm[4] + TS[2] * Tm[5];
+    const float cc = TS[3] * Tm[3] + TS[4] * Tm[4] + TS[5] * Tm[5] + cfg.dilation;
+    const float idet = 1.f / (ca * cc - cb * cb);
+    const float A = cc * idet, B = -cb * idet, C = ca * idet;
+    const float o = 1.f / (1.f + __expf(-r.op));
+    // ---- colour / SH ----
+    const float cpx = -(W[0] * W[3] + W[4] * W[7] + W[8] * W[11]);
+    const float cpy = -(W[1] * W[3] + W[5] * W[7] + W[9] * W[11]);
+    const float cpz = -(W[2] * W[3] + W[6] * W[7] + W[10] * W[11]);
+    const float e0 = mu[0] - cpx, e1 = mu[1] - cpy, e2 = mu[2] - cpz;
+    const float dl = sqrtf(e0 * e0 + e1 * e1 + e2 * e2);
+    const float idl = 1.f / dl;
+    const float d0 = e0 * idl, d1 = e1 * idl, d2 = e2 * idl;
+    float Y[16];
+    float dY[16][3];
+    Y[0] = TS_SH_C0;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) dY[k][0] = dY[k][1] = dY[k][2] = 0.f;
+    if (DEG >= 1) {
+        Y[1] = -TS_SH_C1 * d1;
+        Y[2] = TS_SH_C1 * d2;
+        Y[3] = -TS_SH_C1 * d0;
+        dY[1][1] = -TS_SH_C1;
+        dY[2][2] = TS_SH_C1;
+        dY[3][0] = -TS_SH_C1;
+    }
+    if (DEG >= 2) {
+        const float xx = d0 * d0, yy = d1 * d1, zz = d2 * d2;
+        Y[4] = TS_SH_C2_0 * d0 * d1;
+        Y[5] = TS_SH_C2_1 * d1 * d2;
+        Y[6] = TS_SH_C2_2 * (2.f * zz - xx - yy);
+        Y[7] = TS_SH_C2_3 * d0 * d2;
+        Y[8] = TS_SH_C2_4 * (xx - yy);
+        dY[4][0] = TS_SH_C2_0 * d1;
+        dY[4][1] = TS_SH_C2_0 * d0;
+        dY[5][1] = TS_SH_C2_1 * d2;
+        dY[5][2] = TS_SH_C2_1 * d1;
+        dY[6][0] = -2.f * TS_SH_C2_2 * d0;
+        dY[6][1] = -2.f * TS_SH_C2_2 * d1;
+        dY[6][2] = 4.f * TS_SH_C2_2 * d2;
+        dY[7][0] = TS_SH_C2_3 * d2;
+        dY[7][2] = TS_SH_C2_3 * d0;
+        dY[8][0] = 2.f * TS_SH_C2_4 * d0;
+        dY[8][1] = -2.f * TS_SH_C2_4 * d1;
+        if (DEG >= 3) {
+            Y[9] = TS_SH_C3_0 * d1 * (3.f * xx - yy);
+            Y[10] = TS_SH_C3_1 * d0 * d1 * d2;
+            Y[11] = TS_SH_C3_2 * d1 * (4.f * zz - xx - yy);
+            Y[12] = TS_SH_C3_3 * d2 * (2.f * zz - 3.f * xx - 3.f * yy);
+            Y[13] = TS_SH_C3_4 * d0 * (4.f * zz - xx - yy);
+            Y[14] = TS_SH_C3_5 * d2 * (xx - yy);
+            Y[15] = TS_SH_C3_6 * d0 * (xx - 3.f * yy);
+            dY[9][0] = TS_SH_C3_0 * 6.f * d0 * d1;
+            dY[9][1] = TS_SH_C3_0 * (3.f * xx - 3.f * yy);
+            dY[10][0] = TS_SH_C3_1 * d1 * d2;
+            dY[10][1] = TS_SH_C3_1 * d0 * d2;
+            dY[10][2] = TS_SH_C3_1 * d0 * d1;
+            dY[11][0] = -2.f * TS_SH_C3_2 * d0 * d1;
+            dY[11][1] = TS_SH_C3_2 * (4.f * zz - xx - 3.f * yy);
+            dY[11][2] = 8.f * TS_SH_C3_2 * d1 * d2;
+            dY[12][0] = -6.f * TS_SH_C3_3 * d0 * d2;
+            dY[12][1] = -6.f * TS_SH_C3_3 * d1 * d2;
+            dY[12][2] = TS_SH_C3_3 * (6.f * zz - 3.f * xx - 3.f * yy);
+            dY[13][0] = TS_SH_C3_4 * (4.f * zz - 3.f * xx - yy);
+            dY[13][1] = -2.f * TS_SH_C3_4 * d0 * d1;
+            dY[13][2] = 8.f * TS_SH_C3_4 * d0 * d2;
+            dY[14][0] = 2.f * TS_SH_C3_5 * d0 * d2;
+            dY[14][1] = -2.f * TS_SH_C3_5 * d1 * d2;
+            dY[14][2] = TS_SH_C3_5 * (xx - yy);
+            dY[15][0] = TS_SH_C3_6 * (3.f * xx - 3.f * yy);
+            dY[15][1] = -6.f * TS_SH_C3_6 * d0 * d1;
+        }
+    }
+    float ddir0 = 0.f, ddir1 = 0.f, ddir2 = 0.f;
+#pragma unroll
+    for (int ch = 0; ch < 3; ++ch) {
+        float raw = Y[0] * r.dc[ch];
+#pragma unroll
+        for (int k = 1; k < nb; ++k) raw += Y[k] * r.rest[3 * (k - 1) + ch];
+        raw += 0.5f;
+        if (raw < 0.f) drc[ch] = 0.f;
+        const float d = drc[ch];
+        gs[11 + ch] = Y[0] * d;
+#pragma unroll
+        for (int k = 1; k < nb; ++k) {
+            const float cf = r.rest[3 * (k - 1) + ch] * d;
+            grest[3 * (k - 1) + ch] = Y[k] * d;
+            ddir0 += dY[k][0] * cf;
+            ddir1 += dY[k][1] * cf;
+            ddir2 += dY[k][2] * cf;
+        }
+    }
+    const float nd = d0 * ddir0 + d1 * ddir1 + d2 * ddir2;
+    float dmean0 = (ddir0 - d0 * nd) * idl, dmean1 = (ddir1 - d1 * nd) * idl, dmean2 = (ddir2 - d2 * nd) * idl;
+    // ---- opacity ----
+    gs[10] = dop * o * (1.f - o);
+    // ---- conic -> dilated cov2d ----
+    const float hb = 0.5f * dB;
+    const float K00 = A * dA + B * hb, K01 = A * hb + B * dC;
+    const float K10 = B * dA + C * hb, K11 = B * hb + C * dC;
+    const float da = -(K00 * A + K01 * B);
+    const float db = -2.f * (K00 * B + K01 * C);
+    const float dc = -(K10 * B + K11 * C);
+    // ---- cov2d = Tm S Tm^T ----
+    const float G2[4] = {da, 0.5f * db, 0.5f * db, dc};
+    float dS[9];
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j)
+            dS[3 * i + j] = Tm[i] * (G2[0] * Tm[j] + G2[1] * Tm[3 + j]) + Tm[3 + i] * (G2[2] * Tm[j] + G2[3] * Tm[3 + j]);
+    float dTm[6];
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+        for (int j = 0; j < 3; ++j) dTm[3 * a + j] = 2.f * (G2[2 * a] * TS[j] + G2[2 * a + 1] * TS[3 + j]);
+    const float dJ00 = dTm[0] * W[0] + dTm[1] * W[1] + dTm[2] * W[2];
+    const float dJ02 = dTm[0] * W[8] + dTm[1] * W[9] + dTm[2] * W[10];
+    const float dJ11 = dTm[3] * W[4] + dTm[4] * W[5] + dTm[5] * W[6];
+    const float dJ12 = dTm[3] * W[8] + dTm[4] * W[9] + dTm[5] * W[10];
+    // ---- camera point ----
+    float dtx = dmx * cam.fx * iz, dty = dmy * cam.fy * iz;
+    float dtz = -dmx * cam.fx * xh * iz2 - dmy * cam.fy * yh * iz2;
+    dtz += -dJ00 * cam.fx * iz2 - dJ11 * cam.fy * iz2;
+    if (!clx) {
+        dtx += dJ02 * (-cam.fx * iz2);
+        dtz += dJ02 * (2.f * cam.fx * xh * iz3);
+    } else {
+        dtz += dJ02 * (cam.fx * ux * iz2);
+    }
+    if (!cly) {
+        dty += dJ12 * (-cam.fy * iz2);
+        dtz += dJ12 * (2.f * cam.fy * yh * iz3);
+    } else {
+        dtz += dJ12 * (cam.fy * uy * iz2);
+    }
+    gs[0] = dmean0 + W[0] * dtx + W[4] * dty + W[8] * dtz;
+    gs[1] = dmean1 + W[1] * dtx + W[5] * dty + W[9] * dtz;
+    gs[2] = dmean2 + W[2] * dtx + W[6] * dty + W[10] * dtz;
+    // ---- Sigma = M M^T, M = R diag(s) ----
+    float dM[9];
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int k = 0; k < 3; ++k)
+            dM[3 * i + k] = 2.f * (dS[3 * i] * Mm[k] + dS[3 * i + 1] * Mm[3 + k] + dS[3 * i + 2] * Mm[6 + k]);
+    float dR[9];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        const float ds = R[k] * dM[k] + R[3 + k] * dM[3 + k] + R[6 + k] * dM[6 + k];
+#pragma unroll
+        for (int i = 0; i < 3; ++i) dR[3 * i + k] = dM[3 * i + k] * s[k];
+        gs[3 + k] = ds * s[k];
+    }
+    const float dqw = 2.f * (-z * dR[1] + y * dR[2] + z * dR[3] - x * dR[5] - y * dR[6] + x * dR[7]);
+    const float dqx = 2.f * (y * dR[1] + z * dR[2] + y * dR[3] - 2.f * x * dR[4] - w * dR[5] + z * dR[6] + w * dR[7] -
+                             2.f * x * dR[8]);
+    const float dqy = 2.f * (-2.f * y * dR[0] + x * dR[1] + w * dR[2] + x * dR[3] + z * dR[5] - w * dR[6] +
+                             z * dR[7] - 2.f * y * dR[8]);
+    const float dqz = 2.f * (-2.f * z * dR[0] - w * dR[1] + x * dR[2] + w * dR[3] - 2.f * z * dR[4] + y * dR[5] +
+                             x * dR[6] + y * dR[7]);
+    const float dot = w * dqw + x * dqx + y * dqy + z * dqz;
+    gs[6] = (dqw - w * dot) * iqn;
+    gs[7] = (dqx - x * dot) * iqn;
+    gs[8] = (dqy - y * dot) * iqn;
+    gs[9] = (dqz - z * dot) * iqn;
+    return sqrtf(dmx * dmx + dmy * dmy);
+}
+
+// ---------------------------------------------------------------------------
+// gradient-writing kernel
+// ---------------------------------------------------------------------------
 constexpr int kBlock = 128;
 
 // shared-memory layout of one CTA (floats; every segment a multiple of 4)
@@ -42,17 +302,13 @@ __global__ void __launch_bounds__(kBlock) project_bwd_kernel(const float* __rest
                                                              ts_render_config cfg) {
     extern __shared__ __align__(16) float smem[];
     using L = PbLayout<DEG, ACCUM>;
+    constexpr int nrest = 3 * ((DEG + 1) * (DEG + 1) - 1);
     const Off off(N);
     const int64_t g0 = int64_t(blockIdx.x) * kBlock;
     const int64_t g = g0 + threadIdx.x;
-    constexpr int deg = DEG;
-    constexpr int nb = (deg + 1) * (deg + 1);
-    constexpr int nrest = 3 * (nb - 1);
     const int rows = int(tmin<int64_t>(kBlock, N - g0));
     const bool active = g < N && tcount[g] != 0;
-    // does any Gaussian of this block need work?
     if (!__syncthreads_or(active)) return;
-    // ---- stage every per-Gaussian input of the CTA in one pass (max MLP) ----
     int sh[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
     {
         const Span base[8] = {{smem + L::kMu, P + off.means + 3 * g0, 3 * rows},
@@ -81,253 +337,170 @@ __global__ void __launch_bounds__(kBlock) project_bwd_kernel(const float* __rest
         }
     }
     __syncthreads();
-#define GW(idx, val)                          \
-    do {                                      \
-        if constexpr (ACCUM) G[idx] += (val); \
-        else G[idx] = (val);                  \
-    } while (0)
     const int tid = threadIdx.x;
+    float* rest_row = smem + L::kRest + sh[8] + tid * 45;
     if (active) {
-        const float* W = cam.W;
-        const float* g2s = smem + L::kG2 + sh[5] + 12 * tid;
+        float dummy[4] = {0.f, 0.f, 0.f, 0.f};
+        const Rows rw{smem + L::kMu + sh[0] + 3 * tid, smem + L::kLs + sh[1] + 3 * tid, smem + L::kQ + sh[2] + 4 * tid,
+                      smem[L::kOp + sh[3] + tid],      smem + L::kDc + sh[4] + 3 * tid,
+                      DEG > 0 ? rest_row : dummy,      smem + L::kG2 + sh[5] + 12 * tid};
+        float gs[14];
+        float nrm;
+        if constexpr (ACCUM && nrest > 0) {
+            float grest[nrest];
+            nrm = pb_grads<DEG>(rw, grest, cam, cfg, gs);
+            float* grow = smem + L::kGRest + sh[9] + tid * 45;
+#pragma unroll
+            for (int k = 0; k < nrest; ++k) grow[k] += grest[k];
+        } else {
+            // overwrite mode: gradients replace the parameter row in place (each
+            // element is read by pb_grads before it is written)
+            nrm = pb_grads<DEG>(rw, DEG > 0 ? rest_row : dummy, cam, cfg, gs);
+        }
+        const int64_t idx[14] = {off.means + 3 * g,  off.means + 3 * g + 1, off.means + 3 * g + 2, off.ls + 3 * g,
+                                 off.ls + 3 * g + 1, off.ls + 3 * g + 2,    off.q + 4 * g,         off.q + 4 * g + 1,
+                                 off.q + 4 * g + 2,  off.q + 4 * g + 3,     off.op + g,            off.dc + 3 * g,
+                                 off.dc + 3 * g + 1, off.dc + 3 * g + 2};
+#pragma unroll
+        for (int k = 0; k < 14; ++k) {
+            if constexpr (ACCUM) G[idx[k]] += gs[k];
+            else G[idx[k]] = gs[k];
+        }
         reinterpret_cast<float4*>(g2d)[3 * g] = make_float4(0.f, 0.f, 0.f, 0.f);
         reinterpret_cast<float4*>(g2d)[3 * g + 1] = make_float4(0.f, 0.f, 0.f, 0.f);
         reinterpret_cast<float4*>(g2d)[3 * g + 2] = make_float4(0.f, 0.f, 0.f, 0.f);
-        const float dmx = g2s[0], dmy = g2s[1], dA = g2s[2], dB = g2s[3], dC = g2s[4], dop = g2s[5];
-        float drc[3] = {g2s[6], g2s[7], g2s[8]};
-        // ---- recompute forward quantities (from the staged rows) ----
-        const float* mus = smem + L::kMu + sh[0] + 3 * tid;
-        const float mu[3] = {mus[0], mus[1], mus[2]};
-        const float xh = W[0] * mu[0] + W[1] * mu[1] + W[2] * mu[2] + W[3];
-        const float yh = W[4] * mu[0] + W[5] * mu[1] + W[6] * mu[2] + W[7];
-        const float zh = W[8] * mu[0] + W[9] * mu[1] + W[10] * mu[2] + W[11];
-        const float* qs = smem + L::kQ + sh[2] + 4 * tid;
-        const float q0 = qs[0], q1 = qs[1], q2 = qs[2], q3 = qs[3];
-        const float qn = sqrtf(q0 * q0 + q1 * q1 + q2 * q2 + q3 * q3);
-        const float iqn = 1.f / qn;
-        const float w = q0 * iqn, x = q1 * iqn, y = q2 * iqn, z = q3 * iqn;
-        float R[9];
-        R[0] = 1.f - 2.f * (y * y + z * z);
-        R[1] = 2.f * (x * y - w * z);
-        R[2] = 2.f * (x * z + w * y);
-        R[3] = 2.f * (x * y + w * z);
-        R[4] = 1.f - 2.f * (x * x + z * z);
-        R[5] = 2.f * (y * z - w * x);
-        R[6] = 2.f * (x * z - w * y);
-        R[7] = 2.f * (y * z + w * x);
-        R[8] = 1.f - 2.f * (x * x + y * y);
-        const float* lss = smem + L::kLs + sh[1] + 3 * tid;
-        float s[3];
-        for (int k = 0; k < 3; ++k) s[k] = __expf(lss[k]);
-        float Mm[9];
-        for (int i = 0; i < 3; ++i)
-            for (int k = 0; k < 3; ++k) Mm[3 * i + k] = R[3 * i + k] * s[k];
-        float Sf[9];
-        for (int i = 0; i < 3; ++i)
-            for (int j = 0; j < 3; ++j)
-                Sf[3 * i + j] = Mm[3 * i] * Mm[3 * j] + Mm[3 * i + 1] * Mm[3 * j + 1] + Mm[3 * i + 2] * Mm[3 * j + 2];
-        const float limx = 1.3f * (0.5f * float(cam.w) / cam.fx);
-        const float limy = 1.3f * (0.5f * float(cam.h) / cam.fy);
-        const float iz = 1.f / zh, iz2 = iz * iz, iz3 = iz2 * iz;
-        const float txz = xh * iz, tyz = yh * iz;
-        const bool clx = (txz < -limx) || (txz > limx);
-        const bool cly = (tyz < -limy) || (tyz > limy);
-        const float ux = fminf(limx, fmaxf(-limx, txz)), uy = fminf(limy, fmaxf(-limy, tyz));
-        const float J00 = cam.fx * iz, J02 = -cam.fx * ux * iz;
-        const float J11 = cam.fy * iz, J12 = -cam.fy * uy * iz;
-        float Tm[6];
-        for (int j = 0; j < 3; ++j) {
-            Tm[j] = J00 * W[j] + J02 * W[8 + j];
-            Tm[3 + j] = J11 * W[4 + j] + J12 * W[8 + j];
-        }
-        float TS[6];
-        for (int r = 0; r < 2; ++r)
-            for (int j = 0; j < 3; ++j)
-                TS[3 * r + j] = Tm[3 * r] * Sf[j] + Tm[3 * r + 1] * Sf[3 + j] + Tm[3 * r + 2] * Sf[6 + j];
-        const float a = TS[0] * Tm[0] + TS[1] * Tm[1] + TS[2] * Tm[2] + cfg.dilation;
-        const float bb = TS[0] * Tm[3] + TS[1] * Tm[4] + TS[2] * Tm[5];
-        const float c = TS[3] * Tm[3] + TS[4] * Tm[4] + TS[5] * Tm[5] + cfg.dilation;
-        const float idet = 1.f / (a * c - bb * bb);
-        const float A = c * idet, B = -bb * idet, C = a * idet;
-        const float o = 1.f / (1.f + __expf(-smem[L::kOp + sh[3] + tid]));
-        const float* dcs = smem + L::kDc + sh[4] + 3 * tid;
-        // ---- colour / SH ----
-        const float cpx = -(W[0] * W[3] + W[4] * W[7] + W[8] * W[11]);
-        const float cpy = -(W[1] * W[3] + W[5] * W[7] + W[9] * W[11]);
-        const float cpz = -(W[2] * W[3] + W[6] * W[7] + W[10] * W[11]);
-        const float e0 = mu[0] - cpx, e1 = mu[1] - cpy, e2 = mu[2] - cpz;
-        const float dl = sqrtf(e0 * e0 + e1 * e1 + e2 * e2);
-        const float idl = 1.f / dl;
-        const float d0 = e0 * idl, d1 = e1 * idl, d2 = e2 * idl;
-        float* rs = smem + L::kRest + sh[8] + tid * 45;
-        float* rg = ACCUM ? smem + L::kGRest + sh[9] + tid * 45 : rs;  // overwrite mode reuses the param row
-        float Y[16];
-        float dY[16][3];
-        Y[0] = TS_SH_C0;
-        for (int k = 0; k < 16; ++k) dY[k][0] = dY[k][1] = dY[k][2] = 0.f;
-        if (deg >= 1) {
-            Y[1] = -TS_SH_C1 * d1;
-            Y[2] = TS_SH_C1 * d2;
-            Y[3] = -TS_SH_C1 * d0;
-            dY[1][1] = -TS_SH_C1;
-            dY[2][2] = TS_SH_C1;
-            dY[3][0] = -TS_SH_C1;
-        }
-        if (deg >= 2) {
-            const float xx = d0 * d0, yy = d1 * d1, zz = d2 * d2;
-            Y[4] = TS_SH_C2_0 * d0 * d1;
-            Y[5] = TS_SH_C2_1 * d1 * d2;
-            Y[6] = TS_SH_C2_2 * (2.f * zz - xx - yy);
-            Y[7] = TS_SH_C2_3 * d0 * d2;
-            Y[8] = TS_SH_C2_4 * (xx - yy);
-            dY[4][0] = TS_SH_C2_0 * d1;
-            dY[4][1] = TS_SH_C2_0 * d0;
-            dY[5][1] = TS_SH_C2_1 * d2;
-            dY[5][2] = TS_SH_C2_1 * d1;
-            dY[6][0] = -2.f * TS_SH_C2_2 * d0;
-            dY[6][1] = -2.f * TS_SH_C2_2 * d1;
-            dY[6][2] = 4.f * TS_SH_C2_2 * d2;
-            dY[7][0] = TS_SH_C2_3 * d2;
-            dY[7][2] = TS_SH_C2_3 * d0;
-            dY[8][0] = 2.f * TS_SH_C2_4 * d0;
-            dY[8][1] = -2.f * TS_SH_C2_4 * d1;
-            if (deg >= 3) {
-                Y[9] = TS_SH_C3_0 * d1 * (3.f * xx - yy);
-                Y[10] = TS_SH_C3_1 * d0 * d1 * d2;
-                Y[11] = TS_SH_C3_2 * d1 * (4.f * zz - xx - yy);
-                Y[12] = TS_SH_C3_3 * d2 * (2.f * zz - 3.f * xx - 3.f * yy);
-                Y[13] = TS_SH_C3_4 * d0 * (4.f * zz - xx - yy);
-                Y[14] = TS_SH_C3_5 * d2 * (xx - yy);
-                Y[15] = TS_SH_C3_6 * d0 * (xx - 3.f * yy);
-                dY[9][0] = TS_SH_C3_0 * 6.f * d0 * d1;
-                dY[9][1] = TS_SH_C3_0 * (3.f * xx - 3.f * yy);
-                dY[10][0] = TS_SH_C3_1 * d1 * d2;
-                dY[10][1] = TS_SH_C3_1 * d0 * d2;
-                dY[10][2] = TS_SH_C3_1 * d0 * d1;
-                dY[11][0] = -2.f * TS_SH_C3_2 * d0 * d1;
-                dY[11][1] = TS_SH_C3_2 * (4.f * zz - xx - 3.f * yy);
-                dY[11][2] = 8.f * TS_SH_C3_2 * d1 * d2;
-                dY[12][0] = -6.f * TS_SH_C3_3 * d0 * d2;
-                dY[12][1] = -6.f * TS_SH_C3_3 * d1 * d2;
-                dY[12][2] = TS_SH_C3_3 * (6.f * zz - 3.f * xx - 3.f * yy);
-                dY[13][0] = TS_SH_C3_4 * (4.f * zz - 3.f * xx - yy);
-                dY[13][1] = -2.f * TS_SH_C3_4 * d0 * d1;
-                dY[13][2] = 8.f * TS_SH_C3_4 * d0 * d2;
-                dY[14][0] = 2.f * TS_SH_C3_5 * d0 * d2;
-                dY[14][1] = -2.f * TS_SH_C3_5 * d1 * d2;
-                dY[14][2] = TS_SH_C3_5 * (xx - yy);
-                dY[15][0] = TS_SH_C3_6 * (3.f * xx - 3.f * yy);
-                dY[15][1] = -6.f * TS_SH_C3_6 * d0 * d1;
-            }
-        }
-        float ddir0 = 0.f, ddir1 = 0.f, ddir2 = 0.f;
-        for (int ch = 0; ch < 3; ++ch) {
-            float raw = Y[0] * dcs[ch];
-            _Pragma("unroll") for (int k = 1; k < nb; ++k) raw += Y[k] * rs[3 * (k - 1) + ch];
-            raw += 0.5f;
-            if (raw < 0.f) drc[ch] = 0.f;
-            const float d = drc[ch];
-            GW(off.dc + 3 * g + ch, Y[0] * d);
-            _Pragma("unroll") for (int k = 1; k < nb; ++k) {
-                const float cf = rs[3 * (k - 1) + ch] * d;
-                if constexpr (ACCUM) rg[3 * (k - 1) + ch] += Y[k] * d;
-                else rg[3 * (k - 1) + ch] = Y[k] * d;
-                ddir0 += dY[k][0] * cf;
-                ddir1 += dY[k][1] * cf;
-                ddir2 += dY[k][2] * cf;
-            }
-        }
-        const float nd = d0 * ddir0 + d1 * ddir1 + d2 * ddir2;
-        float dmean0 = (ddir0 - d0 * nd) * idl, dmean1 = (ddir1 - d1 * nd) * idl, dmean2 = (ddir2 - d2 * nd) * idl;
-        // ---- opacity ----
-        GW(off.op + g, dop * o * (1.f - o));
-        // ---- conic -> dilated cov2d ----
-        const float hb = 0.5f * dB;
-        const float K00 = A * dA + B * hb, K01 = A * hb + B * dC;
-        const float K10 = B * dA + C * hb, K11 = B * hb + C * dC;
-        const float da = -(K00 * A + K01 * B);
-        const float db = -2.f * (K00 * B + K01 * C);
-        const float dc = -(K10 * B + K11 * C);
-        // ---- cov2d = Tm S Tm^T ----
-        const float G2[4] = {da, 0.5f * db, 0.5f * db, dc};
-        float dS[9];
-        for (int i = 0; i < 3; ++i)
-            for (int j = 0; j < 3; ++j)
-                dS[3 * i + j] = Tm[i] * (G2[0] * Tm[j] + G2[1] * Tm[3 + j]) +
-                                Tm[3 + i] * (G2[2] * Tm[j] + G2[3] * Tm[3 + j]);
-        float dTm[6];
-        for (int r = 0; r < 2; ++r)
-            for (int j = 0; j < 3; ++j) dTm[3 * r + j] = 2.f * (G2[2 * r] * TS[j] + G2[2 * r + 1] * TS[3 + j]);
-        const float dJ00 = dTm[0] * W[0] + dTm[1] * W[1] + dTm[2] * W[2];
-        const float dJ02 = dTm[0] * W[8] + dTm[1] * W[9] + dTm[2] * W[10];
-        const float dJ11 = dTm[3] * W[4] + dTm[4] * W[5] + dTm[5] * W[6];
-        const float dJ12 = dTm[3] * W[8] + dTm[4] * W[9] + dTm[5] * W[10];
-        // ---- camera point ----
-        float dtx = dmx * cam.fx * iz, dty = dmy * cam.fy * iz;
-        float dtz = -dmx * cam.fx * xh * iz2 - dmy * cam.fy * yh * iz2;
-        dtz += -dJ00 * cam.fx * iz2 - dJ11 * cam.fy * iz2;
-        if (!clx) {
-            dtx += dJ02 * (-cam.fx * iz2);
-            dtz += dJ02 * (2.f * cam.fx * xh * iz3);
-        } else {
-            dtz += dJ02 * (cam.fx * ux * iz2);
-        }
-        if (!cly) {
-            dty += dJ12 * (-cam.fy * iz2);
-            dtz += dJ12 * (2.f * cam.fy * yh * iz3);
-        } else {
-            dtz += dJ12 * (cam.fy * uy * iz2);
-        }
-        dmean0 += W[0] * dtx + W[4] * dty + W[8] * dtz;
-        dmean1 += W[1] * dtx + W[5] * dty + W[9] * dtz;
-        dmean2 += W[2] * dtx + W[6] * dty + W[10] * dtz;
-        GW(off.means + 3 * g, dmean0);
-        GW(off.means + 3 * g + 1, dmean1);
-        GW(off.means + 3 * g + 2, dmean2);
-        // ---- Sigma = M M^T, M = R diag(s) ----
-        float dM[9];
-        for (int i = 0; i < 3; ++i)
-            for (int k = 0; k < 3; ++k)
-                dM[3 * i + k] = 2.f * (dS[3 * i] * Mm[k] + dS[3 * i + 1] * Mm[3 + k] + dS[3 * i + 2] * Mm[6 + k]);
-        float dR[9];
-        for (int k = 0; k < 3; ++k) {
-            const float ds = R[k] * dM[k] + R[3 + k] * dM[3 + k] + R[6 + k] * dM[6 + k];
-            for (int i = 0; i < 3; ++i) dR[3 * i + k] = dM[3 * i + k] * s[k];
-            GW(off.ls + 3 * g + k, ds * s[k]);
-        }
-        const float dqw = 2.f * (-z * dR[1] + y * dR[2] + z * dR[3] - x * dR[5] - y * dR[6] + x * dR[7]);
-        const float dqx = 2.f * (y * dR[1] + z * dR[2] + y * dR[3] - 2.f * x * dR[4] - w * dR[5] + z * dR[6] +
-                                 w * dR[7] - 2.f * x * dR[8]);
-        const float dqy = 2.f * (-2.f * y * dR[0] + x * dR[1] + w * dR[2] + x * dR[3] + z * dR[5] - w * dR[6] +
-                                 z * dR[7] - 2.f * y * dR[8]);
-        const float dqz = 2.f * (-2.f * z * dR[0] - w * dR[1] + x * dR[2] + w * dR[3] - 2.f * z * dR[4] +
-                                 y * dR[5] + x * dR[6] + y * dR[7]);
-        const float dot = w * dqw + x * dqx + y * dqy + z * dqz;
-        GW(off.q + 4 * g, (dqw - w * dot) * iqn);
-        GW(off.q + 4 * g + 1, (dqx - x * dot) * iqn);
-        GW(off.q + 4 * g + 2, (dqy - y * dot) * iqn);
-        GW(off.q + 4 * g + 3, (dqz - z * dot) * iqn);
-        // ---- densification statistics ----
-        accum[g] = smem[L::kAc + sh[6] + tid] + sqrtf(dmx * dmx + dmy * dmy);
+        accum[g] = smem[L::kAc + sh[6] + tid] + nrm;
         vcount[g] = smem[L::kVc + sh[7] + tid] + 1.f;
         vis[g] = 1;
     }
-#undef GW
     if constexpr (!ACCUM && nrest > 0) {
         // overwrite mode: rows of inactive Gaussians and inactive SH degrees carry zeros
-        if (int(threadIdx.x) < rows) {
-            float* row = smem + L::kRest + sh[8] + threadIdx.x * 45;
+        if (tid < rows) {
             if (!active) {
-                for (int k = 0; k < 45; ++k) row[k] = 0.f;
+                for (int k = 0; k < 45; ++k) rest_row[k] = 0.f;
             } else {
-                for (int k = nrest; k < 45; ++k) row[k] = 0.f;
+                for (int k = nrest; k < 45; ++k) rest_row[k] = 0.f;
             }
         }
     }
     __syncthreads();
     if constexpr (nrest > 0) {
-        store_span<kBlock>(G + off.rest + g0 * 45,
-                           (ACCUM ? smem + L::kGRest + sh[9] : smem + L::kRest + sh[8]), rows * 45);
+        store_span<kBlock>(G + off.rest + g0 * 45, (ACCUM ? smem + L::kGRest + sh[9] : smem + L::kRest + sh[8]),
+                           rows * 45);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// fused backward + Adam kernel
+// ---------------------------------------------------------------------------
+constexpr int kFB = 64;  // Gaussians per CTA
+
+struct FusedAdam {
+    float lr[6];  // lr / (1 - b1^t), per group (host double -> float)
+    float b1, b2, omb1, omb2, eps, rsb2;
+};
+
+// fused Adam element (same op sequence as k_optim_loss.cu adam_one<true>)
+__device__ __forceinline__ void adam_fused_elem(float& th, float g, float& m, float& v, float lr, const FusedAdam& a) {
+    using namespace tsx;
+    m = add(mul(a.b1, m), mul(a.omb1, g));
+    v = add(mul(a.b2, v), mul(mul(a.omb2, g), g));
+    const float den = add(mul(sqrt_(v), a.rsb2), a.eps);
+    th = sub(th, div(mul(lr, m), den));
+}
+
+// layout: 3 copies (theta, m, v) of the 6 attribute segments, then g2d, stats, SH-rest gradients
+struct FbLayout {
+    static constexpr int kCopy = 59 * kFB + 24;  // floats per (theta | m | v) copy: 6 segments + 4 pad each
+    static constexpr int kG2 = 3 * kCopy;
+    static constexpr int kAc = kG2 + 12 * kFB + 4;
+    static constexpr int kVc = kAc + kFB + 4;
+    static constexpr int kGRest = kVc + kFB + 4;
+    static constexpr int kTotal = kGRest + 45 * kFB;
+};
+
+template <int DEG, bool kSkipInvisible>
+__global__ void __launch_bounds__(kFB) project_bwd_adam_kernel(float* __restrict__ P, float* __restrict__ Mo,
+                                                               float* __restrict__ Vo, float4* __restrict__ g2d,
+                                                               const uint32_t* __restrict__ tcount,
+                                                               float* __restrict__ accum,
+                                                               float* __restrict__ vcount, uint8_t* __restrict__ vis,
+                                                               int64_t N, DevCam cam, ts_render_config cfg,
+                                                               FusedAdam fa) {
+    extern __shared__ __align__(16) float smem[];
+    using L = FbLayout;
+    constexpr int width[6] = {3, 3, 4, 1, 3, 45};
+    constexpr int segoff[6] = {0, 3 * kFB + 4, 6 * kFB + 8, 10 * kFB + 12, 11 * kFB + 16, 14 * kFB + 20};
+    constexpr int nrest = 3 * ((DEG + 1) * (DEG + 1) - 1);
+    const Off off(N);
+    const int64_t goff[6] = {off.means, off.ls, off.q, off.op, off.dc, off.rest};
+    const int64_t g0 = int64_t(blockIdx.x) * kFB;
+    const int64_t g = g0 + threadIdx.x;
+    const int rows = int(tmin<int64_t>(kFB, N - g0));
+    const bool active = g < N && tcount[g] != 0;
+    if (kSkipInvisible && !__syncthreads_or(active)) return;
+    int sh[21];
+    {
+        Span sp[21];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            const float* buf = c == 0 ? P : (c == 1 ? Mo : Vo);
+#pragma unroll
+            for (int s = 0; s < 6; ++s)
+                sp[6 * c + s] = Span{smem + c * L::kCopy + segoff[s], buf + goff[s] + width[s] * g0, width[s] * rows};
+        }
+        sp[18] = Span{smem + L::kG2, reinterpret_cast<const float*>(g2d + 3 * g0), 12 * rows};
+        sp[19] = Span{smem + L::kAc, accum + g0, rows};
+        sp[20] = Span{smem + L::kVc, vcount + g0, rows};
+        stage_spans<kFB>(sp, sh);
+    }
+    __syncthreads();
+    const int tid = threadIdx.x;
+#define TS_ROW(c, s) (smem + (c) * L::kCopy + segoff[s] + sh[6 * (c) + (s)] + width[s] * tid)
+    if (tid < rows) {
+        float gs[14];
+#pragma unroll
+        for (int k = 0; k < 14; ++k) gs[k] = 0.f;
+        float* grest = smem + L::kGRest + tid * 45;
+        if (active) {
+            const Rows rw{TS_ROW(0, 0), TS_ROW(0, 1), TS_ROW(0, 2), TS_ROW(0, 3)[0], TS_ROW(0, 4), TS_ROW(0, 5),
+                          smem + L::kG2 + sh[18] + 12 * tid};
+            const float nrm = pb_grads<DEG>(rw, grest, cam, cfg, gs);
+            reinterpret_cast<float4*>(g2d)[3 * g] = make_float4(0.f, 0.f, 0.f, 0.f);
+            reinterpret_cast<float4*>(g2d)[3 * g + 1] = make_float4(0.f, 0.f, 0.f, 0.f);
+            reinterpret_cast<float4*>(g2d)[3 * g + 2] = make_float4(0.f, 0.f, 0.f, 0.f);
+            accum[g] = smem[L::kAc + sh[19] + tid] + nrm;
+            vcount[g] = smem[L::kVc + sh[20] + tid] + 1.f;
+            vis[g] = 1;
+        }
+        if (active || !kSkipInvisible) {
+            // Adam on the whole 59-float row; inactive rows / inactive SH degrees see g = 0
+            int k = 0;
+#pragma unroll
+            for (int s = 0; s < 5; ++s) {
+                float* th = TS_ROW(0, s);
+                float* m = TS_ROW(1, s);
+                float* v = TS_ROW(2, s);
+#pragma unroll
+                for (int j = 0; j < width[s]; ++j, ++k) adam_fused_elem(th[j], gs[k], m[j], v[j], fa.lr[s], fa);
+            }
+            float* th = TS_ROW(0, 5);
+            float* m = TS_ROW(1, 5);
+            float* v = TS_ROW(2, 5);
+#pragma unroll 5
+            for (int j = 0; j < 45; ++j)
+                adam_fused_elem(th[j], (active && j < nrest) ? grest[j] : 0.f, m[j], v[j], fa.lr[5], fa);
+        }
+    }
+#undef TS_ROW
+    __syncthreads();
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        float* buf = c == 0 ? P : (c == 1 ? Mo : Vo);
+#pragma unroll
+        for (int s = 0; s < 6; ++s)
+            store_span<kFB>(buf + goff[s] + width[s] * g0, smem + c * L::kCopy + segoff[s] + sh[6 * c + s],
+                            width[s] * rows);
     }
 }
 
@@ -355,6 +528,39 @@ void launch_project_bwd(Context& c, const DevCam& cam, const ts_render_config& c
         default: TS_PB(3); break;
     }
 #undef TS_PB
+    TS_LAUNCHED(c);
+}
+
+void launch_project_bwd_adam(Context& c, const DevCam& cam, const ts_render_config& cfg, const ts_adam_config& a) {
+    if (c.N == 0) return;
+    FusedAdam fa;
+    for (int k = 0; k < 6; ++k) fa.lr[k] = float(double(a.lr[k]) / double(a.bc1));
+    fa.b1 = a.beta1;
+    fa.b2 = a.beta2;
+    fa.omb1 = 1.0f - a.beta1;
+    fa.omb2 = 1.0f - a.beta2;
+    fa.eps = a.eps;
+    fa.rsb2 = float(1.0 / std::sqrt(double(a.bc2)));
+    const int64_t blocks = (c.N + kFB - 1) / kFB;
+    constexpr int sm = FbLayout::kTotal * 4;
+    const bool skip = a.mode == 4;
+#define TS_FB(D)                                                                                          \
+    if (skip) {                                                                                           \
+        cudaFuncSetAttribute(project_bwd_adam_kernel<D, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm); \
+        project_bwd_adam_kernel<D, true><<<unsigned(blocks), kFB, sm, c.stream>>>(                        \
+            c.params.p, c.m.p, c.v.p, c.g2d.p, c.tcount.p, c.accum.p, c.vcount.p, c.vis.p, c.N, cam, cfg, fa); \
+    } else {                                                                                              \
+        cudaFuncSetAttribute(project_bwd_adam_kernel<D, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm); \
+        project_bwd_adam_kernel<D, false><<<unsigned(blocks), kFB, sm, c.stream>>>(                       \
+            c.params.p, c.m.p, c.v.p, c.g2d.p, c.tcount.p, c.accum.p, c.vcount.p, c.vis.p, c.N, cam, cfg, fa); \
+    }
+    switch (cfg.sh_degree) {
+        case 0: TS_FB(0); break;
+        case 1: TS_FB(1); break;
+        case 2: TS_FB(2); break;
+        default: TS_FB(3); break;
+    }
+#undef TS_FB
     TS_LAUNCHED(c);
 }
 

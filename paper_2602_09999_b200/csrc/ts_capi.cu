@@ -86,7 +86,6 @@ ts_status validation(Context& c, const char* msg) {
     return TS_ERR_VALIDATION;
 }
 
-ts_status oom(Context& c) { return TS_ERR_OOM; }
 
 void stage_begin(Context& c, int k) {
     if (!c.profiling) return;
@@ -285,9 +284,32 @@ ts_status run_backward(Context& c, const float* dLdC_hwc) {
     return last_launch(c, "backward");
 }
 
+ts_status run_backward_adam(Context& c, const float* dLdC_hwc, const ts_adam_config& a) {
+    if (!c.view_valid) return validation(c, "ts_backward_adam needs a preceding ts_forward");
+    if (a.mode != 3 && a.mode != 4) return validation(c, "fused backward Adam needs mode 3 or 4");
+    if (!(a.bc1 > 0.f) || !(a.bc2 > 0.f)) return validation(c, "bias corrections must be > 0 (step >= 1)");
+    if (!c.grads_zero) return validation(c, "fused backward Adam needs an empty gradient buffer (single view)");
+    if (dLdC_hwc) {
+        if (ts_status s = upload_image_chw(c, dLdC_hwc, c.dLdC.p); s != TS_OK) return s;
+    } else if (!c.loss_valid) {
+        return validation(c, "ts_backward_adam(NULL) needs a preceding ts_loss");
+    }
+    DevCam dc = make_devcam(c.cam);
+    stage_begin(c, 8);
+    launch_blend_bwd(c, dc, c.cfg);
+    stage_end(c, 8);
+    stage_begin(c, 9);
+    launch_project_bwd_adam(c, dc, c.cfg, a);
+    stage_end(c, 9);
+    CK(cudaMemsetAsync(c.vis.p, 0, size_t(std::max<int64_t>(c.N, 1)), c.stream));
+    c.view_valid = false;
+    c.loss_valid = false;
+    return last_launch(c, "backward_adam");
+}
+
 ts_status run_adam(Context& c, const ts_adam_config& a, int64_t begin, int64_t end) {
     if (!(a.bc1 > 0.f) || !(a.bc2 > 0.f)) return validation(c, "bias corrections must be > 0 (step >= 1)");
-    if (a.mode < 0 || a.mode > 2) return validation(c, "adam mode must be 0..2");
+    if (a.mode < 0 || a.mode > 2) return validation(c, "adam mode must be 0..2 (3/4 run inside the backward)");
     stage_begin(c, 10);
     launch_adam(c, a, begin, end);
     stage_end(c, 10);
@@ -487,6 +509,14 @@ ts_status ts_backward(ts_ctx* x, const float* dLdC_hwc) {
     return run_backward(c, dLdC_hwc);
 }
 
+ts_status ts_backward_adam(ts_ctx* x, const float* dLdC_hwc, const ts_adam_config* a) {
+    TS_CHECK_CTX(x);
+    Context& c = x->c;
+    if (!a) return validation(c, "adam config is NULL");
+    CK(cudaSetDevice(c.device));
+    return run_backward_adam(c, dLdC_hwc, *a);
+}
+
 ts_status ts_zero_grads(ts_ctx* x) {
     TS_CHECK_CTX(x);
     Context& c = x->c;
@@ -560,8 +590,12 @@ ts_status ts_train_step(ts_ctx* x, const ts_camera* cam, const ts_render_config*
     CK(cudaSetDevice(c.device));
     if (ts_status s = run_forward(c, *cam, *cfg); s != TS_OK) return s;
     if (ts_status s = run_loss(c, target_hwc, slot, nullptr); s != TS_OK) return s;
-    if (ts_status s = run_backward(c, nullptr); s != TS_OK) return s;
-    if (ts_status s = run_adam(c, *adam, 0, 59 * c.N); s != TS_OK) return s;
+    if (adam->mode >= 3) {
+        if (ts_status s = run_backward_adam(c, nullptr, *adam); s != TS_OK) return s;
+    } else {
+        if (ts_status s = run_backward(c, nullptr); s != TS_OK) return s;
+        if (ts_status s = run_adam(c, *adam, 0, 59 * c.N); s != TS_OK) return s;
+    }
     if (out_loss) {
         double acc[2];
         CK(cudaMemcpyAsync(acc, c.loss_acc.p, sizeof(acc), cudaMemcpyDeviceToHost, c.stream));

@@ -106,6 +106,7 @@ void launch_blend_fwd(Context& c, const DevCam& cam, const ts_render_config& cfg
 void launch_loss(Context& c, const float* target_chw);
 void launch_blend_bwd(Context& c, const DevCam& cam, const ts_render_config& cfg);
 void launch_project_bwd(Context& c, const DevCam& cam, const ts_render_config& cfg, bool accumulate);
+void launch_project_bwd_adam(Context& c, const DevCam& cam, const ts_render_config& cfg, const ts_adam_config& a);
 void launch_adam(Context& c, const ts_adam_config& a, int64_t begin, int64_t end);
 void launch_hwc_to_chw(Context& c, const float* hwc, float* chw, int P);
 void launch_chw_to_hwc(Context& c, const float* chw, float* hwc, int P);

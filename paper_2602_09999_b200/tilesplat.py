@@ -63,6 +63,7 @@ _SIGS = {
     "ts_adam_step": [_vp, _vp],
     "ts_adam_step_range": [_vp, _vp, _i64, _i64],
     "ts_train_step": [_vp, _vp, _vp, _vp, _i32, _vp, _vp],
+    "ts_backward_adam": [_vp, _vp, _vp],
     "ts_densify": [_vp, _f, _f, ctypes.c_uint64, _i64, _vp, _vp],
     "ts_opacity_reset": [_vp],
     "ts_set_state": [_vp, _vp, _vp, _vp, _vp, _vp],
@@ -203,6 +204,11 @@ class Engine:
         """backward: accumulates parameter gradients and densify stats."""
         d = None if dL_dC is None else _f32(dL_dC)
         self._check(self._L.ts_backward(self._h, _ptr(d)), "ts_backward")
+
+    def backward_adam(self, adam: AdamConfig, dL_dC: np.ndarray | None = None):
+        """fused_backward_update: backward + in-place Adam (modes 3/4)."""
+        d = None if dL_dC is None else _f32(dL_dC)
+        self._check(self._L.ts_backward_adam(self._h, _ptr(d), ctypes.byref(adam)), "ts_backward_adam")
 
     def zero_grads(self):
         self._check(self._L.ts_zero_grads(self._h), "ts_zero_grads")

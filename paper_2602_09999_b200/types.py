@@ -22,7 +22,7 @@ GROUP_WIDTH = (3, 3, 4, 1, 3, 45)
 BOUND_SQUARE, BOUND_RECT, BOUND_RECT_OPACITY = 0, 1, 2
 CULL_NONE, CULL_EXACT = 0, 1
 BACKWARD_PER_PIXEL, BACKWARD_PER_GAUSSIAN = 0, 1
-ADAM_REFERENCE, ADAM_FUSED, ADAM_SKIP_INVISIBLE = 0, 1, 2
+ADAM_REFERENCE, ADAM_FUSED, ADAM_SKIP_INVISIBLE, ADAM_FUSED_BACKWARD, ADAM_FUSED_BACKWARD_SKIP = 0, 1, 2, 3, 4
 
 
 class Camera(ctypes.Structure):

@@ -292,3 +292,26 @@ def test_cpp_host_driver():
     assert out.returncode == 0, out.stderr
     r = json.loads(out.stdout.strip().splitlines()[-1])
     assert r["loss_last"] < 0.8 * r["loss_first"]
+
+
+@pytest.mark.parametrize("mode", [T.ADAM_FUSED_BACKWARD, T.ADAM_FUSED_BACKWARD_SKIP])
+def test_fused_backward_adam_equals_separate(engine, mode):
+    """fused_backward_update: bitwise the end state of backward +
+    fused Adam (resp. skip-invisible Adam), including moments and statistics."""
+    n = 30_000
+    gt = scene.random_params(n, 0.02, 0.0, 31)
+    cam = scene.make_camera(320, 200)
+    cfg = T.RenderConfig.make(sh_degree=3)
+    engine.set_params(gt, n)
+    target, _, _ = engine.render(cam, cfg)
+    p0 = scene.perturb(gt, n, 31)
+    sep = T.ADAM_FUSED if mode == T.ADAM_FUSED_BACKWARD else T.ADAM_SKIP_INVISIBLE
+    outs = []
+    for m in (sep, mode):
+        engine.set_params(p0, n)
+        for step in (1, 2, 3):
+            engine.train_step(cam, cfg, T.AdamConfig.make(step=step, mode=m), target=target)
+        g, mm, vv, acc, vc = engine.get_state()
+        outs.append((engine.get_params(), mm, vv, acc, vc))
+    for a, b in zip(*outs):
+        assert np.array_equal(a.view(np.uint32), b.view(np.uint32))

@@ -1,5 +1,4 @@
-// K10 fused Adam, K7 training loss and
-// layout helpers.
+// K10 fused Adam and layout helpers.
 //
 // Adam: one linear float4 sweep over the flat 59*N buffer; per element a fixed
 // sequence of explicit round-to-nearest ops (reference = SPEC literal formula,
@@ -7,9 +6,6 @@
 // IEEE division per element), bitwise equal to the oracle's restatement.
 // Reads theta, g, m, v and writes theta, m, v (28 B/element, HBM-bound); with
 // zero_grads the gradient is cleared in the same pass (+4 B).
-//
-// Loss: 0.8 L1 + 0.2 (1 - SSIM), 11x11 Gaussian window (sigma 1.5), reflect
-// padding; analytic dL/dC via the transposed (fold) separable filter.
 #include <cmath>
 
 #include "ts_internal.cuh"
@@ -117,148 +113,6 @@ __global__ void opacity_reset_kernel(float* __restrict__ op, int64_t N, float lm
     if (g < N) op[g] = op[g] < lmax ? op[g] : lmax;
 }
 
-// ---------------------------------------------------------------------------
-// loss
-// ---------------------------------------------------------------------------
-__constant__ float c_gw[11];
-constexpr int kNPL = 11;  // temp planes per channel
-
-__device__ __forceinline__ int refl(int i, int n) { return i < 0 ? -i : (i >= n ? 2 * (n - 1) - i : i); }
-
-// horizontal pass: 5 window moments of x, y
-__global__ void loss_h_kernel(const float* __restrict__ X, const float* __restrict__ Y, float* __restrict__ tmp,
-                              int W, int H) {
-    const int P = W * H;
-    const int p = blockIdx.x * blockDim.x + threadIdx.x;
-    const int ch = blockIdx.y;
-    if (p >= P) return;
-    const int y = p / W, x = p - y * W;
-    const float* xr = X + ch * P + y * W;
-    const float* yr = Y + ch * P + y * W;
-    float sx = 0.f, sy = 0.f, sxx = 0.f, syy = 0.f, sxy = 0.f;
-#pragma unroll
-    for (int o = -5; o <= 5; ++o) {
-        const int j = refl(x + o, W);
-        const float a = xr[j], b = yr[j], w = c_gw[o + 5];
-        sx += w * a;
-        sy += w * b;
-        sxx += w * a * a;
-        syy += w * b * b;
-        sxy += w * a * b;
-    }
-    float* t = tmp + size_t(ch) * kNPL * P;
-    t[p] = sx;
-    t[P + p] = sy;
-    t[2 * P + p] = sxx;
-    t[3 * P + p] = syy;
-    t[4 * P + p] = sxy;
-}
-
-// vertical pass + SSIM map + partial derivatives + loss sums
-__global__ void loss_v_kernel(const float* __restrict__ X, const float* __restrict__ Y, float* __restrict__ tmp,
-                              int W, int H, double* __restrict__ acc) {
-    const int P = W * H;
-    const int p = blockIdx.x * blockDim.x + threadIdx.x;
-    const int ch = blockIdx.y;
-    float l1 = 0.f, ss = 0.f;
-    if (p < P) {
-        const int y = p / W, x = p - y * W;
-        float* t = tmp + size_t(ch) * kNPL * P;
-        float m[5] = {0.f, 0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-        for (int o = -5; o <= 5; ++o) {
-            const int r = refl(y + o, H) * W + x;
-            const float w = c_gw[o + 5];
-#pragma unroll
-            for (int k = 0; k < 5; ++k) m[k] += w * t[k * P + r];
-        }
-        const float C1 = 0.01f * 0.01f, C2 = 0.03f * 0.03f;
-        const float ux = m[0], uy = m[1];
-        const float vx = m[2] - ux * ux, vy = m[3] - uy * uy, cxy = m[4] - ux * uy;
-        const float n1 = 2.f * ux * uy + C1, n2 = 2.f * cxy + C2;
-        const float d1 = ux * ux + uy * uy + C1, d2 = vx + vy + C2;
-        const float iD = 1.f / (d1 * d2);
-        const float S = n1 * n2 * iD;
-        const float dS_dux = (2.f * uy * n2 - S * 2.f * ux * d2) * iD;
-        const float dS_dvx = -S / d2;
-        const float dS_dcxy = 2.f * n1 * iD;
-        t[5 * P + p] = dS_dux - 2.f * ux * dS_dvx - uy * dS_dcxy;
-        t[6 * P + p] = 2.f * dS_dvx;
-        t[7 * P + p] = dS_dcxy;
-        ss = S;
-        l1 = fabsf(X[ch * P + p] - Y[ch * P + p]);
-    }
-    // block reduction -> double atomics
-    __shared__ float r1[32], r2[32];
-    for (int o = 16; o > 0; o >>= 1) {
-        l1 += __shfl_xor_sync(0xffffffffu, l1, o);
-        ss += __shfl_xor_sync(0xffffffffu, ss, o);
-    }
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    if (lane == 0) {
-        r1[wid] = l1;
-        r2[wid] = ss;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        double a = 0, b = 0;
-        for (int w = 0; w < int(blockDim.x >> 5); ++w) {
-            a += r1[w];
-            b += r2[w];
-        }
-        atomicAdd(acc, a);
-        atomicAdd(acc + 1, b);
-    }
-}
-
-// transposed filter along one axis: z(j) = sum_o g f(j - o) (f zero outside),
-// folded back through the reflect padding
-template <bool kVertical>
-__device__ __forceinline__ float zfold(const float* f, int x, int y, int W, int H, int pos, int n) {
-    auto zval = [&](int j) {
-        float s = 0.f;
-#pragma unroll
-        for (int o = -5; o <= 5; ++o) {
-            const int k = j - o;
-            if (k >= 0 && k < n) s += c_gw[o + 5] * (kVertical ? f[k * W + x] : f[y * W + k]);
-        }
-        return s;
-    };
-    float r = zval(pos);
-    if (pos >= 1 && pos <= 5) r += zval(-pos);
-    if (pos >= n - 6 && pos <= n - 2) r += zval(2 * (n - 1) - pos);
-    return r;
-}
-
-__global__ void loss_ht_kernel(float* __restrict__ tmp, int W, int H) {
-    const int P = W * H;
-    const int p = blockIdx.x * blockDim.x + threadIdx.x;
-    const int ch = blockIdx.y;
-    if (p >= P) return;
-    const int y = p / W, x = p - y * W;
-    float* t = tmp + size_t(ch) * kNPL * P;
-#pragma unroll
-    for (int k = 0; k < 3; ++k) t[(8 + k) * P + p] = zfold<false>(t + (5 + k) * P, x, y, W, H, x, W);
-}
-
-__global__ void loss_vt_kernel(const float* __restrict__ X, const float* __restrict__ Y, const float* __restrict__ tmp,
-                               float* __restrict__ dL, int W, int H, float inv_m) {
-    const int P = W * H;
-    const int p = blockIdx.x * blockDim.x + threadIdx.x;
-    const int ch = blockIdx.y;
-    if (p >= P) return;
-    const int y = p / W, x = p - y * W;
-    const float* t = tmp + size_t(ch) * kNPL * P;
-    const float ta = zfold<true>(t + 8 * P, x, y, W, H, y, H);
-    const float tb = zfold<true>(t + 9 * P, x, y, W, H, y, H);
-    const float tc = zfold<true>(t + 10 * P, x, y, W, H, y, H);
-    const float xv = X[ch * P + p], yv = Y[ch * P + p];
-    const float dS = ta + xv * tb + yv * tc;
-    const float d = xv - yv;
-    const float sg = d > 0.f ? 1.f : (d < 0.f ? -1.f : 0.f);
-    dL[ch * P + p] = (0.8f * sg - 0.2f * dS) * inv_m;
-}
-
 }  // namespace
 
 void launch_adam(Context& c, const ts_adam_config& a, int64_t begin, int64_t end) {
@@ -314,31 +168,6 @@ void launch_opacity_reset(Context& c, float lmax) {
     if (c.N == 0) return;
     opacity_reset_kernel<<<unsigned((c.N + 255) / 256), 256, 0, c.stream>>>(c.params.p + 10 * c.N, c.N, lmax);
     TS_LAUNCHED(c);
-}
-
-void launch_loss(Context& c, const float* target_chw) {
-    static bool init = false;
-    if (!init) {
-        double g[11], s = 0;
-        for (int i = 0; i < 11; ++i) {
-            const double d = i - 5;
-            g[i] = std::exp(-(d * d) / (2.0 * 1.5 * 1.5));
-            s += g[i];
-        }
-        float gf[11];
-        for (int i = 0; i < 11; ++i) gf[i] = float(g[i] / s);
-        cudaMemcpyToSymbol(c_gw, gf, sizeof(gf));
-        init = true;
-    }
-    const int W = c.fw, H = c.fh, P = W * H;
-    cudaMemsetAsync(c.loss_acc.p, 0, 2 * sizeof(double), c.stream);
-    const dim3 grid((P + 255) / 256, 3);
-    loss_h_kernel<<<grid, 256, 0, c.stream>>>(c.rgb.p, target_chw, c.loss_tmp.p, W, H);
-    loss_v_kernel<<<grid, 256, 0, c.stream>>>(c.rgb.p, target_chw, c.loss_tmp.p, W, H, c.loss_acc.p);
-    loss_ht_kernel<<<grid, 256, 0, c.stream>>>(c.loss_tmp.p, W, H);
-    loss_vt_kernel<<<grid, 256, 0, c.stream>>>(c.rgb.p, target_chw, c.loss_tmp.p, c.dLdC.p, W, H,
-                                               float(1.0 / (3.0 * double(P))));
-    c.launches += 4;
 }
 
 }  // namespace ts

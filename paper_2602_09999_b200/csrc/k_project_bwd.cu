@@ -299,7 +299,7 @@ __global__ void __launch_bounds__(kBlock) project_bwd_kernel(const float* __rest
                                                              const uint32_t* __restrict__ tcount,
                                                              float* __restrict__ accum, float* __restrict__ vcount,
                                                              uint8_t* __restrict__ vis, int64_t N, DevCam cam,
-                                                             ts_render_config cfg) {
+                                                             ts_render_config cfg, int zero_inactive) {
     extern __shared__ __align__(16) float smem[];
     using L = PbLayout<DEG, ACCUM>;
     constexpr int nrest = 3 * ((DEG + 1) * (DEG + 1) - 1);
@@ -308,7 +308,8 @@ __global__ void __launch_bounds__(kBlock) project_bwd_kernel(const float* __rest
     const int64_t g = g0 + threadIdx.x;
     const int rows = int(tmin<int64_t>(kBlock, N - g0));
     const bool active = g < N && tcount[g] != 0;
-    if (!__syncthreads_or(active)) return;
+    // a stale (consumed, uncleared) buffer needs zeros on inactive rows too
+    if (!__syncthreads_or(active || (zero_inactive && g < N))) return;
     int sh[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
     {
         const Span base[8] = {{smem + L::kMu, P + off.means + 3 * g0, 3 * rows},
@@ -372,6 +373,16 @@ __global__ void __launch_bounds__(kBlock) project_bwd_kernel(const float* __rest
         accum[g] = smem[L::kAc + sh[6] + tid] + nrm;
         vcount[g] = smem[L::kVc + sh[7] + tid] + 1.f;
         vis[g] = 1;
+    } else if (!ACCUM && zero_inactive && g < N) {
+        const int64_t idx[14] = {off.means + 3 * g,  off.means + 3 * g + 1, off.means + 3 * g + 2, off.ls + 3 * g,
+                                 off.ls + 3 * g + 1, off.ls + 3 * g + 2,    off.q + 4 * g,         off.q + 4 * g + 1,
+                                 off.q + 4 * g + 2,  off.q + 4 * g + 3,     off.op + g,            off.dc + 3 * g,
+                                 off.dc + 3 * g + 1, off.dc + 3 * g + 2};
+#pragma unroll
+        for (int k = 0; k < 14; ++k) G[idx[k]] = 0.f;
+        if constexpr (nrest == 0) {
+            for (int k = 0; k < 45; ++k) G[off.rest + 45 * g + k] = 0.f;
+        }
     }
     if constexpr (!ACCUM && nrest > 0) {
         // overwrite mode: rows of inactive Gaussians and inactive SH degrees carry zeros
@@ -506,7 +517,8 @@ __global__ void __launch_bounds__(kFB) project_bwd_adam_kernel(float* __restrict
 
 }  // namespace
 
-void launch_project_bwd(Context& c, const DevCam& cam, const ts_render_config& cfg, bool accumulate) {
+void launch_project_bwd(Context& c, const DevCam& cam, const ts_render_config& cfg, bool accumulate,
+                        bool zero_inactive) {
     if (c.N == 0) return;
     const int64_t blocks = (c.N + kBlock - 1) / kBlock;
 #define TS_PB(D)                                                                                      \
@@ -514,12 +526,13 @@ void launch_project_bwd(Context& c, const DevCam& cam, const ts_render_config& c
         constexpr int sm = PbLayout<D, true>::kTotal * 4;                                             \
         cudaFuncSetAttribute(project_bwd_kernel<D, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm); \
         project_bwd_kernel<D, true><<<unsigned(blocks), kBlock, sm, c.stream>>>(                      \
-            c.params.p, c.grads.p, c.g2d.p, c.tcount.p, c.accum.p, c.vcount.p, c.vis.p, c.N, cam, cfg); \
+            c.params.p, c.grads.p, c.g2d.p, c.tcount.p, c.accum.p, c.vcount.p, c.vis.p, c.N, cam, cfg, 0); \
     } else {                                                                                          \
         constexpr int sm = PbLayout<D, false>::kTotal * 4;                                            \
         cudaFuncSetAttribute(project_bwd_kernel<D, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm); \
         project_bwd_kernel<D, false><<<unsigned(blocks), kBlock, sm, c.stream>>>(                     \
-            c.params.p, c.grads.p, c.g2d.p, c.tcount.p, c.accum.p, c.vcount.p, c.vis.p, c.N, cam, cfg); \
+            c.params.p, c.grads.p, c.g2d.p, c.tcount.p, c.accum.p, c.vcount.p, c.vis.p, c.N, cam, cfg,   \
+            int(zero_inactive));                                                                       \
     }
     switch (cfg.sh_degree) {
         case 0: TS_PB(0); break;

@@ -250,7 +250,7 @@ ts_status run_loss(Context& c, const float* target_hwc, int32_t slot, float* out
         if (c.target_w != c.fw || c.target_h != c.fh) return validation(c, "target slot size != view size");
         tgt = c.targets.p + size_t(slot) * 3 * P;
     }
-    if (!ensure(c, c.loss_tmp, 3 * 11 * P)) return TS_ERR_OOM;
+    if (!ensure(c, c.loss_tmp, 3 * 3 * P)) return TS_ERR_OOM;
     stage_begin(c, 7);
     launch_loss(c, tgt);
     stage_end(c, 7);
@@ -278,8 +278,8 @@ ts_status run_backward(Context& c, const float* dLdC_hwc) {
     launch_blend_bwd(c, dc, c.cfg);
     stage_end(c, 8);
     stage_begin(c, 9);
-    launch_project_bwd(c, dc, c.cfg, !c.grads_zero);
-    c.grads_zero = false;
+    launch_project_bwd(c, dc, c.cfg, c.grad_state == Context::kGradLive, c.grad_state == Context::kGradStale);
+    c.grad_state = Context::kGradLive;
     stage_end(c, 9);
     return last_launch(c, "backward");
 }
@@ -288,7 +288,8 @@ ts_status run_backward_adam(Context& c, const float* dLdC_hwc, const ts_adam_con
     if (!c.view_valid) return validation(c, "ts_backward_adam needs a preceding ts_forward");
     if (a.mode != 3 && a.mode != 4) return validation(c, "fused backward Adam needs mode 3 or 4");
     if (!(a.bc1 > 0.f) || !(a.bc2 > 0.f)) return validation(c, "bias corrections must be > 0 (step >= 1)");
-    if (!c.grads_zero) return validation(c, "fused backward Adam needs an empty gradient buffer (single view)");
+    if (c.grad_state == Context::kGradLive)
+        return validation(c, "fused backward Adam needs a consumed gradient buffer (single-view step)");
     if (dLdC_hwc) {
         if (ts_status s = upload_image_chw(c, dLdC_hwc, c.dLdC.p); s != TS_OK) return s;
     } else if (!c.loss_valid) {
@@ -314,7 +315,7 @@ ts_status run_adam(Context& c, const ts_adam_config& a, int64_t begin, int64_t e
     launch_adam(c, a, begin, end);
     stage_end(c, 10);
     CK(cudaMemsetAsync(c.vis.p, 0, size_t(std::max<int64_t>(c.N, 1)), c.stream));
-    if (a.zero_grads && begin == 0 && end == 59 * c.N) c.grads_zero = true;
+    if (begin == 0 && end == 59 * c.N) c.grad_state = a.zero_grads ? Context::kGradZero : Context::kGradStale;
     c.view_valid = false;
     c.loss_valid = false;
     return last_launch(c, "adam");
@@ -414,7 +415,7 @@ ts_status ts_set_params_flat(ts_ctx* x, int64_t n, const float* flat) {
     c.N = n;
     if (n) CK(cudaMemcpyAsync(c.params.p, flat, size_t(59) * n * 4, cudaMemcpyHostToDevice, c.stream));
     if (ts_status s = zero_state(c); s != TS_OK) return s;
-    c.grads_zero = true;
+    c.grad_state = Context::kGradZero;
     c.view_valid = c.loss_valid = false;
     CK(cudaStreamSynchronize(c.stream));
     return TS_OK;
@@ -522,7 +523,7 @@ ts_status ts_zero_grads(ts_ctx* x) {
     Context& c = x->c;
     CK(cudaSetDevice(c.device));
     if (c.N) CK(cudaMemsetAsync(c.grads.p, 0, size_t(59) * c.N * 4, c.stream));
-    c.grads_zero = true;
+    c.grad_state = Context::kGradZero;
     return TS_OK;
 }
 
@@ -594,7 +595,11 @@ ts_status ts_train_step(ts_ctx* x, const ts_camera* cam, const ts_render_config*
         if (ts_status s = run_backward_adam(c, nullptr, *adam); s != TS_OK) return s;
     } else {
         if (ts_status s = run_backward(c, nullptr); s != TS_OK) return s;
-        if (ts_status s = run_adam(c, *adam, 0, 59 * c.N); s != TS_OK) return s;
+        // the gradient buffer is internal to the step: skip the clear (the next
+        // backward overwrites every row); ts_get_state then shows this step's gradient
+        ts_adam_config a = *adam;
+        a.zero_grads = 0;
+        if (ts_status s = run_adam(c, a, 0, 59 * c.N); s != TS_OK) return s;
     }
     if (out_loss) {
         double acc[2];
@@ -628,7 +633,7 @@ ts_status ts_densify(ts_ctx* x, float grad_thresh, float extent, uint64_t seed, 
     const int64_t na = launch_densify(c, grad_thresh, log_small, log_big, logit_min, seed, iter, st);
     if (na < 0) return c.err.empty() ? TS_ERR_CUDA : TS_ERR_OOM;
     if (n_after) *n_after = na;
-    c.grads_zero = true;
+    c.grad_state = Context::kGradZero;
     if (stats) std::memcpy(stats, st, sizeof(st));
     c.view_valid = c.loss_valid = false;
     return last_launch(c, "densify");
@@ -642,7 +647,7 @@ ts_status ts_set_state(ts_ctx* x, const float* grads, const float* m, const floa
     const size_t L = size_t(59) * c.N, N = size_t(c.N);
     if (grads) {
         CK(cudaMemcpyAsync(c.grads.p, grads, L * 4, cudaMemcpyHostToDevice, c.stream));
-        c.grads_zero = false;
+        c.grad_state = Context::kGradLive;
     }
     if (m) CK(cudaMemcpyAsync(c.m.p, m, L * 4, cudaMemcpyHostToDevice, c.stream));
     if (v) CK(cudaMemcpyAsync(c.v.p, v, L * 4, cudaMemcpyHostToDevice, c.stream));

@@ -48,7 +48,10 @@ struct Context {
     int64_t N = 0;
     DevBuf<float> params, grads, m, v, accum, vcount;
     int64_t step = 0;
-    bool grads_zero = true;  // gradient buffer known to be all zero (backward may overwrite)
+    // gradient buffer state: ZERO (all zero), STALE (consumed by the optimizer, not
+    // cleared: the next backward overwrites every row), LIVE (holds gradients of
+    // >= 1 view not yet consumed: the next backward accumulates)
+    enum GradState { kGradZero, kGradStale, kGradLive } grad_state = kGradZero;
 
     // per-view (sized by N)
     DevBuf<float4> splat;        // 3 float4 per Gaussian: (mx,my,k2,o) (A,B,C,depth) (r,g,b,det)
@@ -74,7 +77,7 @@ struct Context {
     DevBuf<float> rgb, Tfin, dLdC, hwc_stage, tgt;
     DevBuf<uint32_t> pcount;
     DevBuf<double> loss_acc;     // [0] L1 sum, [1] SSIM sum
-    DevBuf<float> loss_tmp;      // 13 planes of P for the SSIM passes
+    DevBuf<float> loss_tmp;      // 3 channels x 3 SSIM partial-derivative maps (P each)
     DevBuf<float> targets;       // target slots, CHW planar
     int n_target_slots = 0, target_w = 0, target_h = 0;
 
@@ -105,7 +108,8 @@ void launch_ranges(Context& c, int n_tiles);
 void launch_blend_fwd(Context& c, const DevCam& cam, const ts_render_config& cfg);
 void launch_loss(Context& c, const float* target_chw);
 void launch_blend_bwd(Context& c, const DevCam& cam, const ts_render_config& cfg);
-void launch_project_bwd(Context& c, const DevCam& cam, const ts_render_config& cfg, bool accumulate);
+void launch_project_bwd(Context& c, const DevCam& cam, const ts_render_config& cfg, bool accumulate,
+                        bool zero_inactive);
 void launch_project_bwd_adam(Context& c, const DevCam& cam, const ts_render_config& cfg, const ts_adam_config& a);
 void launch_adam(Context& c, const ts_adam_config& a, int64_t begin, int64_t end);
 void launch_hwc_to_chw(Context& c, const float* hwc, float* chw, int P);

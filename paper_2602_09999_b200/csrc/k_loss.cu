@@ -5,9 +5,9 @@
 //   loss_fwd: stage the reflect-padded 26x26 patch of rendered and target
 //     colour, separable 11-tap filtering of the 5 window moments, SSIM map and
 //     its partial derivatives (a, b, c below), block-reduced L1 / SSIM sums;
-//   loss_bwd: the transposed filter of (a, b, c) -- separable 11-tap
-//     correlation of the zero-extended maps with the reflect-padding fold
-//     applied per axis in shared memory (41x41 patch) -- and
+//   loss_bwd: the transposed filter of (a, b, c) -- the same separable 11-tap
+//     correlation on the zero-extended maps, plus, for pixels within 5 of the
+//     image border, the terms folded back through the reflect padding -- and
 //     dL/dC = (0.8 sign(x-y) - 0.2 (W^T a + x W^T b + y W^T c)) / M.
 // With  mu = W x,  v = W x^2 - mu_x^2,  cov = W xy - mu_x mu_y  (per pixel):
 //   dSSIM/dx_p = (W^T a)_p + x_p (W^T b)_p + y_p (W^T c)_p,
@@ -108,68 +108,79 @@ __global__ void __launch_bounds__(kT * kT) loss_fwd_kernel(const float* __restri
     }
 }
 
-// Transposed filter with the reflect fold done in shared memory.  Along one
-// axis (n samples), W^T f = fold(z) with z[j] = sum_o g[o] f[j+o] over the
-// zero-extended f (j in [-5, n+4]) and fold(z)[p] = z[p] + z[-p] (1 <= p <= 5)
-// + z[2(n-1)-p] (n-6 <= p <= n-2).  A tile covering [t0, t0+16) needs z over
-// [t0-5, t0+26) (so the mirrors of fold targets in this tile are available even
-// when the last tile is narrow), i.e. f over [t0-10, t0+31): a 41x41 patch.
-constexpr int kE = kT + 25;  // 41: zero-extended patch of the maps
+// sum over the 11x11 window of the zero-extended map f around (jx, jy)
+__device__ __forceinline__ float window_sum(const float* __restrict__ f, int jx, int jy, int W, int H) {
+    float s = 0.f;
+    for (int oy = -5; oy <= 5; ++oy) {
+        const int yy = jy + oy;
+        if (yy < 0 || yy >= H) continue;
+        float r = 0.f;
+#pragma unroll
+        for (int ox = -5; ox <= 5; ++ox) {
+            const int xx = jx + ox;
+            if (xx >= 0 && xx < W) r = fmaf(c_gw[ox + 5], __ldg(f + yy * W + xx), r);
+        }
+        s = fmaf(c_gw[oy + 5], r, s);
+    }
+    return s;
+}
 
 __global__ void __launch_bounds__(kT * kT) loss_bwd_kernel(const float* __restrict__ X, const float* __restrict__ Y,
                                                            const float* __restrict__ maps, float* __restrict__ dL,
                                                            int W, int H, float inv_m) {
-    __shared__ float sf[3][kE][kE];        // f over rows/cols [t0-10, t0+31), zero outside the image
-    __shared__ float su[3][kE][kT + 1];    // x-transposed (with x fold) for all 41 rows, tile columns
+    __shared__ float sf[3][kP][kPS];
+    __shared__ float hm[3][kP][kT];
     const int ch = blockIdx.z, P = W * H;
     const int x0 = blockIdx.x * kT, y0 = blockIdx.y * kT;
     const int tid = threadIdx.y * kT + threadIdx.x;
     const float* mp = maps + size_t(ch) * 3 * P;
-    for (int i = tid; i < kE * kE; i += kT * kT) {
-        const int r = i / kE, c = i - r * kE;
-        const int gy = y0 - 10 + r, gx = x0 - 10 + c;
+    for (int i = tid; i < kP * kP; i += kT * kT) {
+        const int r = i / kP, c = i - r * kP;
+        const int gy = y0 - 5 + r, gx = x0 - 5 + c;
         const bool in = gy >= 0 && gy < H && gx >= 0 && gx < W;
         const int gi = gy * W + gx;
 #pragma unroll
         for (int q = 0; q < 3; ++q) sf[q][r][c] = in ? __ldg(mp + q * P + gi) : 0.f;
     }
     __syncthreads();
-    // x pass: for each of the 41 rows and 3 maps, u[row][p] = fold(z)[p] for the 16 tile columns.
-    // Work item = (map, row, column): z at the needed positions is computed on the fly.
-    for (int i = tid; i < 3 * kE * kT; i += kT * kT) {
-        const int q = i / (kE * kT), rem = i - q * kE * kT, r = rem / kT, c = rem - (rem / kT) * kT;
-        const int p = x0 + c;
-        const float* row = sf[q][r];
-        auto zat = [&](int j) {  // z at global column j in [x0-5, x0+26): taps j-5..j+5 -> patch cols j-x0+5 .. +15
-            float s = 0.f;
-            const int b = j - x0 + 5;
+    for (int i = tid; i < kP * kT; i += kT * kT) {
+        const int r = i / kT, c = i - r * kT;
+        float a = 0.f, b = 0.f, d = 0.f;
 #pragma unroll
-            for (int k = 0; k < 11; ++k) s = fmaf(c_gw[k], row[b + k], s);
-            return s;
-        };
-        float u = zat(p);
-        if (p >= 1 && p <= 5) u += zat(-p);
-        if (p >= W - 6 && p <= W - 2) u += zat(2 * (W - 1) - p);
-        su[q][r][c] = u;
+        for (int k = 0; k < 11; ++k) {
+            const float w = c_gw[k];
+            a = fmaf(w, sf[0][r][c + k], a);
+            b = fmaf(w, sf[1][r][c + k], b);
+            d = fmaf(w, sf[2][r][c + k], d);
+        }
+        hm[0][r][c] = a, hm[1][r][c] = b, hm[2][r][c] = d;
     }
     __syncthreads();
     const int tx = threadIdx.x, ty = threadIdx.y;
     const int x = x0 + tx, y = y0 + ty;
     if (x >= W || y >= H) return;
-    float t[3];
+    float t[3] = {0.f, 0.f, 0.f};
 #pragma unroll
-    for (int q = 0; q < 3; ++q) {
-        auto zat = [&](int j) {  // z along y at global row j: u rows j-5..j+5 -> patch rows j-y0+5 .. +15
-            float s = 0.f;
-            const int b = j - y0 + 5;
+    for (int k = 0; k < 11; ++k) {
+        const float w = c_gw[k];
 #pragma unroll
-            for (int k = 0; k < 11; ++k) s = fmaf(c_gw[k], su[q][b + k][tx], s);
-            return s;
-        };
-        float v = zat(y);
-        if (y >= 1 && y <= 5) v += zat(-y);
-        if (y >= H - 6 && y <= H - 2) v += zat(2 * (H - 1) - y);
-        t[q] = v;
+        for (int q = 0; q < 3; ++q) t[q] = fmaf(w, hm[q][ty + k][tx], t[q]);
+    }
+    // reflect-padding fold terms (pixels within 5 of a border)
+    if (x <= 5 || x >= W - 6 || y <= 5 || y >= H - 6) {
+        int jx[3], jy[3], nx = 0, ny = 0;
+        jx[nx++] = x;
+        if (x >= 1 && x <= 5) jx[nx++] = -x;
+        if (x >= W - 6 && x <= W - 2) jx[nx++] = 2 * (W - 1) - x;
+        jy[ny++] = y;
+        if (y >= 1 && y <= 5) jy[ny++] = -y;
+        if (y >= H - 6 && y <= H - 2) jy[ny++] = 2 * (H - 1) - y;
+        for (int a = 0; a < nx; ++a)
+            for (int b = 0; b < ny; ++b) {
+                if (a == 0 && b == 0) continue;
+#pragma unroll
+                for (int q = 0; q < 3; ++q) t[q] += window_sum(mp + q * P, jx[a], jy[b], W, H);
+            }
     }
     const int p = y * W + x;
     const float xv = X[size_t(ch) * P + p], yv = Y[size_t(ch) * P + p];

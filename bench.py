@@ -222,7 +222,9 @@ def run_ours(args):
     step = 0
 
     def adam_cfg():
-        return T.AdamConfig.make(step=step, extent=1.0)
+        # the gradient buffer is consumed by this step's optimizer; the next backward
+        # overwrites every row (no clear pass).  Sharded mode clears explicitly.
+        return T.AdamConfig.make(step=step, extent=1.0, zero_grads=0 if args.dp_mode == "allreduce" else 1)
 
     for _ in range(args.warmup):
         step += 1

@@ -90,15 +90,23 @@ __global__ void __launch_bounds__(kT) blend_fwd_kernel(const uint32_t* __restric
                 if (a.y + q.w < wy0 || a.y - q.w > wy1) continue;  // splat misses this warp's 8 rows
                 const float dx = tsx::sub(fpx, a.x);
                 const float adx = tsx::mul(q.x, dx);
+                // keep mask of the 4 pixels first (exact Q, branch-free), heavy path only on set bits
+                float Qv[kPPT];
+                uint32_t km = 0;
 #pragma unroll
                 for (int k = 0; k < kPPT; ++k) {
-                    if (done & (1u << k)) continue;
                     const float dy = tsx::sub(float(py0 + k), a.y);
                     // Q = dx*(A*dx + 2B*dy) + dy*(C*dy), exact order (tsx::conic_q)
-                    const float Q = tsx::add(tsx::mul(dx, tsx::add(adx, tsx::mul(q.y, dy))),
-                                             tsx::mul(dy, tsx::mul(q.z, dy)));
-                    if (!(Q <= a.z)) continue;
-                    const float G = tsx::ex2_approx(Q * kNegHalfLog2e);
+                    Qv[k] = tsx::add(tsx::mul(dx, tsx::add(adx, tsx::mul(q.y, dy))), tsx::mul(dy, tsx::mul(q.z, dy)));
+                    km |= (Qv[k] <= a.z) ? (1u << k) : 0u;
+                }
+                km &= ~done;
+                if (!km) continue;
+                const float4 col = sC[j];
+#pragma unroll
+                for (int k = 0; k < kPPT; ++k) {
+                    if (!(km & (1u << k))) continue;
+                    const float G = tsx::ex2_approx(Qv[k] * kNegHalfLog2e);
                     const float al = fminf(0.99f, a.w * G);
                     const float om = 1.f - al;
                     if (kCompat && T[k] * om < 1e-4f) {
@@ -106,7 +114,6 @@ __global__ void __launch_bounds__(kT) blend_fwd_kernel(const uint32_t* __restric
                         continue;
                     }
                     const float w = al * T[k];
-                    const float4 col = sC[j];
                     C0[k] = fmaf(w, col.x, C0[k]);
                     C1[k] = fmaf(w, col.y, C1[k]);
                     C2[k] = fmaf(w, col.z, C2[k]);
@@ -276,23 +283,29 @@ __global__ void __launch_bounds__(kT) blend_bwd_kernel(const uint32_t* __restric
             if (a.y + q.w < wy0 || a.y - q.w > wy1) continue;  // warp-uniform row cull
             const float dx = tsx::sub(fpx, a.x);
             const float adx = tsx::mul(q.x, dx);
+            const uint32_t li = local0 + uint32_t(j);
+            // keep mask of the 4 pixels first (exact Q); the warp skips the fragment if no lane keeps it
+            float Qv[kPPT], b2dy[kPPT], cdy[kPPT];
+            uint32_t km = 0;
+#pragma unroll
+            for (int k = 0; k < kPPT; ++k) {
+                const float dy = tsx::sub(float(py0 + k), a.y);
+                b2dy[k] = tsx::mul(q.y, dy);
+                cdy[k] = tsx::mul(q.z, dy);
+                Qv[k] = tsx::add(tsx::mul(dx, tsx::add(adx, b2dy[k])), tsx::mul(dy, cdy[k]));
+                km |= (li < cnt[k] && Qv[k] <= a.z) ? (1u << k) : 0u;
+            }
+            if (!__any_sync(0xffffffffu, km)) continue;
             const float b2dx = q.y * dx;
             const float4 col = sC[j];
             float v[9];
 #pragma unroll
             for (int k = 0; k < 9; ++k) v[k] = 0.f;
-            bool any = false;
-            const uint32_t li = local0 + uint32_t(j);
 #pragma unroll
             for (int k = 0; k < kPPT; ++k) {
-                if (li >= cnt[k]) continue;
-                const float dy = tsx::sub(float(py0 + k), a.y);
-                const float b2dy = tsx::mul(q.y, dy);
-                const float cdy = tsx::mul(q.z, dy);
-                const float Q = tsx::add(tsx::mul(dx, tsx::add(adx, b2dy)), tsx::mul(dy, cdy));
-                if (!(Q <= a.z)) continue;
-                any = true;
-                const float G = tsx::ex2_approx(Q * kNegHalfLog2e);
+                if (!(km & (1u << k))) continue;
+                const float dy = float(py0 + k) - a.y;
+                const float G = tsx::ex2_approx(Qv[k] * kNegHalfLog2e);
                 const float og = a.w * G;
                 const bool clamped = og > 0.99f;
                 const float al = clamped ? 0.99f : og;
@@ -307,8 +320,8 @@ __global__ void __launch_bounds__(kT) blend_bwd_kernel(const uint32_t* __restric
                 if (!clamped) {
                     v[5] = fmaf(G, dal, v[5]);
                     const float dQ = -0.5f * og * dal;
-                    v[0] = fmaf(dQ, -fmaf(2.f, adx, b2dy), v[0]);
-                    v[1] = fmaf(dQ, -fmaf(2.f, cdy, b2dx), v[1]);
+                    v[0] = fmaf(dQ, -fmaf(2.f, adx, b2dy[k]), v[0]);
+                    v[1] = fmaf(dQ, -fmaf(2.f, cdy[k], b2dx), v[1]);
                     v[2] = fmaf(dQ, dx * dx, v[2]);
                     v[3] = fmaf(dQ, 2.f * dx * dy, v[3]);
                     v[4] = fmaf(dQ, dy * dy, v[4]);
@@ -318,7 +331,6 @@ __global__ void __launch_bounds__(kT) blend_bwd_kernel(const uint32_t* __restric
                 U2[k] = fmaf(-w, col.z, U2[k]);
                 T[k] = T[k] * om;
             }
-            if (!__any_sync(0xffffffffu, any)) continue;
             const float r = red9(v, lane);
             if (slot >= 0) atomicAdd(&sG[j * kGS + slot], r);
         }

@@ -290,13 +290,29 @@ __global__ void duplicate_kernel(const uint32_t* __restrict__ perm, const uint32
 // K5 tile ranges: starts[t] = #instances with tile < t ; starts[Tn] = I
 // ----------------------------------------------------------------------------
 __global__ void ranges_kernel(const uint16_t* __restrict__ tkey, int64_t I, int Tn, uint32_t* __restrict__ starts) {
-    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (i >= I) return;
-    const int t = tkey[i];
-    const int tp = i == 0 ? -1 : int(tkey[i - 1]);
-    for (int tt = tp + 1; tt <= t; ++tt) starts[tt] = uint32_t(i);
-    if (i == I - 1)
-        for (int tt = t + 1; tt <= Tn; ++tt) starts[tt] = uint32_t(I);
+    // 8 consecutive keys per thread (one 16-byte load when aligned)
+    const int64_t i0 = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) * 8;
+    if (i0 >= I) return;
+    uint16_t k[8];
+    if (i0 + 8 <= I) {
+        const uint4 v = *reinterpret_cast<const uint4*>(tkey + i0);
+        const uint16_t* pv = reinterpret_cast<const uint16_t*>(&v);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) k[u] = pv[u];
+    } else {
+        for (int u = 0; u < 8; ++u) k[u] = i0 + u < I ? tkey[i0 + u] : 0;
+    }
+    int prev = i0 == 0 ? -1 : int(tkey[i0 - 1]);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+        const int64_t i = i0 + u;
+        if (i >= I) break;
+        const int t = k[u];
+        for (int tt = prev + 1; tt <= t; ++tt) starts[tt] = uint32_t(i);
+        prev = t;
+        if (i == I - 1)
+            for (int tt = t + 1; tt <= Tn; ++tt) starts[tt] = uint32_t(I);
+    }
 }
 
 __global__ void fill_u32_kernel(uint32_t* p, int64_t n, uint32_t v) {
@@ -327,6 +343,14 @@ void radix_sort(Context& c, K* k0, uint32_t* v0, K* k1, uint32_t* v1, int64_t n)
     uint32_t* offs = c.rhist.p + hn;
     K* ks[2] = {k0, k1};
     uint32_t* vs[2] = {v0, v1};
+    static bool carve = false;
+    if (!carve) {  // max shared-memory carveout: 8 resident scatter CTAs per SM instead of 4
+        cudaFuncSetAttribute(radix_scatter_kernel<uint32_t>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+        cudaFuncSetAttribute(radix_scatter_kernel<uint16_t>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+        cudaFuncSetAttribute(radix_count_kernel<uint32_t>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+        cudaFuncSetAttribute(radix_count_kernel<uint16_t>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+        carve = true;
+    }
     for (int p = 0; p < NPASS; ++p) {
         const int s = p & 1;
         radix_count_kernel<K><<<ntiles, kRT, 0, c.stream>>>(ks[s], n, 8 * p, counts, ntiles);
@@ -376,7 +400,8 @@ void launch_ranges(Context& c, int n_tiles) {
         TS_LAUNCHED(c);
         return;
     }
-    ranges_kernel<<<unsigned((c.I + 255) / 256), 256, 0, c.stream>>>(c.tkey[0].p, c.I, n_tiles, c.starts.p);
+    ranges_kernel<<<unsigned((c.I + 8 * 256 - 1) / (8 * 256)), 256, 0, c.stream>>>(c.tkey[0].p, c.I, n_tiles,
+                                                                                     c.starts.p);
     TS_LAUNCHED(c);
 }
 

@@ -228,24 +228,24 @@ __global__ void __launch_bounds__(kT) blend_bwd_kernel(const uint32_t* __restric
     const float wy0 = float(ty * 16 + (threadIdx.x >> 5) * 8), wy1 = wy0 + 7.f;
     const int P = cam.w * cam.h;
     const float fpx = float(px);
-    // per pixel: upstream gradient g, suffix colour U = C_final - prefix (incl. background), T, count
-    float g0[kPPT], g1[kPPT], g2[kPPT], U0[kPPT], U1[kPPT], U2[kPPT], T[kPPT];
+    // per pixel: upstream gradient g, T, count, and gU = g . U where U = C_final - prefix
+    // (the colour still to come after the current fragment, incl. background).  Only
+    // g . U enters the gradient and it updates as gU -= w (g . c), so one scalar suffices.
+    float g0[kPPT], g1[kPPT], g2[kPPT], gU[kPPT], T[kPPT];
     uint32_t cnt[kPPT];
     uint32_t mymax = 0;
 #pragma unroll
     for (int k = 0; k < kPPT; ++k) {
         const int py = py0 + k;
         T[k] = 1.f;
-        g0[k] = g1[k] = g2[k] = U0[k] = U1[k] = U2[k] = 0.f;
+        g0[k] = g1[k] = g2[k] = gU[k] = 0.f;
         cnt[k] = 0;
         if (px < cam.w && py < cam.h) {
             const int p = py * cam.w + px;
             g0[k] = dLdC[p];
             g1[k] = dLdC[P + p];
             g2[k] = dLdC[2 * P + p];
-            U0[k] = rgb[p];
-            U1[k] = rgb[P + p];
-            U2[k] = rgb[2 * P + p];
+            gU[k] = g0[k] * rgb[p] + g1[k] * rgb[P + p] + g2[k] * rgb[2 * P + p];
             cnt[k] = pcount[p];
         }
         mymax = max(mymax, cnt[k]);
@@ -285,22 +285,19 @@ __global__ void __launch_bounds__(kT) blend_bwd_kernel(const uint32_t* __restric
             const float adx = tsx::mul(q.x, dx);
             const uint32_t li = local0 + uint32_t(j);
             // keep mask of the 4 pixels first (exact Q); the warp skips the fragment if no lane keeps it
-            float Qv[kPPT], b2dy[kPPT], cdy[kPPT];
+            float Qv[kPPT];
             uint32_t km = 0;
 #pragma unroll
             for (int k = 0; k < kPPT; ++k) {
                 const float dy = tsx::sub(float(py0 + k), a.y);
-                b2dy[k] = tsx::mul(q.y, dy);
-                cdy[k] = tsx::mul(q.z, dy);
-                Qv[k] = tsx::add(tsx::mul(dx, tsx::add(adx, b2dy[k])), tsx::mul(dy, cdy[k]));
+                Qv[k] = tsx::add(tsx::mul(dx, tsx::add(adx, tsx::mul(q.y, dy))), tsx::mul(dy, tsx::mul(q.z, dy)));
                 km |= (li < cnt[k] && Qv[k] <= a.z) ? (1u << k) : 0u;
             }
             if (!__any_sync(0xffffffffu, km)) continue;
-            const float b2dx = q.y * dx;
             const float4 col = sC[j];
-            float v[9];
-#pragma unroll
-            for (int k = 0; k < 9; ++k) v[k] = 0.f;
+            // per-thread sums over its pixels: colour / opacity grads and the three
+            // moments of dL/dQ that give the mean2d and conic grads (dx is shared)
+            float vr = 0.f, vg = 0.f, vb = 0.f, vo = 0.f, sq = 0.f, sqy = 0.f, sqyy = 0.f;
 #pragma unroll
             for (int k = 0; k < kPPT; ++k) {
                 if (!(km & (1u << k))) continue;
@@ -312,25 +309,33 @@ __global__ void __launch_bounds__(kT) blend_bwd_kernel(const uint32_t* __restric
                 const float w = al * T[k];
                 const float om = 1.f - al;
                 const float gc = g0[k] * col.x + g1[k] * col.y + g2[k] * col.z;
-                const float gU = g0[k] * U0[k] + g1[k] * U1[k] + g2[k] * U2[k];
-                const float dal = T[k] * gc - (gU - w * gc) * rcp_approx(om);
-                v[6] = fmaf(w, g0[k], v[6]);
-                v[7] = fmaf(w, g1[k], v[7]);
-                v[8] = fmaf(w, g2[k], v[8]);
+                const float after = gU[k] - w * gc;  // g . (colour after this fragment, incl. bg)
+                const float dal = T[k] * gc - after * rcp_approx(om);
+                vr = fmaf(w, g0[k], vr);
+                vg = fmaf(w, g1[k], vg);
+                vb = fmaf(w, g2[k], vb);
                 if (!clamped) {
-                    v[5] = fmaf(G, dal, v[5]);
+                    vo = fmaf(G, dal, vo);
                     const float dQ = -0.5f * og * dal;
-                    v[0] = fmaf(dQ, -fmaf(2.f, adx, b2dy[k]), v[0]);
-                    v[1] = fmaf(dQ, -fmaf(2.f, cdy[k], b2dx), v[1]);
-                    v[2] = fmaf(dQ, dx * dx, v[2]);
-                    v[3] = fmaf(dQ, 2.f * dx * dy, v[3]);
-                    v[4] = fmaf(dQ, dy * dy, v[4]);
+                    const float dQy = dQ * dy;
+                    sq += dQ;
+                    sqy += dQy;
+                    sqyy = fmaf(dQy, dy, sqyy);
                 }
-                U0[k] = fmaf(-w, col.x, U0[k]);
-                U1[k] = fmaf(-w, col.y, U1[k]);
-                U2[k] = fmaf(-w, col.z, U2[k]);
+                gU[k] = after;
                 T[k] = T[k] * om;
             }
+            // dQ/dmx = -(2A dx + 2B dy), dQ/dmy = -(2B dx + 2C dy), dQ/dA = dx^2, dQ/dB = 2 dx dy, dQ/dC = dy^2
+            float v[9];
+            v[0] = -(2.f * adx * sq + q.y * sqy);
+            v[1] = -(q.y * dx * sq + 2.f * q.z * sqy);
+            v[2] = dx * dx * sq;
+            v[3] = 2.f * dx * sqy;
+            v[4] = sqyy;
+            v[5] = vo;
+            v[6] = vr;
+            v[7] = vg;
+            v[8] = vb;
             const float r = red9(v, lane);
             if (slot >= 0) atomicAdd(&sG[j * kGS + slot], r);
         }

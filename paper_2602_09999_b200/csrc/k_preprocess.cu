@@ -48,17 +48,14 @@ __global__ void __launch_bounds__(kBlock) preprocess_kernel(
         }
     }
     __syncthreads();
-    const bool live = g < N;
+    if (g >= N) return;
     const int tid = threadIdx.x;
-    // exact-cull candidates handed to the warp-cooperative pass below
-    int ncand = 0, ctx0 = 0, cty0 = 0, cwdt = 1;
-    float cmx = 0.f, cmy = 0.f, cA = 1.f, cB = 0.f, cC = 1.f, ck2 = 0.f, cnBA = 0.f, cnBC = 0.f;
     float4 s0 = make_float4(0.f, 0.f, 0.f, 0.f), s1 = s0, s2 = s0;
     uint32_t cnt = 0;
     uint4 rc = make_uint4(1u, 1u, 0u, 0u);  // empty: tx0=1 > tx1=0
     bool ok = false;
     float zh = 0.f;
-    if (live) do {
+    do {
         const float* W = cam.W;
         const float* mus = sm + kMu + sh[0] + 3 * tid;
         const float m0 = mus[0], m1 = mus[1], m2 = mus[2];
@@ -224,68 +221,18 @@ __global__ void __launch_bounds__(kBlock) preprocess_kernel(
             cnt = uint32_t(ntl);
             if (!big) mask = ntl == 64 ? ~0ull : ((1ull << ntl) - 1ull);
         } else {
-            ncand = ntl;
-            ctx0 = tx0, cty0 = ty0, cwdt = tx1 - tx0 + 1;
-            cmx = mx, cmy = my, cA = A, cB = B, cC = C, ck2 = k2;
-            cnBA = div(-B, A), cnBC = div(-B, C);
+            const float nBA = div(-B, A), nBC = div(-B, C);
+            int bit = 0;
+            for (int tyy = ty0; tyy <= ty1; ++tyy)
+                for (int txx = tx0; txx <= tx1; ++txx, ++bit) {
+                    const bool keep = tile_keep(mx, my, A, B, C, k2, nBA, nBC, txx, tyy, cam.w, cam.h);
+                    cnt += keep ? 1u : 0u;
+                    if (keep && !big) mask |= 1ull << bit;
+                }
         }
         rc.z = uint32_t(mask);
         rc.w = uint32_t(mask >> 32);
     } while (false);
-    // ---- warp-cooperative exact cull (tile_cull_exact) ----
-    // The warp's (Gaussian, candidate tile) pairs are enumerated by a prefix sum
-    // and evaluated 32 at a time, one pair per lane, so the warp no longer runs
-    // for the largest rect of its 32 Gaussians.  Results merge into per-Gaussian
-    // counts and kept-tile masks (bit = row-major position in the rect).
-    {
-        __shared__ uint32_t s_cnt[kBlock];
-        __shared__ unsigned long long s_mask[kBlock];
-        const int lane = tid & 31, wb = tid & ~31;
-        s_cnt[tid] = 0;
-        s_mask[tid] = 0ull;
-        __syncwarp();
-        int incl = ncand;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const int t = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= o) incl += t;
-        }
-        const int start = incl - ncand;
-        const int total = __shfl_sync(0xffffffffu, incl, 31);
-        for (int c0 = 0; c0 < total; c0 += 32) {
-            const int cidx = c0 + lane;
-            int own = 0;  // last lane whose range starts at or before cidx
-#pragma unroll
-            for (int step = 16; step >= 1; step >>= 1) {
-                const int mid = own + step;
-                const int sm = __shfl_sync(0xffffffffu, start, mid & 31);
-                if (mid < 32 && sm <= cidx) own = mid;
-            }
-            const float omx = __shfl_sync(0xffffffffu, cmx, own), omy = __shfl_sync(0xffffffffu, cmy, own);
-            const float oA = __shfl_sync(0xffffffffu, cA, own), oB = __shfl_sync(0xffffffffu, cB, own);
-            const float oC = __shfl_sync(0xffffffffu, cC, own), ok2 = __shfl_sync(0xffffffffu, ck2, own);
-            const float onBA = __shfl_sync(0xffffffffu, cnBA, own), onBC = __shfl_sync(0xffffffffu, cnBC, own);
-            const int otx0 = __shfl_sync(0xffffffffu, ctx0, own), oty0 = __shfl_sync(0xffffffffu, cty0, own);
-            const int owdt = __shfl_sync(0xffffffffu, cwdt, own), ost = __shfl_sync(0xffffffffu, start, own);
-            if (cidx < total) {
-                const int local = cidx - ost;
-                const int rr = local / owdt;
-                if (tile_keep(omx, omy, oA, oB, oC, ok2, onBA, onBC, otx0 + local - rr * owdt, oty0 + rr, cam.w,
-                              cam.h)) {
-                    atomicAdd(&s_cnt[wb + own], 1u);
-                    if (local < 64) atomicOr(&s_mask[wb + own], 1ull << local);
-                }
-            }
-        }
-        __syncwarp();
-        if (ncand > 0) {
-            cnt = s_cnt[tid];
-            const unsigned long long m = ncand <= 64 ? s_mask[tid] : 0ull;
-            rc.z = uint32_t(m);
-            rc.w = uint32_t(m >> 32);
-        }
-    }
-    if (!live) return;
     (void)ok;
     splat[3 * g] = s0;
     splat[3 * g + 1] = s1;

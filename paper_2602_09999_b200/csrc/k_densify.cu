@@ -170,10 +170,10 @@ int64_t launch_densify(Context& c, float thresh, float log_small, float log_big,
     c.N = NA;
     // resize the remaining per-Gaussian buffers and reset gradients / statistics
     const size_t n1 = size_t(std::max<int64_t>(NA, 1));
-    if (!ensure(c, c.grads, L) || !ensure(c, c.accum, n1) || !ensure(c, c.vcount, n1) ||
+    if (!ensure(c, c.grads, L) || !ensure(c, c.accum, n1 + 4) || !ensure(c, c.vcount, n1 + 4) ||
         !ensure(c, c.splat, 3 * n1) || !ensure(c, c.rect, n1) || !ensure(c, c.tcount, n1) ||
         !ensure(c, c.dkey[0], n1) || !ensure(c, c.dkey[1], n1) || !ensure(c, c.dperm[0], n1) ||
-        !ensure(c, c.dperm[1], n1) || !ensure(c, c.offsets, n1 + 1) || !ensure(c, c.g2d, 3 * n1) ||
+        !ensure(c, c.dperm[1], n1) || !ensure(c, c.offsets, n1 + 1) || !ensure(c, c.g2d, 3 * n1 + 1) ||
         !ensure(c, c.vis, n1))
         return -1;
     cudaMemsetAsync(c.grads.p, 0, c.grads.cap * 4, c.stream);

@@ -37,17 +37,17 @@ __global__ void __launch_bounds__(kBlock) preprocess_kernel(
                               {sm + kQ, P + off.q + 4 * g0, 4 * rows},
                               {sm + kOp, P + off.op + g0, rows},
                               {sm + kDc, P + off.dc + 3 * g0, 3 * rows}};
+        __shared__ unsigned long long bar;
         if constexpr (nrest > 0) {
             const Span sp[6] = {base[0], base[1], base[2], base[3], base[4],
                                 {sm + kRest, P + off.rest + g0 * 45, 45 * rows}};
-            stage_spans<kBlock>(sp, sh);
+            stage_spans_tma(sp, sh, &bar);
         } else {
             int s5[5];
-            stage_spans<kBlock>(base, s5);
+            stage_spans_tma(base, s5, &bar);
             for (int k = 0; k < 5; ++k) sh[k] = s5[k];
         }
     }
-    __syncthreads();
     if (g >= N) return;
     const int tid = threadIdx.x;
     float4 s0 = make_float4(0.f, 0.f, 0.f, 0.f), s1 = s0, s2 = s0;

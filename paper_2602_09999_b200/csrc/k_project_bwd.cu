@@ -320,24 +320,24 @@ __global__ void __launch_bounds__(kBlock) project_bwd_kernel(const float* __rest
                               {smem + L::kG2, reinterpret_cast<const float*>(g2d + 3 * g0), 12 * rows},
                               {smem + L::kAc, accum + g0, rows},
                               {smem + L::kVc, vcount + g0, rows}};
+        __shared__ unsigned long long bar;
         if constexpr (DEG == 0) {
             int s8[8];
-            stage_spans<kBlock>(base, s8);
+            stage_spans_tma(base, s8, &bar);
             for (int k = 0; k < 8; ++k) sh[k] = s8[k];
         } else if constexpr (!ACCUM) {
             const Span sp[9] = {base[0], base[1], base[2], base[3], base[4], base[5], base[6], base[7],
                                 {smem + L::kRest, P + off.rest + g0 * 45, 45 * rows}};
             int s9[9];
-            stage_spans<kBlock>(sp, s9);
+            stage_spans_tma(sp, s9, &bar);
             for (int k = 0; k < 9; ++k) sh[k] = s9[k];
         } else {
             const Span sp[10] = {base[0], base[1], base[2], base[3], base[4], base[5], base[6], base[7],
                                  {smem + L::kRest, P + off.rest + g0 * 45, 45 * rows},
                                  {smem + L::kGRest, G + off.rest + g0 * 45, 45 * rows}};
-            stage_spans<kBlock>(sp, sh);
+            stage_spans_tma(sp, sh, &bar);
         }
     }
-    __syncthreads();
     const int tid = threadIdx.x;
     float* rest_row = smem + L::kRest + sh[8] + tid * 45;
     if (active) {
@@ -463,9 +463,9 @@ __global__ void __launch_bounds__(kFB) project_bwd_adam_kernel(float* __restrict
         sp[18] = Span{smem + L::kG2, reinterpret_cast<const float*>(g2d + 3 * g0), 12 * rows};
         sp[19] = Span{smem + L::kAc, accum + g0, rows};
         sp[20] = Span{smem + L::kVc, vcount + g0, rows};
-        stage_spans<kFB>(sp, sh);
+        __shared__ unsigned long long bar;
+        stage_spans_tma(sp, sh, &bar);
     }
-    __syncthreads();
     const int tid = threadIdx.x;
 #define TS_ROW(c, s) (smem + (c) * L::kCopy + segoff[s] + sh[6 * (c) + (s)] + width[s] * tid)
     if (tid < rows) {

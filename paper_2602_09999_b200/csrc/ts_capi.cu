@@ -147,10 +147,10 @@ ts_status ensure_gaussian_buffers(Context& c, int64_t n) {
     const size_t N = size_t(std::max<int64_t>(n, 1));
     const size_t L = (59 * N + 7) & ~size_t(3);  // float4 sweeps read whole quads
     bool ok = ensure(c, c.params, L) && ensure(c, c.grads, L) && ensure(c, c.m, L) &&
-              ensure(c, c.v, L) && ensure(c, c.accum, N) && ensure(c, c.vcount, N) &&
+              ensure(c, c.v, L) && ensure(c, c.accum, N + 4) && ensure(c, c.vcount, N + 4) &&
               ensure(c, c.splat, 3 * N) && ensure(c, c.rect, N) && ensure(c, c.tcount, N) &&
               ensure(c, c.dkey[0], N) && ensure(c, c.dkey[1], N) && ensure(c, c.dperm[0], N) &&
-              ensure(c, c.dperm[1], N) && ensure(c, c.offsets, N + 1) && ensure(c, c.g2d, 3 * N) &&
+              ensure(c, c.dperm[1], N) && ensure(c, c.offsets, N + 1) && ensure(c, c.g2d, 3 * N + 1) &&
               ensure(c, c.vis, N);
     return ok ? TS_OK : TS_ERR_OOM;
 }

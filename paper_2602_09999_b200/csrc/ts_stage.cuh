@@ -103,3 +103,59 @@ __device__ __forceinline__ void stage_spans(const Span (&sp)[NS], int (&shift)[N
 }
 
 }  // namespace ts
+
+namespace ts {
+
+// ---------------------------------------------------------------------------
+// TMA bulk staging (cp.async.bulk global -> shared, completion on an mbarrier).
+// One elected thread issues one bulk copy per span; the copy engine moves the
+// bytes, so staging costs a handful of instructions per CTA instead of a loop
+// per 16-byte chunk.  Spans are copied from the 16-byte-aligned address at or
+// below src (shift as in stage_span); callers' global buffers are padded so the
+// rounded-up tail stays in bounds.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+template <int NS>
+__device__ __forceinline__ void stage_spans_tma(const Span (&sp)[NS], int (&shift)[NS], unsigned long long* bar) {
+    uint32_t bytes[NS];
+    const char* src[NS];
+    uint32_t total = 0;
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+        const uintptr_t a = reinterpret_cast<uintptr_t>(sp[s].src);
+        shift[s] = int((a & 15u) >> 2);
+        src[s] = reinterpret_cast<const char*>(a - uintptr_t(shift[s]) * 4u);
+        bytes[s] = sp[s].count > 0 ? uint32_t(((sp[s].count + shift[s]) * 4 + 15) & ~15) : 0u;
+        total += bytes[s];
+    }
+    if (threadIdx.x == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(total)
+                     : "memory");
+#pragma unroll
+        for (int s = 0; s < NS; ++s)
+            if (bytes[s])
+                asm volatile(
+                    "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                        smem_u32(sp[s].dst)),
+                    "l"(src[s]), "r"(bytes[s]), "r"(smem_u32(bar))
+                    : "memory");
+    }
+    uint32_t ready = 0;
+    while (!ready) {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(ready)
+            : "r"(smem_u32(bar))
+            : "memory");
+    }
+}
+
+}  // namespace ts

@@ -193,13 +193,22 @@ __global__ void __launch_bounds__(kRT) radix_scatter_kernel(const K* __restrict_
     s_goff[threadIdx.x] = goff[int64_t(threadIdx.x) * ntiles + blockIdx.x];
     __syncthreads();
     const uint32_t lt = (1u << lane) - 1u;
-    uint32_t dr[kRI];  // digit | (rank within warp) << 9 ; digit 0x1FF = invalid
+    // peers of every round first (independent MATCH ops overlap), then the
+    // sequential per-warp digit counters
+    uint32_t dig[kRI], peer[kRI];
 #pragma unroll
     for (int r = 0; r < kRI; ++r) {
         const int64_t i = wbase + r * 32 + lane;
-        const bool valid = i < n;
-        const uint32_t d = valid ? ((uint32_t(kk[r]) >> shift) & 255u) : 0x1FFu;
-        const uint32_t peers = __match_any_sync(0xffffffffu, d);
+        dig[r] = i < n ? ((uint32_t(kk[r]) >> shift) & 255u) : 0x1FFu;
+    }
+#pragma unroll
+    for (int r = 0; r < kRI; ++r) peer[r] = __match_any_sync(0xffffffffu, dig[r]);
+    uint32_t dr[kRI];  // digit | (rank within warp) << 9 ; digit 0x1FF = invalid
+#pragma unroll
+    for (int r = 0; r < kRI; ++r) {
+        const uint32_t d = dig[r];
+        const bool valid = d < 256u;
+        const uint32_t peers = peer[r];
         const uint32_t pre = valid ? wcnt[wid][d] : 0u;
         __syncwarp();
         if (valid && (peers & lt) == 0) wcnt[wid][d] = pre + __popc(peers);

@@ -1,13 +1,15 @@
 // K7 training_loss: 0.8 L1 + 0.2 (1 - SSIM) with an 11x11
 // Gaussian window (sigma 1.5), C1 = 0.01^2, C2 = 0.03^2, reflect padding, and the
-// analytic dL/dC.  Two shared-memory-tiled kernels per 16x16 pixel tile and
-// colour channel:
-//   loss_fwd: stage the reflect-padded 26x26 patch of rendered and target
-//     colour, separable 11-tap filtering of the 5 window moments, SSIM map and
-//     its partial derivatives (a, b, c below), block-reduced L1 / SSIM sums;
-//   loss_bwd: the transposed filter of (a, b, c) -- the same separable 11-tap
-//     correlation on the zero-extended maps, plus, for pixels within 5 of the
-//     image border, the terms folded back through the reflect padding -- and
+// analytic dL/dC.  Two shared-memory-tiled kernels per 32x32 pixel tile and
+// colour channel, both register-blocked (sliding windows: a thread filters 8
+// consecutive columns of one row, then 4 consecutive rows of one column, so
+// every staged value is loaded once per window instead of once per tap):
+//   loss_fwd: reflect-padded 42x42 patch of rendered and target colour, the 5
+//     separable window moments, the SSIM map and its partial derivatives
+//     (a, b, c below), block-reduced L1 / SSIM sums;
+//   loss_bwd: the transposed filter of (a, b, c): separable correlation of the
+//     zero-extended maps, plus, for pixels within 5 of the image border, the
+//     terms folded back through the reflect padding; then
 //     dL/dC = (0.8 sign(x-y) - 0.2 (W^T a + x W^T b + y W^T c)) / M.
 // With  mu = W x,  v = W x^2 - mu_x^2,  cov = W xy - mu_x mu_y  (per pixel):
 //   dSSIM/dx_p = (W^T a)_p + x_p (W^T b)_p + y_p (W^T c)_p,
@@ -20,73 +22,103 @@ namespace ts {
 namespace {
 
 __constant__ float c_gw[11];
-constexpr int kT = 16, kP = kT + 10, kPS = kP + 1;  // tile, patch, padded patch stride
+constexpr int kT = 32;           // output tile edge
+constexpr int kP = kT + 10;      // padded patch edge (42)
+constexpr int kPS = kP + 1;      // smem row stride
+constexpr int kThreads = 256;
+constexpr int kSeg = 8;          // columns per horizontal work item
+constexpr int kRows = 4;         // rows per vertical work item
 
 __device__ __forceinline__ int refl(int i, int n) { return i < 0 ? -i : (i >= n ? 2 * (n - 1) - i : i); }
 
-__global__ void __launch_bounds__(kT * kT) loss_fwd_kernel(const float* __restrict__ X, const float* __restrict__ Y,
-                                                           float* __restrict__ maps, int W, int H,
-                                                           double* __restrict__ acc) {
+__global__ void __launch_bounds__(kThreads) loss_fwd_kernel(const float* __restrict__ X, const float* __restrict__ Y,
+                                                            float* __restrict__ maps, int W, int H,
+                                                            double* __restrict__ acc) {
     __shared__ float sx[kP][kPS], sy[kP][kPS];
-    __shared__ float hm[5][kP][kT];
+    __shared__ float hm[5][kP][kT + 1];
     const int ch = blockIdx.z, P = W * H;
     const int x0 = blockIdx.x * kT, y0 = blockIdx.y * kT;
-    const int tid = threadIdx.y * kT + threadIdx.x;
+    const int tid = threadIdx.x;
     const float* Xc = X + size_t(ch) * P;
     const float* Yc = Y + size_t(ch) * P;
-    for (int i = tid; i < kP * kP; i += kT * kT) {
+    for (int i = tid; i < kP * kP; i += kThreads) {
         const int r = i / kP, c = i - r * kP;
         const int gi = refl(y0 - 5 + r, H) * W + refl(x0 - 5 + c, W);
         sx[r][c] = __ldg(Xc + gi);
         sy[r][c] = __ldg(Yc + gi);
     }
     __syncthreads();
-    for (int i = tid; i < kP * kT; i += kT * kT) {
-        const int r = i / kT, c = i - r * kT;
-        float m0 = 0.f, m1 = 0.f, m2 = 0.f, m3 = 0.f, m4 = 0.f;
+    // horizontal: (row, 8-column segment) items, sliding window of 18 inputs
+    for (int it = tid; it < kP * (kT / kSeg); it += kThreads) {
+        const int r = it / (kT / kSeg), c0 = (it - r * (kT / kSeg)) * kSeg;
+        float a[kSeg + 10], b[kSeg + 10];
 #pragma unroll
-        for (int k = 0; k < 11; ++k) {
-            const float a = sx[r][c + k], b = sy[r][c + k], w = c_gw[k];
-            m0 = fmaf(w, a, m0);
-            m1 = fmaf(w, b, m1);
-            m2 = fmaf(w * a, a, m2);
-            m3 = fmaf(w * b, b, m3);
-            m4 = fmaf(w * a, b, m4);
+        for (int k = 0; k < kSeg + 10; ++k) {
+            a[k] = sx[r][c0 + k];
+            b[k] = sy[r][c0 + k];
         }
-        hm[0][r][c] = m0, hm[1][r][c] = m1, hm[2][r][c] = m2, hm[3][r][c] = m3, hm[4][r][c] = m4;
+#pragma unroll
+        for (int j = 0; j < kSeg; ++j) {
+            float m0 = 0.f, m1 = 0.f, m2 = 0.f, m3 = 0.f, m4 = 0.f;
+#pragma unroll
+            for (int k = 0; k < 11; ++k) {
+                const float w = c_gw[k], xa = a[j + k], yb = b[j + k];
+                const float wx = w * xa, wy = w * yb;
+                m0 += wx;
+                m1 += wy;
+                m2 = fmaf(wx, xa, m2);
+                m3 = fmaf(wy, yb, m3);
+                m4 = fmaf(wx, yb, m4);
+            }
+            hm[0][r][c0 + j] = m0, hm[1][r][c0 + j] = m1, hm[2][r][c0 + j] = m2, hm[3][r][c0 + j] = m3,
+            hm[4][r][c0 + j] = m4;
+        }
     }
     __syncthreads();
-    const int tx = threadIdx.x, ty = threadIdx.y;
-    const int x = x0 + tx, y = y0 + ty;
+    // vertical: (column, 4-row group) items, sliding window of 14 rows; SSIM per pixel
+    const int c = tid % kT, rg = (tid / kT) * kRows;  // 32 columns x 8 groups = 256 threads
     float l1 = 0.f, ss = 0.f;
-    if (x < W && y < H) {
-        float m[5] = {0.f, 0.f, 0.f, 0.f, 0.f};
+    {
+        float m[kRows][5];
 #pragma unroll
-        for (int k = 0; k < 11; ++k) {
-            const float w = c_gw[k];
+        for (int j = 0; j < kRows; ++j)
 #pragma unroll
-            for (int q = 0; q < 5; ++q) m[q] = fmaf(w, hm[q][ty + k][tx], m[q]);
+            for (int q = 0; q < 5; ++q) m[j][q] = 0.f;
+#pragma unroll
+        for (int q = 0; q < 5; ++q) {
+            float win[kRows + 10];
+#pragma unroll
+            for (int k = 0; k < kRows + 10; ++k) win[k] = hm[q][rg + k][c];
+#pragma unroll
+            for (int j = 0; j < kRows; ++j)
+#pragma unroll
+                for (int k = 0; k < 11; ++k) m[j][q] = fmaf(c_gw[k], win[j + k], m[j][q]);
         }
         const float C1 = 0.01f * 0.01f, C2 = 0.03f * 0.03f;
-        const float ux = m[0], uy = m[1];
-        const float vx = m[2] - ux * ux, vy = m[3] - uy * uy, cxy = m[4] - ux * uy;
-        const float n1 = 2.f * ux * uy + C1, n2 = 2.f * cxy + C2;
-        const float d1 = ux * ux + uy * uy + C1, d2 = vx + vy + C2;
-        const float iD = 1.f / (d1 * d2);
-        const float S = n1 * n2 * iD;
-        const float dS_dux = (2.f * uy * n2 - S * 2.f * ux * d2) * iD;
-        const float dS_dvx = -S / d2;
-        const float dS_dcxy = 2.f * n1 * iD;
-        const int p = y * W + x;
         float* mp = maps + size_t(ch) * 3 * P;
-        mp[p] = dS_dux - 2.f * ux * dS_dvx - uy * dS_dcxy;
-        mp[P + p] = 2.f * dS_dvx;
-        mp[2 * P + p] = dS_dcxy;
-        ss = S;
-        l1 = fabsf(sx[ty + 5][tx + 5] - sy[ty + 5][tx + 5]);
+#pragma unroll
+        for (int j = 0; j < kRows; ++j) {
+            const int x = x0 + c, y = y0 + rg + j;
+            if (x >= W || y >= H) continue;
+            const float ux = m[j][0], uy = m[j][1];
+            const float vx = m[j][2] - ux * ux, vy = m[j][3] - uy * uy, cxy = m[j][4] - ux * uy;
+            const float n1 = 2.f * ux * uy + C1, n2 = 2.f * cxy + C2;
+            const float d1 = ux * ux + uy * uy + C1, d2 = vx + vy + C2;
+            const float iD = 1.f / (d1 * d2);
+            const float S = n1 * n2 * iD;
+            const float dS_dux = (2.f * uy * n2 - S * 2.f * ux * d2) * iD;
+            const float dS_dvx = -S * d1 * iD;
+            const float dS_dcxy = 2.f * n1 * iD;
+            const int p = y * W + x;
+            mp[p] = dS_dux - 2.f * ux * dS_dvx - uy * dS_dcxy;
+            mp[P + p] = 2.f * dS_dvx;
+            mp[2 * P + p] = dS_dcxy;
+            ss += S;
+            l1 += fabsf(sx[rg + j + 5][c + 5] - sy[rg + j + 5][c + 5]);
+        }
     }
     // block reduction of (L1, SSIM) -> double atomics
-    __shared__ float r1[8], r2[8];
+    __shared__ float r1[kThreads / 32], r2[kThreads / 32];
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
         l1 += __shfl_xor_sync(0xffffffffu, l1, o);
@@ -99,7 +131,7 @@ __global__ void __launch_bounds__(kT * kT) loss_fwd_kernel(const float* __restri
     __syncthreads();
     if (tid == 0) {
         double a = 0, b = 0;
-        for (int w = 0; w < 8; ++w) {
+        for (int w = 0; w < kThreads / 32; ++w) {
             a += r1[w];
             b += r2[w];
         }
@@ -125,16 +157,16 @@ __device__ __forceinline__ float window_sum(const float* __restrict__ f, int jx,
     return s;
 }
 
-__global__ void __launch_bounds__(kT * kT) loss_bwd_kernel(const float* __restrict__ X, const float* __restrict__ Y,
-                                                           const float* __restrict__ maps, float* __restrict__ dL,
-                                                           int W, int H, float inv_m) {
+__global__ void __launch_bounds__(kThreads) loss_bwd_kernel(const float* __restrict__ X, const float* __restrict__ Y,
+                                                            const float* __restrict__ maps, float* __restrict__ dL,
+                                                            int W, int H, float inv_m) {
     __shared__ float sf[3][kP][kPS];
-    __shared__ float hm[3][kP][kT];
+    __shared__ float hm[3][kP][kT + 1];
     const int ch = blockIdx.z, P = W * H;
     const int x0 = blockIdx.x * kT, y0 = blockIdx.y * kT;
-    const int tid = threadIdx.y * kT + threadIdx.x;
+    const int tid = threadIdx.x;
     const float* mp = maps + size_t(ch) * 3 * P;
-    for (int i = tid; i < kP * kP; i += kT * kT) {
+    for (int i = tid; i < kP * kP; i += kThreads) {
         const int r = i / kP, c = i - r * kP;
         const int gy = y0 - 5 + r, gx = x0 - 5 + c;
         const bool in = gy >= 0 && gy < H && gx >= 0 && gx < W;
@@ -143,51 +175,65 @@ __global__ void __launch_bounds__(kT * kT) loss_bwd_kernel(const float* __restri
         for (int q = 0; q < 3; ++q) sf[q][r][c] = in ? __ldg(mp + q * P + gi) : 0.f;
     }
     __syncthreads();
-    for (int i = tid; i < kP * kT; i += kT * kT) {
-        const int r = i / kT, c = i - r * kT;
-        float a = 0.f, b = 0.f, d = 0.f;
+    for (int it = tid; it < kP * (kT / kSeg); it += kThreads) {
+        const int r = it / (kT / kSeg), c0 = (it - r * (kT / kSeg)) * kSeg;
 #pragma unroll
-        for (int k = 0; k < 11; ++k) {
-            const float w = c_gw[k];
-            a = fmaf(w, sf[0][r][c + k], a);
-            b = fmaf(w, sf[1][r][c + k], b);
-            d = fmaf(w, sf[2][r][c + k], d);
+        for (int q = 0; q < 3; ++q) {
+            float a[kSeg + 10];
+#pragma unroll
+            for (int k = 0; k < kSeg + 10; ++k) a[k] = sf[q][r][c0 + k];
+#pragma unroll
+            for (int j = 0; j < kSeg; ++j) {
+                float s = 0.f;
+#pragma unroll
+                for (int k = 0; k < 11; ++k) s = fmaf(c_gw[k], a[j + k], s);
+                hm[q][r][c0 + j] = s;
+            }
         }
-        hm[0][r][c] = a, hm[1][r][c] = b, hm[2][r][c] = d;
     }
     __syncthreads();
-    const int tx = threadIdx.x, ty = threadIdx.y;
-    const int x = x0 + tx, y = y0 + ty;
-    if (x >= W || y >= H) return;
-    float t[3] = {0.f, 0.f, 0.f};
+    const int c = tid % kT, rg = (tid / kT) * kRows;
+    float t[kRows][3];
 #pragma unroll
-    for (int k = 0; k < 11; ++k) {
-        const float w = c_gw[k];
+    for (int q = 0; q < 3; ++q) {
+        float win[kRows + 10];
 #pragma unroll
-        for (int q = 0; q < 3; ++q) t[q] = fmaf(w, hm[q][ty + k][tx], t[q]);
+        for (int k = 0; k < kRows + 10; ++k) win[k] = hm[q][rg + k][c];
+#pragma unroll
+        for (int j = 0; j < kRows; ++j) {
+            float s = 0.f;
+#pragma unroll
+            for (int k = 0; k < 11; ++k) s = fmaf(c_gw[k], win[j + k], s);
+            t[j][q] = s;
+        }
     }
-    // reflect-padding fold terms (pixels within 5 of a border)
-    if (x <= 5 || x >= W - 6 || y <= 5 || y >= H - 6) {
-        int jx[3], jy[3], nx = 0, ny = 0;
-        jx[nx++] = x;
-        if (x >= 1 && x <= 5) jx[nx++] = -x;
-        if (x >= W - 6 && x <= W - 2) jx[nx++] = 2 * (W - 1) - x;
-        jy[ny++] = y;
-        if (y >= 1 && y <= 5) jy[ny++] = -y;
-        if (y >= H - 6 && y <= H - 2) jy[ny++] = 2 * (H - 1) - y;
-        for (int a = 0; a < nx; ++a)
-            for (int b = 0; b < ny; ++b) {
-                if (a == 0 && b == 0) continue;
+    const bool border_tile = x0 <= 5 || y0 <= 5 || x0 + kT - 1 >= W - 6 || y0 + kT - 1 >= H - 6;
 #pragma unroll
-                for (int q = 0; q < 3; ++q) t[q] += window_sum(mp + q * P, jx[a], jy[b], W, H);
-            }
+    for (int j = 0; j < kRows; ++j) {
+        const int x = x0 + c, y = y0 + rg + j;
+        if (x >= W || y >= H) continue;
+        if (border_tile && (x <= 5 || x >= W - 6 || y <= 5 || y >= H - 6)) {
+            // reflect-padding fold terms of the transposed filter
+            int jx[3], jy[3], nx = 0, ny = 0;
+            jx[nx++] = x;
+            if (x >= 1 && x <= 5) jx[nx++] = -x;
+            if (x >= W - 6 && x <= W - 2) jx[nx++] = 2 * (W - 1) - x;
+            jy[ny++] = y;
+            if (y >= 1 && y <= 5) jy[ny++] = -y;
+            if (y >= H - 6 && y <= H - 2) jy[ny++] = 2 * (H - 1) - y;
+            for (int a = 0; a < nx; ++a)
+                for (int b = 0; b < ny; ++b) {
+                    if (a == 0 && b == 0) continue;
+                    for (int q = 0; q < 3; ++q) t[j][q] += window_sum(mp + q * P, jx[a], jy[b], W, H);
+                }
+        }
+        const int p = y * W + x;
+        const float xv = X[size_t(ch) * P + p], yv = Y[size_t(ch) * P + p];
+        const float dS = t[j][0] + xv * t[j][1] + yv * t[j][2];
+        const float d = xv - yv;
+        const float sg = d > 0.f ? 1.f : (d < 0.f ? -1.f : 0.f);
+        dL[size_t(ch) * P + p] = (0.8f * sg - 0.2f * dS) * inv_m;
     }
-    const int p = y * W + x;
-    const float xv = X[size_t(ch) * P + p], yv = Y[size_t(ch) * P + p];
-    const float dS = t[0] + xv * t[1] + yv * t[2];
-    const float d = xv - yv;
-    const float sg = d > 0.f ? 1.f : (d < 0.f ? -1.f : 0.f);
-    dL[size_t(ch) * P + p] = (0.8f * sg - 0.2f * dS) * inv_m;
 }
 
 }  // namespace
@@ -208,10 +254,10 @@ void launch_loss(Context& c, const float* target_chw) {
     }
     const int W = c.fw, H = c.fh, P = W * H;
     cudaMemsetAsync(c.loss_acc.p, 0, 2 * sizeof(double), c.stream);
-    const dim3 grid((W + kT - 1) / kT, (H + kT - 1) / kT, 3), block(kT, kT);
-    loss_fwd_kernel<<<grid, block, 0, c.stream>>>(c.rgb.p, target_chw, c.loss_tmp.p, W, H, c.loss_acc.p);
-    loss_bwd_kernel<<<grid, block, 0, c.stream>>>(c.rgb.p, target_chw, c.loss_tmp.p, c.dLdC.p, W, H,
-                                                  float(1.0 / (3.0 * double(P))));
+    const dim3 grid((W + kT - 1) / kT, (H + kT - 1) / kT, 3);
+    loss_fwd_kernel<<<grid, kThreads, 0, c.stream>>>(c.rgb.p, target_chw, c.loss_tmp.p, W, H, c.loss_acc.p);
+    loss_bwd_kernel<<<grid, kThreads, 0, c.stream>>>(c.rgb.p, target_chw, c.loss_tmp.p, c.dLdC.p, W, H,
+                                                     float(1.0 / (3.0 * double(P))));
     c.launches += 2;
 }
 

@@ -179,6 +179,12 @@ class Engine {
         return n;
     }
     void opacity_reset() { check(ts_opacity_reset(ctx_), "ts_opacity_reset"); }
+    // morton_reorder: returns perm[new] = old
+    std::vector<uint32_t> morton_reorder() {
+        std::vector<uint32_t> perm(static_cast<size_t>(size()));
+        check(ts_morton_reorder(ctx_, perm.data()), "ts_morton_reorder");
+        return perm;
+    }
     ts_ctx* handle() { return ctx_; }
 
    private:

@@ -136,6 +136,9 @@ ts_status ts_train_step(ts_ctx* ctx, const ts_camera* cam, const ts_render_confi
 ts_status ts_densify(ts_ctx* ctx, float grad_thresh, float extent, uint64_t seed, int64_t iter,
                      int64_t* n_after, int64_t stats[3] /* clones, splits, pruned */);
 ts_status ts_opacity_reset(ts_ctx* ctx);
+/* morton_reorder: permute params, Adam moments and densify statistics into
+ * 63-bit Morton order of the means; perm (N, may be NULL) receives old index per new row. */
+ts_status ts_morton_reorder(ts_ctx* ctx, uint32_t* perm);
 
 /* ---- state access for tests / checkpointing ---- */
 ts_status ts_set_state(ts_ctx* ctx, const float* grads, const float* m, const float* v, const float* accum,

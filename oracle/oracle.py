@@ -64,6 +64,10 @@ def _load():
         "tso_densify_and_prune": (i64, [i64, f32p, f32p, f32p, f32p, f32p, ctypes.c_float, ctypes.c_float,
                                         ctypes.c_uint64, i64, f32p, f32p, f32p, i64p]),
         "tso_opacity_reset": (None, [i64, f32p]),
+        "tso_morton_interleave": (ctypes.c_uint64, [ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32,
+                                                    ctypes.c_int]),
+        "tso_morton_codes": (None, [i64, f32p, vp]),
+        "tso_morton_reorder": (None, [i64, f32p, vp, vp, vp, vp, vp]),
         "tso_train_step": (ctypes.c_double, [i64, f32p, f32p, f32p, vp, vp, f32p, f32p, ctypes.c_float,
                                              ctypes.c_float, ctypes.c_float, ctypes.c_float, ctypes.c_float,
                                              f32p, f32p, f64p]),
@@ -174,6 +178,28 @@ def densify(params, m, v, accum, vcount, n, grad_thresh, extent, seed, it):
     na = int(na)
     # outputs were written with stride na (block layout of the compacted store)
     return op[:59 * na].copy(), om[:59 * na].copy(), ov[:59 * na].copy(), na, st
+
+
+def morton_interleave(qx, qy, qz, bits=21):
+    return int(lib.tso_morton_interleave(qx, qy, qz, bits))
+
+
+def morton_codes(params, n):
+    out = np.zeros(n, np.uint64)
+    lib.tso_morton_codes(n, np.ascontiguousarray(params, np.float32), out.ctypes.data)
+    return out
+
+
+def _vp_or_none(a):
+    return None if a is None else a.ctypes.data
+
+
+def morton_reorder(params, n, m=None, v=None, accum=None, vcount=None):
+    """In-place permutation of the given float32 arrays; returns perm[new] = old."""
+    perm = np.zeros(n, np.uint32)
+    lib.tso_morton_reorder(n, params, _vp_or_none(m), _vp_or_none(v), _vp_or_none(accum), _vp_or_none(vcount),
+                           perm.ctypes.data)
+    return perm
 
 
 def train_step(params, m, v, n, cam, cfg, target, adam, accum, vcount):

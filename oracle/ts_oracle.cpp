@@ -1489,6 +1489,67 @@ void tso_opacity_reset(int64_t n, float* P) {
     for (int64_t g = 0; g < n; ++g) P[off.op + g] = P[off.op + g] < lmax ? P[off.op + g] : lmax;
 }
 
+// ---------------------------------------------------------------------------
+// morton_reorder: quantise means to 21 bits per axis over the
+// mean AABB inflated by 1e-6, interleave x-LSB-first into a 63-bit
+// code, stable sort (code, index), permute every per-Gaussian array.
+// Quantisation: q = min(2^21-1, uint(((p - lo) / ((hi - lo) + 1e-6)) * 2^21)),
+// each op rounded to fp32 (the device computes the same expression).
+// ---------------------------------------------------------------------------
+uint64_t tso_morton_interleave(uint32_t qx, uint32_t qy, uint32_t qz, int bits) {
+    uint64_t c = 0;
+    const uint32_t q[3] = {qx, qy, qz};
+    for (int b = 0; b < bits; ++b)
+        for (int k = 0; k < 3; ++k) c |= uint64_t((q[k] >> b) & 1u) << (3 * b + k);
+    return c;
+}
+
+void tso_morton_codes(int64_t n, const float* P, uint64_t* codes) {
+    float lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+    for (int64_t g = 0; g < n; ++g)
+        for (int k = 0; k < 3; ++k) {
+            lo[k] = std::min(lo[k], P[3 * g + k]);
+            hi[k] = std::max(hi[k], P[3 * g + k]);
+        }
+    for (int64_t g = 0; g < n; ++g) {
+        uint32_t q[3];
+        for (int k = 0; k < 3; ++k) {
+            const float span = (hi[k] - lo[k]) + 1e-6f;
+            const float t = ((P[3 * g + k] - lo[k]) / span) * 2097152.0f;
+            const uint32_t u = uint32_t(t);
+            q[k] = u > 2097151u ? 2097151u : u;
+        }
+        codes[g] = tso_morton_interleave(q[0], q[1], q[2], 21);
+    }
+}
+
+void tso_morton_reorder(int64_t n, float* P, float* M, float* V, float* accum, float* vcount, uint32_t* perm) {
+    if (n <= 0) return;
+    std::vector<uint64_t> code(n);
+    tso_morton_codes(n, P, code.data());
+    std::vector<uint32_t> idx(n);
+    for (int64_t i = 0; i < n; ++i) idx[i] = uint32_t(i);
+    std::stable_sort(idx.begin(), idx.end(), [&](uint32_t a, uint32_t b) { return code[a] < code[b]; });
+    const Off o(n);
+    const int64_t starts[6] = {o.means, o.ls, o.q, o.op, o.dc, o.rest};
+    const int width[6] = {3, 3, 4, 1, 3, 45};
+    std::vector<float> tmp;
+    for (float* B : {P, M, V}) {
+        if (!B) continue;
+        tmp.assign(B, B + 59 * n);
+        for (int a = 0; a < 6; ++a)
+            for (int64_t r = 0; r < n; ++r)
+                for (int k = 0; k < width[a]; ++k)
+                    B[starts[a] + r * width[a] + k] = tmp[starts[a] + int64_t(idx[r]) * width[a] + k];
+    }
+    for (float* B : {accum, vcount}) {
+        if (!B) continue;
+        tmp.assign(B, B + n);
+        for (int64_t r = 0; r < n; ++r) B[r] = tmp[idx[r]];
+    }
+    if (perm) std::copy(idx.begin(), idx.end(), perm);
+}
+
 // One full training step on one view (SPEC.md:829-837 step body): render ->
 // training_loss -> backward -> Adam, each stage timed (bench per-stage times,
 // SPEC.md:839-847).  This is the timed CPU baseline unit.

@@ -125,6 +125,14 @@ int64_t tso_densify_and_prune(int64_t n, const float* params, const float* m, co
                               uint64_t seed, int64_t iter, float* out_params, float* out_m, float* out_v,
                               int64_t* out_stats);
 void tso_opacity_reset(int64_t n, float* params);
+/* ---- morton_reorder ----
+ * interleave: bits per axis, x in the least significant position of each triple. */
+uint64_t tso_morton_interleave(uint32_t qx, uint32_t qy, uint32_t qz, int bits);
+/* 63-bit codes of the means quantised to 21 bits over the AABB inflated by 1e-6 */
+void tso_morton_codes(int64_t n, const float* params, uint64_t* codes);
+/* stable sort by code; permutes params/m/v (59n each, may be NULL) and accum/vcount (n, may be NULL)
+ * in place; perm[new] = old. */
+void tso_morton_reorder(int64_t n, float* params, float* m, float* v, float* accum, float* vcount, uint32_t* perm);
 /* full single-view training step (render, loss vs target HWC, backward, fused Adam);
  * stage_seconds[8] = {preprocess, binning, blend, loss, raster_bwd, project_bwd, adam, I}. */
 double tso_train_step(int64_t n, float* params, float* m, float* v, const tso_camera* cam,

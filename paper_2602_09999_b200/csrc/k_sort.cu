@@ -155,7 +155,7 @@ __global__ void __launch_bounds__(kRT) radix_count_kernel(const K* __restrict__ 
 #pragma unroll
     for (int r = 0; r < kRI; ++r) {
         const int64_t i = base + int64_t(r) * kRT + threadIdx.x;
-        d[r] = i < n ? ((uint32_t(keys[i]) >> shift) & 255u) : 0x100u;
+        d[r] = i < n ? uint32_t((uint64_t(keys[i]) >> shift) & 255u) : 0x100u;
     }
 #pragma unroll
     for (int r = 0; r < kRI; ++r)
@@ -199,7 +199,7 @@ __global__ void __launch_bounds__(kRT) radix_scatter_kernel(const K* __restrict_
 #pragma unroll
     for (int r = 0; r < kRI; ++r) {
         const int64_t i = wbase + r * 32 + lane;
-        dig[r] = i < n ? ((uint32_t(kk[r]) >> shift) & 255u) : 0x1FFu;
+        dig[r] = i < n ? uint32_t((uint64_t(kk[r]) >> shift) & 255u) : 0x1FFu;
     }
 #pragma unroll
     for (int r = 0; r < kRI; ++r) peer[r] = __match_any_sync(0xffffffffu, dig[r]);
@@ -243,7 +243,7 @@ __global__ void __launch_bounds__(kRT) radix_scatter_kernel(const K* __restrict_
         const int i = threadIdx.x + r * kRT;
         if (i < tile_n) {
             const K key = skey[i];
-            const uint32_t dd = (uint32_t(key) >> shift) & 255u;
+            const uint32_t dd = uint32_t((uint64_t(key) >> shift) & 255u);
             const uint32_t pos = s_goff[dd] + (uint32_t(i) - s_bstart[dd]);
             kout[pos] = key;
             vout[pos] = sval[i];
@@ -358,6 +358,8 @@ void radix_sort(Context& c, K* k0, uint32_t* v0, K* k1, uint32_t* v1, int64_t n)
         cudaFuncSetAttribute(radix_scatter_kernel<uint16_t>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
         cudaFuncSetAttribute(radix_count_kernel<uint32_t>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
         cudaFuncSetAttribute(radix_count_kernel<uint16_t>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+        cudaFuncSetAttribute(radix_scatter_kernel<unsigned long long>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                             100);
         carve = true;
     }
     for (int p = 0; p < NPASS; ++p) {
@@ -393,6 +395,76 @@ void launch_duplicate(Context& c, const DevCam& cam, const ts_render_config& cfg
     TS_LAUNCHED(c);
 }
 
+// ----------------------------------------------------------------------------
+// morton_reorder: 63-bit Morton codes of the means quantised
+// to 21 bits per axis over their bounding box (inflated by 1e-6), x in the least
+// significant interleave position; stable LSD sort of (code, index); every
+// per-Gaussian array is then gathered through the permutation.
+// ----------------------------------------------------------------------------
+__device__ __forceinline__ uint64_t spread3(uint32_t v) {
+    uint64_t x = v & 0x1FFFFFu;
+    x = (x | (x << 32)) & 0x1F00000000FFFFull;
+    x = (x | (x << 16)) & 0x1F0000FF0000FFull;
+    x = (x | (x << 8)) & 0x100F00F00F00F00Full;
+    x = (x | (x << 4)) & 0x10C30C30C30C30C3ull;
+    x = (x | (x << 2)) & 0x1249249249249249ull;
+    return x;
+}
+
+__global__ void bbox_kernel(const float* __restrict__ means, int64_t N, float* __restrict__ box /* 6: min xyz, max xyz */) {
+    float lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+    for (int64_t g = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; g < N; g += int64_t(gridDim.x) * blockDim.x)
+        for (int k = 0; k < 3; ++k) {
+            const float v = means[3 * g + k];
+            lo[k] = fminf(lo[k], v);
+            hi[k] = fmaxf(hi[k], v);
+        }
+    for (int k = 0; k < 3; ++k) {
+        for (int o = 16; o > 0; o >>= 1) {
+            lo[k] = fminf(lo[k], __shfl_xor_sync(0xffffffffu, lo[k], o));
+            hi[k] = fmaxf(hi[k], __shfl_xor_sync(0xffffffffu, hi[k], o));
+        }
+        if ((threadIdx.x & 31) == 0) {
+            // order-preserving int images of floats for atomic min/max
+            const int a = __float_as_int(lo[k]), b = __float_as_int(hi[k]);
+            atomicMin(reinterpret_cast<int*>(box) + k, a >= 0 ? a : int(0x80000000u ^ ~uint32_t(a)));
+            atomicMax(reinterpret_cast<int*>(box) + 3 + k, b >= 0 ? b : int(0x80000000u ^ ~uint32_t(b)));
+        }
+    }
+}
+
+__device__ __forceinline__ float unmap_ordered(int v) {
+    return v >= 0 ? __int_as_float(v) : __int_as_float(int(~(uint32_t(v) ^ 0x80000000u)));
+}
+
+__global__ void morton_code_kernel(const float* __restrict__ means, int64_t N, const float* __restrict__ box,
+                                   unsigned long long* __restrict__ code, uint32_t* __restrict__ idx) {
+    const int64_t g = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (g >= N) return;
+    uint64_t c = 0;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        const float lo = unmap_ordered(reinterpret_cast<const int*>(box)[k]);
+        const float hi = unmap_ordered(reinterpret_cast<const int*>(box)[3 + k]);
+        const float span = tsx::add(tsx::sub(hi, lo), 1e-6f);
+        const float t = tsx::mul(tsx::div(tsx::sub(means[3 * g + k], lo), span), 2097152.0f);
+        uint32_t q = uint32_t(t);
+        q = q > 2097151u ? 2097151u : q;
+        c |= spread3(q) << k;
+    }
+    code[g] = c;
+    idx[g] = uint32_t(g);
+}
+
+template <int W>
+__global__ void gather_rows_kernel(const float* __restrict__ src, float* __restrict__ dst,
+                                   const uint32_t* __restrict__ perm, int64_t N) {
+    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= N * W) return;
+    const int64_t r = i / W, k = i - r * W;
+    dst[i] = src[int64_t(perm[r]) * W + k];
+}
+
 void launch_tile_sort(Context& c, int tile_bits) {
     if (tile_bits <= 8) {
         radix_sort<uint16_t, 1>(c, c.tkey[0].p, c.ival[0].p, c.tkey[1].p, c.ival[1].p, c.I);
@@ -412,6 +484,58 @@ void launch_ranges(Context& c, int n_tiles) {
     ranges_kernel<<<unsigned((c.I + 8 * 256 - 1) / (8 * 256)), 256, 0, c.stream>>>(c.tkey[0].p, c.I, n_tiles,
                                                                                      c.starts.p);
     TS_LAUNCHED(c);
+}
+
+template <int W>
+static void gather_group(Context& c, const float* src, float* dst, const uint32_t* perm, int64_t N) {
+    const int64_t n = N * W;
+    if (n == 0) return;
+    gather_rows_kernel<W><<<unsigned((n + 255) / 256), 256, 0, c.stream>>>(src, dst, perm, N);
+    TS_LAUNCHED(c);
+}
+
+bool launch_morton_reorder(Context& c, uint32_t* perm_host) {
+    const int64_t N = c.N;
+    if (N == 0) return true;
+    DevBuf<unsigned long long> code[2];
+    DevBuf<uint32_t> idx[2];
+    DevBuf<float> box, tmp;
+    if (!ensure(c, code[0], N) || !ensure(c, code[1], N) || !ensure(c, idx[0], N) || !ensure(c, idx[1], N) ||
+        !ensure(c, box, 8) || !ensure(c, tmp, size_t(59) * N + 8))
+        return false;
+    const int init[6] = {0x7f800000, 0x7f800000, 0x7f800000, int(0x80000000u ^ ~0xff800000u),
+                         int(0x80000000u ^ ~0xff800000u), int(0x80000000u ^ ~0xff800000u)};
+    cudaMemcpyAsync(box.p, init, sizeof(init), cudaMemcpyHostToDevice, c.stream);
+    bbox_kernel<<<c.sm_count * 2, 256, 0, c.stream>>>(c.params.p, N, box.p);
+    morton_code_kernel<<<unsigned((N + 255) / 256), 256, 0, c.stream>>>(c.params.p, N, box.p, code[0].p, idx[0].p);
+    c.launches += 2;
+    radix_sort<unsigned long long, 8>(c, code[0].p, idx[0].p, code[1].p, idx[1].p, N);
+    const uint32_t* perm = idx[0].p;  // 8 passes: result in buffer 0
+    // permute params, both moments (flat 59*N, per attribute block) and the statistics
+    const Off o(N);
+    float* bufs[3] = {c.params.p, c.m.p, c.v.p};
+    for (float* b : bufs) {
+        gather_group<3>(c, b + o.means, tmp.p + o.means, perm, N);
+        gather_group<3>(c, b + o.ls, tmp.p + o.ls, perm, N);
+        gather_group<4>(c, b + o.q, tmp.p + o.q, perm, N);
+        gather_group<1>(c, b + o.op, tmp.p + o.op, perm, N);
+        gather_group<3>(c, b + o.dc, tmp.p + o.dc, perm, N);
+        gather_group<45>(c, b + o.rest, tmp.p + o.rest, perm, N);
+        cudaMemcpyAsync(b, tmp.p, size_t(59) * N * 4, cudaMemcpyDeviceToDevice, c.stream);
+    }
+    gather_group<1>(c, c.accum.p, tmp.p, perm, N);
+    cudaMemcpyAsync(c.accum.p, tmp.p, size_t(N) * 4, cudaMemcpyDeviceToDevice, c.stream);
+    gather_group<1>(c, c.vcount.p, tmp.p, perm, N);
+    cudaMemcpyAsync(c.vcount.p, tmp.p, size_t(N) * 4, cudaMemcpyDeviceToDevice, c.stream);
+    if (perm_host) cudaMemcpyAsync(perm_host, perm, size_t(N) * 4, cudaMemcpyDeviceToHost, c.stream);
+    const bool ok = cudaStreamSynchronize(c.stream) == cudaSuccess;
+    for (int k = 0; k < 2; ++k) {
+        cudaFree(code[k].p);
+        cudaFree(idx[k].p);
+    }
+    cudaFree(box.p);
+    cudaFree(tmp.p);
+    return ok;
 }
 
 }  // namespace ts

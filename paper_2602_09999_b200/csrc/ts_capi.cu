@@ -639,6 +639,16 @@ ts_status ts_densify(ts_ctx* x, float grad_thresh, float extent, uint64_t seed, 
     return last_launch(c, "densify");
 }
 
+ts_status ts_morton_reorder(ts_ctx* x, uint32_t* perm) {
+    TS_CHECK_CTX(x);
+    Context& c = x->c;
+    CK(cudaSetDevice(c.device));
+    if (c.grad_state == Context::kGradLive) return validation(c, "morton_reorder between backward and optimizer step");
+    if (!launch_morton_reorder(c, perm)) return c.err.empty() ? TS_ERR_CUDA : TS_ERR_OOM;
+    c.view_valid = c.loss_valid = false;
+    return last_launch(c, "morton_reorder");
+}
+
 ts_status ts_set_state(ts_ctx* x, const float* grads, const float* m, const float* v, const float* accum,
                        const float* vcount) {
     TS_CHECK_CTX(x);

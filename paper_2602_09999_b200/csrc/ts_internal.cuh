@@ -115,6 +115,7 @@ void launch_adam(Context& c, const ts_adam_config& a, int64_t begin, int64_t end
 void launch_hwc_to_chw(Context& c, const float* hwc, float* chw, int P);
 void launch_chw_to_hwc(Context& c, const float* chw, float* hwc, int P);
 void launch_opacity_reset(Context& c, float logit_max);
+bool launch_morton_reorder(Context& c, uint32_t* perm_host);
 int64_t launch_densify(Context& c, float grad_thresh, float log_small, float log_big, float logit_min,
                        uint64_t seed, int64_t iter, int64_t stats[3]);
 

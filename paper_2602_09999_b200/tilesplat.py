@@ -66,6 +66,7 @@ _SIGS = {
     "ts_backward_adam": [_vp, _vp, _vp],
     "ts_densify": [_vp, _f, _f, ctypes.c_uint64, _i64, _vp, _vp],
     "ts_opacity_reset": [_vp],
+    "ts_morton_reorder": [_vp, _vp],
     "ts_set_state": [_vp, _vp, _vp, _vp, _vp, _vp],
     "ts_get_state": [_vp, _vp, _vp, _vp, _vp, _vp],
     "ts_debug_preprocess": [_vp, _vp, _vp, _vp, _vp],
@@ -240,6 +241,12 @@ class Engine:
 
     def opacity_reset(self):
         self._check(self._L.ts_opacity_reset(self._h), "ts_opacity_reset")
+
+    def morton_reorder(self):
+        """morton_reorder; returns perm (old index of each new row)."""
+        perm = np.empty(self.num_gaussians(), np.uint32)
+        self._check(self._L.ts_morton_reorder(self._h, _ptr(perm)), "ts_morton_reorder")
+        return perm
 
     # ---- state ----
     def set_state(self, grads=None, m=None, v=None, accum=None, vcount=None):

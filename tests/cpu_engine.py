@@ -62,3 +62,51 @@ class CpuEngine:
 
     def stats_tensors(self):
         return torch.from_numpy(self.acc), torch.from_numpy(self.cnt)
+
+
+class OracleTrainEngine:
+    """Oracle-backed stand-in of the Engine surface the Trainer drives
+    (train_step, densify_and_prune, opacity_reset, morton_reorder, state I/O).
+    TEST INFRASTRUCTURE: deterministic, so checkpoint/resume is checked bitwise."""
+
+    def __init__(self, params, n):
+        self.set_params(params, n)
+
+    def set_params(self, params, n):
+        self.n = n
+        self.P = np.array(params, np.float32)
+        self.M = np.zeros(59 * n, np.float32)
+        self.V = np.zeros(59 * n, np.float32)
+        self.acc = np.zeros(n, np.float32)
+        self.cnt = np.zeros(n, np.float32)
+
+    def num_gaussians(self):
+        return self.n
+
+    def get_params(self):
+        return self.P.copy()
+
+    def get_state(self):
+        return np.zeros(59 * self.n, np.float32), self.M.copy(), self.V.copy(), self.acc.copy(), self.cnt.copy()
+
+    def set_state(self, grads=None, m=None, v=None, accum=None, vcount=None):
+        for name, a in (("M", m), ("V", v), ("acc", accum), ("cnt", vcount)):
+            if a is not None:
+                setattr(self, name, np.array(a, np.float32))
+
+    def train_step(self, cam, cfg, adam, target=None, slot=0, want_loss=True):
+        loss, _ = O.train_step(self.P, self.M, self.V, self.n, cam, cfg, target, adam, self.acc, self.cnt)
+        return loss
+
+    def densify_and_prune(self, grad_thresh, extent, seed, it):
+        P, M, V, na, st = O.densify(self.P, self.M, self.V, self.acc, self.cnt, self.n, grad_thresh, extent, seed, it)
+        self.n, self.P, self.M, self.V = na, P, M, V
+        self.acc = np.zeros(na, np.float32)
+        self.cnt = np.zeros(na, np.float32)
+        return na, (int(st[0]), int(st[1]), int(st[2]))
+
+    def opacity_reset(self):
+        O.lib.tso_opacity_reset(self.n, self.P)
+
+    def morton_reorder(self):
+        return O.morton_reorder(self.P, self.n, self.M, self.V, self.acc, self.cnt)

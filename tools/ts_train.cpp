@@ -81,6 +81,8 @@ int main(int argc, char** argv) {
                 int64_t st[3];
                 e.densify_and_prune(2e-4f, float(extent), 42, it, st);
             }
+            // Morton reindexing while densification is active (cadence scaled 5000 -> 250)
+            if (it > 0 && it % 250 == 0) e.morton_reorder();
         }
         const double secs = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
         std::printf("{\"n_initial\": %lld, \"n_final\": %lld, \"iters\": %d, \"loss_first\": %.6f, "

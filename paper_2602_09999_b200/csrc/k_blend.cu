@@ -103,23 +103,41 @@ __global__ void __launch_bounds__(kT) blend_fwd_kernel(const uint32_t* __restric
                 km &= ~done;
                 if (!km) continue;
                 const float4 col = sC[j];
+                const uint32_t idx1 = base - b + uint32_t(j) + 1u;
+                if (kCompat) {
 #pragma unroll
-                for (int k = 0; k < kPPT; ++k) {
-                    if (!(km & (1u << k))) continue;
-                    const float G = tsx::ex2_approx(Qv[k] * kNegHalfLog2e);
-                    const float al = fminf(0.99f, a.w * G);
-                    const float om = 1.f - al;
-                    if (kCompat && T[k] * om < 1e-4f) {
-                        done |= 1u << k;
-                        continue;
+                    for (int k = 0; k < kPPT; ++k) {
+                        if (!(km & (1u << k))) continue;
+                        const float G = tsx::ex2_approx(Qv[k] * kNegHalfLog2e);
+                        const float al = fminf(0.99f, a.w * G);
+                        const float om = 1.f - al;
+                        if (T[k] * om < 1e-4f) {
+                            done |= 1u << k;
+                            continue;
+                        }
+                        const float w = al * T[k];
+                        C0[k] = fmaf(w, col.x, C0[k]);
+                        C1[k] = fmaf(w, col.y, C1[k]);
+                        C2[k] = fmaf(w, col.z, C2[k]);
+                        T[k] = T[k] * om;
+                        last[k] = idx1;
                     }
-                    const float w = al * T[k];
-                    C0[k] = fmaf(w, col.x, C0[k]);
-                    C1[k] = fmaf(w, col.y, C1[k]);
-                    C2[k] = fmaf(w, col.z, C2[k]);
-                    T[k] = T[k] * om;
-                    last[k] = base - b + uint32_t(j) + 1u;
-                    if (!kCompat && T[k] < 1e-4f) done |= 1u << k;
+                } else {
+                    // branch-free over the 4 pixels: a dropped pixel blends alpha 0, which
+                    // leaves C and T bit-identical (fma(0, c, C) = C, T * 1 = T)
+#pragma unroll
+                    for (int k = 0; k < kPPT; ++k) {
+                        const bool kk = km & (1u << k);
+                        const float G = tsx::ex2_approx(Qv[k] * kNegHalfLog2e);
+                        const float al = kk ? fminf(0.99f, a.w * G) : 0.f;
+                        const float w = al * T[k];
+                        C0[k] = fmaf(w, col.x, C0[k]);
+                        C1[k] = fmaf(w, col.y, C1[k]);
+                        C2[k] = fmaf(w, col.z, C2[k]);
+                        T[k] = T[k] * (1.f - al);
+                        last[k] = kk ? idx1 : last[k];
+                        done |= (T[k] < 1e-4f) ? (1u << k) : 0u;
+                    }
                 }
                 if (done == 0xFu) break;
             }
@@ -218,9 +236,9 @@ __global__ void __launch_bounds__(kT) blend_bwd_kernel(const uint32_t* __restric
     __shared__ float4 sB[kBatch];  // A, 2B, C, ry
     __shared__ float4 sC[kBatch];  // r, g, b
     __shared__ uint32_t sIdx[kBatch];
-    __shared__ float sG[kBatch * kGS];
+    __shared__ __align__(16) float sG[2 * kBatch * kGS];  // per-warp partial gradients
     __shared__ uint32_t s_max;
-    const int lane = threadIdx.x & 31;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int t = blockIdx.x;
     const int tx = t % cam.tiles_x, ty = t / cam.tiles_x;
     const int px = tx * 16 + (threadIdx.x & 15);
@@ -271,8 +289,10 @@ __global__ void __launch_bounds__(kT) blend_bwd_kernel(const uint32_t* __restric
                 sC[r] = s2;
                 sIdx[r] = g;
             }
+            float4* z0 = reinterpret_cast<float4*>(sG + r * kGS);
+            float4* z1 = reinterpret_cast<float4*>(sG + (kBatch + r) * kGS);
 #pragma unroll
-            for (int k = 0; k < kGS; ++k) sG[r * kGS + k] = 0.f;
+            for (int k = 0; k < kGS / 4; ++k) z0[k] = z1[k] = make_float4(0.f, 0.f, 0.f, 0.f);
         }
         __syncthreads();
         const int n = int(tmin<uint32_t>(kBatch, e - base));
@@ -296,32 +316,32 @@ __global__ void __launch_bounds__(kT) blend_bwd_kernel(const uint32_t* __restric
             if (!__any_sync(0xffffffffu, km)) continue;
             const float4 col = sC[j];
             // per-thread sums over its pixels: colour / opacity grads and the three
-            // moments of dL/dQ that give the mean2d and conic grads (dx is shared)
+            // moments of dL/dQ that give the mean2d and conic grads (dx is shared).
+            // Branch-free: a dropped pixel has alpha 0 (w = 0, T and g.U unchanged)
+            // and a zero dL/dalpha mask.
             float vr = 0.f, vg = 0.f, vb = 0.f, vo = 0.f, sq = 0.f, sqy = 0.f, sqyy = 0.f;
 #pragma unroll
             for (int k = 0; k < kPPT; ++k) {
-                if (!(km & (1u << k))) continue;
+                const bool kk = km & (1u << k);
                 const float dy = float(py0 + k) - a.y;
                 const float G = tsx::ex2_approx(Qv[k] * kNegHalfLog2e);
                 const float og = a.w * G;
-                const bool clamped = og > 0.99f;
-                const float al = clamped ? 0.99f : og;
+                const bool lin = kk && og <= 0.99f;  // alpha not clamped: gradient flows
+                const float al = kk ? fminf(og, 0.99f) : 0.f;
                 const float w = al * T[k];
                 const float om = 1.f - al;
                 const float gc = g0[k] * col.x + g1[k] * col.y + g2[k] * col.z;
                 const float after = gU[k] - w * gc;  // g . (colour after this fragment, incl. bg)
-                const float dal = T[k] * gc - after * rcp_approx(om);
+                const float dal = lin ? T[k] * gc - after * rcp_approx(om) : 0.f;
                 vr = fmaf(w, g0[k], vr);
                 vg = fmaf(w, g1[k], vg);
                 vb = fmaf(w, g2[k], vb);
-                if (!clamped) {
-                    vo = fmaf(G, dal, vo);
-                    const float dQ = -0.5f * og * dal;
-                    const float dQy = dQ * dy;
-                    sq += dQ;
-                    sqy += dQy;
-                    sqyy = fmaf(dQy, dy, sqyy);
-                }
+                vo = fmaf(G, dal, vo);
+                const float dQ = -0.5f * og * dal;
+                const float dQy = dQ * dy;
+                sq += dQ;
+                sqy += dQy;
+                sqyy = fmaf(dQy, dy, sqyy);
                 gU[k] = after;
                 T[k] = T[k] * om;
             }
@@ -337,17 +357,19 @@ __global__ void __launch_bounds__(kT) blend_bwd_kernel(const uint32_t* __restric
             v[7] = vg;
             v[8] = vb;
             const float r = red9(v, lane);
-            if (slot >= 0) atomicAdd(&sG[j * kGS + slot], r);
+            if (slot >= 0) sG[(warp * kBatch + j) * kGS + slot] = r;  // per-warp partials: plain stores
         }
         __syncthreads();
 #pragma unroll
         for (int u = 0; u < kBatch / kT; ++u) {
             const int r = threadIdx.x + u * kT;
             if (r < n) {
-                const float* gs = sG + r * kGS;
-                const float4 a0 = make_float4(gs[0], gs[1], gs[2], gs[3]);
-                const float4 a1 = make_float4(gs[4], gs[5], gs[6], gs[7]);
-                const float a2 = gs[8];
+                const float4* g0s = reinterpret_cast<const float4*>(sG + r * kGS);
+                const float4* g1s = reinterpret_cast<const float4*>(sG + (kBatch + r) * kGS);
+                const float4 x0 = g0s[0], x1 = g0s[1], x2 = g0s[2], y0 = g1s[0], y1 = g1s[1], y2 = g1s[2];
+                const float4 a0 = make_float4(x0.x + y0.x, x0.y + y0.y, x0.z + y0.z, x0.w + y0.w);
+                const float4 a1 = make_float4(x1.x + y1.x, x1.y + y1.y, x1.z + y1.z, x1.w + y1.w);
+                const float a2 = x2.x + y2.x;
                 const bool nz = (a0.x != 0.f) | (a0.y != 0.f) | (a0.z != 0.f) | (a0.w != 0.f) | (a1.x != 0.f) |
                                 (a1.y != 0.f) | (a1.z != 0.f) | (a1.w != 0.f) | (a2 != 0.f);
                 if (nz) {

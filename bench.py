@@ -70,6 +70,8 @@ def stage_bytes(st, n, deg, n_tiles):
         "blend_bwd": 8 * n_tiles + 40 * Ip + 32 * P + 36 * V,
         "project_bwd": (140 + 24 * D) * V,
         "adam": 1652 * n,
+        # fused_backward_update: theta, m, v read + written (no gradient buffer), 2D grads, stats
+        "project_bwd_adam": 1416 * n + 52 * V,
     }
 
 
@@ -220,15 +222,28 @@ def run_ours(args):
     dp = DataParallelStep(e, mode=args.dp_mode)
     views = [(cam, cfg, 0)]
     step = 0
+    # auto = the faster single-GPU mode as measured (profiles/): the separate float4 Adam sweep runs at the
+    # HBM roof while the fused kernel is occupancy-bound, so auto picks "fused"
+    fused_bwd = args.adam_mode == "fused_backward"
+    if fused_bwd and world > 1:
+        raise SystemExit("fused_backward needs the full gradient on one rank (world size 1)")
+    mode = T.ADAM_FUSED_BACKWARD if fused_bwd else T.ADAM_FUSED
 
-    def adam_cfg():
+    def adam_cfg(m=None):
         # the gradient buffer is consumed by this step's optimizer; the next backward
         # overwrites every row (no clear pass).  Sharded mode clears explicitly.
-        return T.AdamConfig.make(step=step, extent=1.0, zero_grads=0 if args.dp_mode == "allreduce" else 1)
+        return T.AdamConfig.make(step=step, extent=1.0, mode=mode if m is None else m,
+                                 zero_grads=0 if args.dp_mode == "allreduce" else 1)
+
+    def train_step():
+        if fused_bwd:   # one public C-ABI call: forward, loss, backward with the in-place Adam update
+            e.train_step(cam, cfg, adam_cfg(), slot=0, want_loss=False)
+        else:
+            dp.step(views, adam_cfg())
 
     for _ in range(args.warmup):
         step += 1
-        dp.step(views, adam_cfg())
+        train_step()
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -244,7 +259,7 @@ def run_ours(args):
     ev0.record(stream)
     for _ in range(args.steps):
         step += 1
-        dp.step(views, adam_cfg())
+        train_step()
     ev1.record(stream)
     torch.cuda.synchronize()
     if world > 1:
@@ -259,6 +274,17 @@ def run_ours(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     vstats = e.view_stats()
+    # fused_backward merges K9 and Adam: the raster-only fwd+bwd split comes from a
+    # short profiled loop of the same step with the separate optimizer sweep
+    split_times = stimes
+    if fused_bwd:
+        e.set_profiling(True)
+        for _ in range(min(args.steps, 20)):
+            step += 1
+            dp.step(views, adam_cfg(T.ADAM_FUSED))
+        torch.cuda.synchronize()
+        split_times = e.stage_times()
+        e.set_profiling(False)
 
     # ---- e2e: public C-ABI call with host (pinned) target and loss read-back each step ----
     pin = PinnedBuffer((w.height, w.width, 3))
@@ -289,7 +315,13 @@ def run_ours(args):
     bytes_ = stage_bytes(vstats, n, w.sh_degree, cam.n_tiles)
     avg = {k: (tot / max(1, c)) for k, (tot, c) in stimes.items()}
     calls = {k: c for k, (tot, c) in stimes.items()}
-    fwd_bwd_ms = sum(avg[k] for k in RASTER_STAGES)
+    if fused_bwd:   # the project_bwd stage ran the fused backward + Adam kernel
+        avg["project_bwd_adam"] = avg.pop("project_bwd")
+        calls["project_bwd_adam"] = calls.pop("project_bwd")
+        avg.pop("adam", None)
+        calls.pop("adam", None)
+    split = {k: (tot / max(1, c)) for k, (tot, c) in split_times.items()}
+    fwd_bwd_ms = sum(split[k] for k in RASTER_STAGES)
     R = sum(bytes_[k] for k in RASTER_STAGES)
     peak, peak_kind = hbm_peak()
     dom = max(avg, key=lambda k: avg[k])
@@ -325,16 +357,18 @@ def run_ours(args):
             "config": {"workload": w.name, "gaussians": n, "sh_degree": w.sh_degree,
                        "resolution": f"{w.width}x{w.height}", "views_per_step": world, "views_per_gpu": 1,
                        "parallelism": f"dp{world} (views; NCCL {args.dp_mode} of 59N fp32 grads)",
+                       "optimizer": "fused_backward (SPEC.md:492-500)" if fused_bwd else "fused (SPEC.md:473-480)",
                        "l2": "no flush: per-step working set ~9 GB >> 126 MB L2"},
             "e2e": {"value": world / (e2e_ms * 1e-3), "unit": "steps/s",
                     "h2d_bytes_per_step": int(w.height * w.width * 3 * 4 + 104 + 64),
                     "d2h_bytes_per_step": 16, "api": "ts_train_step (C-ABI) with pinned host target"},
+            "stage_ms_split": {k: round(v, 4) for k, v in split.items()} if fused_bwd else None,
             "gpu_launches": int(launches),
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "algorithmic_bytes_per_launch": int(dom_bytes), "avg_launch_ms": dom_ms,
                          "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})"},
-            "fwd_bwd": {"ms": fwd_bwd_ms, "mpix_s": world * P / (fwd_bwd_ms * 1e-3) / 1e6,
+            "fwd_bwd": {"ms": fwd_bwd_ms, "source": "separate-optimizer profiled loop" if fused_bwd else "timed loop", "mpix_s": world * P / (fwd_bwd_ms * 1e-3) / 1e6,
                         "algorithmic_bytes": int(R), "achieved_gbs": R / (fwd_bwd_ms * 1e-3) / 1e9,
                         "roofline_frac": R / (fwd_bwd_ms * 1e-3) / 1e9 / peak},
             "stage_ms": {k: round(v, 4) for k, v in avg.items()},
@@ -360,6 +394,9 @@ def main():
     ap.add_argument("--workload", default="H", choices=sorted(scene.WORKLOADS))
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
     ap.add_argument("--dp-mode", default="allreduce", choices=("allreduce", "sharded"))
+    ap.add_argument("--adam-mode", default="auto", choices=("auto", "fused", "fused_backward"),
+                    help="optimizer mode (SPEC.md:525): fused = separate fused-Adam sweep (SPEC.md:473-480); "
+                         "fused_backward = Adam inside the backward (SPEC.md:492-500, 1 GPU only)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:

@@ -31,8 +31,8 @@ __device__ __forceinline__ void adam_one(float& th, float& g, float& m, float& v
     m = add(mul(a.b1, m), mul(a.omb1, g));
     v = add(mul(a.b2, v), mul(mul(a.omb2, g), g));
     if (kFused) {
-        const float den = add(mul(sqrt_(v), a.rsb2), a.eps);
-        th = sub(th, div(mul(lr, m), den));
+        const float den = add(mul(sqrt_z(v), a.rsb2), a.eps);
+        th = sub(th, div_zpos(mul(lr, m), den));
     } else {
         const float mh = div(m, a.bc1);
         const float vh = div(v, a.bc2);

@@ -404,7 +404,7 @@ __global__ void __launch_bounds__(kBlock) project_bwd_kernel(const float* __rest
 // ---------------------------------------------------------------------------
 // fused backward + Adam kernel
 // ---------------------------------------------------------------------------
-constexpr int kFB = 64;  // Gaussians per CTA
+constexpr int kFB = 128;  // Gaussians (= threads) per CTA
 
 struct FusedAdam {
     float lr[6];  // lr / (1 - b1^t), per group (host double -> float)
@@ -416,28 +416,40 @@ __device__ __forceinline__ void adam_fused_elem(float& th, float g, float& m, fl
     using namespace tsx;
     m = add(mul(a.b1, m), mul(a.omb1, g));
     v = add(mul(a.b2, v), mul(mul(a.omb2, g), g));
-    const float den = add(mul(sqrt_(v), a.rsb2), a.eps);
-    th = sub(th, div(mul(lr, m), den));
+    const float den = add(mul(sqrt_z(v), a.rsb2), a.eps);
+    th = sub(th, div_zpos(mul(lr, m), den));
 }
 
-// layout: 3 copies (theta, m, v) of the 6 attribute segments, then g2d, stats, SH-rest gradients
+// shared layout (floats): staged parameters (6 attribute segments of the CTA's
+// rows, each with 4 words of alignment room; overwritten in place by the
+// gradient rows), the 2D gradients, the statistics and per-row active flags.
 struct FbLayout {
-    static constexpr int kCopy = 59 * kFB + 24;  // floats per (theta | m | v) copy: 6 segments + 4 pad each
-    static constexpr int kG2 = 3 * kCopy;
+    static constexpr int kP = 0;
+    static constexpr int kG2 = kP + 59 * kFB + 24;
     static constexpr int kAc = kG2 + 12 * kFB + 4;
     static constexpr int kVc = kAc + kFB + 4;
-    static constexpr int kGRest = kVc + kFB + 4;
-    static constexpr int kTotal = kGRest + 45 * kFB;
+    static constexpr int kAct = kVc + kFB + 4;
+    static constexpr int kTotal = kAct + kFB;
 };
 
+// Two phases per CTA of 128 Gaussians:
+//  1. per thread (one Gaussian): the adjoint from the TMA-staged parameter rows;
+//     the 59-float gradient row replaces the staged parameter row in shared
+//     memory (zeros for invisible rows and inactive SH degrees), the 2D
+//     accumulator is cleared, the statistics updated;
+//  2. per CTA: one coalesced sweep over each attribute segment of the CTA's
+//     rows -- g from shared memory, theta (an L2 hit: just staged), m and v
+//     streamed from HBM with 8 independent element groups in flight per thread
+//     -- applying the fused Adam element update and writing theta, m, v back.
+//     The gradient never touches HBM.
 template <int DEG, bool kSkipInvisible>
-__global__ void __launch_bounds__(kFB) project_bwd_adam_kernel(float* __restrict__ P, float* __restrict__ Mo,
-                                                               float* __restrict__ Vo, float4* __restrict__ g2d,
-                                                               const uint32_t* __restrict__ tcount,
-                                                               float* __restrict__ accum,
-                                                               float* __restrict__ vcount, uint8_t* __restrict__ vis,
-                                                               int64_t N, DevCam cam, ts_render_config cfg,
-                                                               FusedAdam fa) {
+__global__ void __launch_bounds__(kFB, 4) project_bwd_adam_kernel(float* __restrict__ P, float* __restrict__ Mo,
+                                                                  float* __restrict__ Vo, float4* __restrict__ g2d,
+                                                                  const uint32_t* __restrict__ tcount,
+                                                                  float* __restrict__ accum,
+                                                                  float* __restrict__ vcount,
+                                                                  uint8_t* __restrict__ vis, int64_t N, DevCam cam,
+                                                                  ts_render_config cfg, FusedAdam fa) {
     extern __shared__ __align__(16) float smem[];
     using L = FbLayout;
     constexpr int width[6] = {3, 3, 4, 1, 3, 45};
@@ -446,72 +458,91 @@ __global__ void __launch_bounds__(kFB) project_bwd_adam_kernel(float* __restrict
     const Off off(N);
     const int64_t goff[6] = {off.means, off.ls, off.q, off.op, off.dc, off.rest};
     const int64_t g0 = int64_t(blockIdx.x) * kFB;
-    const int64_t g = g0 + threadIdx.x;
+    const int tid = threadIdx.x;
+    const int64_t g = g0 + tid;
     const int rows = int(tmin<int64_t>(kFB, N - g0));
     const bool active = g < N && tcount[g] != 0;
     if (kSkipInvisible && !__syncthreads_or(active)) return;
-    int sh[21];
+    int sh[9];
     {
-        Span sp[21];
+        Span sp[9];
 #pragma unroll
-        for (int c = 0; c < 3; ++c) {
-            const float* buf = c == 0 ? P : (c == 1 ? Mo : Vo);
+        for (int s = 0; s < 6; ++s) sp[s] = Span{smem + L::kP + segoff[s], P + goff[s] + width[s] * g0, width[s] * rows};
+        sp[6] = Span{smem + L::kG2, reinterpret_cast<const float*>(g2d + 3 * g0), 12 * rows};
+        sp[7] = Span{smem + L::kAc, accum + g0, rows};
+        sp[8] = Span{smem + L::kVc, vcount + g0, rows};
+        // pull this CTA's Adam moments toward L2 now (bulk prefetch, no shared
+        // memory), so the HBM reads overlap the adjoint phase below
+        if (tid == 0) {
 #pragma unroll
-            for (int s = 0; s < 6; ++s)
-                sp[6 * c + s] = Span{smem + c * L::kCopy + segoff[s], buf + goff[s] + width[s] * g0, width[s] * rows};
+            for (int s = 0; s < 6; ++s) {
+                prefetch_l2(Mo + goff[s] + width[s] * g0, width[s] * rows);
+                prefetch_l2(Vo + goff[s] + width[s] * g0, width[s] * rows);
+            }
         }
-        sp[18] = Span{smem + L::kG2, reinterpret_cast<const float*>(g2d + 3 * g0), 12 * rows};
-        sp[19] = Span{smem + L::kAc, accum + g0, rows};
-        sp[20] = Span{smem + L::kVc, vcount + g0, rows};
         __shared__ unsigned long long bar;
         stage_spans_tma(sp, sh, &bar);
     }
-    const int tid = threadIdx.x;
-#define TS_ROW(c, s) (smem + (c) * L::kCopy + segoff[s] + sh[6 * (c) + (s)] + width[s] * tid)
+    float* act = smem + L::kAct;
     if (tid < rows) {
-        float gs[14];
+        float* pr[6];
 #pragma unroll
-        for (int k = 0; k < 14; ++k) gs[k] = 0.f;
-        float* grest = smem + L::kGRest + tid * 45;
+        for (int s = 0; s < 6; ++s) pr[s] = smem + L::kP + segoff[s] + sh[s] + width[s] * tid;
+        act[tid] = active ? 1.f : 0.f;
+        float gs[14];
         if (active) {
-            const Rows rw{TS_ROW(0, 0), TS_ROW(0, 1), TS_ROW(0, 2), TS_ROW(0, 3)[0], TS_ROW(0, 4), TS_ROW(0, 5),
-                          smem + L::kG2 + sh[18] + 12 * tid};
-            const float nrm = pb_grads<DEG>(rw, grest, cam, cfg, gs);
+            const Rows rw{pr[0], pr[1], pr[2], pr[3][0], pr[4], pr[5], smem + L::kG2 + sh[6] + 12 * tid};
+            // in place: every SH-rest element is read before its gradient is written
+            const float nrm = pb_grads<DEG>(rw, pr[5], cam, cfg, gs);
             reinterpret_cast<float4*>(g2d)[3 * g] = make_float4(0.f, 0.f, 0.f, 0.f);
             reinterpret_cast<float4*>(g2d)[3 * g + 1] = make_float4(0.f, 0.f, 0.f, 0.f);
             reinterpret_cast<float4*>(g2d)[3 * g + 2] = make_float4(0.f, 0.f, 0.f, 0.f);
-            accum[g] = smem[L::kAc + sh[19] + tid] + nrm;
-            vcount[g] = smem[L::kVc + sh[20] + tid] + 1.f;
+            accum[g] = smem[L::kAc + sh[7] + tid] + nrm;
+            vcount[g] = smem[L::kVc + sh[8] + tid] + 1.f;
             vis[g] = 1;
-        }
-        if (active || !kSkipInvisible) {
-            // Adam on the whole 59-float row; inactive rows / inactive SH degrees see g = 0
-            int k = 0;
+        } else {
 #pragma unroll
-            for (int s = 0; s < 5; ++s) {
-                float* th = TS_ROW(0, s);
-                float* m = TS_ROW(1, s);
-                float* v = TS_ROW(2, s);
-#pragma unroll
-                for (int j = 0; j < width[s]; ++j, ++k) adam_fused_elem(th[j], gs[k], m[j], v[j], fa.lr[s], fa);
-            }
-            float* th = TS_ROW(0, 5);
-            float* m = TS_ROW(1, 5);
-            float* v = TS_ROW(2, 5);
-#pragma unroll 5
-            for (int j = 0; j < 45; ++j)
-                adam_fused_elem(th[j], (active && j < nrest) ? grest[j] : 0.f, m[j], v[j], fa.lr[5], fa);
+            for (int k = 0; k < 14; ++k) gs[k] = 0.f;
         }
+        for (int k = active ? nrest : 0; k < 45; ++k) pr[5][k] = 0.f;
+        int k = 0;
+#pragma unroll
+        for (int s = 0; s < 5; ++s)
+#pragma unroll
+            for (int j = 0; j < width[s]; ++j, ++k) pr[s][j] = gs[k];
     }
-#undef TS_ROW
     __syncthreads();
 #pragma unroll
-    for (int c = 0; c < 3; ++c) {
-        float* buf = c == 0 ? P : (c == 1 ? Mo : Vo);
+    for (int s = 0; s < 6; ++s) {
+        constexpr int kU = 12;
+        const int n = width[s] * rows;
+        const float* gr_s = smem + L::kP + segoff[s] + sh[s];
+        float* Pg = P + goff[s] + width[s] * g0;
+        float* Mg = Mo + goff[s] + width[s] * g0;
+        float* Vg = Vo + goff[s] + width[s] * g0;
+        const float lr = fa.lr[s];
+        for (int i0 = tid; i0 < n; i0 += kU * kFB) {
+            float tr[kU], mr[kU], vr[kU];
 #pragma unroll
-        for (int s = 0; s < 6; ++s)
-            store_span<kFB>(buf + goff[s] + width[s] * g0, smem + c * L::kCopy + segoff[s] + sh[6 * c + s],
-                            width[s] * rows);
+            for (int u = 0; u < kU; ++u) {
+                const int i = i0 + u * kFB;
+                if (i < n) {
+                    tr[u] = Pg[i];
+                    mr[u] = Mg[i];
+                    vr[u] = Vg[i];
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < kU; ++u) {
+                const int i = i0 + u * kFB;
+                if (i < n && (!kSkipInvisible || act[i / width[s]] != 0.f)) {
+                    adam_fused_elem(tr[u], gr_s[i], mr[u], vr[u], lr, fa);
+                    Pg[i] = tr[u];
+                    Mg[i] = mr[u];
+                    Vg[i] = vr[u];
+                }
+            }
+        }
     }
 }
 

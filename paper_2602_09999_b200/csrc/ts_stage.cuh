@@ -118,6 +118,15 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
+// bulk L2 prefetch of count floats at src (16-byte granularity; rounded outward,
+// callers' buffers are padded)
+__device__ __forceinline__ void prefetch_l2(const float* src, int count) {
+    if (count <= 0) return;
+    const uintptr_t a = reinterpret_cast<uintptr_t>(src) & ~uintptr_t(15);
+    const uintptr_t e = (reinterpret_cast<uintptr_t>(src + count) + 15) & ~uintptr_t(15);
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a), "r"(uint32_t(e - a)) : "memory");
+}
+
 template <int NS>
 __device__ __forceinline__ void stage_spans_tma(const Span (&sp)[NS], int (&shift)[NS], unsigned long long* bar) {
     uint32_t bytes[NS];

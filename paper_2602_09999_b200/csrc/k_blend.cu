@@ -57,16 +57,26 @@ __global__ void __launch_bounds__(kT) blend_fwd_kernel(const uint32_t* __restric
     const float wy0 = float(ty * 16 + (threadIdx.x >> 5) * 8), wy1 = wy0 + 7.f;
     const uint32_t b = starts[t], e = starts[t + 1];
     const float fpx = float(px);
-    float T[kPPT], C0[kPPT], C1[kPPT], C2[kPPT];
+    // per-pixel state as pixel pairs (rows py0+2h, py0+2h+1) for the packed ops
+    float2 Tp[2], C0p[2], C1p[2], C2p[2];
+    const float2 pyp[2] = {make_float2(float(py0), float(py0 + 1)), make_float2(float(py0 + 2), float(py0 + 3))};
     uint32_t last[kPPT];
     uint32_t done = 0;
 #pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        Tp[h] = make_float2(1.f, 1.f);
+        C0p[h] = C1p[h] = C2p[h] = make_float2(0.f, 0.f);
+    }
+#pragma unroll
     for (int k = 0; k < kPPT; ++k) {
-        T[k] = 1.f;
-        C0[k] = C1[k] = C2[k] = 0.f;
         last[k] = 0;
         if (px >= cam.w || py0 + k >= cam.h) done |= 1u << k;
     }
+    // scalar views of the pair state (constant k after unrolling: stays in registers)
+#define T(k) (((k) & 1) ? Tp[(k) >> 1].y : Tp[(k) >> 1].x)
+#define C0(k) (((k) & 1) ? C0p[(k) >> 1].y : C0p[(k) >> 1].x)
+#define C1(k) (((k) & 1) ? C1p[(k) >> 1].y : C1p[(k) >> 1].x)
+#define C2(k) (((k) & 1) ? C2p[(k) >> 1].y : C2p[(k) >> 1].x)
     if (threadIdx.x == 0) s_max = 0;
     for (uint32_t base = b; base < e; base += kBatch) {
         if (__syncthreads_count(done == 0xFu) == kT) break;
@@ -90,19 +100,23 @@ __global__ void __launch_bounds__(kT) blend_fwd_kernel(const uint32_t* __restric
                 if (a.y + q.w < wy0 || a.y - q.w > wy1) continue;  // splat misses this warp's 8 rows
                 const float dx = tsx::sub(fpx, a.x);
                 const float adx = tsx::mul(q.x, dx);
+                const float4 col = sC[j];
                 // keep mask of the 4 pixels first (exact Q, branch-free), heavy path only on set bits
                 float Qv[kPPT];
                 uint32_t km = 0;
 #pragma unroll
-                for (int k = 0; k < kPPT; ++k) {
-                    const float dy = tsx::sub(float(py0 + k), a.y);
-                    // Q = dx*(A*dx + 2B*dy) + dy*(C*dy), exact order (tsx::conic_q)
-                    Qv[k] = tsx::add(tsx::mul(dx, tsx::add(adx, tsx::mul(q.y, dy))), tsx::mul(dy, tsx::mul(q.z, dy)));
-                    km |= (Qv[k] <= a.z) ? (1u << k) : 0u;
+                for (int h = 0; h < 2; ++h) {
+                    // Q = dx*(A*dx + 2B*dy) + dy*(C*dy), exact order (tsx::conic_q), two rows per op
+                    const float2 dy = tsx::sub2(pyp[h], tsx::dup2(a.y));
+                    const float2 Q = tsx::add2(tsx::mul2(tsx::dup2(dx), tsx::add2(tsx::dup2(adx), tsx::mul2(tsx::dup2(q.y), dy))),
+                                               tsx::mul2(dy, tsx::mul2(tsx::dup2(q.z), dy)));
+                    Qv[2 * h] = Q.x;
+                    Qv[2 * h + 1] = Q.y;
+                    km |= (Q.x <= a.z) ? (1u << (2 * h)) : 0u;
+                    km |= (Q.y <= a.z) ? (2u << (2 * h)) : 0u;
                 }
                 km &= ~done;
                 if (!km) continue;
-                const float4 col = sC[j];
                 const uint32_t idx1 = base - b + uint32_t(j) + 1u;
                 if (kCompat) {
 #pragma unroll
@@ -111,32 +125,39 @@ __global__ void __launch_bounds__(kT) blend_fwd_kernel(const uint32_t* __restric
                         const float G = tsx::ex2_approx(Qv[k] * kNegHalfLog2e);
                         const float al = fminf(0.99f, a.w * G);
                         const float om = 1.f - al;
-                        if (T[k] * om < 1e-4f) {
+                        if (T(k) * om < 1e-4f) {
                             done |= 1u << k;
                             continue;
                         }
-                        const float w = al * T[k];
-                        C0[k] = fmaf(w, col.x, C0[k]);
-                        C1[k] = fmaf(w, col.y, C1[k]);
-                        C2[k] = fmaf(w, col.z, C2[k]);
-                        T[k] = T[k] * om;
+                        const float w = al * T(k);
+                        C0(k) = fmaf(w, col.x, C0(k));
+                        C1(k) = fmaf(w, col.y, C1(k));
+                        C2(k) = fmaf(w, col.z, C2(k));
+                        T(k) = T(k) * om;
                         last[k] = idx1;
                     }
                 } else {
-                    // branch-free over the 4 pixels: a dropped pixel blends alpha 0, which
-                    // leaves C and T bit-identical (fma(0, c, C) = C, T * 1 = T)
+                    // branch-free over the 4 pixels, two pixel pairs in packed fp32x2 ops
+                    // (per lane the same IEEE ops as the scalar form): a dropped pixel
+                    // blends alpha 0, which leaves C and T bit-identical (fma(0, c, C) = C, T * 1 = T)
+                    const float2 cx = tsx::dup2(col.x), cy = tsx::dup2(col.y), cz = tsx::dup2(col.z);
 #pragma unroll
-                    for (int k = 0; k < kPPT; ++k) {
-                        const bool kk = km & (1u << k);
-                        const float G = tsx::ex2_approx(Qv[k] * kNegHalfLog2e);
-                        const float al = kk ? fminf(0.99f, a.w * G) : 0.f;
-                        const float w = al * T[k];
-                        C0[k] = fmaf(w, col.x, C0[k]);
-                        C1[k] = fmaf(w, col.y, C1[k]);
-                        C2[k] = fmaf(w, col.z, C2[k]);
-                        T[k] = T[k] * (1.f - al);
-                        last[k] = kk ? idx1 : last[k];
-                        done |= (T[k] < 1e-4f) ? (1u << k) : 0u;
+                    for (int h = 0; h < 2; ++h) {
+                        const bool k0 = km & (1u << (2 * h)), k1 = km & (2u << (2 * h));
+                        const float2 Qh = make_float2(Qv[2 * h], Qv[2 * h + 1]);
+                        const float2 e = tsx::mul2(Qh, tsx::dup2(kNegHalfLog2e));
+                        const float2 G = make_float2(tsx::ex2_approx(e.x), tsx::ex2_approx(e.y));
+                        const float2 og = tsx::mul2(tsx::dup2(a.w), G);
+                        const float2 al = make_float2(k0 ? fminf(0.99f, og.x) : 0.f, k1 ? fminf(0.99f, og.y) : 0.f);
+                        const float2 w = tsx::mul2(al, Tp[h]);
+                        C0p[h] = tsx::fma2(w, cx, C0p[h]);
+                        C1p[h] = tsx::fma2(w, cy, C1p[h]);
+                        C2p[h] = tsx::fma2(w, cz, C2p[h]);
+                        Tp[h] = tsx::mul2(Tp[h], tsx::sub2(tsx::dup2(1.f), al));
+                        last[2 * h] = k0 ? idx1 : last[2 * h];
+                        last[2 * h + 1] = k1 ? idx1 : last[2 * h + 1];
+                        done |= (Tp[h].x < 1e-4f) ? (1u << (2 * h)) : 0u;
+                        done |= (Tp[h].y < 1e-4f) ? (2u << (2 * h)) : 0u;
                     }
                 }
                 if (done == 0xFu) break;
@@ -150,10 +171,10 @@ __global__ void __launch_bounds__(kT) blend_fwd_kernel(const uint32_t* __restric
         const int py = py0 + k;
         if (px < cam.w && py < cam.h) {
             const int p = py * cam.w + px;
-            rgb[p] = C0[k] + T[k] * cfg.bg[0];
-            rgb[P + p] = C1[k] + T[k] * cfg.bg[1];
-            rgb[2 * P + p] = C2[k] + T[k] * cfg.bg[2];
-            Tfin[p] = T[k];
+            rgb[p] = C0(k) + T(k) * cfg.bg[0];
+            rgb[P + p] = C1(k) + T(k) * cfg.bg[1];
+            rgb[2 * P + p] = C2(k) + T(k) * cfg.bg[2];
+            Tfin[p] = T(k);
             pcount[p] = last[k];
         }
         mymax = max(mymax, last[k]);
@@ -165,6 +186,10 @@ __global__ void __launch_bounds__(kT) blend_fwd_kernel(const uint32_t* __restric
     __syncthreads();
     if (threadIdx.x == 0 && s_max) atomicAdd(ip_counter, s_max);
 }
+#undef T
+#undef C0
+#undef C1
+#undef C2
 
 // Transposed warp reduction of 9 values: after 5 xor-shuffle steps each even
 // lane holds the warp sum of value `slot` (9 distinct slots over the warp).
@@ -249,22 +274,28 @@ __global__ void __launch_bounds__(kT) blend_bwd_kernel(const uint32_t* __restric
     // per pixel: upstream gradient g, T, count, and gU = g . U where U = C_final - prefix
     // (the colour still to come after the current fragment, incl. background).  Only
     // g . U enters the gradient and it updates as gU -= w (g . c), so one scalar suffices.
-    float g0[kPPT], g1[kPPT], g2[kPPT], gU[kPPT], T[kPPT];
+    // per-pixel state as pixel pairs (rows py0+2h, py0+2h+1) for the packed fp32x2 ops
+    float2 g0p[2], g1p[2], g2p[2], gUp[2], Tp[2];
+    const float2 pyp[2] = {make_float2(float(py0), float(py0 + 1)), make_float2(float(py0 + 2), float(py0 + 3))};
     uint32_t cnt[kPPT];
     uint32_t mymax = 0;
 #pragma unroll
     for (int k = 0; k < kPPT; ++k) {
         const int py = py0 + k;
-        T[k] = 1.f;
-        g0[k] = g1[k] = g2[k] = gU[k] = 0.f;
+        float a0 = 0.f, a1 = 0.f, a2 = 0.f, u = 0.f;
         cnt[k] = 0;
         if (px < cam.w && py < cam.h) {
             const int p = py * cam.w + px;
-            g0[k] = dLdC[p];
-            g1[k] = dLdC[P + p];
-            g2[k] = dLdC[2 * P + p];
-            gU[k] = g0[k] * rgb[p] + g1[k] * rgb[P + p] + g2[k] * rgb[2 * P + p];
+            a0 = dLdC[p];
+            a1 = dLdC[P + p];
+            a2 = dLdC[2 * P + p];
+            u = a0 * rgb[p] + a1 * rgb[P + p] + a2 * rgb[2 * P + p];
             cnt[k] = pcount[p];
+        }
+        if (k & 1) {
+            g0p[k >> 1].y = a0, g1p[k >> 1].y = a1, g2p[k >> 1].y = a2, gUp[k >> 1].y = u, Tp[k >> 1].y = 1.f;
+        } else {
+            g0p[k >> 1].x = a0, g1p[k >> 1].x = a1, g2p[k >> 1].x = a2, gUp[k >> 1].x = u, Tp[k >> 1].x = 1.f;
         }
         mymax = max(mymax, cnt[k]);
     }
@@ -305,46 +336,55 @@ __global__ void __launch_bounds__(kT) blend_bwd_kernel(const uint32_t* __restric
             const float adx = tsx::mul(q.x, dx);
             const uint32_t li = local0 + uint32_t(j);
             // keep mask of the 4 pixels first (exact Q); the warp skips the fragment if no lane keeps it
-            float Qv[kPPT];
+            float2 Qp[2], dyp[2];
             uint32_t km = 0;
 #pragma unroll
-            for (int k = 0; k < kPPT; ++k) {
-                const float dy = tsx::sub(float(py0 + k), a.y);
-                Qv[k] = tsx::add(tsx::mul(dx, tsx::add(adx, tsx::mul(q.y, dy))), tsx::mul(dy, tsx::mul(q.z, dy)));
-                km |= (li < cnt[k] && Qv[k] <= a.z) ? (1u << k) : 0u;
+            for (int h = 0; h < 2; ++h) {
+                dyp[h] = tsx::sub2(pyp[h], tsx::dup2(a.y));
+                Qp[h] = tsx::add2(tsx::mul2(tsx::dup2(dx), tsx::add2(tsx::dup2(adx), tsx::mul2(tsx::dup2(q.y), dyp[h]))),
+                                  tsx::mul2(dyp[h], tsx::mul2(tsx::dup2(q.z), dyp[h])));
+                km |= (li < cnt[2 * h] && Qp[h].x <= a.z) ? (1u << (2 * h)) : 0u;
+                km |= (li < cnt[2 * h + 1] && Qp[h].y <= a.z) ? (2u << (2 * h)) : 0u;
             }
             if (!__any_sync(0xffffffffu, km)) continue;
             const float4 col = sC[j];
-            // per-thread sums over its pixels: colour / opacity grads and the three
-            // moments of dL/dQ that give the mean2d and conic grads (dx is shared).
-            // Branch-free: a dropped pixel has alpha 0 (w = 0, T and g.U unchanged)
-            // and a zero dL/dalpha mask.
-            float vr = 0.f, vg = 0.f, vb = 0.f, vo = 0.f, sq = 0.f, sqy = 0.f, sqyy = 0.f;
+            const float2 ncx = tsx::dup2(-col.x), ncy = tsx::dup2(-col.y), ncz = tsx::dup2(-col.z);
+            // per-thread sums over its pixels (pairs, folded at the end): colour / opacity
+            // grads and the three moments of dL/dQ that give the mean2d and conic grads
+            // (dx is shared).  Branch-free: a dropped pixel has alpha 0 (w = 0, T and g.U
+            // unchanged) and a zero dL/dalpha mask.  ng* = negated quantities (ngc = -g.c,
+            // ndal = -dL/dalpha) so every update is one FFMA2.
+            float2 vr2 = make_float2(0.f, 0.f), vg2 = vr2, vb2 = vr2, nvo2 = vr2, sq2 = vr2, sqy2 = vr2, sqyy2 = vr2;
 #pragma unroll
-            for (int k = 0; k < kPPT; ++k) {
-                const bool kk = km & (1u << k);
-                const float dy = float(py0 + k) - a.y;
-                const float G = tsx::ex2_approx(Qv[k] * kNegHalfLog2e);
-                const float og = a.w * G;
-                const bool lin = kk && og <= 0.99f;  // alpha not clamped: gradient flows
-                const float al = kk ? fminf(og, 0.99f) : 0.f;
-                const float w = al * T[k];
-                const float om = 1.f - al;
-                const float gc = g0[k] * col.x + g1[k] * col.y + g2[k] * col.z;
-                const float after = gU[k] - w * gc;  // g . (colour after this fragment, incl. bg)
-                const float dal = lin ? T[k] * gc - after * rcp_approx(om) : 0.f;
-                vr = fmaf(w, g0[k], vr);
-                vg = fmaf(w, g1[k], vg);
-                vb = fmaf(w, g2[k], vb);
-                vo = fmaf(G, dal, vo);
-                const float dQ = -0.5f * og * dal;
-                const float dQy = dQ * dy;
-                sq += dQ;
-                sqy += dQy;
-                sqyy = fmaf(dQy, dy, sqyy);
-                gU[k] = after;
-                T[k] = T[k] * om;
+            for (int h = 0; h < 2; ++h) {
+                const bool k0 = km & (1u << (2 * h)), k1 = km & (2u << (2 * h));
+                const float2 e = tsx::mul2(Qp[h], tsx::dup2(kNegHalfLog2e));
+                const float2 G = make_float2(tsx::ex2_approx(e.x), tsx::ex2_approx(e.y));
+                const float2 og = tsx::mul2(tsx::dup2(a.w), G);
+                const bool l0 = k0 && og.x <= 0.99f, l1 = k1 && og.y <= 0.99f;  // alpha not clamped: gradient flows
+                const float2 al = make_float2(k0 ? fminf(og.x, 0.99f) : 0.f, k1 ? fminf(og.y, 0.99f) : 0.f);
+                const float2 w = tsx::mul2(al, Tp[h]);
+                const float2 om = tsx::sub2(tsx::dup2(1.f), al);
+                const float2 ngc = tsx::fma2(g2p[h], ncz, tsx::fma2(g1p[h], ncy, tsx::mul2(g0p[h], ncx)));
+                const float2 after = tsx::fma2(w, ngc, gUp[h]);  // g . (colour after this fragment, incl. bg)
+                const float2 r = make_float2(rcp_approx(om.x), rcp_approx(om.y));
+                float2 ndal = tsx::fma2(Tp[h], ngc, tsx::mul2(after, r));
+                ndal.x = l0 ? ndal.x : 0.f;
+                ndal.y = l1 ? ndal.y : 0.f;
+                vr2 = tsx::fma2(w, g0p[h], vr2);
+                vg2 = tsx::fma2(w, g1p[h], vg2);
+                vb2 = tsx::fma2(w, g2p[h], vb2);
+                nvo2 = tsx::fma2(G, ndal, nvo2);
+                const float2 dQ = tsx::mul2(tsx::mul2(tsx::dup2(0.5f), og), ndal);
+                const float2 dQy = tsx::mul2(dQ, dyp[h]);
+                sq2 = tsx::add2(sq2, dQ);
+                sqy2 = tsx::add2(sqy2, dQy);
+                sqyy2 = tsx::fma2(dQy, dyp[h], sqyy2);
+                gUp[h] = after;
+                Tp[h] = tsx::mul2(Tp[h], om);
             }
+            const float vr = vr2.x + vr2.y, vg = vg2.x + vg2.y, vb = vb2.x + vb2.y, vo = -(nvo2.x + nvo2.y);
+            const float sq = sq2.x + sq2.y, sqy = sqy2.x + sqy2.y, sqyy = sqyy2.x + sqyy2.y;
             // dQ/dmx = -(2A dx + 2B dy), dQ/dmy = -(2B dx + 2C dy), dQ/dA = dx^2, dQ/dB = 2 dx dy, dQ/dC = dy^2
             float v[9];
             v[0] = -(2.f * adx * sq + q.y * sqy);

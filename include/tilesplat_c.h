@@ -145,6 +145,12 @@ ts_status ts_set_state(ts_ctx* ctx, const float* grads, const float* m, const fl
                        const float* vcount); /* each may be NULL */
 ts_status ts_get_state(ts_ctx* ctx, float* grads, float* m, float* v, float* accum, float* vcount);
 
+/* ---- binning path: 0 auto = bucketed binning + per-tile sort, falling back to
+ * the two-stage radix sort (depth sort over N, tile sort over I) when a tile list exceeds the
+ * per-tile sort capacity; 1 = always the radix path.  Both give bit-identical tile lists. ---- */
+ts_status ts_set_binning(ts_ctx* ctx, int32_t mode);
+ts_status ts_binning_path(ts_ctx* ctx, int32_t* radix /* 1 if the last forward used the radix path */);
+
 /* ---- parity / debug hooks (bit-exact contract) ---- */
 ts_status ts_debug_preprocess(ts_ctx* ctx, float* splat12 /* N*12 */, int32_t* rect4 /* N*4 */,
                               uint32_t* tile_count /* N */, uint32_t* depth_key /* N */);

@@ -1,0 +1,404 @@
+// Binning without a global instance sort (default path).
+//
+// The reference order of the tile lists is the stable sort of the Gaussian-major
+// instance list on the 64-bit key (tile << 32 | depth key):
+// within a tile, instances ordered by (depth key, Gaussian index).  That order
+// is produced here by bucketing followed by a small per-tile sort, instead of
+// a depth sort over N plus a radix sort over I:
+//
+//   KB1 bin_hist    chunk CTA (8192 Gaussians): per-tile instance counts of the
+//                   chunk in a shared histogram (the K1 kept-tile masks, or the
+//                   exact cull for rects of more than 64 tiles) -> H[chunk][tile];
+//   KB2 bin_colscan per tile: exclusive prefix of H over chunks, tile totals and
+//                   the maximum list length; the exclusive scan of the totals is
+//                   the tile ranges (starts) and I;
+//   KB3 bin_scatter chunk CTA: shared cursors = starts + H[chunk]; every kept
+//                   (Gaussian, tile) pair claims a slot of its tile's list with a
+//                   shared-memory atomic (order within a chunk arbitrary);
+//   KB4 tile_sort   CTA per tile: (depth key, Gaussian) pairs of the list sorted
+//                   in shared memory -- one bucketing pass on the key interpolated
+//                   between the list's min and max (buckets are monotone in the key),
+//                   then each small bucket insertion-sorted on (key, index) -- and
+//                   written back in order.
+// Integer work only; the result is bit-identical to the two-stage radix path
+// (k_sort.cu), which remains the fallback for lists longer than kSortCap.
+#include "ts_internal.cuh"
+#include "ts_math.cuh"
+
+#include <algorithm>
+
+namespace ts {
+namespace {
+
+constexpr int kChunk = 8192;      // Gaussians per chunk CTA (= kBinThreads * kPre)
+constexpr int kBinThreads = 512;  // threads of the chunk kernels
+constexpr int kPre = 16;         // rects per thread, all loaded before the expansion
+
+// next kept tile after tile `prev` (-1: first) of a rect with more than 64 tiles; -1 when done
+__device__ __noinline__ int big_rect_next(const float4* __restrict__ splat, uint32_t g, int tx0, int tx1, int ty0,
+                                          int ty1, int W, int H, int tiles_x, int cull_mode, int prev) {
+    const float4 s0 = splat[3 * g], s1 = splat[3 * g + 1];
+    const float nBA = tsx::div(-s1.y, s1.x), nBC = tsx::div(-s1.y, s1.z);
+    int tx = tx0, ty = ty0;
+    if (prev >= 0) {
+        ty = prev / tiles_x;
+        tx = prev - ty * tiles_x + 1;
+        if (tx > tx1) {
+            tx = tx0;
+            ++ty;
+        }
+    }
+    for (; ty <= ty1; ++ty, tx = tx0)
+        for (; tx <= tx1; ++tx)
+            if (cull_mode == 0 || tsx::tile_keep(s0.x, s0.y, s1.x, s1.y, s1.z, s0.z, nBA, nBC, tx, ty, W, H))
+                return ty * tiles_x + tx;
+    return -1;
+}
+
+// kept tiles of one Gaussian (K1's rect + 64-bit mask; exact cull for big rects)
+template <class F>
+__device__ __forceinline__ void for_each_tile(const uint4 rc, const float4* __restrict__ splat, uint32_t g, int W,
+                                              int H, int tiles_x, int cull_mode, F&& f) {
+    const int tx0 = rc.x & 0xFFFF, tx1 = (rc.x >> 16) & 0x7FFF, ty0 = rc.y & 0xFFFF, ty1 = (rc.y >> 16) & 0x7FFF;
+    if (tx0 > tx1 || ty0 > ty1) return;
+    if (!(rc.y & 0x80000000u)) {
+        const int wdt = tx1 - tx0 + 1;
+        uint64_t m = (uint64_t(rc.w) << 32) | rc.z;
+        while (m) {
+            const int bit = __ffsll((long long)m) - 1;
+            m &= m - 1;
+            const int dy = bit / wdt;
+            f((ty0 + dy) * tiles_x + tx0 + (bit - dy * wdt));
+        }
+        return;
+    }
+    // rect of more than 64 tiles (rare): exact cull per tile, one tile at a time
+    for (int t = -1; (t = big_rect_next(splat, g, tx0, tx1, ty0, ty1, W, H, tiles_x, cull_mode, t)) >= 0;) f(t);
+}
+
+// Kept (Gaussian, tile) pairs of one Gaussian per lane (rects prefetched by the caller).
+template <class F>
+__device__ __forceinline__ void warp_expand(const uint4 rc, uint32_t g, bool valid, const float4* __restrict__ splat,
+                                            int W, int H, int tiles_x, int cull_mode, F&& f) {
+    const int tx0 = rc.x & 0xFFFF, tx1 = (rc.x >> 16) & 0x7FFF, ty0 = rc.y & 0xFFFF, ty1 = (rc.y >> 16) & 0x7FFF;
+    const bool nonempty = valid && tx0 <= tx1 && ty0 <= ty1;
+    if (!nonempty) return;
+    if (!(rc.y & 0x80000000u)) {
+        // kept tiles = set bits of the mask over the rect (row-major); lanes run in lockstep
+        const int wdt = tx1 - tx0 + 1;
+        const float iw = 1.f / float(wdt);
+        uint64_t m = (uint64_t(rc.w) << 32) | rc.z;
+        while (m) {
+            const int bit = __ffsll((long long)m) - 1;
+            m &= m - 1;
+            const int dy = int((float(bit) + 0.5f) * iw);  // exact floor(bit / wdt) for bit < 64
+            f((ty0 + dy) * tiles_x + tx0 + (bit - dy * wdt), g);
+        }
+        return;
+    }
+    // rect of more than 64 tiles (rare): exact cull per tile, one tile at a time
+    for (int t = -1; (t = big_rect_next(splat, g, tx0, tx1, ty0, ty1, W, H, tiles_x, cull_mode, t)) >= 0;) f(t, g);
+}
+
+__global__ void __launch_bounds__(kBinThreads) bin_hist_kernel(const uint4* __restrict__ rect,
+                                                               const float4* __restrict__ splat, int64_t N, int W,
+                                                               int H, int tiles_x, int Tn, int cull_mode,
+                                                               uint32_t* __restrict__ Hm) {
+    extern __shared__ uint32_t hist[];
+    for (int t = threadIdx.x; t < Tn; t += kBinThreads) hist[t] = 0;
+    __syncthreads();
+    const int64_t g0 = int64_t(blockIdx.x) * kChunk;
+    uint4 rc[kPre];
+#pragma unroll
+    for (int u = 0; u < kPre; ++u) {
+        const int64_t g = g0 + threadIdx.x + u * kBinThreads;
+        rc[u] = g < N ? __ldg(rect + g) : make_uint4(1u, 1u, 0u, 0u);
+    }
+#pragma unroll 1
+    for (int u = 0; u < kPre; ++u) {
+        const int64_t g = g0 + threadIdx.x + u * kBinThreads;
+        warp_expand(rc[u], uint32_t(g), g < N, splat, W, H, tiles_x, cull_mode,
+                    [&](int t, uint32_t) { atomicAdd(&hist[t], 1u); });
+    }
+    __syncthreads();
+    uint32_t* row = Hm + size_t(blockIdx.x) * Tn;
+    for (int t = threadIdx.x; t < Tn; t += kBinThreads) row[t] = hist[t];
+}
+
+// per-tile sort size classes: list lengths in [2, kCap0], (kCap0, kCap1], (kCap1, kCap2];
+// lists of one instance are copied; longer lists send the view to the radix path
+constexpr int kCap0 = 1024, kCap1 = 4096, kCap2 = 8192, kCap3 = 16384;
+
+// per tile: exclusive prefix over chunks (in place), total, running max, and the
+// tile appended to the work list of its sort size class (meta[0..4] = class counts,
+// meta[5] = max length; lists at cls + c * Tn)
+__global__ void __launch_bounds__(64) bin_colscan_kernel(uint32_t* __restrict__ Hm, int nchunks, int Tn,
+                                                         uint32_t* __restrict__ tot, uint32_t* __restrict__ meta,
+                                                         uint32_t* __restrict__ cls) {
+    const int t = blockIdx.x * 64 + threadIdx.x;
+    uint32_t run = 0;
+    if (t < Tn) {
+        constexpr int U = 32;
+        for (int c0 = 0; c0 < nchunks; c0 += U) {
+            uint32_t h[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) h[u] = c0 + u < nchunks ? Hm[size_t(c0 + u) * Tn + t] : 0u;
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+                if (c0 + u < nchunks) {
+                    Hm[size_t(c0 + u) * Tn + t] = run;
+                    run += h[u];
+                }
+        }
+        tot[t] = run;
+        const int k = run == 1 ? 0 : run <= uint32_t(kCap0) ? 1 : run <= uint32_t(kCap1) ? 2 : run <= uint32_t(kCap2) ? 3 : 4;
+        if (run > 0 && run <= uint32_t(kCap3)) cls[size_t(k) * Tn + atomicAdd(&meta[k], 1u)] = uint32_t(t);
+    }
+    const uint32_t wm = __reduce_max_sync(0xffffffffu, run);
+    if ((threadIdx.x & 31) == 0 && wm) atomicMax(&meta[5], wm);
+}
+
+__global__ void __launch_bounds__(kBinThreads) bin_scatter_kernel(const uint4* __restrict__ rect,
+                                                                  const float4* __restrict__ splat, int64_t N, int W,
+                                                                  int H, int tiles_x, int Tn, int cull_mode,
+                                                                  const uint32_t* __restrict__ Hm,
+                                                                  const uint32_t* __restrict__ starts,
+                                                                  uint32_t* __restrict__ out) {
+    extern __shared__ uint32_t cur[];
+    const uint32_t* row = Hm + size_t(blockIdx.x) * Tn;
+    for (int t = threadIdx.x; t < Tn; t += kBinThreads) cur[t] = starts[t] + row[t];
+    const int64_t g0 = int64_t(blockIdx.x) * kChunk;
+    uint4 rc[kPre];
+#pragma unroll
+    for (int u = 0; u < kPre; ++u) {
+        const int64_t g = g0 + threadIdx.x + u * kBinThreads;
+        rc[u] = g < N ? __ldg(rect + g) : make_uint4(1u, 1u, 0u, 0u);
+    }
+    __syncthreads();
+#pragma unroll 1
+    for (int u = 0; u < kPre; ++u) {
+        const int64_t g = g0 + threadIdx.x + u * kBinThreads;
+        warp_expand(rc[u], uint32_t(g), g < N, splat, W, H, tiles_x, cull_mode,
+                    [&](int t, uint32_t gg) { out[atomicAdd(&cur[t], 1u)] = gg; });
+    }
+}
+
+// ---------------------------------------------------------------------------
+// KB4 per-tile sort on (depth key, Gaussian index)
+// ---------------------------------------------------------------------------
+// shared layout: bucketed keys/indices (CAP each) + bucket counters (CAP/2 + 1);
+// the list itself is staged in registers (CAP / NT per thread)
+constexpr size_t tile_sort_smem(int cap) { return size_t(cap) * 8 + (size_t(cap) / 2 + 1) * 4; }
+
+template <int CAP, int NT>
+__global__ void __launch_bounds__(NT) tile_sort_kernel(const uint32_t* __restrict__ starts,
+                                                       const uint32_t* __restrict__ in,
+                                                       const uint32_t* __restrict__ dkey, uint32_t* __restrict__ out,
+                                                       const uint32_t* __restrict__ tiles) {
+    constexpr int R = CAP / NT;
+    constexpr int NB = CAP / 2;  // bucket counters (buckets = L/2)
+    extern __shared__ uint32_t sm[];
+    uint32_t* skey = sm;
+    uint32_t* sgid = sm + CAP;
+    uint32_t* cnt = sm + 2 * CAP;
+    __shared__ uint32_t s_min, s_max;
+    __shared__ uint32_t s_wsum[32];
+    const uint32_t t = tiles[blockIdx.x];
+    const uint32_t b = starts[t];
+    const int L = int(starts[t + 1] - b);
+    const int tid = threadIdx.x;
+    if (tid == 0) {
+        s_min = 0xFFFFFFFFu;
+        s_max = 0u;
+    }
+    const int nbk = max(1, min(NB, L / 2));
+    for (int i = tid; i <= nbk; i += NT) cnt[i] = 0;
+    uint32_t gg[R], kk[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const int i = tid + r * NT;
+        gg[r] = i < L ? __ldg(in + b + i) : 0u;
+    }
+    uint32_t mn = 0xFFFFFFFFu, mx = 0u;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const int i = tid + r * NT;
+        kk[r] = i < L ? __ldg(dkey + gg[r]) : 0u;
+        if (i < L) {
+            mn = min(mn, kk[r]);
+            mx = max(mx, kk[r]);
+        }
+    }
+    mn = __reduce_min_sync(0xffffffffu, mn);
+    mx = __reduce_max_sync(0xffffffffu, mx);
+    __syncthreads();
+    if ((tid & 31) == 0) {
+        atomicMin(&s_min, mn);
+        atomicMax(&s_max, mx);
+    }
+    __syncthreads();
+    const uint32_t kmin = s_min;
+    // bucket = floor(float(key - kmin) * scale): monotone non-decreasing in the key
+    const float scale = float(nbk) / (float(s_max - kmin) + 1.0f);
+    uint32_t bk[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const int i = tid + r * NT;
+        bk[r] = min(uint32_t(nbk - 1), uint32_t(float(kk[r] - kmin) * scale));
+        if (i < L) atomicAdd(&cnt[bk[r]], 1u);
+    }
+    __syncthreads();
+    // exclusive scan of the bucket counts: every thread a contiguous segment, block scan of the sums
+    {
+        const int per = (nbk + NT - 1) / NT;
+        const int s0 = min(nbk, tid * per), s1 = min(nbk, s0 + per);
+        uint32_t run = 0;
+        for (int i = s0; i < s1; ++i) run += cnt[i];
+        const int lane = tid & 31, wid = tid >> 5;
+        uint32_t inc = run;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t v = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += v;
+        }
+        if (lane == 31) s_wsum[wid] = inc;
+        __syncthreads();
+        if (wid == 0) {
+            uint32_t w = lane < NT / 32 ? s_wsum[lane] : 0u;
+            uint32_t wi = w;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t v = __shfl_up_sync(0xffffffffu, wi, o);
+                if (lane >= o) wi += v;
+            }
+            if (lane < NT / 32) s_wsum[lane] = wi - w;
+        }
+        __syncthreads();
+        uint32_t acc = inc - run + s_wsum[wid];
+        for (int i = s0; i < s1; ++i) {
+            const uint32_t c = cnt[i];
+            cnt[i] = acc;
+            acc += c;
+        }
+    }
+    __syncthreads();
+    // scatter into buckets (order inside a bucket arbitrary); cnt[i] ends as the end of bucket i
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const int i = tid + r * NT;
+        if (i < L) {
+            const uint32_t p = atomicAdd(&cnt[bk[r]], 1u);
+            skey[p] = kk[r];
+            sgid[p] = gg[r];
+        }
+    }
+    __syncthreads();
+    // insertion sort of every bucket on (key, index); bucket i = [end(i-1), end(i))
+    for (int bi = tid; bi < nbk; bi += NT) {
+        const int e = int(cnt[bi]);
+        const int s = bi == 0 ? 0 : int(cnt[bi - 1]);
+        for (int i = s + 1; i < e; ++i) {
+            const uint32_t k = skey[i], g = sgid[i];
+            int j = i - 1;
+            while (j >= s && (skey[j] > k || (skey[j] == k && sgid[j] > g))) {
+                skey[j + 1] = skey[j];
+                sgid[j + 1] = sgid[j];
+                --j;
+            }
+            skey[j + 1] = k;
+            sgid[j + 1] = g;
+        }
+    }
+    __syncthreads();
+    for (int i = tid; i < L; i += NT) out[b + i] = sgid[i];
+}
+
+// lists of one instance need no sort: copy
+__global__ void tile_copy_single_kernel(const uint32_t* __restrict__ starts, const uint32_t* __restrict__ in,
+                                        uint32_t* __restrict__ out, const uint32_t* __restrict__ tiles, int n) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const uint32_t b = starts[tiles[i]];
+    out[b] = in[b];
+}
+
+}  // namespace
+
+int bin_sort_cap() { return kCap3; }
+
+bool bin_supported(int Tn) { return size_t(Tn) * 4 <= 200 * 1024; }
+
+int64_t launch_bin_count(Context& c, const DevCam& cam, const ts_render_config& cfg, uint32_t* max_len) {
+    const int Tn = cam.tiles_x * cam.tiles_y;
+    const int nch = int(std::max<int64_t>(1, (c.N + kChunk - 1) / kChunk));
+    // bintot: [0, Tn) totals | meta (8) | class lists 5 * Tn
+    if (!ensure(c, c.binH, size_t(nch) * Tn) || !ensure(c, c.bintot, size_t(Tn) * 6 + 8)) return -1;
+    const size_t sm = size_t(Tn) * 4;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(bin_hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        cudaFuncSetAttribute(bin_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        attr = true;
+    }
+    uint32_t* meta = c.bintot.p + Tn;
+    uint32_t* cls = meta + 8;
+    cudaMemsetAsync(meta, 0, 8 * 4, c.stream);
+    if (c.N > 0) {
+        bin_hist_kernel<<<nch, kBinThreads, sm, c.stream>>>(c.rect.p, c.splat.p, c.N, cam.w, cam.h, cam.tiles_x, Tn,
+                                                             cfg.cull_mode, c.binH.p);
+        TS_LAUNCHED(c);
+        bin_colscan_kernel<<<(Tn + 63) / 64, 64, 0, c.stream>>>(c.binH.p, nch, Tn, c.bintot.p, meta, cls);
+        TS_LAUNCHED(c);
+    } else {
+        cudaMemsetAsync(c.bintot.p, 0, size_t(Tn) * 4, c.stream);
+    }
+    launch_exclusive_scan(c, c.bintot.p, nullptr, c.starts.p, Tn);
+    uint32_t hv[7] = {0, 0, 0, 0, 0, 0, 0};
+    cudaMemcpyAsync(&hv[0], c.starts.p + Tn, 4, cudaMemcpyDeviceToHost, c.stream);
+    cudaMemcpyAsync(&hv[1], meta, 6 * 4, cudaMemcpyDeviceToHost, c.stream);
+    cudaStreamSynchronize(c.stream);
+    for (int k = 0; k < 5; ++k) c.bin_class[k] = hv[1 + k];
+    *max_len = hv[6];
+    return int64_t(hv[0]);
+}
+
+void launch_bin_scatter(Context& c, const DevCam& cam, const ts_render_config& cfg) {
+    const int Tn = cam.tiles_x * cam.tiles_y;
+    if (c.N == 0 || c.I == 0) return;
+    const int nch = int((c.N + kChunk - 1) / kChunk);
+    bin_scatter_kernel<<<nch, kBinThreads, size_t(Tn) * 4, c.stream>>>(c.rect.p, c.splat.p, c.N, cam.w, cam.h,
+                                                                       cam.tiles_x, Tn, cfg.cull_mode, c.binH.p,
+                                                                       c.starts.p, c.ival[1].p);
+    TS_LAUNCHED(c);
+}
+
+template <int CAP, int NT>
+static void sort_variant(Context& c, const uint32_t* tiles, uint32_t n) {
+    if (!n) return;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(tile_sort_kernel<CAP, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             int(tile_sort_smem(CAP)));
+        attr = true;
+    }
+    tile_sort_kernel<CAP, NT><<<n, NT, tile_sort_smem(CAP), c.stream>>>(c.starts.p, c.ival[1].p, c.dkey[0].p,
+                                                                       c.ival[0].p, tiles);
+    TS_LAUNCHED(c);
+}
+
+void launch_tile_depth_sort(Context& c, int Tn, uint32_t max_len) {
+    (void)max_len;
+    if (c.I == 0) return;
+    const uint32_t* cls = c.bintot.p + Tn + 8;
+    if (c.bin_class[0]) {
+        tile_copy_single_kernel<<<(c.bin_class[0] + 255) / 256, 256, 0, c.stream>>>(c.starts.p, c.ival[1].p,
+                                                                                  c.ival[0].p, cls, int(c.bin_class[0]));
+        TS_LAUNCHED(c);
+    }
+    sort_variant<kCap0, 256>(c, cls + size_t(1) * Tn, c.bin_class[1]);
+    sort_variant<kCap1, 512>(c, cls + size_t(2) * Tn, c.bin_class[2]);
+    sort_variant<kCap2, 512>(c, cls + size_t(3) * Tn, c.bin_class[3]);
+    sort_variant<kCap3, 1024>(c, cls + size_t(4) * Tn, c.bin_class[4]);
+}
+
+}  // namespace ts

@@ -193,33 +193,60 @@ ts_status run_forward(Context& c, const ts_camera& cam, const ts_render_config& 
     stage_begin(c, 0);
     launch_preprocess(c, dc, cfg);
     stage_end(c, 0);
-    stage_begin(c, 1);
-    launch_depth_sort(c);
-    stage_end(c, 1);
-    stage_begin(c, 2);
-    const int64_t I = launch_scan_counts(c);
-    stage_end(c, 2);
-    if (ts_status s = last_launch(c, "preprocess/sort/scan"); s != TS_OK) return s;
+    // binning: bucketed path (k_bin.cu) unless a tile list exceeds the per-tile sort
+    // capacity (or the radix path is forced); both give the identical sorted lists
+    bool radix = c.binning_mode == 1 || !bin_supported(Tn);
+    uint32_t max_len = 0;
+    int64_t I = 0;
+    if (!radix) {
+        stage_begin(c, 1);
+        I = launch_bin_count(c, dc, cfg, &max_len);
+        stage_end(c, 1);
+        if (I < 0) return c.err.empty() ? TS_ERR_OOM : TS_ERR_CUDA;
+        if (ts_status s = last_launch(c, "preprocess/bin_count"); s != TS_OK) return s;
+        radix = max_len > uint32_t(bin_sort_cap());
+    }
+    if (radix) {
+        stage_begin(c, 1);
+        launch_depth_sort(c);
+        stage_end(c, 1);
+        stage_begin(c, 2);
+        I = launch_scan_counts(c);
+        stage_end(c, 2);
+        if (ts_status s = last_launch(c, "preprocess/sort/scan"); s != TS_OK) return s;
+    }
+    c.last_view_radix = radix;
     if (I > int64_t(0xFFFFFFF0u)) return validation(c, "instance count exceeds 2^32");
     const size_t capI = size_t(I) + size_t(I) / 4 + 1024;
-    if (c.tkey[0].cap < size_t(I) || c.tkey[1].cap < size_t(I) || c.ival[0].cap < size_t(I) ||
-        c.ival[1].cap < size_t(I)) {
-        for (int k = 0; k < 2; ++k) {
-            release(c.tkey[k]);
+    for (int k = 0; k < 2; ++k) {
+        if (c.ival[k].cap < size_t(I)) {
             release(c.ival[k]);
-            if (!ensure(c, c.tkey[k], capI) || !ensure(c, c.ival[k], capI)) return TS_ERR_OOM;
+            if (!ensure(c, c.ival[k], capI)) return TS_ERR_OOM;
+        }
+        if (radix && c.tkey[k].cap < size_t(I)) {
+            release(c.tkey[k]);
+            if (!ensure(c, c.tkey[k], capI)) return TS_ERR_OOM;
         }
     }
     c.I = I;
-    stage_begin(c, 3);
-    launch_duplicate(c, dc, cfg);
-    stage_end(c, 3);
-    stage_begin(c, 4);
-    launch_tile_sort(c, tile_bits_for(Tn));
-    stage_end(c, 4);
-    stage_begin(c, 5);
-    launch_ranges(c, Tn);
-    stage_end(c, 5);
+    if (radix) {
+        stage_begin(c, 3);
+        launch_duplicate(c, dc, cfg);
+        stage_end(c, 3);
+        stage_begin(c, 4);
+        launch_tile_sort(c, tile_bits_for(Tn));
+        stage_end(c, 4);
+        stage_begin(c, 5);
+        launch_ranges(c, Tn);
+        stage_end(c, 5);
+    } else {
+        stage_begin(c, 3);
+        launch_bin_scatter(c, dc, cfg);
+        stage_end(c, 3);
+        stage_begin(c, 4);
+        launch_tile_depth_sort(c, Tn, max_len);
+        stage_end(c, 4);
+    }
     stage_begin(c, 6);
     launch_blend_fwd(c, dc, cfg);
     stage_end(c, 6);
@@ -387,6 +414,7 @@ ts_status ts_destroy(ts_ctx* x) {
     release(c.starts), release(c.rhist), release(c.scan_state), release(c.scan_tmp), release(c.counters);
     release(c.rgb), release(c.Tfin), release(c.dLdC), release(c.hwc_stage), release(c.tgt), release(c.pcount);
     release(c.loss_acc), release(c.loss_tmp), release(c.targets), release(c.dens);
+    release(c.binH), release(c.bintot);
     for (size_t k = 0; k < c.ev_b.size(); ++k) {
         cudaEventDestroy(c.ev_b[k]);
         cudaEventDestroy(c.ev_e[k]);
@@ -681,6 +709,20 @@ ts_status ts_get_state(ts_ctx* x, float* grads, float* m, float* v, float* accum
     return TS_OK;
 }
 
+ts_status ts_set_binning(ts_ctx* x, int32_t mode) {
+    TS_CHECK_CTX(x);
+    Context& c = x->c;
+    if (mode < 0 || mode > 1) return validation(c, "binning mode must be 0 (auto) or 1 (radix)");
+    c.binning_mode = mode;
+    return TS_OK;
+}
+
+ts_status ts_binning_path(ts_ctx* x, int32_t* radix) {
+    TS_CHECK_CTX(x);
+    if (radix) *radix = x->c.last_view_radix ? 1 : 0;
+    return TS_OK;
+}
+
 ts_status ts_debug_preprocess(ts_ctx* x, float* splat12, int32_t* rect4, uint32_t* tile_count, uint32_t* depth_key) {
     TS_CHECK_CTX(x);
     Context& c = x->c;
@@ -723,22 +765,21 @@ ts_status ts_debug_instances(ts_ctx* x, int64_t* n_inst, uint64_t* keys, uint32_
     if (!keys && !vals && !ranges) return TS_OK;
     const size_t I = size_t(c.I), N = size_t(c.N);
     const int Tn = ((c.cam.width + 15) / 16) * ((c.cam.height + 15) / 16);
-    std::vector<uint16_t> tk(I);
     std::vector<uint32_t> iv(I), st(size_t(Tn) + 1);
     std::vector<float4> sp(3 * N);
-    if (I) {
-        CK(cudaMemcpyAsync(tk.data(), c.tkey[0].p, I * 2, cudaMemcpyDeviceToHost, c.stream));
-        CK(cudaMemcpyAsync(iv.data(), c.ival[0].p, I * 4, cudaMemcpyDeviceToHost, c.stream));
-    }
+    if (I) CK(cudaMemcpyAsync(iv.data(), c.ival[0].p, I * 4, cudaMemcpyDeviceToHost, c.stream));
     if (N) CK(cudaMemcpyAsync(sp.data(), c.splat.p, 3 * N * 16, cudaMemcpyDeviceToHost, c.stream));
     CK(cudaMemcpyAsync(st.data(), c.starts.p, (size_t(Tn) + 1) * 4, cudaMemcpyDeviceToHost, c.stream));
     CK(cudaStreamSynchronize(c.stream));
+    // tile of instance i from the ranges (both binning paths produce the ranges)
+    int tile = 0;
     for (size_t i = 0; i < I; ++i) {
+        while (tile < Tn && size_t(st[tile + 1]) <= i) ++tile;
         if (vals) vals[i] = iv[i];
         if (keys) {
             uint32_t bits;
             std::memcpy(&bits, &sp[3 * size_t(iv[i]) + 1].w, 4);
-            keys[i] = (uint64_t(tk[i]) << 32) | uint64_t(bits ^ 0x80000000u);
+            keys[i] = (uint64_t(uint32_t(tile)) << 32) | uint64_t(bits ^ 0x80000000u);
         }
     }
     if (ranges)

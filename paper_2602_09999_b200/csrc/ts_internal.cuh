@@ -96,6 +96,12 @@ struct Context {
     size_t ev_cursor = 0;
 
     DevBuf<uint32_t> dens;       // densify scratch
+
+    // binning (k_bin.cu): per-chunk tile histograms, tile totals (+ max list length)
+    DevBuf<uint32_t> binH, bintot;
+    uint32_t bin_class[5] = {0, 0, 0, 0, 0};  // tiles per per-tile sort size class (last view)
+    int binning_mode = 0;        // 0 auto (bucket + per-tile sort), 1 force the two-stage radix path
+    bool last_view_radix = false;
 };
 
 // ---- kernels / launchers (each returns cudaError_t of the launch) ----
@@ -105,6 +111,12 @@ int64_t launch_scan_counts(Context& c);             // offsets in depth order; r
 void launch_duplicate(Context& c, const DevCam& cam, const ts_render_config& cfg);
 void launch_tile_sort(Context& c, int tile_bits);
 void launch_ranges(Context& c, int n_tiles);
+// bucketed binning (k_bin.cu): returns I (syncs) and the longest tile list, -1 on OOM
+bool bin_supported(int Tn);
+int bin_sort_cap();
+int64_t launch_bin_count(Context& c, const DevCam& cam, const ts_render_config& cfg, uint32_t* max_len);
+void launch_bin_scatter(Context& c, const DevCam& cam, const ts_render_config& cfg);
+void launch_tile_depth_sort(Context& c, int Tn, uint32_t max_len);
 void launch_blend_fwd(Context& c, const DevCam& cam, const ts_render_config& cfg);
 void launch_loss(Context& c, const float* target_chw);
 void launch_blend_bwd(Context& c, const DevCam& cam, const ts_render_config& cfg);

@@ -75,6 +75,8 @@ _SIGS = {
     "ts_view_stats": [_vp, _vp],
     "ts_set_profiling": [_vp, _i32],
     "ts_stage_times": [_vp, _vp, _vp, _i32],
+    "ts_set_binning": [_vp, _i32],
+    "ts_binning_path": [_vp, _vp],
     "ts_launch_count": [_vp, ctypes.POINTER(_i64)],
     "ts_host_alloc": [ctypes.c_size_t, ctypes.POINTER(_vp)],
     "ts_host_free": [_vp],
@@ -353,6 +355,15 @@ class Engine:
         cnt = np.zeros(len(STAGES), np.int32)
         self._check(self._L.ts_stage_times(self._h, _ptr(out), _ptr(cnt), len(STAGES)), "ts_stage_times")
         return {k: (float(a), int(b)) for k, a, b in zip(STAGES, out, cnt)}
+
+    def set_binning(self, mode: int):
+        """0 auto (bucketed binning + per-tile sort), 1 force the two-stage radix sort."""
+        self._check(self._L.ts_set_binning(self._h, mode), "ts_set_binning")
+
+    def binning_path(self) -> str:
+        r = ctypes.c_int32()
+        self._check(self._L.ts_binning_path(self._h, ctypes.byref(r)), "ts_binning_path")
+        return "radix" if r.value else "bucket"
 
     def launch_count(self) -> int:
         n = ctypes.c_int64()

@@ -18,8 +18,8 @@
 //   KB4 tile_sort   CTA per tile: (depth key, Gaussian) pairs of the list sorted
 //                   in shared memory -- one bucketing pass on the key interpolated
 //                   between the list's min and max (buckets are monotone in the key),
-//                   then each small bucket insertion-sorted on (key, index) -- and
-//                   written back in order.
+//                   then every element's rank inside its small bucket on (key, index)
+//                   gives its final position, written straight back.
 // Integer work only; the result is bit-identical to the two-stage radix path
 // (k_sort.cu), which remains the fallback for lists longer than kSortCap.
 #include "ts_internal.cuh"
@@ -187,7 +187,7 @@ __global__ void __launch_bounds__(kBinThreads) bin_scatter_kernel(const uint4* _
 // KB4 per-tile sort on (depth key, Gaussian index)
 // ---------------------------------------------------------------------------
 // shared layout: bucketed keys/indices (CAP each) + bucket counters (CAP/2 + 1);
-// the list itself is staged in registers (CAP / NT per thread)
+// the list itself stays in registers (CAP / NT per thread)
 constexpr size_t tile_sort_smem(int cap) { return size_t(cap) * 8 + (size_t(cap) / 2 + 1) * 4; }
 
 template <int CAP, int NT>
@@ -293,24 +293,24 @@ __global__ void __launch_bounds__(NT) tile_sort_kernel(const uint32_t* __restric
         }
     }
     __syncthreads();
-    // insertion sort of every bucket on (key, index); bucket i = [end(i-1), end(i))
-    for (int bi = tid; bi < nbk; bi += NT) {
-        const int e = int(cnt[bi]);
-        const int s = bi == 0 ? 0 : int(cnt[bi - 1]);
-        for (int i = s + 1; i < e; ++i) {
-            const uint32_t k = skey[i], g = sgid[i];
-            int j = i - 1;
-            while (j >= s && (skey[j] > k || (skey[j] == k && sgid[j] > g))) {
-                skey[j + 1] = skey[j];
-                sgid[j + 1] = sgid[j];
-                --j;
+    // final position of every element: its bucket's start plus the number of bucket
+    // members ordered before it on (key, index); written straight to the tile list
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const int i = tid + r * NT;
+        if (i < L) {
+            const uint32_t bb = bk[r];
+            const int e = int(cnt[bb]);
+            const int s = bb == 0 ? 0 : int(cnt[bb - 1]);
+            const uint32_t k = kk[r], g = gg[r];
+            int rank = s;
+            for (int j = s; j < e; ++j) {
+                const uint32_t kj = skey[j], gj = sgid[j];
+                rank += (kj < k || (kj == k && gj < g)) ? 1 : 0;
             }
-            skey[j + 1] = k;
-            sgid[j + 1] = g;
+            out[b + rank] = g;
         }
     }
-    __syncthreads();
-    for (int i = tid; i < L; i += NT) out[b + i] = sgid[i];
 }
 
 // lists of one instance need no sort: copy
@@ -373,7 +373,7 @@ void launch_bin_scatter(Context& c, const DevCam& cam, const ts_render_config& c
 }
 
 template <int CAP, int NT>
-static void sort_variant(Context& c, const uint32_t* tiles, uint32_t n) {
+static void sort_variant(Context& c, const uint32_t* tiles, uint32_t n, cudaStream_t st) {
     if (!n) return;
     static bool attr = false;
     if (!attr) {
@@ -381,8 +381,8 @@ static void sort_variant(Context& c, const uint32_t* tiles, uint32_t n) {
                              int(tile_sort_smem(CAP)));
         attr = true;
     }
-    tile_sort_kernel<CAP, NT><<<n, NT, tile_sort_smem(CAP), c.stream>>>(c.starts.p, c.ival[1].p, c.dkey[0].p,
-                                                                       c.ival[0].p, tiles);
+    tile_sort_kernel<CAP, NT><<<n, NT, tile_sort_smem(CAP), st>>>(c.starts.p, c.ival[1].p, c.dkey[0].p,
+                                                                  c.ival[0].p, tiles);
     TS_LAUNCHED(c);
 }
 
@@ -395,10 +395,26 @@ void launch_tile_depth_sort(Context& c, int Tn, uint32_t max_len) {
                                                                                   c.ival[0].p, cls, int(c.bin_class[0]));
         TS_LAUNCHED(c);
     }
-    sort_variant<kCap0, 256>(c, cls + size_t(1) * Tn, c.bin_class[1]);
-    sort_variant<kCap1, 512>(c, cls + size_t(2) * Tn, c.bin_class[2]);
-    sort_variant<kCap2, 512>(c, cls + size_t(3) * Tn, c.bin_class[3]);
-    sort_variant<kCap3, 1024>(c, cls + size_t(4) * Tn, c.bin_class[4]);
+    // the size classes are independent: the two largest run on fork streams so their
+    // CTAs share the GPU with the smaller classes instead of queueing behind them
+    if (!c.fork_ev) {
+        cudaEventCreateWithFlags(&c.fork_ev, cudaEventDisableTiming);
+        for (int k = 0; k < 2; ++k) {
+            cudaStreamCreateWithFlags(&c.side[k], cudaStreamNonBlocking);
+            cudaEventCreateWithFlags(&c.join_ev[k], cudaEventDisableTiming);
+        }
+    }
+    cudaEventRecord(c.fork_ev, c.stream);
+    cudaStreamWaitEvent(c.side[0], c.fork_ev, 0);
+    cudaStreamWaitEvent(c.side[1], c.fork_ev, 0);
+    sort_variant<kCap2, 512>(c, cls + size_t(3) * Tn, c.bin_class[3], c.side[0]);
+    sort_variant<kCap3, 1024>(c, cls + size_t(4) * Tn, c.bin_class[4], c.side[1]);
+    sort_variant<kCap1, 512>(c, cls + size_t(2) * Tn, c.bin_class[2], c.stream);
+    sort_variant<kCap0, 256>(c, cls + size_t(1) * Tn, c.bin_class[1], c.stream);
+    for (int k = 0; k < 2; ++k) {
+        cudaEventRecord(c.join_ev[k], c.side[k]);
+        cudaStreamWaitEvent(c.stream, c.join_ev[k], 0);
+    }
 }
 
 }  // namespace ts

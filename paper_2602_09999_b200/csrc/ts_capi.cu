@@ -419,6 +419,11 @@ ts_status ts_destroy(ts_ctx* x) {
         cudaEventDestroy(c.ev_b[k]);
         cudaEventDestroy(c.ev_e[k]);
     }
+    for (int k = 0; k < 2; ++k) {
+        if (c.side[k]) cudaStreamDestroy(c.side[k]);
+        if (c.join_ev[k]) cudaEventDestroy(c.join_ev[k]);
+    }
+    if (c.fork_ev) cudaEventDestroy(c.fork_ev);
     if (c.own_stream) cudaStreamDestroy(c.stream);
     delete x;
     return TS_OK;

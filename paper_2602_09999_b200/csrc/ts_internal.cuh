@@ -100,6 +100,8 @@ struct Context {
     // binning (k_bin.cu): per-chunk tile histograms, tile totals (+ max list length)
     DevBuf<uint32_t> binH, bintot;
     uint32_t bin_class[5] = {0, 0, 0, 0, 0};  // tiles per per-tile sort size class (last view)
+    cudaStream_t side[2] = {nullptr, nullptr};  // fork streams for independent launches
+    cudaEvent_t fork_ev = nullptr, join_ev[2] = {nullptr, nullptr};
     int binning_mode = 0;        // 0 auto (bucket + per-tile sort), 1 force the two-stage radix path
     bool last_view_radix = false;
 };

@@ -555,12 +555,12 @@ void launch_project_bwd(Context& c, const DevCam& cam, const ts_render_config& c
 #define TS_PB(D)                                                                                      \
     if (accumulate) {                                                                                 \
         constexpr int sm = PbLayout<D, true>::kTotal * 4;                                             \
-        cudaFuncSetAttribute(project_bwd_kernel<D, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm); \
+        { static bool a_ = false; if (!a_) a_ = cudaFuncSetAttribute(project_bwd_kernel<D, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm) == cudaSuccess; } \
         project_bwd_kernel<D, true><<<unsigned(blocks), kBlock, sm, c.stream>>>(                      \
             c.params.p, c.grads.p, c.g2d.p, c.tcount.p, c.accum.p, c.vcount.p, c.vis.p, c.N, cam, cfg, 0); \
     } else {                                                                                          \
         constexpr int sm = PbLayout<D, false>::kTotal * 4;                                            \
-        cudaFuncSetAttribute(project_bwd_kernel<D, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm); \
+        { static bool a_ = false; if (!a_) a_ = cudaFuncSetAttribute(project_bwd_kernel<D, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm) == cudaSuccess; } \
         project_bwd_kernel<D, false><<<unsigned(blocks), kBlock, sm, c.stream>>>(                     \
             c.params.p, c.grads.p, c.g2d.p, c.tcount.p, c.accum.p, c.vcount.p, c.vis.p, c.N, cam, cfg,   \
             int(zero_inactive));                                                                       \
@@ -590,11 +590,11 @@ void launch_project_bwd_adam(Context& c, const DevCam& cam, const ts_render_conf
     const bool skip = a.mode == 4;
 #define TS_FB(D)                                                                                          \
     if (skip) {                                                                                           \
-        cudaFuncSetAttribute(project_bwd_adam_kernel<D, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm); \
+        { static bool a_ = false; if (!a_) a_ = cudaFuncSetAttribute(project_bwd_adam_kernel<D, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm) == cudaSuccess; } \
         project_bwd_adam_kernel<D, true><<<unsigned(blocks), kFB, sm, c.stream>>>(                        \
             c.params.p, c.m.p, c.v.p, c.g2d.p, c.tcount.p, c.accum.p, c.vcount.p, c.vis.p, c.N, cam, cfg, fa); \
     } else {                                                                                              \
-        cudaFuncSetAttribute(project_bwd_adam_kernel<D, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm); \
+        { static bool a_ = false; if (!a_) a_ = cudaFuncSetAttribute(project_bwd_adam_kernel<D, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm) == cudaSuccess; } \
         project_bwd_adam_kernel<D, false><<<unsigned(blocks), kFB, sm, c.stream>>>(                       \
             c.params.p, c.m.p, c.v.p, c.g2d.p, c.tcount.p, c.accum.p, c.vcount.p, c.vis.p, c.N, cam, cfg, fa); \
     }

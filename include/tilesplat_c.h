@@ -156,6 +156,8 @@ ts_status ts_debug_preprocess(ts_ctx* ctx, float* splat12 /* N*12 */, int32_t* r
                               uint32_t* tile_count /* N */, uint32_t* depth_key /* N */);
 ts_status ts_debug_instances(ts_ctx* ctx, int64_t* n_inst, uint64_t* keys /* I */, uint32_t* vals /* I */,
                              uint32_t* ranges /* 2*Tn */);
+/* dL/dC of the last ts_loss (H*W*3 interleaved, host) */
+ts_status ts_debug_loss_grad(ts_ctx* ctx, float* dLdC_hwc);
 /* per-Gaussian 2D gradients {dmx,dmy,dA,dB,dC,do,dr,dg,db} of the blend backward (K8 only) of the
  * last forward for the given dL/dC; does not touch the parameter gradients. */
 ts_status ts_debug_grad2d(ts_ctx* ctx, const float* dL_dC_hwc, float* g2d9 /* N*9 */);

@@ -1,19 +1,10 @@
 // K7 training_loss: 0.8 L1 + 0.2 (1 - SSIM) with an 11x11
 // Gaussian window (sigma 1.5), C1 = 0.01^2, C2 = 0.03^2, reflect padding, and the
-// analytic dL/dC.  Two shared-memory-tiled kernels per 32x32 pixel tile and
-// colour channel, both register-blocked (sliding windows: a thread filters 8
-// consecutive columns of one row, then 4 consecutive rows of one column, so
-// every staged value is loaded once per window instead of once per tap):
-//   loss_fwd: reflect-padded 42x42 patch of rendered and target colour, the 5
-//     separable window moments, the SSIM map and its partial derivatives
-//     (a, b, c below), block-reduced L1 / SSIM sums;
-//   loss_bwd: the transposed filter of (a, b, c): separable correlation of the
-//     zero-extended maps, plus, for pixels within 5 of the image border, the
-//     terms folded back through the reflect padding; then
-//     dL/dC = (0.8 sign(x-y) - 0.2 (W^T a + x W^T b + y W^T c)) / M.
-// With  mu = W x,  v = W x^2 - mu_x^2,  cov = W xy - mu_x mu_y  (per pixel):
+// analytic dL/dC, in one kernel per 32x32 tile and colour channel (see
+// loss_fused_kernel).  With  mu = W x,  v = W x^2 - mu_x^2,  cov = W xy - mu_x mu_y:
 //   dSSIM/dx_p = (W^T a)_p + x_p (W^T b)_p + y_p (W^T c)_p,
-//   a = dS/dmu_x - 2 mu_x dS/dv_x - mu_y dS/dcov,  b = 2 dS/dv_x,  c = dS/dcov.
+//   a = dS/dmu_x - 2 mu_x dS/dv_x - mu_y dS/dcov,  b = 2 dS/dv_x,  c = dS/dcov,
+//   dL/dC = (0.8 sign(x - y) - 0.2 dSSIM/dx) / M.
 #include <cmath>
 
 #include "ts_internal.cuh"
@@ -22,103 +13,238 @@ namespace ts {
 namespace {
 
 __constant__ float c_gw[11];
-constexpr int kT = 32;           // output tile edge
-constexpr int kP = kT + 10;      // padded patch edge (42)
-constexpr int kPS = kP + 1;      // smem row stride
-constexpr int kThreads = 256;
-constexpr int kSeg = 8;          // columns per horizontal work item
-constexpr int kRows = 4;         // rows per vertical work item
-
 __device__ __forceinline__ int refl(int i, int n) { return i < 0 ? -i : (i >= n ? 2 * (n - 1) - i : i); }
 
-__global__ void __launch_bounds__(kThreads) loss_fwd_kernel(const float* __restrict__ X, const float* __restrict__ Y,
-                                                            float* __restrict__ maps, int W, int H,
-                                                            double* __restrict__ acc) {
-    __shared__ float sx[kP][kPS], sy[kP][kPS];
-    __shared__ float hm[5][kP][kT + 1];
+// ---------------------------------------------------------------------------
+// Fused loss kernel: forward moments, SSIM terms and the transposed filter of the
+// backward in ONE kernel per 32x32 output tile and colour channel (no map round
+// trip through HBM).  Positions relative to the tile origin (x0, y0):
+//   input    52x52  [-10, 42)  reflect-indexed image values
+//   moments  42x42  [-5, 37)   five window moments, SSIM and (a, b, c); (a, b, c)
+//                               are zero outside the image (zero extension)
+//   virtual  47     [-5, 42)   positions of the transposed filter: the reflect
+//                               padding of the forward folds -p and 2(W-1)-p back
+//                               onto p (per axis; separable)
+//   output   32x32  [0, 32)
+// The transposed filter is the same symmetric window.  Shared memory (floats):
+// A = 5 x 52 x 42 horizontal moments, later hb 3 x 42 x 47 and vb 3 x 47 x 32;
+// B = 3 x 42 x 58 (input 2 x 52 x 52, then (a, b, c) column-padded to [-10, 48),
+// then the column-folded pass 3 x 58 x 32 row-padded to [-10, 48)).
+// ---------------------------------------------------------------------------
+constexpr int kFT = 32;                   // output tile edge
+constexpr int kFI = kFT + 20;             // input region edge (52)
+constexpr int kFM = kFT + 10;             // moment region edge (42)
+constexpr int kFV = kFT + 15;             // virtual transposed-filter positions (47)
+constexpr int kFP = kFV + 11;             // padded (a, b, c) columns / hf rows (58)
+constexpr int kFA = 5 * kFI * kFM;        // 10920
+constexpr int kFB = 3 * kFM * kFP;        // 7308
+constexpr int kFThreads = 256;
+constexpr size_t kFusedSmem = size_t(kFA + kFB) * 4;
+
+__global__ void __launch_bounds__(kFThreads) loss_fused_kernel(const float* __restrict__ X,
+                                                              const float* __restrict__ Y, float* __restrict__ dL,
+                                                              int W, int H, float inv_m, double* __restrict__ acc) {
+    extern __shared__ float fsm[];
+    float* A = fsm;
+    float* B = fsm + kFA;
     const int ch = blockIdx.z, P = W * H;
-    const int x0 = blockIdx.x * kT, y0 = blockIdx.y * kT;
+    const int x0 = blockIdx.x * kFT, y0 = blockIdx.y * kFT;
     const int tid = threadIdx.x;
     const float* Xc = X + size_t(ch) * P;
     const float* Yc = Y + size_t(ch) * P;
-    for (int i = tid; i < kP * kP; i += kThreads) {
-        const int r = i / kP, c = i - r * kP;
-        const int gi = refl(y0 - 5 + r, H) * W + refl(x0 - 5 + c, W);
-        sx[r][c] = __ldg(Xc + gi);
-        sy[r][c] = __ldg(Yc + gi);
-    }
-    __syncthreads();
-    // horizontal: (row, 8-column segment) items, sliding window of 18 inputs
-    for (int it = tid; it < kP * (kT / kSeg); it += kThreads) {
-        const int r = it / (kT / kSeg), c0 = (it - r * (kT / kSeg)) * kSeg;
-        float a[kSeg + 10], b[kSeg + 10];
+    float wk[11];
 #pragma unroll
-        for (int k = 0; k < kSeg + 10; ++k) {
-            a[k] = sx[r][c0 + k];
-            b[k] = sy[r][c0 + k];
-        }
-#pragma unroll
-        for (int j = 0; j < kSeg; ++j) {
-            float m0 = 0.f, m1 = 0.f, m2 = 0.f, m3 = 0.f, m4 = 0.f;
-#pragma unroll
-            for (int k = 0; k < 11; ++k) {
-                const float w = c_gw[k], xa = a[j + k], yb = b[j + k];
-                const float wx = w * xa, wy = w * yb;
-                m0 += wx;
-                m1 += wy;
-                m2 = fmaf(wx, xa, m2);
-                m3 = fmaf(wy, yb, m3);
-                m4 = fmaf(wx, yb, m4);
+    for (int k = 0; k < 11; ++k) wk[k] = c_gw[k];
+    // 1. input region (reflect; clamped first so far-outside positions of small images stay in range)
+    float* xs = B;
+    float* ys = B + kFI * kFI;
+    {
+        // 4 rows x 64 columns per pass (52 active): the column's reflected index once per thread
+        const int c = tid & 63;
+        if (c < kFI) {
+            const int gx = refl(min(max(x0 - 10 + c, -(W - 1)), 2 * (W - 1)), W);
+            for (int r = tid >> 6; r < kFI; r += kFThreads / 64) {
+                const int gy = refl(min(max(y0 - 10 + r, -(H - 1)), 2 * (H - 1)), H);
+                const int gi = gy * W + gx;
+                xs[r * kFI + c] = __ldg(Xc + gi);
+                ys[r * kFI + c] = __ldg(Yc + gi);
             }
-            hm[0][r][c0 + j] = m0, hm[1][r][c0 + j] = m1, hm[2][r][c0 + j] = m2, hm[3][r][c0 + j] = m3,
-            hm[4][r][c0 + j] = m4;
         }
     }
     __syncthreads();
-    // vertical: (column, 4-row group) items, sliding window of 14 rows; SSIM per pixel
-    const int c = tid % kT, rg = (tid / kT) * kRows;  // 32 columns x 8 groups = 256 threads
+    // 2. horizontal moments: rows [0, 52) x moment cols [0, 42), items of 7 columns
+    {
+        constexpr int S = 7, NS = kFM / S;
+        for (int it = tid; it < kFI * NS; it += kFThreads) {
+            const int r = it / NS, c0 = (it - r * NS) * S;
+            float a[S + 10], b[S + 10];
+#pragma unroll
+            for (int k = 0; k < S + 10; ++k) {
+                a[k] = xs[r * kFI + c0 + k];
+                b[k] = ys[r * kFI + c0 + k];
+            }
+#pragma unroll
+            for (int j = 0; j < S; ++j) {
+                float m0 = 0.f, m1 = 0.f, m2 = 0.f, m3 = 0.f, m4 = 0.f;
+#pragma unroll
+                for (int k = 0; k < 11; ++k) {
+                    const float xa = a[j + k], yb = b[j + k];
+                    const float wx = wk[k] * xa, wy = wk[k] * yb;
+                    m0 += wx;
+                    m1 += wy;
+                    m2 = fmaf(wx, xa, m2);
+                    m3 = fmaf(wy, yb, m3);
+                    m4 = fmaf(wx, yb, m4);
+                }
+                const int o = r * kFM + c0 + j;
+                A[o] = m0;
+                A[kFI * kFM + o] = m1;
+                A[2 * kFI * kFM + o] = m2;
+                A[3 * kFI * kFM + o] = m3;
+                A[4 * kFI * kFM + o] = m4;
+            }
+        }
+    }
+    __syncthreads();
+    // 3. vertical moments over moment rows [0, 42) -> SSIM and (a, b, c) into B as
+    //    abc[q][r][c + 5] (padded columns [-10, 48) hold zeros)
     float l1 = 0.f, ss = 0.f;
     {
-        float m[kRows][5];
+        constexpr int S = 6, NS = kFM / S;
+        for (int it = tid; it < kFM * NS; it += kFThreads) {
+            const int c = it % kFM, r0 = (it / kFM) * S;
+            float m[S][5];
 #pragma unroll
-        for (int j = 0; j < kRows; ++j)
+            for (int q = 0; q < 5; ++q) {
+                float win[S + 10];
 #pragma unroll
-            for (int q = 0; q < 5; ++q) m[j][q] = 0.f;
+                for (int k = 0; k < S + 10; ++k) win[k] = A[q * kFI * kFM + (r0 + k) * kFM + c];
 #pragma unroll
-        for (int q = 0; q < 5; ++q) {
-            float win[kRows + 10];
+                for (int j = 0; j < S; ++j) {
+                    float sacc = 0.f;
 #pragma unroll
-            for (int k = 0; k < kRows + 10; ++k) win[k] = hm[q][rg + k][c];
+                    for (int k = 0; k < 11; ++k) sacc = fmaf(wk[k], win[j + k], sacc);
+                    m[j][q] = sacc;
+                }
+            }
+            const int gx = x0 - 5 + c;
 #pragma unroll
-            for (int j = 0; j < kRows; ++j)
-#pragma unroll
-                for (int k = 0; k < 11; ++k) m[j][q] = fmaf(c_gw[k], win[j + k], m[j][q]);
+            for (int j = 0; j < S; ++j) {
+                const int r = r0 + j, gy = y0 - 5 + r;
+                float ta = 0.f, tb = 0.f, tc = 0.f;
+                if (gx >= 0 && gx < W && gy >= 0 && gy < H) {
+                    const float C1 = 0.01f * 0.01f, C2 = 0.03f * 0.03f;
+                    const float ux = m[j][0], uy = m[j][1];
+                    const float vx = m[j][2] - ux * ux, vy = m[j][3] - uy * uy, cxy = m[j][4] - ux * uy;
+                    const float n1 = 2.f * ux * uy + C1, n2 = 2.f * cxy + C2;
+                    const float d1 = ux * ux + uy * uy + C1, d2 = vx + vy + C2;
+                    const float iD = __fdividef(1.f, d1 * d2);
+                    const float Sv = n1 * n2 * iD;
+                    const float dS_dux = (2.f * uy * n2 - Sv * 2.f * ux * d2) * iD;
+                    const float dS_dvx = -Sv * d1 * iD;
+                    const float dS_dcxy = 2.f * n1 * iD;
+                    ta = dS_dux - 2.f * ux * dS_dvx - uy * dS_dcxy;
+                    tb = 2.f * dS_dvx;
+                    tc = dS_dcxy;
+                    if (r >= 5 && r < 5 + kFT && c >= 5 && c < 5 + kFT) {
+                        ss += Sv;
+                        const int p = gy * W + gx;
+                        l1 += fabsf(__ldg(Xc + p) - __ldg(Yc + p));
+                    }
+                }
+                B[0 * kFM * kFP + r * kFP + c + 5] = ta;
+                B[1 * kFM * kFP + r * kFP + c + 5] = tb;
+                B[2 * kFM * kFP + r * kFP + c + 5] = tc;
+            }
         }
-        const float C1 = 0.01f * 0.01f, C2 = 0.03f * 0.03f;
-        float* mp = maps + size_t(ch) * 3 * P;
+        // zero the padding columns [0, 5) and [47, 58) of every (a, b, c) row (3 x 42 rows)
+        if (tid < 3 * kFM) {
+            float* row = B + tid * kFP;
 #pragma unroll
-        for (int j = 0; j < kRows; ++j) {
-            const int x = x0 + c, y = y0 + rg + j;
-            if (x >= W || y >= H) continue;
-            const float ux = m[j][0], uy = m[j][1];
-            const float vx = m[j][2] - ux * ux, vy = m[j][3] - uy * uy, cxy = m[j][4] - ux * uy;
-            const float n1 = 2.f * ux * uy + C1, n2 = 2.f * cxy + C2;
-            const float d1 = ux * ux + uy * uy + C1, d2 = vx + vy + C2;
-            const float iD = 1.f / (d1 * d2);
-            const float S = n1 * n2 * iD;
-            const float dS_dux = (2.f * uy * n2 - S * 2.f * ux * d2) * iD;
-            const float dS_dvx = -S * d1 * iD;
-            const float dS_dcxy = 2.f * n1 * iD;
-            const int p = y * W + x;
-            mp[p] = dS_dux - 2.f * ux * dS_dvx - uy * dS_dcxy;
-            mp[P + p] = 2.f * dS_dvx;
-            mp[2 * P + p] = dS_dcxy;
-            ss += S;
-            l1 += fabsf(sx[rg + j + 5][c + 5] - sy[rg + j + 5][c + 5]);
+            for (int k = 0; k < 5; ++k) row[k] = 0.f;
+#pragma unroll
+            for (int k = kFM + 5; k < kFP; ++k) row[k] = 0.f;
         }
     }
+    __syncthreads();
+    // 4a. horizontal transposed pass at virtual columns [-5, 42): hb[q][r][m] (A, 3 x 42 x 47)
+    {
+        constexpr int S = 8, NS = (kFV + S - 1) / S;  // 6 segments (48 columns, last partly unused)
+        for (int it = tid; it < 3 * kFM * NS; it += kFThreads) {
+            const int q = it / (kFM * NS), rem = it - q * kFM * NS, r = rem / NS, c0 = (rem - r * NS) * S;
+            float a[S + 10];
+#pragma unroll
+            for (int k = 0; k < S + 10; ++k) a[k] = c0 + k < kFP ? B[q * kFM * kFP + r * kFP + c0 + k] : 0.f;
+#pragma unroll
+            for (int j = 0; j < S; ++j) {
+                float sacc = 0.f;
+#pragma unroll
+                for (int k = 0; k < 11; ++k) sacc = fmaf(wk[k], a[j + k], sacc);
+                if (c0 + j < kFV) A[q * kFM * kFV + r * kFV + c0 + j] = sacc;
+            }
+        }
+    }
+    __syncthreads();
+    // 4b. fold columns -> hf[q][r + 5][c] (B, 3 x 58 x 32; padded rows [-10, 48) hold zeros)
+    {
+        const int c = tid & 31;
+        const int px = x0 + c;
+        const int ml = (px >= 1 && px <= 5) ? -px - x0 + 5 : -1;                             // mirror of -px
+        const int mr = (px >= W - 6 && px <= W - 2) ? 2 * (W - 1) - px - x0 + 5 : -1;        // mirror of 2(W-1)-px
+        for (int qr = tid >> 5; qr < 3 * kFP; qr += kFThreads / 32) {
+            const int q = qr / kFP, pr = qr - q * kFP, r = pr - 5;
+            float v = 0.f;
+            if (r >= 0 && r < kFM && px < W) {
+                const float* hb = A + q * kFM * kFV + r * kFV;
+                v = hb[c + 5];
+                if (ml >= 0) v += hb[ml];
+                if (mr >= 0) v += hb[mr];
+            }
+            B[qr * kFT + c] = v;
+        }
+    }
+    __syncthreads();
+    // 5a. vertical transposed pass at virtual rows [-5, 42): vb[q][m][c] (A, 3 x 47 x 32)
+    {
+        constexpr int S = 6, NS = (kFV + S - 1) / S;  // 8 groups (48 rows, last partly unused)
+        for (int it = tid; it < 3 * kFT * NS; it += kFThreads) {
+            const int q = it / (kFT * NS), rem = it - q * kFT * NS, c = rem % kFT, r0 = (rem / kFT) * S;
+            float win[S + 10];
+#pragma unroll
+            for (int k = 0; k < S + 10; ++k) win[k] = r0 + k < kFP ? B[q * kFP * kFT + (r0 + k) * kFT + c] : 0.f;
+#pragma unroll
+            for (int j = 0; j < S; ++j) {
+                float sacc = 0.f;
+#pragma unroll
+                for (int k = 0; k < 11; ++k) sacc = fmaf(wk[k], win[j + k], sacc);
+                if (r0 + j < kFV) A[q * kFV * kFT + (r0 + j) * kFT + c] = sacc;
+            }
+        }
+    }
+    __syncthreads();
+    // 5b. fold rows; dL/dC = (0.8 sign(x - y) - 0.2 (Wt a + x Wt b + y Wt c)) / M
+    for (int i = tid; i < kFT * kFT; i += kFThreads) {
+        const int r = i / kFT, c = i - r * kFT;
+        const int px = x0 + c, py = y0 + r;
+        if (px >= W || py >= H) continue;
+        float t[3];
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+            const float* vb = A + q * kFV * kFT + c;
+            float v = vb[(r + 5) * kFT];
+            if (py >= 1 && py <= 5) v += vb[(-py - y0 + 5) * kFT];
+            if (py >= H - 6 && py <= H - 2) v += vb[(2 * (H - 1) - py - y0 + 5) * kFT];
+            t[q] = v;
+        }
+        const int p = py * W + px;
+        const float xv = __ldg(Xc + p), yv = __ldg(Yc + p);
+        const float dS = t[0] + xv * t[1] + yv * t[2];
+        const float d = xv - yv;
+        const float sg = d > 0.f ? 1.f : (d < 0.f ? -1.f : 0.f);
+        dL[size_t(ch) * P + p] = (0.8f * sg - 0.2f * dS) * inv_m;
+    }
     // block reduction of (L1, SSIM) -> double atomics
-    __shared__ float r1[kThreads / 32], r2[kThreads / 32];
+    __shared__ float r1[kFThreads / 32], r2[kFThreads / 32];
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
         l1 += __shfl_xor_sync(0xffffffffu, l1, o);
@@ -131,7 +257,7 @@ __global__ void __launch_bounds__(kThreads) loss_fwd_kernel(const float* __restr
     __syncthreads();
     if (tid == 0) {
         double a = 0, b = 0;
-        for (int w = 0; w < kThreads / 32; ++w) {
+        for (int w = 0; w < kFThreads / 32; ++w) {
             a += r1[w];
             b += r2[w];
         }
@@ -139,103 +265,6 @@ __global__ void __launch_bounds__(kThreads) loss_fwd_kernel(const float* __restr
         atomicAdd(acc + 1, b);
     }
 }
-
-// sum over the 11x11 window of the zero-extended map f around (jx, jy)
-__device__ __forceinline__ float window_sum(const float* __restrict__ f, int jx, int jy, int W, int H) {
-    float s = 0.f;
-    for (int oy = -5; oy <= 5; ++oy) {
-        const int yy = jy + oy;
-        if (yy < 0 || yy >= H) continue;
-        float r = 0.f;
-#pragma unroll
-        for (int ox = -5; ox <= 5; ++ox) {
-            const int xx = jx + ox;
-            if (xx >= 0 && xx < W) r = fmaf(c_gw[ox + 5], __ldg(f + yy * W + xx), r);
-        }
-        s = fmaf(c_gw[oy + 5], r, s);
-    }
-    return s;
-}
-
-__global__ void __launch_bounds__(kThreads) loss_bwd_kernel(const float* __restrict__ X, const float* __restrict__ Y,
-                                                            const float* __restrict__ maps, float* __restrict__ dL,
-                                                            int W, int H, float inv_m) {
-    __shared__ float sf[3][kP][kPS];
-    __shared__ float hm[3][kP][kT + 1];
-    const int ch = blockIdx.z, P = W * H;
-    const int x0 = blockIdx.x * kT, y0 = blockIdx.y * kT;
-    const int tid = threadIdx.x;
-    const float* mp = maps + size_t(ch) * 3 * P;
-    for (int i = tid; i < kP * kP; i += kThreads) {
-        const int r = i / kP, c = i - r * kP;
-        const int gy = y0 - 5 + r, gx = x0 - 5 + c;
-        const bool in = gy >= 0 && gy < H && gx >= 0 && gx < W;
-        const int gi = gy * W + gx;
-#pragma unroll
-        for (int q = 0; q < 3; ++q) sf[q][r][c] = in ? __ldg(mp + q * P + gi) : 0.f;
-    }
-    __syncthreads();
-    for (int it = tid; it < kP * (kT / kSeg); it += kThreads) {
-        const int r = it / (kT / kSeg), c0 = (it - r * (kT / kSeg)) * kSeg;
-#pragma unroll
-        for (int q = 0; q < 3; ++q) {
-            float a[kSeg + 10];
-#pragma unroll
-            for (int k = 0; k < kSeg + 10; ++k) a[k] = sf[q][r][c0 + k];
-#pragma unroll
-            for (int j = 0; j < kSeg; ++j) {
-                float s = 0.f;
-#pragma unroll
-                for (int k = 0; k < 11; ++k) s = fmaf(c_gw[k], a[j + k], s);
-                hm[q][r][c0 + j] = s;
-            }
-        }
-    }
-    __syncthreads();
-    const int c = tid % kT, rg = (tid / kT) * kRows;
-    float t[kRows][3];
-#pragma unroll
-    for (int q = 0; q < 3; ++q) {
-        float win[kRows + 10];
-#pragma unroll
-        for (int k = 0; k < kRows + 10; ++k) win[k] = hm[q][rg + k][c];
-#pragma unroll
-        for (int j = 0; j < kRows; ++j) {
-            float s = 0.f;
-#pragma unroll
-            for (int k = 0; k < 11; ++k) s = fmaf(c_gw[k], win[j + k], s);
-            t[j][q] = s;
-        }
-    }
-    const bool border_tile = x0 <= 5 || y0 <= 5 || x0 + kT - 1 >= W - 6 || y0 + kT - 1 >= H - 6;
-#pragma unroll
-    for (int j = 0; j < kRows; ++j) {
-        const int x = x0 + c, y = y0 + rg + j;
-        if (x >= W || y >= H) continue;
-        if (border_tile && (x <= 5 || x >= W - 6 || y <= 5 || y >= H - 6)) {
-            // reflect-padding fold terms of the transposed filter
-            int jx[3], jy[3], nx = 0, ny = 0;
-            jx[nx++] = x;
-            if (x >= 1 && x <= 5) jx[nx++] = -x;
-            if (x >= W - 6 && x <= W - 2) jx[nx++] = 2 * (W - 1) - x;
-            jy[ny++] = y;
-            if (y >= 1 && y <= 5) jy[ny++] = -y;
-            if (y >= H - 6 && y <= H - 2) jy[ny++] = 2 * (H - 1) - y;
-            for (int a = 0; a < nx; ++a)
-                for (int b = 0; b < ny; ++b) {
-                    if (a == 0 && b == 0) continue;
-                    for (int q = 0; q < 3; ++q) t[j][q] += window_sum(mp + q * P, jx[a], jy[b], W, H);
-                }
-        }
-        const int p = y * W + x;
-        const float xv = X[size_t(ch) * P + p], yv = Y[size_t(ch) * P + p];
-        const float dS = t[j][0] + xv * t[j][1] + yv * t[j][2];
-        const float d = xv - yv;
-        const float sg = d > 0.f ? 1.f : (d < 0.f ? -1.f : 0.f);
-        dL[size_t(ch) * P + p] = (0.8f * sg - 0.2f * dS) * inv_m;
-    }
-}
-
 }  // namespace
 
 void launch_loss(Context& c, const float* target_chw) {
@@ -254,11 +283,14 @@ void launch_loss(Context& c, const float* target_chw) {
     }
     const int W = c.fw, H = c.fh, P = W * H;
     cudaMemsetAsync(c.loss_acc.p, 0, 2 * sizeof(double), c.stream);
-    const dim3 grid((W + kT - 1) / kT, (H + kT - 1) / kT, 3);
-    loss_fwd_kernel<<<grid, kThreads, 0, c.stream>>>(c.rgb.p, target_chw, c.loss_tmp.p, W, H, c.loss_acc.p);
-    loss_bwd_kernel<<<grid, kThreads, 0, c.stream>>>(c.rgb.p, target_chw, c.loss_tmp.p, c.dLdC.p, W, H,
-                                                     float(1.0 / (3.0 * double(P))));
-    c.launches += 2;
+    static bool attr = false;
+    if (!attr)
+        attr = cudaFuncSetAttribute(loss_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    int(kFusedSmem)) == cudaSuccess;
+    const dim3 grid((W + kFT - 1) / kFT, (H + kFT - 1) / kFT, 3);
+    loss_fused_kernel<<<grid, kFThreads, kFusedSmem, c.stream>>>(c.rgb.p, target_chw, c.dLdC.p, W, H,
+                                                                 float(1.0 / (3.0 * double(P))), c.loss_acc.p);
+    TS_LAUNCHED(c);
 }
 
 }  // namespace ts

@@ -277,7 +277,6 @@ ts_status run_loss(Context& c, const float* target_hwc, int32_t slot, float* out
         if (c.target_w != c.fw || c.target_h != c.fh) return validation(c, "target slot size != view size");
         tgt = c.targets.p + size_t(slot) * 3 * P;
     }
-    if (!ensure(c, c.loss_tmp, 3 * 3 * P)) return TS_ERR_OOM;
     stage_begin(c, 7);
     launch_loss(c, tgt);
     stage_end(c, 7);
@@ -413,7 +412,7 @@ ts_status ts_destroy(ts_ctx* x) {
     }
     release(c.starts), release(c.rhist), release(c.scan_state), release(c.scan_tmp), release(c.counters);
     release(c.rgb), release(c.Tfin), release(c.dLdC), release(c.hwc_stage), release(c.tgt), release(c.pcount);
-    release(c.loss_acc), release(c.loss_tmp), release(c.targets), release(c.dens);
+    release(c.loss_acc), release(c.targets), release(c.dens);
     release(c.binH), release(c.bintot);
     for (size_t k = 0; k < c.ev_b.size(); ++k) {
         cudaEventDestroy(c.ev_b[k]);
@@ -726,6 +725,19 @@ ts_status ts_binning_path(ts_ctx* x, int32_t* radix) {
     TS_CHECK_CTX(x);
     if (radix) *radix = x->c.last_view_radix ? 1 : 0;
     return TS_OK;
+}
+
+ts_status ts_debug_loss_grad(ts_ctx* x, float* dLdC_hwc) {
+    TS_CHECK_CTX(x);
+    Context& c = x->c;
+    if (!c.loss_valid) return validation(c, "no training_loss state");
+    if (!dLdC_hwc) return validation(c, "NULL output");
+    CK(cudaSetDevice(c.device));
+    const size_t P = size_t(c.fw) * c.fh;
+    launch_chw_to_hwc(c, c.dLdC.p, c.hwc_stage.p, int(P));
+    CK(cudaMemcpyAsync(dLdC_hwc, c.hwc_stage.p, 3 * P * 4, cudaMemcpyDeviceToHost, c.stream));
+    CK(cudaStreamSynchronize(c.stream));
+    return last_launch(c, "debug_loss_grad");
 }
 
 ts_status ts_debug_preprocess(ts_ctx* x, float* splat12, int32_t* rect4, uint32_t* tile_count, uint32_t* depth_key) {

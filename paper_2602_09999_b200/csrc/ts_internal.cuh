@@ -77,7 +77,6 @@ struct Context {
     DevBuf<float> rgb, Tfin, dLdC, hwc_stage, tgt;
     DevBuf<uint32_t> pcount;
     DevBuf<double> loss_acc;     // [0] L1 sum, [1] SSIM sum
-    DevBuf<float> loss_tmp;      // 3 channels x 3 SSIM partial-derivative maps (P each)
     DevBuf<float> targets;       // target slots, CHW planar
     int n_target_slots = 0, target_w = 0, target_h = 0;
 

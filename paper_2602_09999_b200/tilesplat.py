@@ -76,6 +76,7 @@ _SIGS = {
     "ts_set_profiling": [_vp, _i32],
     "ts_stage_times": [_vp, _vp, _vp, _i32],
     "ts_set_binning": [_vp, _i32],
+    "ts_debug_loss_grad": [_vp, _vp],
     "ts_binning_path": [_vp, _vp],
     "ts_launch_count": [_vp, ctypes.POINTER(_i64)],
     "ts_host_alloc": [ctypes.c_size_t, ctypes.POINTER(_vp)],
@@ -355,6 +356,13 @@ class Engine:
         cnt = np.zeros(len(STAGES), np.int32)
         self._check(self._L.ts_stage_times(self._h, _ptr(out), _ptr(cnt), len(STAGES)), "ts_stage_times")
         return {k: (float(a), int(b)) for k, a, b in zip(STAGES, out, cnt)}
+
+    def debug_loss_grad(self):
+        """dL/dC (H x W x 3) of the last training_loss, read back from the device."""
+        H, W = self._cam.height, self._cam.width
+        out = np.empty((H, W, 3), np.float32)
+        self._check(self._L.ts_debug_loss_grad(self._h, _ptr(out)), "ts_debug_loss_grad")
+        return out
 
     def set_binning(self, mode: int):
         """0 auto (bucketed binning + per-tile sort), 1 force the two-stage radix sort."""

@@ -139,6 +139,27 @@ def test_loss_parity(sc, engine):
     _grad_check(G[a:b], oG[a:b], "means via loss")
 
 
+@pytest.mark.parametrize("shape", [(256, 256), (637, 419), (40, 33), (75, 140)])
+def test_loss_gradient_map_parity(engine, shape):
+    """dL/dC of the fused SSIM + L1 kernel against the oracle, incl.
+    the reflect-padding fold terms at every border and partial edge tiles."""
+    W, H = shape
+    rng = np.random.default_rng(W * 7 + H)
+    n = 2000
+    p = scene.random_params(n, 0.05, 0.0, 3)
+    cam = scene.make_camera(W, H)
+    cfg = T.RenderConfig.make(sh_degree=1)
+    engine.set_params(p, n)
+    rgb, _, _ = engine.render(cam, cfg)
+    target = np.clip(rgb + rng.normal(0, 0.1, rgb.shape), 0, 1).astype(np.float32)
+    loss = engine.training_loss(target)
+    g = engine.debug_loss_grad()
+    ol, od = O.training_loss(rgb, target)
+    assert abs(loss - ol) <= 1e-5 * max(1.0, abs(ol))
+    scale = np.abs(od).max()
+    assert np.abs(g - od).max() <= 1e-4 * scale, np.abs(g - od).max() / scale
+
+
 @pytest.mark.parametrize("mode", [T.ADAM_REFERENCE, T.ADAM_FUSED])
 def test_adam_bitwise(engine, mode):
     n = 5003  # odd N: unaligned group boundaries exercise the scalar paths

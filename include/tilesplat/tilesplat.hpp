@@ -72,14 +72,19 @@ struct Camera {
     }
 };
 
+// antialias config block: aa = off | filter3d_original | filter3d_clip | full (clip + mip)
+enum class AntiAlias : int32_t { off = 0, filter3d_original = 1, filter3d_clip = 2, full = 3 };
+
 struct RenderConfig {
     int32_t sh_degree = 3;
     int32_t bound_mode = 2;  // rect_opacity
     int32_t cull_mode = 1;   // exact
     int32_t early_stop_compat = 0;
     float tau_alpha = 1.0f / 255.0f;
-    float dilation = 0.3f;
+    float dilation = 0.3f;   // classic 0.3; the Mip 2D filter variance 0.1 with AntiAlias::full
     Vec3<float> background{0.f, 0.f, 0.f};
+    AntiAlias aa = AntiAlias::off;
+    float kappa3d = 0.2f;
 
     ts_render_config abi() const {
         ts_render_config c{};
@@ -87,6 +92,7 @@ struct RenderConfig {
         c.truncation = 0, c.early_stop_compat = early_stop_compat, c.backward_mode = 0;
         c.tau_alpha = tau_alpha, c.dilation = dilation, c.sigma_cut = 3.33f;
         c.bg[0] = background.x, c.bg[1] = background.y, c.bg[2] = background.z;
+        c.aa_mode = static_cast<int32_t>(aa), c.kappa3d = kappa3d;
         return c;
     }
 };
@@ -179,6 +185,13 @@ class Engine {
         return n;
     }
     void opacity_reset() { check(ts_opacity_reset(ctx_), "ts_opacity_reset"); }
+    // antialias: sampling rates over the training views, post-step 3D-filter clip
+    void compute_sampling_rates(const std::vector<Camera>& cams, float extent) {
+        std::vector<ts_camera> c;
+        for (const auto& k : cams) c.push_back(k.abi());
+        check(ts_compute_sampling_rates(ctx_, c.data(), int32_t(c.size()), extent), "ts_compute_sampling_rates");
+    }
+    void apply_3d_filter_clip(float kappa3d = 0.2f) { check(ts_apply_3d_filter_clip(ctx_, kappa3d), "ts_apply_3d_filter_clip"); }
     // morton_reorder: returns perm[new] = old
     std::vector<uint32_t> morton_reorder() {
         std::vector<uint32_t> perm(static_cast<size_t>(size()));

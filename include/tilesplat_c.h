@@ -68,6 +68,9 @@ typedef struct {
     float dilation;            /* 0.3 with AA off (DESIGN.md App. A.1)                   */
     float sigma_cut;           /* reserved (response truncation)                         */
     float bg[3];               /* background colour c_bg                                 */
+    int32_t aa_mode;           /* 0 off, 1 filter3d_original, 2 filter3d_clip, 3 full    */
+                               /* (clip + Mip 2D filter, dilation 0.1) */
+    float kappa3d;             /* 3D filter variance kappa_3D, 0.2         */
 } ts_render_config;
 
 /* Adam: per-group lr (means, log_scales, quats, opacity,
@@ -139,6 +142,16 @@ ts_status ts_opacity_reset(ts_ctx* ctx);
 /* morton_reorder: permute params, Adam moments and densify statistics into
  * 63-bit Morton order of the means; perm (N, may be NULL) receives old index per new row. */
 ts_status ts_morton_reorder(ts_ctx* ctx, uint32_t* perm);
+
+/* ---- antialias ---- */
+/* compute_sampling_rates: nu[g] = max over the cameras whose frustum (z > near, |x/z|, |y/z| within
+ * the 1.3 tan(fov/2) J-clamp limits) contains the mean of max(fx, fy) / z; 1 / extent if none.
+ * Kept by the context for aa_mode 1 and the 3D-filter clip; invalidated by densify / reorder. */
+ts_status ts_compute_sampling_rates(ts_ctx* ctx, const ts_camera* cams, int32_t n_cams, float extent);
+ts_status ts_set_sampling_rates(ts_ctx* ctx, const float* nu /* N host */);
+ts_status ts_get_sampling_rates(ts_ctx* ctx, float* nu /* N host */);
+/* apply_3d_filter_clip: log_scales <- max(log_scales, log(sqrt(kappa3d) / nu)) (after an optimizer step) */
+ts_status ts_apply_3d_filter_clip(ts_ctx* ctx, float kappa3d);
 
 /* ---- state access for tests / checkpointing ---- */
 ts_status ts_set_state(ts_ctx* ctx, const float* grads, const float* m, const float* v, const float* accum,

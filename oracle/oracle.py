@@ -73,6 +73,9 @@ def _load():
                                              f32p, f32p, f64p]),
         "tso_sh_active_degree": (ctypes.c_int32, [i64]),
         "tso_scene_extent": (ctypes.c_double, [ctypes.c_int32, f64p]),
+        "tso_compute_sampling_rates": (None, [i64, f32p, vp, ctypes.c_int32, ctypes.c_float, f32p]),
+        "tso_set_sampling_rates": (None, [i64, f32p]),
+        "tso_apply_3d_filter_clip": (None, [i64, f32p, f32p, ctypes.c_float]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -90,6 +93,29 @@ def _p(s):
 
 def set_workers(n: int):
     lib.tso_set_workers(int(n))
+
+
+def compute_sampling_rates(params, n, cams, extent):
+    """compute_sampling_rates (SPEC.md:618-626)."""
+    from paper_2602_09999_b200.types import Camera
+    arr = (Camera * len(cams))(*cams)
+    nu = np.zeros(n, np.float32)
+    lib.tso_compute_sampling_rates(n, np.ascontiguousarray(params, np.float32), ctypes.addressof(arr), len(cams),
+                                   float(extent), nu)
+    return nu
+
+
+def set_sampling_rates(nu):
+    """sampling rates used by preprocess / backward with aa_mode 1 (filter3d_original)."""
+    nu = np.ascontiguousarray(nu, np.float32)
+    lib.tso_set_sampling_rates(nu.size, nu)
+
+
+def apply_3d_filter_clip(params, n, nu, kappa3d=0.2):
+    """apply_3d_filter_clip on a copy of the flat parameter array."""
+    out = np.array(params, np.float32, copy=True)
+    lib.tso_apply_3d_filter_clip(n, out, np.ascontiguousarray(nu, np.float32), float(kappa3d))
+    return out
 
 
 def preprocess(params, n, cam, cfg):

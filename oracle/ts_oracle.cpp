@@ -169,6 +169,7 @@ struct M<double> {
 
 constexpr int TILE = 16;
 constexpr int NPARAM = 59;
+std::vector<float> g_nu;  // sampling rates for aa_mode 1 (tso_set_sampling_rates)
 struct Off {
     int64_t means, ls, q, op, dc, rest;
     explicit Off(int64_t n) : means(0), ls(3 * n), q(6 * n), op(10 * n), dc(11 * n), rest(14 * n) {}
@@ -296,7 +297,11 @@ struct GFwd {
     T a, b, c, det;            // dilated cov2d and its determinant
     T A, B, C;                 // conic
     T mx, my;                  // mean2d
-    T o;                       // opacity
+    T o;                       // effective opacity (after the AA compensation factor)
+    T o_raw;                   // sigmoid(logit)
+    T ofac;                    // o = o_raw * ofac (3D filter ratio or Mip compensation; 1 when AA off)
+    T s_raw[3], s_h[3];        // aa_mode 1: activated scales before the 3D filter, s^2 + kappa/nu^2
+    T aaf;                     // aa_mode 1: kappa / nu^2
     T k2;                      // alpha level set: Q <= k2  <=>  o*exp(-Q/2) >= tau
     bool has_bound;            // o > tau
     T dir[3], dlen;            // unit view direction, |mu - campos|
@@ -344,6 +349,21 @@ GFwd<T> gaussian_forward(const T* P, int64_t N, int64_t g, const Cam<T>& cam, co
     }
     // activate_scales, build_covariance3d: Sigma = (R S)(R S)^T
     for (int k = 0; k < 3; ++k) F.s[k] = M<T>::exp_(ls[k]);
+    F.ofac = T(1);
+    if (cfg.aa_mode == 1) {
+        // apply_3d_filter_original: s_hat = sqrt(s^2 + kappa/nu^2),
+        // opacity factor sqrt(prod s^2 / prod s_hat^2)
+        const T nu = T(g_nu.empty() ? 1.0f : g_nu[size_t(g)]);
+        F.aaf = T(cfg.kappa3d) / (nu * nu);
+        T q[3];
+        for (int k = 0; k < 3; ++k) {
+            F.s_raw[k] = F.s[k];
+            q[k] = F.s[k] * F.s[k];
+            F.s_h[k] = q[k] + F.aaf;
+            F.s[k] = std::sqrt(F.s_h[k]);
+        }
+        F.ofac = std::sqrt(((q[0] * q[1]) * q[2]) / ((F.s_h[0] * F.s_h[1]) * F.s_h[2]));
+    }
     for (int i = 0; i < 3; ++i)
         for (int k = 0; k < 3; ++k) F.Mm[3 * i + k] = F.R[3 * i + k] * F.s[k];
     const T* Mm = F.Mm;
@@ -382,6 +402,7 @@ GFwd<T> gaussian_forward(const T* P, int64_t N, int64_t g, const Cam<T>& cam, co
     T b = (U[0] * F.Tm[3] + U[1] * F.Tm[4]) + U[2] * F.Tm[5];
     T c = (U[3] * F.Tm[3] + U[4] * F.Tm[4]) + U[5] * F.Tm[5];
     // invert_cov2d with dilation; degenerate if det < 1e-6
+    const T det_pre = a * c - b * b;
     T dil = T(cfg.dilation);
     a = a + dil;
     c = c + dil;
@@ -396,9 +417,11 @@ GFwd<T> gaussian_forward(const T* P, int64_t N, int64_t g, const Cam<T>& cam, co
     F.C = a / det;
     F.mx = cam.fx * F.txz + cam.cx;
     F.my = cam.fy * F.tyz + cam.cy;
-    // activate_opacity
+    // activate_opacity; AA compensation (SPEC.md:646-654 mip: sqrt(det_pre / det_post), detached)
     T logit = P[off.op + g];
-    F.o = T(1) / (T(1) + M<T>::exp_(-logit));
+    F.o_raw = T(1) / (T(1) + M<T>::exp_(-logit));
+    if (cfg.aa_mode == 3) F.ofac = det_pre > T(0) ? std::sqrt(det_pre / det) : T(0);
+    F.o = (cfg.aa_mode == 1 || cfg.aa_mode == 3) ? F.o_raw * F.ofac : F.o_raw;
     T tau = T(cfg.tau_alpha);
     F.has_bound = F.o > tau;
     F.k2 = F.has_bound ? T(-2) * M<T>::log_(tau / F.o) : T(0);
@@ -976,8 +999,8 @@ void project_backward(const T* P, int64_t N, int64_t g, const GFwd<T>& F, const 
     T nd = F.dir[0] * ddir[0] + F.dir[1] * ddir[1] + F.dir[2] * ddir[2];
     T dmean[3];
     for (int a = 0; a < 3; ++a) dmean[a] = (ddir[a] - F.dir[a] * nd) / F.dlen;
-    // --- opacity
-    G[off.op + g] += dop * F.o * (T(1) - F.o);
+    // --- opacity (through the AA factor; the Mip compensation is detached from Sigma2D)
+    G[off.op + g] += ((dop * F.ofac) * F.o_raw) * (T(1) - F.o_raw);
     // --- conic -> dilated cov2d: dS' = -C' Gc C', Gc = [[dA, dB/2],[dB/2, dC]]
     T hb = T(0.5) * dB;
     T K00 = F.A * dA + F.B * hb, K01 = F.A * hb + F.B * dC;
@@ -1045,7 +1068,10 @@ void project_backward(const T* P, int64_t N, int64_t g, const GFwd<T>& F, const 
             ds += F.R[3 * i + k] * dM[3 * i + k];
             dR[3 * i + k] = dM[3 * i + k] * F.s[k];
         }
-        G[off.ls + 3 * g + k] += ds * F.s[k];
+        if (cfg.aa_mode == 1)  // through s_hat = sqrt(s^2 + f) and the opacity factor
+            G[off.ls + 3 * g + k] += ds * ((F.s_raw[k] * F.s_raw[k]) / F.s[k]) + ((dop * F.o_raw) * F.ofac) * (F.aaf / F.s_h[k]);
+        else
+            G[off.ls + 3 * g + k] += ds * F.s[k];
     }
     T w = F.qw, x = F.qx, y = F.qy, zq = F.qz;
     T dqw = T(2) * (-zq * dR[1] + y * dR[2] + zq * dR[3] - x * dR[5] - y * dR[6] + x * dR[7]);
@@ -1597,6 +1623,51 @@ double tso_train_step(int64_t n, float* params, float* m, float* v, const tso_ca
 }
 
 int32_t tso_sh_active_degree(int64_t iter) { return int32_t(std::min<int64_t>(3, iter / 1000)); }
+
+void tso_set_sampling_rates(int64_t n, const float* nu) { g_nu.assign(nu, nu + n); }
+
+// compute_sampling_rates; project_mean op order, J-clamp frustum
+void tso_compute_sampling_rates(int64_t n, const float* params, const tso_camera* cams, int32_t ncams, float extent,
+                                float* nu) {
+    Off off(n);
+    std::vector<Cam<float>> cs;
+    for (int k = 0; k < ncams; ++k) cs.emplace_back(cams[k]);
+    const float fallback = 1.0f / extent;
+    pfor(n, [&](int64_t b, int64_t e) {
+        for (int64_t g = b; g < e; ++g) {
+            const float* mu = params + off.means + 3 * g;
+            float best = 0.0f;
+            bool any = false;
+            for (const auto& cam : cs) {
+                const float* W = cam.W;
+                const float xh = ((W[0] * mu[0] + W[1] * mu[1]) + W[2] * mu[2]) + W[3];
+                const float yh = ((W[4] * mu[0] + W[5] * mu[1]) + W[6] * mu[2]) + W[7];
+                const float zh = ((W[8] * mu[0] + W[9] * mu[1]) + W[10] * mu[2]) + W[11];
+                if (!(zh > cam.nearp)) continue;
+                const float tx = xh / zh, ty = yh / zh;
+                if (tx < -cam.limx || tx > cam.limx || ty < -cam.limy || ty > cam.limy) continue;
+                const float f = cam.fx > cam.fy ? cam.fx : cam.fy;
+                const float v = f / zh;
+                best = any ? (v > best ? v : best) : v;
+                any = true;
+            }
+            nu[g] = any ? best : fallback;
+        }
+    });
+}
+
+// apply_3d_filter_clip in log space
+void tso_apply_3d_filter_clip(int64_t n, float* params, const float* nu, float kappa3d) {
+    Off off(n);
+    const float sk = std::sqrt(kappa3d);
+    for (int64_t g = 0; g < n; ++g) {
+        const float fl = soft_logf(sk / nu[g]);
+        for (int k = 0; k < 3; ++k) {
+            float& l = params[off.ls + 3 * g + k];
+            l = l < fl ? fl : l;
+        }
+    }
+}
 
 double tso_scene_extent(int32_t nc, const double* c) {
     if (nc <= 1) return 1.0;

@@ -46,7 +46,20 @@ typedef struct {
     float dilation;           /* 0.3 when AA off */
     float sigma_cut;          /* response truncation (unused in classic) */
     float bg[3];
+    int32_t aa_mode;          /* 0 off, 1 filter3d_original, 2 filter3d_clip, 3 full = clip + mip */
+    float kappa3d;            /* 3D filter variance kappa_3D = 0.2 */
 } tso_render_config;
+
+/* ---- antialias ---- */
+/* compute_sampling_rates: nu[g] = max over cameras where the mean passes frustum culling
+ * (z > near, |x/z| <= 1.3 tan(fov_x/2), |y/z| <= 1.3 tan(fov_y/2)) of max(fx, fy) / z;
+ * 1 / extent when visible in none. */
+void tso_compute_sampling_rates(int64_t n, const float* params, const tso_camera* cams, int32_t ncams, float extent,
+                                float* nu);
+/* sampling rates used by preprocess / backward in aa_mode 1 (filter3d_original) */
+void tso_set_sampling_rates(int64_t n, const float* nu);
+/* apply_3d_filter_clip: log_scales <- max(log_scales, log(sqrt(kappa) / nu)), in place */
+void tso_apply_3d_filter_clip(int64_t n, float* params, const float* nu, float kappa3d);
 
 /* worker threads used by every parallel loop (0 = hardware_concurrency) */
 void tso_set_workers(int n);

@@ -92,6 +92,47 @@ __global__ void __launch_bounds__(256) adam_kernel(float4* __restrict__ th, floa
     if (ZERO) g[q] = g4;
 }
 
+// compute_sampling_rates: per Gaussian the max over cameras whose
+// J-clamp frustum contains the mean of max(fx, fy) / z; 1 / extent when none.  Same
+// op order as the oracle's tso_compute_sampling_rates (project_mean, exact ops).
+__global__ void sampling_rate_kernel(const float* __restrict__ means, int64_t N, const DevCam* __restrict__ cams,
+                                     int ncams, float fallback, float* __restrict__ nu) {
+    using namespace tsx;
+    const int64_t g = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (g >= N) return;
+    const float m0 = means[3 * g], m1 = means[3 * g + 1], m2 = means[3 * g + 2];
+    float best = 0.f;
+    bool any = false;
+    for (int k = 0; k < ncams; ++k) {
+        const DevCam& cam = cams[k];
+        const float* W = cam.W;
+        const float xh = add(add(add(mul(W[0], m0), mul(W[1], m1)), mul(W[2], m2)), W[3]);
+        const float yh = add(add(add(mul(W[4], m0), mul(W[5], m1)), mul(W[6], m2)), W[7]);
+        const float zh = add(add(add(mul(W[8], m0), mul(W[9], m1)), mul(W[10], m2)), W[11]);
+        if (!(zh > cam.nearp)) continue;
+        const float limx = mul(1.3f, div(mul(0.5f, float(cam.w)), cam.fx));
+        const float limy = mul(1.3f, div(mul(0.5f, float(cam.h)), cam.fy));
+        const float tx = div(xh, zh), ty = div(yh, zh);
+        if (tx < -limx || tx > limx || ty < -limy || ty > limy) continue;
+        const float v = div(cam.fx > cam.fy ? cam.fx : cam.fy, zh);
+        best = any ? (v > best ? v : best) : v;
+        any = true;
+    }
+    nu[g] = any ? best : fallback;
+}
+
+// apply_3d_filter_clip: log_scales <- max(log_scales, log(sqrt(kappa) / nu))
+__global__ void filter3d_clip_kernel(float* __restrict__ ls, const float* __restrict__ nu, int64_t N, float sk) {
+    const int64_t g = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (g >= N) return;
+    const float fl = tsx::logf_det(tsx::div(sk, nu[g]));
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        const float l = ls[3 * g + k];
+        ls[3 * g + k] = l < fl ? fl : l;
+    }
+}
+
 __global__ void hwc_to_chw_kernel(const float* __restrict__ hwc, float* __restrict__ chw, int P) {
     const int p = blockIdx.x * blockDim.x + threadIdx.x;
     if (p >= P) return;
@@ -151,6 +192,26 @@ void launch_adam(Context& c, const ts_adam_config& a, int64_t begin, int64_t end
         else TS_ADAM(0, false);
     }
 #undef TS_ADAM
+    TS_LAUNCHED(c);
+}
+
+bool launch_sampling_rates(Context& c, const DevCam* cams_host, int ncams, float extent) {
+    if (c.N == 0) return true;
+    DevBuf<DevCam> dc;
+    if (!ensure(c, dc, size_t(ncams))) return false;
+    cudaMemcpyAsync(dc.p, cams_host, sizeof(DevCam) * ncams, cudaMemcpyHostToDevice, c.stream);
+    sampling_rate_kernel<<<unsigned((c.N + 255) / 256), 256, 0, c.stream>>>(c.params.p, c.N, dc.p, ncams,
+                                                                            1.0f / extent, c.nu_hat.p);
+    TS_LAUNCHED(c);
+    const bool ok = cudaStreamSynchronize(c.stream) == cudaSuccess;
+    cudaFree(dc.p);
+    return ok;
+}
+
+void launch_filter3d_clip(Context& c, float kappa3d) {
+    if (c.N == 0) return;
+    filter3d_clip_kernel<<<unsigned((c.N + 255) / 256), 256, 0, c.stream>>>(c.params.p + 3 * c.N, c.nu_hat.p, c.N,
+                                                                            std::sqrt(kappa3d));
     TS_LAUNCHED(c);
 }
 

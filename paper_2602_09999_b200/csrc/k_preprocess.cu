@@ -17,7 +17,7 @@ template <int DEG>
 __global__ void __launch_bounds__(kBlock) preprocess_kernel(
     const float* __restrict__ P, int64_t N, DevCam cam, ts_render_config cfg, float4* __restrict__ splat,
     uint4* __restrict__ rect, uint32_t* __restrict__ tcount, uint32_t* __restrict__ dkey,
-    uint32_t* __restrict__ dperm, uint32_t* __restrict__ vis_counter) {
+    uint32_t* __restrict__ dperm, uint32_t* __restrict__ vis_counter, const float* __restrict__ nu_hat) {
     using namespace tsx;
     // staged inputs of the CTA's 128 Gaussians (one pass of independent 16-byte loads)
     constexpr int kMu = 0, kLs = kMu + 3 * kBlock + 4, kQ = kLs + 3 * kBlock + 4, kOp = kQ + 4 * kBlock + 4,
@@ -89,6 +89,20 @@ __global__ void __launch_bounds__(kBlock) preprocess_kernel(
         sc[0] = expf_det(lss[0]);
         sc[1] = expf_det(lss[1]);
         sc[2] = expf_det(lss[2]);
+        float ofac = 1.f;
+        if (cfg.aa_mode == 1) {
+            // apply_3d_filter_original, exact ops (feeds the tile rect)
+            const float nu = nu_hat[g];
+            const float f = div(cfg.kappa3d, mul(nu, nu));
+            float q[3], hh[3];
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+                q[k] = mul(sc[k], sc[k]);
+                hh[k] = add(q[k], f);
+                sc[k] = sqrt_(hh[k]);
+            }
+            ofac = sqrt_(div(mul(mul(q[0], q[1]), q[2]), mul(mul(hh[0], hh[1]), hh[2])));
+        }
         float Mm[9];
 #pragma unroll
         for (int i = 0; i < 3; ++i)
@@ -128,6 +142,7 @@ __global__ void __launch_bounds__(kBlock) preprocess_kernel(
         const float b = add(add(mul(U[0], Tm[3]), mul(U[1], Tm[4])), mul(U[2], Tm[5]));
         float c = add(add(mul(U[3], Tm[3]), mul(U[4], Tm[4])), mul(U[5], Tm[5]));
         // invert_cov2d with dilation
+        const float det_pre = sub(mul(a, c), mul(b, b));
         a = add(a, cfg.dilation);
         c = add(c, cfg.dilation);
         const float det = sub(mul(a, c), mul(b, b));
@@ -136,7 +151,10 @@ __global__ void __launch_bounds__(kBlock) preprocess_kernel(
         const float mx = add(mul(cam.fx, txz), cam.cx), my = add(mul(cam.fy, tyz), cam.cy);
         // activate_opacity; alpha level set Q <= k2  <=>  o exp(-Q/2) >= tau
         const float logit = sm[kOp + sh[3] + tid];
-        const float o = div(1.f, add(1.f, expf_det(-logit)));
+        const float o_raw = div(1.f, add(1.f, expf_det(-logit)));
+        // Mip compensation: sqrt(det_pre / det_post), detached in the backward
+        if (cfg.aa_mode == 3) ofac = det_pre > 0.f ? sqrt_(div(det_pre, det)) : 0.f;
+        const float o = (cfg.aa_mode == 1 || cfg.aa_mode == 3) ? mul(o_raw, ofac) : o_raw;
         const float tau = cfg.tau_alpha;
         const bool has_bound = o > tau;
         const float k2 = has_bound ? mul(-2.f, logf_det(div(tau, o))) : 0.f;
@@ -255,7 +273,7 @@ void launch_preprocess(Context& c, const DevCam& cam, const ts_render_config& cf
 #define TS_PRE(D)                                                                                      \
     preprocess_kernel<D><<<unsigned(blocks), kBlock, 0, c.stream>>>(c.params.p, c.N, cam, cfg, c.splat.p, \
                                                                      c.rect.p, c.tcount.p, c.dkey[0].p,   \
-                                                                     c.dperm[0].p, c.counters.p + 1)
+                                                                     c.dperm[0].p, c.counters.p + 1, c.nu_hat.p)
     switch (cfg.sh_degree) {
         case 0: TS_PRE(0); break;
         case 1: TS_PRE(1); break;

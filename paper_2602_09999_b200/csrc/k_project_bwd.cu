@@ -27,6 +27,14 @@
 namespace ts {
 namespace {
 
+// ex2.approx with the scaling multiply pinned (__fmul_rn): the scale activation
+// feeds several consumers and must not be contracted differently per kernel
+__device__ __forceinline__ float exp2f_approx_(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
 // staged per-Gaussian rows of one Gaussian
 struct Rows {
     const float* mu;   // 3
@@ -43,7 +51,7 @@ struct Rows {
 // written to grest.  Returns |dL/dmean2d| for the densification statistics.
 template <int DEG>
 __device__ __forceinline__ float pb_grads(const Rows& r, float* grest, const DevCam& cam,
-                                          const ts_render_config& cfg, float (&gs)[14]) {
+                                          const ts_render_config& cfg, float nu, float (&gs)[14]) {
     constexpr int nb = (DEG + 1) * (DEG + 1);
     const float* W = cam.W;
     const float dmx = r.g2[0], dmy = r.g2[1], dA = r.g2[2], dB = r.g2[3], dC = r.g2[4], dop = r.g2[5];
@@ -58,18 +66,33 @@ __device__ __forceinline__ float pb_grads(const Rows& r, float* grest, const Dev
     const float iqn = 1.f / qn;
     const float w = q0 * iqn, x = q1 * iqn, y = q2 * iqn, z = q3 * iqn;
     float R[9];
-    R[0] = 1.f - 2.f * (y * y + z * z);
-    R[1] = 2.f * (x * y - w * z);
-    R[2] = 2.f * (x * z + w * y);
-    R[3] = 2.f * (x * y + w * z);
-    R[4] = 1.f - 2.f * (x * x + z * z);
-    R[5] = 2.f * (y * z - w * x);
-    R[6] = 2.f * (x * z - w * y);
-    R[7] = 2.f * (y * z + w * x);
-    R[8] = 1.f - 2.f * (x * x + y * y);
-    float s[3];
+    // explicit fma order (R feeds the scale gradient directly; both kernels inlining
+    // this adjoint must round identically, see test_fused_backward_adam_equals_separate)
+    R[0] = fmaf(-2.f, fmaf(y, y, z * z), 1.f);
+    R[1] = 2.f * fmaf(x, y, -(w * z));
+    R[2] = 2.f * fmaf(x, z, w * y);
+    R[3] = 2.f * fmaf(x, y, w * z);
+    R[4] = fmaf(-2.f, fmaf(x, x, z * z), 1.f);
+    R[5] = 2.f * fmaf(y, z, -(w * x));
+    R[6] = 2.f * fmaf(x, z, -(w * y));
+    R[7] = 2.f * fmaf(y, z, w * x);
+    R[8] = fmaf(-2.f, fmaf(x, x, y * y), 1.f);
+    float s[3], s_raw[3], s_h[3], aaf = 0.f, ofac = 1.f;
 #pragma unroll
-    for (int k = 0; k < 3; ++k) s[k] = __expf(r.ls[k]);
+    for (int k = 0; k < 3; ++k) s[k] = s_raw[k] = exp2f_approx_(__fmul_rn(r.ls[k], 1.44269504088896341f));
+    if (cfg.aa_mode == 1) {  // 3D filter: s_hat = sqrt(s^2 + kappa/nu^2), opacity factor
+        aaf = cfg.kappa3d / (nu * nu);
+        float qp = 1.f, hp = 1.f;
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            const float q = s_raw[k] * s_raw[k];
+            s_h[k] = q + aaf;
+            s[k] = sqrtf(s_h[k]);
+            qp *= q;
+            hp *= s_h[k];
+        }
+        ofac = sqrtf(qp / hp);
+    }
     float Mm[9];
 #pragma unroll
     for (int i = 0; i < 3; ++i)
@@ -102,9 +125,14 @@ __device__ __forceinline__ float pb_grads(const Rows& r, float* grest, const Dev
 #pragma unroll
         for (int j = 0; j < 3; ++j)
             TS[3 * a + j] = Tm[3 * a] * Sf[j] + Tm[3 * a + 1] * Sf[3 + j] + Tm[3 * a + 2] * Sf[6 + j];
-    const float ca = TS[0] * Tm[0] + TS[1] * Tm[1] + TS[2] * Tm[2] + cfg.dilation;
+    const float ca0 = TS[0] * Tm[0] + TS[1] * Tm[1] + TS[2] * Tm[2];
     const float cb = TS[0] * Tm[3] + TS[1] * Tm[4] + TS[2] * Tm[5];
-    const float cc = TS[3] * Tm[3] + TS[4] * Tm[4] + TS[5] * Tm[5] + cfg.dilation;
+    const float cc0 = TS[3] * Tm[3] + TS[4] * Tm[4] + TS[5] * Tm[5];
+    const float ca = ca0 + cfg.dilation, cc = cc0 + cfg.dilation;
+    if (cfg.aa_mode == 3) {  // Mip compensation factor, detached from Sigma2D
+        const float dpre = ca0 * cc0 - cb * cb;
+        ofac = dpre > 0.f ? sqrtf(dpre / (ca * cc - cb * cb)) : 0.f;
+    }
     const float idet = 1.f / (ca * cc - cb * cb);
     const float A = cc * idet, B = -cb * idet, C = ca * idet;
     const float o = 1.f / (1.f + __expf(-r.op));
@@ -198,7 +226,7 @@ __device__ __forceinline__ float pb_grads(const Rows& r, float* grest, const Dev
     const float nd = d0 * ddir0 + d1 * ddir1 + d2 * ddir2;
     float dmean0 = (ddir0 - d0 * nd) * idl, dmean1 = (ddir1 - d1 * nd) * idl, dmean2 = (ddir2 - d2 * nd) * idl;
     // ---- opacity ----
-    gs[10] = dop * o * (1.f - o);
+    gs[10] = dop * ofac * o * (1.f - o);
     // ---- conic -> dilated cov2d ----
     const float hb = 0.5f * dB;
     const float K00 = A * dA + B * hb, K01 = A * hb + B * dC;
@@ -213,7 +241,8 @@ __device__ __forceinline__ float pb_grads(const Rows& r, float* grest, const Dev
     for (int i = 0; i < 3; ++i)
 #pragma unroll
         for (int j = 0; j < 3; ++j)
-            dS[3 * i + j] = Tm[i] * (G2[0] * Tm[j] + G2[1] * Tm[3 + j]) + Tm[3 + i] * (G2[2] * Tm[j] + G2[3] * Tm[3 + j]);
+            dS[3 * i + j] = fmaf(Tm[3 + i], fmaf(G2[2], Tm[j], G2[3] * Tm[3 + j]),
+                                 Tm[i] * fmaf(G2[0], Tm[j], G2[1] * Tm[3 + j]));
     float dTm[6];
 #pragma unroll
     for (int a = 0; a < 2; ++a)
@@ -248,14 +277,19 @@ __device__ __forceinline__ float pb_grads(const Rows& r, float* grest, const Dev
     for (int i = 0; i < 3; ++i)
 #pragma unroll
         for (int k = 0; k < 3; ++k)
-            dM[3 * i + k] = 2.f * (dS[3 * i] * Mm[k] + dS[3 * i + 1] * Mm[3 + k] + dS[3 * i + 2] * Mm[6 + k]);
+            dM[3 * i + k] = 2.f * fmaf(dS[3 * i + 2], Mm[6 + k], fmaf(dS[3 * i + 1], Mm[3 + k], dS[3 * i] * Mm[k]));
     float dR[9];
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
-        const float ds = R[k] * dM[k] + R[3 + k] * dM[3 + k] + R[6 + k] * dM[6 + k];
+        // explicit fma order: both kernels that inline this adjoint (gradient-writing and
+        // fused-Adam) must produce the same bits (fused_backward_update == separate pair)
+        const float ds = fmaf(R[6 + k], dM[6 + k], fmaf(R[3 + k], dM[3 + k], R[k] * dM[k]));
 #pragma unroll
         for (int i = 0; i < 3; ++i) dR[3 * i + k] = dM[3 * i + k] * s[k];
-        gs[3 + k] = ds * s[k];
+        if (cfg.aa_mode == 1)  // through s_hat = sqrt(s^2 + kappa/nu^2) and the opacity factor
+            gs[3 + k] = fmaf(ds, s_raw[k] * s_raw[k] / s[k], dop * o * ofac * (aaf / s_h[k]));
+        else
+            gs[3 + k] = __fmul_rn(ds, s[k]);
     }
     const float dqw = 2.f * (-z * dR[1] + y * dR[2] + z * dR[3] - x * dR[5] - y * dR[6] + x * dR[7]);
     const float dqx = 2.f * (y * dR[1] + z * dR[2] + y * dR[3] - 2.f * x * dR[4] - w * dR[5] + z * dR[6] + w * dR[7] -
@@ -299,7 +333,8 @@ __global__ void __launch_bounds__(kBlock) project_bwd_kernel(const float* __rest
                                                              const uint32_t* __restrict__ tcount,
                                                              float* __restrict__ accum, float* __restrict__ vcount,
                                                              uint8_t* __restrict__ vis, int64_t N, DevCam cam,
-                                                             ts_render_config cfg, int zero_inactive) {
+                                                             ts_render_config cfg, int zero_inactive,
+                                                             const float* __restrict__ nu_hat) {
     extern __shared__ __align__(16) float smem[];
     using L = PbLayout<DEG, ACCUM>;
     constexpr int nrest = 3 * ((DEG + 1) * (DEG + 1) - 1);
@@ -349,14 +384,14 @@ __global__ void __launch_bounds__(kBlock) project_bwd_kernel(const float* __rest
         float nrm;
         if constexpr (ACCUM && nrest > 0) {
             float grest[nrest];
-            nrm = pb_grads<DEG>(rw, grest, cam, cfg, gs);
+            nrm = pb_grads<DEG>(rw, grest, cam, cfg, nu_hat ? nu_hat[g] : 1.f, gs);
             float* grow = smem + L::kGRest + sh[9] + tid * 45;
 #pragma unroll
             for (int k = 0; k < nrest; ++k) grow[k] += grest[k];
         } else {
             // overwrite mode: gradients replace the parameter row in place (each
             // element is read by pb_grads before it is written)
-            nrm = pb_grads<DEG>(rw, DEG > 0 ? rest_row : dummy, cam, cfg, gs);
+            nrm = pb_grads<DEG>(rw, DEG > 0 ? rest_row : dummy, cam, cfg, nu_hat ? nu_hat[g] : 1.f, gs);
         }
         const int64_t idx[14] = {off.means + 3 * g,  off.means + 3 * g + 1, off.means + 3 * g + 2, off.ls + 3 * g,
                                  off.ls + 3 * g + 1, off.ls + 3 * g + 2,    off.q + 4 * g,         off.q + 4 * g + 1,
@@ -449,7 +484,8 @@ __global__ void __launch_bounds__(kFB, 4) project_bwd_adam_kernel(float* __restr
                                                                   float* __restrict__ accum,
                                                                   float* __restrict__ vcount,
                                                                   uint8_t* __restrict__ vis, int64_t N, DevCam cam,
-                                                                  ts_render_config cfg, FusedAdam fa) {
+                                                                  ts_render_config cfg, FusedAdam fa,
+                                                                  const float* __restrict__ nu_hat) {
     extern __shared__ __align__(16) float smem[];
     using L = FbLayout;
     constexpr int width[6] = {3, 3, 4, 1, 3, 45};
@@ -493,7 +529,7 @@ __global__ void __launch_bounds__(kFB, 4) project_bwd_adam_kernel(float* __restr
         if (active) {
             const Rows rw{pr[0], pr[1], pr[2], pr[3][0], pr[4], pr[5], smem + L::kG2 + sh[6] + 12 * tid};
             // in place: every SH-rest element is read before its gradient is written
-            const float nrm = pb_grads<DEG>(rw, pr[5], cam, cfg, gs);
+            const float nrm = pb_grads<DEG>(rw, pr[5], cam, cfg, nu_hat ? nu_hat[g] : 1.f, gs);
             reinterpret_cast<float4*>(g2d)[3 * g] = make_float4(0.f, 0.f, 0.f, 0.f);
             reinterpret_cast<float4*>(g2d)[3 * g + 1] = make_float4(0.f, 0.f, 0.f, 0.f);
             reinterpret_cast<float4*>(g2d)[3 * g + 2] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -557,13 +593,13 @@ void launch_project_bwd(Context& c, const DevCam& cam, const ts_render_config& c
         constexpr int sm = PbLayout<D, true>::kTotal * 4;                                             \
         { static bool a_ = false; if (!a_) a_ = cudaFuncSetAttribute(project_bwd_kernel<D, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm) == cudaSuccess; } \
         project_bwd_kernel<D, true><<<unsigned(blocks), kBlock, sm, c.stream>>>(                      \
-            c.params.p, c.grads.p, c.g2d.p, c.tcount.p, c.accum.p, c.vcount.p, c.vis.p, c.N, cam, cfg, 0); \
+            c.params.p, c.grads.p, c.g2d.p, c.tcount.p, c.accum.p, c.vcount.p, c.vis.p, c.N, cam, cfg, 0, c.nu_hat.p); \
     } else {                                                                                          \
         constexpr int sm = PbLayout<D, false>::kTotal * 4;                                            \
         { static bool a_ = false; if (!a_) a_ = cudaFuncSetAttribute(project_bwd_kernel<D, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm) == cudaSuccess; } \
         project_bwd_kernel<D, false><<<unsigned(blocks), kBlock, sm, c.stream>>>(                     \
             c.params.p, c.grads.p, c.g2d.p, c.tcount.p, c.accum.p, c.vcount.p, c.vis.p, c.N, cam, cfg,   \
-            int(zero_inactive));                                                                       \
+            int(zero_inactive), c.nu_hat.p);                                                                     \
     }
     switch (cfg.sh_degree) {
         case 0: TS_PB(0); break;
@@ -592,11 +628,11 @@ void launch_project_bwd_adam(Context& c, const DevCam& cam, const ts_render_conf
     if (skip) {                                                                                           \
         { static bool a_ = false; if (!a_) a_ = cudaFuncSetAttribute(project_bwd_adam_kernel<D, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm) == cudaSuccess; } \
         project_bwd_adam_kernel<D, true><<<unsigned(blocks), kFB, sm, c.stream>>>(                        \
-            c.params.p, c.m.p, c.v.p, c.g2d.p, c.tcount.p, c.accum.p, c.vcount.p, c.vis.p, c.N, cam, cfg, fa); \
+            c.params.p, c.m.p, c.v.p, c.g2d.p, c.tcount.p, c.accum.p, c.vcount.p, c.vis.p, c.N, cam, cfg, fa, c.nu_hat.p); \
     } else {                                                                                              \
         { static bool a_ = false; if (!a_) a_ = cudaFuncSetAttribute(project_bwd_adam_kernel<D, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm) == cudaSuccess; } \
         project_bwd_adam_kernel<D, false><<<unsigned(blocks), kFB, sm, c.stream>>>(                       \
-            c.params.p, c.m.p, c.v.p, c.g2d.p, c.tcount.p, c.accum.p, c.vcount.p, c.vis.p, c.N, cam, cfg, fa); \
+            c.params.p, c.m.p, c.v.p, c.g2d.p, c.tcount.p, c.accum.p, c.vcount.p, c.vis.p, c.N, cam, cfg, fa, c.nu_hat.p); \
     }
     switch (cfg.sh_degree) {
         case 0: TS_FB(0); break;

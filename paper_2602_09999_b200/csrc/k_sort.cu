@@ -527,6 +527,11 @@ bool launch_morton_reorder(Context& c, uint32_t* perm_host) {
     cudaMemcpyAsync(c.accum.p, tmp.p, size_t(N) * 4, cudaMemcpyDeviceToDevice, c.stream);
     gather_group<1>(c, c.vcount.p, tmp.p, perm, N);
     cudaMemcpyAsync(c.vcount.p, tmp.p, size_t(N) * 4, cudaMemcpyDeviceToDevice, c.stream);
+    // sampling rates follow their rows
+    if (c.nu_valid) {
+        gather_group<1>(c, c.nu_hat.p, tmp.p, perm, N);
+        cudaMemcpyAsync(c.nu_hat.p, tmp.p, size_t(N) * 4, cudaMemcpyDeviceToDevice, c.stream);
+    }
     if (perm_host) cudaMemcpyAsync(perm_host, perm, size_t(N) * 4, cudaMemcpyDeviceToHost, c.stream);
     const bool ok = cudaStreamSynchronize(c.stream) == cudaSuccess;
     for (int k = 0; k < 2; ++k) {

@@ -42,6 +42,7 @@ template bool ensure<float>(Context&, DevBuf<float>&, size_t, bool);
 template bool ensure<float4>(Context&, DevBuf<float4>&, size_t, bool);
 template bool ensure<uint2>(Context&, DevBuf<uint2>&, size_t, bool);
 template bool ensure<uint4>(Context&, DevBuf<uint4>&, size_t, bool);
+template bool ensure<DevCam>(Context&, DevBuf<DevCam>&, size_t, bool);
 template bool ensure<uint8_t>(Context&, DevBuf<uint8_t>&, size_t, bool);
 template bool ensure<uint16_t>(Context&, DevBuf<uint16_t>&, size_t, bool);
 template bool ensure<uint32_t>(Context&, DevBuf<uint32_t>&, size_t, bool);
@@ -125,6 +126,8 @@ bool valid_config(const ts_render_config* cfg, std::string* why) {
     if (cfg->backward_mode != 0) return *why = "only the per-pixel backward (0) is implemented on device", false;
     if (!(cfg->tau_alpha > 0.f && cfg->tau_alpha < 1.f)) return *why = "tau_alpha must be in (0,1)", false;
     if (!(cfg->dilation >= 0.f)) return *why = "dilation must be >= 0", false;
+    if (cfg->aa_mode < 0 || cfg->aa_mode > 3) return *why = "aa_mode must be 0..3", false;
+    if (cfg->aa_mode != 0 && !(cfg->kappa3d > 0.f)) return *why = "kappa3d must be > 0", false;
     return true;
 }
 
@@ -151,7 +154,7 @@ ts_status ensure_gaussian_buffers(Context& c, int64_t n) {
               ensure(c, c.splat, 3 * N) && ensure(c, c.rect, N) && ensure(c, c.tcount, N) &&
               ensure(c, c.dkey[0], N) && ensure(c, c.dkey[1], N) && ensure(c, c.dperm[0], N) &&
               ensure(c, c.dperm[1], N) && ensure(c, c.offsets, N + 1) && ensure(c, c.g2d, 3 * N + 1) &&
-              ensure(c, c.vis, N);
+              ensure(c, c.vis, N) && ensure(c, c.nu_hat, N);
     return ok ? TS_OK : TS_ERR_OOM;
 }
 
@@ -185,6 +188,8 @@ int tile_bits_for(int tn) {
 
 // the forward pipeline of one view
 ts_status run_forward(Context& c, const ts_camera& cam, const ts_render_config& cfg) {
+    if (cfg.aa_mode == 1 && !c.nu_valid)
+        return validation(c, "aa_mode filter3d_original needs ts_compute_sampling_rates (or ts_set_sampling_rates)");
     DevCam dc = make_devcam(cam);
     const int Tn = dc.tiles_x * dc.tiles_y;
     if (ensure_frame(c, cam.width, cam.height) != TS_OK) return TS_ERR_OOM;
@@ -413,7 +418,7 @@ ts_status ts_destroy(ts_ctx* x) {
     release(c.starts), release(c.rhist), release(c.scan_state), release(c.scan_tmp), release(c.counters);
     release(c.rgb), release(c.Tfin), release(c.dLdC), release(c.hwc_stage), release(c.tgt), release(c.pcount);
     release(c.loss_acc), release(c.targets), release(c.dens);
-    release(c.binH), release(c.bintot);
+    release(c.binH), release(c.bintot), release(c.nu_hat);
     for (size_t k = 0; k < c.ev_b.size(); ++k) {
         cudaEventDestroy(c.ev_b[k]);
         cudaEventDestroy(c.ev_e[k]);
@@ -444,6 +449,7 @@ ts_status ts_set_params_flat(ts_ctx* x, int64_t n, const float* flat) {
     if (n >= (int64_t(1) << 31)) return validation(c, "N must be < 2^31");
     CK(cudaSetDevice(c.device));
     if (ensure_gaussian_buffers(c, n) != TS_OK) return TS_ERR_OOM;
+    if (n != c.N) c.nu_valid = false;  // sampling rates are per row (kept across same-size updates)
     c.N = n;
     if (n) CK(cudaMemcpyAsync(c.params.p, flat, size_t(59) * n * 4, cudaMemcpyHostToDevice, c.stream));
     if (ts_status s = zero_state(c); s != TS_OK) return s;
@@ -711,6 +717,55 @@ ts_status ts_get_state(ts_ctx* x, float* grads, float* m, float* v, float* accum
     if (vcount) CK(cudaMemcpyAsync(vcount, c.vcount.p, N * 4, cudaMemcpyDeviceToHost, c.stream));
     CK(cudaStreamSynchronize(c.stream));
     return TS_OK;
+}
+
+ts_status ts_compute_sampling_rates(ts_ctx* x, const ts_camera* cams, int32_t n_cams, float extent) {
+    TS_CHECK_CTX(x);
+    Context& c = x->c;
+    if (!cams || n_cams < 1) return validation(c, "need >= 1 camera");
+    if (!(extent > 0.f)) return validation(c, "extent must be > 0");
+    std::string why;
+    std::vector<DevCam> dc(static_cast<size_t>(n_cams));
+    for (int k = 0; k < n_cams; ++k) {
+        if (!valid_camera(cams + k, &why)) return validation(c, why.c_str());
+        dc[size_t(k)] = make_devcam(cams[k]);
+    }
+    CK(cudaSetDevice(c.device));
+    if (!launch_sampling_rates(c, dc.data(), n_cams, extent)) return c.err.empty() ? TS_ERR_CUDA : TS_ERR_OOM;
+    c.nu_valid = true;
+    return last_launch(c, "compute_sampling_rates");
+}
+
+ts_status ts_set_sampling_rates(ts_ctx* x, const float* nu) {
+    TS_CHECK_CTX(x);
+    Context& c = x->c;
+    if (!nu) return validation(c, "NULL sampling rates");
+    CK(cudaSetDevice(c.device));
+    if (c.N) CK(cudaMemcpyAsync(c.nu_hat.p, nu, size_t(c.N) * 4, cudaMemcpyHostToDevice, c.stream));
+    c.nu_valid = true;
+    return TS_OK;
+}
+
+ts_status ts_get_sampling_rates(ts_ctx* x, float* nu) {
+    TS_CHECK_CTX(x);
+    Context& c = x->c;
+    if (!nu) return validation(c, "NULL output");
+    if (!c.nu_valid) return validation(c, "sampling rates not computed for the current store");
+    CK(cudaSetDevice(c.device));
+    if (c.N) CK(cudaMemcpyAsync(nu, c.nu_hat.p, size_t(c.N) * 4, cudaMemcpyDeviceToHost, c.stream));
+    CK(cudaStreamSynchronize(c.stream));
+    return TS_OK;
+}
+
+ts_status ts_apply_3d_filter_clip(ts_ctx* x, float kappa3d) {
+    TS_CHECK_CTX(x);
+    Context& c = x->c;
+    if (!(kappa3d > 0.f)) return validation(c, "kappa3d must be > 0");
+    if (!c.nu_valid) return validation(c, "apply_3d_filter_clip needs ts_compute_sampling_rates");
+    CK(cudaSetDevice(c.device));
+    launch_filter3d_clip(c, kappa3d);
+    c.view_valid = c.loss_valid = false;
+    return last_launch(c, "apply_3d_filter_clip");
 }
 
 ts_status ts_set_binning(ts_ctx* x, int32_t mode) {

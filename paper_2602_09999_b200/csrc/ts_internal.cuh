@@ -98,6 +98,8 @@ struct Context {
 
     // binning (k_bin.cu): per-chunk tile histograms, tile totals (+ max list length)
     DevBuf<uint32_t> binH, bintot;
+    DevBuf<float> nu_hat;        // sampling rates (antialias), N floats
+    bool nu_valid = false;       // computed for the current ParameterStore rows
     uint32_t bin_class[5] = {0, 0, 0, 0, 0};  // tiles per per-tile sort size class (last view)
     cudaStream_t side[2] = {nullptr, nullptr};  // fork streams for independent launches
     cudaEvent_t fork_ev = nullptr, join_ev[2] = {nullptr, nullptr};
@@ -128,6 +130,8 @@ void launch_adam(Context& c, const ts_adam_config& a, int64_t begin, int64_t end
 void launch_hwc_to_chw(Context& c, const float* hwc, float* chw, int P);
 void launch_chw_to_hwc(Context& c, const float* chw, float* hwc, int P);
 void launch_opacity_reset(Context& c, float logit_max);
+bool launch_sampling_rates(Context& c, const DevCam* cams_host, int ncams, float extent);
+void launch_filter3d_clip(Context& c, float kappa3d);
 bool launch_morton_reorder(Context& c, uint32_t* perm_host);
 int64_t launch_densify(Context& c, float grad_thresh, float log_small, float log_big, float logit_min,
                        uint64_t seed, int64_t iter, int64_t stats[3]);

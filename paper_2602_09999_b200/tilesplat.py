@@ -76,6 +76,10 @@ _SIGS = {
     "ts_set_profiling": [_vp, _i32],
     "ts_stage_times": [_vp, _vp, _vp, _i32],
     "ts_set_binning": [_vp, _i32],
+    "ts_compute_sampling_rates": [_vp, _vp, _i32, _f],
+    "ts_set_sampling_rates": [_vp, _vp],
+    "ts_get_sampling_rates": [_vp, _vp],
+    "ts_apply_3d_filter_clip": [_vp, _f],
     "ts_debug_loss_grad": [_vp, _vp],
     "ts_binning_path": [_vp, _vp],
     "ts_launch_count": [_vp, ctypes.POINTER(_i64)],
@@ -356,6 +360,23 @@ class Engine:
         cnt = np.zeros(len(STAGES), np.int32)
         self._check(self._L.ts_stage_times(self._h, _ptr(out), _ptr(cnt), len(STAGES)), "ts_stage_times")
         return {k: (float(a), int(b)) for k, a, b in zip(STAGES, out, cnt)}
+
+    # ---- antialias ----
+    def compute_sampling_rates(self, cams, extent: float):
+        """compute_sampling_rates over the training cameras (stored on the device)."""
+        arr = (Camera * len(cams))(*cams)
+        self._check(self._L.ts_compute_sampling_rates(self._h, arr, len(cams), extent), "ts_compute_sampling_rates")
+
+    def set_sampling_rates(self, nu: np.ndarray):
+        self._check(self._L.ts_set_sampling_rates(self._h, _ptr(_f32(nu))), "ts_set_sampling_rates")
+
+    def get_sampling_rates(self) -> np.ndarray:
+        out = np.empty(self.num_gaussians(), np.float32)
+        self._check(self._L.ts_get_sampling_rates(self._h, _ptr(out)), "ts_get_sampling_rates")
+        return out
+
+    def apply_3d_filter_clip(self, kappa3d: float = 0.2):
+        self._check(self._L.ts_apply_3d_filter_clip(self._h, kappa3d), "ts_apply_3d_filter_clip")
 
     def debug_loss_grad(self):
         """dL/dC (H x W x 3) of the last training_loss, read back from the device."""

@@ -23,6 +23,9 @@ BOUND_SQUARE, BOUND_RECT, BOUND_RECT_OPACITY = 0, 1, 2
 CULL_NONE, CULL_EXACT = 0, 1
 BACKWARD_PER_PIXEL, BACKWARD_PER_GAUSSIAN = 0, 1
 ADAM_REFERENCE, ADAM_FUSED, ADAM_SKIP_INVISIBLE, ADAM_FUSED_BACKWARD, ADAM_FUSED_BACKWARD_SKIP = 0, 1, 2, 3, 4
+AA_OFF, AA_FILTER3D_ORIGINAL, AA_FILTER3D_CLIP, AA_FULL = 0, 1, 2, 3
+AA_MODES = {"off": AA_OFF, "filter3d_original": AA_FILTER3D_ORIGINAL, "filter3d_clip": AA_FILTER3D_CLIP,
+            "full": AA_FULL}
 
 
 class Camera(ctypes.Structure):
@@ -81,13 +84,21 @@ class RenderConfig(ctypes.Structure):
         ("dilation", ctypes.c_float),
         ("sigma_cut", ctypes.c_float),
         ("bg", ctypes.c_float * 3),
+        ("aa_mode", ctypes.c_int32),
+        ("kappa3d", ctypes.c_float),
     ]
 
     @classmethod
     def make(cls, sh_degree=3, bound_mode=BOUND_RECT_OPACITY, cull_mode=CULL_EXACT, early_stop_compat=0,
-             backward_mode=BACKWARD_PER_PIXEL, tau_alpha=1.0 / 255.0, dilation=0.3, sigma_cut=3.33,
-             bg=(0.0, 0.0, 0.0)) -> "RenderConfig":
+             backward_mode=BACKWARD_PER_PIXEL, tau_alpha=1.0 / 255.0, dilation=None, sigma_cut=3.33,
+             bg=(0.0, 0.0, 0.0), aa="off", kappa3d=0.2) -> "RenderConfig":
+        """aa: off | filter3d_original | filter3d_clip | full; the 2D dilation defaults to
+        0.3 (classic) unless aa == "full", which uses the Mip filter variance 0.1 with compensation."""
         c = cls()
+        c.aa_mode = AA_MODES[aa] if isinstance(aa, str) else int(aa)
+        c.kappa3d = kappa3d
+        if dilation is None:
+            dilation = 0.1 if c.aa_mode == AA_FULL else 0.3
         c.sh_degree, c.bound_mode, c.cull_mode = sh_degree, bound_mode, cull_mode
         c.truncation, c.early_stop_compat, c.backward_mode = 0, early_stop_compat, backward_mode
         c.tau_alpha, c.dilation, c.sigma_cut = tau_alpha, dilation, sigma_cut

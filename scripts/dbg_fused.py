@@ -11,6 +11,11 @@ cfg = T.RenderConfig.make(sh_degree=3)
 e.set_params(gt, n)
 target, _, _ = e.render(cam, cfg)
 p0 = scene.perturb(gt, n, 31)
+e.set_params(p0, n)
+e.render(cam, cfg, outputs=False)
+_, _, tc, _ = e.debug_preprocess()
+single = tc <= 1
+rowmask = {}
 outs = []
 for m in (1, 3):
     e.set_params(p0, n)
@@ -19,7 +24,11 @@ for m in (1, 3):
     outs.append((e.get_params(), mm, vv, acc, vc))
 names = ["params", "m", "v", "acc", "vc"]
 for nm, a, b in zip(names, *outs):
-    d = np.flatnonzero(a.view(np.uint32) != b.view(np.uint32))
+    if a.size == 59 * n:
+        keep = np.concatenate([np.repeat(single, w) for w in T.GROUP_WIDTH])
+    else:
+        keep = single
+    d = np.flatnonzero((a.view(np.uint32) != b.view(np.uint32)) & keep)
     print(nm, "ndiff", d.size, "first", d[:8], "maxabs", np.abs(a - b).max() if a.size else 0)
     if d.size:
         for (s, t), gn in zip(T.group_slices(n), T.GROUPS):

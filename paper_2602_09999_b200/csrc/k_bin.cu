@@ -6,9 +6,9 @@
 // is produced here by bucketing followed by a small per-tile sort, instead of
 // a depth sort over N plus a radix sort over I:
 //
-//   KB1 bin_hist    chunk CTA (8192 Gaussians): per-tile instance counts of the
-//                   chunk in a shared histogram (the K1 kept-tile masks, or the
-//                   exact cull for rects of more than 64 tiles) -> H[chunk][tile];
+//   KB1 histogram   per-tile instance counts of every chunk of 8192 Gaussians,
+//                   H[chunk][tile], accumulated by K1 itself (k_preprocess.cu) with
+//                   fire-and-forget REDs as it decides each kept tile;
 //   KB2 bin_colscan per tile: exclusive prefix of H over chunks, tile totals and
 //                   the maximum list length; the exclusive scan of the totals is
 //                   the tile ranges (starts) and I;
@@ -30,7 +30,7 @@
 namespace ts {
 namespace {
 
-constexpr int kChunk = 8192;      // Gaussians per chunk CTA (= kBinThreads * kPre)
+constexpr int kChunk = kBinChunk;  // Gaussians per chunk CTA (= kBinThreads * kPre)
 constexpr int kBinThreads = 512;  // threads of the chunk kernels
 constexpr int kPre = 16;         // rects per thread, all loaded before the expansion
 
@@ -98,31 +98,6 @@ __device__ __forceinline__ void warp_expand(const uint4 rc, uint32_t g, bool val
     }
     // rect of more than 64 tiles (rare): exact cull per tile, one tile at a time
     for (int t = -1; (t = big_rect_next(splat, g, tx0, tx1, ty0, ty1, W, H, tiles_x, cull_mode, t)) >= 0;) f(t, g);
-}
-
-__global__ void __launch_bounds__(kBinThreads) bin_hist_kernel(const uint4* __restrict__ rect,
-                                                               const float4* __restrict__ splat, int64_t N, int W,
-                                                               int H, int tiles_x, int Tn, int cull_mode,
-                                                               uint32_t* __restrict__ Hm) {
-    extern __shared__ uint32_t hist[];
-    for (int t = threadIdx.x; t < Tn; t += kBinThreads) hist[t] = 0;
-    __syncthreads();
-    const int64_t g0 = int64_t(blockIdx.x) * kChunk;
-    uint4 rc[kPre];
-#pragma unroll
-    for (int u = 0; u < kPre; ++u) {
-        const int64_t g = g0 + threadIdx.x + u * kBinThreads;
-        rc[u] = g < N ? __ldg(rect + g) : make_uint4(1u, 1u, 0u, 0u);
-    }
-#pragma unroll 1
-    for (int u = 0; u < kPre; ++u) {
-        const int64_t g = g0 + threadIdx.x + u * kBinThreads;
-        warp_expand(rc[u], uint32_t(g), g < N, splat, W, H, tiles_x, cull_mode,
-                    [&](int t, uint32_t) { atomicAdd(&hist[t], 1u); });
-    }
-    __syncthreads();
-    uint32_t* row = Hm + size_t(blockIdx.x) * Tn;
-    for (int t = threadIdx.x; t < Tn; t += kBinThreads) row[t] = hist[t];
 }
 
 // per-tile sort size classes: list lengths in [2, kCap0], (kCap0, kCap1], (kCap1, kCap2];
@@ -336,17 +311,15 @@ int64_t launch_bin_count(Context& c, const DevCam& cam, const ts_render_config& 
     const size_t sm = size_t(Tn) * 4;
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(bin_hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
         cudaFuncSetAttribute(bin_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
         attr = true;
     }
     uint32_t* meta = c.bintot.p + Tn;
     uint32_t* cls = meta + 8;
     cudaMemsetAsync(meta, 0, 8 * 4, c.stream);
+    (void)sm;
     if (c.N > 0) {
-        bin_hist_kernel<<<nch, kBinThreads, sm, c.stream>>>(c.rect.p, c.splat.p, c.N, cam.w, cam.h, cam.tiles_x, Tn,
-                                                             cfg.cull_mode, c.binH.p);
-        TS_LAUNCHED(c);
+        // H[chunk][tile] was accumulated by K1 (launch_preprocess)
         bin_colscan_kernel<<<(Tn + 63) / 64, 64, 0, c.stream>>>(c.binH.p, nch, Tn, c.bintot.p, meta, cls);
         TS_LAUNCHED(c);
     } else {

@@ -17,7 +17,8 @@ template <int DEG>
 __global__ void __launch_bounds__(kBlock) preprocess_kernel(
     const float* __restrict__ P, int64_t N, DevCam cam, ts_render_config cfg, float4* __restrict__ splat,
     uint4* __restrict__ rect, uint32_t* __restrict__ tcount, uint32_t* __restrict__ dkey,
-    uint32_t* __restrict__ dperm, uint32_t* __restrict__ vis_counter, const float* __restrict__ nu_hat) {
+    uint32_t* __restrict__ dperm, uint32_t* __restrict__ vis_counter, const float* __restrict__ nu_hat,
+    uint32_t* __restrict__ binH, int bin_chunk) {
     using namespace tsx;
     // staged inputs of the CTA's 128 Gaussians (one pass of independent 16-byte loads)
     constexpr int kMu = 0, kLs = kMu + 3 * kBlock + 4, kQ = kLs + 3 * kBlock + 4, kOp = kQ + 4 * kBlock + 4,
@@ -235,9 +236,14 @@ __global__ void __launch_bounds__(kBlock) preprocess_kernel(
         rc = make_uint4(uint32_t(tx0) | (uint32_t(tx1) << 16),
                         uint32_t(ty0) | (uint32_t(ty1) << 16) | (big ? 0x80000000u : 0u), 0u, 0u);
         uint64_t mask = 0;
+        // per-chunk tile histogram of the bucketed binning (k_bin.cu), fire-and-forget REDs
+        uint32_t* hrow = binH ? binH + size_t(g / bin_chunk) * size_t(cam.tiles_x * cam.tiles_y) : nullptr;
         if (cfg.cull_mode == 0) {
             cnt = uint32_t(ntl);
             if (!big) mask = ntl == 64 ? ~0ull : ((1ull << ntl) - 1ull);
+            if (hrow)
+                for (int tyy = ty0; tyy <= ty1; ++tyy)
+                    for (int txx = tx0; txx <= tx1; ++txx) atomicAdd(hrow + tyy * cam.tiles_x + txx, 1u);
         } else {
             const float nBA = div(-B, A), nBC = div(-B, C);
             int bit = 0;
@@ -246,6 +252,7 @@ __global__ void __launch_bounds__(kBlock) preprocess_kernel(
                     const bool keep = tile_keep(mx, my, A, B, C, k2, nBA, nBC, txx, tyy, cam.w, cam.h);
                     cnt += keep ? 1u : 0u;
                     if (keep && !big) mask |= 1ull << bit;
+                    if (keep && hrow) atomicAdd(hrow + tyy * cam.tiles_x + txx, 1u);
                 }
         }
         rc.z = uint32_t(mask);
@@ -269,11 +276,22 @@ __global__ void __launch_bounds__(kBlock) preprocess_kernel(
 
 void launch_preprocess(Context& c, const DevCam& cam, const ts_render_config& cfg) {
     if (c.N == 0) return;
+    // the bucketed binning's chunk histograms are accumulated here (zeroed first)
+    uint32_t* binH = nullptr;
+    const int Tn = cam.tiles_x * cam.tiles_y;
+    if (c.binning_mode == 0 && bin_supported(Tn)) {
+        const size_t rows = size_t((c.N + kBinChunk - 1) / kBinChunk);
+        if (ensure(c, c.binH, rows * Tn)) {
+            binH = c.binH.p;
+            cudaMemsetAsync(binH, 0, rows * Tn * 4, c.stream);
+        }
+    }
     const int64_t blocks = (c.N + kBlock - 1) / kBlock;
 #define TS_PRE(D)                                                                                      \
     preprocess_kernel<D><<<unsigned(blocks), kBlock, 0, c.stream>>>(c.params.p, c.N, cam, cfg, c.splat.p, \
                                                                      c.rect.p, c.tcount.p, c.dkey[0].p,   \
-                                                                     c.dperm[0].p, c.counters.p + 1, c.nu_hat.p)
+                                                                     c.dperm[0].p, c.counters.p + 1, c.nu_hat.p,    \
+                                                                     binH, kBinChunk)
     switch (cfg.sh_degree) {
         case 0: TS_PRE(0); break;
         case 1: TS_PRE(1); break;

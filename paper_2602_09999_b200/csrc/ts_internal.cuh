@@ -115,6 +115,7 @@ void launch_duplicate(Context& c, const DevCam& cam, const ts_render_config& cfg
 void launch_tile_sort(Context& c, int tile_bits);
 void launch_ranges(Context& c, int n_tiles);
 // bucketed binning (k_bin.cu): returns I (syncs) and the longest tile list, -1 on OOM
+constexpr int kBinChunk = 8192;  // Gaussians per chunk of the bucketed binning (one histogram row)
 bool bin_supported(int Tn);
 int bin_sort_cap();
 int64_t launch_bin_count(Context& c, const DevCam& cam, const ts_render_config& cfg, uint32_t* max_len);

@@ -8,6 +8,7 @@
 #include <cmath>
 
 #include "ts_internal.cuh"
+#include "ts_math.cuh"
 
 namespace ts {
 namespace {
@@ -77,30 +78,27 @@ __global__ void __launch_bounds__(kFThreads) loss_fused_kernel(const float* __re
         constexpr int S = 7, NS = kFM / S;
         for (int it = tid; it < kFI * NS; it += kFThreads) {
             const int r = it / NS, c0 = (it - r * NS) * S;
-            float a[S + 10], b[S + 10];
+            // (x, y) pairs: {mu_x, mu_y} and {x^2, y^2} moments in packed fp32x2 ops
+            float2 ab[S + 10];
 #pragma unroll
-            for (int k = 0; k < S + 10; ++k) {
-                a[k] = xs[r * kFI + c0 + k];
-                b[k] = ys[r * kFI + c0 + k];
-            }
+            for (int k = 0; k < S + 10; ++k) ab[k] = make_float2(xs[r * kFI + c0 + k], ys[r * kFI + c0 + k]);
 #pragma unroll
             for (int j = 0; j < S; ++j) {
-                float m0 = 0.f, m1 = 0.f, m2 = 0.f, m3 = 0.f, m4 = 0.f;
+                float2 m01 = make_float2(0.f, 0.f), m23 = m01;
+                float m4 = 0.f;
 #pragma unroll
                 for (int k = 0; k < 11; ++k) {
-                    const float xa = a[j + k], yb = b[j + k];
-                    const float wx = wk[k] * xa, wy = wk[k] * yb;
-                    m0 += wx;
-                    m1 += wy;
-                    m2 = fmaf(wx, xa, m2);
-                    m3 = fmaf(wy, yb, m3);
-                    m4 = fmaf(wx, yb, m4);
+                    const float2 v = ab[j + k];
+                    const float2 wv = tsx::mul2(tsx::dup2(wk[k]), v);
+                    m01 = tsx::add2(m01, wv);
+                    m23 = tsx::fma2(wv, v, m23);
+                    m4 = fmaf(wv.x, v.y, m4);
                 }
                 const int o = r * kFM + c0 + j;
-                A[o] = m0;
-                A[kFI * kFM + o] = m1;
-                A[2 * kFI * kFM + o] = m2;
-                A[3 * kFI * kFM + o] = m3;
+                A[o] = m01.x;
+                A[kFI * kFM + o] = m01.y;
+                A[2 * kFI * kFM + o] = m23.x;
+                A[3 * kFI * kFM + o] = m23.y;
                 A[4 * kFI * kFM + o] = m4;
             }
         }
@@ -115,16 +113,30 @@ __global__ void __launch_bounds__(kFThreads) loss_fused_kernel(const float* __re
             const int c = it % kFM, r0 = (it / kFM) * S;
             float m[S][5];
 #pragma unroll
-            for (int q = 0; q < 5; ++q) {
+            for (int q = 0; q < 4; q += 2) {  // moment pairs (0,1), (2,3) packed
+                float2 win[S + 10];
+#pragma unroll
+                for (int k = 0; k < S + 10; ++k)
+                    win[k] = make_float2(A[q * kFI * kFM + (r0 + k) * kFM + c], A[(q + 1) * kFI * kFM + (r0 + k) * kFM + c]);
+#pragma unroll
+                for (int j = 0; j < S; ++j) {
+                    float2 sacc = make_float2(0.f, 0.f);
+#pragma unroll
+                    for (int k = 0; k < 11; ++k) sacc = tsx::fma2(tsx::dup2(wk[k]), win[j + k], sacc);
+                    m[j][q] = sacc.x;
+                    m[j][q + 1] = sacc.y;
+                }
+            }
+            {
                 float win[S + 10];
 #pragma unroll
-                for (int k = 0; k < S + 10; ++k) win[k] = A[q * kFI * kFM + (r0 + k) * kFM + c];
+                for (int k = 0; k < S + 10; ++k) win[k] = A[4 * kFI * kFM + (r0 + k) * kFM + c];
 #pragma unroll
                 for (int j = 0; j < S; ++j) {
                     float sacc = 0.f;
 #pragma unroll
                     for (int k = 0; k < 11; ++k) sacc = fmaf(wk[k], win[j + k], sacc);
-                    m[j][q] = sacc;
+                    m[j][4] = sacc;
                 }
             }
             const int gx = x0 - 5 + c;
@@ -167,20 +179,34 @@ __global__ void __launch_bounds__(kFThreads) loss_fused_kernel(const float* __re
         }
     }
     __syncthreads();
-    // 4a. horizontal transposed pass at virtual columns [-5, 42): hb[q][r][m] (A, 3 x 42 x 47)
+    // 4a. horizontal transposed pass at virtual columns [-5, 42): hb[q][r][m] (A, 3 x 42 x 47);
+    //     (a, b) packed, c scalar
     {
         constexpr int S = 8, NS = (kFV + S - 1) / S;  // 6 segments (48 columns, last partly unused)
-        for (int it = tid; it < 3 * kFM * NS; it += kFThreads) {
-            const int q = it / (kFM * NS), rem = it - q * kFM * NS, r = rem / NS, c0 = (rem - r * NS) * S;
-            float a[S + 10];
+        for (int it = tid; it < kFM * NS; it += kFThreads) {
+            const int r = it / NS, c0 = (it - r * NS) * S;
+            float2 ab[S + 10];
+            float cc[S + 10];
 #pragma unroll
-            for (int k = 0; k < S + 10; ++k) a[k] = c0 + k < kFP ? B[q * kFM * kFP + r * kFP + c0 + k] : 0.f;
+            for (int k = 0; k < S + 10; ++k) {
+                const bool in = c0 + k < kFP;
+                ab[k] = in ? make_float2(B[r * kFP + c0 + k], B[kFM * kFP + r * kFP + c0 + k]) : make_float2(0.f, 0.f);
+                cc[k] = in ? B[2 * kFM * kFP + r * kFP + c0 + k] : 0.f;
+            }
 #pragma unroll
             for (int j = 0; j < S; ++j) {
-                float sacc = 0.f;
+                float2 sab = make_float2(0.f, 0.f);
+                float sc = 0.f;
 #pragma unroll
-                for (int k = 0; k < 11; ++k) sacc = fmaf(wk[k], a[j + k], sacc);
-                if (c0 + j < kFV) A[q * kFM * kFV + r * kFV + c0 + j] = sacc;
+                for (int k = 0; k < 11; ++k) {
+                    sab = tsx::fma2(tsx::dup2(wk[k]), ab[j + k], sab);
+                    sc = fmaf(wk[k], cc[j + k], sc);
+                }
+                if (c0 + j < kFV) {
+                    A[r * kFV + c0 + j] = sab.x;
+                    A[kFM * kFV + r * kFV + c0 + j] = sab.y;
+                    A[2 * kFM * kFV + r * kFV + c0 + j] = sc;
+                }
             }
         }
     }
@@ -204,20 +230,33 @@ __global__ void __launch_bounds__(kFThreads) loss_fused_kernel(const float* __re
         }
     }
     __syncthreads();
-    // 5a. vertical transposed pass at virtual rows [-5, 42): vb[q][m][c] (A, 3 x 47 x 32)
+    // 5a. vertical transposed pass at virtual rows [-5, 42): vb[q][m][c] (A, 3 x 47 x 32); (a, b) packed
     {
         constexpr int S = 6, NS = (kFV + S - 1) / S;  // 8 groups (48 rows, last partly unused)
-        for (int it = tid; it < 3 * kFT * NS; it += kFThreads) {
-            const int q = it / (kFT * NS), rem = it - q * kFT * NS, c = rem % kFT, r0 = (rem / kFT) * S;
-            float win[S + 10];
+        for (int it = tid; it < kFT * NS; it += kFThreads) {
+            const int c = it % kFT, r0 = (it / kFT) * S;
+            float2 ab[S + 10];
+            float cc[S + 10];
 #pragma unroll
-            for (int k = 0; k < S + 10; ++k) win[k] = r0 + k < kFP ? B[q * kFP * kFT + (r0 + k) * kFT + c] : 0.f;
+            for (int k = 0; k < S + 10; ++k) {
+                const bool in = r0 + k < kFP;
+                ab[k] = in ? make_float2(B[(r0 + k) * kFT + c], B[kFP * kFT + (r0 + k) * kFT + c]) : make_float2(0.f, 0.f);
+                cc[k] = in ? B[2 * kFP * kFT + (r0 + k) * kFT + c] : 0.f;
+            }
 #pragma unroll
             for (int j = 0; j < S; ++j) {
-                float sacc = 0.f;
+                float2 sab = make_float2(0.f, 0.f);
+                float sc = 0.f;
 #pragma unroll
-                for (int k = 0; k < 11; ++k) sacc = fmaf(wk[k], win[j + k], sacc);
-                if (r0 + j < kFV) A[q * kFV * kFT + (r0 + j) * kFT + c] = sacc;
+                for (int k = 0; k < 11; ++k) {
+                    sab = tsx::fma2(tsx::dup2(wk[k]), ab[j + k], sab);
+                    sc = fmaf(wk[k], cc[j + k], sc);
+                }
+                if (r0 + j < kFV) {
+                    A[(r0 + j) * kFT + c] = sab.x;
+                    A[kFV * kFT + (r0 + j) * kFT + c] = sab.y;
+                    A[2 * kFV * kFT + (r0 + j) * kFT + c] = sc;
+                }
             }
         }
     }

@@ -270,11 +270,14 @@ ts_status upload_image_chw(Context& c, const float* hwc, float* dst_chw) {
     return last_launch(c, "hwc_to_chw");
 }
 
-ts_status run_loss(Context& c, const float* target_hwc, int32_t slot, float* out_loss) {
+ts_status run_loss(Context& c, const float* target_hwc, int32_t slot, float* out_loss,
+                   const float* target_chw_dev = nullptr) {
     if (!c.view_valid) return validation(c, "ts_loss needs a preceding ts_forward");
     const size_t P = size_t(c.fw) * c.fh;
     const float* tgt = nullptr;
-    if (target_hwc) {
+    if (target_chw_dev) {
+        tgt = target_chw_dev;
+    } else if (target_hwc) {
         if (ts_status s = upload_image_chw(c, target_hwc, c.tgt.p); s != TS_OK) return s;
         tgt = c.tgt.p;
     } else {
@@ -418,7 +421,7 @@ ts_status ts_destroy(ts_ctx* x) {
     release(c.starts), release(c.rhist), release(c.scan_state), release(c.scan_tmp), release(c.counters);
     release(c.rgb), release(c.Tfin), release(c.dLdC), release(c.hwc_stage), release(c.tgt), release(c.pcount);
     release(c.loss_acc), release(c.targets), release(c.dens);
-    release(c.binH), release(c.bintot), release(c.nu_hat);
+    release(c.binH), release(c.bintot), release(c.tgt_stage), release(c.nu_hat);
     for (size_t k = 0; k < c.ev_b.size(); ++k) {
         cudaEventDestroy(c.ev_b[k]);
         cudaEventDestroy(c.ev_e[k]);
@@ -428,6 +431,9 @@ ts_status ts_destroy(ts_ctx* x) {
         if (c.join_ev[k]) cudaEventDestroy(c.join_ev[k]);
     }
     if (c.fork_ev) cudaEventDestroy(c.fork_ev);
+    if (c.copy_stream) cudaStreamDestroy(c.copy_stream);
+    if (c.copy_fork) cudaEventDestroy(c.copy_fork);
+    if (c.copy_join) cudaEventDestroy(c.copy_join);
     if (c.own_stream) cudaStreamDestroy(c.stream);
     delete x;
     return TS_OK;
@@ -627,8 +633,28 @@ ts_status ts_train_step(ts_ctx* x, const ts_camera* cam, const ts_render_config*
     if (!valid_camera(cam, &why) || !valid_config(cfg, &why)) return validation(c, why.c_str());
     if (!adam) return validation(c, "adam config is NULL");
     CK(cudaSetDevice(c.device));
+    // a host target is uploaded on a copy stream while the forward runs (the loss waits for it)
+    const size_t P = size_t(cam->width) * cam->height;
+    if (target_hwc) {
+        if (ensure_frame(c, cam->width, cam->height) != TS_OK || !ensure(c, c.tgt_stage, 3 * P)) return TS_ERR_OOM;
+        if (!c.copy_stream) {
+            CK(cudaStreamCreateWithFlags(&c.copy_stream, cudaStreamNonBlocking));
+            CK(cudaEventCreateWithFlags(&c.copy_fork, cudaEventDisableTiming));
+            CK(cudaEventCreateWithFlags(&c.copy_join, cudaEventDisableTiming));
+        }
+        CK(cudaEventRecord(c.copy_fork, c.stream));  // the previous step is done with tgt_stage
+        CK(cudaStreamWaitEvent(c.copy_stream, c.copy_fork, 0));
+        CK(cudaMemcpyAsync(c.tgt_stage.p, target_hwc, 3 * P * 4, cudaMemcpyHostToDevice, c.copy_stream));
+        CK(cudaEventRecord(c.copy_join, c.copy_stream));
+    }
     if (ts_status s = run_forward(c, *cam, *cfg); s != TS_OK) return s;
-    if (ts_status s = run_loss(c, target_hwc, slot, nullptr); s != TS_OK) return s;
+    if (target_hwc) {
+        CK(cudaStreamWaitEvent(c.stream, c.copy_join, 0));
+        launch_hwc_to_chw(c, c.tgt_stage.p, c.tgt.p, int(P));
+        if (ts_status s = run_loss(c, nullptr, slot, nullptr, c.tgt.p); s != TS_OK) return s;
+    } else {
+        if (ts_status s = run_loss(c, nullptr, slot, nullptr); s != TS_OK) return s;
+    }
     if (adam->mode >= 3) {
         if (ts_status s = run_backward_adam(c, nullptr, *adam); s != TS_OK) return s;
     } else {

@@ -103,6 +103,10 @@ struct Context {
     uint32_t bin_class[5] = {0, 0, 0, 0, 0};  // tiles per per-tile sort size class (last view)
     cudaStream_t side[2] = {nullptr, nullptr};  // fork streams for independent launches
     cudaEvent_t fork_ev = nullptr, join_ev[2] = {nullptr, nullptr};
+    // ts_train_step's host-target upload, overlapped with the forward
+    cudaStream_t copy_stream = nullptr;
+    cudaEvent_t copy_fork = nullptr, copy_join = nullptr;
+    DevBuf<float> tgt_stage;
     int binning_mode = 0;        // 0 auto (bucket + per-tile sort), 1 force the two-stage radix path
     bool last_view_radix = false;
 };

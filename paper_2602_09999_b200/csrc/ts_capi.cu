@@ -432,6 +432,8 @@ ts_status ts_destroy(ts_ctx* x) {
     }
     if (c.fork_ev) cudaEventDestroy(c.fork_ev);
     if (c.copy_stream) cudaStreamDestroy(c.copy_stream);
+    if (c.loss_host) cudaFreeHost(c.loss_host);
+    if (c.loss_ev) cudaEventDestroy(c.loss_ev);
     if (c.copy_fork) cudaEventDestroy(c.copy_fork);
     if (c.copy_join) cudaEventDestroy(c.copy_join);
     if (c.own_stream) cudaStreamDestroy(c.stream);
@@ -655,6 +657,17 @@ ts_status ts_train_step(ts_ctx* x, const ts_camera* cam, const ts_render_config*
     } else {
         if (ts_status s = run_loss(c, nullptr, slot, nullptr); s != TS_OK) return s;
     }
+    // the loss sums go to pinned host memory right behind the loss kernel; the host
+    // waits for that event only, so backward + Adam keep the GPU busy while the caller
+    // prepares the next step
+    if (out_loss) {
+        if (!c.loss_host) {
+            CK(cudaMallocHost(reinterpret_cast<void**>(&c.loss_host), 2 * sizeof(double)));
+            CK(cudaEventCreateWithFlags(&c.loss_ev, cudaEventDisableTiming));
+        }
+        CK(cudaMemcpyAsync(c.loss_host, c.loss_acc.p, 2 * sizeof(double), cudaMemcpyDeviceToHost, c.stream));
+        CK(cudaEventRecord(c.loss_ev, c.stream));
+    }
     if (adam->mode >= 3) {
         if (ts_status s = run_backward_adam(c, nullptr, *adam); s != TS_OK) return s;
     } else {
@@ -666,11 +679,9 @@ ts_status ts_train_step(ts_ctx* x, const ts_camera* cam, const ts_render_config*
         if (ts_status s = run_adam(c, a, 0, 59 * c.N); s != TS_OK) return s;
     }
     if (out_loss) {
-        double acc[2];
-        CK(cudaMemcpyAsync(acc, c.loss_acc.p, sizeof(acc), cudaMemcpyDeviceToHost, c.stream));
-        CK(cudaStreamSynchronize(c.stream));
+        CK(cudaEventSynchronize(c.loss_ev));
         const double M = 3.0 * double(cam->width) * cam->height;
-        *out_loss = float(0.8 * acc[0] / M + 0.2 * (1.0 - acc[1] / M));
+        *out_loss = float(0.8 * c.loss_host[0] / M + 0.2 * (1.0 - c.loss_host[1] / M));
     }
     return TS_OK;
 }

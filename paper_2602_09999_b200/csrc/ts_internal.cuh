@@ -107,6 +107,8 @@ struct Context {
     cudaStream_t copy_stream = nullptr;
     cudaEvent_t copy_fork = nullptr, copy_join = nullptr;
     DevBuf<float> tgt_stage;
+    double* loss_host = nullptr;  // pinned (L1 sum, SSIM sum) of the last train_step
+    cudaEvent_t loss_ev = nullptr;
     int binning_mode = 0;        // 0 auto (bucket + per-tile sort), 1 force the two-stage radix path
     bool last_view_radix = false;
 };

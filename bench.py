@@ -236,7 +236,7 @@ def run_ours(args):
                                  zero_grads=0 if args.dp_mode == "allreduce" else 1)
 
     def train_step():
-        if fused_bwd:   # one public C-ABI call: forward, loss, backward with the in-place Adam update
+        if world == 1:  # one public C-ABI call: forward, loss, backward, Adam (target slot on the device)
             e.train_step(cam, cfg, adam_cfg(), slot=0, want_loss=False)
         else:
             dp.step(views, adam_cfg())
@@ -248,10 +248,19 @@ def run_ours(args):
     if world > 1:
         dist.barrier()
 
+    # per-stage breakdown: a profiled loop (CUDA events around every stage on the
+    # context stream) before the timed region, which runs without the stage events
+    e.set_profiling(True)
+    for _ in range(min(args.steps, 30)):
+        step += 1
+        train_step()
+    torch.cuda.synchronize()
+    stimes = e.stage_times()
+    e.set_profiling(False)
+
     # ---- timed region (device-resident targets) ----
     clk = ClockSampler(local)
     clk.start()
-    e.set_profiling(True)
     l0 = e.launch_count()
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
@@ -266,8 +275,6 @@ def run_ours(args):
         dist.barrier()
     clocks = clk.stop()
     launches = e.launch_count() - l0
-    stimes = e.stage_times()
-    e.set_profiling(False)
     ms = ev0.elapsed_time(ev1) / args.steps
     if world > 1:
         t = torch.tensor([ms], device=f"cuda:{local}")
@@ -370,7 +377,9 @@ def run_ours(args):
                          "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})",
                          "note": ("the peak is a 1:1 read:write copy test; this kernel's mix (Adam: 4 reads : 3 "
                                   "writes) streams faster than it, hence frac > 1" if achieved > peak else None)},
-            "fwd_bwd": {"ms": fwd_bwd_ms, "source": "separate-optimizer profiled loop" if fused_bwd else "timed loop", "mpix_s": world * P / (fwd_bwd_ms * 1e-3) / 1e6,
+            "fwd_bwd": {"ms": fwd_bwd_ms,
+                        "source": "profiled loop (stage CUDA events; separate-optimizer steps)" if fused_bwd
+                        else "profiled loop (stage CUDA events)", "mpix_s": world * P / (fwd_bwd_ms * 1e-3) / 1e6,
                         "algorithmic_bytes": int(R), "achieved_gbs": R / (fwd_bwd_ms * 1e-3) / 1e9,
                         "roofline_frac": R / (fwd_bwd_ms * 1e-3) / 1e9 / peak},
             "stage_ms": {k: round(v, 4) for k, v in avg.items()},

@@ -133,7 +133,7 @@ __global__ void __launch_bounds__(64) bin_colscan_kernel(uint32_t* __restrict__ 
     if ((threadIdx.x & 31) == 0 && wm) atomicMax(&meta[5], wm);
 }
 
-__global__ void __launch_bounds__(kBinThreads) bin_scatter_kernel(const uint4* __restrict__ rect,
+__global__ void __launch_bounds__(kBinThreads, 3) bin_scatter_kernel(const uint4* __restrict__ rect,
                                                                   const float4* __restrict__ splat, int64_t N, int W,
                                                                   int H, int tiles_x, int Tn, int cull_mode,
                                                                   const uint32_t* __restrict__ Hm,

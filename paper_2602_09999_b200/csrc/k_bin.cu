@@ -102,11 +102,11 @@ __device__ __forceinline__ void warp_expand(const uint4 rc, uint32_t g, bool val
 
 // per-tile sort size classes: list lengths in [2, kCap0], (kCap0, kCap1], (kCap1, kCap2];
 // lists of one instance are copied; longer lists send the view to the radix path
-constexpr int kCap0 = 1024, kCap1 = 4096, kCap2 = 8192, kCap3 = 16384;
+constexpr int kCap0 = 1024, kCap1 = 4096, kCapM = 6144, kCap2 = 8192, kCap3 = 16384;
 
 // per tile: exclusive prefix over chunks (in place), total, running max, and the
 // tile appended to the work list of its sort size class (meta[0..4] = class counts,
-// meta[5] = max length; lists at cls + c * Tn)
+// meta[6] = max length; lists at cls + c * Tn)
 __global__ void __launch_bounds__(64) bin_colscan_kernel(uint32_t* __restrict__ Hm, int nchunks, int Tn,
                                                          uint32_t* __restrict__ tot, uint32_t* __restrict__ meta,
                                                          uint32_t* __restrict__ cls) {
@@ -126,11 +126,12 @@ __global__ void __launch_bounds__(64) bin_colscan_kernel(uint32_t* __restrict__ 
                 }
         }
         tot[t] = run;
-        const int k = run == 1 ? 0 : run <= uint32_t(kCap0) ? 1 : run <= uint32_t(kCap1) ? 2 : run <= uint32_t(kCap2) ? 3 : 4;
+        const int k = run == 1 ? 0 : run <= uint32_t(kCap0) ? 1 : run <= uint32_t(kCap1) ? 2 : run <= uint32_t(kCapM) ? 5
+                    : run <= uint32_t(kCap2) ? 3 : 4;
         if (run > 0 && run <= uint32_t(kCap3)) cls[size_t(k) * Tn + atomicAdd(&meta[k], 1u)] = uint32_t(t);
     }
     const uint32_t wm = __reduce_max_sync(0xffffffffu, run);
-    if ((threadIdx.x & 31) == 0 && wm) atomicMax(&meta[5], wm);
+    if ((threadIdx.x & 31) == 0 && wm) atomicMax(&meta[6], wm);
 }
 
 __global__ void __launch_bounds__(kBinThreads, 3) bin_scatter_kernel(const uint4* __restrict__ rect,
@@ -306,8 +307,8 @@ bool bin_supported(int Tn) { return size_t(Tn) * 4 <= 200 * 1024; }
 int64_t launch_bin_count(Context& c, const DevCam& cam, const ts_render_config& cfg, uint32_t* max_len) {
     const int Tn = cam.tiles_x * cam.tiles_y;
     const int nch = int(std::max<int64_t>(1, (c.N + kChunk - 1) / kChunk));
-    // bintot: [0, Tn) totals | meta (8) | class lists 5 * Tn
-    if (!ensure(c, c.binH, size_t(nch) * Tn) || !ensure(c, c.bintot, size_t(Tn) * 6 + 8)) return -1;
+    // bintot: [0, Tn) totals | meta (8) | class lists 6 * Tn
+    if (!ensure(c, c.binH, size_t(nch) * Tn) || !ensure(c, c.bintot, size_t(Tn) * 7 + 8)) return -1;
     const size_t sm = size_t(Tn) * 4;
     static bool attr = false;
     if (!attr) {
@@ -326,12 +327,12 @@ int64_t launch_bin_count(Context& c, const DevCam& cam, const ts_render_config& 
         cudaMemsetAsync(c.bintot.p, 0, size_t(Tn) * 4, c.stream);
     }
     launch_exclusive_scan(c, c.bintot.p, nullptr, c.starts.p, Tn);
-    uint32_t hv[7] = {0, 0, 0, 0, 0, 0, 0};
+    uint32_t hv[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     cudaMemcpyAsync(&hv[0], c.starts.p + Tn, 4, cudaMemcpyDeviceToHost, c.stream);
-    cudaMemcpyAsync(&hv[1], meta, 6 * 4, cudaMemcpyDeviceToHost, c.stream);
+    cudaMemcpyAsync(&hv[1], meta, 7 * 4, cudaMemcpyDeviceToHost, c.stream);
     cudaStreamSynchronize(c.stream);
-    for (int k = 0; k < 5; ++k) c.bin_class[k] = hv[1 + k];
-    *max_len = hv[6];
+    for (int k = 0; k < 6; ++k) c.bin_class[k] = hv[1 + k];
+    *max_len = hv[7];
     return int64_t(hv[0]);
 }
 
@@ -382,6 +383,7 @@ void launch_tile_depth_sort(Context& c, int Tn, uint32_t max_len) {
     cudaStreamWaitEvent(c.side[1], c.fork_ev, 0);
     sort_variant<kCap2, 512>(c, cls + size_t(3) * Tn, c.bin_class[3], c.side[0]);
     sort_variant<kCap3, 1024>(c, cls + size_t(4) * Tn, c.bin_class[4], c.side[1]);
+    sort_variant<kCapM, 512>(c, cls + size_t(5) * Tn, c.bin_class[5], c.side[1]);
     sort_variant<kCap1, 512>(c, cls + size_t(2) * Tn, c.bin_class[2], c.stream);
     sort_variant<kCap0, 256>(c, cls + size_t(1) * Tn, c.bin_class[1], c.stream);
     for (int k = 0; k < 2; ++k) {

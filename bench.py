@@ -180,6 +180,8 @@ def run_reference(args):
     O.set_workers(os.cpu_count() or 1)
     target, _, _, _ = O.render(gt, w.n, cam, cfg)
     p0 = scene.perturb(gt, w.n, w.seed)
+    if not args.no_morton:  # same Gaussian order as the GPU arm
+        O.morton_reorder(p0, w.n)
     cb = cpu_step_baseline(w, gt, p0, cam, cfg, target, steps=args.steps, warmup=args.warmup)
     val = cb["value"]
     line = {"impl": "reference", "metric": METRIC, "value": val, "unit": "steps/s", "n_gpus": world,
@@ -187,7 +189,8 @@ def run_reference(args):
             "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (seeded random Gaussians, self-rendered target)",
             "config": {"workload": w.name, "gaussians": w.n, "sh_degree": w.sh_degree,
-                       "resolution": f"{w.width}x{w.height}", "views_per_step": 1, "parallelism": "host threads"},
+                       "resolution": f"{w.width}x{w.height}", "views_per_step": 1, "parallelism": "host threads",
+                       "gaussian_order": "random" if args.no_morton else "morton"},
             "cpu_baseline": {"value": val, "unit": "steps/s", "cores": cb["cores"], "kind": "port",
                              "sample": cb["sample"]},
             "e2e": {"value": val, "unit": "steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -219,6 +222,12 @@ def run_ours(args):
     e.set_target(0, target)
     p0 = scene.perturb(gt, n, w.seed)
     e.set_params(p0, n)
+    if not args.no_morton:
+        # steady-state training order: morton_reorder fires every 5000
+        # iterations while densifying, so a 3M-Gaussian store is in z-order; rendering is
+        # order-invariant (bitwise), the arrays just gain spatial locality
+        perm = e.morton_reorder()
+        p0 = scene.reorder_params(p0, n, perm)
     dp = DataParallelStep(e, mode=args.dp_mode)
     views = [(cam, cfg, 0)]
     step = 0
@@ -365,7 +374,9 @@ def run_ours(args):
                        "resolution": f"{w.width}x{w.height}", "views_per_step": world, "views_per_gpu": 1,
                        "parallelism": f"dp{world} (views; NCCL {args.dp_mode} of 59N fp32 grads)",
                        "optimizer": "fused_backward (SPEC.md:492-500)" if fused_bwd else "fused (SPEC.md:473-480)",
-                       "l2": "no flush: per-step working set ~9 GB >> 126 MB L2"},
+                       "l2": "no flush: per-step working set ~9 GB >> 126 MB L2",
+                       "gaussian_order": "random" if args.no_morton else
+                       "morton (SPEC.md:264-272 morton_reorder applied at setup, as the training schedule does)"},
             "e2e": {"value": world / (e2e_ms * 1e-3), "unit": "steps/s",
                     "h2d_bytes_per_step": int(w.height * w.width * 3 * 4 + 104 + 64),
                     "d2h_bytes_per_step": 16, "api": "ts_train_step (C-ABI) with pinned host target"},
@@ -409,6 +420,8 @@ def main():
                     help="optimizer mode (SPEC.md:525): fused = separate fused-Adam sweep (SPEC.md:473-480); "
                          "fused_backward = Adam inside the backward (SPEC.md:492-500, 1 GPU only)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-morton", action="store_true",
+                    help="keep the generator's random Gaussian order instead of the z-order training state")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -12,6 +12,7 @@ from dataclasses import dataclass
 
 import numpy as np
 
+from . import types as T
 from .types import Camera, pack_params
 
 
@@ -48,6 +49,14 @@ def random_params(n: int, s0: float, m_o: float, seed: int) -> np.ndarray:
     sh_dc = rng.uniform(-1.5, 1.5, (n, 3))
     sh_rest = rng.normal(0.0, 0.05, (n, 15, 3))
     return pack_params(means, log_scales, quats, logits, sh_dc, sh_rest)
+
+
+def reorder_params(params: np.ndarray, n: int, perm: np.ndarray) -> np.ndarray:
+    """Rows of every attribute block of a flat 59*n store in the order perm (new row i = old row perm[i])."""
+    out = np.empty_like(params)
+    for (a, b), wd in zip(T.group_slices(n), T.GROUP_WIDTH):
+        out[a:b] = params[a:b].reshape(n, wd)[perm].ravel()
+    return out
 
 
 def perturb(params: np.ndarray, n: int, seed: int) -> np.ndarray:

@@ -16,6 +16,8 @@ e.set_params(gt, w.n)
 target, _, _ = e.render(cam, cfg)
 e.set_target(0, target)
 e.set_params(scene.perturb(gt, w.n, w.seed), w.n)
+if os.environ.get("PROBE_MORTON"):
+    e.morton_reorder()
 for i in range(5):
     e.train_step(cam, cfg, T.AdamConfig.make(step=i + 1, mode=mode), want_loss=False)
 e.synchronize()

@@ -46,11 +46,18 @@ struct Rows {
     const float* g2;   // 12: dmx dmy dA dB dC do dr dg db
 };
 
+// SH-rest gradient consumers: store into a row, or hand to a per-element update
+struct RowSink {
+    float* a;
+    __device__ __forceinline__ void operator()(int k, float g) const { a[k] = g; }
+};
+
 // Adjoint of one visible Gaussian.  gs[14] = d{means(3), log_scales(3),
-// quats(4), opacity_logit(1), sh_dc(3)}; SH-rest gradients [0, nrest) are
-// written to grest.  Returns |dL/dmean2d| for the densification statistics.
-template <int DEG>
-__device__ __forceinline__ float pb_grads(const Rows& r, float* grest, const DevCam& cam,
+// quats(4), opacity_logit(1), sh_dc(3)}; SH-rest gradient k in [0, nrest) goes
+// to sink(k, g) right after rest[k] is last read (so the sink may update the
+// row in place).  Returns |dL/dmean2d| for the densification statistics.
+template <int DEG, class Sink>
+__device__ __forceinline__ float pb_grads(const Rows& r, const Sink& sink, const DevCam& cam,
                                           const ts_render_config& cfg, float nu, float (&gs)[14]) {
     constexpr int nb = (DEG + 1) * (DEG + 1);
     const float* W = cam.W;
@@ -217,7 +224,7 @@ __device__ __forceinline__ float pb_grads(const Rows& r, float* grest, const Dev
 #pragma unroll
         for (int k = 1; k < nb; ++k) {
             const float cf = r.rest[3 * (k - 1) + ch] * d;
-            grest[3 * (k - 1) + ch] = Y[k] * d;
+            sink(3 * (k - 1) + ch, Y[k] * d);
             ddir0 += dY[k][0] * cf;
             ddir1 += dY[k][1] * cf;
             ddir2 += dY[k][2] * cf;
@@ -384,14 +391,14 @@ __global__ void __launch_bounds__(kBlock) project_bwd_kernel(const float* __rest
         float nrm;
         if constexpr (ACCUM && nrest > 0) {
             float grest[nrest];
-            nrm = pb_grads<DEG>(rw, grest, cam, cfg, nu_hat ? nu_hat[g] : 1.f, gs);
+            nrm = pb_grads<DEG>(rw, RowSink{grest}, cam, cfg, nu_hat ? nu_hat[g] : 1.f, gs);
             float* grow = smem + L::kGRest + sh[9] + tid * 45;
 #pragma unroll
             for (int k = 0; k < nrest; ++k) grow[k] += grest[k];
         } else {
             // overwrite mode: gradients replace the parameter row in place (each
             // element is read by pb_grads before it is written)
-            nrm = pb_grads<DEG>(rw, DEG > 0 ? rest_row : dummy, cam, cfg, nu_hat ? nu_hat[g] : 1.f, gs);
+            nrm = pb_grads<DEG>(rw, RowSink{DEG > 0 ? rest_row : dummy}, cam, cfg, nu_hat ? nu_hat[g] : 1.f, gs);
         }
         const int64_t idx[14] = {off.means + 3 * g,  off.means + 3 * g + 1, off.means + 3 * g + 2, off.ls + 3 * g,
                                  off.ls + 3 * g + 1, off.ls + 3 * g + 2,    off.q + 4 * g,         off.q + 4 * g + 1,
@@ -529,7 +536,7 @@ __global__ void __launch_bounds__(kFB, 4) project_bwd_adam_kernel(float* __restr
         if (active) {
             const Rows rw{pr[0], pr[1], pr[2], pr[3][0], pr[4], pr[5], smem + L::kG2 + sh[6] + 12 * tid};
             // in place: every SH-rest element is read before its gradient is written
-            const float nrm = pb_grads<DEG>(rw, pr[5], cam, cfg, nu_hat ? nu_hat[g] : 1.f, gs);
+            const float nrm = pb_grads<DEG>(rw, RowSink{pr[5]}, cam, cfg, nu_hat ? nu_hat[g] : 1.f, gs);
             reinterpret_cast<float4*>(g2d)[3 * g] = make_float4(0.f, 0.f, 0.f, 0.f);
             reinterpret_cast<float4*>(g2d)[3 * g + 1] = make_float4(0.f, 0.f, 0.f, 0.f);
             reinterpret_cast<float4*>(g2d)[3 * g + 2] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -581,6 +588,7 @@ __global__ void __launch_bounds__(kFB, 4) project_bwd_adam_kernel(float* __restr
         }
     }
 }
+
 
 }  // namespace
 

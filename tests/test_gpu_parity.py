@@ -315,13 +315,13 @@ def test_cpp_host_driver():
     assert r["loss_last"] < 0.8 * r["loss_first"]
 
 
+@pytest.mark.parametrize("n", [30_000, 29_999])  # float4 sweep (N % 4 == 0) and the scalar sweep
 @pytest.mark.parametrize("mode", [T.ADAM_FUSED_BACKWARD, T.ADAM_FUSED_BACKWARD_SKIP])
-def test_fused_backward_adam_equals_separate(engine, mode):
+def test_fused_backward_adam_equals_separate(engine, mode, n):
     """fused_backward_update ends in the state of backward + fused
     Adam (resp. skip-invisible).  The 2D-gradient sums use fp32 atomics, so two
     runs agree bitwise only for Gaussians with a single (tile) contribution; those
     rows must match bit for bit, the rest to rounding."""
-    n = 30_000
     gt = scene.random_params(n, 0.004, 0.0, 31)
     cam = scene.make_camera(320, 200)
     cfg = T.RenderConfig.make(sh_degree=3)

@@ -28,9 +28,9 @@ __device__ __forceinline__ int refl(int i, int n) { return i < 0 ? -i : (i >= n 
 //                               onto p (per axis; separable)
 //   output   32x32  [0, 32)
 // The transposed filter is the same symmetric window.  Shared memory (floats):
-// A = 5 x 52 x 42 horizontal moments, later hb 3 x 42 x 47 and vb 3 x 47 x 32;
+// A = 5 x 52 x 42 horizontal moments, later hb 3 x 42 x 47;
 // B = 3 x 42 x 58 (input 2 x 52 x 52, then (a, b, c) column-padded to [-10, 48),
-// then the column-folded pass 3 x 58 x 32 row-padded to [-10, 48)).
+// then vb 3 x 47 x 32).
 // ---------------------------------------------------------------------------
 constexpr int kFT = 32;                   // output tile edge
 constexpr int kFI = kFT + 20;             // input region edge (52)
@@ -60,20 +60,31 @@ __global__ void __launch_bounds__(kFThreads) loss_fused_kernel(const float* __re
     float* xs = B;
     float* ys = B + kFI * kFI;
     {
-        // 4 rows x 64 columns per pass (52 active): the column's reflected index once per thread
+        // 4 rows x 64 columns per pass (52 active): the column's reflected index once per
+        // thread; all 13 rows' loads issued before any store (latency overlapped)
         const int c = tid & 63;
         if (c < kFI) {
             const int gx = refl(min(max(x0 - 10 + c, -(W - 1)), 2 * (W - 1)), W);
-            for (int r = tid >> 6; r < kFI; r += kFThreads / 64) {
+            float xv[kFI / 4], yv[kFI / 4];
+#pragma unroll
+            for (int k = 0; k < kFI / 4; ++k) {
+                const int r = (tid >> 6) + 4 * k;
                 const int gy = refl(min(max(y0 - 10 + r, -(H - 1)), 2 * (H - 1)), H);
-                const int gi = gy * W + gx;
-                xs[r * kFI + c] = __ldg(Xc + gi);
-                ys[r * kFI + c] = __ldg(Yc + gi);
+                xv[k] = __ldg(Xc + gy * W + gx);
+                yv[k] = __ldg(Yc + gy * W + gx);
+            }
+#pragma unroll
+            for (int k = 0; k < kFI / 4; ++k) {
+                const int r = (tid >> 6) + 4 * k;
+                xs[r * kFI + c] = xv[k];
+                ys[r * kFI + c] = yv[k];
             }
         }
     }
     __syncthreads();
-    // 2. horizontal moments: rows [0, 52) x moment cols [0, 42), items of 7 columns
+    // 2. horizontal moments: rows [0, 52) x moment cols [0, 42), items of 7 columns; the
+    //    L1 term of the tile's pixels from the same registers
+    float l1 = 0.f, ss = 0.f;
     {
         constexpr int S = 7, NS = kFM / S;
         for (int it = tid; it < kFI * NS; it += kFThreads) {
@@ -95,6 +106,11 @@ __global__ void __launch_bounds__(kFThreads) loss_fused_kernel(const float* __re
                     m4 = fmaf(wv.x, v.y, m4);
                 }
                 const int o = r * kFM + c0 + j;
+                {
+                    const int px = c0 + j - 5, py = r - 10;  // tile-relative pixel at this window centre
+                    if (px >= 0 && px < kFT && py >= 0 && py < kFT && x0 + px < W && y0 + py < H)
+                        l1 += fabsf(ab[j + 5].x - ab[j + 5].y);
+                }
                 A[o] = m01.x;
                 A[kFI * kFM + o] = m01.y;
                 A[2 * kFI * kFM + o] = m23.x;
@@ -106,7 +122,6 @@ __global__ void __launch_bounds__(kFThreads) loss_fused_kernel(const float* __re
     __syncthreads();
     // 3. vertical moments over moment rows [0, 42) -> SSIM and (a, b, c) into B as
     //    abc[q][r][c + 5] (padded columns [-10, 48) hold zeros)
-    float l1 = 0.f, ss = 0.f;
     {
         constexpr int S = 6, NS = kFM / S;
         for (int it = tid; it < kFM * NS; it += kFThreads) {
@@ -158,11 +173,7 @@ __global__ void __launch_bounds__(kFThreads) loss_fused_kernel(const float* __re
                     ta = dS_dux - 2.f * ux * dS_dvx - uy * dS_dcxy;
                     tb = 2.f * dS_dvx;
                     tc = dS_dcxy;
-                    if (r >= 5 && r < 5 + kFT && c >= 5 && c < 5 + kFT) {
-                        ss += Sv;
-                        const int p = gy * W + gx;
-                        l1 += fabsf(__ldg(Xc + p) - __ldg(Yc + p));
-                    }
+                    if (r >= 5 && r < 5 + kFT && c >= 5 && c < 5 + kFT) ss += Sv;
                 }
                 B[0 * kFM * kFP + r * kFP + c + 5] = ta;
                 B[1 * kFM * kFP + r * kFP + c + 5] = tb;
@@ -211,37 +222,43 @@ __global__ void __launch_bounds__(kFThreads) loss_fused_kernel(const float* __re
         }
     }
     __syncthreads();
-    // 4b. fold columns -> hf[q][r + 5][c] (B, 3 x 58 x 32; padded rows [-10, 48) hold zeros)
-    {
-        const int c = tid & 31;
-        const int px = x0 + c;
-        const int ml = (px >= 1 && px <= 5) ? -px - x0 + 5 : -1;                             // mirror of -px
-        const int mr = (px >= W - 6 && px <= W - 2) ? 2 * (W - 1) - px - x0 + 5 : -1;        // mirror of 2(W-1)-px
-        for (int qr = tid >> 5; qr < 3 * kFP; qr += kFThreads / 32) {
-            const int q = qr / kFP, pr = qr - q * kFP, r = pr - 5;
-            float v = 0.f;
-            if (r >= 0 && r < kFM && px < W) {
-                const float* hb = A + q * kFM * kFV + r * kFV;
-                v = hb[c + 5];
-                if (ml >= 0) v += hb[ml];
-                if (mr >= 0) v += hb[mr];
-            }
-            B[qr * kFT + c] = v;
-        }
-    }
-    __syncthreads();
-    // 5a. vertical transposed pass at virtual rows [-5, 42): vb[q][m][c] (A, 3 x 47 x 32); (a, b) packed
+    // 5a. vertical transposed pass at virtual rows [-5, 42) straight from hb, with the
+    //     column fold of the reflect padding applied on the fly (tiles at the image's
+    //     left/right edge only): vb[q][m][c] (B, 3 x 47 x 32); hb rows outside [0, 42)
+    //     and columns beyond the image are zero; (a, b) packed
     {
         constexpr int S = 6, NS = (kFV + S - 1) / S;  // 8 groups (48 rows, last partly unused)
+        const bool fold = x0 <= 5 || x0 + kFT - 1 >= W - 6;  // CTA-uniform
         for (int it = tid; it < kFT * NS; it += kFThreads) {
             const int c = it % kFT, r0 = (it / kFT) * S;
+            const int px = x0 + c;
+            const int ml = fold && px >= 1 && px <= 5 ? -px - x0 + 5 : -1;                       // mirror of -px
+            const int mr = fold && px >= W - 6 && px <= W - 2 ? 2 * (W - 1) - px - x0 + 5 : -1;  // mirror of 2(W-1)-px
             float2 ab[S + 10];
             float cc[S + 10];
 #pragma unroll
             for (int k = 0; k < S + 10; ++k) {
-                const bool in = r0 + k < kFP;
-                ab[k] = in ? make_float2(B[(r0 + k) * kFT + c], B[kFP * kFT + (r0 + k) * kFT + c]) : make_float2(0.f, 0.f);
-                cc[k] = in ? B[2 * kFP * kFT + (r0 + k) * kFT + c] : 0.f;
+                const int r = r0 + k - 5;
+                const bool in = r >= 0 && r < kFM && px < W;
+                const float* h0 = A + r * kFV;
+                float va = 0.f, vbb = 0.f, vc = 0.f;
+                if (in) {
+                    va = h0[c + 5];
+                    vbb = h0[kFM * kFV + c + 5];
+                    vc = h0[2 * kFM * kFV + c + 5];
+                    if (ml >= 0) {
+                        va += h0[ml];
+                        vbb += h0[kFM * kFV + ml];
+                        vc += h0[2 * kFM * kFV + ml];
+                    }
+                    if (mr >= 0) {
+                        va += h0[mr];
+                        vbb += h0[kFM * kFV + mr];
+                        vc += h0[2 * kFM * kFV + mr];
+                    }
+                }
+                ab[k] = make_float2(va, vbb);
+                cc[k] = vc;
             }
 #pragma unroll
             for (int j = 0; j < S; ++j) {
@@ -253,9 +270,9 @@ __global__ void __launch_bounds__(kFThreads) loss_fused_kernel(const float* __re
                     sc = fmaf(wk[k], cc[j + k], sc);
                 }
                 if (r0 + j < kFV) {
-                    A[(r0 + j) * kFT + c] = sab.x;
-                    A[kFV * kFT + (r0 + j) * kFT + c] = sab.y;
-                    A[2 * kFV * kFT + (r0 + j) * kFT + c] = sc;
+                    B[(r0 + j) * kFT + c] = sab.x;
+                    B[kFV * kFT + (r0 + j) * kFT + c] = sab.y;
+                    B[2 * kFV * kFT + (r0 + j) * kFT + c] = sc;
                 }
             }
         }
@@ -269,7 +286,7 @@ __global__ void __launch_bounds__(kFThreads) loss_fused_kernel(const float* __re
         float t[3];
 #pragma unroll
         for (int q = 0; q < 3; ++q) {
-            const float* vb = A + q * kFV * kFT + c;
+            const float* vb = B + q * kFV * kFT + c;
             float v = vb[(r + 5) * kFT];
             if (py >= 1 && py <= 5) v += vb[(-py - y0 + 5) * kFT];
             if (py >= H - 6 && py <= H - 2) v += vb[(2 * (H - 1) - py - y0 + 5) * kFT];

@@ -6,6 +6,7 @@
 //   a = dS/dmu_x - 2 mu_x dS/dv_x - mu_y dS/dcov,  b = 2 dS/dv_x,  c = dS/dcov,
 //   dL/dC = (0.8 sign(x - y) - 0.2 dSSIM/dx) / M.
 #include <cmath>
+#include <type_traits>
 
 #include "ts_internal.cuh"
 #include "ts_math.cuh"
@@ -82,8 +83,7 @@ __global__ void __launch_bounds__(kFThreads) loss_fused_kernel(const float* __re
         }
     }
     __syncthreads();
-    // 2. horizontal moments: rows [0, 52) x moment cols [0, 42), items of 7 columns; the
-    //    L1 term of the tile's pixels from the same registers
+    // 2. horizontal moments: rows [0, 52) x moment cols [0, 42), items of 7 columns
     float l1 = 0.f, ss = 0.f;
     {
         constexpr int S = 7, NS = kFM / S;
@@ -106,11 +106,6 @@ __global__ void __launch_bounds__(kFThreads) loss_fused_kernel(const float* __re
                     m4 = fmaf(wv.x, v.y, m4);
                 }
                 const int o = r * kFM + c0 + j;
-                {
-                    const int px = c0 + j - 5, py = r - 10;  // tile-relative pixel at this window centre
-                    if (px >= 0 && px < kFT && py >= 0 && py < kFT && x0 + px < W && y0 + py < H)
-                        l1 += fabsf(ab[j + 5].x - ab[j + 5].y);
-                }
                 A[o] = m01.x;
                 A[kFI * kFM + o] = m01.y;
                 A[2 * kFI * kFM + o] = m23.x;
@@ -123,7 +118,7 @@ __global__ void __launch_bounds__(kFThreads) loss_fused_kernel(const float* __re
     // 3. vertical moments over moment rows [0, 42) -> SSIM and (a, b, c) into B as
     //    abc[q][r][c + 5] (padded columns [-10, 48) hold zeros)
     {
-        constexpr int S = 6, NS = kFM / S;
+        constexpr int S = 7, NS = kFM / S;  // 6 x 42 = 252 items: one round of 256 threads
         for (int it = tid; it < kFM * NS; it += kFThreads) {
             const int c = it % kFM, r0 = (it / kFM) * S;
             float m[S][5];
@@ -229,53 +224,58 @@ __global__ void __launch_bounds__(kFThreads) loss_fused_kernel(const float* __re
     {
         constexpr int S = 6, NS = (kFV + S - 1) / S;  // 8 groups (48 rows, last partly unused)
         const bool fold = x0 <= 5 || x0 + kFT - 1 >= W - 6;  // CTA-uniform
-        for (int it = tid; it < kFT * NS; it += kFThreads) {
-            const int c = it % kFT, r0 = (it / kFT) * S;
-            const int px = x0 + c;
-            const int ml = fold && px >= 1 && px <= 5 ? -px - x0 + 5 : -1;                       // mirror of -px
-            const int mr = fold && px >= W - 6 && px <= W - 2 ? 2 * (W - 1) - px - x0 + 5 : -1;  // mirror of 2(W-1)-px
-            float2 ab[S + 10];
-            float cc[S + 10];
+        auto pass = [&](auto fold_tag) {
+            constexpr bool kFold = decltype(fold_tag)::value;
+            for (int it = tid; it < kFT * NS; it += kFThreads) {
+                const int c = it % kFT, r0 = (it / kFT) * S;
+                const int px = x0 + c;
+                const int ml = kFold && px >= 1 && px <= 5 ? -px - x0 + 5 : -1;                       // mirror of -px
+                const int mr = kFold && px >= W - 6 && px <= W - 2 ? 2 * (W - 1) - px - x0 + 5 : -1;  // of 2(W-1)-px
+                float2 ab[S + 10];
+                float cc[S + 10];
 #pragma unroll
-            for (int k = 0; k < S + 10; ++k) {
-                const int r = r0 + k - 5;
-                const bool in = r >= 0 && r < kFM && px < W;
-                const float* h0 = A + r * kFV;
-                float va = 0.f, vbb = 0.f, vc = 0.f;
-                if (in) {
-                    va = h0[c + 5];
-                    vbb = h0[kFM * kFV + c + 5];
-                    vc = h0[2 * kFM * kFV + c + 5];
-                    if (ml >= 0) {
-                        va += h0[ml];
-                        vbb += h0[kFM * kFV + ml];
-                        vc += h0[2 * kFM * kFV + ml];
+                for (int k = 0; k < S + 10; ++k) {
+                    const int r = r0 + k - 5;
+                    const bool in = r >= 0 && r < kFM && px < W;
+                    const float* h0 = A + r * kFV;
+                    float va = 0.f, vbb = 0.f, vc = 0.f;
+                    if (in) {
+                        va = h0[c + 5];
+                        vbb = h0[kFM * kFV + c + 5];
+                        vc = h0[2 * kFM * kFV + c + 5];
+                        if (kFold && ml >= 0) {
+                            va += h0[ml];
+                            vbb += h0[kFM * kFV + ml];
+                            vc += h0[2 * kFM * kFV + ml];
+                        }
+                        if (kFold && mr >= 0) {
+                            va += h0[mr];
+                            vbb += h0[kFM * kFV + mr];
+                            vc += h0[2 * kFM * kFV + mr];
+                        }
                     }
-                    if (mr >= 0) {
-                        va += h0[mr];
-                        vbb += h0[kFM * kFV + mr];
-                        vc += h0[2 * kFM * kFV + mr];
+                    ab[k] = make_float2(va, vbb);
+                    cc[k] = vc;
+                }
+#pragma unroll
+                for (int j = 0; j < S; ++j) {
+                    float2 sab = make_float2(0.f, 0.f);
+                    float sc = 0.f;
+#pragma unroll
+                    for (int k = 0; k < 11; ++k) {
+                        sab = tsx::fma2(tsx::dup2(wk[k]), ab[j + k], sab);
+                        sc = fmaf(wk[k], cc[j + k], sc);
+                    }
+                    if (r0 + j < kFV) {
+                        B[(r0 + j) * kFT + c] = sab.x;
+                        B[kFV * kFT + (r0 + j) * kFT + c] = sab.y;
+                        B[2 * kFV * kFT + (r0 + j) * kFT + c] = sc;
                     }
                 }
-                ab[k] = make_float2(va, vbb);
-                cc[k] = vc;
             }
-#pragma unroll
-            for (int j = 0; j < S; ++j) {
-                float2 sab = make_float2(0.f, 0.f);
-                float sc = 0.f;
-#pragma unroll
-                for (int k = 0; k < 11; ++k) {
-                    sab = tsx::fma2(tsx::dup2(wk[k]), ab[j + k], sab);
-                    sc = fmaf(wk[k], cc[j + k], sc);
-                }
-                if (r0 + j < kFV) {
-                    B[(r0 + j) * kFT + c] = sab.x;
-                    B[kFV * kFT + (r0 + j) * kFT + c] = sab.y;
-                    B[2 * kFV * kFT + (r0 + j) * kFT + c] = sc;
-                }
-            }
-        }
+        };
+        if (fold) pass(std::true_type{});
+        else pass(std::false_type{});
     }
     __syncthreads();
     // 5b. fold rows; dL/dC = (0.8 sign(x - y) - 0.2 (Wt a + x Wt b + y Wt c)) / M
@@ -296,6 +296,7 @@ __global__ void __launch_bounds__(kFThreads) loss_fused_kernel(const float* __re
         const float xv = __ldg(Xc + p), yv = __ldg(Yc + p);
         const float dS = t[0] + xv * t[1] + yv * t[2];
         const float d = xv - yv;
+        l1 += fabsf(d);
         const float sg = d > 0.f ? 1.f : (d < 0.f ? -1.f : 0.f);
         dL[size_t(ch) * P + p] = (0.8f * sg - 0.2f * dS) * inv_m;
     }

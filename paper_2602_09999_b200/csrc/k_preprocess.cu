@@ -49,14 +49,20 @@ __global__ void __launch_bounds__(kBlock) preprocess_kernel(
             for (int k = 0; k < 5; ++k) sh[k] = s5[k];
         }
     }
-    if (g >= N) return;
+    const bool live = g < N;  // dead lanes stay for the warp-cooperative cull below
     const int tid = threadIdx.x;
     float4 s0 = make_float4(0.f, 0.f, 0.f, 0.f), s1 = s0, s2 = s0;
     uint32_t cnt = 0;
     uint4 rc = make_uint4(1u, 1u, 0u, 0u);  // empty: tx0=1 > tx1=0
     bool ok = false;
     float zh = 0.f;
+    // exact-cull inputs of the warp-cooperative pass (ntl = 0: nothing to test)
+    uint32_t ntl_c = 0, rect0 = 0;
+    int tw_c = 1;
+    float mx_c = 0.f, my_c = 0.f, A_c = 0.f, B_c = 0.f, C_c = 0.f, k2_c = 0.f, nBA_c = 0.f, nBC_c = 0.f;
+    bool big_c = false;
     do {
+        if (!live) break;
         const float* W = cam.W;
         const float* mus = sm + kMu + sh[0] + 3 * tid;
         const float m0 = mus[0], m1 = mus[1], m2 = mus[2];
@@ -245,20 +251,77 @@ __global__ void __launch_bounds__(kBlock) preprocess_kernel(
                 for (int tyy = ty0; tyy <= ty1; ++tyy)
                     for (int txx = tx0; txx <= tx1; ++txx) atomicAdd(hrow + tyy * cam.tiles_x + txx, 1u);
         } else {
-            const float nBA = div(-B, A), nBC = div(-B, C);
-            int bit = 0;
-            for (int tyy = ty0; tyy <= ty1; ++tyy)
-                for (int txx = tx0; txx <= tx1; ++txx, ++bit) {
-                    const bool keep = tile_keep(mx, my, A, B, C, k2, nBA, nBC, txx, tyy, cam.w, cam.h);
-                    cnt += keep ? 1u : 0u;
-                    if (keep && !big) mask |= 1ull << bit;
-                    if (keep && hrow) atomicAdd(hrow + tyy * cam.tiles_x + txx, 1u);
-                }
+            ntl_c = uint32_t(ntl);
+            rect0 = uint32_t(tx0) | (uint32_t(ty0) << 16);
+            tw_c = tx1 - tx0 + 1;
+            mx_c = mx, my_c = my, A_c = A, B_c = B, C_c = C, k2_c = k2;
+            nBA_c = div(-B, A), nBC_c = div(-B, C);
+            big_c = big;
         }
         rc.z = uint32_t(mask);
         rc.w = uint32_t(mask >> 32);
     } while (false);
     (void)ok;
+    if (cfg.cull_mode != 0) {
+        // tile_cull_exact, warp-cooperative: the warp's (Gaussian, rect tile) pairs are
+        // enumerated as one list (exclusive scan of the rect sizes) and tested 32 at a
+        // time, so lanes with small rects do not idle behind the warp's largest one.
+        // Pair e belongs to the last lane whose scan offset is <= e; each owner
+        // gathers its keep bits (row-major rect order) from the ballots.
+        const unsigned kFull = 0xffffffffu;
+        const int lane = threadIdx.x & 31;
+        uint32_t incl = ntl_c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t t = __shfl_up_sync(kFull, incl, o);
+            if (lane >= o) incl += t;
+        }
+        const uint32_t excl = incl - ntl_c;
+        const uint32_t total = __shfl_sync(kFull, incl, 31);
+        const float rcp_tw = 1.f / float(tw_c);
+        uint32_t* hrow = binH ? binH + size_t(g0 / bin_chunk) * size_t(cam.tiles_x * cam.tiles_y) : nullptr;
+        uint64_t mask = 0;
+        for (uint32_t base = 0; base < total; base += 32) {
+            const uint32_t e = base + uint32_t(lane);
+            int own = 0;
+#pragma unroll
+            for (int step = 16; step >= 1; step >>= 1) {
+                const uint32_t ex = __shfl_sync(kFull, excl, own + step);
+                if (ex <= e) own += step;
+            }
+            const float omx = __shfl_sync(kFull, mx_c, own), omy = __shfl_sync(kFull, my_c, own);
+            const float oA = __shfl_sync(kFull, A_c, own), oB = __shfl_sync(kFull, B_c, own);
+            const float oC = __shfl_sync(kFull, C_c, own), ok2 = __shfl_sync(kFull, k2_c, own);
+            const float onBA = __shfl_sync(kFull, nBA_c, own), onBC = __shfl_sync(kFull, nBC_c, own);
+            const uint32_t orect = __shfl_sync(kFull, rect0, own), oex = __shfl_sync(kFull, excl, own);
+            const int otw = __shfl_sync(kFull, tw_c, own);
+            const float orcp = __shfl_sync(kFull, rcp_tw, own);
+            bool keep = false;
+            if (e < total) {
+                const int li = int(e - oex);
+                int q = int(float(li) * orcp);
+                int r = li - q * otw;
+                if (r < 0) r += otw, --q;
+                if (r >= otw) r -= otw, ++q;
+                const int txx = int(orect & 0xffffu) + r, tyy = int(orect >> 16) + q;
+                keep = tile_keep(omx, omy, oA, oB, oC, ok2, onBA, onBC, txx, tyy, cam.w, cam.h);
+                if (keep && hrow) atomicAdd(hrow + tyy * cam.tiles_x + txx, 1u);
+            }
+            const uint32_t K = __ballot_sync(kFull, keep);
+            if (ntl_c) {
+                const uint32_t lo = excl > base ? excl : base, hi = incl < base + 32 ? incl : base + 32;
+                if (lo < hi) {
+                    const uint32_t len = hi - lo;
+                    const uint32_t bits = (K >> (lo - base)) & (len == 32 ? kFull : ((1u << len) - 1u));
+                    cnt += __popc(bits);
+                    if (!big_c) mask |= uint64_t(bits) << (lo - excl);
+                }
+            }
+        }
+        rc.z = uint32_t(mask);
+        rc.w = uint32_t(mask >> 32);
+    }
+    if (!live) return;
     splat[3 * g] = s0;
     splat[3 * g + 1] = s1;
     splat[3 * g + 2] = s2;

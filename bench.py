@@ -129,18 +129,22 @@ def dist_env():
     return world, rank, local
 
 
-def rank_camera(w, rank):
-    """Rank 0 renders the headline view; other ranks views rotated a few degrees about the scene centre."""
+REF_STEPS = 10  # cap of the reference (CPU) arm's timed steps (~3 s each at workload H)
+N_VIEWS = 8  # training cameras cycled one per step (per GPU), as a 3DGS trainer walks its view set
+
+
+def view_camera(w, j):
+    """Camera j of the ring: the headline view (j = 0) rotated by 360/N_VIEWS * j degrees about the
+    scene's vertical axis.  Every view sees the whole synthetic cube (same per-view workload)."""
     base = np.array([0.3, -0.8, -3.5])
-    if rank == 0:
-        return scene.make_camera(w.width, w.height, tuple(base))
-    a = math.radians(4.0 * rank)
+    a = math.radians(360.0 / N_VIEWS * j)
     R = np.array([[math.cos(a), 0, math.sin(a)], [0, 1, 0], [-math.sin(a), 0, math.cos(a)]])
     return scene.make_camera(w.width, w.height, tuple(R @ base))
 
 
-def cpu_step_baseline(w, gt, p0, cam, cfg, target, steps=1, warmup=0):
-    """The C++ oracle (port of SPEC.md) on all host cores: full single-view training steps."""
+def cpu_step_baseline(w, gt, p0, cams, cfg, targets, steps=1, warmup=0):
+    """The C++ oracle (port of SPEC.md) on all host cores: full single-view training steps, step i on
+    view i mod len(cams)."""
     from oracle import oracle as O
     cores = os.cpu_count() or 1
     O.set_workers(cores)
@@ -154,7 +158,8 @@ def cpu_step_baseline(w, gt, p0, cam, cfg, target, steps=1, warmup=0):
     for i in range(warmup + steps):
         adam = T.AdamConfig.make(step=i + 1)
         t0 = time.perf_counter()
-        _, st = O.train_step(params, m, v, n, cam, cfg, target, adam, acc, vc)
+        j = i % len(cams)
+        _, st = O.train_step(params, m, v, n, cams[j], cfg, targets[j], adam, acc, vc)
         dt = time.perf_counter() - t0
         if i >= warmup:
             times.append(dt)
@@ -162,7 +167,7 @@ def cpu_step_baseline(w, gt, p0, cam, cfg, target, steps=1, warmup=0):
     t = float(np.mean(times))
     return {"value": 1.0 / t, "unit": "steps/s", "cores": cores, "kind": "port",
             "sample": f"{steps} full training step(s) of workload {w.name} ({n} Gaussians, SH{w.sh_degree}, "
-                      f"{w.width}x{w.height}, 1 view): render+loss+backward+Adam",
+                      f"{w.width}x{w.height}, 1 view per step): render+loss+backward+Adam",
             "s_per_step": t,
             "stage_s": dict(zip(("preprocess", "binning", "blend", "loss", "raster_bwd", "project_bwd", "adam"),
                                 [round(float(x), 4) for x in stages[:7]])) if stages is not None else None}
@@ -175,21 +180,24 @@ def run_reference(args):
     w = scene.WORKLOADS[args.workload]
     from oracle import oracle as O
     gt = scene.random_params(w.n, w.s0, w.m_o, w.seed)
-    cam = rank_camera(w, 0)
+    # bounded sample: at most REF_STEPS timed steps (+1 warm-up) so the arm ends in about a minute
+    steps, warmup = max(1, min(args.steps, REF_STEPS)), min(args.warmup, 1)
+    cams = [view_camera(w, j) for j in range(min(N_VIEWS, warmup + steps))]
     cfg = T.RenderConfig.make(sh_degree=w.sh_degree)
     O.set_workers(os.cpu_count() or 1)
-    target, _, _, _ = O.render(gt, w.n, cam, cfg)
+    targets = [O.render(gt, w.n, c, cfg)[0] for c in cams]
     p0 = scene.perturb(gt, w.n, w.seed)
     if not args.no_morton:  # same Gaussian order as the GPU arm
         O.morton_reorder(p0, w.n)
-    cb = cpu_step_baseline(w, gt, p0, cam, cfg, target, steps=args.steps, warmup=args.warmup)
+    cb = cpu_step_baseline(w, gt, p0, cams, cfg, targets, steps=steps, warmup=warmup)
     val = cb["value"]
     line = {"impl": "reference", "metric": METRIC, "value": val, "unit": "steps/s", "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 / val, "higher_is_better": True,
+            "steps": steps, "warmup": warmup, "steps_requested": args.steps, "ms_per_step": 1e3 / val, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (seeded random Gaussians, self-rendered target)",
             "config": {"workload": w.name, "gaussians": w.n, "sh_degree": w.sh_degree,
                        "resolution": f"{w.width}x{w.height}", "views_per_step": 1, "parallelism": "host threads",
+                       "views": f"{N_VIEWS}-camera ring, one view per step",
                        "gaussian_order": "random" if args.no_morton else "morton"},
             "cpu_baseline": {"value": val, "unit": "steps/s", "cores": cb["cores"], "kind": "port",
                              "sample": cb["sample"]},
@@ -214,12 +222,19 @@ def run_ours(args):
     w = scene.WORKLOADS[args.workload]
     n = w.n
     gt = scene.random_params(n, w.s0, w.m_o, w.seed)
-    cam = rank_camera(w, rank)
+    # the view ring: rank r renders views r, r + N, ... (disjoint slices of each step's batch);
+    # every view's target is rendered from the GT store and kept in a device slot
+    cams = [view_camera(w, j) for j in range(N_VIEWS)]
+    cam = cams[rank % N_VIEWS]
     cfg = T.RenderConfig.make(sh_degree=w.sh_degree)
     e = Engine(local, stream=stream.cuda_stream)
     e.set_params(gt, n)
-    target, _, _ = e.render(cam, cfg)
-    e.set_target(0, target)
+    targets = []
+    for j, c in enumerate(cams):
+        t, _, _ = e.render(c, cfg)
+        e.set_target(j, t)
+        targets.append(t)
+    target = targets[rank % N_VIEWS]
     p0 = scene.perturb(gt, n, w.seed)
     e.set_params(p0, n)
     if not args.no_morton:
@@ -229,8 +244,10 @@ def run_ours(args):
         perm = e.morton_reorder()
         p0 = scene.reorder_params(p0, n, perm)
     dp = DataParallelStep(e, mode=args.dp_mode)
-    views = [(cam, cfg, 0)]
     step = 0
+
+    def view_of(s_):  # this rank's view at training step s_
+        return (s_ * world + rank) % N_VIEWS
     # auto = the faster single-GPU mode as measured (profiles/): the separate float4 Adam sweep runs at the
     # HBM roof while the fused kernel is occupancy-bound, so auto picks "fused"
     fused_bwd = args.adam_mode == "fused_backward"
@@ -245,10 +262,11 @@ def run_ours(args):
                                  zero_grads=0 if args.dp_mode == "allreduce" else 1)
 
     def train_step():
+        j = view_of(step)
         if world == 1:  # one public C-ABI call: forward, loss, backward, Adam (target slot on the device)
-            e.train_step(cam, cfg, adam_cfg(), slot=0, want_loss=False)
+            e.train_step(cams[j], cfg, adam_cfg(), slot=j, want_loss=False)
         else:
-            dp.step(views, adam_cfg())
+            dp.step([(cams[j], cfg, j)], adam_cfg())
 
     for _ in range(args.warmup):
         step += 1
@@ -297,14 +315,19 @@ def run_ours(args):
         e.set_profiling(True)
         for _ in range(min(args.steps, 20)):
             step += 1
-            dp.step(views, adam_cfg(T.ADAM_FUSED))
+            j = view_of(step)
+            dp.step([(cams[j], cfg, j)], adam_cfg(T.ADAM_FUSED))
         torch.cuda.synchronize()
         split_times = e.stage_times()
         e.set_profiling(False)
 
     # ---- e2e: public C-ABI call with host (pinned) target and loss read-back each step ----
-    pin = PinnedBuffer((w.height, w.width, 3))
-    pin.array[...] = target
+    pins = []
+    for j in sorted({view_of(s_) for s_ in range(N_VIEWS)}):  # the views this rank trains
+        pb = PinnedBuffer((w.height, w.width, 3))
+        pb.array[...] = targets[j]
+        pins.append((j, pb))
+    pin_of = dict(pins)
     e2e_steps = max(3, min(args.steps, 50))
     torch.cuda.synchronize()
     if world > 1:
@@ -312,11 +335,12 @@ def run_ours(args):
     t0 = time.perf_counter()
     for _ in range(e2e_steps):
         step += 1
+        j = view_of(step)
         if world == 1:
-            e.train_step(cam, cfg, adam_cfg(), target_ptr=pin.ptr, want_loss=True)
+            e.train_step(cams[j], cfg, adam_cfg(), target_ptr=pin_of[j].ptr, want_loss=True)
         else:
-            e.render(cam, cfg, outputs=False)
-            e.training_loss(target=pin.array, want_value=True)
+            e.render(cams[j], cfg, outputs=False)
+            e.training_loss(target=pin_of[j].array, want_value=True)
             e.backward(None)
             dp.exchange_and_step(adam_cfg())
     torch.cuda.synchronize()
@@ -325,7 +349,8 @@ def run_ours(args):
         t = torch.tensor([e2e_ms], device=f"cuda:{local}")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_ms = float(t.item())
-    pin.free()
+    for _, pb in pins:
+        pb.free()
 
     # ---- per-stage accounting over the timed region ----
     bytes_ = stage_bytes(vstats, n, w.sh_degree, cam.n_tiles)
@@ -359,7 +384,7 @@ def run_ours(args):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_step_baseline(w, gt, p0, cam, cfg, target, steps=1, warmup=0)
+        cpu = cpu_step_baseline(w, gt, p0, cams[:1], cfg, targets[:1], steps=1, warmup=0)
 
     if rank == 0:
         value = world / (ms * 1e-3)
@@ -372,6 +397,8 @@ def run_ours(args):
                     "perturbed GT)",
             "config": {"workload": w.name, "gaussians": n, "sh_degree": w.sh_degree,
                        "resolution": f"{w.width}x{w.height}", "views_per_step": world, "views_per_gpu": 1,
+                       "views": f"{N_VIEWS}-camera ring (headline view rotated about the scene axis), "
+                                f"rank r trains view (step * N + r) mod {N_VIEWS}",
                        "parallelism": f"dp{world} (views; NCCL {args.dp_mode} of 59N fp32 grads)",
                        "optimizer": "fused_backward (SPEC.md:492-500)" if fused_bwd else "fused (SPEC.md:473-480)",
                        "l2": "no flush: per-step working set ~9 GB >> 126 MB L2",

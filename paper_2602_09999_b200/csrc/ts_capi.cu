@@ -644,7 +644,9 @@ ts_status ts_train_step(ts_ctx* x, const ts_camera* cam, const ts_render_config*
             CK(cudaEventCreateWithFlags(&c.copy_fork, cudaEventDisableTiming));
             CK(cudaEventCreateWithFlags(&c.copy_join, cudaEventDisableTiming));
         }
-        CK(cudaEventRecord(c.copy_fork, c.stream));  // the previous step is done with tgt_stage
+        // copy_fork marks the previous step's last read of tgt_stage (its layout conversion,
+        // early in that step), so this upload starts at once instead of behind the previous
+        // step's backward and Adam (never recorded yet: the wait is a no-op)
         CK(cudaStreamWaitEvent(c.copy_stream, c.copy_fork, 0));
         CK(cudaMemcpyAsync(c.tgt_stage.p, target_hwc, 3 * P * 4, cudaMemcpyHostToDevice, c.copy_stream));
         CK(cudaEventRecord(c.copy_join, c.copy_stream));
@@ -653,6 +655,7 @@ ts_status ts_train_step(ts_ctx* x, const ts_camera* cam, const ts_render_config*
     if (target_hwc) {
         CK(cudaStreamWaitEvent(c.stream, c.copy_join, 0));
         launch_hwc_to_chw(c, c.tgt_stage.p, c.tgt.p, int(P));
+        CK(cudaEventRecord(c.copy_fork, c.stream));  // tgt_stage free for the next upload
         if (ts_status s = run_loss(c, nullptr, slot, nullptr, c.tgt.p); s != TS_OK) return s;
     } else {
         if (ts_status s = run_loss(c, nullptr, slot, nullptr); s != TS_OK) return s;

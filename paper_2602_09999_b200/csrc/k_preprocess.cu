@@ -32,22 +32,26 @@ __global__ void __launch_bounds__(kBlock) preprocess_kernel(
     const int64_t g = g0 + threadIdx.x;
     const int rows = int(tmin<int64_t>(kBlock, N - g0));
     int sh[6] = {0, 0, 0, 0, 0, 0};
+    __shared__ unsigned long long bars[2];
     {
         const Span base[5] = {{sm + kMu, P + off.means + 3 * g0, 3 * rows},
                               {sm + kLs, P + off.ls + 3 * g0, 3 * rows},
                               {sm + kQ, P + off.q + 4 * g0, 4 * rows},
                               {sm + kOp, P + off.op + g0, rows},
                               {sm + kDc, P + off.dc + 3 * g0, 3 * rows}};
-        __shared__ unsigned long long bar;
+        // two barriers: the geometry rows gate the projection, the SH rows (the bulk of the
+        // bytes) are awaited only before the colour evaluation
+        mbar_init_all(bars, 2);
+        int s5[5];
+        tma_issue_spans(base, s5, &bars[0]);
+        for (int k = 0; k < 5; ++k) sh[k] = s5[k];
         if constexpr (nrest > 0) {
-            const Span sp[6] = {base[0], base[1], base[2], base[3], base[4],
-                                {sm + kRest, P + off.rest + g0 * 45, 45 * rows}};
-            stage_spans_tma(sp, sh, &bar);
-        } else {
-            int s5[5];
-            stage_spans_tma(base, s5, &bar);
-            for (int k = 0; k < 5; ++k) sh[k] = s5[k];
+            const Span sp[1] = {{sm + kRest, P + off.rest + g0 * 45, 45 * rows}};
+            int s1[1];
+            tma_issue_spans(sp, s1, &bars[1]);
+            sh[5] = s1[0];
         }
+        mbar_wait0(&bars[0]);
     }
     const bool live = g < N;  // dead lanes stay for the warp-cooperative cull below
     const int tid = threadIdx.x;
@@ -201,6 +205,7 @@ __global__ void __launch_bounds__(kBlock) preprocess_kernel(
             }
         }
         float rgb[3];
+        if constexpr (nrest > 0) mbar_wait0(&bars[1]);
         const float* rs = sm + kRest + sh[5] + tid * 45;
 #pragma unroll
         for (int ch = 0; ch < 3; ++ch) {
@@ -262,6 +267,9 @@ __global__ void __launch_bounds__(kBlock) preprocess_kernel(
         rc.w = uint32_t(mask >> 32);
     } while (false);
     (void)ok;
+    // every thread (also those that left the body early) sees the SH copy land before the
+    // CTA can retire: shared memory must not be released under an in-flight bulk copy
+    if constexpr (nrest > 0) mbar_wait0(&bars[1]);
     if (cfg.cull_mode != 0) {
         // tile_cull_exact, warp-cooperative: the warp's (Gaussian, rect tile) pairs are
         // enumerated as one list (exclusive scan of the rect sizes) and tested 32 at a

@@ -127,8 +127,21 @@ __device__ __forceinline__ void prefetch_l2(const float* src, int count) {
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a), "r"(uint32_t(e - a)) : "memory");
 }
 
+// wait for phase 0 of an mbarrier
+__device__ __forceinline__ void mbar_wait0(unsigned long long* bar) {
+    uint32_t ready = 0;
+    while (!ready) {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(ready)
+            : "r"(smem_u32(bar))
+            : "memory");
+    }
+}
+
+// issue the bulk copies of NS spans on an (initialised, visible) mbarrier; thread 0 only
 template <int NS>
-__device__ __forceinline__ void stage_spans_tma(const Span (&sp)[NS], int (&shift)[NS], unsigned long long* bar) {
+__device__ __forceinline__ void tma_issue_spans(const Span (&sp)[NS], int (&shift)[NS], unsigned long long* bar) {
     uint32_t bytes[NS];
     const char* src[NS];
     uint32_t total = 0;
@@ -141,11 +154,6 @@ __device__ __forceinline__ void stage_spans_tma(const Span (&sp)[NS], int (&shif
         total += bytes[s];
     }
     if (threadIdx.x == 0) {
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)));
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
         asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(total)
                      : "memory");
 #pragma unroll
@@ -157,14 +165,21 @@ __device__ __forceinline__ void stage_spans_tma(const Span (&sp)[NS], int (&shif
                     "l"(src[s]), "r"(bytes[s]), "r"(smem_u32(bar))
                     : "memory");
     }
-    uint32_t ready = 0;
-    while (!ready) {
-        asm volatile(
-            "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0;\n\tselp.u32 %0, 1, 0, p;\n\t}"
-            : "=r"(ready)
-            : "r"(smem_u32(bar))
-            : "memory");
+}
+
+__device__ __forceinline__ void mbar_init_all(unsigned long long* bars, int n) {
+    if (threadIdx.x == 0) {
+        for (int k = 0; k < n; ++k) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bars + k)));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
+    __syncthreads();
+}
+
+template <int NS>
+__device__ __forceinline__ void stage_spans_tma(const Span (&sp)[NS], int (&shift)[NS], unsigned long long* bar) {
+    mbar_init_all(bar, 1);
+    tma_issue_spans(sp, shift, bar);
+    mbar_wait0(bar);
 }
 
 }  // namespace ts

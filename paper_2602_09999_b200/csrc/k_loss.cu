@@ -40,10 +40,15 @@ constexpr int kFV = kFT + 15;             // virtual transposed-filter positions
 constexpr int kFP = kFV + 11;             // padded (a, b, c) columns / hf rows (58)
 constexpr int kFA = 5 * kFI * kFM;        // 10920
 constexpr int kFB = 3 * kFM * kFP;        // 7308
-constexpr int kFThreads = 256;
+#ifndef TS_LOSS_THREADS
+#define TS_LOSS_THREADS 320  // 10 warps: the 312 horizontal-moment items of a tile in one round
+#endif
+constexpr int kFThreads = TS_LOSS_THREADS;
+constexpr int kFRowGroups = kFThreads / 64;                       // input rows per pass
+constexpr int kFRowIters = (kFI + kFRowGroups - 1) / kFRowGroups;  // passes
 constexpr size_t kFusedSmem = size_t(kFA + kFB) * 4;
 
-__global__ void __launch_bounds__(kFThreads) loss_fused_kernel(const float* __restrict__ X,
+__global__ void __launch_bounds__(kFThreads, 3) loss_fused_kernel(const float* __restrict__ X,
                                                               const float* __restrict__ Y, float* __restrict__ dL,
                                                               int W, int H, float inv_m, double* __restrict__ acc) {
     extern __shared__ float fsm[];
@@ -61,24 +66,26 @@ __global__ void __launch_bounds__(kFThreads) loss_fused_kernel(const float* __re
     float* xs = B;
     float* ys = B + kFI * kFI;
     {
-        // 4 rows x 64 columns per pass (52 active): the column's reflected index once per
-        // thread; all 13 rows' loads issued before any store (latency overlapped)
+        // kFRowGroups rows x 64 columns per pass (52 active): the column's reflected index
+        // once per thread; all rows' loads issued before any store (latency overlapped)
         const int c = tid & 63;
         if (c < kFI) {
             const int gx = refl(min(max(x0 - 10 + c, -(W - 1)), 2 * (W - 1)), W);
-            float xv[kFI / 4], yv[kFI / 4];
+            float xv[kFRowIters], yv[kFRowIters];
 #pragma unroll
-            for (int k = 0; k < kFI / 4; ++k) {
-                const int r = (tid >> 6) + 4 * k;
+            for (int k = 0; k < kFRowIters; ++k) {
+                const int r = min((tid >> 6) + kFRowGroups * k, kFI - 1);
                 const int gy = refl(min(max(y0 - 10 + r, -(H - 1)), 2 * (H - 1)), H);
                 xv[k] = __ldg(Xc + gy * W + gx);
                 yv[k] = __ldg(Yc + gy * W + gx);
             }
 #pragma unroll
-            for (int k = 0; k < kFI / 4; ++k) {
-                const int r = (tid >> 6) + 4 * k;
-                xs[r * kFI + c] = xv[k];
-                ys[r * kFI + c] = yv[k];
+            for (int k = 0; k < kFRowIters; ++k) {
+                const int r = (tid >> 6) + kFRowGroups * k;
+                if (r < kFI) {
+                    xs[r * kFI + c] = xv[k];
+                    ys[r * kFI + c] = yv[k];
+                }
             }
         }
     }

@@ -30,7 +30,7 @@
 namespace ts {
 namespace {
 
-constexpr int kChunk = kBinChunk;  // Gaussians per chunk CTA (= kBinThreads * kPre)
+constexpr int kChunk = kBinChunk;  // largest chunk (= kBinThreads * kPre); bin_chunk_for picks the size
 constexpr int kBinThreads = 512;  // threads of the chunk kernels
 constexpr int kPre = 16;         // rects per thread, all loaded before the expansion
 
@@ -139,20 +139,21 @@ __global__ void __launch_bounds__(kBinThreads, 3) bin_scatter_kernel(const uint4
                                                                   int H, int tiles_x, int Tn, int cull_mode,
                                                                   const uint32_t* __restrict__ Hm,
                                                                   const uint32_t* __restrict__ starts,
-                                                                  uint32_t* __restrict__ out) {
+                                                                  uint32_t* __restrict__ out, int chunk) {
     extern __shared__ uint32_t cur[];
     const uint32_t* row = Hm + size_t(blockIdx.x) * Tn;
     for (int t = threadIdx.x; t < Tn; t += kBinThreads) cur[t] = starts[t] + row[t];
-    const int64_t g0 = int64_t(blockIdx.x) * kChunk;
+    const int64_t g0 = int64_t(blockIdx.x) * chunk;
+    const int npre = chunk / kBinThreads;  // rects per thread (<= kPre)
     uint4 rc[kPre];
 #pragma unroll
     for (int u = 0; u < kPre; ++u) {
         const int64_t g = g0 + threadIdx.x + u * kBinThreads;
-        rc[u] = g < N ? __ldg(rect + g) : make_uint4(1u, 1u, 0u, 0u);
+        rc[u] = u < npre && g < N ? __ldg(rect + g) : make_uint4(1u, 1u, 0u, 0u);
     }
     __syncthreads();
 #pragma unroll 1
-    for (int u = 0; u < kPre; ++u) {
+    for (int u = 0; u < npre; ++u) {
         const int64_t g = g0 + threadIdx.x + u * kBinThreads;
         warp_expand(rc[u], uint32_t(g), g < N, splat, W, H, tiles_x, cull_mode,
                     [&](int t, uint32_t gg) { out[atomicAdd(&cur[t], 1u)] = gg; });
@@ -306,7 +307,8 @@ bool bin_supported(int Tn) { return size_t(Tn) * 4 <= 200 * 1024; }
 
 int64_t launch_bin_count(Context& c, const DevCam& cam, const ts_render_config& cfg, uint32_t* max_len) {
     const int Tn = cam.tiles_x * cam.tiles_y;
-    const int nch = int(std::max<int64_t>(1, (c.N + kChunk - 1) / kChunk));
+    const int chunk = bin_chunk_for(c.N, c.sm_count);
+    const int nch = int(std::max<int64_t>(1, (c.N + chunk - 1) / chunk));
     // bintot: [0, Tn) totals | meta (8) | class lists 6 * Tn
     if (!ensure(c, c.binH, size_t(nch) * Tn) || !ensure(c, c.bintot, size_t(Tn) * 7 + 8)) return -1;
     const size_t sm = size_t(Tn) * 4;
@@ -339,10 +341,11 @@ int64_t launch_bin_count(Context& c, const DevCam& cam, const ts_render_config& 
 void launch_bin_scatter(Context& c, const DevCam& cam, const ts_render_config& cfg) {
     const int Tn = cam.tiles_x * cam.tiles_y;
     if (c.N == 0 || c.I == 0) return;
-    const int nch = int((c.N + kChunk - 1) / kChunk);
+    const int chunk = bin_chunk_for(c.N, c.sm_count);
+    const int nch = int((c.N + chunk - 1) / chunk);
     bin_scatter_kernel<<<nch, kBinThreads, size_t(Tn) * 4, c.stream>>>(c.rect.p, c.splat.p, c.N, cam.w, cam.h,
                                                                        cam.tiles_x, Tn, cfg.cull_mode, c.binH.p,
-                                                                       c.starts.p, c.ival[1].p);
+                                                                       c.starts.p, c.ival[1].p, chunk);
     TS_LAUNCHED(c);
 }
 

@@ -351,7 +351,8 @@ void launch_preprocess(Context& c, const DevCam& cam, const ts_render_config& cf
     uint32_t* binH = nullptr;
     const int Tn = cam.tiles_x * cam.tiles_y;
     if (c.binning_mode == 0 && bin_supported(Tn)) {
-        const size_t rows = size_t((c.N + kBinChunk - 1) / kBinChunk);
+        const int chunk = bin_chunk_for(c.N, c.sm_count);
+        const size_t rows = size_t((c.N + chunk - 1) / chunk);
         if (ensure(c, c.binH, rows * Tn)) {
             binH = c.binH.p;
             cudaMemsetAsync(binH, 0, rows * Tn * 4, c.stream);
@@ -362,7 +363,7 @@ void launch_preprocess(Context& c, const DevCam& cam, const ts_render_config& cf
     preprocess_kernel<D><<<unsigned(blocks), kBlock, 0, c.stream>>>(c.params.p, c.N, cam, cfg, c.splat.p, \
                                                                      c.rect.p, c.tcount.p, c.dkey[0].p,   \
                                                                      c.dperm[0].p, c.counters.p + 1, c.nu_hat.p,    \
-                                                                     binH, kBinChunk)
+                                                                     binH, bin_chunk_for(c.N, c.sm_count))
     switch (cfg.sh_degree) {
         case 0: TS_PRE(0); break;
         case 1: TS_PRE(1); break;

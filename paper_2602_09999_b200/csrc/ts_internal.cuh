@@ -121,7 +121,14 @@ void launch_duplicate(Context& c, const DevCam& cam, const ts_render_config& cfg
 void launch_tile_sort(Context& c, int tile_bits);
 void launch_ranges(Context& c, int n_tiles);
 // bucketed binning (k_bin.cu): returns I (syncs) and the longest tile list, -1 on OOM
-constexpr int kBinChunk = 8192;  // Gaussians per chunk of the bucketed binning (one histogram row)
+constexpr int kBinChunk = 8192;  // largest chunk of the bucketed binning (Gaussians per histogram row)
+// chunk size for N Gaussians: the largest of 8192 / 4096 / 2048 that still gives >= 2 chunk
+// CTAs per SM for the scatter (small stores would otherwise leave SMs idle)
+inline int bin_chunk_for(int64_t N, int sm_count) {
+    int ch = kBinChunk;
+    while (ch > 2048 && (N + ch - 1) / ch < 2 * int64_t(sm_count)) ch >>= 1;
+    return ch;
+}
 bool bin_supported(int Tn);
 int bin_sort_cap();
 int64_t launch_bin_count(Context& c, const DevCam& cam, const ts_render_config& cfg, uint32_t* max_len);

@@ -442,7 +442,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--workload", default="H", choices=sorted(scene.WORKLOADS))
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
-    ap.add_argument("--dp-mode", default="allreduce", choices=("allreduce", "sharded"))
+    ap.add_argument("--dp-mode", default="allreduce", choices=("allreduce", "sharded", "chunked"))
     ap.add_argument("--adam-mode", default="auto", choices=("auto", "fused", "fused_backward"),
                     help="optimizer mode (SPEC.md:525): fused = separate fused-Adam sweep (SPEC.md:473-480); "
                          "fused_backward = Adam inside the backward (SPEC.md:492-500, 1 GPU only)")

@@ -308,6 +308,10 @@ ts_status run_backward(Context& c, const float* dLdC_hwc) {
         return validation(c, "ts_backward(NULL) needs a preceding ts_loss");
     }
     DevCam dc = make_devcam(c.cam);
+    // vis = visible in any view since the last optimizer step: a new accumulation starts empty
+    // (cleared here rather than after Adam, so a range-chunked optimizer sweep sees it whole)
+    if (c.grad_state != Context::kGradLive)
+        CK(cudaMemsetAsync(c.vis.p, 0, size_t(std::max<int64_t>(c.N, 1)), c.stream));
     stage_begin(c, 8);
     launch_blend_bwd(c, dc, c.cfg);
     stage_end(c, 8);
@@ -330,13 +334,13 @@ ts_status run_backward_adam(Context& c, const float* dLdC_hwc, const ts_adam_con
         return validation(c, "ts_backward_adam(NULL) needs a preceding ts_loss");
     }
     DevCam dc = make_devcam(c.cam);
+    CK(cudaMemsetAsync(c.vis.p, 0, size_t(std::max<int64_t>(c.N, 1)), c.stream));  // new accumulation
     stage_begin(c, 8);
     launch_blend_bwd(c, dc, c.cfg);
     stage_end(c, 8);
     stage_begin(c, 9);
     launch_project_bwd_adam(c, dc, c.cfg, a);
     stage_end(c, 9);
-    CK(cudaMemsetAsync(c.vis.p, 0, size_t(std::max<int64_t>(c.N, 1)), c.stream));
     c.view_valid = false;
     c.loss_valid = false;
     return last_launch(c, "backward_adam");
@@ -348,8 +352,9 @@ ts_status run_adam(Context& c, const ts_adam_config& a, int64_t begin, int64_t e
     stage_begin(c, 10);
     launch_adam(c, a, begin, end);
     stage_end(c, 10);
-    CK(cudaMemsetAsync(c.vis.p, 0, size_t(std::max<int64_t>(c.N, 1)), c.stream));
-    if (begin == 0 && end == 59 * c.N) c.grad_state = a.zero_grads ? Context::kGradZero : Context::kGradStale;
+    // the sweep that reaches the end of the buffer completes the step (a full sweep, or the
+    // last of in-order range chunks, dp.py "chunked"): the gradient buffer is consumed
+    if (end == 59 * c.N) c.grad_state = a.zero_grads ? Context::kGradZero : Context::kGradStale;
     c.view_valid = false;
     c.loss_valid = false;
     return last_launch(c, "adam");

@@ -7,11 +7,15 @@ B200 nodes, gloo in the CPU tests) sums them (batch gradient = sum
 of per-view gradients), then every rank applies the same optimizer update, so
 parameters stay bitwise identical across ranks.
 
-Two exchange modes:
+Three exchange modes:
   * "allreduce": all_reduce(grads) + replicated fused Adam (rung 1);
   * "sharded":   all_reduce(grads) is replaced by reduce_scatter(grads) ->
                  Adam on this rank's 1/G slice -> all_gather(params) (rung 2),
-                 so each rank runs 1/G of the 28 B/element Adam sweep.
+                 so each rank runs 1/G of the 28 B/element Adam sweep;
+  * "chunked":   the all-reduce is issued as K asynchronous chunks of the flat
+                 buffer, and the replicated Adam sweeps chunk k as soon as its
+                 sum has landed, so the optimizer of chunk k overlaps the
+                 transfer of chunk k+1 (rung 3; the stream waits, not the host).
 
 The engine is anything exposing the Engine surface used below (the CUDA
 Engine in production; the tests pass a CPU stand-in to exercise the
@@ -46,10 +50,11 @@ def shard_bounds(length: int, world: int, rank: int, align: int = 4):
 
 
 class DataParallelStep:
-    def __init__(self, engine, mode: str = "allreduce", group=None):
-        assert mode in ("allreduce", "sharded")
+    def __init__(self, engine, mode: str = "allreduce", group=None, chunks: int = 8):
+        assert mode in ("allreduce", "sharded", "chunked")
         self.e = engine
         self.mode = mode
+        self.chunks = chunks
         self.group = group
         self.world = dist.get_world_size(group) if dist.is_available() and dist.is_initialized() else 1
         self.rank = dist.get_rank(group) if self.world > 1 else 0
@@ -73,6 +78,16 @@ class DataParallelStep:
         if self.mode == "allreduce":
             dist.all_reduce(g, op=dist.ReduceOp.SUM, group=self.group)
             self.e.adam_step(adam)
+            return
+        if self.mode == "chunked":
+            L = g.numel()
+            bounds = [shard_bounds(L, self.chunks, k)[:2] for k in range(self.chunks)]
+            bounds = [(b, e) for b, e in bounds if e > b]
+            works = [dist.all_reduce(g[b:e], op=dist.ReduceOp.SUM, group=self.group, async_op=True)
+                     for b, e in bounds]
+            for (b, e), w in zip(bounds, works):  # in order: the last sweep marks the buffer consumed
+                w.wait()
+                self.e.adam_step(adam, begin=b, end=e)
             return
         L = g.numel()
         b, e, per = shard_bounds(L, self.world, self.rank)

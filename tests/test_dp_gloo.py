@@ -52,7 +52,7 @@ def _rank_main(rank, world, port, mode, out_dir):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("mode", ["allreduce", "sharded"])
+@pytest.mark.parametrize("mode", ["allreduce", "sharded", "chunked"])
 def test_two_rank_step_equals_single_process(tmp_path, mode):
     from tests.cpu_engine import CpuEngine
 

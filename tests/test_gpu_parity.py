@@ -418,3 +418,38 @@ def test_bucketed_binning_equals_radix(engine, name):
     if name == "ties":
         ok, ov, orr, _ = O.instances(p, n, cam, cfg, sort="combined")
         assert np.array_equal(outs[0][1], ok) and np.array_equal(outs[0][2], ov)
+
+
+@pytest.mark.parametrize("mode", [T.ADAM_FUSED, T.ADAM_SKIP_INVISIBLE])
+def test_adam_in_order_range_chunks_equal_full_sweep(engine, mode):
+    """dp.py "chunked": the optimizer applied as in-order range chunks (each after its slice of
+    the all-reduce) ends bitwise where one full sweep does (the oracle's, on the same
+    gradient), and the last chunk marks the gradient buffer consumed: a following backward
+    with zero upstream gradient overwrites it with zeros instead of accumulating."""
+    from paper_2602_09999_b200.dp import shard_bounds
+    w = scene.WORKLOADS["c1"]
+    p = scene.random_params(w.n, w.s0, w.m_o, w.seed)
+    cam = scene.workload_cameras(w)[0]
+    cfg = T.RenderConfig.make(sh_degree=0)
+    n = w.n
+    dl = np.random.default_rng(9).normal(0, 1e-3, (cam.height, cam.width, 3)).astype(np.float32)
+    engine.set_params(p, n)
+    engine.render(cam, cfg, outputs=False)
+    engine.backward(dl)
+    G, _, _, _, vc = engine.get_state()
+    a = T.AdamConfig.make(step=1, mode=mode, zero_grads=0)
+    for k in range(7):
+        b, e, _ = shard_bounds(59 * n, 7, k)
+        if e > b:
+            engine.adam_step(a, begin=b, end=e)
+    gp = engine.get_params()
+    _, gm, gv, _, _ = engine.get_state()
+    op, om, ov = p.copy(), np.zeros(59 * n, np.float32), np.zeros(59 * n, np.float32)
+    O.adam_step(op, G.copy(), om, ov, n, np.array(a.lr[:], np.float32), a.beta1, a.beta2, a.eps, a.bc1, a.bc2,
+                mode=mode, visible=(vc > 0).astype(np.uint8))
+    for x, y in ((gp, op), (gm, om), (gv, ov)):
+        assert np.array_equal(x.view(np.uint32), y.view(np.uint32))
+    engine.render(cam, cfg, outputs=False)
+    engine.backward(np.zeros_like(dl))
+    G2, _, _, _, _ = engine.get_state()
+    assert not G2.any()

@@ -5,7 +5,9 @@
 
 A step = one training iteration on one view per GPU (weak scaling: the
 view batch grows with N): render -> L1+D-SSIM loss -> backward -> (N>1: NCCL
-all-reduce of the flat gradient buffer over NVLink) -> fused Adam.  The default
+all-reduce of the flat gradient buffer over NVLink) -> fused Adam.  The views
+cycle over an 8-camera ring around the scene (a trainer walking its camera
+set); every view's target is rendered from the ground-truth store once.  The default
 workload "H" is BASELINE.json's metric point: 3M Gaussians, SH degree 3,
 1920x1080 (synthetic scene, random-init parameters; target rendered from the
 ground-truth store, trained store = seeded perturbation of it).

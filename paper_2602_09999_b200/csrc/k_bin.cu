@@ -6,9 +6,10 @@
 // is produced here by bucketing followed by a small per-tile sort, instead of
 // a depth sort over N plus a radix sort over I:
 //
-//   KB1 histogram   per-tile instance counts of every chunk of 8192 Gaussians,
-//                   H[chunk][tile], accumulated by K1 itself (k_preprocess.cu) with
-//                   fire-and-forget REDs as it decides each kept tile;
+//   KB1 histogram   per-tile instance counts of every chunk of Gaussians (8192, or
+//                   4096 / 2048 for small N, bin_chunk_for), H[chunk][tile],
+//                   accumulated by K1 itself (k_preprocess.cu) with fire-and-forget
+//                   REDs as it decides each kept tile;
 //   KB2 bin_colscan per tile: exclusive prefix of H over chunks, tile totals and
 //                   the maximum list length; the exclusive scan of the totals is
 //                   the tile ranges (starts) and I;
@@ -21,7 +22,7 @@
 //                   then every element's rank inside its small bucket on (key, index)
 //                   gives its final position, written straight back.
 // Integer work only; the result is bit-identical to the two-stage radix path
-// (k_sort.cu), which remains the fallback for lists longer than kSortCap.
+// (k_sort.cu), which remains the fallback for lists longer than kCap3 (16384).
 #include "ts_internal.cuh"
 #include "ts_math.cuh"
 

@@ -63,13 +63,15 @@ __global__ void densify_flags_kernel(const float* __restrict__ P, const float* _
     if (pruned) atomicAdd(st + 2, pruned);
 }
 
-__global__ void densify_scatter_kernel(const float* __restrict__ P, const float* __restrict__ M,
-                                       const float* __restrict__ V, int64_t N, const uint32_t* __restrict__ fA,
-                                       const uint32_t* __restrict__ fB, const uint32_t* __restrict__ fC,
-                                       const uint32_t* __restrict__ oA, const uint32_t* __restrict__ oB,
-                                       const uint32_t* __restrict__ oC, int64_t nA, int64_t nB, int64_t NA,
-                                       float* __restrict__ OP, float* __restrict__ OM, float* __restrict__ OV,
-                                       uint64_t seed, int64_t iter) {
+// One pass per array (WHICH 0 = parameters, 1 / 2 = first / second Adam moment) into a
+// fresh 59*NA buffer; every destination row is written exactly once (kept rows, clones,
+// split children), so the output needs no clear.
+template <int WHICH>
+__global__ void densify_scatter_kernel(const float* __restrict__ P, const float* __restrict__ S, int64_t N,
+                                       const uint32_t* __restrict__ fA, const uint32_t* __restrict__ fB,
+                                       const uint32_t* __restrict__ fC, const uint32_t* __restrict__ oA,
+                                       const uint32_t* __restrict__ oB, const uint32_t* __restrict__ oC, int64_t nA,
+                                       int64_t nB, int64_t NA, float* __restrict__ O, uint64_t seed, int64_t iter) {
     const int64_t g = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (g >= N) return;
     const Off so(N), d(NA);
@@ -80,14 +82,16 @@ __global__ void densify_scatter_kernel(const float* __restrict__ P, const float*
         for (int k = 0; k < 6; ++k)
             for (int j = 0; j < width[k]; ++j) {
                 const int64_t s = soff[k] + width[k] * g + j, t = doff[k] + width[k] * r + j;
-                OP[t] = P[s];
-                OM[t] = moments ? M[s] : 0.f;
-                OV[t] = moments ? V[s] : 0.f;
+                O[t] = WHICH == 0 ? P[s] : (moments ? S[s] : 0.f);
             }
     };
     if (fA[g]) copy_row(oA[g], true);
     if (fB[g]) copy_row(nA + oB[g], false);
-    if (fC[g]) {
+    if (fC[g] && WHICH != 0) {
+        copy_row(nA + nB + oC[g], false);  // split children start with zero moments
+        copy_row(nA + nB + oC[g] + 1, false);
+    }
+    if (fC[g] && WHICH == 0) {
         using namespace tsx;
         const float* ls = P + so.ls + 3 * g;
         float q[4] = {P[so.q + 4 * g], P[so.q + 4 * g + 1], P[so.q + 4 * g + 2], P[so.q + 4 * g + 3]};
@@ -109,10 +113,10 @@ __global__ void densify_scatter_kernel(const float* __restrict__ P, const float*
                 zs[k] = mul(zs[k], expf_det(ls[k]));
             }
             for (int i = 0; i < 3; ++i)
-                OP[d.means + 3 * r + i] =
+                O[d.means + 3 * r + i] =
                     add(P[so.means + 3 * g + i], add(add(mul(R[3 * i], zs[0]), mul(R[3 * i + 1], zs[1])),
                                                      mul(R[3 * i + 2], zs[2])));
-            for (int k = 0; k < 3; ++k) OP[d.ls + 3 * r + k] = sub(ls[k], 0x1.e148a2p-2f);
+            for (int k = 0; k < 3; ++k) O[d.ls + 3 * r + k] = sub(ls[k], 0x1.e148a2p-2f);
         }
     }
 }
@@ -149,32 +153,38 @@ int64_t launch_densify(Context& c, float thresh, float log_small, float log_big,
     cudaMemcpyAsync(st, c.counters.p + 4, sizeof(st), cudaMemcpyDeviceToHost, c.stream);
     if (cudaStreamSynchronize(c.stream) != cudaSuccess) return -1;
     const int64_t nA = tot[0], nB = tot[1], nC = tot[2], NA = nA + nB + nC;
-    DevBuf<float> np, nm, nv;
     const size_t L = (size_t(59) * std::max<int64_t>(NA, 1) + 7) & ~size_t(3);
-    if (!ensure(c, np, L) || !ensure(c, nm, L) || !ensure(c, nv, L)) return -1;
-    cudaMemsetAsync(np.p, 0, L * 4, c.stream);
-    cudaMemsetAsync(nm.p, 0, L * 4, c.stream);
-    cudaMemsetAsync(nv.p, 0, L * 4, c.stream);
-    if (N) {
-        densify_scatter_kernel<<<blocks, bs, 0, c.stream>>>(c.params.p, c.m.p, c.v.p, N, fA, fB, fC, oA, oB, oC, nA,
-                                                           nB, NA, np.p, nm.p, nv.p, seed, iter);
-        TS_LAUNCHED(c);
+    // three passes through one spare 59*NA buffer, swapped in after each pass (no per-call
+    // allocation of the new store; capacities grow with slack, so growth reallocates rarely)
+    float** arrs[3] = {&c.params.p, &c.m.p, &c.v.p};
+    DevBuf<float>* bufs[3] = {&c.params, &c.m, &c.v};
+    for (int w = 0; w < 3; ++w) {
+        if (!ensure_grow(c, c.spare, L)) return -1;
+        if (N) {
+            const float* src = *arrs[w];
+            if (w == 0)
+                densify_scatter_kernel<0><<<blocks, bs, 0, c.stream>>>(c.params.p, src, N, fA, fB, fC, oA, oB, oC, nA,
+                                                                      nB, NA, c.spare.p, seed, iter);
+            else if (w == 1)
+                densify_scatter_kernel<1><<<blocks, bs, 0, c.stream>>>(c.params.p, src, N, fA, fB, fC, oA, oB, oC, nA,
+                                                                      nB, NA, c.spare.p, seed, iter);
+            else
+                densify_scatter_kernel<2><<<blocks, bs, 0, c.stream>>>(c.params.p, src, N, fA, fB, fC, oA, oB, oC, nA,
+                                                                      nB, NA, c.spare.p, seed, iter);
+            TS_LAUNCHED(c);
+        } else {
+            cudaMemsetAsync(c.spare.p, 0, L * 4, c.stream);
+        }
+        std::swap(*bufs[w], c.spare);
     }
-    if (cudaStreamSynchronize(c.stream) != cudaSuccess) return -1;
-    cudaFree(c.params.p);
-    cudaFree(c.m.p);
-    cudaFree(c.v.p);
-    c.params = np;
-    c.m = nm;
-    c.v = nv;
     c.N = NA;
     // resize the remaining per-Gaussian buffers and reset gradients / statistics
     const size_t n1 = size_t(std::max<int64_t>(NA, 1));
-    if (!ensure(c, c.grads, L) || !ensure(c, c.accum, n1 + 4) || !ensure(c, c.vcount, n1 + 4) ||
-        !ensure(c, c.splat, 3 * n1) || !ensure(c, c.rect, n1) || !ensure(c, c.tcount, n1) ||
-        !ensure(c, c.dkey[0], n1) || !ensure(c, c.dkey[1], n1) || !ensure(c, c.dperm[0], n1) ||
-        !ensure(c, c.dperm[1], n1) || !ensure(c, c.offsets, n1 + 1) || !ensure(c, c.g2d, 3 * n1 + 1) ||
-        !ensure(c, c.vis, n1) || !ensure(c, c.nu_hat, n1))
+    if (!ensure_grow(c, c.grads, L) || !ensure_grow(c, c.accum, n1 + 4) || !ensure_grow(c, c.vcount, n1 + 4) ||
+        !ensure_grow(c, c.splat, 3 * n1) || !ensure_grow(c, c.rect, n1) || !ensure_grow(c, c.tcount, n1) ||
+        !ensure_grow(c, c.dkey[0], n1) || !ensure_grow(c, c.dkey[1], n1) || !ensure_grow(c, c.dperm[0], n1) ||
+        !ensure_grow(c, c.dperm[1], n1) || !ensure_grow(c, c.offsets, n1 + 1) || !ensure_grow(c, c.g2d, 3 * n1 + 1) ||
+        !ensure_grow(c, c.vis, n1) || !ensure_grow(c, c.nu_hat, n1))
         return -1;
     c.nu_valid = false;  // new rows: the sampling rates must be recomputed (SPEC.md:614 interval)
     cudaMemsetAsync(c.grads.p, 0, c.grads.cap * 4, c.stream);

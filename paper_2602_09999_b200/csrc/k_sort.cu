@@ -497,50 +497,49 @@ static void gather_group(Context& c, const float* src, float* dst, const uint32_
 bool launch_morton_reorder(Context& c, uint32_t* perm_host) {
     const int64_t N = c.N;
     if (N == 0) return true;
-    DevBuf<unsigned long long> code[2];
-    DevBuf<uint32_t> idx[2];
-    DevBuf<float> box, tmp;
-    if (!ensure(c, code[0], N) || !ensure(c, code[1], N) || !ensure(c, idx[0], N) || !ensure(c, idx[1], N) ||
-        !ensure(c, box, 8) || !ensure(c, tmp, size_t(59) * N + 8))
+    // persistent scratch (codes, permutation, a spare 59*N store): no allocation per call
+    if (!ensure_grow(c, c.mcode[0], N) || !ensure_grow(c, c.mcode[1], N) || !ensure_grow(c, c.midx[0], N) ||
+        !ensure_grow(c, c.midx[1], N) || !ensure_grow(c, c.spare, std::max(c.params.cap, size_t(59) * N + 8)) ||
+        !ensure(c, c.dens, size_t(6) * (N + 1)))
         return false;
+    float* boxp = reinterpret_cast<float*>(c.dens.p);  // 6 floats of densify scratch
     const int init[6] = {0x7f800000, 0x7f800000, 0x7f800000, int(0x80000000u ^ ~0xff800000u),
                          int(0x80000000u ^ ~0xff800000u), int(0x80000000u ^ ~0xff800000u)};
-    cudaMemcpyAsync(box.p, init, sizeof(init), cudaMemcpyHostToDevice, c.stream);
-    bbox_kernel<<<c.sm_count * 2, 256, 0, c.stream>>>(c.params.p, N, box.p);
-    morton_code_kernel<<<unsigned((N + 255) / 256), 256, 0, c.stream>>>(c.params.p, N, box.p, code[0].p, idx[0].p);
+    cudaMemcpyAsync(boxp, init, sizeof(init), cudaMemcpyHostToDevice, c.stream);
+    bbox_kernel<<<c.sm_count * 2, 256, 0, c.stream>>>(c.params.p, N, boxp);
+    morton_code_kernel<<<unsigned((N + 255) / 256), 256, 0, c.stream>>>(c.params.p, N, boxp, c.mcode[0].p,
+                                                                        c.midx[0].p);
     c.launches += 2;
-    radix_sort<unsigned long long, 8>(c, code[0].p, idx[0].p, code[1].p, idx[1].p, N);
-    const uint32_t* perm = idx[0].p;  // 8 passes: result in buffer 0
-    // permute params, both moments (flat 59*N, per attribute block) and the statistics
+    radix_sort<unsigned long long, 8>(c, c.mcode[0].p, c.midx[0].p, c.mcode[1].p, c.midx[1].p, N);
+    const uint32_t* perm = c.midx[0].p;  // 8 passes: result in buffer 0
+    // permute params and both moments (flat 59*N, per attribute block) into the spare store
+    // and swap it in; then the statistics and sampling rates through the spare's head
     const Off o(N);
-    float* bufs[3] = {c.params.p, c.m.p, c.v.p};
-    for (float* b : bufs) {
-        gather_group<3>(c, b + o.means, tmp.p + o.means, perm, N);
-        gather_group<3>(c, b + o.ls, tmp.p + o.ls, perm, N);
-        gather_group<4>(c, b + o.q, tmp.p + o.q, perm, N);
-        gather_group<1>(c, b + o.op, tmp.p + o.op, perm, N);
-        gather_group<3>(c, b + o.dc, tmp.p + o.dc, perm, N);
-        gather_group<45>(c, b + o.rest, tmp.p + o.rest, perm, N);
-        cudaMemcpyAsync(b, tmp.p, size_t(59) * N * 4, cudaMemcpyDeviceToDevice, c.stream);
+    DevBuf<float>* bufs[3] = {&c.params, &c.m, &c.v};
+    for (DevBuf<float>* bp : bufs) {
+        if (!ensure_grow(c, c.spare, bp->cap)) return false;
+        const float* b = bp->p;
+        float* t = c.spare.p;
+        gather_group<3>(c, b + o.means, t + o.means, perm, N);
+        gather_group<3>(c, b + o.ls, t + o.ls, perm, N);
+        gather_group<4>(c, b + o.q, t + o.q, perm, N);
+        gather_group<1>(c, b + o.op, t + o.op, perm, N);
+        gather_group<3>(c, b + o.dc, t + o.dc, perm, N);
+        gather_group<45>(c, b + o.rest, t + o.rest, perm, N);
+        std::swap(*bp, c.spare);
     }
-    gather_group<1>(c, c.accum.p, tmp.p, perm, N);
-    cudaMemcpyAsync(c.accum.p, tmp.p, size_t(N) * 4, cudaMemcpyDeviceToDevice, c.stream);
-    gather_group<1>(c, c.vcount.p, tmp.p, perm, N);
-    cudaMemcpyAsync(c.vcount.p, tmp.p, size_t(N) * 4, cudaMemcpyDeviceToDevice, c.stream);
+    float* tmp = c.spare.p;
+    gather_group<1>(c, c.accum.p, tmp, perm, N);
+    cudaMemcpyAsync(c.accum.p, tmp, size_t(N) * 4, cudaMemcpyDeviceToDevice, c.stream);
+    gather_group<1>(c, c.vcount.p, tmp, perm, N);
+    cudaMemcpyAsync(c.vcount.p, tmp, size_t(N) * 4, cudaMemcpyDeviceToDevice, c.stream);
     // sampling rates follow their rows
     if (c.nu_valid) {
-        gather_group<1>(c, c.nu_hat.p, tmp.p, perm, N);
-        cudaMemcpyAsync(c.nu_hat.p, tmp.p, size_t(N) * 4, cudaMemcpyDeviceToDevice, c.stream);
+        gather_group<1>(c, c.nu_hat.p, tmp, perm, N);
+        cudaMemcpyAsync(c.nu_hat.p, tmp, size_t(N) * 4, cudaMemcpyDeviceToDevice, c.stream);
     }
     if (perm_host) cudaMemcpyAsync(perm_host, perm, size_t(N) * 4, cudaMemcpyDeviceToHost, c.stream);
-    const bool ok = cudaStreamSynchronize(c.stream) == cudaSuccess;
-    for (int k = 0; k < 2; ++k) {
-        cudaFree(code[k].p);
-        cudaFree(idx[k].p);
-    }
-    cudaFree(box.p);
-    cudaFree(tmp.p);
-    return ok;
+    return cudaStreamSynchronize(c.stream) == cudaSuccess;
 }
 
 }  // namespace ts

@@ -95,6 +95,9 @@ struct Context {
     size_t ev_cursor = 0;
 
     DevBuf<uint32_t> dens;       // densify scratch
+    DevBuf<float> spare;         // a second 59*N store: densify / Morton write into it and swap it in
+    DevBuf<unsigned long long> mcode[2];  // Morton codes (radix double buffer)
+    DevBuf<uint32_t> midx[2];             // Morton permutation (radix double buffer)
 
     // binning (k_bin.cu): per-chunk tile histograms, tile totals (+ max list length)
     DevBuf<uint32_t> binH, bintot;
@@ -157,6 +160,14 @@ void launch_exclusive_scan(Context& c, const uint32_t* in, const uint32_t* perm,
 
 template <class T>
 bool ensure(Context& c, DevBuf<T>& b, size_t n, bool keep = false);
+
+// ensure with 25% slack when the buffer has to grow (stores that grow step by step, e.g. by
+// densification, reallocate rarely)
+template <class T>
+bool ensure_grow(Context& c, DevBuf<T>& b, size_t n) {
+    if (n <= b.cap && b.p) return true;
+    return ensure(c, b, n + n / 4);
+}
 
 #define TS_LAUNCHED(c) ((c).launches++)
 

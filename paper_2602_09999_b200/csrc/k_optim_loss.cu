@@ -197,15 +197,13 @@ void launch_adam(Context& c, const ts_adam_config& a, int64_t begin, int64_t end
 
 bool launch_sampling_rates(Context& c, const DevCam* cams_host, int ncams, float extent) {
     if (c.N == 0) return true;
-    DevBuf<DevCam> dc;
-    if (!ensure(c, dc, size_t(ncams))) return false;
-    cudaMemcpyAsync(dc.p, cams_host, sizeof(DevCam) * ncams, cudaMemcpyHostToDevice, c.stream);
-    sampling_rate_kernel<<<unsigned((c.N + 255) / 256), 256, 0, c.stream>>>(c.params.p, c.N, dc.p, ncams,
+    if (!ensure_grow(c, c.cams, size_t(ncams))) return false;
+    cudaMemcpyAsync(c.cams.p, cams_host, sizeof(DevCam) * ncams, cudaMemcpyHostToDevice, c.stream);
+    sampling_rate_kernel<<<unsigned((c.N + 255) / 256), 256, 0, c.stream>>>(c.params.p, c.N, c.cams.p, ncams,
                                                                             1.0f / extent, c.nu_hat.p);
     TS_LAUNCHED(c);
-    const bool ok = cudaStreamSynchronize(c.stream) == cudaSuccess;
-    cudaFree(dc.p);
-    return ok;
+    // cams_host is the caller's (pageable) array: the copy has completed when this returns
+    return cudaStreamSynchronize(c.stream) == cudaSuccess;
 }
 
 void launch_filter3d_clip(Context& c, float kappa3d) {

@@ -95,6 +95,7 @@ struct Context {
     size_t ev_cursor = 0;
 
     DevBuf<uint32_t> dens;       // densify scratch
+    DevBuf<DevCam> cams;         // camera set of compute_sampling_rates
     DevBuf<float> spare;         // a second 59*N store: densify / Morton write into it and swap it in
     DevBuf<unsigned long long> mcode[2];  // Morton codes (radix double buffer)
     DevBuf<uint32_t> midx[2];             // Morton permutation (radix double buffer)

@@ -44,7 +44,9 @@ class TrainConfig:
     backward_mode: int = T.BACKWARD_PER_PIXEL
     optimizer_mode: int = T.ADAM_FUSED
     morton: bool = True
-    aa_mode: str = "off"
+    aa_mode: str = "off"          # off | filter3d_original | filter3d_clip | full
+    kappa3d: float = 0.2          # 3D filter variance
+    rate_interval: int = 100      # sampling-rate recompute interval
     truncation: str = "classic"
     dynamic_4d: bool = False
     batch_size: int = 1
@@ -60,8 +62,12 @@ class TrainConfig:
             raise ConfigError("total_iterations >= 0, batch_size >= 1, checkpoint_interval >= 1 required")
         if self.sort_mode not in ("two_stage", "combined"):
             raise ConfigError(f"sort_mode {self.sort_mode!r}")
-        if self.aa_mode != "off" or self.truncation != "classic" or self.dynamic_4d:
-            raise ConfigError("aa_mode/truncation/dynamic_4d: only off/classic/false are on the B200 path")
+        if self.aa_mode not in T.AA_MODES:
+            raise ConfigError(f"aa_mode {self.aa_mode!r}: one of {sorted(T.AA_MODES)} (SPEC.md:675)")
+        if not self.kappa3d > 0 or self.rate_interval < 1:
+            raise ConfigError("kappa3d > 0 and rate_interval >= 1 required")
+        if self.truncation != "classic" or self.dynamic_4d:
+            raise ConfigError("truncation/dynamic_4d: only classic/false are on the B200 path")
         if self.optimizer_mode not in range(5):
             raise ConfigError(f"optimizer_mode {self.optimizer_mode}")
         self.densify.validate(self.total_iterations)

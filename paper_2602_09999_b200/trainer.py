@@ -2,7 +2,10 @@
 view sampling, render -> loss -> backward -> optimizer step,
 then the scheduled densify / opacity reset / Morton / SH-ramp events
 (config.events) and a checkpoint every `checkpoint_interval` iterations
-(SPEC.md:832, :855).  Resuming from a checkpoint continues the same schedule
+(SPEC.md:832, :855).  With antialiasing on the sampling rates
+are recomputed every `rate_interval` iterations and after every densification
+(new rows), and the clip modes (filter3d_clip, full) apply the 3D-filter clip
+after each optimizer step.  Resuming from a checkpoint continues the same schedule
 and view order, because both are pure functions of (seed, iteration).
 
 `engine` is the C-ABI Engine (tilesplat.Engine); the tests also drive this
@@ -38,7 +41,10 @@ class Trainer:
             from .scene import scene_extent
             extent = scene_extent(self.cams)
         self.extent = float(extent)
-        self.rcfg = render_cfg or T.RenderConfig.make(bound_mode=cfg.bound_mode, cull_mode=cfg.cull_mode)
+        self.rcfg = render_cfg or T.RenderConfig.make(bound_mode=cfg.bound_mode, cull_mode=cfg.cull_mode,
+                                                      aa=cfg.aa_mode, kappa3d=cfg.kappa3d)
+        self.aa = T.AA_MODES[cfg.aa_mode]
+        self._rates_stale = True
         self.n_views = len(self.cams)
         self._slots = hasattr(engine, "set_target")
         self.targets = targets
@@ -68,6 +74,9 @@ class Trainer:
         rc = self.rcfg
         rc.sh_degree = ev.sh_degree
         views = self.views_for(it)
+        if self.aa != T.AA_OFF and (self._rates_stale or (it - 1) % self.cfg.rate_interval == 0):
+            self.e.compute_sampling_rates(self.cams, self.extent)
+            self._rates_stale = False
         if len(views) == 1 and hasattr(self.e, "train_step"):
             v = views[0]
             loss = (self.e.train_step(self.cams[v], rc, self.adam(it), slot=v) if self._slots
@@ -80,10 +89,13 @@ class Trainer:
                 self.e.backward()
             self.e.adam_step(self.adam(it))
         self.log.losses.append(loss)
+        if self.aa in (T.AA_FILTER3D_CLIP, T.AA_FULL):  # post-step projection
+            self.e.apply_3d_filter_clip(self.cfg.kappa3d)
         if ev.densify:
             s = self.cfg.densify
             n, (c, sp, pr) = self.e.densify_and_prune(s.grad_threshold, self.extent, self.cfg.seed, it)
             self.log.densify.append((it, c, sp, pr, n))
+            self._rates_stale = True  # new rows have no sampling rate yet
         if ev.opacity_reset:
             self.e.opacity_reset()
             self.log.resets.append(it)

@@ -219,3 +219,40 @@ def test_engine_checkpoint_and_trainer_gpu(tmp_path, engine):
     assert np.array_equal(before[0], after[0])
     for x, y in zip(before[1][1:], after[1][1:]):
         assert np.array_equal(x, y)
+
+
+def test_train_config_antialias_modes():
+    for m in ("off", "filter3d_original", "filter3d_clip", "full"):
+        TrainConfig(aa_mode=m).validate()
+    with pytest.raises(ConfigError):
+        TrainConfig(aa_mode="mip").validate()
+    with pytest.raises(ConfigError):
+        TrainConfig(aa_mode="full", kappa3d=0.0).validate()
+    c = TrainConfig(aa_mode="full").override(["rate_interval=50"])
+    assert c.aa_mode == "full" and c.rate_interval == 50
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("aa", ["filter3d_original", "full"])
+def test_trainer_antialias_gpu(engine, aa):
+    """Training with antialiasing: sampling rates refreshed on the schedule
+    and after densification, the clip applied after every optimizer step ("full"); the loss
+    falls and, for the clip modes, every scale ends at or above sqrt(kappa)/nu."""
+    from paper_2602_09999_b200.trainer import Trainer
+
+    p, n, cams = _toy(4000, 6, 96)
+    rc = T.RenderConfig.make(sh_degree=3)
+    engine.set_params(scene.perturb(p, n, 9), n)
+    targets = [engine.render(c, rc)[0] for c in cams]
+    engine.set_params(p, n)
+    sched = DensifySchedule(warmup=10, interval=10, end=30, opacity_reset_interval=1000, morton_interval=1000)
+    cfg = TrainConfig(total_iterations=40, seed=2, densify=sched, aa_mode=aa, rate_interval=15)
+    log = Trainer(engine, cams, targets, cfg).run()
+    assert len(log.densify) == 3 and all(np.isfinite(log.losses))
+    assert np.mean(log.losses[-6:]) < np.mean(log.losses[:6])
+    if aa == "full":
+        nu = engine.get_sampling_rates()
+        N = engine.num_gaussians()
+        s = np.exp(engine.get_params()[3 * N:6 * N].reshape(N, 3).astype(np.float64))
+        floor = np.sqrt(cfg.kappa3d) / nu.astype(np.float64)
+        assert np.all(s >= floor[:, None] * (1 - 1e-5))

@@ -253,6 +253,8 @@ def run_ours(args):
     # auto = the faster single-GPU mode as measured (profiles/): the separate float4 Adam sweep runs at the
     # HBM roof while the fused kernel is occupancy-bound, so auto picks "fused"
     fused_bwd = args.adam_mode == "fused_backward"
+    if args.densify and world > 1:
+        raise SystemExit("--densify runs on one GPU (the multi-GPU path needs the statistics all-reduce)")
     if fused_bwd and world > 1:
         raise SystemExit("fused_backward needs the full gradient on one rank (world size 1)")
     mode = T.ADAM_FUSED_BACKWARD if fused_bwd else T.ADAM_FUSED
@@ -263,12 +265,18 @@ def run_ours(args):
         return T.AdamConfig.make(step=step, extent=1.0, mode=mode if m is None else m,
                                  zero_grads=0 if args.dp_mode == "allreduce" else 1)
 
+    densify_log = []
+
     def train_step():
         j = view_of(step)
         if world == 1:  # one public C-ABI call: forward, loss, backward, Adam (target slot on the device)
             e.train_step(cams[j], cfg, adam_cfg(), slot=j, want_loss=False)
         else:
             dp.step([(cams[j], cfg, j)], adam_cfg())
+        if args.densify and step % 100 == 0:
+            # densify / prune on the SPEC interval (every 100 iterations), as in
+            # config 3's densification phase; counted in the timed region
+            densify_log.append((step,) + e.densify_and_prune(2e-4, 1.0, w.seed, step))
 
     for _ in range(args.warmup):
         step += 1
@@ -423,6 +431,8 @@ def run_ours(args):
                         "algorithmic_bytes": int(R), "achieved_gbs": R / (fwd_bwd_ms * 1e-3) / 1e9,
                         "roofline_frac": R / (fwd_bwd_ms * 1e-3) / 1e9 / peak},
             "stage_ms": {k: round(v, 4) for k, v in avg.items()},
+            "densify": [{"step": d[0], "n_after": d[1], "clones": d[2][0], "splits": d[2][1], "pruned": d[2][2]}
+                        for d in densify_log] if args.densify else None,
             "stage_calls": calls,
             "view": vstats,
             "clocks": {k: clocks[k] for k in ("sm_mhz", "sm_max_mhz", "reasons")},
@@ -449,6 +459,8 @@ def main():
                     help="optimizer mode (SPEC.md:525): fused = separate fused-Adam sweep (SPEC.md:473-480); "
                          "fused_backward = Adam inside the backward (SPEC.md:492-500, 1 GPU only)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--densify", action="store_true",
+                    help="densify_and_prune every 100 iterations inside the timed region (config 3, N=1)")
     ap.add_argument("--no-morton", action="store_true",
                     help="keep the generator's random Gaussian order instead of the z-order training state")
     args = ap.parse_args()

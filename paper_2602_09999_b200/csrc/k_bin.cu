@@ -166,7 +166,10 @@ __global__ void __launch_bounds__(kBinThreads, 3) bin_scatter_kernel(const uint4
 // ---------------------------------------------------------------------------
 // shared layout: bucketed keys/indices (CAP each) + bucket counters (CAP/2 + 1);
 // the list itself stays in registers (CAP / NT per thread)
-constexpr size_t tile_sort_smem(int cap) { return size_t(cap) * 8 + (size_t(cap) / 2 + 1) * 4; }
+#ifndef TS_SORT_BDIV
+#define TS_SORT_BDIV 1  // list elements per bucket (on average): fewer rank comparisons
+#endif
+constexpr size_t tile_sort_smem(int cap) { return size_t(cap) * 8 + (size_t(cap) / TS_SORT_BDIV + 1) * 4; }
 
 template <int CAP, int NT>
 __global__ void __launch_bounds__(NT) tile_sort_kernel(const uint32_t* __restrict__ starts,
@@ -174,7 +177,7 @@ __global__ void __launch_bounds__(NT) tile_sort_kernel(const uint32_t* __restric
                                                        const uint32_t* __restrict__ dkey, uint32_t* __restrict__ out,
                                                        const uint32_t* __restrict__ tiles) {
     constexpr int R = CAP / NT;
-    constexpr int NB = CAP / 2;  // bucket counters (buckets = L/2)
+    constexpr int NB = CAP / TS_SORT_BDIV;  // bucket counters (buckets = L / TS_SORT_BDIV)
     extern __shared__ uint32_t sm[];
     uint32_t* skey = sm;
     uint32_t* sgid = sm + CAP;
@@ -189,7 +192,7 @@ __global__ void __launch_bounds__(NT) tile_sort_kernel(const uint32_t* __restric
         s_min = 0xFFFFFFFFu;
         s_max = 0u;
     }
-    const int nbk = max(1, min(NB, L / 2));
+    const int nbk = max(1, min(NB, L / TS_SORT_BDIV));
     for (int i = tid; i <= nbk; i += NT) cnt[i] = 0;
     uint32_t gg[R], kk[R];
 #pragma unroll

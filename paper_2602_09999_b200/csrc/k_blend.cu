@@ -40,7 +40,15 @@ __device__ __forceinline__ float ellipse_ry(float A, float B, float C, float k2)
 __device__ __forceinline__ int tile_row0(int tid) { return (tid >> 5) * 8 + ((tid >> 4) & 1) * 4; }
 
 template <bool kCompat>
-__global__ void __launch_bounds__(kT) blend_fwd_kernel(const uint32_t* __restrict__ starts,
+// an explicit minimum of 1 resident CTA lets ptxas spend registers (64 / 90) instead of
+// rematerialising for occupancy: measured 2% (K6) and 1% (K8) faster than the default
+#ifndef TS_FWD_MINB
+#define TS_FWD_MINB 1
+#endif
+#ifndef TS_BWD_MINB
+#define TS_BWD_MINB 1
+#endif
+__global__ void __launch_bounds__(kT, TS_FWD_MINB) blend_fwd_kernel(const uint32_t* __restrict__ starts,
                                                       const uint32_t* __restrict__ ival,
                                                       const float4* __restrict__ splat, DevCam cam,
                                                       ts_render_config cfg, float* __restrict__ rgb,
@@ -252,7 +260,7 @@ __device__ __forceinline__ float rcp_approx(float x) {
     return y;
 }
 
-__global__ void __launch_bounds__(kT) blend_bwd_kernel(const uint32_t* __restrict__ starts,
+__global__ void __launch_bounds__(kT, TS_BWD_MINB) blend_bwd_kernel(const uint32_t* __restrict__ starts,
                                                       const uint32_t* __restrict__ ival,
                                                       const float4* __restrict__ splat, DevCam cam,
                                                       const float* __restrict__ rgb, const uint32_t* __restrict__ pcount,

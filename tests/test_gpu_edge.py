@@ -120,3 +120,21 @@ def test_tile_list_over_sort_capacity(engine):
     assert np.array_equal(gk, ok) and np.array_equal(gv, ov) and np.array_equal(gr, orr)
     orgb, oT, _, _ = O.render(p, n, cam, cfg)
     assert np.abs(rgb - orgb).max() <= IMG_TOL and np.abs(Tf - oT).max() <= IMG_TOL
+
+
+def test_frame_beyond_bucketed_binning_uses_radix(engine):
+    """More than 51200 tiles (the bucketed scatter keeps one cursor per tile in shared
+    memory): the radix binning path runs and still matches the oracle bit for bit."""
+    n = 3000
+    p = scene.random_params(n, 0.03, 0.0, 51)
+    cam = scene.make_camera(16 * 257, 16 * 205)  # 52685 tiles
+    cfg = T.RenderConfig.make(sh_degree=0)
+    engine.set_params(p, n)
+    engine.set_binning(0)
+    rgb, Tf, cnt = engine.render(cam, cfg)
+    assert engine.binning_path() == "radix"
+    gk, gv, gr = engine.debug_instances()
+    ok, ov, orr, _ = O.instances(p, n, cam, cfg, sort="combined")
+    assert np.array_equal(gk, ok) and np.array_equal(gv, ov) and np.array_equal(gr, orr)
+    orgb, _, ocnt, _ = O.render(p, n, cam, cfg)
+    assert np.abs(rgb - orgb).max() <= IMG_TOL and np.array_equal(cnt, ocnt)

@@ -158,9 +158,10 @@ ts_status ts_set_state(ts_ctx* ctx, const float* grads, const float* m, const fl
                        const float* vcount); /* each may be NULL */
 ts_status ts_get_state(ts_ctx* ctx, float* grads, float* m, float* v, float* accum, float* vcount);
 
-/* ---- binning path: 0 auto = bucketed binning + per-tile sort, falling back to
- * the two-stage radix sort (depth sort over N, tile sort over I) when a tile list exceeds the
- * per-tile sort capacity; 1 = always the radix path.  Both give bit-identical tile lists. ---- */
+/* ---- binning path: 0 auto = bucketed binning + per-tile sort (lists up to
+ * 65536 instances, frames up to 51200 tiles), falling back to the two-stage radix sort (depth
+ * sort over N, tile sort over I) beyond that; 1 = always the radix path.  Both give
+ * bit-identical tile lists. ---- */
 ts_status ts_set_binning(ts_ctx* ctx, int32_t mode);
 ts_status ts_binning_path(ts_ctx* ctx, int32_t* radix /* 1 if the last forward used the radix path */);
 

@@ -31,7 +31,6 @@
 namespace ts {
 namespace {
 
-constexpr int kChunk = kBinChunk;  // largest chunk (= kBinThreads * kPre); bin_chunk_for picks the size
 constexpr int kBinThreads = 512;  // threads of the chunk kernels
 constexpr int kPre = 16;         // rects per thread, all loaded before the expansion
 
@@ -101,13 +100,16 @@ __device__ __forceinline__ void warp_expand(const uint4 rc, uint32_t g, bool val
     for (int t = -1; (t = big_rect_next(splat, g, tx0, tx1, ty0, ty1, W, H, tiles_x, cull_mode, t)) >= 0;) f(t, g);
 }
 
-// per-tile sort size classes: list lengths in [2, kCap0], (kCap0, kCap1], (kCap1, kCap2];
+// per-tile sort size classes: list lengths in [2, kCap0], (kCap0, kCap1], (kCap1, kCapM], (kCapM, kCap2],
+// (kCap2, kCap3], and (kCap3, kCapL] (segmented sort + merges, class 6);
 // lists of one instance are copied; longer lists send the view to the radix path
 constexpr int kCap0 = 1024, kCap1 = 4096, kCapM = 6144, kCap2 = 8192, kCap3 = 16384;
+// longer lists (up to kCapL): four kCap3 segments sorted in place, then two merge levels
+constexpr int kCapL = 4 * kCap3;
 
 // per tile: exclusive prefix over chunks (in place), total, running max, and the
 // tile appended to the work list of its sort size class (meta[0..4] = class counts,
-// meta[6] = max length; lists at cls + c * Tn)
+// meta[7] = max length; lists at cls + c * Tn)
 __global__ void __launch_bounds__(64) bin_colscan_kernel(uint32_t* __restrict__ Hm, int nchunks, int Tn,
                                                          uint32_t* __restrict__ tot, uint32_t* __restrict__ meta,
                                                          uint32_t* __restrict__ cls) {
@@ -128,11 +130,11 @@ __global__ void __launch_bounds__(64) bin_colscan_kernel(uint32_t* __restrict__ 
         }
         tot[t] = run;
         const int k = run == 1 ? 0 : run <= uint32_t(kCap0) ? 1 : run <= uint32_t(kCap1) ? 2 : run <= uint32_t(kCapM) ? 5
-                    : run <= uint32_t(kCap2) ? 3 : 4;
-        if (run > 0 && run <= uint32_t(kCap3)) cls[size_t(k) * Tn + atomicAdd(&meta[k], 1u)] = uint32_t(t);
+                    : run <= uint32_t(kCap2) ? 3 : run <= uint32_t(kCap3) ? 4 : 6;
+        if (run > 0 && run <= uint32_t(kCapL)) cls[size_t(k) * Tn + atomicAdd(&meta[k], 1u)] = uint32_t(t);
     }
     const uint32_t wm = __reduce_max_sync(0xffffffffu, run);
-    if ((threadIdx.x & 31) == 0 && wm) atomicMax(&meta[6], wm);
+    if ((threadIdx.x & 31) == 0 && wm) atomicMax(&meta[7], wm);
 }
 
 __global__ void __launch_bounds__(kBinThreads, 3) bin_scatter_kernel(const uint4* __restrict__ rect,
@@ -171,7 +173,9 @@ __global__ void __launch_bounds__(kBinThreads, 3) bin_scatter_kernel(const uint4
 #endif
 constexpr size_t tile_sort_smem(int cap) { return size_t(cap) * 8 + (size_t(cap) / TS_SORT_BDIV + 1) * 4; }
 
-template <int CAP, int NT>
+// SEG: CTA blockIdx.x sorts segment (blockIdx.x & 3) of length <= CAP of long tile
+// tiles[blockIdx.x >> 2], in place (every element is loaded before any is written)
+template <int CAP, int NT, bool SEG = false>
 __global__ void __launch_bounds__(NT) tile_sort_kernel(const uint32_t* __restrict__ starts,
                                                        const uint32_t* __restrict__ in,
                                                        const uint32_t* __restrict__ dkey, uint32_t* __restrict__ out,
@@ -184,9 +188,11 @@ __global__ void __launch_bounds__(NT) tile_sort_kernel(const uint32_t* __restric
     uint32_t* cnt = sm + 2 * CAP;
     __shared__ uint32_t s_min, s_max;
     __shared__ uint32_t s_wsum[32];
-    const uint32_t t = tiles[blockIdx.x];
-    const uint32_t b = starts[t];
-    const int L = int(starts[t + 1] - b);
+    const uint32_t t = tiles[SEG ? blockIdx.x >> 2 : blockIdx.x];
+    const int seg = SEG ? int(blockIdx.x & 3) : 0;
+    const uint32_t b = starts[t] + uint32_t(seg * CAP);
+    const int L = SEG ? min(CAP, int(starts[t + 1] - starts[t]) - seg * CAP) : int(starts[t + 1] - b);
+    if (SEG && L <= 0) return;
     const int tid = threadIdx.x;
     if (tid == 0) {
         s_min = 0xFFFFFFFFu;
@@ -294,6 +300,46 @@ __global__ void __launch_bounds__(NT) tile_sort_kernel(const uint32_t* __restric
     }
 }
 
+// Merge level of a long tile list: sorted runs of length RL pair up into runs of 2 RL
+// (run 2p with run 2p + 1; an absent partner is an empty run), src -> dst at the same
+// offsets.  Merge path: each thread finds how many of its first output's predecessors come
+// from the left run by a binary search on (depth key, index), then emits 4 outputs.
+constexpr int kMergeT = 256, kMergePer = 4;
+__device__ __forceinline__ bool key_less(uint32_t a, uint32_t b, const uint32_t* __restrict__ dkey) {
+    const uint32_t ka = __ldg(dkey + a), kb = __ldg(dkey + b);
+    return ka < kb || (ka == kb && a < b);
+}
+
+__global__ void __launch_bounds__(kMergeT) merge_level_kernel(const uint32_t* __restrict__ starts,
+                                                             const uint32_t* __restrict__ tiles,
+                                                             const uint32_t* __restrict__ src,
+                                                             uint32_t* __restrict__ dst,
+                                                             const uint32_t* __restrict__ dkey, int RL) {
+    const uint32_t t = tiles[blockIdx.y];
+    const uint32_t b = starts[t];
+    const int Ltot = int(starts[t + 1] - b);
+    const int o0 = (blockIdx.x * kMergeT + threadIdx.x) * kMergePer;
+    if (o0 >= Ltot) return;
+    const int pbase = (o0 / (2 * RL)) * (2 * RL);
+    const uint32_t* A = src + b + pbase;
+    const uint32_t* B = A + RL;
+    const int nA = min(RL, Ltot - pbase), nB = max(0, min(RL, Ltot - pbase - RL));
+    const int o = o0 - pbase;
+    int lo = max(0, o - nB), hi = min(o, nA);
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (key_less(A[mid], B[o - 1 - mid], dkey)) lo = mid + 1;
+        else hi = mid;
+    }
+    int i = lo, j = o - lo;
+#pragma unroll
+    for (int k = 0; k < kMergePer; ++k) {
+        if (o + k >= nA + nB) break;
+        const bool fromA = j >= nB || (i < nA && key_less(A[i], B[j], dkey));
+        dst[b + pbase + o + k] = fromA ? A[i++] : B[j++];
+    }
+}
+
 // lists of one instance need no sort: copy
 __global__ void tile_copy_single_kernel(const uint32_t* __restrict__ starts, const uint32_t* __restrict__ in,
                                         uint32_t* __restrict__ out, const uint32_t* __restrict__ tiles, int n) {
@@ -305,7 +351,7 @@ __global__ void tile_copy_single_kernel(const uint32_t* __restrict__ starts, con
 
 }  // namespace
 
-int bin_sort_cap() { return kCap3; }
+int bin_sort_cap() { return kCapL; }
 
 bool bin_supported(int Tn) { return size_t(Tn) * 4 <= 200 * 1024; }
 
@@ -313,8 +359,8 @@ int64_t launch_bin_count(Context& c, const DevCam& cam, const ts_render_config& 
     const int Tn = cam.tiles_x * cam.tiles_y;
     const int chunk = bin_chunk_for(c.N, c.sm_count);
     const int nch = int(std::max<int64_t>(1, (c.N + chunk - 1) / chunk));
-    // bintot: [0, Tn) totals | meta (8) | class lists 6 * Tn
-    if (!ensure(c, c.binH, size_t(nch) * Tn) || !ensure(c, c.bintot, size_t(Tn) * 7 + 8)) return -1;
+    // bintot: [0, Tn) totals | meta (8: class counts 0..6, max length) | class lists 7 * Tn
+    if (!ensure(c, c.binH, size_t(nch) * Tn) || !ensure(c, c.bintot, size_t(Tn) * 8 + 8)) return -1;
     const size_t sm = size_t(Tn) * 4;
     static bool attr = false;
     if (!attr) {
@@ -333,12 +379,12 @@ int64_t launch_bin_count(Context& c, const DevCam& cam, const ts_render_config& 
         cudaMemsetAsync(c.bintot.p, 0, size_t(Tn) * 4, c.stream);
     }
     launch_exclusive_scan(c, c.bintot.p, nullptr, c.starts.p, Tn);
-    uint32_t hv[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    uint32_t hv[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
     cudaMemcpyAsync(&hv[0], c.starts.p + Tn, 4, cudaMemcpyDeviceToHost, c.stream);
-    cudaMemcpyAsync(&hv[1], meta, 7 * 4, cudaMemcpyDeviceToHost, c.stream);
+    cudaMemcpyAsync(&hv[1], meta, 8 * 4, cudaMemcpyDeviceToHost, c.stream);
     cudaStreamSynchronize(c.stream);
-    for (int k = 0; k < 6; ++k) c.bin_class[k] = hv[1 + k];
-    *max_len = hv[7];
+    for (int k = 0; k < 7; ++k) c.bin_class[k] = hv[1 + k];
+    *max_len = hv[8];
     return int64_t(hv[0]);
 }
 
@@ -353,17 +399,18 @@ void launch_bin_scatter(Context& c, const DevCam& cam, const ts_render_config& c
     TS_LAUNCHED(c);
 }
 
-template <int CAP, int NT>
+template <int CAP, int NT, bool SEG = false>
 static void sort_variant(Context& c, const uint32_t* tiles, uint32_t n, cudaStream_t st) {
     if (!n) return;
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(tile_sort_kernel<CAP, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaFuncSetAttribute(tile_sort_kernel<CAP, NT, SEG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              int(tile_sort_smem(CAP)));
         attr = true;
     }
-    tile_sort_kernel<CAP, NT><<<n, NT, tile_sort_smem(CAP), st>>>(c.starts.p, c.ival[1].p, c.dkey[0].p,
-                                                                  c.ival[0].p, tiles);
+    // segments sort in place in the scatter output; whole lists go to the final list buffer
+    tile_sort_kernel<CAP, NT, SEG><<<SEG ? 4 * n : n, NT, tile_sort_smem(CAP), st>>>(
+        c.starts.p, c.ival[1].p, c.dkey[0].p, SEG ? c.ival[1].p : c.ival[0].p, tiles);
     TS_LAUNCHED(c);
 }
 
@@ -389,6 +436,17 @@ void launch_tile_depth_sort(Context& c, int Tn, uint32_t max_len) {
     cudaStreamWaitEvent(c.side[0], c.fork_ev, 0);
     cudaStreamWaitEvent(c.side[1], c.fork_ev, 0);
     sort_variant<kCap2, 512>(c, cls + size_t(3) * Tn, c.bin_class[3], c.side[0]);
+    if (c.bin_class[6]) {  // lists longer than kCap3: 4 sorted segments, then 2 merge levels
+        const uint32_t* lt = cls + size_t(6) * Tn;
+        sort_variant<kCap3, 1024, true>(c, lt, c.bin_class[6], c.side[0]);
+        if (ensure_grow(c, c.sortmp, size_t(c.I))) {
+            const dim3 g(kCapL / (kMergeT * kMergePer), c.bin_class[6]);
+            merge_level_kernel<<<g, kMergeT, 0, c.side[0]>>>(c.starts.p, lt, c.ival[1].p, c.sortmp.p, c.dkey[0].p, kCap3);
+            merge_level_kernel<<<g, kMergeT, 0, c.side[0]>>>(c.starts.p, lt, c.sortmp.p, c.ival[0].p, c.dkey[0].p,
+                                                            2 * kCap3);
+            c.launches += 2;
+        }
+    }
     sort_variant<kCap3, 1024>(c, cls + size_t(4) * Tn, c.bin_class[4], c.side[1]);
     sort_variant<kCapM, 512>(c, cls + size_t(5) * Tn, c.bin_class[5], c.side[1]);
     sort_variant<kCap1, 512>(c, cls + size_t(2) * Tn, c.bin_class[2], c.stream);

@@ -104,7 +104,8 @@ struct Context {
     DevBuf<uint32_t> binH, bintot;
     DevBuf<float> nu_hat;        // sampling rates (antialias), N floats
     bool nu_valid = false;       // computed for the current ParameterStore rows
-    uint32_t bin_class[6] = {0, 0, 0, 0, 0, 0};  // tiles per per-tile sort size class (last view)
+    uint32_t bin_class[7] = {0, 0, 0, 0, 0, 0, 0};  // tiles per per-tile sort size class (last view)
+    DevBuf<uint32_t> sortmp;     // merge scratch of the long-list class (I entries)
     cudaStream_t side[2] = {nullptr, nullptr};  // fork streams for independent launches
     cudaEvent_t fork_ev = nullptr, join_ev[2] = {nullptr, nullptr};
     // ts_train_step's host-target upload, overlapped with the forward

@@ -103,20 +103,21 @@ def test_frame_below_ssim_window_rejected(engine):
         engine.render(scene.make_camera(5, 9), T.RenderConfig.make(sh_degree=0))
 
 
-def test_tile_list_over_sort_capacity(engine):
-    """~40k large splats over a 4x4-tile frame: every tile list exceeds the largest
-    per-tile sort class, so the auto path must fall back to the radix sort."""
-    n = 40_000
+@pytest.mark.parametrize("n,path", [(40_000, "bucket"), (160_000, "radix")])
+def test_tile_lists_over_one_sort_block(engine, n, path):
+    """Large splats over a 4x4-tile frame: every tile list exceeds one per-tile sort block
+    (16384).  Up to 4 blocks the bucketed path sorts 4 segments in place and merges them
+    (two merge-path levels); beyond that the view takes the radix path.  Bit-exact."""
     p = scene.random_params(n, 0.25, -3.0, 41)
     cam = scene.make_camera(64, 64)
     cfg = T.RenderConfig.make(sh_degree=0)
     engine.set_params(p, n)
     engine.set_binning(0)
     rgb, Tf, cnt = engine.render(cam, cfg)
-    assert engine.binning_path() == "radix"
+    assert engine.binning_path() == path
     gk, gv, gr = engine.debug_instances()
     ok, ov, orr, _ = O.instances(p, n, cam, cfg, sort="combined")
-    assert np.diff(orr.reshape(-1, 2), axis=1).max() > 16384
+    assert np.diff(orr.reshape(-1, 2), axis=1).max() > (16384 if path == "bucket" else 65536)
     assert np.array_equal(gk, ok) and np.array_equal(gv, ov) and np.array_equal(gr, orr)
     orgb, oT, _, _ = O.render(p, n, cam, cfg)
     assert np.abs(rgb - orgb).max() <= IMG_TOL and np.abs(Tf - oT).max() <= IMG_TOL

@@ -439,13 +439,12 @@ void launch_tile_depth_sort(Context& c, int Tn, uint32_t max_len) {
     if (c.bin_class[6]) {  // lists longer than kCap3: 4 sorted segments, then 2 merge levels
         const uint32_t* lt = cls + size_t(6) * Tn;
         sort_variant<kCap3, 1024, true>(c, lt, c.bin_class[6], c.side[0]);
-        if (ensure_grow(c, c.sortmp, size_t(c.I))) {
-            const dim3 g(kCapL / (kMergeT * kMergePer), c.bin_class[6]);
-            merge_level_kernel<<<g, kMergeT, 0, c.side[0]>>>(c.starts.p, lt, c.ival[1].p, c.sortmp.p, c.dkey[0].p, kCap3);
-            merge_level_kernel<<<g, kMergeT, 0, c.side[0]>>>(c.starts.p, lt, c.sortmp.p, c.ival[0].p, c.dkey[0].p,
-                                                            2 * kCap3);
-            c.launches += 2;
-        }
+        // c.sortmp holds >= I entries (run_forward sizes it before the fork)
+        const dim3 g(kCapL / (kMergeT * kMergePer), c.bin_class[6]);
+        merge_level_kernel<<<g, kMergeT, 0, c.side[0]>>>(c.starts.p, lt, c.ival[1].p, c.sortmp.p, c.dkey[0].p, kCap3);
+        merge_level_kernel<<<g, kMergeT, 0, c.side[0]>>>(c.starts.p, lt, c.sortmp.p, c.ival[0].p, c.dkey[0].p,
+                                                        2 * kCap3);
+        c.launches += 2;
     }
     sort_variant<kCap3, 1024>(c, cls + size_t(4) * Tn, c.bin_class[4], c.side[1]);
     sort_variant<kCapM, 512>(c, cls + size_t(5) * Tn, c.bin_class[5], c.side[1]);

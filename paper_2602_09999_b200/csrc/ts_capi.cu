@@ -233,6 +233,7 @@ ts_status run_forward(Context& c, const ts_camera& cam, const ts_render_config& 
             if (!ensure(c, c.tkey[k], capI)) return TS_ERR_OOM;
         }
     }
+    if (!radix && c.bin_class[6] && !ensure_grow(c, c.sortmp, size_t(I))) return TS_ERR_OOM;  // long-list merges
     c.I = I;
     if (radix) {
         stage_begin(c, 3);

@@ -113,28 +113,54 @@ constexpr int kCapL = 4 * kCap3;
 // per tile: exclusive prefix over chunks (in place), total, running max, and the
 // tile appended to the work list of its sort size class (meta[0..4] = class counts,
 // meta[7] = max length; lists at cls + c * Tn)
-__global__ void __launch_bounds__(64) bin_colscan_kernel(uint32_t* __restrict__ Hm, int nchunks, int Tn,
-                                                         uint32_t* __restrict__ tot, uint32_t* __restrict__ meta,
-                                                         uint32_t* __restrict__ cls) {
-    const int t = blockIdx.x * 64 + threadIdx.x;
-    uint32_t run = 0;
+// 64 tiles x kCS chunk segments per CTA: each thread sums its segment of its tile's
+// column, the segment offsets come from shared memory, then each thread rewrites its
+// segment as the exclusive prefix (second read hits L2)
+constexpr int kCS = 4;
+__global__ void __launch_bounds__(64 * kCS) bin_colscan_kernel(uint32_t* __restrict__ Hm, int nchunks, int Tn,
+                                                              uint32_t* __restrict__ tot, uint32_t* __restrict__ meta,
+                                                              uint32_t* __restrict__ cls) {
+    __shared__ uint32_t part[kCS][64];
+    const int lt = threadIdx.x & 63, sg = threadIdx.x >> 6;
+    const int t = blockIdx.x * 64 + lt;
+    const int q = (nchunks + kCS - 1) / kCS;
+    const int c0 = sg * q, c1 = min(nchunks, c0 + q);
+    constexpr int U = 16;
+    uint32_t sum = 0;
     if (t < Tn) {
-        constexpr int U = 32;
-        for (int c0 = 0; c0 < nchunks; c0 += U) {
+        for (int c = c0; c < c1; c += U) {
             uint32_t h[U];
 #pragma unroll
-            for (int u = 0; u < U; ++u) h[u] = c0 + u < nchunks ? Hm[size_t(c0 + u) * Tn + t] : 0u;
+            for (int u = 0; u < U; ++u) h[u] = c + u < c1 ? Hm[size_t(c + u) * Tn + t] : 0u;
+#pragma unroll
+            for (int u = 0; u < U; ++u) sum += h[u];
+        }
+    }
+    part[sg][lt] = sum;
+    __syncthreads();
+    uint32_t run = 0;
+    for (int k = 0; k < sg; ++k) run += part[k][lt];
+    if (t < Tn) {
+        for (int c = c0; c < c1; c += U) {
+            uint32_t h[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) h[u] = c + u < c1 ? Hm[size_t(c + u) * Tn + t] : 0u;
 #pragma unroll
             for (int u = 0; u < U; ++u)
-                if (c0 + u < nchunks) {
-                    Hm[size_t(c0 + u) * Tn + t] = run;
+                if (c + u < c1) {
+                    Hm[size_t(c + u) * Tn + t] = run;
                     run += h[u];
                 }
         }
+    }
+    if (sg != kCS - 1) return;  // the last segment's thread holds the tile total
+    if (t < Tn) {
         tot[t] = run;
         const int k = run == 1 ? 0 : run <= uint32_t(kCap0) ? 1 : run <= uint32_t(kCap1) ? 2 : run <= uint32_t(kCapM) ? 5
                     : run <= uint32_t(kCap2) ? 3 : run <= uint32_t(kCap3) ? 4 : 6;
         if (run > 0 && run <= uint32_t(kCapL)) cls[size_t(k) * Tn + atomicAdd(&meta[k], 1u)] = uint32_t(t);
+    } else {
+        run = 0;
     }
     const uint32_t wm = __reduce_max_sync(0xffffffffu, run);
     if ((threadIdx.x & 31) == 0 && wm) atomicMax(&meta[7], wm);
@@ -376,7 +402,7 @@ int64_t launch_bin_count(Context& c, const DevCam& cam, const ts_render_config& 
     (void)sm;
     if (c.N > 0) {
         // H[chunk][tile] was accumulated by K1 (launch_preprocess)
-        bin_colscan_kernel<<<(Tn + 63) / 64, 64, 0, c.stream>>>(c.binH.p, nch, Tn, c.bintot.p, meta, cls);
+        bin_colscan_kernel<<<(Tn + 63) / 64, 64 * kCS, 0, c.stream>>>(c.binH.p, nch, Tn, c.bintot.p, meta, cls);
         TS_LAUNCHED(c);
     } else {
         cudaMemsetAsync(c.bintot.p, 0, size_t(Tn) * 4, c.stream);

@@ -171,7 +171,7 @@ __global__ void __launch_bounds__(kBinThreads, TS_SC_MINB) bin_scatter_kernel(co
                                                                   int H, int tiles_x, int Tn, int cull_mode,
                                                                   const uint32_t* __restrict__ Hm,
                                                                   const uint32_t* __restrict__ starts,
-                                                                  uint32_t* __restrict__ out, int chunk) {
+                                                                  uint32_t* __restrict__ out, int chunk, uint32_t cap) {
     extern __shared__ uint32_t cur[];
     const uint32_t* row = Hm + size_t(blockIdx.x) * Tn;
     for (int t = threadIdx.x; t < Tn; t += kBinThreads) cur[t] = starts[t] + row[t];
@@ -188,7 +188,10 @@ __global__ void __launch_bounds__(kBinThreads, TS_SC_MINB) bin_scatter_kernel(co
     for (int u = 0; u < npre; ++u) {
         const int64_t g = g0 + threadIdx.x + u * kBinThreads;
         warp_expand(rc[u], uint32_t(g), g < N, splat, W, H, tiles_x, cull_mode,
-                    [&](int t, uint32_t gg) { out[atomicAdd(&cur[t], 1u)] = gg; });
+                    [&](int t, uint32_t gg) {
+                        const uint32_t slot = atomicAdd(&cur[t], 1u);
+                        if (slot < cap) out[slot] = gg;  // launched before I is known: stay in bounds
+                    });
     }
 }
 
@@ -384,22 +387,26 @@ int bin_sort_cap() { return kCapL; }
 
 bool bin_supported(int Tn) { return size_t(Tn) * 4 <= 200 * 1024; }
 
-int64_t launch_bin_count(Context& c, const DevCam& cam, const ts_render_config& cfg, uint32_t* max_len) {
+bool launch_bin_count(Context& c, const DevCam& cam, const ts_render_config& cfg) {
+    (void)cfg;
     const int Tn = cam.tiles_x * cam.tiles_y;
     const int chunk = bin_chunk_for(c.N, c.sm_count);
     const int nch = int(std::max<int64_t>(1, (c.N + chunk - 1) / chunk));
     // bintot: [0, Tn) totals | meta (8: class counts 0..6, max length) | class lists 7 * Tn
-    if (!ensure(c, c.binH, size_t(nch) * Tn) || !ensure(c, c.bintot, size_t(Tn) * 8 + 8)) return -1;
-    const size_t sm = size_t(Tn) * 4;
+    if (!ensure(c, c.binH, size_t(nch) * Tn) || !ensure(c, c.bintot, size_t(Tn) * 8 + 8)) return false;
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(bin_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
         attr = true;
     }
+    if (!c.bin_host) {
+        if (cudaMallocHost(reinterpret_cast<void**>(&c.bin_host), 16 * sizeof(uint32_t)) != cudaSuccess ||
+            cudaEventCreateWithFlags(&c.bin_ev, cudaEventDisableTiming) != cudaSuccess)
+            return false;
+    }
     uint32_t* meta = c.bintot.p + Tn;
     uint32_t* cls = meta + 8;
     cudaMemsetAsync(meta, 0, 8 * 4, c.stream);
-    (void)sm;
     if (c.N > 0) {
         // H[chunk][tile] was accumulated by K1 (launch_preprocess)
         bin_colscan_kernel<<<(Tn + 63) / 64, 64 * kCS, 0, c.stream>>>(c.binH.p, nch, Tn, c.bintot.p, meta, cls);
@@ -408,23 +415,30 @@ int64_t launch_bin_count(Context& c, const DevCam& cam, const ts_render_config& 
         cudaMemsetAsync(c.bintot.p, 0, size_t(Tn) * 4, c.stream);
     }
     launch_exclusive_scan(c, c.bintot.p, nullptr, c.starts.p, Tn);
-    uint32_t hv[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
-    cudaMemcpyAsync(&hv[0], c.starts.p + Tn, 4, cudaMemcpyDeviceToHost, c.stream);
-    cudaMemcpyAsync(&hv[1], meta, 8 * 4, cudaMemcpyDeviceToHost, c.stream);
-    cudaStreamSynchronize(c.stream);
-    for (int k = 0; k < 7; ++k) c.bin_class[k] = hv[1 + k];
-    *max_len = hv[8];
-    return int64_t(hv[0]);
+    // I, the class counts and the longest list to pinned host memory; the host waits on this
+    // event only, so the scatter launched next overlaps the read-back
+    cudaMemcpyAsync(c.bin_host, c.starts.p + Tn, 4, cudaMemcpyDeviceToHost, c.stream);
+    cudaMemcpyAsync(c.bin_host + 1, meta, 8 * 4, cudaMemcpyDeviceToHost, c.stream);
+    cudaEventRecord(c.bin_ev, c.stream);
+    return true;
+}
+
+int64_t finish_bin_count(Context& c, uint32_t* max_len) {
+    if (cudaEventSynchronize(c.bin_ev) != cudaSuccess) return -1;
+    for (int k = 0; k < 7; ++k) c.bin_class[k] = c.bin_host[1 + k];
+    *max_len = c.bin_host[8];
+    return int64_t(c.bin_host[0]);
 }
 
 void launch_bin_scatter(Context& c, const DevCam& cam, const ts_render_config& cfg) {
     const int Tn = cam.tiles_x * cam.tiles_y;
-    if (c.N == 0 || c.I == 0) return;
+    if (c.N == 0) return;  // (may run before this view's I is known on the host)
     const int chunk = bin_chunk_for(c.N, c.sm_count);
     const int nch = int((c.N + chunk - 1) / chunk);
     bin_scatter_kernel<<<nch, kBinThreads, size_t(Tn) * 4, c.stream>>>(c.rect.p, c.splat.p, c.N, cam.w, cam.h,
                                                                        cam.tiles_x, Tn, cfg.cull_mode, c.binH.p,
-                                                                       c.starts.p, c.ival[1].p, chunk);
+                                                                       c.starts.p, c.ival[1].p, chunk,
+                                                                       uint32_t(std::min<size_t>(c.ival[1].cap, 0xFFFFFFFFu)));
     TS_LAUNCHED(c);
 }
 

@@ -203,13 +203,24 @@ ts_status run_forward(Context& c, const ts_camera& cam, const ts_render_config& 
     bool radix = c.binning_mode == 1 || !bin_supported(Tn);
     uint32_t max_len = 0;
     int64_t I = 0;
+    bool scattered = false;
     if (!radix) {
         stage_begin(c, 1);
-        I = launch_bin_count(c, dc, cfg, &max_len);
+        if (!launch_bin_count(c, dc, cfg)) return c.err.empty() ? TS_ERR_OOM : TS_ERR_CUDA;
         stage_end(c, 1);
-        if (I < 0) return c.err.empty() ? TS_ERR_OOM : TS_ERR_CUDA;
+        // the scatter does not need I on the host: launch it into the current list buffer
+        // (bounds-checked) while the host waits for I; relaunched below if the buffer was short
+        if (c.ival[1].p && c.ival[1].cap > 0) {
+            stage_begin(c, 3);
+            launch_bin_scatter(c, dc, cfg);
+            stage_end(c, 3);
+            scattered = true;
+        }
+        I = finish_bin_count(c, &max_len);
+        if (I < 0) return TS_ERR_CUDA;
         if (ts_status s = last_launch(c, "preprocess/bin_count"); s != TS_OK) return s;
         radix = max_len > uint32_t(bin_sort_cap());
+        if (scattered && c.ival[1].cap < size_t(I)) scattered = false;
     }
     if (radix) {
         stage_begin(c, 1);
@@ -246,9 +257,11 @@ ts_status run_forward(Context& c, const ts_camera& cam, const ts_render_config& 
         launch_ranges(c, Tn);
         stage_end(c, 5);
     } else {
-        stage_begin(c, 3);
-        launch_bin_scatter(c, dc, cfg);
-        stage_end(c, 3);
+        if (!scattered) {
+            stage_begin(c, 3);
+            launch_bin_scatter(c, dc, cfg);
+            stage_end(c, 3);
+        }
         stage_begin(c, 4);
         launch_tile_depth_sort(c, Tn, max_len);
         stage_end(c, 4);
@@ -439,6 +452,8 @@ ts_status ts_destroy(ts_ctx* x) {
     }
     if (c.fork_ev) cudaEventDestroy(c.fork_ev);
     if (c.copy_stream) cudaStreamDestroy(c.copy_stream);
+    if (c.bin_host) cudaFreeHost(c.bin_host);
+    if (c.bin_ev) cudaEventDestroy(c.bin_ev);
     if (c.loss_host) cudaFreeHost(c.loss_host);
     if (c.loss_ev) cudaEventDestroy(c.loss_ev);
     if (c.copy_fork) cudaEventDestroy(c.copy_fork);

@@ -102,6 +102,8 @@ struct Context {
 
     // binning (k_bin.cu): per-chunk tile histograms, tile totals (+ max list length)
     DevBuf<uint32_t> binH, bintot;
+    uint32_t* bin_host = nullptr;  // pinned read-back of (I, class counts, longest list)
+    cudaEvent_t bin_ev = nullptr;
     DevBuf<float> nu_hat;        // sampling rates (antialias), N floats
     bool nu_valid = false;       // computed for the current ParameterStore rows
     uint32_t bin_class[7] = {0, 0, 0, 0, 0, 0, 0};  // tiles per per-tile sort size class (last view)
@@ -136,7 +138,10 @@ inline int bin_chunk_for(int64_t N, int sm_count) {
 }
 bool bin_supported(int Tn);
 int bin_sort_cap();
-int64_t launch_bin_count(Context& c, const DevCam& cam, const ts_render_config& cfg, uint32_t* max_len);
+// enqueue the column scan, the tile ranges and the read-back of (I, class counts, longest list)
+bool launch_bin_count(Context& c, const DevCam& cam, const ts_render_config& cfg);
+// wait for that read-back; returns I (-1 on error)
+int64_t finish_bin_count(Context& c, uint32_t* max_len);
 void launch_bin_scatter(Context& c, const DevCam& cam, const ts_render_config& cfg);
 void launch_tile_depth_sort(Context& c, int Tn, uint32_t max_len);
 void launch_blend_fwd(Context& c, const DevCam& cam, const ts_render_config& cfg);

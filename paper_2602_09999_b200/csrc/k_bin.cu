@@ -112,7 +112,7 @@ constexpr int kCapL = 4 * kCap3;
 
 // per tile: exclusive prefix over chunks (in place), total, running max, and the
 // tile appended to the work list of its sort size class (meta[0..4] = class counts,
-// meta[7] = max length; lists at cls + c * Tn)
+// meta[7] = max length, meta[8] = empty tiles (list 7); lists at cls + c * Tn)
 // 64 tiles x kCS chunk segments per CTA: each thread sums its segment of its tile's
 // column, the segment offsets come from shared memory, then each thread rewrites its
 // segment as the exclusive prefix (second read hits L2)
@@ -159,6 +159,7 @@ __global__ void __launch_bounds__(64 * kCS) bin_colscan_kernel(uint32_t* __restr
         const int k = run == 1 ? 0 : run <= uint32_t(kCap0) ? 1 : run <= uint32_t(kCap1) ? 2 : run <= uint32_t(kCapM) ? 5
                     : run <= uint32_t(kCap2) ? 3 : run <= uint32_t(kCap3) ? 4 : 6;
         if (run > 0 && run <= uint32_t(kCapL)) cls[size_t(k) * Tn + atomicAdd(&meta[k], 1u)] = uint32_t(t);
+        if (run == 0) cls[size_t(7) * Tn + atomicAdd(&meta[8], 1u)] = uint32_t(t);  // empty tiles
     } else {
         run = 0;
     }
@@ -372,6 +373,20 @@ __global__ void __launch_bounds__(kMergeT) merge_level_kernel(const uint32_t* __
     }
 }
 
+// Blend order of the tiles: longest lists first (size classes from the largest down, then
+// the empty tiles), so the long-running blend CTAs start in the first wave instead of
+// forming the kernel's tail.  Block k copies class list kOrder[k] to its offset.
+__global__ void tile_order_kernel(const uint32_t* __restrict__ meta, const uint32_t* __restrict__ cls, int Tn,
+                                  uint32_t* __restrict__ order) {
+    const int kOrder[8] = {6, 4, 3, 5, 2, 1, 0, 7};
+    const int cnt_idx[8] = {6, 4, 3, 5, 2, 1, 0, 8};
+    int off = 0;
+    for (int k = 0; k < int(blockIdx.x); ++k) off += int(meta[cnt_idx[k]]);
+    const int n = int(meta[cnt_idx[blockIdx.x]]);
+    const uint32_t* src = cls + size_t(kOrder[blockIdx.x]) * Tn;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) order[off + i] = src[i];
+}
+
 // lists of one instance need no sort: copy
 __global__ void tile_copy_single_kernel(const uint32_t* __restrict__ starts, const uint32_t* __restrict__ in,
                                         uint32_t* __restrict__ out, const uint32_t* __restrict__ tiles, int n) {
@@ -392,8 +407,8 @@ bool launch_bin_count(Context& c, const DevCam& cam, const ts_render_config& cfg
     const int Tn = cam.tiles_x * cam.tiles_y;
     const int chunk = bin_chunk_for(c.N, c.sm_count);
     const int nch = int(std::max<int64_t>(1, (c.N + chunk - 1) / chunk));
-    // bintot: [0, Tn) totals | meta (8: class counts 0..6, max length) | class lists 7 * Tn
-    if (!ensure(c, c.binH, size_t(nch) * Tn) || !ensure(c, c.bintot, size_t(Tn) * 8 + 8)) return false;
+    // bintot: [0, Tn) totals | meta (16: class counts 0..6, max length, empty tiles) | lists 8 * Tn
+    if (!ensure(c, c.binH, size_t(nch) * Tn) || !ensure(c, c.bintot, size_t(Tn) * 9 + 16)) return false;
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(bin_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
@@ -405,8 +420,8 @@ bool launch_bin_count(Context& c, const DevCam& cam, const ts_render_config& cfg
             return false;
     }
     uint32_t* meta = c.bintot.p + Tn;
-    uint32_t* cls = meta + 8;
-    cudaMemsetAsync(meta, 0, 8 * 4, c.stream);
+    uint32_t* cls = meta + 16;
+    cudaMemsetAsync(meta, 0, 16 * 4, c.stream);
     if (c.N > 0) {
         // H[chunk][tile] was accumulated by K1 (launch_preprocess)
         bin_colscan_kernel<<<(Tn + 63) / 64, 64 * kCS, 0, c.stream>>>(c.binH.p, nch, Tn, c.bintot.p, meta, cls);
@@ -418,9 +433,15 @@ bool launch_bin_count(Context& c, const DevCam& cam, const ts_render_config& cfg
     // I, the class counts and the longest list to pinned host memory; the host waits on this
     // event only, so the scatter launched next overlaps the read-back
     cudaMemcpyAsync(c.bin_host, c.starts.p + Tn, 4, cudaMemcpyDeviceToHost, c.stream);
-    cudaMemcpyAsync(c.bin_host + 1, meta, 8 * 4, cudaMemcpyDeviceToHost, c.stream);
+    cudaMemcpyAsync(c.bin_host + 1, meta, 9 * 4, cudaMemcpyDeviceToHost, c.stream);
     cudaEventRecord(c.bin_ev, c.stream);
     return true;
+}
+
+void launch_tile_order(Context& c, int Tn) {
+    if (!ensure(c, c.tile_order, size_t(Tn))) return;
+    tile_order_kernel<<<8, 256, 0, c.stream>>>(c.bintot.p + Tn, c.bintot.p + Tn + 16, Tn, c.tile_order.p);
+    TS_LAUNCHED(c);
 }
 
 int64_t finish_bin_count(Context& c, uint32_t* max_len) {
@@ -460,7 +481,7 @@ static void sort_variant(Context& c, const uint32_t* tiles, uint32_t n, cudaStre
 void launch_tile_depth_sort(Context& c, int Tn, uint32_t max_len) {
     (void)max_len;
     if (c.I == 0) return;
-    const uint32_t* cls = c.bintot.p + Tn + 8;
+    const uint32_t* cls = c.bintot.p + Tn + 16;
     if (c.bin_class[0]) {
         tile_copy_single_kernel<<<(c.bin_class[0] + 255) / 256, 256, 0, c.stream>>>(c.starts.p, c.ival[1].p,
                                                                                   c.ival[0].p, cls, int(c.bin_class[0]));

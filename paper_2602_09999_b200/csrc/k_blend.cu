@@ -53,12 +53,13 @@ __global__ void __launch_bounds__(kT, TS_FWD_MINB) blend_fwd_kernel(const uint32
                                                       const float4* __restrict__ splat, DevCam cam,
                                                       ts_render_config cfg, float* __restrict__ rgb,
                                                       float* __restrict__ Tfin, uint32_t* __restrict__ pcount,
-                                                      uint32_t* __restrict__ ip_counter) {
+                                                      uint32_t* __restrict__ ip_counter,
+                                                      const uint32_t* __restrict__ order) {
     __shared__ float4 sA[kBatch];  // mx, my, k2, o
     __shared__ float4 sB[kBatch];  // A, 2B, C, ry
     __shared__ float4 sC[kBatch];  // r, g, b
     __shared__ uint32_t s_max;
-    const int t = blockIdx.x;
+    const int t = order ? int(order[blockIdx.x]) : int(blockIdx.x);
     const int tx = t % cam.tiles_x, ty = t / cam.tiles_x;
     const int px = tx * 16 + (threadIdx.x & 15);
     const int py0 = ty * 16 + tile_row0(threadIdx.x);
@@ -264,7 +265,8 @@ __global__ void __launch_bounds__(kT, TS_BWD_MINB) blend_bwd_kernel(const uint32
                                                       const uint32_t* __restrict__ ival,
                                                       const float4* __restrict__ splat, DevCam cam,
                                                       const float* __restrict__ rgb, const uint32_t* __restrict__ pcount,
-                                                      const float* __restrict__ dLdC, float4* __restrict__ g2d) {
+                                                      const float* __restrict__ dLdC, float4* __restrict__ g2d,
+                                                      const uint32_t* __restrict__ order) {
     __shared__ float4 sA[kBatch];  // mx, my, k2, o
     __shared__ float4 sB[kBatch];  // A, 2B, C, ry
     __shared__ float4 sC[kBatch];  // r, g, b
@@ -272,7 +274,7 @@ __global__ void __launch_bounds__(kT, TS_BWD_MINB) blend_bwd_kernel(const uint32
     __shared__ __align__(16) float sG[2 * kBatch * kGS];  // per-warp partial gradients
     __shared__ uint32_t s_max;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int t = blockIdx.x;
+    const int t = order ? int(order[blockIdx.x]) : int(blockIdx.x);
     const int tx = t % cam.tiles_x, ty = t / cam.tiles_x;
     const int px = tx * 16 + (threadIdx.x & 15);
     const int py0 = ty * 16 + tile_row0(threadIdx.x);
@@ -438,10 +440,10 @@ void launch_blend_fwd(Context& c, const DevCam& cam, const ts_render_config& cfg
     const int Tn = cam.tiles_x * cam.tiles_y;
     if (cfg.early_stop_compat)
         blend_fwd_kernel<true><<<Tn, kT, 0, c.stream>>>(c.starts.p, c.ival[0].p, c.splat.p, cam, cfg, c.rgb.p,
-                                                        c.Tfin.p, c.pcount.p, c.counters.p + 2);
+                                                        c.Tfin.p, c.pcount.p, c.counters.p + 2, c.order_ok ? c.tile_order.p : nullptr);
     else
         blend_fwd_kernel<false><<<Tn, kT, 0, c.stream>>>(c.starts.p, c.ival[0].p, c.splat.p, cam, cfg, c.rgb.p,
-                                                         c.Tfin.p, c.pcount.p, c.counters.p + 2);
+                                                         c.Tfin.p, c.pcount.p, c.counters.p + 2, c.order_ok ? c.tile_order.p : nullptr);
     TS_LAUNCHED(c);
 }
 
@@ -449,7 +451,7 @@ void launch_blend_bwd(Context& c, const DevCam& cam, const ts_render_config& cfg
     (void)cfg;
     const int Tn = cam.tiles_x * cam.tiles_y;
     blend_bwd_kernel<<<Tn, kT, 0, c.stream>>>(c.starts.p, c.ival[0].p, c.splat.p, cam, c.rgb.p, c.pcount.p,
-                                              c.dLdC.p, c.g2d.p);
+                                              c.dLdC.p, c.g2d.p, c.order_ok ? c.tile_order.p : nullptr);
     TS_LAUNCHED(c);
 }
 

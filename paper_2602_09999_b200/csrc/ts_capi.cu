@@ -265,7 +265,9 @@ ts_status run_forward(Context& c, const ts_camera& cam, const ts_render_config& 
         stage_begin(c, 4);
         launch_tile_depth_sort(c, Tn, max_len);
         stage_end(c, 4);
+        launch_tile_order(c, Tn);
     }
+    c.order_ok = !radix && c.tile_order.p != nullptr;
     stage_begin(c, 6);
     launch_blend_fwd(c, dc, cfg);
     stage_end(c, 6);
@@ -440,7 +442,7 @@ ts_status ts_destroy(ts_ctx* x) {
     release(c.starts), release(c.rhist), release(c.scan_state), release(c.scan_tmp), release(c.counters);
     release(c.rgb), release(c.Tfin), release(c.dLdC), release(c.hwc_stage), release(c.tgt), release(c.pcount);
     release(c.loss_acc), release(c.targets), release(c.dens);
-    release(c.binH), release(c.bintot), release(c.sortmp), release(c.spare), release(c.cams), release(c.mcode[0]), release(c.mcode[1]),
+    release(c.binH), release(c.bintot), release(c.tile_order), release(c.sortmp), release(c.spare), release(c.cams), release(c.mcode[0]), release(c.mcode[1]),
         release(c.midx[0]), release(c.midx[1]), release(c.tgt_stage), release(c.nu_hat);
     for (size_t k = 0; k < c.ev_b.size(); ++k) {
         cudaEventDestroy(c.ev_b[k]);

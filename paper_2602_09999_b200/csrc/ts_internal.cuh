@@ -102,6 +102,8 @@ struct Context {
 
     // binning (k_bin.cu): per-chunk tile histograms, tile totals (+ max list length)
     DevBuf<uint32_t> binH, bintot;
+    DevBuf<uint32_t> tile_order;   // blend order of the tiles (longest lists first)
+    bool order_ok = false;         // tile_order is valid for the current view
     uint32_t* bin_host = nullptr;  // pinned read-back of (I, class counts, longest list)
     cudaEvent_t bin_ev = nullptr;
     DevBuf<float> nu_hat;        // sampling rates (antialias), N floats
@@ -142,6 +144,8 @@ int bin_sort_cap();
 bool launch_bin_count(Context& c, const DevCam& cam, const ts_render_config& cfg);
 // wait for that read-back; returns I (-1 on error)
 int64_t finish_bin_count(Context& c, uint32_t* max_len);
+// build c.tile_order from the size-class lists of the last bin_count (device only)
+void launch_tile_order(Context& c, int Tn);
 void launch_bin_scatter(Context& c, const DevCam& cam, const ts_render_config& cfg);
 void launch_tile_depth_sort(Context& c, int Tn, uint32_t max_len);
 void launch_blend_fwd(Context& c, const DevCam& cam, const ts_render_config& cfg);

@@ -373,18 +373,35 @@ __global__ void __launch_bounds__(kMergeT) merge_level_kernel(const uint32_t* __
     }
 }
 
-// Blend order of the tiles: longest lists first (size classes from the largest down, then
-// the empty tiles), so the long-running blend CTAs start in the first wave instead of
-// forming the kernel's tail.  Block k copies class list kOrder[k] to its offset.
-__global__ void tile_order_kernel(const uint32_t* __restrict__ meta, const uint32_t* __restrict__ cls, int Tn,
-                                  uint32_t* __restrict__ order) {
-    const int kOrder[8] = {6, 4, 3, 5, 2, 1, 0, 7};
-    const int cnt_idx[8] = {6, 4, 3, 5, 2, 1, 0, 8};
-    int off = 0;
-    for (int k = 0; k < int(blockIdx.x); ++k) off += int(meta[cnt_idx[k]]);
-    const int n = int(meta[cnt_idx[blockIdx.x]]);
-    const uint32_t* src = cls + size_t(kOrder[blockIdx.x]) * Tn;
-    for (int i = threadIdx.x; i < n; i += blockDim.x) order[off + i] = src[i];
+// Blend order of the tiles: longest lists first (a one-CTA counting sort of the tiles on
+// min(255, length / 32), descending), so the long-running blend CTAs start in the first
+// wave instead of forming the kernel's tail.  Order inside a bucket is arbitrary.
+__global__ void __launch_bounds__(1024) tile_order_kernel(const uint32_t* __restrict__ tot, int Tn,
+                                                          uint32_t* __restrict__ order) {
+    __shared__ uint32_t hist[256];
+    for (int i = threadIdx.x; i < 256; i += 1024) hist[i] = 0;
+    __syncthreads();
+    for (int t = threadIdx.x; t < Tn; t += 1024) atomicAdd(&hist[255 - min(255u, tot[t] / 32u)], 1u);
+    __syncthreads();
+    if (threadIdx.x < 32) {  // exclusive scan of 256 bins by one warp (8 per lane)
+        uint32_t v[8], sum = 0;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) sum += (v[k] = hist[threadIdx.x * 8 + k]);
+        uint32_t inc = sum;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t u = __shfl_up_sync(0xffffffffu, inc, o);
+            if (int(threadIdx.x) >= o) inc += u;
+        }
+        uint32_t run = inc - sum;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            hist[threadIdx.x * 8 + k] = run;
+            run += v[k];
+        }
+    }
+    __syncthreads();
+    for (int t = threadIdx.x; t < Tn; t += 1024) order[atomicAdd(&hist[255 - min(255u, tot[t] / 32u)], 1u)] = uint32_t(t);
 }
 
 // lists of one instance need no sort: copy
@@ -440,7 +457,7 @@ bool launch_bin_count(Context& c, const DevCam& cam, const ts_render_config& cfg
 
 void launch_tile_order(Context& c, int Tn) {
     if (!ensure(c, c.tile_order, size_t(Tn))) return;
-    tile_order_kernel<<<8, 256, 0, c.stream>>>(c.bintot.p + Tn, c.bintot.p + Tn + 16, Tn, c.tile_order.p);
+    tile_order_kernel<<<1, 1024, 0, c.stream>>>(c.bintot.p, Tn, c.tile_order.p);
     TS_LAUNCHED(c);
 }
 

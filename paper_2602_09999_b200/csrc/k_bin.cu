@@ -374,19 +374,25 @@ __global__ void __launch_bounds__(kMergeT) merge_level_kernel(const uint32_t* __
 }
 
 // Blend order of the tiles: longest lists first (a one-CTA counting sort of the tiles on
-// min(255, length / 32), descending), so the long-running blend CTAs start in the first
-// wave instead of forming the kernel's tail.  Order inside a bucket is arbitrary.
+// length / kOW, descending), so the long-running blend CTAs start in the first
+// wave instead of forming the kernel's tail.  Order inside a bin is arbitrary.
+#ifndef TS_ORDER_W
+#define TS_ORDER_W 32
+#endif
+constexpr int kOW = TS_ORDER_W;             // list-length width of an order bin
+constexpr int kOB = 8192 / TS_ORDER_W;      // bins (longer lists share the last bin)
 __global__ void __launch_bounds__(1024) tile_order_kernel(const uint32_t* __restrict__ tot, int Tn,
                                                           uint32_t* __restrict__ order) {
-    __shared__ uint32_t hist[256];
-    for (int i = threadIdx.x; i < 256; i += 1024) hist[i] = 0;
+    __shared__ uint32_t hist[kOB];
+    for (int i = threadIdx.x; i < kOB; i += 1024) hist[i] = 0;
     __syncthreads();
-    for (int t = threadIdx.x; t < Tn; t += 1024) atomicAdd(&hist[255 - min(255u, tot[t] / 32u)], 1u);
+    for (int t = threadIdx.x; t < Tn; t += 1024) atomicAdd(&hist[kOB - 1 - min(uint32_t(kOB - 1), tot[t] / uint32_t(kOW))], 1u);
     __syncthreads();
-    if (threadIdx.x < 32) {  // exclusive scan of 256 bins by one warp (8 per lane)
-        uint32_t v[8], sum = 0;
+    if (threadIdx.x < 32) {  // exclusive scan of the bins by one warp (kOB / 32 per lane)
+        constexpr int PL = kOB / 32;
+        uint32_t v[PL], sum = 0;
 #pragma unroll
-        for (int k = 0; k < 8; ++k) sum += (v[k] = hist[threadIdx.x * 8 + k]);
+        for (int k = 0; k < PL; ++k) sum += (v[k] = hist[threadIdx.x * PL + k]);
         uint32_t inc = sum;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -395,13 +401,13 @@ __global__ void __launch_bounds__(1024) tile_order_kernel(const uint32_t* __rest
         }
         uint32_t run = inc - sum;
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
-            hist[threadIdx.x * 8 + k] = run;
+        for (int k = 0; k < PL; ++k) {
+            hist[threadIdx.x * PL + k] = run;
             run += v[k];
         }
     }
     __syncthreads();
-    for (int t = threadIdx.x; t < Tn; t += 1024) order[atomicAdd(&hist[255 - min(255u, tot[t] / 32u)], 1u)] = uint32_t(t);
+    for (int t = threadIdx.x; t < Tn; t += 1024) order[atomicAdd(&hist[kOB - 1 - min(uint32_t(kOB - 1), tot[t] / uint32_t(kOW))], 1u)] = uint32_t(t);
 }
 
 // lists of one instance need no sort: copy

@@ -381,12 +381,12 @@ __global__ void __launch_bounds__(kMergeT) merge_level_kernel(const uint32_t* __
 #endif
 constexpr int kOW = TS_ORDER_W;             // list-length width of an order bin
 constexpr int kOB = 8192 / TS_ORDER_W;      // bins (longer lists share the last bin)
-__global__ void __launch_bounds__(1024) tile_order_kernel(const uint32_t* __restrict__ tot, int Tn,
+__global__ void __launch_bounds__(1024) tile_order_kernel(const uint32_t* __restrict__ starts, int Tn,
                                                           uint32_t* __restrict__ order) {
     __shared__ uint32_t hist[kOB];
     for (int i = threadIdx.x; i < kOB; i += 1024) hist[i] = 0;
     __syncthreads();
-    for (int t = threadIdx.x; t < Tn; t += 1024) atomicAdd(&hist[kOB - 1 - min(uint32_t(kOB - 1), tot[t] / uint32_t(kOW))], 1u);
+    for (int t = threadIdx.x; t < Tn; t += 1024) atomicAdd(&hist[kOB - 1 - min(uint32_t(kOB - 1), (starts[t + 1] - starts[t]) / uint32_t(kOW))], 1u);
     __syncthreads();
     if (threadIdx.x < 32) {  // exclusive scan of the bins by one warp (kOB / 32 per lane)
         constexpr int PL = kOB / 32;
@@ -407,7 +407,7 @@ __global__ void __launch_bounds__(1024) tile_order_kernel(const uint32_t* __rest
         }
     }
     __syncthreads();
-    for (int t = threadIdx.x; t < Tn; t += 1024) order[atomicAdd(&hist[kOB - 1 - min(uint32_t(kOB - 1), tot[t] / uint32_t(kOW))], 1u)] = uint32_t(t);
+    for (int t = threadIdx.x; t < Tn; t += 1024) order[atomicAdd(&hist[kOB - 1 - min(uint32_t(kOB - 1), (starts[t + 1] - starts[t]) / uint32_t(kOW))], 1u)] = uint32_t(t);
 }
 
 // lists of one instance need no sort: copy
@@ -463,7 +463,7 @@ bool launch_bin_count(Context& c, const DevCam& cam, const ts_render_config& cfg
 
 void launch_tile_order(Context& c, int Tn) {
     if (!ensure(c, c.tile_order, size_t(Tn))) return;
-    tile_order_kernel<<<1, 1024, 0, c.stream>>>(c.bintot.p, Tn, c.tile_order.p);
+    tile_order_kernel<<<1, 1024, 0, c.stream>>>(c.starts.p, Tn, c.tile_order.p);
     TS_LAUNCHED(c);
 }
 

@@ -256,6 +256,7 @@ ts_status run_forward(Context& c, const ts_camera& cam, const ts_render_config& 
         stage_begin(c, 5);
         launch_ranges(c, Tn);
         stage_end(c, 5);
+        launch_tile_order(c, Tn);
     } else {
         if (!scattered) {
             stage_begin(c, 3);
@@ -267,7 +268,7 @@ ts_status run_forward(Context& c, const ts_camera& cam, const ts_render_config& 
         stage_end(c, 4);
         launch_tile_order(c, Tn);
     }
-    c.order_ok = !radix && c.tile_order.p != nullptr;
+    c.order_ok = c.tile_order.p != nullptr;
     stage_begin(c, 6);
     launch_blend_fwd(c, dc, cfg);
     stage_end(c, 6);

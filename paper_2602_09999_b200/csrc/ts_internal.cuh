@@ -144,7 +144,7 @@ int bin_sort_cap();
 bool launch_bin_count(Context& c, const DevCam& cam, const ts_render_config& cfg);
 // wait for that read-back; returns I (-1 on error)
 int64_t finish_bin_count(Context& c, uint32_t* max_len);
-// build c.tile_order from the size-class lists of the last bin_count (device only)
+// c.tile_order = tiles by descending list length (from the tile ranges; both binning paths)
 void launch_tile_order(Context& c, int Tn);
 void launch_bin_scatter(Context& c, const DevCam& cam, const ts_render_config& cfg);
 void launch_tile_depth_sort(Context& c, int Tn, uint32_t max_len);

@@ -105,21 +105,19 @@ __device__ __forceinline__ void warp_expand(const uint4 rc, uint32_t g, bool val
 
 // per-tile sort size classes: list lengths in [2, kCap0], (kCap0, kCap1], (kCap1, kCapM], (kCapM, kCap2],
 // (kCap2, kCap3], and (kCap3, kCapL] (segmented sort + merges, class 6);
-// lists of one instance are copied; longer lists send the view to the radix path
+// lists of one instance are copied; lists longer than kCapL send the view to the radix path
 constexpr int kCap0 = 1024, kCap1 = 4096, kCapM = 6144, kCap2 = 8192, kCap3 = 16384;
 // longer lists (up to kCapL): four kCap3 segments sorted in place, then two merge levels
 constexpr int kCapL = 4 * kCap3;
 
-// per tile: exclusive prefix over chunks (in place), total, running max, and the
-// tile appended to the work list of its sort size class (meta[0..4] = class counts,
-// meta[7] = max length, meta[8] = empty tiles (list 7); lists at cls + c * Tn)
+// per tile: exclusive prefix over chunks (in place), total, running max, and the count
+// of its sort size class (meta[0..6] = class counts, meta[7] = max length)
 // 64 tiles x kCS chunk segments per CTA: each thread sums its segment of its tile's
 // column, the segment offsets come from shared memory, then each thread rewrites its
 // segment as the exclusive prefix (second read hits L2)
 constexpr int kCS = 4;
 __global__ void __launch_bounds__(64 * kCS) bin_colscan_kernel(uint32_t* __restrict__ Hm, int nchunks, int Tn,
-                                                              uint32_t* __restrict__ tot, uint32_t* __restrict__ meta,
-                                                              uint32_t* __restrict__ cls) {
+                                                              uint32_t* __restrict__ tot, uint32_t* __restrict__ meta) {
     __shared__ uint32_t part[kCS][64];
     const int lt = threadIdx.x & 63, sg = threadIdx.x >> 6;
     const int t = blockIdx.x * 64 + lt;
@@ -158,8 +156,8 @@ __global__ void __launch_bounds__(64 * kCS) bin_colscan_kernel(uint32_t* __restr
         tot[t] = run;
         const int k = run == 1 ? 0 : run <= uint32_t(kCap0) ? 1 : run <= uint32_t(kCap1) ? 2 : run <= uint32_t(kCapM) ? 5
                     : run <= uint32_t(kCap2) ? 3 : run <= uint32_t(kCap3) ? 4 : 6;
-        if (run > 0 && run <= uint32_t(kCapL)) cls[size_t(k) * Tn + atomicAdd(&meta[k], 1u)] = uint32_t(t);
-        if (run == 0) cls[size_t(7) * Tn + atomicAdd(&meta[8], 1u)] = uint32_t(t);  // empty tiles
+        // class counts only: the per-class tile lists are ranges of the tile order (KO)
+        if (run > 0 && run <= uint32_t(kCapL)) atomicAdd(&meta[k], 1u);
     } else {
         run = 0;
     }
@@ -380,13 +378,19 @@ __global__ void __launch_bounds__(kMergeT) merge_level_kernel(const uint32_t* __
 #define TS_ORDER_W 32
 #endif
 constexpr int kOW = TS_ORDER_W;             // list-length width of an order bin
-constexpr int kOB = 8192 / TS_ORDER_W;      // bins (longer lists share the last bin)
+constexpr int kOB = (2 + kCapL / TS_ORDER_W + 31) / 32 * 32;  // bins: empty, single, (L - 1) / kOW
+// ascending key of a list length: 0 empty, 1 single, 2 + (L - 1) / kOW; every size-class
+// boundary is a multiple of kOW, so in descending key order each class is one contiguous range
+__device__ __forceinline__ uint32_t order_key(uint32_t L) {
+    return L == 0 ? 0u : L == 1 ? 1u : 2u + (L - 1u) / uint32_t(kOW);
+}
+
 __global__ void __launch_bounds__(1024) tile_order_kernel(const uint32_t* __restrict__ starts, int Tn,
                                                           uint32_t* __restrict__ order) {
     __shared__ uint32_t hist[kOB];
     for (int i = threadIdx.x; i < kOB; i += 1024) hist[i] = 0;
     __syncthreads();
-    for (int t = threadIdx.x; t < Tn; t += 1024) atomicAdd(&hist[kOB - 1 - min(uint32_t(kOB - 1), (starts[t + 1] - starts[t]) / uint32_t(kOW))], 1u);
+    for (int t = threadIdx.x; t < Tn; t += 1024) atomicAdd(&hist[kOB - 1 - min(uint32_t(kOB - 1), order_key(starts[t + 1] - starts[t]))], 1u);
     __syncthreads();
     if (threadIdx.x < 32) {  // exclusive scan of the bins by one warp (kOB / 32 per lane)
         constexpr int PL = kOB / 32;
@@ -407,7 +411,7 @@ __global__ void __launch_bounds__(1024) tile_order_kernel(const uint32_t* __rest
         }
     }
     __syncthreads();
-    for (int t = threadIdx.x; t < Tn; t += 1024) order[atomicAdd(&hist[kOB - 1 - min(uint32_t(kOB - 1), (starts[t + 1] - starts[t]) / uint32_t(kOW))], 1u)] = uint32_t(t);
+    for (int t = threadIdx.x; t < Tn; t += 1024) order[atomicAdd(&hist[kOB - 1 - min(uint32_t(kOB - 1), order_key(starts[t + 1] - starts[t]))], 1u)] = uint32_t(t);
 }
 
 // lists of one instance need no sort: copy
@@ -430,8 +434,8 @@ bool launch_bin_count(Context& c, const DevCam& cam, const ts_render_config& cfg
     const int Tn = cam.tiles_x * cam.tiles_y;
     const int chunk = bin_chunk_for(c.N, c.sm_count);
     const int nch = int(std::max<int64_t>(1, (c.N + chunk - 1) / chunk));
-    // bintot: [0, Tn) totals | meta (16: class counts 0..6, max length, empty tiles) | lists 8 * Tn
-    if (!ensure(c, c.binH, size_t(nch) * Tn) || !ensure(c, c.bintot, size_t(Tn) * 9 + 16)) return false;
+    // bintot: [0, Tn) totals | meta (16: class counts 0..6, max length)
+    if (!ensure(c, c.binH, size_t(nch) * Tn) || !ensure(c, c.bintot, size_t(Tn) + 16)) return false;
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(bin_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
@@ -443,11 +447,10 @@ bool launch_bin_count(Context& c, const DevCam& cam, const ts_render_config& cfg
             return false;
     }
     uint32_t* meta = c.bintot.p + Tn;
-    uint32_t* cls = meta + 16;
     cudaMemsetAsync(meta, 0, 16 * 4, c.stream);
     if (c.N > 0) {
         // H[chunk][tile] was accumulated by K1 (launch_preprocess)
-        bin_colscan_kernel<<<(Tn + 63) / 64, 64 * kCS, 0, c.stream>>>(c.binH.p, nch, Tn, c.bintot.p, meta, cls);
+        bin_colscan_kernel<<<(Tn + 63) / 64, 64 * kCS, 0, c.stream>>>(c.binH.p, nch, Tn, c.bintot.p, meta);
         TS_LAUNCHED(c);
     } else {
         cudaMemsetAsync(c.bintot.p, 0, size_t(Tn) * 4, c.stream);
@@ -456,7 +459,7 @@ bool launch_bin_count(Context& c, const DevCam& cam, const ts_render_config& cfg
     // I, the class counts and the longest list to pinned host memory; the host waits on this
     // event only, so the scatter launched next overlaps the read-back
     cudaMemcpyAsync(c.bin_host, c.starts.p + Tn, 4, cudaMemcpyDeviceToHost, c.stream);
-    cudaMemcpyAsync(c.bin_host + 1, meta, 9 * 4, cudaMemcpyDeviceToHost, c.stream);
+    cudaMemcpyAsync(c.bin_host + 1, meta, 8 * 4, cudaMemcpyDeviceToHost, c.stream);
     cudaEventRecord(c.bin_ev, c.stream);
     return true;
 }
@@ -504,10 +507,21 @@ static void sort_variant(Context& c, const uint32_t* tiles, uint32_t n, cudaStre
 void launch_tile_depth_sort(Context& c, int Tn, uint32_t max_len) {
     (void)max_len;
     if (c.I == 0) return;
-    const uint32_t* cls = c.bintot.p + Tn + 16;
+    // the size classes are contiguous ranges of the tile order (descending list length), so
+    // every class kernel also starts with its longest lists; c.tile_order is built first
+    const uint32_t* ord = c.tile_order.p;
+    uint32_t off[7];
+    off[6] = 0;
+    off[4] = off[6] + c.bin_class[6];
+    off[3] = off[4] + c.bin_class[4];
+    off[5] = off[3] + c.bin_class[3];
+    off[2] = off[5] + c.bin_class[5];
+    off[1] = off[2] + c.bin_class[2];
+    off[0] = off[1] + c.bin_class[1];
+    (void)Tn;
     if (c.bin_class[0]) {
         tile_copy_single_kernel<<<(c.bin_class[0] + 255) / 256, 256, 0, c.stream>>>(c.starts.p, c.ival[1].p,
-                                                                                  c.ival[0].p, cls, int(c.bin_class[0]));
+                                                                                  c.ival[0].p, ord + off[0], int(c.bin_class[0]));
         TS_LAUNCHED(c);
     }
     // the size classes are independent: the two largest run on fork streams so their
@@ -522,9 +536,9 @@ void launch_tile_depth_sort(Context& c, int Tn, uint32_t max_len) {
     cudaEventRecord(c.fork_ev, c.stream);
     cudaStreamWaitEvent(c.side[0], c.fork_ev, 0);
     cudaStreamWaitEvent(c.side[1], c.fork_ev, 0);
-    sort_variant<kCap2, 512>(c, cls + size_t(3) * Tn, c.bin_class[3], c.side[0]);
+    sort_variant<kCap2, 512>(c, ord + off[3], c.bin_class[3], c.side[0]);
     if (c.bin_class[6]) {  // lists longer than kCap3: 4 sorted segments, then 2 merge levels
-        const uint32_t* lt = cls + size_t(6) * Tn;
+        const uint32_t* lt = ord + off[6];
         sort_variant<kCap3, 1024, true>(c, lt, c.bin_class[6], c.side[0]);
         // c.sortmp holds >= I entries (run_forward sizes it before the fork)
         const dim3 g(kCapL / (kMergeT * kMergePer), c.bin_class[6]);
@@ -533,10 +547,10 @@ void launch_tile_depth_sort(Context& c, int Tn, uint32_t max_len) {
                                                         2 * kCap3);
         c.launches += 2;
     }
-    sort_variant<kCap3, 1024>(c, cls + size_t(4) * Tn, c.bin_class[4], c.side[1]);
-    sort_variant<kCapM, 512>(c, cls + size_t(5) * Tn, c.bin_class[5], c.side[1]);
-    sort_variant<kCap1, 512>(c, cls + size_t(2) * Tn, c.bin_class[2], c.stream);
-    sort_variant<kCap0, 256>(c, cls + size_t(1) * Tn, c.bin_class[1], c.stream);
+    sort_variant<kCap3, 1024>(c, ord + off[4], c.bin_class[4], c.side[1]);
+    sort_variant<kCapM, 512>(c, ord + off[5], c.bin_class[5], c.side[1]);
+    sort_variant<kCap1, 512>(c, ord + off[2], c.bin_class[2], c.stream);
+    sort_variant<kCap0, 256>(c, ord + off[1], c.bin_class[1], c.stream);
     for (int k = 0; k < 2; ++k) {
         cudaEventRecord(c.join_ev[k], c.side[k]);
         cudaStreamWaitEvent(c.stream, c.join_ev[k], 0);

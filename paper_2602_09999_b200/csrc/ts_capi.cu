@@ -263,10 +263,11 @@ ts_status run_forward(Context& c, const ts_camera& cam, const ts_render_config& 
             launch_bin_scatter(c, dc, cfg);
             stage_end(c, 3);
         }
+        launch_tile_order(c, Tn);  // also the per-class tile lists of the sorts (longest first)
+        if (!c.tile_order.p) return TS_ERR_OOM;
         stage_begin(c, 4);
         launch_tile_depth_sort(c, Tn, max_len);
         stage_end(c, 4);
-        launch_tile_order(c, Tn);
     }
     c.order_ok = c.tile_order.p != nullptr;
     stage_begin(c, 6);

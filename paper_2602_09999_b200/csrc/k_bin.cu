@@ -6,8 +6,8 @@
 // is produced here by bucketing followed by a small per-tile sort, instead of
 // a depth sort over N plus a radix sort over I:
 //
-//   KB1 histogram   per-tile instance counts of every chunk of Gaussians (8192, or
-//                   4096 / 2048 for small N, bin_chunk_for), H[chunk][tile],
+//   KB1 histogram   per-tile instance counts of every chunk of Gaussians (6144, or
+//                   3072 / 1536 for small N, bin_chunk_for), H[chunk][tile],
 //                   accumulated by K1 itself (k_preprocess.cu) with fire-and-forget
 //                   REDs as it decides each kept tile;
 //   KB2 bin_colscan per tile: exclusive prefix of H over chunks, tile totals and

@@ -130,8 +130,11 @@ void launch_duplicate(Context& c, const DevCam& cam, const ts_render_config& cfg
 void launch_tile_sort(Context& c, int tile_bits);
 void launch_ranges(Context& c, int n_tiles);
 // bucketed binning (k_bin.cu): returns I (syncs) and the longest tile list, -1 on OOM
-constexpr int kBinChunk = 8192;  // largest chunk of the bucketed binning (Gaussians per histogram row)
-// chunk size for N Gaussians: the largest of 8192 / 4096 / 2048 that still gives >= 2 chunk
+#ifndef TS_BIN_CHUNK
+#define TS_BIN_CHUNK 6144  // measured: 6144 beats 8192 (fewer same-address histogram REDs, fuller scatter waves)
+#endif
+constexpr int kBinChunk = TS_BIN_CHUNK;  // largest chunk of the bucketed binning (Gaussians per histogram row)
+// chunk size for N Gaussians: the largest of 6144 / 3072 / 1536 that still gives >= 2 chunk
 // CTAs per SM for the scatter (small stores would otherwise leave SMs idle)
 inline int bin_chunk_for(int64_t N, int sm_count) {
     int ch = kBinChunk;

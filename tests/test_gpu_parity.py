@@ -380,14 +380,14 @@ def test_stale_gradient_buffer_overwrite(engine):
         assert np.array_equal(A[det].view(np.uint32), B[det].view(np.uint32))
 
 
-@pytest.mark.parametrize("name", ["mid", "dense", "H", "ties", "chunk4096"])
+@pytest.mark.parametrize("name", ["mid", "dense", "H", "ties", "chunk_mid"])
 def test_bucketed_binning_equals_radix(engine, name):
     """Bucketed binning + per-tile sort (k_bin.cu, default) and the two-stage radix
     sort (k_sort.cu) give identical tile lists and ranges; "ties" duplicates rows so
     equal depth keys must break by Gaussian index (SPEC.md:247 stable order).  The
-    chunk size of the bucketed path depends on N: small scenes use 2048, "chunk4096"
-    (1.5M Gaussians) 4096 and "H" 8192 Gaussians per histogram row."""
-    if name == "chunk4096":
+    chunk size of the bucketed path depends on N: small scenes use 1536, "chunk_mid"
+    (1.5M Gaussians) 3072 and "H" 6144 Gaussians per histogram row."""
+    if name == "chunk_mid":
         n = 1_500_000
         p = scene.random_params(n, 0.01, 0.0, 22)
         cam, cfg = scene.make_camera(640, 480), T.RenderConfig.make(sh_degree=1)

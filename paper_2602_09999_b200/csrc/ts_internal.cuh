@@ -135,10 +135,12 @@ void launch_ranges(Context& c, int n_tiles);
 #endif
 constexpr int kBinChunk = TS_BIN_CHUNK;  // largest chunk of the bucketed binning (Gaussians per histogram row)
 // chunk size for N Gaussians: the largest of 6144 / 3072 / 1536 that still gives >= 2 chunk
-// CTAs per SM for the scatter (small stores would otherwise leave SMs idle)
+// CTAs per SM for the scatter (small stores would otherwise leave SMs idle).  Every size is a
+// multiple of the scatter's 512 threads (whole rects per thread) and of a warp (K1's per-warp row).
 inline int bin_chunk_for(int64_t N, int sm_count) {
     int ch = kBinChunk;
     while (ch > 2048 && (N + ch - 1) / ch < 2 * int64_t(sm_count)) ch >>= 1;
+    static_assert(kBinChunk % 2048 == 0 || kBinChunk == 6144, "chunk halvings must stay multiples of 512");
     return ch;
 }
 bool bin_supported(int Tn);

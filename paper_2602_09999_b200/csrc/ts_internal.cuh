@@ -140,7 +140,7 @@ constexpr int kBinChunk = TS_BIN_CHUNK;  // largest chunk of the bucketed binnin
 inline int bin_chunk_for(int64_t N, int sm_count) {
     int ch = kBinChunk;
     while (ch > 2048 && (N + ch - 1) / ch < 2 * int64_t(sm_count)) ch >>= 1;
-    static_assert(kBinChunk % 2048 == 0 || kBinChunk == 6144, "chunk halvings must stay multiples of 512");
+    static_assert(kBinChunk % 2048 == 0, "chunk halvings must stay multiples of 512");
     return ch;
 }
 bool bin_supported(int Tn);

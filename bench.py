@@ -338,6 +338,18 @@ def run_ours(args):
         pb.array[...] = targets[j]
         pins.append((j, pb))
     pin_of = dict(pins)
+    # this box's pinned host -> device bandwidth for one target (the e2e leg's per-step copy)
+    scratch = torch.empty(w.height * w.width * 3, dtype=torch.float32, device=f"cuda:{local}")
+    src = torch.from_numpy(pins[0][1].array.reshape(-1))  # pinned (ts_host_alloc)
+    c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    c0.record(stream)
+    for _ in range(5):
+        scratch.copy_(src, non_blocking=True)
+    c1.record(stream)
+    torch.cuda.synchronize()
+    h2d_ms = c0.elapsed_time(c1) / 5
+    del scratch
     e2e_steps = max(3, min(args.steps, 50))
     torch.cuda.synchronize()
     if world > 1:
@@ -416,7 +428,11 @@ def run_ours(args):
                        "morton (SPEC.md:264-272 morton_reorder applied at setup, as the training schedule does)"},
             "e2e": {"value": world / (e2e_ms * 1e-3), "unit": "steps/s",
                     "h2d_bytes_per_step": int(w.height * w.width * 3 * 4 + 104 + 64),
-                    "d2h_bytes_per_step": 16, "api": "ts_train_step (C-ABI) with pinned host target"},
+                    "d2h_bytes_per_step": 16, "api": "ts_train_step (C-ABI) with pinned host target",
+                    "h2d_ms_per_target": round(h2d_ms, 4),
+                    "h2d_gbs": round(w.height * w.width * 3 * 4 / (h2d_ms * 1e-3) / 1e9, 2),
+                    "note": "the target upload overlaps the previous step; when it takes longer than a "
+                            "device step, the leg is bound by this box's host-to-device bandwidth"},
             "stage_ms_split": {k: round(v, 4) for k, v in split.items()} if fused_bwd else None,
             "gpu_launches": int(launches),
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",

@@ -391,12 +391,14 @@ __device__ __forceinline__ uint32_t order_key(uint32_t L) {
     return L == 0 ? 0u : L == 1 ? 1u : 2u + (L - 1u) / uint32_t(kOW);
 }
 
-__global__ void __launch_bounds__(1024) tile_order_kernel(const uint32_t* __restrict__ starts, int Tn,
+// lens == nullptr: lengths from the tile ranges; else lens[t] (the forward's processed lengths)
+__global__ void __launch_bounds__(1024) tile_order_kernel(const uint32_t* __restrict__ starts,
+                                                          const uint32_t* __restrict__ lens, int Tn,
                                                           uint32_t* __restrict__ order) {
     __shared__ uint32_t hist[kOB];
     for (int i = threadIdx.x; i < kOB; i += 1024) hist[i] = 0;
     __syncthreads();
-    for (int t = threadIdx.x; t < Tn; t += 1024) atomicAdd(&hist[kOB - 1 - min(uint32_t(kOB - 1), order_key(starts[t + 1] - starts[t]))], 1u);
+    for (int t = threadIdx.x; t < Tn; t += 1024) atomicAdd(&hist[kOB - 1 - min(uint32_t(kOB - 1), order_key(lens ? lens[t] : starts[t + 1] - starts[t]))], 1u);
     __syncthreads();
     if (threadIdx.x < 32) {  // exclusive scan of the bins by one warp (kOB / 32 per lane)
         constexpr int PL = kOB / 32;
@@ -417,7 +419,7 @@ __global__ void __launch_bounds__(1024) tile_order_kernel(const uint32_t* __rest
         }
     }
     __syncthreads();
-    for (int t = threadIdx.x; t < Tn; t += 1024) order[atomicAdd(&hist[kOB - 1 - min(uint32_t(kOB - 1), order_key(starts[t + 1] - starts[t]))], 1u)] = uint32_t(t);
+    for (int t = threadIdx.x; t < Tn; t += 1024) order[atomicAdd(&hist[kOB - 1 - min(uint32_t(kOB - 1), order_key(lens ? lens[t] : starts[t + 1] - starts[t]))], 1u)] = uint32_t(t);
 }
 
 // lists of one instance need no sort: copy
@@ -472,7 +474,13 @@ bool launch_bin_count(Context& c, const DevCam& cam, const ts_render_config& cfg
 
 void launch_tile_order(Context& c, int Tn) {
     if (!ensure(c, c.tile_order, size_t(Tn))) return;
-    tile_order_kernel<<<1, 1024, 0, c.stream>>>(c.starts.p, Tn, c.tile_order.p);
+    tile_order_kernel<<<1, 1024, 0, c.stream>>>(c.starts.p, nullptr, Tn, c.tile_order.p);
+    TS_LAUNCHED(c);
+}
+
+void launch_bwd_tile_order(Context& c, int Tn) {
+    if (!c.tile_proc.p || !ensure(c, c.bwd_order, size_t(Tn))) return;
+    tile_order_kernel<<<1, 1024, 0, c.stream>>>(c.starts.p, c.tile_proc.p, Tn, c.bwd_order.p);
     TS_LAUNCHED(c);
 }
 

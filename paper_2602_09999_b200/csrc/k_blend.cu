@@ -54,7 +54,8 @@ __global__ void __launch_bounds__(kT, TS_FWD_MINB) blend_fwd_kernel(const uint32
                                                       ts_render_config cfg, float* __restrict__ rgb,
                                                       float* __restrict__ Tfin, uint32_t* __restrict__ pcount,
                                                       uint32_t* __restrict__ ip_counter,
-                                                      const uint32_t* __restrict__ order) {
+                                                      const uint32_t* __restrict__ order,
+                                                      uint32_t* __restrict__ tile_proc) {
     __shared__ float4 sA[kBatch];  // mx, my, k2, o
     __shared__ float4 sB[kBatch];  // A, 2B, C, ry
     __shared__ float4 sC[kBatch];  // r, g, b
@@ -194,6 +195,7 @@ __global__ void __launch_bounds__(kT, TS_FWD_MINB) blend_fwd_kernel(const uint32
     if ((threadIdx.x & 31) == 0) atomicMax(&s_max, wm);
     __syncthreads();
     if (threadIdx.x == 0 && s_max) atomicAdd(ip_counter, s_max);
+    if (threadIdx.x == 0 && tile_proc) tile_proc[t] = s_max;
 }
 #undef T
 #undef C0
@@ -438,12 +440,15 @@ __global__ void __launch_bounds__(kT, TS_BWD_MINB) blend_bwd_kernel(const uint32
 
 void launch_blend_fwd(Context& c, const DevCam& cam, const ts_render_config& cfg) {
     const int Tn = cam.tiles_x * cam.tiles_y;
+    ensure(c, c.tile_proc, size_t(Tn));
     if (cfg.early_stop_compat)
         blend_fwd_kernel<true><<<Tn, kT, 0, c.stream>>>(c.starts.p, c.ival[0].p, c.splat.p, cam, cfg, c.rgb.p,
-                                                        c.Tfin.p, c.pcount.p, c.counters.p + 2, c.order_ok ? c.tile_order.p : nullptr);
+                                                        c.Tfin.p, c.pcount.p, c.counters.p + 2, c.order_ok ? c.tile_order.p : nullptr,
+                                                        c.tile_proc.p);
     else
         blend_fwd_kernel<false><<<Tn, kT, 0, c.stream>>>(c.starts.p, c.ival[0].p, c.splat.p, cam, cfg, c.rgb.p,
-                                                         c.Tfin.p, c.pcount.p, c.counters.p + 2, c.order_ok ? c.tile_order.p : nullptr);
+                                                         c.Tfin.p, c.pcount.p, c.counters.p + 2, c.order_ok ? c.tile_order.p : nullptr,
+                                                         c.tile_proc.p);
     TS_LAUNCHED(c);
 }
 
@@ -451,7 +456,7 @@ void launch_blend_bwd(Context& c, const DevCam& cam, const ts_render_config& cfg
     (void)cfg;
     const int Tn = cam.tiles_x * cam.tiles_y;
     blend_bwd_kernel<<<Tn, kT, 0, c.stream>>>(c.starts.p, c.ival[0].p, c.splat.p, cam, c.rgb.p, c.pcount.p,
-                                              c.dLdC.p, c.g2d.p, c.order_ok ? c.tile_order.p : nullptr);
+                                              c.dLdC.p, c.g2d.p, c.bwd_order_ok ? c.bwd_order.p : (c.order_ok ? c.tile_order.p : nullptr));
     TS_LAUNCHED(c);
 }
 

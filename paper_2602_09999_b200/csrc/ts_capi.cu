@@ -270,6 +270,7 @@ ts_status run_forward(Context& c, const ts_camera& cam, const ts_render_config& 
         stage_end(c, 4);
     }
     c.order_ok = c.tile_order.p != nullptr;
+    c.bwd_order_ok = false;  // rebuilt from this view's processed lengths by the backward
     stage_begin(c, 6);
     launch_blend_fwd(c, dc, cfg);
     stage_end(c, 6);
@@ -331,6 +332,9 @@ ts_status run_backward(Context& c, const float* dLdC_hwc) {
     if (c.grad_state != Context::kGradLive)
         CK(cudaMemsetAsync(c.vis.p, 0, size_t(std::max<int64_t>(c.N, 1)), c.stream));
     stage_begin(c, 8);
+    // backward order: tiles by the forward's processed length (the backward's per-tile work)
+    launch_bwd_tile_order(c, dc.tiles_x * dc.tiles_y);
+    c.bwd_order_ok = c.bwd_order.p != nullptr && c.tile_proc.p != nullptr;
     launch_blend_bwd(c, dc, c.cfg);
     stage_end(c, 8);
     stage_begin(c, 9);
@@ -444,7 +448,7 @@ ts_status ts_destroy(ts_ctx* x) {
     release(c.starts), release(c.rhist), release(c.scan_state), release(c.scan_tmp), release(c.counters);
     release(c.rgb), release(c.Tfin), release(c.dLdC), release(c.hwc_stage), release(c.tgt), release(c.pcount);
     release(c.loss_acc), release(c.targets), release(c.dens);
-    release(c.binH), release(c.bintot), release(c.tile_order), release(c.sortmp), release(c.spare), release(c.cams), release(c.mcode[0]), release(c.mcode[1]),
+    release(c.binH), release(c.bintot), release(c.tile_order), release(c.tile_proc), release(c.bwd_order), release(c.sortmp), release(c.spare), release(c.cams), release(c.mcode[0]), release(c.mcode[1]),
         release(c.midx[0]), release(c.midx[1]), release(c.tgt_stage), release(c.nu_hat);
     for (size_t k = 0; k < c.ev_b.size(); ++k) {
         cudaEventDestroy(c.ev_b[k]);

@@ -104,6 +104,9 @@ struct Context {
     DevBuf<uint32_t> binH, bintot;
     DevBuf<uint32_t> tile_order;   // blend order of the tiles (longest lists first)
     bool order_ok = false;         // tile_order is valid for the current view
+    DevBuf<uint32_t> tile_proc;    // per tile: list positions the forward processed (its max contributor count)
+    DevBuf<uint32_t> bwd_order;    // blend-backward order: tiles by descending processed length
+    bool bwd_order_ok = false;
     uint32_t* bin_host = nullptr;  // pinned read-back of (I, class counts, longest list)
     cudaEvent_t bin_ev = nullptr;
     DevBuf<float> nu_hat;        // sampling rates (antialias), N floats
@@ -151,6 +154,8 @@ bool launch_bin_count(Context& c, const DevCam& cam, const ts_render_config& cfg
 int64_t finish_bin_count(Context& c, uint32_t* max_len);
 // c.tile_order = tiles by descending list length (from the tile ranges; both binning paths)
 void launch_tile_order(Context& c, int Tn);
+// c.bwd_order from the forward's processed lengths (the backward's per-tile work)
+void launch_bwd_tile_order(Context& c, int Tn);
 void launch_bin_scatter(Context& c, const DevCam& cam, const ts_render_config& cfg);
 void launch_tile_depth_sort(Context& c, int Tn, uint32_t max_len);
 void launch_blend_fwd(Context& c, const DevCam& cam, const ts_render_config& cfg);

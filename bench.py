@@ -3,24 +3,34 @@
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--workload H] [--impl ours|reference]
 
-A step = one training iteration on one view per GPU (weak scaling: the
-view batch grows with N): render -> L1+D-SSIM loss -> backward -> (N>1: NCCL
-all-reduce of the flat gradient buffer over NVLink) -> fused Adam.  The views
-cycle over an 8-camera ring around the scene (a trainer walking its camera
-set); every view's target is rendered from the ground-truth store once.  The default
-workload "H" is BASELINE.json's metric point: 3M Gaussians, SH degree 3,
-1920x1080 (synthetic scene, random-init parameters; target rendered from the
-ground-truth store, trained store = seeded perturbation of it).
+A step = one training iteration over the step's view batch: per view render -> L1+D-SSIM
+loss -> backward (gradients summed over the batch), then (N>1: one NCCL
+exchange of the flat 59N gradient buffer over NVLink) -> fused Adam.  The views cycle
+over an 8-camera ring around the scene (a trainer walking its camera set); every view's
+target is rendered from the ground-truth store once.
 
-`value`  : view-steps/s over all ranks, inputs (targets) resident in HBM.
-`e2e`    : the same through the public C-ABI call (ts_train_step) with the
-           target copied from pinned host memory every step and the loss read
-           back every step.
-`roofline`: dominant kernel of the step, algorithmic bytes per
-           launch / its CUDA-event duration measured over the timed region.
-`cpu_baseline`: the C++ CPU oracle (oracle/, a port of SPEC.md) timed on this
-           host's cores on one full step of the same workload (rank 0, N=1).
---impl reference: the CPU oracle alone, K steps on the host cores.
+Batches (`config.views_per_step`):
+  * every workload but c4 trains ONE view per GPU per step (weak scaling: the batch grows
+    with N).  The default "H" is BASELINE.json's metric point: 3M Gaussians, SH3, 1920x1080;
+  * c4 (6M Gaussians, 1080p) trains a fixed 8-view batch per step, split 8/N views per GPU
+    (strong scaling, north_star's 1/2/4/8-GPU config): N=1 accumulates all 8 views, then one Adam.
+With --gpus N > 1 and no torchrun environment the script re-launches itself under
+torch.distributed.run with N ranks (one per GPU, NCCL); the default exchange for N > 1 is
+"sharded" (reduce-scatter -> Adam on 1/N -> all-gather).
+
+`value`  : steps/s x (views per step / views per step at N=1) for weak scaling, i.e. view-steps/s
+           over all ranks; steps/s of the fixed batch for strong scaling.  Inputs (targets)
+           resident in HBM.
+`e2e`    : the same through the public C-ABI (ts_train_step, or forward/loss/backward + the
+           exchange for batches) with every step's targets copied from pinned host memory and
+           the loss read back; warmed up, then timed in 5 chunks (spread reported).
+`roofline`: dominant kernel of the step, algorithmic bytes per launch / its
+           CUDA-event duration measured over the timed region.
+`compute`: blend kernels' fragment evaluations/s and issue-slot fraction (ncu instruction
+           counts in profiles/inst.json over the live duration and SM clock).
+`cpu_baseline`: the C++ CPU oracle (oracle/, a port of SPEC.md) timed on this host's cores on
+           one full step of the same workload (rank 0, N=1).
+--impl reference: the CPU oracle alone, a bounded number of steps on the host cores.
 """
 from __future__ import annotations
 
@@ -131,22 +141,48 @@ def dist_env():
     return world, rank, local
 
 
-REF_STEPS = 10  # cap of the reference (CPU) arm's timed steps (~3 s each at workload H)
-N_VIEWS = 8  # training cameras cycled one per step (per GPU), as a 3DGS trainer walks its view set
+REF_VIEW_STEPS = 10  # cap of the reference (CPU) arm's timed views (~3 s each at workload H)
+N_VIEWS = scene.RING_VIEWS  # training cameras cycled per step, as a 3DGS trainer walks its view set
 
 
 def view_camera(w, j):
-    """Camera j of the ring: the headline view (j = 0) rotated by 360/N_VIEWS * j degrees about the
-    scene's vertical axis.  Every view sees the whole synthetic cube (same per-view workload)."""
-    base = np.array([0.3, -0.8, -3.5])
-    a = math.radians(360.0 / N_VIEWS * j)
-    R = np.array([[math.cos(a), 0, math.sin(a)], [0, 1, 0], [-math.sin(a), 0, math.cos(a)]])
-    return scene.make_camera(w.width, w.height, tuple(R @ base))
+    """Camera j of the benchmark's view ring (scene.ring_camera)."""
+    return scene.ring_camera(w, j, N_VIEWS)
 
 
-def cpu_step_baseline(w, gt, p0, cams, cfg, targets, steps=1, warmup=0):
-    """The C++ oracle (port of SPEC.md) on all host cores: full single-view training steps, step i on
-    view i mod len(cams)."""
+def batch_of(w, world):
+    """(views per step, scaling): c4 is a fixed 8-view batch split over the GPUs (strong); every
+    other workload trains one view per GPU per step (weak)."""
+    if w.views > 1:
+        if w.views % world:
+            raise SystemExit(f"workload {w.name}: {w.views} views per step do not split over {world} GPUs")
+        return w.views, "strong"
+    return world, "weak"
+
+
+def step_views(step, batch, world, rank):
+    """Ring views of this rank at training step `step` (1-based): the step's batch is the global
+    view indices [step*batch, step*batch + batch); rank r takes every world-th one."""
+    return [(step * batch + k) % N_VIEWS for k in range(rank, batch, world)]
+
+
+def bench_config(w, args, world, batch, scaling):
+    """The config dict of BOTH arms (identical keys and values for the same workload)."""
+    return {"workload": w.name, "gaussians": w.n, "sh_degree": w.sh_degree,
+            "resolution": f"{w.width}x{w.height}", "views_per_step": batch if scaling == "strong" else 1,
+            "batch_scaling": scaling,
+            "views": f"{N_VIEWS}-camera ring (headline view rotated about the scene axis)",
+            "optimizer": "fused_backward (SPEC.md:492-500)" if args.adam_mode == "fused_backward"
+            else "fused (SPEC.md:473-480)",
+            "precision": "fp32",
+            "l2": "no flush: per-step working set ~9 GB >> 126 MB L2",
+            "gaussian_order": "random" if args.no_morton else
+            "morton (SPEC.md:264-272 morton_reorder applied at setup, as the training schedule does)"}
+
+
+def cpu_step_baseline(w, p0, cams, cfg, targets, views_per_step=1, steps=1, warmup=0):
+    """The C++ oracle (port of SPEC.md) on all host cores: full training steps of `views_per_step`
+    views each (render, loss, backward summed over the views, then Adam), views cycling over cams."""
     from oracle import oracle as O
     cores = os.cpu_count() or 1
     O.set_workers(cores)
@@ -157,11 +193,27 @@ def cpu_step_baseline(w, gt, p0, cams, cfg, targets, steps=1, warmup=0):
     acc = np.zeros(n, np.float32)
     vc = np.zeros(n, np.float32)
     times, stages = [], None
+    k = 0
     for i in range(warmup + steps):
         adam = T.AdamConfig.make(step=i + 1)
         t0 = time.perf_counter()
-        j = i % len(cams)
-        _, st = O.train_step(params, m, v, n, cams[j], cfg, targets[j], adam, acc, vc)
+        if views_per_step == 1:
+            _, st = O.train_step(params, m, v, n, cams[k % len(cams)], cfg, targets[k % len(cams)], adam, acc, vc)
+            k += 1
+        else:
+            G = np.zeros_like(params)
+            st = None
+            for _ in range(views_per_step):
+                j = k % len(cams)
+                k += 1
+                rgb, _, _, _ = O.render(params, n, cams[j], cfg)
+                _, dl = O.training_loss(rgb, targets[j])
+                g, _, a_, c_ = O.backward(params, n, cams[j], cfg, dl)
+                G += g
+                acc += a_
+                vc += c_
+            O.adam_step(params, G, m, v, n, list(adam.lr), adam.beta1, adam.beta2, adam.eps, adam.bc1, adam.bc2,
+                        mode=T.ADAM_FUSED)
         dt = time.perf_counter() - t0
         if i >= warmup:
             times.append(dt)
@@ -169,7 +221,7 @@ def cpu_step_baseline(w, gt, p0, cams, cfg, targets, steps=1, warmup=0):
     t = float(np.mean(times))
     return {"value": 1.0 / t, "unit": "steps/s", "cores": cores, "kind": "port",
             "sample": f"{steps} full training step(s) of workload {w.name} ({n} Gaussians, SH{w.sh_degree}, "
-                      f"{w.width}x{w.height}, 1 view per step): render+loss+backward+Adam",
+                      f"{w.width}x{w.height}, {views_per_step} view(s) per step): render+loss+backward+Adam",
             "s_per_step": t,
             "stage_s": dict(zip(("preprocess", "binning", "blend", "loss", "raster_bwd", "project_bwd", "adam"),
                                 [round(float(x), 4) for x in stages[:7]])) if stages is not None else None}
@@ -181,32 +233,67 @@ def run_reference(args):
         return 0
     w = scene.WORKLOADS[args.workload]
     from oracle import oracle as O
+    batch, scaling = batch_of(w, world)
+    vps = batch if scaling == "strong" else 1
     gt = scene.random_params(w.n, w.s0, w.m_o, w.seed)
-    # bounded sample: at most REF_STEPS timed steps (+1 warm-up) so the arm ends in about a minute
-    steps, warmup = max(1, min(args.steps, REF_STEPS)), min(args.warmup, 1)
-    cams = [view_camera(w, j) for j in range(min(N_VIEWS, warmup + steps))]
+    # bounded sample: at most REF_VIEW_STEPS timed views (+1 warm-up step) so the arm ends in minutes
+    steps = max(1, min(args.steps, REF_VIEW_STEPS // vps))
+    warmup = min(args.warmup, 1)
+    cams = [view_camera(w, j) for j in range(min(N_VIEWS, (warmup + steps) * vps))]
     cfg = T.RenderConfig.make(sh_degree=w.sh_degree)
     O.set_workers(os.cpu_count() or 1)
     targets = [O.render(gt, w.n, c, cfg)[0] for c in cams]
     p0 = scene.perturb(gt, w.n, w.seed)
+    del gt
     if not args.no_morton:  # same Gaussian order as the GPU arm
         O.morton_reorder(p0, w.n)
-    cb = cpu_step_baseline(w, gt, p0, cams, cfg, targets, steps=steps, warmup=warmup)
+    cb = cpu_step_baseline(w, p0, cams, cfg, targets, views_per_step=vps, steps=steps, warmup=warmup)
+    # the same unit as our arm: view-steps/s for the weak (one view per GPU) workloads, steps/s of
+    # the fixed batch for c4; the CPU arm is one host, so it is compared at its own batch
     val = cb["value"]
     line = {"impl": "reference", "metric": METRIC, "value": val, "unit": "steps/s", "n_gpus": world,
-            "steps": steps, "warmup": warmup, "steps_requested": args.steps, "ms_per_step": 1e3 / val, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-            "data": "synthetic (seeded random Gaussians, self-rendered target)",
-            "config": {"workload": w.name, "gaussians": w.n, "sh_degree": w.sh_degree,
-                       "resolution": f"{w.width}x{w.height}", "views_per_step": 1, "parallelism": "host threads",
-                       "views": f"{N_VIEWS}-camera ring, one view per step",
-                       "gaussian_order": "random" if args.no_morton else "morton"},
+            "steps": steps, "warmup": warmup, "steps_requested": args.steps, "ms_per_step": 1e3 / val,
+            "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (seeded random Gaussians; target self-rendered from the GT store; trained store = "
+                    "perturbed GT)",
+            "config": bench_config(w, args, 1, vps if scaling == "strong" else 1, scaling),
+            "parallelism": f"{cb['cores']} host threads (std::thread pool)",
             "cpu_baseline": {"value": val, "unit": "steps/s", "cores": cb["cores"], "kind": "port",
                              "sample": cb["sample"]},
             "e2e": {"value": val, "unit": "steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
             "stage_s": cb["stage_s"]}
     print(json.dumps(line), flush=True)
     return 0
+
+
+def compute_roofline(avg_ms, vstats, clocks, n_tiles):
+    """Blend kernels (K6 / K8): fragment evaluations per second (256 pixels x processed list
+    positions Ip per pass) and the issue-slot fraction = warp instructions per launch (ncu,
+    profiles/inst.json, same workload) / (duration x 148 SMs x 4 schedulers x SM clock)."""
+    inst = {}
+    f = os.path.join(ROOT, "profiles", "inst.json")
+    if os.path.exists(f):
+        try:
+            with open(f) as fh:
+                inst = json.load(fh)
+        except Exception:
+            inst = {}
+    mhz = clocks.get("sm_mhz") or 1965.0
+    out = {"fragment_evals_per_pass": 256 * vstats["Ip"], "sm_mhz": mhz,
+           "issue_peak_winst_per_s": 148 * 4 * mhz * 1e6}
+    for k in ("blend", "blend_bwd", "preprocess", "loss", "project_bwd"):
+        if k not in avg_ms or avg_ms[k] <= 0:
+            continue
+        t = avg_ms[k] * 1e-3
+        row = {"ms": round(avg_ms[k], 4)}
+        if k in ("blend", "blend_bwd"):
+            row["fragment_evals_per_s"] = 256 * vstats["Ip"] / t
+        wi = inst.get(k)
+        if wi:
+            row["warp_inst_per_launch"] = wi
+            row["issue_frac"] = wi / (t * out["issue_peak_winst_per_s"])
+        out[k] = row
+    return out
 
 
 def run_ours(args):
@@ -223,21 +310,20 @@ def run_ours(args):
     stream = torch.cuda.current_stream()
     w = scene.WORKLOADS[args.workload]
     n = w.n
+    batch, scaling = batch_of(w, world)
     gt = scene.random_params(n, w.s0, w.m_o, w.seed)
-    # the view ring: rank r renders views r, r + N, ... (disjoint slices of each step's batch);
-    # every view's target is rendered from the GT store and kept in a device slot
     cams = [view_camera(w, j) for j in range(N_VIEWS)]
-    cam = cams[rank % N_VIEWS]
     cfg = T.RenderConfig.make(sh_degree=w.sh_degree)
     e = Engine(local, stream=stream.cuda_stream)
     e.set_params(gt, n)
-    targets = []
-    for j, c in enumerate(cams):
-        t, _, _ = e.render(c, cfg)
+    mine = sorted({j for s_ in range(N_VIEWS) for j in step_views(s_, batch, world, rank)})
+    targets = {}
+    for j in mine:   # every view this rank trains: target rendered from the GT store, kept in a device slot
+        t, _, _ = e.render(cams[j], cfg)
         e.set_target(j, t)
-        targets.append(t)
-    target = targets[rank % N_VIEWS]
+        targets[j] = t
     p0 = scene.perturb(gt, n, w.seed)
+    del gt
     e.set_params(p0, n)
     if not args.no_morton:
         # steady-state training order: morton_reorder fires every 5000
@@ -245,34 +331,30 @@ def run_ours(args):
         # order-invariant (bitwise), the arrays just gain spatial locality
         perm = e.morton_reorder()
         p0 = scene.reorder_params(p0, n, perm)
-    dp = DataParallelStep(e, mode=args.dp_mode)
+    dp_mode = args.dp_mode or ("sharded" if world > 1 else "allreduce")
+    dp = DataParallelStep(e, mode=dp_mode)
     step = 0
-
-    def view_of(s_):  # this rank's view at training step s_
-        return (s_ * world + rank) % N_VIEWS
-    # auto = the faster single-GPU mode as measured (profiles/): the separate float4 Adam sweep runs at the
-    # HBM roof while the fused kernel is occupancy-bound, so auto picks "fused"
     fused_bwd = args.adam_mode == "fused_backward"
     if args.densify and world > 1:
         raise SystemExit("--densify runs on one GPU (the multi-GPU path needs the statistics all-reduce)")
-    if fused_bwd and world > 1:
-        raise SystemExit("fused_backward needs the full gradient on one rank (world size 1)")
+    if fused_bwd and (world > 1 or len(step_views(1, batch, world, rank)) > 1):
+        raise SystemExit("fused_backward needs the full single-view gradient on one rank")
     mode = T.ADAM_FUSED_BACKWARD if fused_bwd else T.ADAM_FUSED
+    single_call = world == 1 and batch == 1
 
     def adam_cfg(m=None):
         # the gradient buffer is consumed by this step's optimizer; the next backward
-        # overwrites every row (no clear pass).  Sharded mode clears explicitly.
-        return T.AdamConfig.make(step=step, extent=1.0, mode=mode if m is None else m,
-                                 zero_grads=0 if args.dp_mode == "allreduce" else 1)
+        # overwrites every row (no clear pass)
+        return T.AdamConfig.make(step=step, extent=1.0, mode=mode if m is None else m, zero_grads=0)
 
     densify_log = []
 
     def train_step():
-        j = view_of(step)
-        if world == 1:  # one public C-ABI call: forward, loss, backward, Adam (target slot on the device)
-            e.train_step(cams[j], cfg, adam_cfg(), slot=j, want_loss=False)
+        vs = step_views(step, batch, world, rank)
+        if single_call:  # one public C-ABI call: forward, loss, backward, Adam (target slot on the device)
+            e.train_step(cams[vs[0]], cfg, adam_cfg(), slot=vs[0], want_loss=False)
         else:
-            dp.step([(cams[j], cfg, j)], adam_cfg())
+            dp.step([(cams[j], cfg, j) for j in vs], adam_cfg())
         if args.densify and step % 100 == 0:
             # densify / prune on the SPEC interval (every 100 iterations), as in
             # config 3's densification phase; counted in the timed region
@@ -294,6 +376,8 @@ def run_ours(args):
     torch.cuda.synchronize()
     stimes = e.stage_times()
     e.set_profiling(False)
+    if world > 1:
+        dist.barrier()
 
     # ---- timed region (device-resident targets) ----
     clk = ClockSampler(local)
@@ -325,22 +409,21 @@ def run_ours(args):
         e.set_profiling(True)
         for _ in range(min(args.steps, 20)):
             step += 1
-            j = view_of(step)
-            dp.step([(cams[j], cfg, j)], adam_cfg(T.ADAM_FUSED))
+            dp.step([(cams[j], cfg, j) for j in step_views(step, batch, world, rank)], adam_cfg(T.ADAM_FUSED))
         torch.cuda.synchronize()
         split_times = e.stage_times()
         e.set_profiling(False)
 
-    # ---- e2e: public C-ABI call with host (pinned) target and loss read-back each step ----
-    pins = []
-    for j in sorted({view_of(s_) for s_ in range(N_VIEWS)}):  # the views this rank trains
+    # ---- e2e: public C-ABI calls with host (pinned) targets and the loss read back each step ----
+    P = w.width * w.height
+    pins = {}
+    for j in mine:
         pb = PinnedBuffer((w.height, w.width, 3))
         pb.array[...] = targets[j]
-        pins.append((j, pb))
-    pin_of = dict(pins)
+        pins[j] = pb
     # this box's pinned host -> device bandwidth for one target (the e2e leg's per-step copy)
-    scratch = torch.empty(w.height * w.width * 3, dtype=torch.float32, device=f"cuda:{local}")
-    src = torch.from_numpy(pins[0][1].array.reshape(-1))  # pinned (ts_host_alloc)
+    scratch = torch.empty(P * 3, dtype=torch.float32, device=f"cuda:{local}")
+    src = torch.from_numpy(pins[mine[0]].array.reshape(-1))  # pinned (ts_host_alloc)
     c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
     c0.record(stream)
@@ -350,32 +433,45 @@ def run_ours(args):
     torch.cuda.synchronize()
     h2d_ms = c0.elapsed_time(c1) / 5
     del scratch
-    e2e_steps = max(3, min(args.steps, 50))
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    t0 = time.perf_counter()
-    for _ in range(e2e_steps):
-        step += 1
-        j = view_of(step)
-        if world == 1:
-            e.train_step(cams[j], cfg, adam_cfg(), target_ptr=pin_of[j].ptr, want_loss=True)
-        else:
+
+    def e2e_step():
+        vs = step_views(step, batch, world, rank)
+        if single_call:
+            e.train_step(cams[vs[0]], cfg, adam_cfg(), target_ptr=pins[vs[0]].ptr, want_loss=True)
+            return
+        for i, j in enumerate(vs):
             e.render(cams[j], cfg, outputs=False)
-            e.training_loss(target=pin_of[j].array, want_value=True)
+            e.training_loss(target=pins[j].array, want_value=(i == len(vs) - 1))
             e.backward(None)
-            dp.exchange_and_step(adam_cfg())
+        dp.exchange_and_step(adam_cfg())
+
+    for _ in range(3):            # warm-up: copy stream, staging buffers, pinned loss slot
+        step += 1
+        e2e_step()
     torch.cuda.synchronize()
-    e2e_ms = (time.perf_counter() - t0) * 1e3 / e2e_steps
+    chunks = 5
+    per_chunk = max(2, args.steps // chunks)
+    chunk_ms = []
+    for _ in range(chunks):
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(per_chunk):
+            step += 1
+            e2e_step()
+        torch.cuda.synchronize()
+        chunk_ms.append((time.perf_counter() - t0) * 1e3 / per_chunk)
+    e2e_ms = float(np.mean(chunk_ms))
     if world > 1:
         t = torch.tensor([e2e_ms], device=f"cuda:{local}")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_ms = float(t.item())
-    for _, pb in pins:
+    for pb in pins.values():
         pb.free()
 
-    # ---- per-stage accounting over the timed region ----
-    bytes_ = stage_bytes(vstats, n, w.sh_degree, cam.n_tiles)
+    # ---- per-stage accounting over the profiled loop ----
+    bytes_ = stage_bytes(vstats, n, w.sh_degree, cams[0].n_tiles)
     avg = {k: (tot / max(1, c)) for k, (tot, c) in stimes.items()}
     calls = {k: c for k, (tot, c) in stimes.items()}
     if fused_bwd:   # the project_bwd stage ran the fused backward + Adam kernel
@@ -387,7 +483,9 @@ def run_ours(args):
     fwd_bwd_ms = sum(split[k] for k in RASTER_STAGES)
     R = sum(bytes_[k] for k in RASTER_STAGES)
     peak, peak_kind = hbm_peak()
-    dom = max(avg, key=lambda k: avg[k])
+    # dominant kernel: largest device time per STEP (a batch step runs the raster stages once per view)
+    per_step = {k: avg[k] * calls[k] for k in avg}
+    dom = max(per_step, key=lambda k: per_step[k])
     dom_bytes = bytes_[dom] if dom != "depth_sort" else 0
     if dom in ("depth_sort", "tile_sort"):
         dom, dom_bytes = "sort", bytes_["tile_sort"]
@@ -406,33 +504,34 @@ def run_ours(args):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_step_baseline(w, gt, p0, cams[:1], cfg, targets[:1], steps=1, warmup=0)
+        vps = batch if scaling == "strong" else 1
+        cpu = cpu_step_baseline(w, p0, cams[:vps], cfg, [targets[j] for j in range(vps)], views_per_step=vps,
+                                steps=1, warmup=0)
 
     if rank == 0:
-        value = world / (ms * 1e-3)
-        P = w.width * w.height
+        # weak: every rank trains one view per step -> view-steps/s over the job; strong: steps/s
+        value = (world if scaling == "weak" else 1) / (ms * 1e-3)
+        e2e_value = (world if scaling == "weak" else 1) / (e2e_ms * 1e-3)
+        vpr = len(step_views(1, batch, world, rank))
+        spread = [round((world if scaling == "weak" else 1) / (x * 1e-3), 2) for x in chunk_ms]
         line = {
             "metric": METRIC, "value": value, "unit": "steps/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": scaling,
             "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (seeded random Gaussians; target self-rendered from the GT store; trained store = "
                     "perturbed GT)",
-            "config": {"workload": w.name, "gaussians": n, "sh_degree": w.sh_degree,
-                       "resolution": f"{w.width}x{w.height}", "views_per_step": world, "views_per_gpu": 1,
-                       "views": f"{N_VIEWS}-camera ring (headline view rotated about the scene axis), "
-                                f"rank r trains view (step * N + r) mod {N_VIEWS}",
-                       "parallelism": f"dp{world} (views; NCCL {args.dp_mode} of 59N fp32 grads)",
-                       "optimizer": "fused_backward (SPEC.md:492-500)" if fused_bwd else "fused (SPEC.md:473-480)",
-                       "l2": "no flush: per-step working set ~9 GB >> 126 MB L2",
-                       "gaussian_order": "random" if args.no_morton else
-                       "morton (SPEC.md:264-272 morton_reorder applied at setup, as the training schedule does)"},
-            "e2e": {"value": world / (e2e_ms * 1e-3), "unit": "steps/s",
-                    "h2d_bytes_per_step": int(w.height * w.width * 3 * 4 + 104 + 64),
-                    "d2h_bytes_per_step": 16, "api": "ts_train_step (C-ABI) with pinned host target",
+            "config": bench_config(w, args, world, batch, scaling),
+            "parallelism": f"dp{world} (views; NCCL {dp_mode} of the 59N fp32 gradient buffer)" if world > 1
+            else "1 GPU",
+            "views_per_gpu_per_step": vpr,
+            "e2e": {"value": e2e_value, "unit": "steps/s",
+                    "h2d_bytes_per_step": int(vpr * (P * 3 * 4) + 104 + 64),
+                    "d2h_bytes_per_step": 16,
+                    "api": "ts_train_step (C-ABI) with pinned host target" if single_call
+                    else "ts_forward + ts_loss(pinned host target) + ts_backward per view, exchange, ts_adam_step",
+                    "chunks_steps_s": spread, "warmup_steps": 3, "timed_steps": chunks * per_chunk,
                     "h2d_ms_per_target": round(h2d_ms, 4),
-                    "h2d_gbs": round(w.height * w.width * 3 * 4 / (h2d_ms * 1e-3) / 1e9, 2),
-                    "note": "the target upload overlaps the previous step; when it takes longer than a "
-                            "device step, the leg is bound by this box's host-to-device bandwidth"},
+                    "h2d_gbs": round(P * 3 * 4 / (h2d_ms * 1e-3) / 1e9, 2)},
             "stage_ms_split": {k: round(v, 4) for k, v in split.items()} if fused_bwd else None,
             "gpu_launches": int(launches),
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
@@ -443,9 +542,10 @@ def run_ours(args):
                                   "writes) streams faster than it, hence frac > 1" if achieved > peak else None)},
             "fwd_bwd": {"ms": fwd_bwd_ms,
                         "source": "profiled loop (stage CUDA events; separate-optimizer steps)" if fused_bwd
-                        else "profiled loop (stage CUDA events)", "mpix_s": world * P / (fwd_bwd_ms * 1e-3) / 1e6,
+                        else "profiled loop (stage CUDA events)", "mpix_s": P / (fwd_bwd_ms * 1e-3) / 1e6,
                         "algorithmic_bytes": int(R), "achieved_gbs": R / (fwd_bwd_ms * 1e-3) / 1e9,
                         "roofline_frac": R / (fwd_bwd_ms * 1e-3) / 1e9 / peak},
+            "compute": compute_roofline(avg, vstats, clocks, cams[0].n_tiles),
             "stage_ms": {k: round(v, 4) for k, v in avg.items()},
             "densify": [{"step": d[0], "n_after": d[1], "clones": d[2][0], "splits": d[2][1], "pruned": d[2][2]}
                         for d in densify_log] if args.densify else None,
@@ -463,6 +563,40 @@ def run_ours(args):
     return 0
 
 
+def selftest_launcher(args):
+    """The multi-rank plumbing without GPU work (CPU test): gloo rendezvous over 127.0.0.1,
+    one all-reduce and a max-over-ranks timing reduction, rank 0 prints the JSON line."""
+    import torch
+    import torch.distributed as dist
+    world, rank, _ = dist_env()
+    dist.init_process_group("gloo")
+    x = torch.ones(4) * (rank + 1)
+    dist.all_reduce(x)
+    t = torch.tensor([float(rank)])
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    w = scene.WORKLOADS[args.workload]
+    batch, scaling = batch_of(w, world)
+    if rank == 0:
+        print(json.dumps({"selftest": "launcher", "n_gpus": world, "backend": dist.get_backend(),
+                          "allreduce_sum": float(x[0]), "max_rank": float(t[0]), "scaling": scaling,
+                          "views_per_step": batch if scaling == "strong" else 1,
+                          "views_of_rank0_step1": step_views(1, batch, world, 0)}), flush=True)
+    dist.destroy_process_group()
+    return 0
+
+
+def self_launch(args):
+    """--gpus N > 1 outside torchrun: re-run this script under torch.distributed.run, one rank per GPU."""
+    import socket
+    s_ = socket.socket()
+    s_.bind(("127.0.0.1", 0))
+    port = s_.getsockname()[1]
+    s_.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -470,7 +604,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--workload", default="H", choices=sorted(scene.WORKLOADS))
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
-    ap.add_argument("--dp-mode", default="allreduce", choices=("allreduce", "sharded", "chunked"))
+    ap.add_argument("--dp-mode", default=None, choices=("allreduce", "sharded", "chunked"),
+                    help="gradient exchange for N > 1 (default sharded)")
     ap.add_argument("--adam-mode", default="auto", choices=("auto", "fused", "fused_backward"),
                     help="optimizer mode (SPEC.md:525): fused = separate fused-Adam sweep (SPEC.md:473-480); "
                          "fused_backward = Adam inside the backward (SPEC.md:492-500, 1 GPU only)")
@@ -479,12 +614,18 @@ def main():
                     help="densify_and_prune every 100 iterations inside the timed region (config 3, N=1)")
     ap.add_argument("--no-morton", action="store_true",
                     help="keep the generator's random Gaussian order instead of the z-order training state")
+    ap.add_argument("--selftest-launcher", action="store_true", help=argparse.SUPPRESS)
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    world = int(os.environ.get("WORLD_SIZE", "0"))
+    if args.gpus > 1 and world == 0:
+        return self_launch(args)
+    if world and world != args.gpus and not args.selftest_launcher:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    if args.selftest_launcher:
+        return selftest_launcher(args)
     if args.impl == "reference":
-        if args.steps > 20:
-            args.steps = 20   # each CPU step is a full multi-second H step; keep the run within minutes
         return run_reference(args)
     return run_ours(args)
 

@@ -111,6 +111,10 @@ ts_status ts_loss(ts_ctx* ctx, const float* target_hwc /* host, or NULL to use s
 /* ---- backward: accumulates into the gradient buffer ---- */
 ts_status ts_backward(ts_ctx* ctx, const float* dL_dC_hwc /* host, or NULL: use ts_loss result */);
 ts_status ts_zero_grads(ts_ctx* ctx);
+/* mark the gradient buffer consumed without clearing it (data-parallel sharded optimizer:
+ * each rank's Adam consumed only its own slice): the next backward overwrites every row
+ * (zeros for Gaussians it does not see) instead of accumulating. */
+ts_status ts_mark_grads_consumed(ts_ctx* ctx);
 ts_status ts_grad_buffer(ts_ctx* ctx, float** dev_ptr, int64_t* count); /* 59*N device fp32 (for NCCL) */
 ts_status ts_param_buffer(ts_ctx* ctx, float** dev_ptr, int64_t* count);
 ts_status ts_stats_buffer(ts_ctx* ctx, float** dev_accum, float** dev_count);

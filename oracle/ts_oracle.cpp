@@ -645,6 +645,8 @@ int64_t sort_two_stage(int64_t I, int tile_bits, uint64_t* keys, uint32_t* vals)
     std::memcpy(keys, nk.data(), I * 8);
     std::memcpy(vals, nv.data(), I * 4);
     // key bytes touched per SPEC.md:283 accounting: 4 B depth x 4 passes + tile bytes x passes
+    // (16-bit tile keys up to 2^16 tiles, 32-bit keys above: SPEC.md:193)
+    if (tb > 16) return I * 4 * 4 + I * 4 * (tb / 8);
     return I * 4 * 4 + I * (tb / 8) * (tb / 8);
 }
 
@@ -729,8 +731,10 @@ void blend_all(const View<T>& V, const Cam<T>& cam, const tso_render_config& cfg
 template <class T>
 bool valid_cam(const tso_camera* c) {
     if (!c || c->width <= 0 || c->height <= 0) return false;
+    // TileGrid: 16-bit tile keys below 2^16 tiles, 32-bit keys above
+    // (selected automatically: the combined key is tile << 32 | depth either way)
     int64_t tn = int64_t((c->width + 15) / 16) * ((c->height + 15) / 16);
-    return tn < 65536;
+    return tn < (int64_t(1) << 24);
 }
 
 template <class T>
@@ -864,46 +868,87 @@ double loss_impl(int H, int W, const T* X, const T* Yt, T* dX) {
 }
 
 // ----------------------------------------------------------------------------
-// raster_backward: per-pixel front-to-back replay with
-// deterministic tile-major merge, or per-Gaussian buckets of 32
-// restoring checkpoints.  Both sum each instance's pixel
-// contributions in pixel order, so they agree bitwise.
+// raster_backward.  Per pixel, a front-to-back pass over its
+// list (up to the contributor count) evaluates each kept fragment's alpha and
+// transmittance T_i; a reverse pass then maintains the normalised suffix colour
+//   U_i = alpha_{i+1} c_{i+1} + (1 - alpha_{i+1}) U_{i+1},   U_last = c_bg
+// (colour still to come behind fragment i, per unit of T_{i+1}/(1-alpha_i)), so
+//   dL/dalpha_i = T_i * sum_ch g_ch (c_i,ch - U_i,ch)
+// with no division by (1 - alpha) (SPEC.md:385, :430 design decision).
+// backward_mode 0 runs this per pixel over the whole list; backward_mode 1
+// (per-Gaussian buckets of 32) restores T at each bucket's
+// start (forward checkpoints) and U at its end (checkpoints of
+// the reverse pass), then replays the bucket's 32 instances for all pixels.  Both
+// run the identical per-fragment op sequence and sum each instance's pixel
+// contributions in pixel order, so they agree bitwise; the merge into per-Gaussian
+// gradients is tile-major then instance order.
 // Per-instance 2D grads: {dmx, dmy, dA, dB, dC, do, dr, dg, db}; B is the conic
 // off-diagonal entering Q as 2B.
 // ----------------------------------------------------------------------------
 template <class T>
-struct PixState {
-    T Tt, P[3];
+struct FragRec {
+    T al, G, Tt, dx, dy;
+    bool clamped;
+    uint32_t i;  // instance position
 };
 
+// forward quantities of one fragment at transmittance Tt; false if not kept (Q > k2)
 template <class T>
-inline void frag_backward(const GFwd<T>& F, T px, T py, const T* gC, const T* Rc, PixState<T>& st, T* ig) {
+inline bool frag_eval(const GFwd<T>& F, T px, T py, T Tt, FragRec<T>& r) {
     T dx = px - F.mx, dy = py - F.my;
     T Q = conic_q(F.A, F.B + F.B, F.C, dx, dy);
-    if (!(Q <= F.k2)) return;
+    if (!(Q <= F.k2)) return false;
     T G = M<T>::exp_blend(T(-0.5) * Q);
     T og = F.o * G;
-    bool clamped = og > T(0.99);
-    T al = clamped ? T(0.99) : og;
-    T w = al * st.Tt;
-    T one_m = T(1) - al;
-    T dal = T(0);
+    r.clamped = og > T(0.99);
+    r.al = r.clamped ? T(0.99) : og;
+    r.G = G;
+    r.Tt = Tt;
+    r.dx = dx;
+    r.dy = dy;
+    return true;
+}
+
+// gradient of one fragment given the normalised suffix colour U behind it; then U <- U_{i-1}
+template <class T>
+inline void frag_grad(const GFwd<T>& F, const FragRec<T>& r, const T* gC, T* U, T* ig) {
+    T w = r.al * r.Tt;
+    T s = T(0);
     for (int ch = 0; ch < 3; ++ch) {
         ig[6 + ch] += w * gC[ch];
-        T after = Rc[ch] - st.P[ch] - w * F.rgb[ch];  // S_i + T_final c_bg
-        dal += gC[ch] * (st.Tt * F.rgb[ch] - after / one_m);
+        s += gC[ch] * (F.rgb[ch] - U[ch]);
     }
-    if (!clamped) {
-        ig[5] += G * dal;
-        T dQ = T(-0.5) * G * F.o * dal;
-        ig[0] += dQ * (T(-2) * (F.A * dx + F.B * dy));
-        ig[1] += dQ * (T(-2) * (F.B * dx + F.C * dy));
-        ig[2] += dQ * dx * dx;
-        ig[3] += dQ * T(2) * dx * dy;
-        ig[4] += dQ * dy * dy;
+    T dal = r.Tt * s;
+    if (!r.clamped) {
+        ig[5] += r.G * dal;
+        T dQ = T(-0.5) * r.G * F.o * dal;
+        ig[0] += dQ * (T(-2) * (F.A * r.dx + F.B * r.dy));
+        ig[1] += dQ * (T(-2) * (F.B * r.dx + F.C * r.dy));
+        ig[2] += dQ * r.dx * r.dx;
+        ig[3] += dQ * T(2) * r.dx * r.dy;
+        ig[4] += dQ * r.dy * r.dy;
     }
-    for (int ch = 0; ch < 3; ++ch) st.P[ch] = st.P[ch] + w * F.rgb[ch];
-    st.Tt = st.Tt * one_m;
+    for (int ch = 0; ch < 3; ++ch) U[ch] = r.al * F.rgb[ch] + (T(1) - r.al) * U[ch];
+}
+
+// list positions [j0, j1) of pixel (px, py) starting at transmittance T0, with the
+// normalised suffix U_end behind position j1 (recs: scratch)
+template <class T>
+inline void pixel_range_backward(const View<T>& V, uint32_t b, uint32_t j0, uint32_t j1, T px, T py, const T* gC,
+                                 T T0, const T* U_end, T* ig, std::vector<FragRec<T>>& recs) {
+    recs.clear();
+    T Tt = T0;
+    for (uint32_t j = j0; j < j1; ++j) {
+        FragRec<T> r;
+        if (frag_eval(V.F[V.vals[b + j]], px, py, Tt, r)) {
+            r.i = b + j;
+            recs.push_back(r);
+            Tt = Tt * (T(1) - r.al);
+        }
+    }
+    T U[3] = {U_end[0], U_end[1], U_end[2]};
+    for (size_t k = recs.size(); k-- > 0;)
+        frag_grad(V.F[V.vals[recs[k].i]], recs[k], gC, U, ig + size_t(recs[k].i) * 9);
 }
 
 template <class T>
@@ -913,39 +958,57 @@ void raster_backward(const View<T>& V, const Cam<T>& cam, const tso_render_confi
     std::vector<T> ig(size_t(V.I) * 9, T(0));
     int Tn = cam.tiles_x * cam.tiles_y;
     const int BK = 32;
+    const T bg[3] = {T(cfg.bg[0]), T(cfg.bg[1]), T(cfg.bg[2])};
     pfor_dyn(Tn, [&](int64_t t) {
         int tx = int(t % cam.tiles_x), ty = int(t / cam.tiles_x);
         uint32_t b = V.ranges[2 * t], e = V.ranges[2 * t + 1];
         if (b == e) return;
         int x0 = tx * TILE, y0 = ty * TILE;
         int x1 = std::min(Wd, x0 + TILE), y1 = std::min(Hd, y0 + TILE);
+        std::vector<FragRec<T>> recs;
         if (cfg.backward_mode == 0) {
             for (int py = y0; py < y1; ++py)
                 for (int px = x0; px < x1; ++px) {
                     size_t p = size_t(py) * Wd + px;
-                    PixState<T> st{T(1), {T(0), T(0), T(0)}};
-                    for (uint32_t i = b; i < b + fb.count[p]; ++i)
-                        frag_backward(V.F[V.vals[i]], T(px), T(py), dLdC + 3 * p, fb.rgb.data() + 3 * p, st,
-                                      ig.data() + size_t(i) * 9);
+                    pixel_range_backward(V, b, 0u, fb.count[p], T(px), T(py), dLdC + 3 * p, T(1), bg, ig.data(),
+                                         recs);
                 }
         } else {
-            // forward replay records (T, P) checkpoints at every 32-instance boundary
+            // checkpoints per pixel and bucket: T at the bucket's start (forward replay) and the
+            // normalised suffix U behind its end (reverse replay)
             uint32_t maxc = 0;
             for (int py = y0; py < y1; ++py)
                 for (int px = x0; px < x1; ++px) maxc = std::max(maxc, fb.count[size_t(py) * Wd + px]);
             uint32_t nb = (maxc + BK - 1) / BK;
             int npx = (x1 - x0) * (y1 - y0);
-            std::vector<PixState<T>> ck(size_t(nb) * npx);
+            std::vector<T> ckT(size_t(nb) * npx), ckU(size_t(nb) * npx * 3);
             for (int py = y0; py < y1; ++py)
                 for (int px = x0; px < x1; ++px) {
                     size_t p = size_t(py) * Wd + px;
                     int lp = (py - y0) * (x1 - x0) + (px - x0);
-                    PixState<T> st{T(1), {T(0), T(0), T(0)}};
-                    T scratch[9] = {T(0), T(0), T(0), T(0), T(0), T(0), T(0), T(0), T(0)};
+                    const uint32_t cnt = fb.count[p];
+                    recs.clear();
+                    std::vector<uint32_t> first_rec(nb + 1, 0);  // first kept fragment of each bucket
+                    T Tt = T(1);
                     for (uint32_t j = 0; j < nb * BK; ++j) {
-                        if (j % BK == 0) ck[size_t(j / BK) * npx + lp] = st;
-                        if (j < fb.count[p]) frag_backward(V.F[V.vals[b + j]], T(px), T(py), dLdC + 3 * p,
-                                                           fb.rgb.data() + 3 * p, st, scratch);
+                        if (j % BK == 0) {
+                            ckT[size_t(j / BK) * npx + lp] = Tt;
+                            first_rec[j / BK] = uint32_t(recs.size());
+                        }
+                        FragRec<T> r;
+                        if (j < cnt && frag_eval(V.F[V.vals[b + j]], T(px), T(py), Tt, r)) {
+                            r.i = b + j;
+                            recs.push_back(r);
+                            Tt = Tt * (T(1) - r.al);
+                        }
+                    }
+                    first_rec[nb] = uint32_t(recs.size());
+                    T U[3] = {bg[0], bg[1], bg[2]};
+                    T scratch[9];
+                    for (uint32_t k = nb; k-- > 0;) {
+                        for (int ch = 0; ch < 3; ++ch) ckU[(size_t(k) * npx + lp) * 3 + ch] = U[ch];
+                        for (uint32_t q = first_rec[k + 1]; q-- > first_rec[k];)
+                            frag_grad(V.F[V.vals[recs[q].i]], recs[q], dLdC + 3 * p, U, scratch);
                     }
                 }
             for (uint32_t k = 0; k < nb; ++k)          // buckets (32, 32, ..., rest)
@@ -953,10 +1016,11 @@ void raster_backward(const View<T>& V, const Cam<T>& cam, const tso_render_confi
                     for (int px = x0; px < x1; ++px) {
                         size_t p = size_t(py) * Wd + px;
                         int lp = (py - y0) * (x1 - x0) + (px - x0);
-                        PixState<T> st = ck[size_t(k) * npx + lp];
-                        for (uint32_t j = k * BK; j < std::min<uint32_t>((k + 1) * BK, fb.count[p]); ++j)
-                            frag_backward(V.F[V.vals[b + j]], T(px), T(py), dLdC + 3 * p,
-                                          fb.rgb.data() + 3 * p, st, ig.data() + size_t(b + j) * 9);
+                        const uint32_t j1 = std::min<uint32_t>((k + 1) * BK, fb.count[p]);
+                        if (k * BK >= j1) continue;
+                        pixel_range_backward(V, b, k * BK, j1, T(px), T(py), dLdC + 3 * p,
+                                             ckT[size_t(k) * npx + lp], &ckU[(size_t(k) * npx + lp) * 3], ig.data(),
+                                             recs);
                     }
         }
     });
@@ -1136,17 +1200,6 @@ inline void adam_elem(T& th, T g, T& m, T& v, T lr, T b1, T b2, T omb1, T omb2, 
     T vh = v / bc2;
     T den = std::sqrt(vh) + eps;
     th = th - (lr * mh) / den;
-}
-
-// adam_step_fused: same contract, bias corrections folded
-// into per-step constants lr_eff = lr / bc1 and rsb2 = 1 / sqrt(bc2) computed in
-// double on the host -> one sqrt and one division per element.
-inline void adam_elem_fused(float& th, float g, float& m, float& v, float lr_eff, float b1, float b2, float omb1,
-                            float omb2, float eps, float rsb2) {
-    m = b1 * m + omb1 * g;
-    v = b2 * v + omb2 * g * g;
-    float den = std::sqrt(v) * rsb2 + eps;
-    th = th - (lr_eff * m) / den;
 }
 
 }  // namespace
@@ -1353,23 +1406,40 @@ void tso_backward_f64(int64_t n, const double* params, const tso_camera* cam, co
 
 void tso_adam_step(int64_t n, float* th, const float* g, float* m, float* v, const float lr[6], float b1, float b2,
                    float eps, float bc1, float bc2, int32_t mode, const uint8_t* visible) {
+    // Every mode applies the reference per-element op order, so
+    // fused == reference bitwise.  mode 0 is restated as the
+    // textbook multi-sweep form (moments sweep, then update sweep), modes 1/2 as the
+    // single fused sweep; fused_backward modes (3, 4) have the end state of fused
+    // (1) / skip-invisible (2).
     int64_t L = 59 * n;
     float omb1 = 1.0f - b1, omb2 = 1.0f - b2;
-    float lr_eff[6];
-    for (int k = 0; k < 6; ++k) lr_eff[k] = float(double(lr[k]) / double(bc1));
-    const float rsb2 = float(1.0 / std::sqrt(double(bc2)));
-    // fused_backward modes (3, 4) have the end state of fused (1) / skip-invisible (2)
     if (mode == 3) mode = 1;
     if (mode == 4) mode = 2;
+    if (mode == 0) {
+        pfor(L, [&](int64_t b, int64_t e) {
+            for (int64_t i = b; i < e; ++i) {
+                m[i] = b1 * m[i] + omb1 * g[i];
+                v[i] = b2 * v[i] + omb2 * g[i] * g[i];
+            }
+        });
+        pfor(L, [&](int64_t b, int64_t e) {
+            for (int64_t i = b; i < e; ++i) {
+                int64_t gi;
+                int grp = group_of(i, n, &gi);
+                float mh = m[i] / bc1;
+                float vh = v[i] / bc2;
+                float den = std::sqrt(vh) + eps;
+                th[i] = th[i] - (lr[grp] * mh) / den;
+            }
+        });
+        return;
+    }
     pfor(L, [&](int64_t b, int64_t e) {
         for (int64_t i = b; i < e; ++i) {
             int64_t gi;
             int grp = group_of(i, n, &gi);
             if (mode == 2 && visible && !visible[gi]) continue;
-            if (mode == 0)
-                adam_elem<float>(th[i], g[i], m[i], v[i], lr[grp], b1, b2, omb1, omb2, eps, bc1, bc2);
-            else
-                adam_elem_fused(th[i], g[i], m[i], v[i], lr_eff[grp], b1, b2, omb1, omb2, eps, rsb2);
+            adam_elem<float>(th[i], g[i], m[i], v[i], lr[grp], b1, b2, omb1, omb2, eps, bc1, bc2);
         }
     });
 }

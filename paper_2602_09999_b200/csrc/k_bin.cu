@@ -444,11 +444,8 @@ bool launch_bin_count(Context& c, const DevCam& cam, const ts_render_config& cfg
     const int nch = int(std::max<int64_t>(1, (c.N + chunk - 1) / chunk));
     // bintot: [0, Tn) totals | meta (16: class counts 0..6, max length)
     if (!ensure(c, c.binH, size_t(nch) * Tn) || !ensure(c, c.bintot, size_t(Tn) + 16)) return false;
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(bin_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        attr = true;
-    }
+    set_func_attr(c, reinterpret_cast<const void*>(bin_scatter_kernel), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                  200 * 1024);
     if (!c.bin_host) {
         if (cudaMallocHost(reinterpret_cast<void**>(&c.bin_host), 16 * sizeof(uint32_t)) != cudaSuccess ||
             cudaEventCreateWithFlags(&c.bin_ev, cudaEventDisableTiming) != cudaSuccess)
@@ -506,12 +503,8 @@ void launch_bin_scatter(Context& c, const DevCam& cam, const ts_render_config& c
 template <int CAP, int NT, bool SEG = false>
 static void sort_variant(Context& c, const uint32_t* tiles, uint32_t n, cudaStream_t st) {
     if (!n) return;
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(tile_sort_kernel<CAP, NT, SEG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             int(tile_sort_smem(CAP)));
-        attr = true;
-    }
+    set_func_attr(c, reinterpret_cast<const void*>(tile_sort_kernel<CAP, NT, SEG>),
+                  cudaFuncAttributeMaxDynamicSharedMemorySize, int(tile_sort_smem(CAP)));
     // segments sort in place in the scatter output; whole lists go to the final list buffer
     tile_sort_kernel<CAP, NT, SEG><<<SEG ? 4 * n : n, NT, tile_sort_smem(CAP), st>>>(
         c.starts.p, c.ival[1].p, c.dkey[0].p, SEG ? c.ival[1].p : c.ival[0].p, tiles);

@@ -153,6 +153,10 @@ int64_t launch_densify(Context& c, float thresh, float log_small, float log_big,
     cudaMemcpyAsync(st, c.counters.p + 4, sizeof(st), cudaMemcpyDeviceToHost, c.stream);
     if (cudaStreamSynchronize(c.stream) != cudaSuccess) return -1;
     const int64_t nA = tot[0], nB = tot[1], nC = tot[2], NA = nA + nB + nC;
+    if (NA > kMaxGaussians) {  // nothing has been modified yet
+        c.err = "densify would exceed the 32-bit flat-index limit (~72.8M Gaussians)";
+        return -2;
+    }
     const size_t L = (size_t(59) * std::max<int64_t>(NA, 1) + 7) & ~size_t(3);
     // three passes through one spare 59*NA buffer, swapped in after each pass (no per-call
     // allocation of the new store; capacities grow with slack, so growth reallocates rarely)

@@ -332,8 +332,7 @@ __global__ void __launch_bounds__(kFThreads, 3) loss_fused_kernel(const float* _
 }  // namespace
 
 void launch_loss(Context& c, const float* target_chw) {
-    static bool init = false;
-    if (!init) {
+    if (first_on_device(c, reinterpret_cast<const void*>(&c_gw))) {  // __constant__ is per device
         double g[11], s = 0;
         for (int i = 0; i < 11; ++i) {
             const double d = i - 5;
@@ -343,14 +342,11 @@ void launch_loss(Context& c, const float* target_chw) {
         float gf[11];
         for (int i = 0; i < 11; ++i) gf[i] = float(g[i] / s);
         cudaMemcpyToSymbol(c_gw, gf, sizeof(gf));
-        init = true;
     }
     const int W = c.fw, H = c.fh, P = W * H;
     cudaMemsetAsync(c.loss_acc.p, 0, 2 * sizeof(double), c.stream);
-    static bool attr = false;
-    if (!attr)
-        attr = cudaFuncSetAttribute(loss_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    int(kFusedSmem)) == cudaSuccess;
+    set_func_attr(c, reinterpret_cast<const void*>(loss_fused_kernel), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                  int(kFusedSmem));
     const dim3 grid((W + kFT - 1) / kFT, (H + kFT - 1) / kFT, 3);
     loss_fused_kernel<<<grid, kFThreads, kFusedSmem, c.stream>>>(c.rgb.p, target_chw, c.dLdC.p, W, H,
                                                                  float(1.0 / (3.0 * double(P))), c.loss_acc.p);

@@ -1,9 +1,10 @@
 // K10 fused Adam and layout helpers.
 //
-// Adam: one linear float4 sweep over the flat 59*N buffer; per element a fixed
-// sequence of explicit round-to-nearest ops (reference = SPEC literal formula,
-// fused = bias corrections folded into host constants: one IEEE sqrt and one
-// IEEE division per element), bitwise equal to the oracle's restatement.
+// Adam: one linear float4 sweep over the flat 59*N buffer; per element the SPEC's
+// literal op sequence with explicit round-to-nearest ops, so every
+// mode is bitwise equal to adam_step_reference and to the
+// oracle's restatement.  "fused" is the single sweep itself (moments and update in
+// one pass); the per-element arithmetic is the reference's.
 // Reads theta, g, m, v and writes theta, m, v (28 B/element, HBM-bound); with
 // zero_grads the gradient is cleared in the same pass (+4 B).
 #include <cmath>
@@ -15,31 +16,10 @@ namespace ts {
 namespace {
 
 struct AdamArgs {
-    float lr[6];      // reference: lr ; fused: lr / (1 - b1^t) (host double -> float)
+    float lr[6];
     float b1, b2, omb1, omb2, eps, bc1, bc2;
-    float rsb2;       // fused: 1 / sqrt(1 - b2^t) (host double -> float)
     int mode, zero;
 };
-
-// reference (SPEC.md:466 literal): theta -= lr * (m / bc1) / (sqrt(v / bc2) + eps)
-// fused:         theta -= (lr/bc1) * m / (sqrt(v) * (1/sqrt(bc2)) + eps)
-// Both fixed op sequences with explicit round-to-nearest ops; the oracle
-// restates each bit for bit.
-template <bool kFused>
-__device__ __forceinline__ void adam_one(float& th, float& g, float& m, float& v, float lr, const AdamArgs& a) {
-    using namespace tsx;
-    m = add(mul(a.b1, m), mul(a.omb1, g));
-    v = add(mul(a.b2, v), mul(mul(a.omb2, g), g));
-    if (kFused) {
-        const float den = add(mul(sqrt_z(v), a.rsb2), a.eps);
-        th = sub(th, div_zpos(mul(lr, m), den));
-    } else {
-        const float mh = div(m, a.bc1);
-        const float vh = div(v, a.bc2);
-        const float den = add(sqrt_(vh), a.eps);
-        th = sub(th, div(mul(lr, mh), den));
-    }
-}
 
 // flat-buffer group boundaries (elements): means | scales | quats | opacity | sh_dc | sh_rest
 struct Bounds {
@@ -83,7 +63,8 @@ __global__ void __launch_bounds__(256) adam_kernel(float4* __restrict__ th, floa
                          : i < bd.b4 ? a.lr[3]
                          : i < bd.b5 ? a.lr[4]
                                      : a.lr[5];
-        if (visible_of<MODE>(i, bd, vis)) adam_one<MODE != 0>(tp[k], gp[k], mp[k], vp[k], lr, a);
+        if (visible_of<MODE>(i, bd, vis))
+            tsx::adam_elem(tp[k], gp[k], mp[k], vp[k], lr, a.b1, a.b2, a.omb1, a.omb2, a.eps, a.bc1, a.bc2);
         if (ZERO) gp[k] = 0.f;
     }
     th[q] = t4;
@@ -159,8 +140,7 @@ __global__ void opacity_reset_kernel(float* __restrict__ op, int64_t N, float lm
 void launch_adam(Context& c, const ts_adam_config& a, int64_t begin, int64_t end) {
     if (end <= begin) return;
     AdamArgs x;
-    const bool fused = a.mode != 0;
-    for (int k = 0; k < 6; ++k) x.lr[k] = fused ? float(double(a.lr[k]) / double(a.bc1)) : a.lr[k];
+    for (int k = 0; k < 6; ++k) x.lr[k] = a.lr[k];
     x.b1 = a.beta1;
     x.b2 = a.beta2;
     x.omb1 = 1.0f - a.beta1;
@@ -168,7 +148,6 @@ void launch_adam(Context& c, const ts_adam_config& a, int64_t begin, int64_t end
     x.eps = a.eps;
     x.bc1 = a.bc1;
     x.bc2 = a.bc2;
-    x.rsb2 = float(1.0 / std::sqrt(double(a.bc2)));
     x.mode = a.mode;
     x.zero = a.zero_grads;
     const uint32_t N = uint32_t(c.N);

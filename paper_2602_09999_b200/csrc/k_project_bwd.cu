@@ -452,17 +452,13 @@ __global__ void __launch_bounds__(kBlock, TS_PB_MINB) project_bwd_kernel(const f
 constexpr int kFB = 128;  // Gaussians (= threads) per CTA
 
 struct FusedAdam {
-    float lr[6];  // lr / (1 - b1^t), per group (host double -> float)
-    float b1, b2, omb1, omb2, eps, rsb2;
+    float lr[6];  // per group
+    float b1, b2, omb1, omb2, eps, bc1, bc2;
 };
 
-// fused Adam element (same op sequence as k_optim_loss.cu adam_one<true>)
+// Adam element: the reference op sequence (ts_math.cuh adam_elem)
 __device__ __forceinline__ void adam_fused_elem(float& th, float g, float& m, float& v, float lr, const FusedAdam& a) {
-    using namespace tsx;
-    m = add(mul(a.b1, m), mul(a.omb1, g));
-    v = add(mul(a.b2, v), mul(mul(a.omb2, g), g));
-    const float den = add(mul(sqrt_z(v), a.rsb2), a.eps);
-    th = sub(th, div_zpos(mul(lr, m), den));
+    tsx::adam_elem(th, g, m, v, lr, a.b1, a.b2, a.omb1, a.omb2, a.eps, a.bc1, a.bc2);
 }
 
 // shared layout (floats): staged parameters (6 attribute segments of the CTA's
@@ -602,12 +598,12 @@ void launch_project_bwd(Context& c, const DevCam& cam, const ts_render_config& c
 #define TS_PB(D)                                                                                      \
     if (accumulate) {                                                                                 \
         constexpr int sm = PbLayout<D, true>::kTotal * 4;                                             \
-        { static bool a_ = false; if (!a_) a_ = cudaFuncSetAttribute(project_bwd_kernel<D, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm) == cudaSuccess; } \
+        set_func_attr(c, reinterpret_cast<const void*>(project_bwd_kernel<D, true>), cudaFuncAttributeMaxDynamicSharedMemorySize, sm); \
         project_bwd_kernel<D, true><<<unsigned(blocks), kBlock, sm, c.stream>>>(                      \
             c.params.p, c.grads.p, c.g2d.p, c.tcount.p, c.accum.p, c.vcount.p, c.vis.p, c.N, cam, cfg, 0, c.nu_hat.p); \
     } else {                                                                                          \
         constexpr int sm = PbLayout<D, false>::kTotal * 4;                                            \
-        { static bool a_ = false; if (!a_) a_ = cudaFuncSetAttribute(project_bwd_kernel<D, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm) == cudaSuccess; } \
+        set_func_attr(c, reinterpret_cast<const void*>(project_bwd_kernel<D, false>), cudaFuncAttributeMaxDynamicSharedMemorySize, sm); \
         project_bwd_kernel<D, false><<<unsigned(blocks), kBlock, sm, c.stream>>>(                     \
             c.params.p, c.grads.p, c.g2d.p, c.tcount.p, c.accum.p, c.vcount.p, c.vis.p, c.N, cam, cfg,   \
             int(zero_inactive), c.nu_hat.p);                                                                     \
@@ -625,23 +621,24 @@ void launch_project_bwd(Context& c, const DevCam& cam, const ts_render_config& c
 void launch_project_bwd_adam(Context& c, const DevCam& cam, const ts_render_config& cfg, const ts_adam_config& a) {
     if (c.N == 0) return;
     FusedAdam fa;
-    for (int k = 0; k < 6; ++k) fa.lr[k] = float(double(a.lr[k]) / double(a.bc1));
+    for (int k = 0; k < 6; ++k) fa.lr[k] = a.lr[k];
     fa.b1 = a.beta1;
     fa.b2 = a.beta2;
     fa.omb1 = 1.0f - a.beta1;
     fa.omb2 = 1.0f - a.beta2;
     fa.eps = a.eps;
-    fa.rsb2 = float(1.0 / std::sqrt(double(a.bc2)));
+    fa.bc1 = a.bc1;
+    fa.bc2 = a.bc2;
     const int64_t blocks = (c.N + kFB - 1) / kFB;
     constexpr int sm = FbLayout::kTotal * 4;
     const bool skip = a.mode == 4;
 #define TS_FB(D)                                                                                          \
     if (skip) {                                                                                           \
-        { static bool a_ = false; if (!a_) a_ = cudaFuncSetAttribute(project_bwd_adam_kernel<D, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm) == cudaSuccess; } \
+        set_func_attr(c, reinterpret_cast<const void*>(project_bwd_adam_kernel<D, true>), cudaFuncAttributeMaxDynamicSharedMemorySize, sm); \
         project_bwd_adam_kernel<D, true><<<unsigned(blocks), kFB, sm, c.stream>>>(                        \
             c.params.p, c.m.p, c.v.p, c.g2d.p, c.tcount.p, c.accum.p, c.vcount.p, c.vis.p, c.N, cam, cfg, fa, c.nu_hat.p); \
     } else {                                                                                              \
-        { static bool a_ = false; if (!a_) a_ = cudaFuncSetAttribute(project_bwd_adam_kernel<D, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm) == cudaSuccess; } \
+        set_func_attr(c, reinterpret_cast<const void*>(project_bwd_adam_kernel<D, false>), cudaFuncAttributeMaxDynamicSharedMemorySize, sm); \
         project_bwd_adam_kernel<D, false><<<unsigned(blocks), kFB, sm, c.stream>>>(                       \
             c.params.p, c.m.p, c.v.p, c.g2d.p, c.tcount.p, c.accum.p, c.vcount.p, c.vis.p, c.N, cam, cfg, fa, c.nu_hat.p); \
     }

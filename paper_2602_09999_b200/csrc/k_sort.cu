@@ -259,9 +259,10 @@ __global__ void __launch_bounds__(kRT) radix_scatter_kernel(const K* __restrict_
 // Gaussian's kept tiles come from the 64-bit mask K1 recorded over its tile
 // rect (bit = row-major position in the rect), so the exact-cull test is NOT
 // re-evaluated; rects of more than 64 tiles (flag bit) re-run it.
+template <class K>
 __global__ void duplicate_kernel(const uint32_t* __restrict__ perm, const uint32_t* __restrict__ offsets,
                                  const uint4* __restrict__ binrec, const float4* __restrict__ splat, int64_t N, int W,
-                                 int H, int tiles_x, int cull_mode, uint16_t* __restrict__ tkey,
+                                 int H, int tiles_x, int cull_mode, K* __restrict__ tkey,
                                  uint32_t* __restrict__ ival) {
     const int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (j >= N) return;
@@ -277,7 +278,7 @@ __global__ void duplicate_kernel(const uint32_t* __restrict__ perm, const uint32
             const int bit = __ffsll((long long)m) - 1;
             m &= m - 1;
             const int ty = ty0 + bit / wdt, tx = tx0 + bit % wdt;
-            tkey[o] = uint16_t(ty * tiles_x + tx);
+            tkey[o] = K(ty * tiles_x + tx);
             ival[o] = g;
             ++o;
         }
@@ -288,7 +289,7 @@ __global__ void duplicate_kernel(const uint32_t* __restrict__ perm, const uint32
     for (int ty = ty0; ty <= ty1; ++ty)
         for (int tx = tx0; tx <= tx1; ++tx) {
             if (cull_mode == 0 || tsx::tile_keep(s0.x, s0.y, s1.x, s1.y, s1.z, s0.z, nBA, nBC, tx, ty, W, H)) {
-                tkey[o] = uint16_t(ty * tiles_x + tx);
+                tkey[o] = K(ty * tiles_x + tx);
                 ival[o] = g;
                 ++o;
             }
@@ -298,25 +299,30 @@ __global__ void duplicate_kernel(const uint32_t* __restrict__ perm, const uint32
 // ----------------------------------------------------------------------------
 // K5 tile ranges: starts[t] = #instances with tile < t ; starts[Tn] = I
 // ----------------------------------------------------------------------------
-__global__ void ranges_kernel(const uint16_t* __restrict__ tkey, int64_t I, int Tn, uint32_t* __restrict__ starts) {
-    // 8 consecutive keys per thread (one 16-byte load when aligned)
+template <class K>
+__global__ void ranges_kernel(const K* __restrict__ tkey, int64_t I, int Tn, uint32_t* __restrict__ starts) {
+    // 8 consecutive keys per thread (one or two 16-byte loads when aligned)
     const int64_t i0 = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) * 8;
     if (i0 >= I) return;
-    uint16_t k[8];
+    K k[8];
     if (i0 + 8 <= I) {
-        const uint4 v = *reinterpret_cast<const uint4*>(tkey + i0);
-        const uint16_t* pv = reinterpret_cast<const uint16_t*>(&v);
+        const uint4* src = reinterpret_cast<const uint4*>(tkey + i0);
 #pragma unroll
-        for (int u = 0; u < 8; ++u) k[u] = pv[u];
+        for (int q = 0; q < int(sizeof(K)) / 2; ++q) {
+            const uint4 v = src[q];
+            const K* pv = reinterpret_cast<const K*>(&v);
+#pragma unroll
+            for (int u = 0; u < 16 / int(sizeof(K)); ++u) k[q * (16 / int(sizeof(K))) + u] = pv[u];
+        }
     } else {
-        for (int u = 0; u < 8; ++u) k[u] = i0 + u < I ? tkey[i0 + u] : 0;
+        for (int u = 0; u < 8; ++u) k[u] = i0 + u < I ? tkey[i0 + u] : K(0);
     }
     int prev = i0 == 0 ? -1 : int(tkey[i0 - 1]);
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
         const int64_t i = i0 + u;
         if (i >= I) break;
-        const int t = k[u];
+        const int t = int(k[u]);
         for (int tt = prev + 1; tt <= t; ++tt) starts[tt] = uint32_t(i);
         prev = t;
         if (i == I - 1)
@@ -352,15 +358,13 @@ void radix_sort(Context& c, K* k0, uint32_t* v0, K* k1, uint32_t* v1, int64_t n)
     uint32_t* offs = c.rhist.p + hn;
     K* ks[2] = {k0, k1};
     uint32_t* vs[2] = {v0, v1};
-    static bool carve = false;
-    if (!carve) {  // max shared-memory carveout: 8 resident scatter CTAs per SM instead of 4
-        cudaFuncSetAttribute(radix_scatter_kernel<uint32_t>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-        cudaFuncSetAttribute(radix_scatter_kernel<uint16_t>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-        cudaFuncSetAttribute(radix_count_kernel<uint32_t>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-        cudaFuncSetAttribute(radix_count_kernel<uint16_t>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-        cudaFuncSetAttribute(radix_scatter_kernel<unsigned long long>, cudaFuncAttributePreferredSharedMemoryCarveout,
-                             100);
-        carve = true;
+    {  // max shared-memory carveout: 8 resident scatter CTAs per SM instead of 4
+        const auto carve = cudaFuncAttributePreferredSharedMemoryCarveout;
+        set_func_attr(c, reinterpret_cast<const void*>(radix_scatter_kernel<uint32_t>), carve, 100);
+        set_func_attr(c, reinterpret_cast<const void*>(radix_scatter_kernel<uint16_t>), carve, 100);
+        set_func_attr(c, reinterpret_cast<const void*>(radix_count_kernel<uint32_t>), carve, 100);
+        set_func_attr(c, reinterpret_cast<const void*>(radix_count_kernel<uint16_t>), carve, 100);
+        set_func_attr(c, reinterpret_cast<const void*>(radix_scatter_kernel<unsigned long long>), carve, 100);
     }
     for (int p = 0; p < NPASS; ++p) {
         const int s = p & 1;
@@ -389,9 +393,15 @@ int64_t launch_scan_counts(Context& c) {
 void launch_duplicate(Context& c, const DevCam& cam, const ts_render_config& cfg) {
     if (c.N == 0 || c.I == 0) return;
     const int bs = 256;
-    duplicate_kernel<<<unsigned((c.N + bs - 1) / bs), bs, 0, c.stream>>>(
-        c.dperm[0].p, c.offsets.p, c.rect.p, c.splat.p, c.N, cam.w, cam.h, cam.tiles_x, cfg.cull_mode, c.tkey[0].p,
-        c.ival[0].p);
+    const unsigned grid = unsigned((c.N + bs - 1) / bs);
+    if (cam.tiles_x * cam.tiles_y >= 65536)  // 32-bit tile keys
+        duplicate_kernel<uint32_t><<<grid, bs, 0, c.stream>>>(c.dperm[0].p, c.offsets.p, c.rect.p, c.splat.p, c.N,
+                                                              cam.w, cam.h, cam.tiles_x, cfg.cull_mode, c.tkey32[0].p,
+                                                              c.ival[0].p);
+    else
+        duplicate_kernel<uint16_t><<<grid, bs, 0, c.stream>>>(c.dperm[0].p, c.offsets.p, c.rect.p, c.splat.p, c.N,
+                                                              cam.w, cam.h, cam.tiles_x, cfg.cull_mode, c.tkey[0].p,
+                                                              c.ival[0].p);
     TS_LAUNCHED(c);
 }
 
@@ -465,8 +475,12 @@ __global__ void gather_rows_kernel(const float* __restrict__ src, float* __restr
     dst[i] = src[int64_t(perm[r]) * W + k];
 }
 
-void launch_tile_sort(Context& c, int tile_bits) {
-    if (tile_bits <= 8) {
+void launch_tile_sort(Context& c, int tile_bits, bool key32) {
+    if (key32) {  // >= 2^16 tiles: 32-bit tile keys, ceil(bits / 8) passes (3 up to 2^24 tiles)
+        radix_sort<uint32_t, 3>(c, c.tkey32[0].p, c.ival[0].p, c.tkey32[1].p, c.ival[1].p, c.I);
+        std::swap(c.tkey32[0], c.tkey32[1]);  // odd pass count: keep the sorted list in buffer 0
+        std::swap(c.ival[0], c.ival[1]);
+    } else if (tile_bits <= 8) {
         radix_sort<uint16_t, 1>(c, c.tkey[0].p, c.ival[0].p, c.tkey[1].p, c.ival[1].p, c.I);
         std::swap(c.tkey[0], c.tkey[1]);  // keep the sorted list in buffer 0
         std::swap(c.ival[0], c.ival[1]);
@@ -475,14 +489,17 @@ void launch_tile_sort(Context& c, int tile_bits) {
     }
 }
 
-void launch_ranges(Context& c, int n_tiles) {
+void launch_ranges(Context& c, int n_tiles, bool key32) {
     if (c.I == 0) {
         fill_u32_kernel<<<(n_tiles + 256) / 256, 256, 0, c.stream>>>(c.starts.p, n_tiles + 1, 0u);
         TS_LAUNCHED(c);
         return;
     }
-    ranges_kernel<<<unsigned((c.I + 8 * 256 - 1) / (8 * 256)), 256, 0, c.stream>>>(c.tkey[0].p, c.I, n_tiles,
-                                                                                     c.starts.p);
+    const unsigned grid = unsigned((c.I + 8 * 256 - 1) / (8 * 256));
+    if (key32)
+        ranges_kernel<uint32_t><<<grid, 256, 0, c.stream>>>(c.tkey32[0].p, c.I, n_tiles, c.starts.p);
+    else
+        ranges_kernel<uint16_t><<<grid, 256, 0, c.stream>>>(c.tkey[0].p, c.I, n_tiles, c.starts.p);
     TS_LAUNCHED(c);
 }
 

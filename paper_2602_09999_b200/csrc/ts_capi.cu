@@ -5,7 +5,11 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <new>
+#include <set>
+#include <tuple>
 #include <vector>
 
 #include "ts_internal.cuh"
@@ -36,6 +40,27 @@ bool ensure(Context& c, DevBuf<T>& b, size_t n, bool keep) {
     b.p = p;
     b.cap = cap;
     return true;
+}
+
+namespace {
+std::mutex g_dev_mu;
+std::map<std::tuple<const void*, int, int>, int> g_attr;  // (fn, device, attribute) -> value set
+std::set<std::pair<const void*, int>> g_first;              // (key, device) already initialised
+}  // namespace
+
+bool set_func_attr(const Context& c, const void* fn, cudaFuncAttribute attr, int value) {
+    std::lock_guard<std::mutex> lk(g_dev_mu);
+    const auto key = std::make_tuple(fn, c.device, int(attr));
+    auto it = g_attr.find(key);
+    if (it != g_attr.end() && it->second == value) return true;
+    if (cudaFuncSetAttribute(fn, attr, value) != cudaSuccess) return false;  // the launch reports it
+    g_attr[key] = value;
+    return true;
+}
+
+bool first_on_device(const Context& c, const void* key) {
+    std::lock_guard<std::mutex> lk(g_dev_mu);
+    return g_first.insert(std::make_pair(key, c.device)).second;
 }
 
 template bool ensure<float>(Context&, DevBuf<float>&, size_t, bool);
@@ -112,8 +137,11 @@ bool valid_camera(const ts_camera* cam, std::string* why) {
     if (!cam) return *why = "camera is NULL", false;
     if (cam->width < 6 || cam->height < 6) return *why = "image must be at least 6x6", false;
     if (!(cam->fx > 0.f) || !(cam->fy > 0.f)) return *why = "fx, fy must be > 0", false;
+    // TileGrid: 16-bit tile keys below 2^16 tiles, 32-bit keys above (selected
+    // in launch_duplicate / launch_tile_sort); rect fields hold 15-bit tile coordinates
     int64_t tn = int64_t((cam->width + 15) / 16) * ((cam->height + 15) / 16);
-    if (tn > 65535) return *why = "more than 65535 tiles (16-bit tile keys, ~16 MP)", false;
+    if (tn >= (int64_t(1) << 24) || cam->width > 32767 * 16 || cam->height > 32767 * 16)
+        return *why = "frame too large (>= 2^24 tiles)", false;
     return true;
 }
 
@@ -239,9 +267,13 @@ ts_status run_forward(Context& c, const ts_camera& cam, const ts_render_config& 
             release(c.ival[k]);
             if (!ensure(c, c.ival[k], capI)) return TS_ERR_OOM;
         }
-        if (radix && c.tkey[k].cap < size_t(I)) {
+        if (radix && Tn < 65536 && c.tkey[k].cap < size_t(I)) {
             release(c.tkey[k]);
             if (!ensure(c, c.tkey[k], capI)) return TS_ERR_OOM;
+        }
+        if (radix && Tn >= 65536 && c.tkey32[k].cap < size_t(I)) {  // 32-bit tile keys
+            release(c.tkey32[k]);
+            if (!ensure(c, c.tkey32[k], capI)) return TS_ERR_OOM;
         }
     }
     if (!radix && c.bin_class[6] && !ensure_grow(c, c.sortmp, size_t(I))) return TS_ERR_OOM;  // long-list merges
@@ -251,10 +283,10 @@ ts_status run_forward(Context& c, const ts_camera& cam, const ts_render_config& 
         launch_duplicate(c, dc, cfg);
         stage_end(c, 3);
         stage_begin(c, 4);
-        launch_tile_sort(c, tile_bits_for(Tn));
+        launch_tile_sort(c, tile_bits_for(Tn), Tn >= 65536);
         stage_end(c, 4);
         stage_begin(c, 5);
-        launch_ranges(c, Tn);
+        launch_ranges(c, Tn, Tn >= 65536);
         stage_end(c, 5);
         launch_tile_order(c, Tn);
     } else {
@@ -443,7 +475,7 @@ ts_status ts_destroy(ts_ctx* x) {
     release(c.params), release(c.grads), release(c.m), release(c.v), release(c.accum), release(c.vcount);
     release(c.splat), release(c.rect), release(c.tcount), release(c.offsets), release(c.g2d), release(c.vis);
     for (int k = 0; k < 2; ++k) {
-        release(c.dkey[k]), release(c.dperm[k]), release(c.tkey[k]), release(c.ival[k]);
+        release(c.dkey[k]), release(c.dperm[k]), release(c.tkey[k]), release(c.tkey32[k]), release(c.ival[k]);
     }
     release(c.starts), release(c.rhist), release(c.scan_state), release(c.scan_tmp), release(c.counters);
     release(c.rgb), release(c.Tfin), release(c.dLdC), release(c.hwc_stage), release(c.tgt), release(c.pcount);
@@ -484,7 +516,7 @@ ts_status ts_set_params_flat(ts_ctx* x, int64_t n, const float* flat) {
     TS_CHECK_CTX(x);
     Context& c = x->c;
     if (n < 0 || (n > 0 && !flat)) return validation(c, "bad parameter array");
-    if (n >= (int64_t(1) << 31)) return validation(c, "N must be < 2^31");
+    if (n > kMaxGaussians) return validation(c, "N exceeds the 32-bit flat-index limit (~72.8M Gaussians)");
     CK(cudaSetDevice(c.device));
     if (ensure_gaussian_buffers(c, n) != TS_OK) return TS_ERR_OOM;
     if (n != c.N) c.nu_valid = false;  // sampling rates are per row (kept across same-size updates)
@@ -600,6 +632,14 @@ ts_status ts_zero_grads(ts_ctx* x) {
     CK(cudaSetDevice(c.device));
     if (c.N) CK(cudaMemsetAsync(c.grads.p, 0, size_t(59) * c.N * 4, c.stream));
     c.grad_state = Context::kGradZero;
+    return TS_OK;
+}
+
+ts_status ts_mark_grads_consumed(ts_ctx* x) {
+    TS_CHECK_CTX(x);
+    Context& c = x->c;
+    if (c.grad_state == Context::kGradLive) c.grad_state = Context::kGradStale;
+    c.view_valid = c.loss_valid = false;
     return TS_OK;
 }
 
@@ -739,6 +779,7 @@ ts_status ts_densify(ts_ctx* x, float grad_thresh, float extent, uint64_t seed, 
     const float log_big = float(std::log(0.1 * double(extent)));
     const float logit_min = float(std::log(0.05 / 0.95));
     const int64_t na = launch_densify(c, grad_thresh, log_small, log_big, logit_min, seed, iter, st);
+    if (na == -2) return TS_ERR_VALIDATION;  // store unchanged
     if (na < 0) return c.err.empty() ? TS_ERR_CUDA : TS_ERR_OOM;
     if (n_after) *n_after = na;
     c.grad_state = Context::kGradZero;

@@ -14,6 +14,10 @@ constexpr int kTile = 16;
 constexpr int kParams = 59;
 constexpr int kG2D = 12;  // floats per Gaussian in the 2D-gradient accumulator (9 used, 16B aligned)
 constexpr int kNumStages = 11;
+// Largest store: the flat 59*N sweeps (Adam, densify, Morton) index in 32 bits, so
+// 59*N (+ float4 padding) must stay below 2^32.  ~72M Gaussians = ~85 GB of store +
+// moments + gradients, within a 180 GB B200; ts_set_params* and ts_densify reject more.
+constexpr int64_t kMaxGaussians = (int64_t(0xFFFFFFFFu) - 64) / 59;
 
 // flat 59*N buffer block offsets
 struct Off {
@@ -64,7 +68,8 @@ struct Context {
     DevBuf<uint8_t> vis;         // visible in any view since the last optimizer step
     // instances
     int64_t I = 0;
-    DevBuf<uint16_t> tkey[2];
+    DevBuf<uint16_t> tkey[2];    // 16-bit tile keys (radix path, < 2^16 tiles)
+    DevBuf<uint32_t> tkey32[2];  // 32-bit tile keys (radix path, >= 2^16 tiles)
     DevBuf<uint32_t> ival[2];
     DevBuf<uint32_t> starts;     // Tn+1
     // radix scratch
@@ -130,8 +135,8 @@ void launch_preprocess(Context& c, const DevCam& cam, const ts_render_config& cf
 void launch_depth_sort(Context& c);                 // sorts (dkey, perm) for N entries
 int64_t launch_scan_counts(Context& c);             // offsets in depth order; returns I (syncs)
 void launch_duplicate(Context& c, const DevCam& cam, const ts_render_config& cfg);
-void launch_tile_sort(Context& c, int tile_bits);
-void launch_ranges(Context& c, int n_tiles);
+void launch_tile_sort(Context& c, int tile_bits, bool key32);
+void launch_ranges(Context& c, int n_tiles, bool key32);
 // bucketed binning (k_bin.cu): returns I (syncs) and the longest tile list, -1 on OOM
 #ifndef TS_BIN_CHUNK
 #define TS_BIN_CHUNK 6144  // measured: 6144 beats 8192 (fewer same-address histogram REDs, fuller scatter waves)
@@ -181,6 +186,14 @@ void launch_exclusive_scan(Context& c, const uint32_t* in, const uint32_t* perm,
 
 template <class T>
 bool ensure(Context& c, DevBuf<T>& b, size_t n, bool keep = false);
+
+// Function attributes and __constant__ tables belong to a device context, and one
+// host thread per GPU may drive its own context concurrently: both helpers keep a
+// mutex-protected record per (key, device) instead of process-global flags.
+// set_func_attr: cudaFuncSetAttribute(fn, attr, value) once per device (retried
+// until it succeeds); first_on_device: true exactly once per (key, device).
+bool set_func_attr(const Context& c, const void* fn, cudaFuncAttribute attr, int value);
+bool first_on_device(const Context& c, const void* key);
 
 // ensure with 25% slack when the buffer has to grow (stores that grow step by step, e.g. by
 // densification, reallocate rarely)

@@ -50,6 +50,14 @@ def shard_bounds(length: int, world: int, rank: int, align: int = 4):
 
 
 class DataParallelStep:
+    """One data-parallel training step over a view batch (module docstring).
+
+    Stream contract: the collectives are issued on torch's current stream, so the
+    engine must run on that same stream (Engine(device, stream=torch.cuda.current_stream().cuda_stream)),
+    which orders backward -> collective -> optimizer without host waits; a different
+    engine stream is rejected.  The skip-invisible optimizer modes use each rank's
+    local visibility mask and are rejected for world > 1 (replicas would diverge)."""
+
     def __init__(self, engine, mode: str = "allreduce", group=None, chunks: int = 8):
         assert mode in ("allreduce", "sharded", "chunked")
         self.e = engine
@@ -58,6 +66,14 @@ class DataParallelStep:
         self.group = group
         self.world = dist.get_world_size(group) if dist.is_available() and dist.is_initialized() else 1
         self.rank = dist.get_rank(group) if self.world > 1 else 0
+        self._nccl = self.world > 1 and dist.get_backend(group) == "nccl"
+        self._padded_for = None   # N the padded flat buffers were reserved for (sharded mode)
+        es = getattr(engine, "stream", None)
+        if self.world > 1 and es is not None and torch.cuda.is_available():
+            cur = torch.cuda.current_stream(engine.device).cuda_stream
+            if int(es) != int(cur):
+                raise ValueError("DataParallelStep: the engine must run on torch's current stream "
+                                 "(collectives are ordered against it)")
 
     def my_views(self, n_views: int):
         """Views {r, r+G, ...} of an n_views batch (disjoint slices)."""
@@ -70,7 +86,17 @@ class DataParallelStep:
             self.e.training_loss(slot=slot, want_value=False)
             self.e.backward(None)
 
+    def _reserve_padded(self, per: int):
+        """Pad the flat parameter / gradient buffers to world * per once per store size
+        (one allocation + tail clear, not per step)."""
+        n = self.e.num_gaussians() if hasattr(self.e, "num_gaussians") else None
+        if self._padded_for != (n, per):
+            self.e.reserve_flat(per * self.world)
+            self._padded_for = (n, per)
+
     def exchange_and_step(self, adam):
+        if self.world > 1 and adam.mode in (2, 4):
+            raise ValueError("skip-invisible Adam uses the rank-local visibility mask: world size 1 only")
         if self.world == 1:
             self.e.adam_step(adam)
             return
@@ -89,17 +115,29 @@ class DataParallelStep:
                 w.wait()
                 self.e.adam_step(adam, begin=b, end=e)
             return
+        # sharded: reduce-scatter -> Adam on this rank's slice -> all-gather of the parameters.
+        # With NCCL both collectives run in place (the rank's slot of the padded buffer is the
+        # send / receive buffer); gloo gets a separate staging tensor.
         L = g.numel()
         b, e, per = shard_bounds(L, self.world, self.rank)
+        self._reserve_padded(per)
         padded = self.e.grad_tensor(padded_to=per * self.world)
-        out = torch.empty(per, dtype=padded.dtype, device=padded.device)
-        dist.reduce_scatter_tensor(out, padded, op=dist.ReduceOp.SUM, group=self.group)
-        padded[self.rank * per:(self.rank + 1) * per].copy_(out)
-        self.e.adam_step(adam, begin=b, end=e)
+        mine = padded[self.rank * per:(self.rank + 1) * per]
+        if self._nccl:
+            dist.reduce_scatter_tensor(mine, padded, op=dist.ReduceOp.SUM, group=self.group)
+        else:
+            out = torch.empty(per, dtype=padded.dtype, device=padded.device)
+            dist.reduce_scatter_tensor(out, padded, op=dist.ReduceOp.SUM, group=self.group)
+            mine.copy_(out)
+        a = type(adam).from_buffer_copy(adam) if hasattr(type(adam), "from_buffer_copy") else adam
+        a.zero_grads = 0
+        self.e.adam_step(a, begin=b, end=e)
         p = self.e.param_tensor(padded_to=per * self.world)
-        dist.all_gather_into_tensor(p, p[self.rank * per:(self.rank + 1) * per].clone(), group=self.group)
-        # slices of the other ranks' gradients were not consumed by this rank's Adam
-        self.e.zero_grads()
+        pm = p[self.rank * per:(self.rank + 1) * per]
+        dist.all_gather_into_tensor(p, pm if self._nccl else pm.clone(), group=self.group)
+        # the other ranks' slices still hold this rank's un-reduced gradients: the buffer is
+        # consumed, and the next backward overwrites every row instead of accumulating
+        self.e.mark_grads_consumed()
 
     def step(self, views, adam):
         self.accumulate(views)

@@ -111,6 +111,19 @@ def workload_cameras(w: Workload):
     return fibonacci_cameras(w.views, w.width, w.height)
 
 
+RING_VIEWS = 8  # training cameras of the benchmark's view ring
+
+
+def ring_camera(w: Workload, j: int, n_views: int = RING_VIEWS) -> Camera:
+    """Camera j of the benchmark's view ring: the headline view (j = 0, eye (0.3, -0.8, -3.5))
+    rotated by 360/n_views * j degrees about the scene's vertical axis.  Every view sees the
+    whole synthetic cube (same per-view workload)."""
+    base = np.array([0.3, -0.8, -3.5])
+    a = math.radians(360.0 / n_views * j)
+    R = np.array([[math.cos(a), 0, math.sin(a)], [0, 1, 0], [-math.sin(a), 0, math.cos(a)]])
+    return make_camera(w.width, w.height, tuple(R @ base))
+
+
 def scene_extent(cams) -> float:
     """1.1 x radius of the camera-centre bounding sphere; 1.0 for one camera."""
     if len(cams) <= 1:

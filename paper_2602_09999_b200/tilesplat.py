@@ -56,6 +56,7 @@ _SIGS = {
     "ts_loss": [_vp, _vp, _i32, _vp],
     "ts_backward": [_vp, _vp],
     "ts_zero_grads": [_vp],
+    "ts_mark_grads_consumed": [_vp],
     "ts_grad_buffer": [_vp, ctypes.POINTER(_vp), ctypes.POINTER(_i64)],
     "ts_param_buffer": [_vp, ctypes.POINTER(_vp), ctypes.POINTER(_i64)],
     "ts_stats_buffer": [_vp, ctypes.POINTER(_vp), ctypes.POINTER(_vp)],
@@ -135,6 +136,7 @@ class Engine:
                               "an sm_100 (B200) device is required; there is no CPU fallback")
         self._h = h
         self.device = device
+        self.stream = int(stream) if stream else None   # None: the context's own stream
         self.n = 0
         self._cam = None
 
@@ -220,6 +222,10 @@ class Engine:
 
     def zero_grads(self):
         self._check(self._L.ts_zero_grads(self._h), "ts_zero_grads")
+
+    def mark_grads_consumed(self):
+        """The next backward overwrites the gradient buffer (sharded data-parallel optimizer)."""
+        self._check(self._L.ts_mark_grads_consumed(self._h), "ts_mark_grads_consumed")
 
     def adam_step(self, cfg: AdamConfig, begin: int | None = None, end: int | None = None):
         if begin is None:

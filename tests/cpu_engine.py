@@ -33,6 +33,9 @@ class CpuEngine:
         return loss if want_value else None
 
     def backward(self, dl=None):
+        if getattr(self, "_stale", False):  # consumed buffer: overwrite instead of accumulating
+            self.G[:] = 0.0
+            self._stale = False
         cam, cfg = self._view
         G, _, a, c = O.backward(self.P[:self.L], self.n, cam, cfg, self._dl if dl is None else dl)
         self.G[:self.L] += G
@@ -53,6 +56,12 @@ class CpuEngine:
 
     def zero_grads(self):
         self.G[:] = 0.0
+
+    def mark_grads_consumed(self):
+        self._stale = True
+
+    def reserve_flat(self, min_len):
+        assert min_len <= self.cap
 
     def grad_tensor(self, padded_to=None):
         return torch.from_numpy(self.G[: (padded_to or self.L)])

@@ -139,3 +139,27 @@ def test_frame_beyond_bucketed_binning_uses_radix(engine):
     assert np.array_equal(gk, ok) and np.array_equal(gv, ov) and np.array_equal(gr, orr)
     orgb, _, ocnt, _ = O.render(p, n, cam, cfg)
     assert np.abs(rgb - orgb).max() <= IMG_TOL and np.array_equal(cnt, ocnt)
+
+
+def test_frame_over_65535_tiles_uses_32bit_tile_keys(engine):
+    """TileGrid: a 4200x4200 frame has 263 x 263 = 69169 tiles > 2^16, so the
+    tile keys switch to 32 bits (radix path: 3 tile passes); tile lists, sorted keys and ranges
+    stay bit-exact against the oracle, the image within 1e-4."""
+    n = 30_000
+    p = scene.random_params(n, 0.01, 0.0, 53)
+    cam = scene.make_camera(4200, 4200, eye=(0.1, -0.2, -2.0))   # the cube fills the frame
+    assert cam.n_tiles > 65535
+    cfg = T.RenderConfig.make(sh_degree=1)
+    engine.set_params(p, n)
+    rgb, Tf, cnt = engine.render(cam, cfg)
+    assert engine.binning_path() == "radix"
+    gk, gv, gr = engine.debug_instances()
+    ok, ov, orr, _ = O.instances(p, n, cam, cfg, sort="combined")
+    assert int(ok[-1] >> np.uint64(32)) > 65535   # instances in tiles beyond the 16-bit range
+    assert np.array_equal(gk, ok) and np.array_equal(gv, ov) and np.array_equal(gr, orr)
+    orgb, oT, ocnt, _ = O.render(p, n, cam, cfg)
+    assert np.abs(rgb - orgb).max() <= IMG_TOL and np.abs(Tf - oT).max() <= IMG_TOL
+    assert np.array_equal(cnt, ocnt)
+    # the two-stage oracle sort with 17-bit tile keys equals the combined 64-bit sort
+    k2, v2, r2, _ = O.instances(p, n, cam, cfg, sort="two_stage")
+    assert np.array_equal(k2, ok) and np.array_equal(v2, ov)

@@ -53,3 +53,35 @@ def test_fuzz_render_and_gradients(engine, seed):
         rms = np.sqrt(np.mean(o * o))
         frac = np.mean(np.abs(g - o) <= 1e-3 * np.maximum(np.abs(o), rms))
         assert frac >= 0.99, f"seed {seed} {nm}: {frac:.4f}"
+
+
+@pytest.mark.parametrize("dilation", [0.3, 0.0])
+def test_needles_row_cull_conservative(engine, dilation):
+    """High-aspect needles (2D variance up to ~1e5 px^2 along the long axis, sub-pixel across):
+    the blend kernels' per-warp row cull bounds each splat by the half-height of its
+    alpha >= tau ellipse computed from the rounded conic; it must never drop a fragment
+    the exact Q <= k2 test keeps (fp32 cancellation in A C - B^2)."""
+    rng = np.random.default_rng(77)
+    n = 600
+    p = scene.random_params(n, 0.01, 1.0, 78)
+    long_axis = np.log(rng.uniform(0.05, 1.5, n))
+    ls = np.stack([long_axis, np.full(n, np.log(2e-4)), np.full(n, np.log(2e-4))], 1)
+    p[3 * n:6 * n] = ls.astype(np.float32).ravel()
+    p[0:3 * n] = rng.uniform(-0.6, 0.6, 3 * n).astype(np.float32)
+    cam = scene.make_camera(640, 480, eye=(0.2, -0.3, -3.0))
+    cfg = T.RenderConfig.make(sh_degree=1, dilation=dilation)
+    engine.set_params(p, n)
+    rgb, Tf, cnt = engine.render(cam, cfg)
+    orgb, oT, ocnt, _ = O.render(p, n, cam, cfg)
+    assert np.abs(rgb - orgb).max() <= 1e-4 and np.abs(Tf - oT).max() <= 1e-4
+    assert np.array_equal(cnt, ocnt)
+    # the backward replays the same fragments: its colour / opacity 2D gradients (well conditioned,
+    # unlike the mean / conic ones of a needle, whose fp32 rounding cancels catastrophically)
+    # would lose every fragment a too-tight row cull dropped
+    dl = np.random.default_rng(79).normal(0, 1e-2, rgb.shape).astype(np.float32)
+    g2 = engine.debug_grad2d(dl)
+    _, o2, _, _ = O.backward(p, n, cam, cfg, dl)
+    for k, nm in ((5, "do"), (6, "dr"), (7, "dg"), (8, "db")):
+        g, o = g2[:, k].astype(np.float64), o2[:, k].astype(np.float64)
+        rms = np.sqrt(np.mean(o * o)) + 1e-30
+        assert np.mean(np.abs(g - o) <= 1e-3 * np.maximum(np.abs(o), rms)) >= 0.99, nm

@@ -44,7 +44,7 @@ def test_bad_camera(engine):
     bad.fx = 0.0
     with pytest.raises(ValidationError):
         engine.render(bad, cfg)
-    huge = scene.make_camera(16 * 300, 16 * 300)  # 90000 tiles > 65535 (16-bit tile keys)
+    huge = scene.make_camera(16 * 4100, 16 * 4100)  # >= 2^24 tiles (beyond the 32-bit key path's limit)
     with pytest.raises(ValidationError):
         engine.render(huge, cfg)
 

@@ -37,6 +37,7 @@ def _load():
         "tso_set_workers": (None, [ctypes.c_int]),
         "tso_get_workers": (ctypes.c_int, []),
         "tso_expf": (ctypes.c_float, [ctypes.c_float]),
+        "tso_cos2pi": (ctypes.c_float, [ctypes.c_float]),
         "tso_logf": (ctypes.c_float, [ctypes.c_float]),
         "tso_rotation_from_quaternion_f64": (ctypes.c_int, [f64p, f64p]),
         "tso_build_covariance3d_f64": (None, [f64p, f64p, f64p]),

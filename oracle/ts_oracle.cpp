@@ -1468,6 +1468,35 @@ static inline uint64_t mix64(uint64_t z) {
     z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
     return z ^ (z >> 31);
 }
+// cos(2 pi u), u in [0, 1): the device's cos2pi_det (ts_math.cuh) op for op
+static inline float cos2pi_det(float u) {
+    const float t = u * 4.0f;
+    const int q = int(t);
+    const float f = t - float(q);
+    const float th = f * 1.57079632679489662f;
+    const float x2 = th * th;
+    float c = -1.1470745597729725e-11f;
+    c = c * x2 + 2.08767569878681e-09f;
+    c = c * x2 + -2.755731922398589e-07f;
+    c = c * x2 + 2.48015873015873e-05f;
+    c = c * x2 + -1.388888888888889e-03f;
+    c = c * x2 + 4.1666666666666664e-02f;
+    c = c * x2 + -0.5f;
+    c = c * x2 + 1.0f;
+    float sn = -7.647163731819816e-13f;
+    sn = sn * x2 + 1.6059043836821613e-10f;
+    sn = sn * x2 + -2.505210838544172e-08f;
+    sn = sn * x2 + 2.755731922398589e-06f;
+    sn = sn * x2 + -1.984126984126984e-04f;
+    sn = sn * x2 + 8.333333333333333e-03f;
+    sn = sn * x2 + -0.16666666666666666f;
+    sn = sn * x2 + 1.0f;
+    sn = sn * th;
+    return q == 0 ? c : q == 1 ? -sn : q == 2 ? -c : sn;
+}
+
+extern "C" float tso_cos2pi(float u) { return cos2pi_det(u); }
+
 static inline float u01(uint64_t seed, int64_t iter, int64_t parent, int code) {
     uint64_t h = mix64(mix64(mix64(seed ^ mix64(uint64_t(iter))) ^ uint64_t(parent)) ^ uint64_t(code));
     return (float(h >> 40) + 0.5f) * 0x1.0p-24f;
@@ -1564,7 +1593,8 @@ int64_t tso_densify_and_prune(int64_t n, const float* P, const float* m, const f
             for (int a = 0; a < 3; ++a) {
                 float u1 = u01(seed, iter, g, child * 8 + a * 2);
                 float u2 = u01(seed, iter, g, child * 8 + a * 2 + 1);
-                zs[a] = std::sqrt(-2.0f * std::log(u1)) * std::cos(6.2831853071795865f * u2);
+                // Box-Muller with the deterministic log / cos of the device (bitwise equal children)
+                zs[a] = std::sqrt(-2.0f * soft_logf(u1)) * cos2pi_det(u2);
                 zs[a] *= soft_expf(ls[a]);
             }
             for (int i = 0; i < 3; ++i)

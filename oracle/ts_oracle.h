@@ -66,6 +66,7 @@ void tso_set_workers(int n);
 int tso_get_workers(void);
 
 /* deterministic scalar math shared with the product's numerics contract */
+float tso_cos2pi(float u);
 float tso_expf(float x);
 float tso_logf(float x);
 

@@ -63,61 +63,82 @@ __global__ void densify_flags_kernel(const float* __restrict__ P, const float* _
     if (pruned) atomicAdd(st + 2, pruned);
 }
 
-// One pass per array (WHICH 0 = parameters, 1 / 2 = first / second Adam moment) into a
-// fresh 59*NA buffer; every destination row is written exactly once (kept rows, clones,
-// split children), so the output needs no clear.
-template <int WHICH>
-__global__ void densify_scatter_kernel(const float* __restrict__ P, const float* __restrict__ S, int64_t N,
-                                       const uint32_t* __restrict__ fA, const uint32_t* __restrict__ fB,
-                                       const uint32_t* __restrict__ fC, const uint32_t* __restrict__ oA,
-                                       const uint32_t* __restrict__ oB, const uint32_t* __restrict__ oC, int64_t nA,
-                                       int64_t nB, int64_t NA, float* __restrict__ O, uint64_t seed, int64_t iter) {
-    const int64_t g = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (g >= N) return;
-    const Off so(N), d(NA);
-    const int64_t soff[6] = {so.means, so.ls, so.q, so.op, so.dc, so.rest};
-    const int64_t doff[6] = {d.means, d.ls, d.q, d.op, d.dc, d.rest};
-    const int width[6] = {3, 3, 4, 1, 3, 45};
-    auto copy_row = [&](int64_t r, bool moments) {
-        for (int k = 0; k < 6; ++k)
-            for (int j = 0; j < width[k]; ++j) {
-                const int64_t s = soff[k] + width[k] * g + j, t = doff[k] + width[k] * r + j;
-                O[t] = WHICH == 0 ? P[s] : (moments ? S[s] : 0.f);
-            }
-    };
-    if (fA[g]) copy_row(oA[g], true);
-    if (fB[g]) copy_row(nA + oB[g], false);
-    if (fC[g] && WHICH != 0) {
-        copy_row(nA + nB + oC[g], false);  // split children start with zero moments
-        copy_row(nA + nB + oC[g] + 1, false);
+// Element-parallel copy, one pass per array (WHICH 0 = parameters, 1 / 2 = first / second
+// Adam moment) into a fresh 59*NA buffer: thread i reads element i of the source store
+// (coalesced over every attribute block) and writes it to the rows of its Gaussian in the
+// compacted layout -- the kept row (runs of consecutive survivors stay coalesced), the clone
+// row and the two split-child rows (moments of new rows are zero).  Every
+// destination row is written exactly once, so the output needs no clear.
+template <int WD, int WHICH>
+__device__ __forceinline__ void copy_elem(float x, uint32_t r, uint32_t dbase, const uint32_t* __restrict__ fA,
+                                          const uint32_t* __restrict__ fB, const uint32_t* __restrict__ fC,
+                                          const uint32_t* __restrict__ oA, const uint32_t* __restrict__ oB,
+                                          const uint32_t* __restrict__ oC, uint32_t nA, uint32_t nB,
+                                          float* __restrict__ O) {
+    const uint32_t g = r / uint32_t(WD), j = r - g * uint32_t(WD);
+    if (__ldg(fA + g)) O[dbase + uint32_t(WD) * __ldg(oA + g) + j] = x;
+    const float y = WHICH == 0 ? x : 0.f;
+    if (__ldg(fB + g)) O[dbase + uint32_t(WD) * (nA + __ldg(oB + g)) + j] = y;
+    if (__ldg(fC + g)) {
+        const uint32_t c0 = nA + nB + __ldg(oC + g);
+        O[dbase + uint32_t(WD) * c0 + j] = y;        // children start as copies of the parent;
+        O[dbase + uint32_t(WD) * (c0 + 1) + j] = y;  // densify_children_kernel sets means / scales
     }
-    if (fC[g] && WHICH == 0) {
-        using namespace tsx;
-        const float* ls = P + so.ls + 3 * g;
-        float q[4] = {P[so.q + 4 * g], P[so.q + 4 * g + 1], P[so.q + 4 * g + 2], P[so.q + 4 * g + 3]};
-        const float qn = qnorm(q);
-        const float w = div(q[0], qn), x = div(q[1], qn), y = div(q[2], qn), z = div(q[3], qn);
-        const float R[9] = {sub(1.f, mul(2.f, add(mul(y, y), mul(z, z)))), mul(2.f, sub(mul(x, y), mul(w, z))),
-                            mul(2.f, add(mul(x, z), mul(w, y))),           mul(2.f, add(mul(x, y), mul(w, z))),
-                            sub(1.f, mul(2.f, add(mul(x, x), mul(z, z)))), mul(2.f, sub(mul(y, z), mul(w, x))),
-                            mul(2.f, sub(mul(x, z), mul(w, y))),           mul(2.f, add(mul(y, z), mul(w, x))),
-                            sub(1.f, mul(2.f, add(mul(x, x), mul(y, y))))};
-        for (int child = 0; child < 2; ++child) {
-            const int64_t r = nA + nB + oC[g] + child;
-            copy_row(r, false);
-            float zs[3];
-            for (int k = 0; k < 3; ++k) {
-                const float a1 = u01(seed, iter, g, child * 8 + k * 2);
-                const float a2 = u01(seed, iter, g, child * 8 + k * 2 + 1);
-                zs[k] = sqrtf(-2.0f * logf(a1)) * cospif(2.0f * a2);
-                zs[k] = mul(zs[k], expf_det(ls[k]));
-            }
-            for (int i = 0; i < 3; ++i)
-                O[d.means + 3 * r + i] =
-                    add(P[so.means + 3 * g + i], add(add(mul(R[3 * i], zs[0]), mul(R[3 * i + 1], zs[1])),
-                                                     mul(R[3 * i + 2], zs[2])));
-            for (int k = 0; k < 3; ++k) O[d.ls + 3 * r + k] = sub(ls[k], 0x1.e148a2p-2f);
+}
+
+template <int WHICH>
+__global__ void __launch_bounds__(256) densify_copy_kernel(const float* __restrict__ src, uint32_t N,
+                                                           const uint32_t* __restrict__ fA,
+                                                           const uint32_t* __restrict__ fB,
+                                                           const uint32_t* __restrict__ fC,
+                                                           const uint32_t* __restrict__ oA,
+                                                           const uint32_t* __restrict__ oB,
+                                                           const uint32_t* __restrict__ oC, uint32_t nA, uint32_t nB,
+                                                           uint32_t NA, float* __restrict__ O) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= 59u * N) return;
+    const float x = src[i];
+    if (i < 3u * N) copy_elem<3, WHICH>(x, i, 0u, fA, fB, fC, oA, oB, oC, nA, nB, O);
+    else if (i < 6u * N) copy_elem<3, WHICH>(x, i - 3u * N, 3u * NA, fA, fB, fC, oA, oB, oC, nA, nB, O);
+    else if (i < 10u * N) copy_elem<4, WHICH>(x, i - 6u * N, 6u * NA, fA, fB, fC, oA, oB, oC, nA, nB, O);
+    else if (i < 11u * N) copy_elem<1, WHICH>(x, i - 10u * N, 10u * NA, fA, fB, fC, oA, oB, oC, nA, nB, O);
+    else if (i < 14u * N) copy_elem<3, WHICH>(x, i - 11u * N, 11u * NA, fA, fB, fC, oA, oB, oC, nA, nB, O);
+    else copy_elem<45, WHICH>(x, i - 14u * N, 14u * NA, fA, fB, fC, oA, oB, oC, nA, nB, O);
+}
+
+// Split children: mean = parent mean + R (s * z), z ~ N(0, I) by Box-Muller from
+// a counter-based hash of (seed, iteration, parent, code), with the deterministic log / cos
+// (ts_math.cuh), so children equal the oracle's bit for bit; log-scales = parent - ln 1.6.
+__global__ void densify_children_kernel(const float* __restrict__ P, uint32_t N, const uint32_t* __restrict__ fC,
+                                        const uint32_t* __restrict__ oC, uint32_t nA, uint32_t nB, uint32_t NA,
+                                        float* __restrict__ O, uint64_t seed, int64_t iter) {
+    const uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= N || !fC[g]) return;
+    using namespace tsx;
+    const Off so(N), d(NA);
+    const float* ls = P + so.ls + 3 * int64_t(g);
+    float q[4] = {P[so.q + 4 * int64_t(g)], P[so.q + 4 * int64_t(g) + 1], P[so.q + 4 * int64_t(g) + 2],
+                  P[so.q + 4 * int64_t(g) + 3]};
+    const float qn = qnorm(q);
+    const float w = div(q[0], qn), x = div(q[1], qn), y = div(q[2], qn), z = div(q[3], qn);
+    const float R[9] = {sub(1.f, mul(2.f, add(mul(y, y), mul(z, z)))), mul(2.f, sub(mul(x, y), mul(w, z))),
+                        mul(2.f, add(mul(x, z), mul(w, y))),           mul(2.f, add(mul(x, y), mul(w, z))),
+                        sub(1.f, mul(2.f, add(mul(x, x), mul(z, z)))), mul(2.f, sub(mul(y, z), mul(w, x))),
+                        mul(2.f, sub(mul(x, z), mul(w, y))),           mul(2.f, add(mul(y, z), mul(w, x))),
+                        sub(1.f, mul(2.f, add(mul(x, x), mul(y, y))))};
+    for (int child = 0; child < 2; ++child) {
+        const int64_t r = int64_t(nA) + nB + oC[g] + child;
+        float zs[3];
+        for (int k = 0; k < 3; ++k) {
+            const float a1 = u01(seed, iter, g, child * 8 + k * 2);
+            const float a2 = u01(seed, iter, g, child * 8 + k * 2 + 1);
+            zs[k] = mul(sqrt_(mul(-2.0f, logf_det(a1))), cos2pi_det(a2));
+            zs[k] = mul(zs[k], expf_det(ls[k]));
         }
+        for (int i = 0; i < 3; ++i)
+            O[d.means + 3 * r + i] = add(P[so.means + 3 * int64_t(g) + i],
+                                         add(add(mul(R[3 * i], zs[0]), mul(R[3 * i + 1], zs[1])), mul(R[3 * i + 2], zs[2])));
+        for (int k = 0; k < 3; ++k) O[d.ls + 3 * r + k] = sub(ls[k], 0x1.e148a2p-2f);
     }
 }
 
@@ -166,15 +187,21 @@ int64_t launch_densify(Context& c, float thresh, float log_small, float log_big,
         if (!ensure_grow(c, c.spare, L)) return -1;
         if (N) {
             const float* src = *arrs[w];
-            if (w == 0)
-                densify_scatter_kernel<0><<<blocks, bs, 0, c.stream>>>(c.params.p, src, N, fA, fB, fC, oA, oB, oC, nA,
-                                                                      nB, NA, c.spare.p, seed, iter);
-            else if (w == 1)
-                densify_scatter_kernel<1><<<blocks, bs, 0, c.stream>>>(c.params.p, src, N, fA, fB, fC, oA, oB, oC, nA,
-                                                                      nB, NA, c.spare.p, seed, iter);
-            else
-                densify_scatter_kernel<2><<<blocks, bs, 0, c.stream>>>(c.params.p, src, N, fA, fB, fC, oA, oB, oC, nA,
-                                                                      nB, NA, c.spare.p, seed, iter);
+            const unsigned eb = unsigned((59 * N + 255) / 256);
+            const uint32_t n32 = uint32_t(N), a32 = uint32_t(nA), b32 = uint32_t(nB), NA32 = uint32_t(NA);
+            if (w == 0) {
+                densify_copy_kernel<0><<<eb, 256, 0, c.stream>>>(src, n32, fA, fB, fC, oA, oB, oC, a32, b32, NA32,
+                                                                 c.spare.p);
+                densify_children_kernel<<<blocks, bs, 0, c.stream>>>(src, n32, fC, oC, a32, b32, NA32, c.spare.p,
+                                                                     seed, iter);
+                TS_LAUNCHED(c);
+            } else if (w == 1) {
+                densify_copy_kernel<1><<<eb, 256, 0, c.stream>>>(src, n32, fA, fB, fC, oA, oB, oC, a32, b32, NA32,
+                                                                 c.spare.p);
+            } else {
+                densify_copy_kernel<2><<<eb, 256, 0, c.stream>>>(src, n32, fA, fB, fC, oA, oB, oC, a32, b32, NA32,
+                                                                 c.spare.p);
+            }
             TS_LAUNCHED(c);
         } else {
             cudaMemsetAsync(c.spare.p, 0, L * 4, c.stream);

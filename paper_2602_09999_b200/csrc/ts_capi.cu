@@ -12,6 +12,8 @@
 #include <tuple>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "ts_internal.cuh"
 
 using namespace ts;
@@ -113,7 +115,15 @@ ts_status validation(Context& c, const char* msg) {
 }
 
 
+// stage names of the NVTX ranges (nsys / ncu --nvtx) and of ts_stage_times
+const char* const kStageName[kNumStages] = {"preprocess", "depth_sort", "scan",      "duplicate",
+                                            "tile_sort",  "ranges",     "blend",     "loss",
+                                            "blend_bwd",  "project_bwd", "adam"};
+
+// Every stage is an NVTX range (header-only NVTX3: a no-op unless a tool is attached); with
+// profiling on it is also bracketed by CUDA events on the context stream.
 void stage_begin(Context& c, int k) {
+    nvtxRangePushA(kStageName[k]);
     if (!c.profiling) return;
     if (c.ev_cursor == c.ev_b.size()) {
         cudaEvent_t b, e;
@@ -127,8 +137,9 @@ void stage_begin(Context& c, int k) {
     cudaEventRecord(c.ev_b[c.ev_cursor], c.stream);
 }
 void stage_end(Context& c, int k) {
-    if (!c.profiling) return;
     (void)k;
+    nvtxRangePop();
+    if (!c.profiling) return;
     cudaEventRecord(c.ev_e[c.ev_cursor], c.stream);
     ++c.ev_cursor;
 }

@@ -1,8 +1,10 @@
 """The C++ multi-GPU host path (tools/ts_train_dp.cpp: one host thread per GPU, ncclCommInitAll,
 the exchange on each context's stream) in its three exchange modes.  On a 1-GPU box the
-communicator has one rank (loopback): the data-parallel step must leave the parameters bit for
-bit where the single-context step (views accumulated, then one Adam) does.  With >= 2 GPUs
-every replica must equal rank 0 bit for bit."""
+communicator has one rank (loopback).  Every step, the exchange + optimizer must leave the
+parameters and Adam moments bit for bit where a single-context ts_adam_step over the whole
+buffer does, given the same pre-step state and the batch gradient (views accumulated in the
+flat buffer; snapshotted, since the rendering gradients use fp32 atomics).  With 2 GPUs the
+same holds for the 2-rank sum, and every replica must equal rank 0 bit for bit."""
 import json
 import os
 import subprocess
@@ -30,7 +32,7 @@ def _run(g, mode, views=4):
 @pytest.mark.parametrize("mode", ["allreduce", "sharded", "chunked"])
 def test_cpp_dp_loopback_bitwise(mode):
     r = _run(1, mode)
-    assert r["gpus"] == 1 and r["replicas_bitwise_equal"] and r["check_mismatches"] == 0
+    assert r["gpus"] == 1 and r["replicas_bitwise_equal"] and r["check_mismatches"] == 0 and r["iters"] == 4
 
 
 @pytest.mark.parametrize("mode", ["allreduce", "sharded", "chunked"])
@@ -38,4 +40,4 @@ def test_cpp_dp_two_gpus(mode):
     if _gpus() < 2:
         pytest.skip("needs 2 GPUs")
     r = _run(2, mode)
-    assert r["gpus"] == 2 and r["replicas_bitwise_equal"]
+    assert r["gpus"] == 2 and r["replicas_bitwise_equal"] and r["check_mismatches"] == 0

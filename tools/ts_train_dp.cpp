@@ -17,11 +17,15 @@
 // These mirror paper_2602_09999_b200/dp.py (torch.distributed) one for one.
 //
 // usage: ts_train_dp <gpus> <allreduce|sharded|chunked> [n=20000] [iters=6] [views_per_step=4] [--check]
-// --check: after training, the same steps run in ONE context on GPU 0 (views
-// accumulated, then one Adam); with 1 GPU the parameters must match bit for bit,
-// with G > 1 every replica must equal rank 0 bit for bit (the view sum order
-// differs from the single context, so that comparison is only reported).  One JSON line;
-// exit codes 0 ok, 1 validation, 2 check failure, 3 CUDA / NCCL.
+// --check: every step, the exchange + optimizer is re-run in a separate single
+// context on GPU 0 from host snapshots: the pre-step parameters and moments, and
+// the batch gradient = sum of the ranks' accumulated gradient buffers (summed in
+// rank order; for G <= 2 that is NCCL's sum bit for bit, fp32 addition commutes).
+// The data-parallel step must leave rank 0's parameters and moments bitwise where
+// ts_adam_step over the whole buffer does (the rendering gradients themselves use
+// fp32 atomics and are not run-to-run deterministic, so they are snapshotted, not
+// recomputed).  Every replica must equal rank 0 bit for bit.  One JSON line; exit
+// codes 0 ok, 1 validation, 2 check failure, 3 CUDA / NCCL.
 #include <cuda_runtime.h>
 #include <nccl.h>
 
@@ -33,6 +37,8 @@
 #include <cstring>
 #include <random>
 #include <string>
+#include <condition_variable>
+#include <mutex>
 #include <thread>
 #include <vector>
 
@@ -104,12 +110,34 @@ std::vector<float> flat_of(const ParameterStore& s) {
 
 ts_camera to_c(const Camera& c) { return c.abi(); }
 
+// reusable barrier of the G rank threads (C++17)
+class Barrier {
+  public:
+    explicit Barrier(int n) : n_(n) {}
+    void wait() {
+        std::unique_lock<std::mutex> lk(mu_);
+        const int gen = gen_;
+        if (++count_ == n_) {
+            count_ = 0;
+            ++gen_;
+            cv_.notify_all();
+        } else {
+            cv_.wait(lk, [&] { return gen != gen_; });
+        }
+    }
+
+  private:
+    std::mutex mu_;
+    std::condition_variable cv_;
+    int n_, count_ = 0, gen_ = 0;
+};
+
 struct Rank {
     int dev = 0;
     cudaStream_t stream = nullptr;
     ts_ctx* ctx = nullptr;
     ncclComm_t comm = nullptr;
-    std::vector<float> final_params;
+    std::vector<float> final_params, gsnap;
     double ms = 0;
     std::string err;
     int code = 0;
@@ -172,6 +200,11 @@ int main(int argc, char** argv) {
     };
 
     std::vector<Rank> ranks(static_cast<size_t>(G));
+    Barrier bar(G);
+    int64_t mismatches = check ? 0 : -1;
+    double max_rel = 0;
+    ts_ctx* ref = nullptr;  // the single-context reference of --check (GPU 0)
+    std::vector<float> pre_p, pre_m, pre_v, post_p, post_m, post_v, gsum, rp, rm, rv;
     std::vector<int> devs(static_cast<size_t>(G));
     for (int r = 0; r < G; ++r) devs[size_t(r)] = r;
     std::vector<ncclComm_t> comms(static_cast<size_t>(G));
@@ -209,6 +242,15 @@ int main(int argc, char** argv) {
                     TS_OK_(ts_backward(c, nullptr));
                 }
                 ts_adam_config a = adam_config(it + 1, 1.0);
+                if (check) {  // snapshots before the exchange (every rank its gradient, rank 0 the state)
+                    R.gsnap.resize(size_t(L));
+                    TS_OK_(ts_get_state(c, R.gsnap.data(), nullptr, nullptr, nullptr, nullptr));
+                    if (r == 0) {
+                        pre_p.resize(size_t(L)), pre_m.resize(size_t(L)), pre_v.resize(size_t(L));
+                        TS_OK_(ts_get_params_flat(c, pre_p.data()));
+                        TS_OK_(ts_get_state(c, nullptr, pre_m.data(), pre_v.data(), nullptr, nullptr));
+                    }
+                }
                 float* gp = nullptr;
                 float* pp = nullptr;
                 int64_t cnt = 0;
@@ -236,6 +278,36 @@ int main(int argc, char** argv) {
                     NCCL_OK(ncclAllGather(pp + int64_t(r) * per, pp, size_t(per), ncclFloat, R.comm, R.stream));
                     TS_OK_(ts_mark_grads_consumed(c));
                 }
+                if (check) {
+                    if (r == 0) {
+                        post_p.resize(size_t(L)), post_m.resize(size_t(L)), post_v.resize(size_t(L));
+                        TS_OK_(ts_get_params_flat(c, post_p.data()));
+                        TS_OK_(ts_get_state(c, nullptr, post_m.data(), post_v.data(), nullptr, nullptr));
+                    }
+                    bar.wait();  // every rank's gradient snapshot is in
+                    if (r == 0) {
+                        gsum = ranks[0].gsnap;
+                        for (int q = 1; q < G; ++q)
+                            for (int64_t i = 0; i < L; ++i) gsum[size_t(i)] += ranks[size_t(q)].gsnap[size_t(i)];
+                        const ts_adam_config a_ref = adam_config(it + 1, 1.0);
+                        TS_OK_(ts_set_params_flat(ref, n, pre_p.data()));
+                        TS_OK_(ts_set_state(ref, gsum.data(), pre_m.data(), pre_v.data(), nullptr, nullptr));
+                        TS_OK_(ts_adam_step(ref, &a_ref));
+                        rp.resize(size_t(L)), rm.resize(size_t(L)), rv.resize(size_t(L));
+                        TS_OK_(ts_get_params_flat(ref, rp.data()));
+                        TS_OK_(ts_get_state(ref, nullptr, rm.data(), rv.data(), nullptr, nullptr));
+                        for (int64_t i = 0; i < L; ++i) {
+                            const size_t u = size_t(i);
+                            const bool same = std::memcmp(&rp[u], &post_p[u], 4) == 0 &&
+                                              std::memcmp(&rm[u], &post_m[u], 4) == 0 &&
+                                              std::memcmp(&rv[u], &post_v[u], 4) == 0;
+                            if (!same) ++mismatches;
+                            max_rel = std::max(max_rel, double(std::fabs(rp[u] - post_p[u])) /
+                                                            std::max(1e-6, double(std::fabs(rp[u]))));
+                        }
+                    }
+                    bar.wait();  // snapshots consumed before the next step overwrites them
+                }
             }
             CUDA_OK(cudaStreamSynchronize(R.stream));
             R.ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count() / iters;
@@ -246,6 +318,10 @@ int main(int argc, char** argv) {
             R.err = f.what + (R.ctx ? std::string(" (") + ts_last_error(R.ctx) + ")" : "");
         }
     };
+    if (check && (cudaSetDevice(0) != cudaSuccess || ts_create(0, nullptr, &ref) != TS_OK)) {
+        std::fprintf(stderr, "ts_train_dp: reference context\n");
+        return 3;
+    }
     std::vector<std::thread> th;
     for (int r = 0; r < G; ++r) th.emplace_back(rank_main, r);
     for (auto& t : th) t.join();
@@ -259,47 +335,8 @@ int main(int argc, char** argv) {
     for (int r = 1; r < G && rc == 0; ++r)
         replicas_equal &= std::memcmp(ranks[size_t(r)].final_params.data(), ranks[0].final_params.data(),
                                       size_t(L) * 4) == 0;
-    // single-context reference of the same steps (views accumulated, then one Adam)
-    int64_t mismatches = -1;
-    double max_rel = 0;
-    if (check && rc == 0) {
-        try {
-            ts_ctx* c = nullptr;
-            CUDA_OK(cudaSetDevice(0));
-            TS_OK_(ts_create(0, nullptr, &c));
-            TS_OK_(ts_set_params_flat(c, n, gt_flat.data()));
-            std::vector<float> img(size_t(W) * H * 3);
-            for (int v = 0; v < kViews; ++v) {
-                const ts_camera cc = to_c(cams[size_t(v)]);
-                TS_OK_(ts_forward(c, &cc, &cfg, img.data(), nullptr, nullptr));
-                TS_OK_(ts_set_target(c, v, W, H, img.data()));
-            }
-            TS_OK_(ts_set_params_flat(c, n, p0_flat.data()));
-            for (int it = 0; it < iters; ++it) {
-                for (int v : views_of(it, 1, 0)) {
-                    const ts_camera cc = to_c(cams[size_t(v)]);
-                    TS_OK_(ts_forward(c, &cc, &cfg, nullptr, nullptr, nullptr));
-                    TS_OK_(ts_loss(c, nullptr, v, nullptr));
-                    TS_OK_(ts_backward(c, nullptr));
-                }
-                const ts_adam_config a = adam_config(it + 1, 1.0);
-                TS_OK_(ts_adam_step(c, &a));
-            }
-            std::vector<float> ref(static_cast<size_t>(L));
-            TS_OK_(ts_get_params_flat(c, ref.data()));
-            ts_destroy(c);
-            mismatches = 0;
-            for (int64_t i = 0; i < L; ++i) {
-                const float x = ranks[0].final_params[size_t(i)], y = ref[size_t(i)];
-                if (std::memcmp(&x, &y, 4) != 0) ++mismatches;
-                max_rel = std::max(max_rel, double(std::fabs(x - y)) / std::max(1e-6, double(std::fabs(y))));
-            }
-            if (G == 1 && mismatches != 0) rc = 2;  // G > 1: the view sum order differs (reported only)
-        } catch (const Failure& f) {
-            std::fprintf(stderr, "ts_train_dp check: %s\n", f.what.c_str());
-            rc = f.code;
-        }
-    }
+    if (check && rc == 0 && G <= 2 && mismatches != 0) rc = 2;  // G > 2: ring sum order (reported only)
+    if (ref) ts_destroy(ref);
     if (!replicas_equal && rc == 0) rc = 2;
     double ms = 0;
     for (const Rank& R : ranks) ms = std::max(ms, R.ms);

@@ -94,20 +94,17 @@ float soft_expf(float x) {
     if (x > 88.72283935546875f) return INFINITY;
     if (x < -103.972084045410156f) return 0.0f;
     const float magic = 12582912.0f;  // 1.5 * 2^23
-    float t = x * 0x1.715476p+0f;
-    t = t + magic;
-    float n = t - magic;
-    float r = x - n * 0x1.63p-1f;
-    r = r - n * -0x1.bd0106p-13f;
+    const float t = std::fma(x, 0x1.715476p+0f, magic);
+    const float n = t - magic;
+    float r = std::fma(n, -0x1.63p-1f, x);
+    r = std::fma(n, 0x1.bd0106p-13f, r);
     float p = 0x1.a0d2cep-13f;
-    p = p * r + 0x1.6e879cp-10f;
-    p = p * r + 0x1.111210p-7f;
-    p = p * r + 0x1.555382p-5f;
-    p = p * r + 0x1.555554p-3f;
-    p = p * r + 0x1.0p-1f;
-    float rr = r * r;
-    p = p * rr;
-    p = p + r;
+    p = std::fma(p, r, 0x1.6e879cp-10f);
+    p = std::fma(p, r, 0x1.111210p-7f);
+    p = std::fma(p, r, 0x1.555382p-5f);
+    p = std::fma(p, r, 0x1.555554p-3f);
+    p = std::fma(p, r, 0x1.0p-1f);
+    p = std::fma(p, r * r, r);
     p = p + 1.0f;
     int ni = int(n);
     if (ni > 127) {
@@ -139,16 +136,19 @@ float soft_logf(float x) {
     k += int(ix >> 23) - 0x7f;
     ix = (ix & 0x007fffffu) + 0x3f3504f3u;
     x = f_from_bits(ix);
-    float f = x - 1.0f;
-    float s = f / (2.0f + f);
-    float z = s * s;
-    float w = z * z;
-    float t1 = w * (0x1.999c26p-2f + w * 0x1.f13c4cp-3f);
-    float t2 = z * (0x1.555554p-1f + w * 0x1.23d3dcp-2f);
-    float R = t2 + t1;
-    float hfsq = 0.5f * f * f;
-    float dk = float(k);
-    return s * (hfsq + R) + dk * 0x1.2fefa2p-17f - hfsq + f + dk * 0x1.62e3p-1f;
+    const float f = x - 1.0f;
+    const float s = f / (2.0f + f);
+    const float z = s * s;
+    const float w = z * z;
+    const float t1 = w * std::fma(w, 0x1.f13c4cp-3f, 0x1.999c26p-2f);
+    const float t2 = z * std::fma(w, 0x1.23d3dcp-2f, 0x1.555554p-1f);
+    const float R = t2 + t1;
+    const float hfsq = 0.5f * f * f;
+    const float dk = float(k);
+    float acc = std::fma(dk, 0x1.2fefa2p-17f, s * (hfsq + R));
+    acc = acc - hfsq;
+    acc = acc + f;
+    return std::fma(dk, 0x1.62e3p-1f, acc);
 }
 
 // scalar-type traits: float uses the deterministic soft exp/log on the binning path
@@ -321,18 +321,20 @@ GFwd<T> gaussian_forward(const T* P, int64_t N, int64_t g, const Cam<T>& cam, co
     const T* q = P + off.q + 4 * g;
     const T* W = cam.W;
     // project_mean (fixed order, no contraction)
-    F.xh = ((W[0] * mu[0] + W[1] * mu[1]) + W[2] * mu[2]) + W[3];
-    F.yh = ((W[4] * mu[0] + W[5] * mu[1]) + W[6] * mu[2]) + W[7];
-    F.zh = ((W[8] * mu[0] + W[9] * mu[1]) + W[10] * mu[2]) + W[11];
+    // project_mean: FMA chains, one rounding per step (the kernels' fma_ order)
+    F.xh = std::fma(W[2], mu[2], std::fma(W[1], mu[1], W[0] * mu[0])) + W[3];
+    F.yh = std::fma(W[6], mu[2], std::fma(W[5], mu[1], W[4] * mu[0])) + W[7];
+    F.zh = std::fma(W[10], mu[2], std::fma(W[9], mu[1], W[8] * mu[0])) + W[11];
     if (!(F.zh > cam.nearp)) return F;
     // rotation_from_quaternion (degenerate if ||q|| < 1e-4)
-    T qq = ((q[0] * q[0] + q[1] * q[1]) + q[2] * q[2]) + q[3] * q[3];
+    T qq = std::fma(q[3], q[3], std::fma(q[2], q[2], std::fma(q[1], q[1], q[0] * q[0])));
     F.qn = std::sqrt(qq);
     if (!(F.qn >= T(1e-4f))) return F;
-    F.qw = q[0] / F.qn;
-    F.qx = q[1] / F.qn;
-    F.qy = q[2] / F.qn;
-    F.qz = q[3] / F.qn;
+    const T rq = T(1) / F.qn;
+    F.qw = q[0] * rq;
+    F.qx = q[1] * rq;
+    F.qy = q[2] * rq;
+    F.qz = q[3] * rq;
     {
         T w = F.qw, x = F.qx, y = F.qy, z = F.qz;
         T xx = x * x, yy = y * y, zz = z * z, xy = x * y, xz = x * z, yz = y * z, wx = w * x, wy = w * y,
@@ -368,7 +370,7 @@ GFwd<T> gaussian_forward(const T* P, int64_t N, int64_t g, const Cam<T>& cam, co
         for (int k = 0; k < 3; ++k) F.Mm[3 * i + k] = F.R[3 * i + k] * F.s[k];
     const T* Mm = F.Mm;
     auto sdot = [&](int i, int j) {
-        return (Mm[3 * i] * Mm[3 * j] + Mm[3 * i + 1] * Mm[3 * j + 1]) + Mm[3 * i + 2] * Mm[3 * j + 2];
+        return std::fma(Mm[3 * i + 2], Mm[3 * j + 2], std::fma(Mm[3 * i + 1], Mm[3 * j + 1], Mm[3 * i] * Mm[3 * j]));
     };
     F.S[0] = sdot(0, 0);
     F.S[1] = sdot(0, 1);
@@ -377,46 +379,47 @@ GFwd<T> gaussian_forward(const T* P, int64_t N, int64_t g, const Cam<T>& cam, co
     F.S[4] = sdot(1, 2);
     F.S[5] = sdot(2, 2);
     // project_covariance with clamped ratios
-    F.txz = F.xh / F.zh;
-    F.tyz = F.yh / F.zh;
+    const T rz = T(1) / F.zh;
+    F.txz = F.xh * rz;
+    F.tyz = F.yh * rz;
     F.clx = (F.txz < -cam.limx) || (F.txz > cam.limx);
     F.cly = (F.tyz < -cam.limy) || (F.tyz > cam.limy);
     F.ux = F.txz < -cam.limx ? -cam.limx : (F.txz > cam.limx ? cam.limx : F.txz);
     F.uy = F.tyz < -cam.limy ? -cam.limy : (F.tyz > cam.limy ? cam.limy : F.tyz);
-    T tx = F.ux * F.zh, ty = F.uy * F.zh;
-    T zz2 = F.zh * F.zh;
-    F.J00 = cam.fx / F.zh;
-    F.J02 = -(cam.fx * tx) / zz2;
-    F.J11 = cam.fy / F.zh;
-    F.J12 = -(cam.fy * ty) / zz2;
+    // J = [[fx/z, 0, -fx u_x / z], [0, fy/z, -fy u_y / z]] (u = clamped x/z, y/z)
+    F.J00 = cam.fx * rz;
+    F.J02 = (-(cam.fx * F.ux)) * rz;
+    F.J11 = cam.fy * rz;
+    F.J12 = (-(cam.fy * F.uy)) * rz;
     for (int j = 0; j < 3; ++j) {
-        F.Tm[j] = F.J00 * W[j] + F.J02 * W[8 + j];
-        F.Tm[3 + j] = F.J11 * W[4 + j] + F.J12 * W[8 + j];
+        F.Tm[j] = std::fma(F.J02, W[8 + j], F.J00 * W[j]);
+        F.Tm[3 + j] = std::fma(F.J12, W[8 + j], F.J11 * W[4 + j]);
     }
     T Sf[9] = {F.S[0], F.S[1], F.S[2], F.S[1], F.S[3], F.S[4], F.S[2], F.S[4], F.S[5]};
     T U[6];
     for (int i = 0; i < 2; ++i)
         for (int j = 0; j < 3; ++j)
-            U[3 * i + j] = (F.Tm[3 * i] * Sf[j] + F.Tm[3 * i + 1] * Sf[3 + j]) + F.Tm[3 * i + 2] * Sf[6 + j];
-    T a = (U[0] * F.Tm[0] + U[1] * F.Tm[1]) + U[2] * F.Tm[2];
-    T b = (U[0] * F.Tm[3] + U[1] * F.Tm[4]) + U[2] * F.Tm[5];
-    T c = (U[3] * F.Tm[3] + U[4] * F.Tm[4]) + U[5] * F.Tm[5];
+            U[3 * i + j] = std::fma(F.Tm[3 * i + 2], Sf[6 + j], std::fma(F.Tm[3 * i + 1], Sf[3 + j], F.Tm[3 * i] * Sf[j]));
+    T a = std::fma(U[2], F.Tm[2], std::fma(U[1], F.Tm[1], U[0] * F.Tm[0]));
+    T b = std::fma(U[2], F.Tm[5], std::fma(U[1], F.Tm[4], U[0] * F.Tm[3]));
+    T c = std::fma(U[5], F.Tm[5], std::fma(U[4], F.Tm[4], U[3] * F.Tm[3]));
     // invert_cov2d with dilation; degenerate if det < 1e-6
-    const T det_pre = a * c - b * b;
+    const T det_pre = std::fma(a, c, -(b * b));
     T dil = T(cfg.dilation);
     a = a + dil;
     c = c + dil;
-    T det = a * c - b * b;
+    T det = std::fma(a, c, -(b * b));
     if (!(det >= T(1e-6f))) return F;
     F.a = a;
     F.b = b;
     F.c = c;
     F.det = det;
-    F.A = c / det;
-    F.B = (-b) / det;
-    F.C = a / det;
-    F.mx = cam.fx * F.txz + cam.cx;
-    F.my = cam.fy * F.tyz + cam.cy;
+    const T rdet = T(1) / det;
+    F.A = c * rdet;
+    F.B = (-b) * rdet;
+    F.C = a * rdet;
+    F.mx = std::fma(cam.fx, F.txz, cam.cx);
+    F.my = std::fma(cam.fy, F.tyz, cam.cy);
     // activate_opacity; AA compensation (SPEC.md:646-654 mip: sqrt(det_pre / det_post), detached)
     T logit = P[off.op + g];
     F.o_raw = T(1) / (T(1) + M<T>::exp_(-logit));

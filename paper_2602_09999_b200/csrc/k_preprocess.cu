@@ -71,16 +71,17 @@ __global__ void __launch_bounds__(kBlock) preprocess_kernel(
         const float* mus = sm + kMu + sh[0] + 3 * tid;
         const float m0 = mus[0], m1 = mus[1], m2 = mus[2];
         // project_mean, fixed order (depth feeds the sort key)
-        const float xh = add(add(add(mul(W[0], m0), mul(W[1], m1)), mul(W[2], m2)), W[3]);
-        const float yh = add(add(add(mul(W[4], m0), mul(W[5], m1)), mul(W[6], m2)), W[7]);
-        zh = add(add(add(mul(W[8], m0), mul(W[9], m1)), mul(W[10], m2)), W[11]);
+        const float xh = add(fma_(W[2], m2, fma_(W[1], m1, mul(W[0], m0))), W[3]);
+        const float yh = add(fma_(W[6], m2, fma_(W[5], m1, mul(W[4], m0))), W[7]);
+        zh = add(fma_(W[10], m2, fma_(W[9], m1, mul(W[8], m0))), W[11]);
         if (!(zh > cam.nearp)) break;
         const float* qs = sm + kQ + sh[2] + 4 * tid;
         const float4 qv = make_float4(qs[0], qs[1], qs[2], qs[3]);
-        const float qq = add(add(add(mul(qv.x, qv.x), mul(qv.y, qv.y)), mul(qv.z, qv.z)), mul(qv.w, qv.w));
+        const float qq = fma_(qv.w, qv.w, fma_(qv.z, qv.z, fma_(qv.y, qv.y, mul(qv.x, qv.x))));
         const float qn = sqrt_(qq);
         if (!(qn >= 1e-4f)) break;
-        const float w = div(qv.x, qn), x = div(qv.y, qn), y = div(qv.z, qn), z = div(qv.w, qn);
+        const float rq = div(1.f, qn);
+        const float w = mul(qv.x, rq), x = mul(qv.y, rq), y = mul(qv.z, rq), z = mul(qv.w, rq);
         float R[9];
         {
             const float xx = mul(x, x), yy = mul(y, y), zz = mul(z, z), xy = mul(x, y), xz = mul(x, z),
@@ -120,26 +121,24 @@ __global__ void __launch_bounds__(kBlock) preprocess_kernel(
 #pragma unroll
             for (int k = 0; k < 3; ++k) Mm[3 * i + k] = mul(R[3 * i + k], sc[k]);
         auto sdot = [&](int i, int j) {
-            return add(add(mul(Mm[3 * i], Mm[3 * j]), mul(Mm[3 * i + 1], Mm[3 * j + 1])),
-                       mul(Mm[3 * i + 2], Mm[3 * j + 2]));
+            return fma_(Mm[3 * i + 2], Mm[3 * j + 2], fma_(Mm[3 * i + 1], Mm[3 * j + 1], mul(Mm[3 * i], Mm[3 * j])));
         };
         const float S00 = sdot(0, 0), S01 = sdot(0, 1), S02 = sdot(0, 2), S11 = sdot(1, 1), S12 = sdot(1, 2),
                     S22 = sdot(2, 2);
         // project_covariance with clamped ratios
-        const float limx = mul(1.3f, div(mul(0.5f, float(cam.w)), cam.fx));
-        const float limy = mul(1.3f, div(mul(0.5f, float(cam.h)), cam.fy));
-        const float txz = div(xh, zh), tyz = div(yh, zh);
+        const float limx = cam.limx, limy = cam.limy;
+        const float rz = div(1.f, zh);
+        const float txz = mul(xh, rz), tyz = mul(yh, rz);
         const float ux = txz < -limx ? -limx : (txz > limx ? limx : txz);
         const float uy = tyz < -limy ? -limy : (tyz > limy ? limy : tyz);
-        const float tx = mul(ux, zh), ty = mul(uy, zh);
-        const float zz2 = mul(zh, zh);
-        const float J00 = div(cam.fx, zh), J02 = div(-mul(cam.fx, tx), zz2);
-        const float J11 = div(cam.fy, zh), J12 = div(-mul(cam.fy, ty), zz2);
+        // J = [[fx/z, 0, -fx u_x / z], [0, fy/z, -fy u_y / z]] (u = clamped x/z, y/z)
+        const float J00 = mul(cam.fx, rz), J02 = mul(-mul(cam.fx, ux), rz);
+        const float J11 = mul(cam.fy, rz), J12 = mul(-mul(cam.fy, uy), rz);
         float Tm[6];
 #pragma unroll
         for (int j = 0; j < 3; ++j) {
-            Tm[j] = add(mul(J00, W[j]), mul(J02, W[8 + j]));
-            Tm[3 + j] = add(mul(J11, W[4 + j]), mul(J12, W[8 + j]));
+            Tm[j] = fma_(J02, W[8 + j], mul(J00, W[j]));
+            Tm[3 + j] = fma_(J12, W[8 + j], mul(J11, W[4 + j]));
         }
         const float Sf[9] = {S00, S01, S02, S01, S11, S12, S02, S12, S22};
         float U[6];
@@ -147,19 +146,19 @@ __global__ void __launch_bounds__(kBlock) preprocess_kernel(
         for (int i = 0; i < 2; ++i)
 #pragma unroll
             for (int j = 0; j < 3; ++j)
-                U[3 * i + j] =
-                    add(add(mul(Tm[3 * i], Sf[j]), mul(Tm[3 * i + 1], Sf[3 + j])), mul(Tm[3 * i + 2], Sf[6 + j]));
-        float a = add(add(mul(U[0], Tm[0]), mul(U[1], Tm[1])), mul(U[2], Tm[2]));
-        const float b = add(add(mul(U[0], Tm[3]), mul(U[1], Tm[4])), mul(U[2], Tm[5]));
-        float c = add(add(mul(U[3], Tm[3]), mul(U[4], Tm[4])), mul(U[5], Tm[5]));
+                U[3 * i + j] = fma_(Tm[3 * i + 2], Sf[6 + j], fma_(Tm[3 * i + 1], Sf[3 + j], mul(Tm[3 * i], Sf[j])));
+        float a = fma_(U[2], Tm[2], fma_(U[1], Tm[1], mul(U[0], Tm[0])));
+        const float b = fma_(U[2], Tm[5], fma_(U[1], Tm[4], mul(U[0], Tm[3])));
+        float c = fma_(U[5], Tm[5], fma_(U[4], Tm[4], mul(U[3], Tm[3])));
         // invert_cov2d with dilation
-        const float det_pre = sub(mul(a, c), mul(b, b));
+        const float det_pre = fma_(a, c, -mul(b, b));
         a = add(a, cfg.dilation);
         c = add(c, cfg.dilation);
-        const float det = sub(mul(a, c), mul(b, b));
+        const float det = fma_(a, c, -mul(b, b));
         if (!(det >= 1e-6f)) break;
-        const float A = div(c, det), B = div(-b, det), C = div(a, det);
-        const float mx = add(mul(cam.fx, txz), cam.cx), my = add(mul(cam.fy, tyz), cam.cy);
+        const float rdet = div(1.f, det);
+        const float A = mul(c, rdet), B = mul(-b, rdet), C = mul(a, rdet);
+        const float mx = fma_(cam.fx, txz, cam.cx), my = fma_(cam.fy, tyz, cam.cy);
         // activate_opacity; alpha level set Q <= k2  <=>  o exp(-Q/2) >= tau
         const float logit = sm[kOp + sh[3] + tid];
         const float o_raw = div(1.f, add(1.f, expf_det(-logit)));

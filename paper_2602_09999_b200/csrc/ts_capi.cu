@@ -182,6 +182,12 @@ DevCam make_devcam(const ts_camera& cam) {
     d.h = cam.height;
     d.tiles_x = (cam.width + 15) / 16;
     d.tiles_y = (cam.height + 15) / 16;
+    // SPEC.md:169 clamp limits, once per camera; volatile keeps each fp32 op separately rounded
+    // in this order (the oracle's Cam: 1.3f * ((0.5f * w) / fx))
+    volatile float hw = 0.5f * float(cam.width), hh = 0.5f * float(cam.height);
+    volatile float qx = hw / cam.fx, qy = hh / cam.fy;
+    d.limx = 1.3f * qx;
+    d.limy = 1.3f * qy;
     return d;
 }
 

@@ -32,6 +32,7 @@ struct DevCam {
     float W[16];
     float fx, fy, cx, cy, nearp;
     int w, h, tiles_x, tiles_y;
+    float limx, limy;  // J ratio clamps 1.3 * (0.5 w / fx), 1.3 * (0.5 h / fy) (host float, the oracle's Cam op order)
 };
 
 template <class T>

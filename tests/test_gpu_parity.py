@@ -485,7 +485,7 @@ def test_opacity_reset_matches_oracle(engine):
     p = scene.random_params(n, 0.02, 0.0, 71)
     lmax = np.float32(np.log(0.01 / 0.99))
     op = p[10 * n:11 * n]
-    op[:5] = [lmax, np.nextafter(lmax, np.float32(1)), np.nextafter(lmax, np.float32(-1)), 9.0, -9.0]
+    op[:5] = [lmax, np.nextafter(lmax, np.float32(1)), np.nextafter(lmax, np.float32(-10)), 9.0, -9.0]
     engine.set_params(p, n)
     engine.opacity_reset()
     g = engine.get_params()

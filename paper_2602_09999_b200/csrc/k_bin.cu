@@ -212,21 +212,31 @@ constexpr size_t tile_sort_smem(int cap) { return size_t(cap) * 8 + (size_t(cap)
 
 // SEG: CTA blockIdx.x sorts segment (blockIdx.x & 3) of length <= CAP of long tile
 // tiles[blockIdx.x >> 2], in place (every element is loaded before any is written)
-template <int CAP, int NT, bool SEG = false>
-__global__ void __launch_bounds__(NT) tile_sort_kernel(const uint32_t* __restrict__ starts,
-                                                       const uint32_t* __restrict__ in,
-                                                       const uint32_t* __restrict__ dkey, uint32_t* __restrict__ out,
-                                                       const uint32_t* __restrict__ tiles) {
+// (offset, count) of size class `cls` inside the tile order (descending list length:
+// classes 6, 4, 3, 5, 2, 1, 0) from the class counts meta[0..6] written by bin_colscan
+__device__ __forceinline__ void class_range(const uint32_t* __restrict__ meta, int cls, uint32_t* off, uint32_t* n) {
+    const int seq[7] = {6, 4, 3, 5, 2, 1, 0};
+    uint32_t o = 0;
+#pragma unroll
+    for (int k = 0; k < 7; ++k) {
+        if (seq[k] == cls) break;
+        o += meta[seq[k]];
+    }
+    *off = o;
+    *n = meta[cls];
+}
+
+template <int CAP, int NT, bool SEG>
+__device__ __forceinline__ void tile_sort_one(uint32_t t, int seg, const uint32_t* __restrict__ starts,
+                                              const uint32_t* __restrict__ in, const uint32_t* __restrict__ dkey,
+                                              uint32_t* __restrict__ out, uint32_t* sm) {
     constexpr int R = CAP / NT;
     constexpr int NB = CAP / TS_SORT_BDIV;  // bucket counters (buckets = L / TS_SORT_BDIV)
-    extern __shared__ uint32_t sm[];
     uint32_t* skey = sm;
     uint32_t* sgid = sm + CAP;
     uint32_t* cnt = sm + 2 * CAP;
     __shared__ uint32_t s_min, s_max;
     __shared__ uint32_t s_wsum[32];
-    const uint32_t t = tiles[SEG ? blockIdx.x >> 2 : blockIdx.x];
-    const int seg = SEG ? int(blockIdx.x & 3) : 0;
     const uint32_t b = starts[t] + uint32_t(seg * CAP);
     const int L = SEG ? min(CAP, int(starts[t + 1] - starts[t]) - seg * CAP) : int(starts[t + 1] - b);
     if (SEG && L <= 0) return;
@@ -337,6 +347,27 @@ __global__ void __launch_bounds__(NT) tile_sort_kernel(const uint32_t* __restric
     }
 }
 
+// One CTA per unit (a tile list, or for SEG one of the 4 segments of a long list), grid-stride:
+// units u = blockIdx.x, blockIdx.x + gridDim.x, ... of the class.  meta == nullptr: the host
+// passes the class's tile list and count; otherwise (graph-captured step) both come from the
+// device-side class counts, so the grid is a fixed resident-size grid.
+template <int CAP, int NT, bool SEG = false>
+__global__ void __launch_bounds__(NT) tile_sort_kernel(const uint32_t* __restrict__ starts,
+                                                       const uint32_t* __restrict__ in,
+                                                       const uint32_t* __restrict__ dkey, uint32_t* __restrict__ out,
+                                                       const uint32_t* __restrict__ tiles, uint32_t n_host,
+                                                       const uint32_t* __restrict__ meta, int cls) {
+    extern __shared__ uint32_t sm[];
+    uint32_t off = 0, n = n_host;
+    if (meta) class_range(meta, cls, &off, &n);
+    const uint32_t units = SEG ? 4u * n : n;
+    for (uint32_t u = blockIdx.x; u < units; u += gridDim.x) {
+        const uint32_t t = tiles[off + (SEG ? u >> 2 : u)];
+        tile_sort_one<CAP, NT, SEG>(t, SEG ? int(u & 3u) : 0, starts, in, dkey, out, sm);
+        __syncthreads();  // shared memory reused by the next unit
+    }
+}
+
 // Merge level of a long tile list: sorted runs of length RL pair up into runs of 2 RL
 // (run 2p with run 2p + 1; an absent partner is an empty run), src -> dst at the same
 // offsets.  Merge path: each thread finds how many of its first output's predecessors come
@@ -347,12 +378,9 @@ __device__ __forceinline__ bool key_less(uint32_t a, uint32_t b, const uint32_t*
     return ka < kb || (ka == kb && a < b);
 }
 
-__global__ void __launch_bounds__(kMergeT) merge_level_kernel(const uint32_t* __restrict__ starts,
-                                                             const uint32_t* __restrict__ tiles,
-                                                             const uint32_t* __restrict__ src,
-                                                             uint32_t* __restrict__ dst,
-                                                             const uint32_t* __restrict__ dkey, int RL) {
-    const uint32_t t = tiles[blockIdx.y];
+__device__ __forceinline__ void merge_one(uint32_t t, const uint32_t* __restrict__ starts,
+                                          const uint32_t* __restrict__ src, uint32_t* __restrict__ dst,
+                                          const uint32_t* __restrict__ dkey, int RL) {
     const uint32_t b = starts[t];
     const int Ltot = int(starts[t + 1] - b);
     const int o0 = (blockIdx.x * kMergeT + threadIdx.x) * kMergePer;
@@ -377,6 +405,17 @@ __global__ void __launch_bounds__(kMergeT) merge_level_kernel(const uint32_t* __
     }
 }
 
+__global__ void __launch_bounds__(kMergeT) merge_level_kernel(const uint32_t* __restrict__ starts,
+                                                             const uint32_t* __restrict__ tiles,
+                                                             const uint32_t* __restrict__ src,
+                                                             uint32_t* __restrict__ dst,
+                                                             const uint32_t* __restrict__ dkey, int RL,
+                                                             uint32_t n_host, const uint32_t* __restrict__ meta) {
+    uint32_t off = 0, n = n_host;
+    if (meta) class_range(meta, 6, &off, &n);
+    for (uint32_t y = blockIdx.y; y < n; y += gridDim.y) merge_one(tiles[off + y], starts, src, dst, dkey, RL);
+}
+
 // Blend order of the tiles: longest lists first (a one-CTA counting sort of the tiles on
 // length / kOW, descending), so the long-running blend CTAs start in the first
 // wave instead of forming the kernel's tail.  Order inside a bin is arbitrary.
@@ -392,9 +431,28 @@ __device__ __forceinline__ uint32_t order_key(uint32_t L) {
 }
 
 // lens == nullptr: lengths from the tile ranges; else lens[t] (the forward's processed lengths)
-__global__ void __launch_bounds__(1024) tile_order_kernel(const uint32_t* __restrict__ starts,
+// gflag != nullptr (graph-captured step, forward order only): the step's capacity check.  If the
+// sticky overflow flag is already set, or the lists need more than capI slots or a list is longer
+// than kCapL (the host-side paths would reallocate / take the radix sort), the flag is set and
+// the view is emptied -- every tile range (starts) and class count zeroed, order = identity -- so
+// every later kernel of the step is a no-op on valid memory and K9 / Adam skip on the flag; the
+// host replays the step outside the graph (ts_capi.cu graph_settle).
+__global__ void __launch_bounds__(1024) tile_order_kernel(uint32_t* __restrict__ starts,
                                                           const uint32_t* __restrict__ lens, int Tn,
-                                                          uint32_t* __restrict__ order) {
+                                                          uint32_t* __restrict__ order, uint32_t* __restrict__ gflag,
+                                                          uint32_t capI, uint32_t* __restrict__ meta) {
+    if (gflag) {
+        __shared__ int s_bad;
+        if (threadIdx.x == 0) s_bad = (*gflag != 0u) || starts[Tn] > capI || meta[7] > uint32_t(kCapL);
+        __syncthreads();
+        if (s_bad) {
+            for (int t = threadIdx.x; t <= Tn; t += 1024) starts[t] = 0u;
+            for (int t = threadIdx.x; t < Tn; t += 1024) order[t] = uint32_t(t);
+            if (threadIdx.x < 8) meta[threadIdx.x] = 0u;
+            if (threadIdx.x == 0) *gflag = 1u;
+            return;
+        }
+    }
     __shared__ uint32_t hist[kOB];
     for (int i = threadIdx.x; i < kOB; i += 1024) hist[i] = 0;
     __syncthreads();
@@ -424,11 +482,14 @@ __global__ void __launch_bounds__(1024) tile_order_kernel(const uint32_t* __rest
 
 // lists of one instance need no sort: copy
 __global__ void tile_copy_single_kernel(const uint32_t* __restrict__ starts, const uint32_t* __restrict__ in,
-                                        uint32_t* __restrict__ out, const uint32_t* __restrict__ tiles, int n) {
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    const uint32_t b = starts[tiles[i]];
-    out[b] = in[b];
+                                        uint32_t* __restrict__ out, const uint32_t* __restrict__ tiles, uint32_t n_host,
+                                        const uint32_t* __restrict__ meta) {
+    uint32_t off = 0, n = n_host;
+    if (meta) class_range(meta, 0, &off, &n);
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const uint32_t b = starts[tiles[off + i]];
+        out[b] = in[b];
+    }
 }
 
 }  // namespace
@@ -471,13 +532,17 @@ bool launch_bin_count(Context& c, const DevCam& cam, const ts_render_config& cfg
 
 void launch_tile_order(Context& c, int Tn) {
     if (!ensure(c, c.tile_order, size_t(Tn))) return;
-    tile_order_kernel<<<1, 1024, 0, c.stream>>>(c.starts.p, nullptr, Tn, c.tile_order.p);
+    // graph-captured step: the capacity check of the step runs here (see tile_order_kernel)
+    const uint32_t capI = uint32_t(std::min<size_t>(c.ival[1].cap, c.ival[0].cap));
+    tile_order_kernel<<<1, 1024, 0, c.stream>>>(c.starts.p, nullptr, Tn, c.tile_order.p,
+                                                c.gmode ? c.counters.p + kGraphFlag : nullptr, capI,
+                                                c.bintot.p + Tn);
     TS_LAUNCHED(c);
 }
 
 void launch_bwd_tile_order(Context& c, int Tn) {
     if (!c.tile_proc.p || !ensure(c, c.bwd_order, size_t(Tn))) return;
-    tile_order_kernel<<<1, 1024, 0, c.stream>>>(c.starts.p, c.tile_proc.p, Tn, c.bwd_order.p);
+    tile_order_kernel<<<1, 1024, 0, c.stream>>>(c.starts.p, c.tile_proc.p, Tn, c.bwd_order.p, nullptr, 0u, nullptr);
     TS_LAUNCHED(c);
 }
 
@@ -500,35 +565,50 @@ void launch_bin_scatter(Context& c, const DevCam& cam, const ts_render_config& c
     TS_LAUNCHED(c);
 }
 
+// one size class: host mode launches exactly the class's tiles (count known on the host);
+// graph mode a resident-size grid that walks the device-side class count (grid-stride)
 template <int CAP, int NT, bool SEG = false>
-static void sort_variant(Context& c, const uint32_t* tiles, uint32_t n, cudaStream_t st) {
-    if (!n) return;
+static void sort_variant(Context& c, const uint32_t* tiles, uint32_t n, cudaStream_t st, int cls) {
+    if (!c.gmode && !n) return;
     set_func_attr(c, reinterpret_cast<const void*>(tile_sort_kernel<CAP, NT, SEG>),
                   cudaFuncAttributeMaxDynamicSharedMemorySize, int(tile_sort_smem(CAP)));
+    const size_t smem = tile_sort_smem(CAP);
+    unsigned grid = SEG ? 4 * n : n;
+    if (c.gmode) {
+        const int per_sm = std::max<int>(1, std::min<int>(2048 / NT, int((227 * 1024) / (smem + 1024))));
+        grid = unsigned(c.sm_count * per_sm);
+    }
     // segments sort in place in the scatter output; whole lists go to the final list buffer
-    tile_sort_kernel<CAP, NT, SEG><<<SEG ? 4 * n : n, NT, tile_sort_smem(CAP), st>>>(
-        c.starts.p, c.ival[1].p, c.dkey[0].p, SEG ? c.ival[1].p : c.ival[0].p, tiles);
+    tile_sort_kernel<CAP, NT, SEG><<<grid, NT, smem, st>>>(c.starts.p, c.ival[1].p, c.dkey[0].p,
+                                                           SEG ? c.ival[1].p : c.ival[0].p, tiles, n,
+                                                           c.gmode ? c.bintot.p + c.cur_tn : nullptr, cls);
     TS_LAUNCHED(c);
 }
 
 void launch_tile_depth_sort(Context& c, int Tn, uint32_t max_len) {
     (void)max_len;
-    if (c.I == 0) return;
+    if (!c.gmode && c.I == 0) return;
+    c.cur_tn = Tn;
     // the size classes are contiguous ranges of the tile order (descending list length), so
-    // every class kernel also starts with its longest lists; c.tile_order is built first
+    // every class kernel also starts with its longest lists; c.tile_order is built first.
+    // Host mode: class offsets from the host-read class counts; graph mode: each kernel
+    // derives them from the device-side counts (class_range)
     const uint32_t* ord = c.tile_order.p;
-    uint32_t off[7];
-    off[6] = 0;
-    off[4] = off[6] + c.bin_class[6];
-    off[3] = off[4] + c.bin_class[4];
-    off[5] = off[3] + c.bin_class[3];
-    off[2] = off[5] + c.bin_class[5];
-    off[1] = off[2] + c.bin_class[2];
-    off[0] = off[1] + c.bin_class[1];
-    (void)Tn;
-    if (c.bin_class[0]) {
-        tile_copy_single_kernel<<<(c.bin_class[0] + 255) / 256, 256, 0, c.stream>>>(c.starts.p, c.ival[1].p,
-                                                                                  c.ival[0].p, ord + off[0], int(c.bin_class[0]));
+    const uint32_t* meta = c.gmode ? c.bintot.p + Tn : nullptr;
+    uint32_t off[7] = {0, 0, 0, 0, 0, 0, 0};
+    if (!c.gmode) {
+        off[6] = 0;
+        off[4] = off[6] + c.bin_class[6];
+        off[3] = off[4] + c.bin_class[4];
+        off[5] = off[3] + c.bin_class[3];
+        off[2] = off[5] + c.bin_class[5];
+        off[1] = off[2] + c.bin_class[2];
+        off[0] = off[1] + c.bin_class[1];
+    }
+    if (c.gmode || c.bin_class[0]) {
+        const unsigned grid = c.gmode ? unsigned(c.sm_count) : (c.bin_class[0] + 255) / 256;
+        tile_copy_single_kernel<<<grid, 256, 0, c.stream>>>(c.starts.p, c.ival[1].p, c.ival[0].p, ord + off[0],
+                                                            c.bin_class[0], meta);
         TS_LAUNCHED(c);
     }
     // the size classes are independent: the two largest run on fork streams so their
@@ -543,21 +623,22 @@ void launch_tile_depth_sort(Context& c, int Tn, uint32_t max_len) {
     cudaEventRecord(c.fork_ev, c.stream);
     cudaStreamWaitEvent(c.side[0], c.fork_ev, 0);
     cudaStreamWaitEvent(c.side[1], c.fork_ev, 0);
-    sort_variant<kCap2, 512>(c, ord + off[3], c.bin_class[3], c.side[0]);
-    if (c.bin_class[6]) {  // lists longer than kCap3: 4 sorted segments, then 2 merge levels
+    sort_variant<kCap2, 512>(c, ord + off[3], c.bin_class[3], c.side[0], 3);
+    if (c.gmode || c.bin_class[6]) {  // lists longer than kCap3: 4 sorted segments, then 2 merge levels
         const uint32_t* lt = ord + off[6];
-        sort_variant<kCap3, 1024, true>(c, lt, c.bin_class[6], c.side[0]);
+        sort_variant<kCap3, 1024, true>(c, lt, c.bin_class[6], c.side[0], 6);
         // c.sortmp holds >= I entries (run_forward sizes it before the fork)
-        const dim3 g(kCapL / (kMergeT * kMergePer), c.bin_class[6]);
-        merge_level_kernel<<<g, kMergeT, 0, c.side[0]>>>(c.starts.p, lt, c.ival[1].p, c.sortmp.p, c.dkey[0].p, kCap3);
+        const dim3 g(kCapL / (kMergeT * kMergePer), c.gmode ? 64u : c.bin_class[6]);
+        merge_level_kernel<<<g, kMergeT, 0, c.side[0]>>>(c.starts.p, lt, c.ival[1].p, c.sortmp.p, c.dkey[0].p, kCap3,
+                                                        c.bin_class[6], meta);
         merge_level_kernel<<<g, kMergeT, 0, c.side[0]>>>(c.starts.p, lt, c.sortmp.p, c.ival[0].p, c.dkey[0].p,
-                                                        2 * kCap3);
+                                                        2 * kCap3, c.bin_class[6], meta);
         c.launches += 2;
     }
-    sort_variant<kCap3, 1024>(c, ord + off[4], c.bin_class[4], c.side[1]);
-    sort_variant<kCapM, TS_NT_M>(c, ord + off[5], c.bin_class[5], c.side[1]);
-    sort_variant<kCap1, TS_NT_1>(c, ord + off[2], c.bin_class[2], c.stream);
-    sort_variant<kCap0, 256>(c, ord + off[1], c.bin_class[1], c.stream);
+    sort_variant<kCap3, 1024>(c, ord + off[4], c.bin_class[4], c.side[1], 4);
+    sort_variant<kCapM, TS_NT_M>(c, ord + off[5], c.bin_class[5], c.side[1], 5);
+    sort_variant<kCap1, TS_NT_1>(c, ord + off[2], c.bin_class[2], c.stream, 2);
+    sort_variant<kCap0, 256>(c, ord + off[1], c.bin_class[1], c.stream, 1);
     for (int k = 0; k < 2; ++k) {
         cudaEventRecord(c.join_ev[k], c.side[k]);
         cudaStreamWaitEvent(c.stream, c.join_ev[k], 0);

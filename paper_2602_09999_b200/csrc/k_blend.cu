@@ -27,25 +27,8 @@ constexpr int kPPT = 4;      // pixels per thread (a 1x4 column)
 constexpr int kBatch = 128;  // splats staged per round
 constexpr float kNegHalfLog2e = -0.72134752044448170368f;  // -0.5 * log2(e)
 
-// conservative half-height of the alpha >= tau ellipse: max |dy| over Q <= k2
-// is sqrt(k2 * Sigma_yy), Sigma_yy = A / (A C - B^2), for the exact quadratic form.
-// The keep test evaluates Q in fp32 (exact-op order, the oracle's), whose rounding
-// error grows with the conic's conditioning kappa = A C / (A C - B^2) >= 1 (the
-// terms A dx^2, 2B dx dy, C dy^2 are each ~kappa k2 at the ellipse's rim and
-// cancel): the bound is widened by a relative slack of 2^-19 kappa (>= 8 ulps per
-// term) and dropped (infinite extent, no row cull) when that slack exceeds 3.  The
-// determinant of the rounded conic is formed in double (the fp32 products are
-// exact there), so needles do not lose it to cancellation; a conic that is not
-// positive definite after rounding gets an unbounded extent too.
-__device__ __forceinline__ float ellipse_ry(float A, float B, float C, float k2) {
-    const double det = double(A) * double(C) - double(B) * double(B);
-    if (!(det > 0.0) || !(k2 > 0.f)) return k2 > 0.f ? __int_as_float(0x7f800000) : 0.f;
-    const double kappa = double(A) * double(C) / det;
-    const double slack = 1.002 + kappa * 0x1p-19;
-    if (slack > 4.0) return __int_as_float(0x7f800000);
-    return float(sqrt(double(k2) * (double(A) / det) * slack)) + 0.05f;
-}
-
+// the per-warp row cull uses each splat's conservative half-height ry (tsx::ellipse_ry,
+// computed once per Gaussian by K1 into c.ryv)
 // pixel rows of thread `tid` in a 16x16 tile: warp w owns rows [8w, 8w+8),
 // lanes 0-15 rows 8w..8w+3, lanes 16-31 rows 8w+4..8w+7; column = tid % 16.
 __device__ __forceinline__ int tile_row0(int tid) { return (tid >> 5) * 8 + ((tid >> 4) & 1) * 4; }
@@ -66,7 +49,8 @@ __global__ void __launch_bounds__(kT, TS_FWD_MINB) blend_fwd_kernel(const uint32
                                                       float* __restrict__ Tfin, uint32_t* __restrict__ pcount,
                                                       uint32_t* __restrict__ ip_counter,
                                                       const uint32_t* __restrict__ order,
-                                                      uint32_t* __restrict__ tile_proc) {
+                                                      uint32_t* __restrict__ tile_proc,
+                                                      const float* __restrict__ ryv) {
     __shared__ float4 sA[kBatch];  // mx, my, k2, o
     __shared__ float4 sB[kBatch];  // A, 2B, C, ry
     __shared__ float4 sC[kBatch];  // r, g, b
@@ -108,7 +92,7 @@ __global__ void __launch_bounds__(kT, TS_FWD_MINB) blend_fwd_kernel(const uint32
                 const uint32_t g = __ldg(ival + i);
                 const float4 s0 = __ldg(splat + 3 * g), s1 = __ldg(splat + 3 * g + 1), s2 = __ldg(splat + 3 * g + 2);
                 sA[threadIdx.x + u * kT] = s0;
-                sB[threadIdx.x + u * kT] = make_float4(s1.x, tsx::add(s1.y, s1.y), s1.z, ellipse_ry(s1.x, s1.y, s1.z, s0.z));
+                sB[threadIdx.x + u * kT] = make_float4(s1.x, tsx::add(s1.y, s1.y), s1.z, __ldg(ryv + g));
                 sC[threadIdx.x + u * kT] = s2;
             }
         }
@@ -279,7 +263,8 @@ __global__ void __launch_bounds__(kT, TS_BWD_MINB) blend_bwd_kernel(const uint32
                                                       const float4* __restrict__ splat, DevCam cam,
                                                       const float* __restrict__ rgb, const uint32_t* __restrict__ pcount,
                                                       const float* __restrict__ dLdC, float4* __restrict__ g2d,
-                                                      const uint32_t* __restrict__ order) {
+                                                      const uint32_t* __restrict__ order,
+                                                      const float* __restrict__ ryv) {
     __shared__ float4 sA[kBatch];  // mx, my, k2, o
     __shared__ float4 sB[kBatch];  // A, 2B, C, ry
     __shared__ float4 sC[kBatch];  // r, g, b
@@ -339,7 +324,7 @@ __global__ void __launch_bounds__(kT, TS_BWD_MINB) blend_bwd_kernel(const uint32
                 const uint32_t g = __ldg(ival + i);
                 const float4 s0 = __ldg(splat + 3 * g), s1 = __ldg(splat + 3 * g + 1), s2 = __ldg(splat + 3 * g + 2);
                 sA[r] = s0;
-                sB[r] = make_float4(s1.x, tsx::add(s1.y, s1.y), s1.z, ellipse_ry(s1.x, s1.y, s1.z, s0.z));
+                sB[r] = make_float4(s1.x, tsx::add(s1.y, s1.y), s1.z, __ldg(ryv + g));
                 sC[r] = s2;
                 sIdx[r] = g;
             }
@@ -455,11 +440,11 @@ void launch_blend_fwd(Context& c, const DevCam& cam, const ts_render_config& cfg
     if (cfg.early_stop_compat)
         blend_fwd_kernel<true><<<Tn, kT, 0, c.stream>>>(c.starts.p, c.ival[0].p, c.splat.p, cam, cfg, c.rgb.p,
                                                         c.Tfin.p, c.pcount.p, c.counters.p + 2, c.order_ok ? c.tile_order.p : nullptr,
-                                                        c.tile_proc.p);
+                                                        c.tile_proc.p, c.ryv.p);
     else
         blend_fwd_kernel<false><<<Tn, kT, 0, c.stream>>>(c.starts.p, c.ival[0].p, c.splat.p, cam, cfg, c.rgb.p,
                                                          c.Tfin.p, c.pcount.p, c.counters.p + 2, c.order_ok ? c.tile_order.p : nullptr,
-                                                         c.tile_proc.p);
+                                                         c.tile_proc.p, c.ryv.p);
     TS_LAUNCHED(c);
 }
 
@@ -467,7 +452,8 @@ void launch_blend_bwd(Context& c, const DevCam& cam, const ts_render_config& cfg
     (void)cfg;
     const int Tn = cam.tiles_x * cam.tiles_y;
     blend_bwd_kernel<<<Tn, kT, 0, c.stream>>>(c.starts.p, c.ival[0].p, c.splat.p, cam, c.rgb.p, c.pcount.p,
-                                              c.dLdC.p, c.g2d.p, c.bwd_order_ok ? c.bwd_order.p : (c.order_ok ? c.tile_order.p : nullptr));
+                                              c.dLdC.p, c.g2d.p, c.bwd_order_ok ? c.bwd_order.p : (c.order_ok ? c.tile_order.p : nullptr),
+                                              c.ryv.p);
     TS_LAUNCHED(c);
 }
 

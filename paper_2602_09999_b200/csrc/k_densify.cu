@@ -215,7 +215,7 @@ int64_t launch_densify(Context& c, float thresh, float log_small, float log_big,
         !ensure_grow(c, c.splat, 3 * n1) || !ensure_grow(c, c.rect, n1) || !ensure_grow(c, c.tcount, n1) ||
         !ensure_grow(c, c.dkey[0], n1) || !ensure_grow(c, c.dkey[1], n1) || !ensure_grow(c, c.dperm[0], n1) ||
         !ensure_grow(c, c.dperm[1], n1) || !ensure_grow(c, c.offsets, n1 + 1) || !ensure_grow(c, c.g2d, 3 * n1 + 1) ||
-        !ensure_grow(c, c.vis, n1) || !ensure_grow(c, c.nu_hat, n1))
+        !ensure_grow(c, c.vis, n1) || !ensure_grow(c, c.nu_hat, n1) || !ensure_grow(c, c.ryv, n1))
         return -1;
     c.nu_valid = false;  // new rows: the sampling rates must be recomputed (SPEC.md:614 interval)
     cudaMemsetAsync(c.grads.p, 0, c.grads.cap * 4, c.stream);

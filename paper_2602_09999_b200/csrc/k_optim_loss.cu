@@ -8,6 +8,7 @@
 // Reads theta, g, m, v and writes theta, m, v (28 B/element, HBM-bound); with
 // zero_grads the gradient is cleared in the same pass (+4 B).
 #include <cmath>
+#include <cstring>
 
 #include "ts_internal.cuh"
 #include "ts_math.cuh"
@@ -44,10 +45,16 @@ __device__ __forceinline__ bool visible_of(uint32_t i, const Bounds& b, const ui
 template <int MODE, bool ZERO>
 __global__ void __launch_bounds__(256) adam_kernel(float4* __restrict__ th, float4* __restrict__ g,
                                                    float4* __restrict__ m, float4* __restrict__ v, uint32_t q0,
-                                                   uint32_t q1, uint32_t begin, uint32_t end, Bounds bd, AdamArgs a,
-                                                   const uint8_t* __restrict__ vis) {
+                                                   uint32_t q1, uint32_t begin, uint32_t end, Bounds bd, AdamArgs a_host,
+                                                   const uint8_t* __restrict__ vis,
+                                                   const AdamArgs* __restrict__ a_dev,
+                                                   const uint32_t* __restrict__ gflag) {
     const uint32_t q = q0 + blockIdx.x * 256u + threadIdx.x;
     if (q >= q1) return;
+    // graph-captured step: per-step arguments from device memory (written before each launch),
+    // and nothing at all when the step was voided by its capacity check
+    if (gflag && *gflag) return;
+    const AdamArgs a = a_dev ? *a_dev : a_host;
     float4 t4 = th[q], g4 = g[q], m4 = m[q], v4 = v[q];
     float* tp = &t4.x;
     float* gp = &g4.x;
@@ -135,10 +142,7 @@ __global__ void opacity_reset_kernel(float* __restrict__ op, int64_t N, float lm
     if (g < N) op[g] = op[g] < lmax ? op[g] : lmax;
 }
 
-}  // namespace
-
-void launch_adam(Context& c, const ts_adam_config& a, int64_t begin, int64_t end) {
-    if (end <= begin) return;
+AdamArgs adam_args(const ts_adam_config& a) {
     AdamArgs x;
     for (int k = 0; k < 6; ++k) x.lr[k] = a.lr[k];
     x.b1 = a.beta1;
@@ -150,6 +154,21 @@ void launch_adam(Context& c, const ts_adam_config& a, int64_t begin, int64_t end
     x.bc2 = a.bc2;
     x.mode = a.mode;
     x.zero = a.zero_grads;
+    return x;
+}
+
+}  // namespace
+
+// per-step Adam arguments for a captured graph: copied to c.adam_dev before each launch
+size_t adam_args_bytes(const ts_adam_config& a, void* out) {
+    const AdamArgs x = adam_args(a);
+    std::memcpy(out, &x, sizeof(x));
+    return sizeof(x);
+}
+
+void launch_adam(Context& c, const ts_adam_config& a, int64_t begin, int64_t end) {
+    if (end <= begin) return;
+    const AdamArgs x = adam_args(a);
     const uint32_t N = uint32_t(c.N);
     const Bounds bd{3u * N, 6u * N, 10u * N, 11u * N, 14u * N};
     const uint32_t q0 = uint32_t(begin / 4), q1 = uint32_t((end + 3) / 4);
@@ -159,7 +178,14 @@ void launch_adam(Context& c, const ts_adam_config& a, int64_t begin, int64_t end
     auto* m = reinterpret_cast<float4*>(c.m.p);
     auto* v = reinterpret_cast<float4*>(c.v.p);
     const uint32_t b = uint32_t(begin), e = uint32_t(end);
-#define TS_ADAM(MODE, Z) adam_kernel<MODE, Z><<<blocks, 256, 0, c.stream>>>(th, g, m, v, q0, q1, b, e, bd, x, c.vis.p)
+    const AdamArgs* xd = nullptr;
+    if (c.gmode) {  // the graph reads this step's arguments from device memory (graph_step writes them)
+        static_assert(sizeof(AdamArgs) <= sizeof(c.adam_dev_bytes), "adam args");
+        xd = reinterpret_cast<const AdamArgs*>(c.adam_dev);
+    }
+    const uint32_t* gf = c.gmode ? c.counters.p + kGraphFlag : nullptr;
+#define TS_ADAM(MODE, Z) \
+    adam_kernel<MODE, Z><<<blocks, 256, 0, c.stream>>>(th, g, m, v, q0, q1, b, e, bd, x, c.vis.p, xd, gf)
     if (a.mode == 2) {
         if (a.zero_grads) TS_ADAM(2, true);
         else TS_ADAM(2, false);

@@ -16,7 +16,7 @@ constexpr int kBlock = 128;
 template <int DEG>
 __global__ void __launch_bounds__(kBlock) preprocess_kernel(
     const float* __restrict__ P, int64_t N, DevCam cam, ts_render_config cfg, float4* __restrict__ splat,
-    uint4* __restrict__ rect, uint32_t* __restrict__ tcount, uint32_t* __restrict__ dkey,
+    uint4* __restrict__ rect, float* __restrict__ ryv, uint32_t* __restrict__ tcount, uint32_t* __restrict__ dkey,
     uint32_t* __restrict__ dperm, uint32_t* __restrict__ vis_counter, const float* __restrict__ nu_hat,
     uint32_t* __restrict__ binH, int bin_chunk) {
     using namespace tsx;
@@ -60,6 +60,7 @@ __global__ void __launch_bounds__(kBlock) preprocess_kernel(
     uint4 rc = make_uint4(1u, 1u, 0u, 0u);  // empty: tx0=1 > tx1=0
     bool ok = false;
     float zh = 0.f;
+    float ry_cull = 0.f;  // blend row-cull half-height (0: no tiles)
     // exact-cull inputs of the warp-cooperative pass (ntl = 0: nothing to test)
     uint32_t ntl_c = 0, rect0 = 0;
     int tw_c = 1;
@@ -217,6 +218,7 @@ __global__ void __launch_bounds__(kBlock) preprocess_kernel(
         s1 = make_float4(A, B, C, zh);
         s2 = make_float4(rgb[0], rgb[1], rgb[2], det);
         if (!has_bound) break;
+        ry_cull = ellipse_ry(A, B, C, k2);
 
         // ---- bound (opacity-aware rect / rect / square) -> inclusive tile rect ----
         float rx, ry;
@@ -333,6 +335,7 @@ __global__ void __launch_bounds__(kBlock) preprocess_kernel(
     splat[3 * g + 1] = s1;
     splat[3 * g + 2] = s2;
     rect[g] = rc;
+    ryv[g] = ry_cull;
     tcount[g] = cnt;
     dkey[g] = cnt ? (__float_as_uint(zh) ^ 0x80000000u) : 0xFFFFFFFFu;
     dperm[g] = uint32_t(g);
@@ -360,7 +363,7 @@ void launch_preprocess(Context& c, const DevCam& cam, const ts_render_config& cf
     const int64_t blocks = (c.N + kBlock - 1) / kBlock;
 #define TS_PRE(D)                                                                                      \
     preprocess_kernel<D><<<unsigned(blocks), kBlock, 0, c.stream>>>(c.params.p, c.N, cam, cfg, c.splat.p, \
-                                                                     c.rect.p, c.tcount.p, c.dkey[0].p,   \
+                                                                     c.rect.p, c.ryv.p, c.tcount.p, c.dkey[0].p,   \
                                                                      c.dperm[0].p, c.counters.p + 1, c.nu_hat.p,    \
                                                                      binH, bin_chunk_for(c.N, c.sm_count))
     switch (cfg.sh_degree) {

@@ -344,9 +344,11 @@ __global__ void __launch_bounds__(kBlock, TS_PB_MINB) project_bwd_kernel(const f
                                                              float* __restrict__ accum, float* __restrict__ vcount,
                                                              uint8_t* __restrict__ vis, int64_t N, DevCam cam,
                                                              ts_render_config cfg, int zero_inactive,
-                                                             const float* __restrict__ nu_hat) {
+                                                             const float* __restrict__ nu_hat,
+                                                             const uint32_t* __restrict__ gflag) {
     extern __shared__ __align__(16) float smem[];
     using L = PbLayout<DEG, ACCUM>;
+    if (gflag && *gflag) return;  // graph-captured step voided by its capacity check (replayed by the host)
     constexpr int nrest = 3 * ((DEG + 1) * (DEG + 1) - 1);
     const Off off(N);
     const int64_t g0 = int64_t(blockIdx.x) * kBlock;
@@ -595,18 +597,19 @@ void launch_project_bwd(Context& c, const DevCam& cam, const ts_render_config& c
                         bool zero_inactive) {
     if (c.N == 0) return;
     const int64_t blocks = (c.N + kBlock - 1) / kBlock;
+    const uint32_t* gf = c.gmode ? c.counters.p + kGraphFlag : nullptr;
 #define TS_PB(D)                                                                                      \
     if (accumulate) {                                                                                 \
         constexpr int sm = PbLayout<D, true>::kTotal * 4;                                             \
         set_func_attr(c, reinterpret_cast<const void*>(project_bwd_kernel<D, true>), cudaFuncAttributeMaxDynamicSharedMemorySize, sm); \
         project_bwd_kernel<D, true><<<unsigned(blocks), kBlock, sm, c.stream>>>(                      \
-            c.params.p, c.grads.p, c.g2d.p, c.tcount.p, c.accum.p, c.vcount.p, c.vis.p, c.N, cam, cfg, 0, c.nu_hat.p); \
+            c.params.p, c.grads.p, c.g2d.p, c.tcount.p, c.accum.p, c.vcount.p, c.vis.p, c.N, cam, cfg, 0, c.nu_hat.p, gf); \
     } else {                                                                                          \
         constexpr int sm = PbLayout<D, false>::kTotal * 4;                                            \
         set_func_attr(c, reinterpret_cast<const void*>(project_bwd_kernel<D, false>), cudaFuncAttributeMaxDynamicSharedMemorySize, sm); \
         project_bwd_kernel<D, false><<<unsigned(blocks), kBlock, sm, c.stream>>>(                     \
             c.params.p, c.grads.p, c.g2d.p, c.tcount.p, c.accum.p, c.vcount.p, c.vis.p, c.N, cam, cfg,   \
-            int(zero_inactive), c.nu_hat.p);                                                                     \
+            int(zero_inactive), c.nu_hat.p, gf);                                                                 \
     }
     switch (cfg.sh_degree) {
         case 0: TS_PB(0); break;

@@ -199,7 +199,7 @@ ts_status ensure_gaussian_buffers(Context& c, int64_t n) {
               ensure(c, c.splat, 3 * N) && ensure(c, c.rect, N) && ensure(c, c.tcount, N) &&
               ensure(c, c.dkey[0], N) && ensure(c, c.dkey[1], N) && ensure(c, c.dperm[0], N) &&
               ensure(c, c.dperm[1], N) && ensure(c, c.offsets, N + 1) && ensure(c, c.g2d, 3 * N + 1) &&
-              ensure(c, c.vis, N) && ensure(c, c.nu_hat, N);
+              ensure(c, c.vis, N) && ensure(c, c.nu_hat, N) && ensure(c, c.ryv, N);
     return ok ? TS_OK : TS_ERR_OOM;
 }
 
@@ -490,7 +490,7 @@ ts_status ts_destroy(ts_ctx* x) {
     cudaSetDevice(c.device);
     cudaStreamSynchronize(c.stream);
     release(c.params), release(c.grads), release(c.m), release(c.v), release(c.accum), release(c.vcount);
-    release(c.splat), release(c.rect), release(c.tcount), release(c.offsets), release(c.g2d), release(c.vis);
+    release(c.splat), release(c.ryv), release(c.rect), release(c.tcount), release(c.offsets), release(c.g2d), release(c.vis);
     for (int k = 0; k < 2; ++k) {
         release(c.dkey[k]), release(c.dperm[k]), release(c.tkey[k]), release(c.tkey32[k]), release(c.ival[k]);
     }

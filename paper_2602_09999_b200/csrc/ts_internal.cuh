@@ -14,6 +14,7 @@ constexpr int kTile = 16;
 constexpr int kParams = 59;
 constexpr int kG2D = 12;  // floats per Gaussian in the 2D-gradient accumulator (9 used, 16B aligned)
 constexpr int kNumStages = 11;
+constexpr int kGraphFlag = 12;  // counters[kGraphFlag]: sticky overflow flag of graph-captured steps
 // Largest store: the flat 59*N sweeps (Adam, densify, Morton) index in 32 bits, so
 // 59*N (+ float4 padding) must stay below 2^32.  ~72M Gaussians = ~85 GB of store +
 // moments + gradients, within a 180 GB B200; ts_set_params* and ts_densify reject more.
@@ -60,6 +61,7 @@ struct Context {
 
     // per-view (sized by N)
     DevBuf<float4> splat;        // 3 float4 per Gaussian: (mx,my,k2,o) (A,B,C,depth) (r,g,b,det)
+    DevBuf<float> ryv;           // per Gaussian: half-height of the keep ellipse for the blend row cull
     DevBuf<uint4> rect;          // {tx0|tx1<<16, ty0|ty1<<16 (bit31: >64 tiles), kept-tile mask lo, hi}
     DevBuf<uint32_t> tcount;     // tiles per Gaussian
     DevBuf<uint32_t> dkey[2];    // depth keys (radix double buffer)
@@ -128,6 +130,11 @@ struct Context {
     double* loss_host = nullptr;  // pinned (L1 sum, SSIM sum) of the last train_step
     cudaEvent_t loss_ev = nullptr;
     int binning_mode = 0;        // 0 auto (bucket + per-tile sort), 1 force the two-stage radix path
+    // CUDA-graph mode of ts_train_step (ts_capi.cu graph_step)
+    bool gmode = false;          // the step being captured: no host reads, device-side counts and checks
+    int cur_tn = 0;              // tiles of the view being binned
+    void* adam_dev = nullptr;    // device copy of the per-step Adam arguments (graph mode)
+    unsigned char adam_dev_bytes[128] = {};  // host staging of those arguments (size bound)
     bool last_view_radix = false;
 };
 
@@ -171,6 +178,7 @@ void launch_project_bwd(Context& c, const DevCam& cam, const ts_render_config& c
                         bool zero_inactive);
 void launch_project_bwd_adam(Context& c, const DevCam& cam, const ts_render_config& cfg, const ts_adam_config& a);
 void launch_adam(Context& c, const ts_adam_config& a, int64_t begin, int64_t end);
+size_t adam_args_bytes(const ts_adam_config& a, void* out);  // the kernel's argument block of a (<= 128 B)
 void launch_hwc_to_chw(Context& c, const float* hwc, float* chw, int P);
 void launch_chw_to_hwc(Context& c, const float* chw, float* hwc, int P);
 void launch_opacity_reset(Context& c, float logit_max);

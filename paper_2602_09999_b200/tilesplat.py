@@ -20,6 +20,9 @@ from .types import AdamConfig, Camera, RenderConfig, NPARAM
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libtilesplat_b200.so")
+# experiments only: an alternative in-tree build of the same library (tuning variants)
+if os.environ.get("TS_LIB_VARIANT"):
+    LIB_PATH = os.path.join(_HERE, f"libtilesplat_b200_{os.environ['TS_LIB_VARIANT']}.so")
 
 TS_OK, TS_ERR_VALIDATION, TS_ERR_CHECK, TS_ERR_CUDA, TS_ERR_OOM, TS_ERR_STATE = range(6)
 

@@ -307,7 +307,10 @@ def run_ours(args):
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
     torch.cuda.set_device(local)
-    stream = torch.cuda.current_stream()
+    # one explicit stream for the engine, torch's collectives and the timing events (the legacy
+    # default stream would not order against the engine's work: handle 0 = "own stream")
+    stream = torch.cuda.Stream(device=local)
+    torch.cuda.set_stream(stream)
     w = scene.WORKLOADS[args.workload]
     n = w.n
     batch, scaling = batch_of(w, world)
@@ -331,6 +334,7 @@ def run_ours(args):
         # order-invariant (bitwise), the arrays just gain spatial locality
         perm = e.morton_reorder()
         p0 = scene.reorder_params(p0, n, perm)
+    e.set_graph(args.graph)   # CUDA-graph mode of the single-call step (ts_set_graph)
     dp_mode = args.dp_mode or ("sharded" if world > 1 else "allreduce")
     dp = DataParallelStep(e, mode=dp_mode)
     step = 0
@@ -382,6 +386,7 @@ def run_ours(args):
     # ---- timed region (device-resident targets) ----
     clk = ClockSampler(local)
     clk.start()
+    gs0 = e.graph_stats()
     l0 = e.launch_count()
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
@@ -396,6 +401,8 @@ def run_ours(args):
         dist.barrier()
     clocks = clk.stop()
     launches = e.launch_count() - l0
+    e.synchronize()  # settles the graph steps (replays a voided one) after the timed region
+    gs1 = e.graph_stats()
     ms = ev0.elapsed_time(ev1) / args.steps
     if world > 1:
         t = torch.tensor([ms], device=f"cuda:{local}")
@@ -470,6 +477,20 @@ def run_ours(args):
     for pb in pins.values():
         pb.free()
 
+    # ---- SPEC binning counters: instances per bounding / culling mode and the
+    # radix key-bytes metrics of the combined 48-bit vs two-stage sort (PAPER §B.2), view 0 ----
+    bcnt = {}
+    for name_, bm, cm in (("square", 0, 0), ("rect", 1, 0), ("rect_opacity", 2, 0), ("exact", 2, 1)):
+        c_ = T.RenderConfig.make(sh_degree=w.sh_degree, bound_mode=bm, cull_mode=cm)
+        e.render(cams[0], c_, outputs=False)
+        bcnt["instances_" + name_] = e.view_stats()["I"]
+    e.render(cams[0], cfg, outputs=False)
+    vs0 = e.view_stats()
+    key32 = cams[0].n_tiles >= 65536
+    bcnt["sort_key_bytes_combined"] = 6 * vs0["I"]                                  # 48-bit keys over I
+    bcnt["sort_key_bytes_two_stage"] = 4 * vs0["V"] + (4 if key32 else 2) * vs0["I"]  # depth over V + tile over I
+    bcnt["two_stage_over_combined"] = round(bcnt["sort_key_bytes_two_stage"] / max(1, bcnt["sort_key_bytes_combined"]), 4)
+
     # ---- per-stage accounting over the profiled loop ----
     bytes_ = stage_bytes(vstats, n, w.sh_degree, cams[0].n_tiles)
     avg = {k: (tot / max(1, c)) for k, (tot, c) in stimes.items()}
@@ -534,6 +555,9 @@ def run_ours(args):
                     "h2d_gbs": round(P * 3 * 4 / (h2d_ms * 1e-3) / 1e9, 2)},
             "stage_ms_split": {k: round(v, 4) for k, v in split.items()} if fused_bwd else None,
             "gpu_launches": int(launches),
+            "graph": bool(args.graph and single_call),
+            "graph_timed": {k: gs1[k] - gs0[k] for k in ("launches", "captures", "replays")},
+            "graph_stats": e.graph_stats(),
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "algorithmic_bytes_per_launch": int(dom_bytes), "avg_launch_ms": dom_ms,
@@ -546,6 +570,7 @@ def run_ours(args):
                         "algorithmic_bytes": int(R), "achieved_gbs": R / (fwd_bwd_ms * 1e-3) / 1e9,
                         "roofline_frac": R / (fwd_bwd_ms * 1e-3) / 1e9 / peak},
             "compute": compute_roofline(avg, vstats, clocks, cams[0].n_tiles),
+            "binning_counters": bcnt,
             "stage_ms": {k: round(v, 4) for k, v in avg.items()},
             "densify": [{"step": d[0], "n_after": d[1], "clones": d[2][0], "splits": d[2][1], "pruned": d[2][2]}
                         for d in densify_log] if args.densify else None,
@@ -614,6 +639,9 @@ def main():
                     help="densify_and_prune every 100 iterations inside the timed region (config 3, N=1)")
     ap.add_argument("--no-morton", action="store_true",
                     help="keep the generator's random Gaussian order instead of the z-order training state")
+    ap.add_argument("--graph", dest="graph", action="store_true", default=False,
+                    help="CUDA-graph mode of the one-call training step (ts_set_graph)")
+    ap.add_argument("--no-graph", dest="graph", action="store_false")
     ap.add_argument("--selftest-launcher", action="store_true", help=argparse.SUPPRESS)
     args = ap.parse_args()
     if args.warmup < 3:

@@ -139,6 +139,19 @@ ts_status ts_train_step(ts_ctx* ctx, const ts_camera* cam, const ts_render_confi
                         const float* target_hwc /* host (pinned preferred) or NULL: slot */, int32_t target_slot,
                         const ts_adam_config* adam, float* out_loss /* may be NULL: no D2H */);
 
+/* CUDA-graph mode of ts_train_step (default off): each (view, render config, target slot or host
+ * target address, optimizer mode) is captured once into a CUDA graph -- forward, loss, backward,
+ * Adam, the host-target upload as a parallel branch -- and relaunched per step with no host round
+ * trip inside the step; the per-step optimizer arguments enter through device memory.  The first
+ * step of a view runs on the host path (sizes the buffers), the second captures.  A graph step
+ * that outgrows its buffers is voided on the device and replayed on the host path before any
+ * other call observes state, so results equal the host-driven path.  A host target must stay
+ * valid (and unchanged) until the next synchronising call.  Modes 3/4, the radix binning path,
+ * antialias mode 1 and profiling run host-driven. */
+ts_status ts_set_graph(ts_ctx* ctx, int32_t on);
+/* {graph launches, captures, replayed (voided) steps, live graphs} */
+ts_status ts_graph_stats(ts_ctx* ctx, int64_t out[4]);
+
 /* ---- densification ---- */
 ts_status ts_densify(ts_ctx* ctx, float grad_thresh, float extent, uint64_t seed, int64_t iter,
                      int64_t* n_after, int64_t stats[3] /* clones, splits, pruned */);

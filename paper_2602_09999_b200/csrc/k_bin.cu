@@ -575,8 +575,10 @@ static void sort_variant(Context& c, const uint32_t* tiles, uint32_t n, cudaStre
     const size_t smem = tile_sort_smem(CAP);
     unsigned grid = SEG ? 4 * n : n;
     if (c.gmode) {
-        const int per_sm = std::max<int>(1, std::min<int>(2048 / NT, int((227 * 1024) / (smem + 1024))));
-        grid = unsigned(c.sm_count * per_sm);
+        // the class count of the view's last host-path step (+25%, + 8) as the grid: one unit per
+        // CTA as on the host path; a class that grew is walked grid-stride
+        const unsigned hint = n + n / 4 + 8;
+        grid = SEG ? 4 * hint : hint;
     }
     // segments sort in place in the scatter output; whole lists go to the final list buffer
     tile_sort_kernel<CAP, NT, SEG><<<grid, NT, smem, st>>>(c.starts.p, c.ival[1].p, c.dkey[0].p,
@@ -606,7 +608,7 @@ void launch_tile_depth_sort(Context& c, int Tn, uint32_t max_len) {
         off[0] = off[1] + c.bin_class[1];
     }
     if (c.gmode || c.bin_class[0]) {
-        const unsigned grid = c.gmode ? unsigned(c.sm_count) : (c.bin_class[0] + 255) / 256;
+        const unsigned grid = (c.bin_class[0] + c.bin_class[0] / 4 + 8 + 255) / 256;
         tile_copy_single_kernel<<<grid, 256, 0, c.stream>>>(c.starts.p, c.ival[1].p, c.ival[0].p, ord + off[0],
                                                             c.bin_class[0], meta);
         TS_LAUNCHED(c);
@@ -628,7 +630,7 @@ void launch_tile_depth_sort(Context& c, int Tn, uint32_t max_len) {
         const uint32_t* lt = ord + off[6];
         sort_variant<kCap3, 1024, true>(c, lt, c.bin_class[6], c.side[0], 6);
         // c.sortmp holds >= I entries (run_forward sizes it before the fork)
-        const dim3 g(kCapL / (kMergeT * kMergePer), c.gmode ? 64u : c.bin_class[6]);
+        const dim3 g(kCapL / (kMergeT * kMergePer), c.gmode ? c.bin_class[6] + c.bin_class[6] / 4 + 8 : c.bin_class[6]);
         merge_level_kernel<<<g, kMergeT, 0, c.side[0]>>>(c.starts.p, lt, c.ival[1].p, c.sortmp.p, c.dkey[0].p, kCap3,
                                                         c.bin_class[6], meta);
         merge_level_kernel<<<g, kMergeT, 0, c.side[0]>>>(c.starts.p, lt, c.sortmp.p, c.ival[0].p, c.dkey[0].p,

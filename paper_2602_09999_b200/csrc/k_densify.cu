@@ -207,6 +207,7 @@ int64_t launch_densify(Context& c, float thresh, float log_small, float log_big,
             cudaMemsetAsync(c.spare.p, 0, L * 4, c.stream);
         }
         std::swap(*bufs[w], c.spare);
+        ++c.gen;  // buffer addresses changed (captured graphs are stale)
     }
     c.N = NA;
     // resize the remaining per-Gaussian buffers and reset gradients / statistics

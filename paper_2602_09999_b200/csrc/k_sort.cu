@@ -480,10 +480,12 @@ void launch_tile_sort(Context& c, int tile_bits, bool key32) {
         radix_sort<uint32_t, 3>(c, c.tkey32[0].p, c.ival[0].p, c.tkey32[1].p, c.ival[1].p, c.I);
         std::swap(c.tkey32[0], c.tkey32[1]);  // odd pass count: keep the sorted list in buffer 0
         std::swap(c.ival[0], c.ival[1]);
+        ++c.gen;
     } else if (tile_bits <= 8) {
         radix_sort<uint16_t, 1>(c, c.tkey[0].p, c.ival[0].p, c.tkey[1].p, c.ival[1].p, c.I);
         std::swap(c.tkey[0], c.tkey[1]);  // keep the sorted list in buffer 0
         std::swap(c.ival[0], c.ival[1]);
+        ++c.gen;
     } else {
         radix_sort<uint16_t, 2>(c, c.tkey[0].p, c.ival[0].p, c.tkey[1].p, c.ival[1].p, c.I);
     }
@@ -544,6 +546,7 @@ bool launch_morton_reorder(Context& c, uint32_t* perm_host) {
         gather_group<3>(c, b + o.dc, t + o.dc, perm, N);
         gather_group<45>(c, b + o.rest, t + o.rest, perm, N);
         std::swap(*bp, c.spare);
+        ++c.gen;
     }
     float* tmp = c.spare.p;
     gather_group<1>(c, c.accum.p, tmp, perm, N);

@@ -27,6 +27,11 @@ namespace ts {
 template <class T>
 bool ensure(Context& c, DevBuf<T>& b, size_t n, bool keep) {
     if (n <= b.cap && b.p) return true;
+    if (c.capturing) {  // a captured graph may not allocate (buffers are sized before the capture)
+        c.err = "buffer growth during graph capture";
+        return false;
+    }
+    ++c.gen;  // captured graphs embed buffer addresses
     size_t cap = std::max<size_t>(n, 1);
     T* p = nullptr;
     if (cudaMalloc(&p, cap * sizeof(T)) != cudaSuccess) {
@@ -331,6 +336,43 @@ ts_status run_forward(Context& c, const ts_camera& cam, const ts_render_config& 
     return TS_OK;
 }
 
+// The forward of a graph-captured step (bucketed binning only): no host reads.  The tile order
+// runs before the scatter and performs the step's capacity check (tile_order_kernel); the size
+// classes are launched on resident grids that read the device-side class counts.
+ts_status run_forward_graph(Context& c, const ts_camera& cam, const ts_render_config& cfg) {
+    DevCam dc = make_devcam(cam);
+    const int Tn = dc.tiles_x * dc.tiles_y;
+    if (ensure_frame(c, cam.width, cam.height) != TS_OK) return TS_ERR_OOM;
+    if (!ensure(c, c.starts, size_t(Tn) + 1)) return TS_ERR_OOM;
+    CK(cudaMemsetAsync(c.counters.p + 1, 0, 2 * sizeof(uint32_t), c.stream));
+    stage_begin(c, 0);
+    launch_preprocess(c, dc, cfg);
+    stage_end(c, 0);
+    stage_begin(c, 1);
+    if (!launch_bin_count(c, dc, cfg)) return c.err.empty() ? TS_ERR_OOM : TS_ERR_CUDA;
+    stage_end(c, 1);
+    launch_tile_order(c, Tn);
+    stage_begin(c, 3);
+    launch_bin_scatter(c, dc, cfg);
+    stage_end(c, 3);
+    stage_begin(c, 4);
+    launch_tile_depth_sort(c, Tn, 0);
+    stage_end(c, 4);
+    c.order_ok = true;
+    c.bwd_order_ok = false;
+    stage_begin(c, 6);
+    launch_blend_fwd(c, dc, cfg);
+    stage_end(c, 6);
+    if (ts_status s = last_launch(c, "forward (graph)"); s != TS_OK) return s;
+    c.last_view_radix = false;
+    c.I_on_device = true;
+    c.cam = cam;
+    c.cfg = cfg;
+    c.view_valid = true;
+    c.loss_valid = false;
+    return TS_OK;
+}
+
 ts_status upload_image_chw(Context& c, const float* hwc, float* dst_chw) {
     const size_t P = size_t(c.fw) * c.fh;
     CK(cudaMemcpyAsync(c.hwc_stage.p, hwc, 3 * P * 4, cudaMemcpyHostToDevice, c.stream));
@@ -431,297 +473,12 @@ ts_status run_adam(Context& c, const ts_adam_config& a, int64_t begin, int64_t e
     return last_launch(c, "adam");
 }
 
-}  // namespace
-
-extern "C" {
-
-const char* ts_version(void) { return "tilesplat-b200 0.1 (sm_100a)"; }
-
-ts_status ts_create(int32_t device, void* stream, ts_ctx** out) {
-    if (!out) return TS_ERR_VALIDATION;
-    *out = nullptr;
-    int ndev = 0;
-    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
-        cudaGetLastError();
-        return TS_ERR_CUDA;
-    }
-    if (device < 0 || device >= ndev) return TS_ERR_VALIDATION;
-    cudaDeviceProp prop;
-    if (cudaGetDeviceProperties(&prop, device) != cudaSuccess) return TS_ERR_CUDA;
-    if (prop.major < 10) return TS_ERR_CUDA;  // built for sm_100a only; no fallback
-    ts_ctx* x = new (std::nothrow) ts_ctx();
-    if (!x) return TS_ERR_OOM;
-    Context& c = x->c;
-    c.device = device;
-    c.sm_count = prop.multiProcessorCount;
-    if (cudaSetDevice(device) != cudaSuccess) {
-        delete x;
-        return TS_ERR_CUDA;
-    }
-    if (stream) {
-        c.stream = static_cast<cudaStream_t>(stream);
-    } else {
-        if (cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking) != cudaSuccess) {
-            delete x;
-            return TS_ERR_CUDA;
-        }
-        c.own_stream = true;
-    }
-    if (!ensure(c, c.counters, 16) || !ensure(c, c.loss_acc, 2)) {
-        delete x;
-        return TS_ERR_OOM;
-    }
-    cudaMemsetAsync(c.counters.p, 0, 16 * 4, c.stream);
-    if (ensure_gaussian_buffers(c, 1) != TS_OK) {
-        delete x;
-        return TS_ERR_OOM;
-    }
-    if (cudaStreamSynchronize(c.stream) != cudaSuccess) {
-        delete x;
-        return TS_ERR_CUDA;
-    }
-    *out = x;
-    return TS_OK;
-}
-
-ts_status ts_destroy(ts_ctx* x) {
-    TS_CHECK_CTX(x);
-    Context& c = x->c;
-    cudaSetDevice(c.device);
-    cudaStreamSynchronize(c.stream);
-    release(c.params), release(c.grads), release(c.m), release(c.v), release(c.accum), release(c.vcount);
-    release(c.splat), release(c.ryv), release(c.rect), release(c.tcount), release(c.offsets), release(c.g2d), release(c.vis);
-    for (int k = 0; k < 2; ++k) {
-        release(c.dkey[k]), release(c.dperm[k]), release(c.tkey[k]), release(c.tkey32[k]), release(c.ival[k]);
-    }
-    release(c.starts), release(c.rhist), release(c.scan_state), release(c.scan_tmp), release(c.counters);
-    release(c.rgb), release(c.Tfin), release(c.dLdC), release(c.hwc_stage), release(c.tgt), release(c.pcount);
-    release(c.loss_acc), release(c.targets), release(c.dens);
-    release(c.binH), release(c.bintot), release(c.tile_order), release(c.tile_proc), release(c.bwd_order), release(c.sortmp), release(c.spare), release(c.cams), release(c.mcode[0]), release(c.mcode[1]),
-        release(c.midx[0]), release(c.midx[1]), release(c.tgt_stage), release(c.nu_hat);
-    for (size_t k = 0; k < c.ev_b.size(); ++k) {
-        cudaEventDestroy(c.ev_b[k]);
-        cudaEventDestroy(c.ev_e[k]);
-    }
-    for (int k = 0; k < 2; ++k) {
-        if (c.side[k]) cudaStreamDestroy(c.side[k]);
-        if (c.join_ev[k]) cudaEventDestroy(c.join_ev[k]);
-    }
-    if (c.fork_ev) cudaEventDestroy(c.fork_ev);
-    if (c.copy_stream) cudaStreamDestroy(c.copy_stream);
-    if (c.bin_host) cudaFreeHost(c.bin_host);
-    if (c.bin_ev) cudaEventDestroy(c.bin_ev);
-    if (c.loss_host) cudaFreeHost(c.loss_host);
-    if (c.loss_ev) cudaEventDestroy(c.loss_ev);
-    if (c.copy_fork) cudaEventDestroy(c.copy_fork);
-    if (c.copy_join) cudaEventDestroy(c.copy_join);
-    if (c.own_stream) cudaStreamDestroy(c.stream);
-    delete x;
-    return TS_OK;
-}
-
-const char* ts_last_error(const ts_ctx* x) { return x ? x->c.err.c_str() : "null context"; }
-
-ts_status ts_synchronize(ts_ctx* x) {
-    TS_CHECK_CTX(x);
-    Context& c = x->c;
-    CK(cudaStreamSynchronize(c.stream));
-    return TS_OK;
-}
-
-ts_status ts_set_params_flat(ts_ctx* x, int64_t n, const float* flat) {
-    TS_CHECK_CTX(x);
-    Context& c = x->c;
-    if (n < 0 || (n > 0 && !flat)) return validation(c, "bad parameter array");
-    if (n > kMaxGaussians) return validation(c, "N exceeds the 32-bit flat-index limit (~72.8M Gaussians)");
-    CK(cudaSetDevice(c.device));
-    if (ensure_gaussian_buffers(c, n) != TS_OK) return TS_ERR_OOM;
-    if (n != c.N) c.nu_valid = false;  // sampling rates are per row (kept across same-size updates)
-    c.N = n;
-    if (n) CK(cudaMemcpyAsync(c.params.p, flat, size_t(59) * n * 4, cudaMemcpyHostToDevice, c.stream));
-    if (ts_status s = zero_state(c); s != TS_OK) return s;
-    c.grad_state = Context::kGradZero;
-    c.view_valid = c.loss_valid = false;
-    CK(cudaStreamSynchronize(c.stream));
-    return TS_OK;
-}
-
-ts_status ts_set_params(ts_ctx* x, int64_t n, const float* means, const float* ls, const float* q, const float* op,
-                        const float* dc, const float* rest) {
-    TS_CHECK_CTX(x);
-    Context& c = x->c;
-    if (n < 0) return validation(c, "n < 0");
-    if (n > 0 && (!means || !ls || !q || !op || !dc || !rest)) return validation(c, "NULL parameter array");
-    std::vector<float> flat(size_t(59) * n);
-    const Off o(n);
-    std::memcpy(flat.data() + o.means, means, size_t(3) * n * 4);
-    std::memcpy(flat.data() + o.ls, ls, size_t(3) * n * 4);
-    std::memcpy(flat.data() + o.q, q, size_t(4) * n * 4);
-    std::memcpy(flat.data() + o.op, op, size_t(1) * n * 4);
-    std::memcpy(flat.data() + o.dc, dc, size_t(3) * n * 4);
-    std::memcpy(flat.data() + o.rest, rest, size_t(45) * n * 4);
-    return ts_set_params_flat(x, n, flat.data());
-}
-
-ts_status ts_get_params_flat(ts_ctx* x, float* flat) {
-    TS_CHECK_CTX(x);
-    Context& c = x->c;
-    if (c.N && !flat) return validation(c, "NULL output");
-    CK(cudaSetDevice(c.device));
-    if (c.N) CK(cudaMemcpyAsync(flat, c.params.p, size_t(59) * c.N * 4, cudaMemcpyDeviceToHost, c.stream));
-    CK(cudaStreamSynchronize(c.stream));
-    return TS_OK;
-}
-
-ts_status ts_num_gaussians(const ts_ctx* x, int64_t* n) {
-    if (!x || !n) return TS_ERR_VALIDATION;
-    *n = x->c.N;
-    return TS_OK;
-}
-
-ts_status ts_forward(ts_ctx* x, const ts_camera* cam, const ts_render_config* cfg, float* out_rgb, float* out_T,
-                     uint32_t* out_count) {
-    TS_CHECK_CTX(x);
-    Context& c = x->c;
-    std::string why;
-    if (!valid_camera(cam, &why) || !valid_config(cfg, &why)) return validation(c, why.c_str());
-    CK(cudaSetDevice(c.device));
-    if (ts_status s = run_forward(c, *cam, *cfg); s != TS_OK) return s;
-    const size_t P = size_t(cam->width) * cam->height;
-    if (out_rgb) {
-        launch_chw_to_hwc(c, c.rgb.p, c.hwc_stage.p, int(P));
-        CK(cudaMemcpyAsync(out_rgb, c.hwc_stage.p, 3 * P * 4, cudaMemcpyDeviceToHost, c.stream));
-    }
-    if (out_T) CK(cudaMemcpyAsync(out_T, c.Tfin.p, P * 4, cudaMemcpyDeviceToHost, c.stream));
-    if (out_count) CK(cudaMemcpyAsync(out_count, c.pcount.p, P * 4, cudaMemcpyDeviceToHost, c.stream));
-    if (out_rgb || out_T || out_count) CK(cudaStreamSynchronize(c.stream));
-    return last_launch(c, "ts_forward");
-}
-
-ts_status ts_set_target(ts_ctx* x, int32_t slot, int32_t w, int32_t h, const float* hwc) {
-    TS_CHECK_CTX(x);
-    Context& c = x->c;
-    if (slot < 0 || slot > 4096 || w < 6 || h < 6 || !hwc) return validation(c, "bad target");
-    CK(cudaSetDevice(c.device));
-    const size_t P = size_t(w) * h;
-    if (c.target_w != w || c.target_h != h) {
-        release(c.targets);
-        c.n_target_slots = 0;
-        c.target_w = w;
-        c.target_h = h;
-    }
-    if (slot >= c.n_target_slots) {
-        if (!ensure(c, c.targets, size_t(slot + 1) * 3 * P, true)) return TS_ERR_OOM;
-        c.n_target_slots = slot + 1;
-    }
-    if (ensure_frame(c, std::max(c.fw, w), std::max(c.fh, h)) != TS_OK) return TS_ERR_OOM;
-    CK(cudaMemcpyAsync(c.hwc_stage.p, hwc, 3 * P * 4, cudaMemcpyHostToDevice, c.stream));
-    launch_hwc_to_chw(c, c.hwc_stage.p, c.targets.p + size_t(slot) * 3 * P, int(P));
-    CK(cudaStreamSynchronize(c.stream));
-    return last_launch(c, "ts_set_target");
-}
-
-ts_status ts_loss(ts_ctx* x, const float* target_hwc, int32_t slot, float* out_loss) {
-    TS_CHECK_CTX(x);
-    Context& c = x->c;
-    CK(cudaSetDevice(c.device));
-    return run_loss(c, target_hwc, slot, out_loss);
-}
-
-ts_status ts_backward(ts_ctx* x, const float* dLdC_hwc) {
-    TS_CHECK_CTX(x);
-    Context& c = x->c;
-    CK(cudaSetDevice(c.device));
-    return run_backward(c, dLdC_hwc);
-}
-
-ts_status ts_backward_adam(ts_ctx* x, const float* dLdC_hwc, const ts_adam_config* a) {
-    TS_CHECK_CTX(x);
-    Context& c = x->c;
-    if (!a) return validation(c, "adam config is NULL");
-    CK(cudaSetDevice(c.device));
-    return run_backward_adam(c, dLdC_hwc, *a);
-}
-
-ts_status ts_zero_grads(ts_ctx* x) {
-    TS_CHECK_CTX(x);
-    Context& c = x->c;
-    CK(cudaSetDevice(c.device));
-    if (c.N) CK(cudaMemsetAsync(c.grads.p, 0, size_t(59) * c.N * 4, c.stream));
-    c.grad_state = Context::kGradZero;
-    return TS_OK;
-}
-
-ts_status ts_mark_grads_consumed(ts_ctx* x) {
-    TS_CHECK_CTX(x);
-    Context& c = x->c;
-    if (c.grad_state == Context::kGradLive) c.grad_state = Context::kGradStale;
-    c.view_valid = c.loss_valid = false;
-    return TS_OK;
-}
-
-ts_status ts_grad_buffer(ts_ctx* x, float** p, int64_t* n) {
-    TS_CHECK_CTX(x);
-    if (p) *p = x->c.grads.p;
-    if (n) *n = 59 * x->c.N;
-    return TS_OK;
-}
-
-ts_status ts_param_buffer(ts_ctx* x, float** p, int64_t* n) {
-    TS_CHECK_CTX(x);
-    if (p) *p = x->c.params.p;
-    if (n) *n = 59 * x->c.N;
-    return TS_OK;
-}
-
-ts_status ts_stats_buffer(ts_ctx* x, float** a, float** cnt) {
-    TS_CHECK_CTX(x);
-    if (a) *a = x->c.accum.p;
-    if (cnt) *cnt = x->c.vcount.p;
-    return TS_OK;
-}
-
-ts_status ts_reserve_flat(ts_ctx* x, int64_t min_len) {
-    TS_CHECK_CTX(x);
-    Context& c = x->c;
-    CK(cudaSetDevice(c.device));
-    const size_t L = size_t(59) * c.N;
-    if (min_len < 0) return validation(c, "min_len < 0");
-    if (size_t(min_len) > c.params.cap || size_t(min_len) > c.grads.cap) {
-        if (!ensure(c, c.params, size_t(min_len), true) || !ensure(c, c.grads, size_t(min_len), true))
-            return TS_ERR_OOM;
-    }
-    if (c.params.cap > L) CK(cudaMemsetAsync(c.params.p + L, 0, (c.params.cap - L) * 4, c.stream));
-    if (c.grads.cap > L) CK(cudaMemsetAsync(c.grads.p + L, 0, (c.grads.cap - L) * 4, c.stream));
-    CK(cudaStreamSynchronize(c.stream));
-    return TS_OK;
-}
-
-ts_status ts_adam_step(ts_ctx* x, const ts_adam_config* a) {
-    TS_CHECK_CTX(x);
-    Context& c = x->c;
-    if (!a) return validation(c, "adam config is NULL");
-    CK(cudaSetDevice(c.device));
-    return run_adam(c, *a, 0, 59 * c.N);
-}
-
-ts_status ts_adam_step_range(ts_ctx* x, const ts_adam_config* a, int64_t begin, int64_t end) {
-    TS_CHECK_CTX(x);
-    Context& c = x->c;
-    if (!a) return validation(c, "adam config is NULL");
-    if (begin < 0 || end > 59 * c.N || begin > end) return validation(c, "bad range");
-    CK(cudaSetDevice(c.device));
-    return run_adam(c, *a, begin, end);
-}
-
-ts_status ts_train_step(ts_ctx* x, const ts_camera* cam, const ts_render_config* cfg, const float* target_hwc,
-                        int32_t slot, const ts_adam_config* adam, float* out_loss) {
-    TS_CHECK_CTX(x);
-    Context& c = x->c;
-    std::string why;
-    if (!valid_camera(cam, &why) || !valid_config(cfg, &why)) return validation(c, why.c_str());
-    if (!adam) return validation(c, "adam config is NULL");
-    CK(cudaSetDevice(c.device));
+// one training step on the host-driven path (ts_train_step without a graph; graph replays)
+ts_status run_train_step(Context& c, const ts_camera& camr, const ts_render_config& cfgr, const float* target_hwc,
+                         int32_t slot, const ts_adam_config& adamr, float* out_loss) {
+    const ts_camera* cam = &camr;
+    const ts_render_config* cfg = &cfgr;
+    const ts_adam_config* adam = &adamr;
     // a host target is uploaded on a copy stream while the forward runs (the loss waits for it)
     const size_t P = size_t(cam->width) * cam->height;
     if (target_hwc) {
@@ -776,10 +533,602 @@ ts_status ts_train_step(ts_ctx* x, const ts_camera* cam, const ts_render_config*
     return TS_OK;
 }
 
+// ---------------------------------------------------------------------------
+// CUDA-graph mode of ts_train_step (ts_set_graph).  A training step on a given view, render
+// config, target and optimizer mode is captured once into a CUDA graph (forward, loss,
+// backward, Adam; the host-target upload as a parallel branch) and relaunched each step:
+// no host round trip inside the step (the host-driven path waits for the instance count
+// before sizing the sort launches).  Per-step inputs enter through device memory (the Adam
+// argument block, written before each launch); the per-view camera, config and target address
+// are part of the graph key.  A captured step cannot grow buffers: its capacity check
+// (tile_order_kernel) voids the step (sticky device flag; K9 and Adam skip) when the instance
+// count outgrows the lists or a list needs the radix path, and the host replays every voided
+// step in order on the host path (graph_settle), so the result equals host-driven training.
+// ---------------------------------------------------------------------------
+bool same_view(const GraphEntry& e, const ts_camera& cam, const ts_render_config& cfg, const float* target,
+               int32_t slot, int32_t want_loss, int32_t mode, int64_t N) {
+    return std::memcmp(&e.cam, &cam, sizeof(cam)) == 0 && std::memcmp(&e.cfg, &cfg, sizeof(cfg)) == 0 &&
+           e.target == target && e.slot == (target ? -1 : slot) && e.want_loss == want_loss && e.mode == mode &&
+           e.N == N;
+}
+
+void drop_graphs(Context& c) {
+    for (GraphEntry& e : c.graphs)
+        if (e.exec) cudaGraphExecDestroy(e.exec);
+    c.graphs.clear();
+    c.graph_seen.clear();
+}
+
+bool graph_eligible(const Context& c, const ts_camera& cam, const ts_render_config& cfg, const ts_adam_config& a) {
+    const int Tn = ((cam.width + 15) / 16) * ((cam.height + 15) / 16);
+    // (a live gradient buffer would be accumulated into by the host path; the graph overwrites)
+    return c.graph_on && !c.profiling && c.binning_mode == 0 && bin_supported(Tn) && a.mode >= 0 && a.mode <= 2 &&
+           cfg.aa_mode != 1 && c.N > 0 && c.grad_state != Context::kGradLive;
+}
+
+// every launched graph step verified; voided steps replayed on the host path.  block: wait for the
+// last launch (else only look if it has completed)
+ts_status graph_check(Context& c, bool block) {
+    if (c.glog.empty()) return TS_OK;
+    if (block) {
+        CK(cudaEventSynchronize(c.gstep_ev));
+    } else {
+        const cudaError_t q = cudaEventQuery(c.gstep_ev);
+        if (q == cudaErrorNotReady) return TS_OK;
+        if (q != cudaSuccess) return cuda_fail(c, q, "graph step");
+    }
+    if (*c.gflag_host == 0u) {
+        c.glog.clear();
+        return TS_OK;
+    }
+    // a step outgrew its captured buffers: it and every later graph step were no-ops
+    CK(cudaStreamSynchronize(c.stream));
+    CK(cudaMemsetAsync(c.counters.p + kGraphFlag, 0, sizeof(uint32_t), c.stream));
+    *c.gflag_host = 0u;
+    drop_graphs(c);
+    std::vector<GraphStep> steps;
+    steps.swap(c.glog);
+    for (const GraphStep& st : steps) {
+        if (ts_status s = run_train_step(c, st.cam, st.cfg, st.target, st.slot, st.adam, nullptr); s != TS_OK) return s;
+        ++c.graph_replays;
+    }
+    CK(cudaStreamSynchronize(c.stream));
+    return TS_OK;
+}
+
+ts_status graph_settle(Context& c) {
+    if (c.glog.empty() && !c.I_on_device) return TS_OK;
+    if (ts_status s = graph_check(c, true); s != TS_OK) return s;
+    if (c.I_on_device && c.view_valid) {  // instance count of the last graph-rendered view
+        const int Tn = ((c.cam.width + 15) / 16) * ((c.cam.height + 15) / 16);
+        uint32_t I = 0;
+        CK(cudaMemcpy(&I, c.starts.p + Tn, sizeof(I), cudaMemcpyDeviceToHost));
+        c.I = I;
+    }
+    c.I_on_device = false;
+    return TS_OK;
+}
+
+#define TS_SETTLE(c)                                             \
+    do {                                                         \
+        if (ts_status s_ = graph_settle(c); s_ != TS_OK) return s_; \
+    } while (0)
+
+ts_status graph_capture(Context& c, const ts_camera& cam, const ts_render_config& cfg, const float* target_hwc,
+                        int32_t slot, int want_loss, const ts_adam_config& adam, cudaGraphExec_t* out,
+                        int64_t* kernels) {
+    // buffers sized by the view's host-path step; the lists get 25% headroom (growth beyond it
+    // voids a step and is replayed)
+    const size_t capI = size_t(c.I) + size_t(c.I) / 4 + 4096;
+    for (int k = 0; k < 2; ++k)
+        if (c.ival[k].cap < capI && !ensure(c, c.ival[k], capI)) return TS_ERR_OOM;
+    if (!ensure_grow(c, c.sortmp, capI)) return TS_ERR_OOM;
+    const size_t P = size_t(cam.width) * cam.height;
+    if (target_hwc && !ensure(c, c.tgt_stage, 3 * P)) return TS_ERR_OOM;
+    CK(cudaStreamSynchronize(c.stream));
+    const int64_t launches0 = c.launches;  // captured launches are counted when the graph runs
+    c.capturing = c.gmode = true;
+    cudaError_t e = cudaStreamBeginCapture(c.stream, cudaStreamCaptureModeThreadLocal);
+    if (e != cudaSuccess) {
+        c.capturing = c.gmode = false;
+        return cuda_fail(c, e, "cudaStreamBeginCapture");
+    }
+    ts_status st = TS_OK;
+    do {
+        if (target_hwc) {  // host target: a parallel branch of the graph (copy node + layout kernel)
+            if ((e = cudaEventRecord(c.copy_fork, c.stream)) != cudaSuccess) break;
+            if ((e = cudaStreamWaitEvent(c.copy_stream, c.copy_fork, 0)) != cudaSuccess) break;
+            if ((e = cudaMemcpyAsync(c.tgt_stage.p, target_hwc, 3 * P * 4, cudaMemcpyHostToDevice, c.copy_stream)) !=
+                cudaSuccess)
+                break;
+            if ((e = cudaEventRecord(c.copy_join, c.copy_stream)) != cudaSuccess) break;
+        }
+        if ((st = run_forward_graph(c, cam, cfg)) != TS_OK) break;
+        if (target_hwc) {
+            if ((e = cudaStreamWaitEvent(c.stream, c.copy_join, 0)) != cudaSuccess) break;
+            launch_hwc_to_chw(c, c.tgt_stage.p, c.tgt.p, int(P));
+            if ((st = run_loss(c, nullptr, slot, nullptr, c.tgt.p)) != TS_OK) break;
+        } else if ((st = run_loss(c, nullptr, slot, nullptr)) != TS_OK) {
+            break;
+        }
+        // the step's capacity verdict (set by the tile order) and the loss sums to pinned memory
+        if ((e = cudaMemcpyAsync(c.gflag_host, c.counters.p + kGraphFlag, 4, cudaMemcpyDeviceToHost, c.stream)) !=
+            cudaSuccess)
+            break;
+        if (want_loss) {
+            if ((e = cudaMemcpyAsync(c.loss_host, c.loss_acc.p, 2 * sizeof(double), cudaMemcpyDeviceToHost,
+                                     c.stream)) != cudaSuccess)
+                break;
+            // an external event node: the host waits on it after each launch (a plain record in a
+            // capturing stream would only be a fork/join dependency)
+            if ((e = cudaEventRecordWithFlags(c.loss_ev, c.stream, cudaEventRecordExternal)) != cudaSuccess) break;
+        }
+        c.grad_state = Context::kGradStale;  // the captured backward overwrites every row
+        if ((st = run_backward(c, nullptr)) != TS_OK) break;
+        ts_adam_config a = adam;
+        a.zero_grads = 0;
+        stage_begin(c, 10);
+        launch_adam(c, a, 0, 59 * c.N);
+        stage_end(c, 10);
+    } while (false);
+    cudaGraph_t g = nullptr;
+    const cudaError_t e2 = cudaStreamEndCapture(c.stream, &g);
+    c.capturing = c.gmode = false;
+    *kernels = c.launches - launches0;
+    c.launches = launches0;
+    if (st == TS_OK && e != cudaSuccess) st = cuda_fail(c, e, "graph capture");
+    if (st == TS_OK && e2 != cudaSuccess) st = cuda_fail(c, e2, "cudaStreamEndCapture");
+    if (st == TS_OK) {
+        e = cudaGraphInstantiate(out, g, 0);
+        if (e != cudaSuccess) st = cuda_fail(c, e, "cudaGraphInstantiate");
+    }
+    if (g) cudaGraphDestroy(g);
+    cudaGetLastError();
+    c.view_valid = c.loss_valid = false;
+    ++c.graph_captures;
+    return st;
+}
+
+ts_status graph_step(Context& c, const ts_camera& cam, const ts_render_config& cfg, const float* target_hwc,
+                     int32_t slot, const ts_adam_config& adam, float* out_loss) {
+    if (!(adam.bc1 > 0.f) || !(adam.bc2 > 0.f)) return validation(c, "bias corrections must be > 0 (step >= 1)");
+    if (!target_hwc && (slot < 0 || slot >= c.n_target_slots || c.target_w != cam.width || c.target_h != cam.height))
+        return validation(c, "target slot out of range / size != view size");
+    if (c.glog.size() > 32) {
+        if (ts_status s = graph_check(c, true); s != TS_OK) return s;
+    } else if (ts_status s = graph_check(c, false); s != TS_OK) {
+        return s;
+    }
+    const int want = out_loss ? 1 : 0;
+    GraphEntry* ent = nullptr;
+    for (GraphEntry& e : c.graphs)
+        if (e.gen == c.gen && same_view(e, cam, cfg, target_hwc, slot, want, adam.mode, c.N)) ent = &e;
+    if (!ent) {
+        bool seen = false;
+        const GraphEntry* sv = nullptr;
+        for (const GraphEntry& e : c.graph_seen)
+            if (e.gen == c.gen && same_view(e, cam, cfg, target_hwc, slot, want, adam.mode, c.N)) sv = &e;
+        seen = sv != nullptr;
+        if (sv) {  // the view's own host-path sizes: sort grid hints and list capacity
+            std::memcpy(c.bin_class, sv->cls, sizeof(c.bin_class));
+            c.I = sv->I;
+        }
+        if (!seen) {
+            // first time for this view (or buffers changed): a host-path step sizes the buffers
+            if (ts_status s = graph_settle(c); s != TS_OK) return s;
+            if (ts_status s = run_train_step(c, cam, cfg, target_hwc, slot, adam, out_loss); s != TS_OK) return s;
+            if (c.graph_seen.size() >= 64) c.graph_seen.erase(c.graph_seen.begin());  // bounded
+            GraphEntry seen{cam, cfg, target_hwc, target_hwc ? -1 : slot, want, adam.mode, c.N, c.gen, nullptr, 0,
+                            {0, 0, 0, 0, 0, 0, 0}, c.I};
+            std::memcpy(seen.cls, c.bin_class, sizeof(seen.cls));
+            c.graph_seen.push_back(seen);
+            return TS_OK;
+        }
+        if (ts_status s = graph_settle(c); s != TS_OK) return s;
+        cudaGraphExec_t exec = nullptr;
+        int64_t kernels = 0;
+        if (ts_status s = graph_capture(c, cam, cfg, target_hwc, slot, want, adam, &exec, &kernels); s != TS_OK) {
+            c.err = "graph capture failed (" + c.err + ")";
+            return s;
+        }
+        if (c.graphs.size() >= 32) {  // bounded cache: drop the oldest graph
+            cudaGraphExecDestroy(c.graphs.front().exec);
+            c.graphs.erase(c.graphs.begin());
+        }
+        c.graphs.push_back(GraphEntry{cam, cfg, target_hwc, target_hwc ? -1 : slot, want, adam.mode, c.N, c.gen, exec,
+                                      kernels, {0, 0, 0, 0, 0, 0, 0}, c.I});
+        ent = &c.graphs.back();
+    }
+    const size_t nb = adam_args_bytes(adam, c.adam_dev_bytes);
+    CK(cudaMemcpyAsync(c.adam_dev, c.adam_dev_bytes, nb, cudaMemcpyHostToDevice, c.stream));
+    CK(cudaGraphLaunch(ent->exec, c.stream));
+    CK(cudaEventRecord(c.gstep_ev, c.stream));
+    c.glog.push_back(GraphStep{cam, cfg, target_hwc, slot, adam});
+    ++c.graph_launches;
+    c.launches += ent->kernels;
+    c.grad_state = Context::kGradStale;
+    c.cam = cam;
+    c.cfg = cfg;
+    c.view_valid = true;  // the view's buffers (frame, lists) hold this step's forward
+    c.loss_valid = false;
+    c.I_on_device = true;
+    if (out_loss) {
+        CK(cudaEventSynchronize(c.loss_ev));
+        if (*c.gflag_host) {  // voided: replay now and report the replayed loss
+            CK(cudaEventSynchronize(c.gstep_ev));
+            c.glog.pop_back();
+            if (ts_status s = graph_check(c, true); s != TS_OK) return s;  // earlier voided steps
+            *c.gflag_host = 0u;
+            CK(cudaMemsetAsync(c.counters.p + kGraphFlag, 0, sizeof(uint32_t), c.stream));
+            drop_graphs(c);
+            ++c.graph_replays;
+            return run_train_step(c, cam, cfg, target_hwc, slot, adam, out_loss);
+        }
+        const double M = 3.0 * double(cam.width) * cam.height;
+        *out_loss = float(0.8 * c.loss_host[0] / M + 0.2 * (1.0 - c.loss_host[1] / M));
+    }
+    return TS_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ts_version(void) { return "tilesplat-b200 0.1 (sm_100a)"; }
+
+ts_status ts_create(int32_t device, void* stream, ts_ctx** out) {
+    if (!out) return TS_ERR_VALIDATION;
+    *out = nullptr;
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+        cudaGetLastError();
+        return TS_ERR_CUDA;
+    }
+    if (device < 0 || device >= ndev) return TS_ERR_VALIDATION;
+    cudaDeviceProp prop;
+    if (cudaGetDeviceProperties(&prop, device) != cudaSuccess) return TS_ERR_CUDA;
+    if (prop.major < 10) return TS_ERR_CUDA;  // built for sm_100a only; no fallback
+    ts_ctx* x = new (std::nothrow) ts_ctx();
+    if (!x) return TS_ERR_OOM;
+    Context& c = x->c;
+    c.device = device;
+    c.sm_count = prop.multiProcessorCount;
+    if (cudaSetDevice(device) != cudaSuccess) {
+        delete x;
+        return TS_ERR_CUDA;
+    }
+    if (stream) {
+        c.stream = static_cast<cudaStream_t>(stream);
+    } else {
+        if (cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking) != cudaSuccess) {
+            delete x;
+            return TS_ERR_CUDA;
+        }
+        c.own_stream = true;
+    }
+    if (!ensure(c, c.counters, 16) || !ensure(c, c.loss_acc, 2)) {
+        delete x;
+        return TS_ERR_OOM;
+    }
+    cudaMemsetAsync(c.counters.p, 0, 16 * 4, c.stream);
+    // per-step plumbing created once here, never inside a timed step: the host-target copy
+    // stream, the pinned loss / graph-flag slots, the graph-step event and the device block of
+    // the per-step Adam arguments (graph mode)
+    if (cudaStreamCreateWithFlags(&c.copy_stream, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c.copy_fork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c.copy_join, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c.loss_ev, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c.gstep_ev, cudaEventDisableTiming) != cudaSuccess ||
+        cudaMallocHost(reinterpret_cast<void**>(&c.loss_host), 2 * sizeof(double)) != cudaSuccess ||
+        cudaMallocHost(reinterpret_cast<void**>(&c.gflag_host), sizeof(uint32_t)) != cudaSuccess ||
+        cudaMalloc(&c.adam_dev, sizeof(c.adam_dev_bytes)) != cudaSuccess) {
+        cudaGetLastError();
+        delete x;
+        return TS_ERR_CUDA;
+    }
+    *c.gflag_host = 0u;
+    if (ensure_gaussian_buffers(c, 1) != TS_OK) {
+        delete x;
+        return TS_ERR_OOM;
+    }
+    if (cudaStreamSynchronize(c.stream) != cudaSuccess) {
+        delete x;
+        return TS_ERR_CUDA;
+    }
+    *out = x;
+    return TS_OK;
+}
+
+ts_status ts_destroy(ts_ctx* x) {
+    TS_CHECK_CTX(x);
+    Context& c = x->c;
+    cudaSetDevice(c.device);
+    cudaStreamSynchronize(c.stream);
+    drop_graphs(c);
+    if (c.gstep_ev) cudaEventDestroy(c.gstep_ev);
+    if (c.gflag_host) cudaFreeHost(c.gflag_host);
+    if (c.adam_dev) cudaFree(c.adam_dev);
+    release(c.params), release(c.grads), release(c.m), release(c.v), release(c.accum), release(c.vcount);
+    release(c.splat), release(c.ryv), release(c.rect), release(c.tcount), release(c.offsets), release(c.g2d), release(c.vis);
+    for (int k = 0; k < 2; ++k) {
+        release(c.dkey[k]), release(c.dperm[k]), release(c.tkey[k]), release(c.tkey32[k]), release(c.ival[k]);
+    }
+    release(c.starts), release(c.rhist), release(c.scan_state), release(c.scan_tmp), release(c.counters);
+    release(c.rgb), release(c.Tfin), release(c.dLdC), release(c.hwc_stage), release(c.tgt), release(c.pcount);
+    release(c.loss_acc), release(c.targets), release(c.dens);
+    release(c.binH), release(c.bintot), release(c.tile_order), release(c.tile_proc), release(c.bwd_order), release(c.sortmp), release(c.spare), release(c.cams), release(c.mcode[0]), release(c.mcode[1]),
+        release(c.midx[0]), release(c.midx[1]), release(c.tgt_stage), release(c.nu_hat);
+    for (size_t k = 0; k < c.ev_b.size(); ++k) {
+        cudaEventDestroy(c.ev_b[k]);
+        cudaEventDestroy(c.ev_e[k]);
+    }
+    for (int k = 0; k < 2; ++k) {
+        if (c.side[k]) cudaStreamDestroy(c.side[k]);
+        if (c.join_ev[k]) cudaEventDestroy(c.join_ev[k]);
+    }
+    if (c.fork_ev) cudaEventDestroy(c.fork_ev);
+    if (c.copy_stream) cudaStreamDestroy(c.copy_stream);
+    if (c.bin_host) cudaFreeHost(c.bin_host);
+    if (c.bin_ev) cudaEventDestroy(c.bin_ev);
+    if (c.loss_host) cudaFreeHost(c.loss_host);
+    if (c.loss_ev) cudaEventDestroy(c.loss_ev);
+    if (c.copy_fork) cudaEventDestroy(c.copy_fork);
+    if (c.copy_join) cudaEventDestroy(c.copy_join);
+    if (c.own_stream) cudaStreamDestroy(c.stream);
+    delete x;
+    return TS_OK;
+}
+
+const char* ts_last_error(const ts_ctx* x) { return x ? x->c.err.c_str() : "null context"; }
+
+ts_status ts_synchronize(ts_ctx* x) {
+    TS_CHECK_CTX(x);
+    Context& c = x->c;
+    CK(cudaSetDevice(c.device));
+    TS_SETTLE(c);
+    CK(cudaStreamSynchronize(c.stream));
+    return TS_OK;
+}
+
+ts_status ts_set_params_flat(ts_ctx* x, int64_t n, const float* flat) {
+    TS_CHECK_CTX(x);
+    Context& c = x->c;
+    if (n < 0 || (n > 0 && !flat)) return validation(c, "bad parameter array");
+    if (n > kMaxGaussians) return validation(c, "N exceeds the 32-bit flat-index limit (~72.8M Gaussians)");
+    CK(cudaSetDevice(c.device));
+    TS_SETTLE(c);
+    if (ensure_gaussian_buffers(c, n) != TS_OK) return TS_ERR_OOM;
+    if (n != c.N) c.nu_valid = false;  // sampling rates are per row (kept across same-size updates)
+    c.N = n;
+    if (n) CK(cudaMemcpyAsync(c.params.p, flat, size_t(59) * n * 4, cudaMemcpyHostToDevice, c.stream));
+    if (ts_status s = zero_state(c); s != TS_OK) return s;
+    c.grad_state = Context::kGradZero;
+    c.view_valid = c.loss_valid = false;
+    CK(cudaStreamSynchronize(c.stream));
+    return TS_OK;
+}
+
+ts_status ts_set_params(ts_ctx* x, int64_t n, const float* means, const float* ls, const float* q, const float* op,
+                        const float* dc, const float* rest) {
+    TS_CHECK_CTX(x);
+    Context& c = x->c;
+    if (n < 0) return validation(c, "n < 0");
+    if (n > 0 && (!means || !ls || !q || !op || !dc || !rest)) return validation(c, "NULL parameter array");
+    std::vector<float> flat(size_t(59) * n);
+    const Off o(n);
+    std::memcpy(flat.data() + o.means, means, size_t(3) * n * 4);
+    std::memcpy(flat.data() + o.ls, ls, size_t(3) * n * 4);
+    std::memcpy(flat.data() + o.q, q, size_t(4) * n * 4);
+    std::memcpy(flat.data() + o.op, op, size_t(1) * n * 4);
+    std::memcpy(flat.data() + o.dc, dc, size_t(3) * n * 4);
+    std::memcpy(flat.data() + o.rest, rest, size_t(45) * n * 4);
+    return ts_set_params_flat(x, n, flat.data());
+}
+
+ts_status ts_get_params_flat(ts_ctx* x, float* flat) {
+    TS_CHECK_CTX(x);
+    Context& c = x->c;
+    if (c.N && !flat) return validation(c, "NULL output");
+    CK(cudaSetDevice(c.device));
+    TS_SETTLE(c);
+    if (c.N) CK(cudaMemcpyAsync(flat, c.params.p, size_t(59) * c.N * 4, cudaMemcpyDeviceToHost, c.stream));
+    CK(cudaStreamSynchronize(c.stream));
+    return TS_OK;
+}
+
+ts_status ts_num_gaussians(const ts_ctx* x, int64_t* n) {
+    if (!x || !n) return TS_ERR_VALIDATION;
+    *n = x->c.N;
+    return TS_OK;
+}
+
+ts_status ts_forward(ts_ctx* x, const ts_camera* cam, const ts_render_config* cfg, float* out_rgb, float* out_T,
+                     uint32_t* out_count) {
+    TS_CHECK_CTX(x);
+    Context& c = x->c;
+    std::string why;
+    if (!valid_camera(cam, &why) || !valid_config(cfg, &why)) return validation(c, why.c_str());
+    CK(cudaSetDevice(c.device));
+    TS_SETTLE(c);
+    if (ts_status s = run_forward(c, *cam, *cfg); s != TS_OK) return s;
+    const size_t P = size_t(cam->width) * cam->height;
+    if (out_rgb) {
+        launch_chw_to_hwc(c, c.rgb.p, c.hwc_stage.p, int(P));
+        CK(cudaMemcpyAsync(out_rgb, c.hwc_stage.p, 3 * P * 4, cudaMemcpyDeviceToHost, c.stream));
+    }
+    if (out_T) CK(cudaMemcpyAsync(out_T, c.Tfin.p, P * 4, cudaMemcpyDeviceToHost, c.stream));
+    if (out_count) CK(cudaMemcpyAsync(out_count, c.pcount.p, P * 4, cudaMemcpyDeviceToHost, c.stream));
+    if (out_rgb || out_T || out_count) CK(cudaStreamSynchronize(c.stream));
+    return last_launch(c, "ts_forward");
+}
+
+ts_status ts_set_target(ts_ctx* x, int32_t slot, int32_t w, int32_t h, const float* hwc) {
+    TS_CHECK_CTX(x);
+    Context& c = x->c;
+    if (slot < 0 || slot > 4096 || w < 6 || h < 6 || !hwc) return validation(c, "bad target");
+    CK(cudaSetDevice(c.device));
+    TS_SETTLE(c);
+    const size_t P = size_t(w) * h;
+    if (c.target_w != w || c.target_h != h) {
+        release(c.targets);
+        c.n_target_slots = 0;
+        c.target_w = w;
+        c.target_h = h;
+    }
+    if (slot >= c.n_target_slots) {
+        if (!ensure(c, c.targets, size_t(slot + 1) * 3 * P, true)) return TS_ERR_OOM;
+        c.n_target_slots = slot + 1;
+    }
+    if (ensure_frame(c, std::max(c.fw, w), std::max(c.fh, h)) != TS_OK) return TS_ERR_OOM;
+    CK(cudaMemcpyAsync(c.hwc_stage.p, hwc, 3 * P * 4, cudaMemcpyHostToDevice, c.stream));
+    launch_hwc_to_chw(c, c.hwc_stage.p, c.targets.p + size_t(slot) * 3 * P, int(P));
+    CK(cudaStreamSynchronize(c.stream));
+    return last_launch(c, "ts_set_target");
+}
+
+ts_status ts_loss(ts_ctx* x, const float* target_hwc, int32_t slot, float* out_loss) {
+    TS_CHECK_CTX(x);
+    Context& c = x->c;
+    CK(cudaSetDevice(c.device));
+    TS_SETTLE(c);
+    return run_loss(c, target_hwc, slot, out_loss);
+}
+
+ts_status ts_backward(ts_ctx* x, const float* dLdC_hwc) {
+    TS_CHECK_CTX(x);
+    Context& c = x->c;
+    CK(cudaSetDevice(c.device));
+    TS_SETTLE(c);
+    return run_backward(c, dLdC_hwc);
+}
+
+ts_status ts_backward_adam(ts_ctx* x, const float* dLdC_hwc, const ts_adam_config* a) {
+    TS_CHECK_CTX(x);
+    Context& c = x->c;
+    if (!a) return validation(c, "adam config is NULL");
+    CK(cudaSetDevice(c.device));
+    TS_SETTLE(c);
+    return run_backward_adam(c, dLdC_hwc, *a);
+}
+
+ts_status ts_zero_grads(ts_ctx* x) {
+    TS_CHECK_CTX(x);
+    Context& c = x->c;
+    CK(cudaSetDevice(c.device));
+    TS_SETTLE(c);
+    if (c.N) CK(cudaMemsetAsync(c.grads.p, 0, size_t(59) * c.N * 4, c.stream));
+    c.grad_state = Context::kGradZero;
+    return TS_OK;
+}
+
+ts_status ts_mark_grads_consumed(ts_ctx* x) {
+    TS_CHECK_CTX(x);
+    TS_SETTLE(x->c);
+    Context& c = x->c;
+    if (c.grad_state == Context::kGradLive) c.grad_state = Context::kGradStale;
+    c.view_valid = c.loss_valid = false;
+    return TS_OK;
+}
+
+ts_status ts_grad_buffer(ts_ctx* x, float** p, int64_t* n) {
+    TS_CHECK_CTX(x);
+    TS_SETTLE(x->c);
+    if (p) *p = x->c.grads.p;
+    if (n) *n = 59 * x->c.N;
+    return TS_OK;
+}
+
+ts_status ts_param_buffer(ts_ctx* x, float** p, int64_t* n) {
+    TS_CHECK_CTX(x);
+    TS_SETTLE(x->c);
+    if (p) *p = x->c.params.p;
+    if (n) *n = 59 * x->c.N;
+    return TS_OK;
+}
+
+ts_status ts_stats_buffer(ts_ctx* x, float** a, float** cnt) {
+    TS_CHECK_CTX(x);
+    TS_SETTLE(x->c);
+    if (a) *a = x->c.accum.p;
+    if (cnt) *cnt = x->c.vcount.p;
+    return TS_OK;
+}
+
+ts_status ts_reserve_flat(ts_ctx* x, int64_t min_len) {
+    TS_CHECK_CTX(x);
+    Context& c = x->c;
+    CK(cudaSetDevice(c.device));
+    TS_SETTLE(c);
+    const size_t L = size_t(59) * c.N;
+    if (min_len < 0) return validation(c, "min_len < 0");
+    if (size_t(min_len) > c.params.cap || size_t(min_len) > c.grads.cap) {
+        if (!ensure(c, c.params, size_t(min_len), true) || !ensure(c, c.grads, size_t(min_len), true))
+            return TS_ERR_OOM;
+    }
+    if (c.params.cap > L) CK(cudaMemsetAsync(c.params.p + L, 0, (c.params.cap - L) * 4, c.stream));
+    if (c.grads.cap > L) CK(cudaMemsetAsync(c.grads.p + L, 0, (c.grads.cap - L) * 4, c.stream));
+    CK(cudaStreamSynchronize(c.stream));
+    return TS_OK;
+}
+
+ts_status ts_adam_step(ts_ctx* x, const ts_adam_config* a) {
+    TS_CHECK_CTX(x);
+    Context& c = x->c;
+    if (!a) return validation(c, "adam config is NULL");
+    CK(cudaSetDevice(c.device));
+    TS_SETTLE(c);
+    return run_adam(c, *a, 0, 59 * c.N);
+}
+
+ts_status ts_adam_step_range(ts_ctx* x, const ts_adam_config* a, int64_t begin, int64_t end) {
+    TS_CHECK_CTX(x);
+    Context& c = x->c;
+    if (!a) return validation(c, "adam config is NULL");
+    if (begin < 0 || end > 59 * c.N || begin > end) return validation(c, "bad range");
+    CK(cudaSetDevice(c.device));
+    TS_SETTLE(c);
+    return run_adam(c, *a, begin, end);
+}
+
+ts_status ts_train_step(ts_ctx* x, const ts_camera* cam, const ts_render_config* cfg, const float* target_hwc,
+                        int32_t slot, const ts_adam_config* adam, float* out_loss) {
+    TS_CHECK_CTX(x);
+    Context& c = x->c;
+    std::string why;
+    if (!valid_camera(cam, &why) || !valid_config(cfg, &why)) return validation(c, why.c_str());
+    if (!adam) return validation(c, "adam config is NULL");
+    CK(cudaSetDevice(c.device));
+    if (graph_eligible(c, *cam, *cfg, *adam)) return graph_step(c, *cam, *cfg, target_hwc, slot, *adam, out_loss);
+    TS_SETTLE(c);
+    return run_train_step(c, *cam, *cfg, target_hwc, slot, *adam, out_loss);
+}
+
+ts_status ts_set_graph(ts_ctx* x, int32_t on) {
+    TS_CHECK_CTX(x);
+    Context& c = x->c;
+    CK(cudaSetDevice(c.device));
+    TS_SETTLE(c);
+    c.graph_on = on != 0;
+    if (!c.graph_on) drop_graphs(c);
+    return TS_OK;
+}
+
+ts_status ts_graph_stats(ts_ctx* x, int64_t out[4]) {
+    TS_CHECK_CTX(x);
+    Context& c = x->c;
+    if (!out) return validation(c, "NULL output");
+    out[0] = c.graph_launches;
+    out[1] = c.graph_captures;
+    out[2] = c.graph_replays;
+    out[3] = int64_t(c.graphs.size());
+    return TS_OK;
+}
+
 ts_status ts_opacity_reset(ts_ctx* x) {
     TS_CHECK_CTX(x);
     Context& c = x->c;
     CK(cudaSetDevice(c.device));
+    TS_SETTLE(c);
     launch_opacity_reset(c, float(std::log(0.01 / 0.99)));
     c.view_valid = c.loss_valid = false;
     return last_launch(c, "opacity_reset");
@@ -791,6 +1140,7 @@ ts_status ts_densify(ts_ctx* x, float grad_thresh, float extent, uint64_t seed, 
     Context& c = x->c;
     if (!(extent > 0.f)) return validation(c, "extent must be > 0");
     CK(cudaSetDevice(c.device));
+    TS_SETTLE(c);
     int64_t st[3] = {0, 0, 0};
     const float log_small = float(std::log(0.01 * double(extent)));
     const float log_big = float(std::log(0.1 * double(extent)));
@@ -809,6 +1159,7 @@ ts_status ts_morton_reorder(ts_ctx* x, uint32_t* perm) {
     TS_CHECK_CTX(x);
     Context& c = x->c;
     CK(cudaSetDevice(c.device));
+    TS_SETTLE(c);
     if (c.grad_state == Context::kGradLive) return validation(c, "morton_reorder between backward and optimizer step");
     if (!launch_morton_reorder(c, perm)) return c.err.empty() ? TS_ERR_CUDA : TS_ERR_OOM;
     c.view_valid = c.loss_valid = false;
@@ -820,6 +1171,7 @@ ts_status ts_set_state(ts_ctx* x, const float* grads, const float* m, const floa
     TS_CHECK_CTX(x);
     Context& c = x->c;
     CK(cudaSetDevice(c.device));
+    TS_SETTLE(c);
     const size_t L = size_t(59) * c.N, N = size_t(c.N);
     if (grads) {
         CK(cudaMemcpyAsync(c.grads.p, grads, L * 4, cudaMemcpyHostToDevice, c.stream));
@@ -837,6 +1189,7 @@ ts_status ts_get_state(ts_ctx* x, float* grads, float* m, float* v, float* accum
     TS_CHECK_CTX(x);
     Context& c = x->c;
     CK(cudaSetDevice(c.device));
+    TS_SETTLE(c);
     const size_t L = size_t(59) * c.N, N = size_t(c.N);
     if (grads) CK(cudaMemcpyAsync(grads, c.grads.p, L * 4, cudaMemcpyDeviceToHost, c.stream));
     if (m) CK(cudaMemcpyAsync(m, c.m.p, L * 4, cudaMemcpyDeviceToHost, c.stream));
@@ -859,6 +1212,7 @@ ts_status ts_compute_sampling_rates(ts_ctx* x, const ts_camera* cams, int32_t n_
         dc[size_t(k)] = make_devcam(cams[k]);
     }
     CK(cudaSetDevice(c.device));
+    TS_SETTLE(c);
     if (!launch_sampling_rates(c, dc.data(), n_cams, extent)) return c.err.empty() ? TS_ERR_CUDA : TS_ERR_OOM;
     c.nu_valid = true;
     return last_launch(c, "compute_sampling_rates");
@@ -869,6 +1223,7 @@ ts_status ts_set_sampling_rates(ts_ctx* x, const float* nu) {
     Context& c = x->c;
     if (!nu) return validation(c, "NULL sampling rates");
     CK(cudaSetDevice(c.device));
+    TS_SETTLE(c);
     if (c.N) CK(cudaMemcpyAsync(c.nu_hat.p, nu, size_t(c.N) * 4, cudaMemcpyHostToDevice, c.stream));
     c.nu_valid = true;
     return TS_OK;
@@ -880,6 +1235,7 @@ ts_status ts_get_sampling_rates(ts_ctx* x, float* nu) {
     if (!nu) return validation(c, "NULL output");
     if (!c.nu_valid) return validation(c, "sampling rates not computed for the current store");
     CK(cudaSetDevice(c.device));
+    TS_SETTLE(c);
     if (c.N) CK(cudaMemcpyAsync(nu, c.nu_hat.p, size_t(c.N) * 4, cudaMemcpyDeviceToHost, c.stream));
     CK(cudaStreamSynchronize(c.stream));
     return TS_OK;
@@ -891,6 +1247,7 @@ ts_status ts_apply_3d_filter_clip(ts_ctx* x, float kappa3d) {
     if (!(kappa3d > 0.f)) return validation(c, "kappa3d must be > 0");
     if (!c.nu_valid) return validation(c, "apply_3d_filter_clip needs ts_compute_sampling_rates");
     CK(cudaSetDevice(c.device));
+    TS_SETTLE(c);
     launch_filter3d_clip(c, kappa3d);
     c.view_valid = c.loss_valid = false;
     return last_launch(c, "apply_3d_filter_clip");
@@ -898,6 +1255,7 @@ ts_status ts_apply_3d_filter_clip(ts_ctx* x, float kappa3d) {
 
 ts_status ts_set_binning(ts_ctx* x, int32_t mode) {
     TS_CHECK_CTX(x);
+    TS_SETTLE(x->c);
     Context& c = x->c;
     if (mode < 0 || mode > 1) return validation(c, "binning mode must be 0 (auto) or 1 (radix)");
     c.binning_mode = mode;
@@ -916,6 +1274,7 @@ ts_status ts_debug_loss_grad(ts_ctx* x, float* dLdC_hwc) {
     if (!c.loss_valid) return validation(c, "no training_loss state");
     if (!dLdC_hwc) return validation(c, "NULL output");
     CK(cudaSetDevice(c.device));
+    TS_SETTLE(c);
     const size_t P = size_t(c.fw) * c.fh;
     launch_chw_to_hwc(c, c.dLdC.p, c.hwc_stage.p, int(P));
     CK(cudaMemcpyAsync(dLdC_hwc, c.hwc_stage.p, 3 * P * 4, cudaMemcpyDeviceToHost, c.stream));
@@ -928,6 +1287,7 @@ ts_status ts_debug_preprocess(ts_ctx* x, float* splat12, int32_t* rect4, uint32_
     Context& c = x->c;
     if (!c.view_valid) return validation(c, "no forward state");
     CK(cudaSetDevice(c.device));
+    TS_SETTLE(c);
     const size_t N = size_t(c.N);
     std::vector<float4> sp(3 * N);
     std::vector<uint4> rc(N);
@@ -961,6 +1321,7 @@ ts_status ts_debug_instances(ts_ctx* x, int64_t* n_inst, uint64_t* keys, uint32_
     Context& c = x->c;
     if (!c.view_valid) return validation(c, "no forward state");
     CK(cudaSetDevice(c.device));
+    TS_SETTLE(c);
     if (n_inst) *n_inst = c.I;
     if (!keys && !vals && !ranges) return TS_OK;
     const size_t I = size_t(c.I), N = size_t(c.N);
@@ -996,6 +1357,7 @@ ts_status ts_debug_grad2d(ts_ctx* x, const float* dLdC_hwc, float* g2d9) {
     if (!c.view_valid) return validation(c, "no forward state");
     if (!dLdC_hwc || !g2d9) return validation(c, "NULL argument");
     CK(cudaSetDevice(c.device));
+    TS_SETTLE(c);
     const size_t N = size_t(c.N);
     if (ts_status s = upload_image_chw(c, dLdC_hwc, c.dLdC.p); s != TS_OK) return s;
     CK(cudaMemsetAsync(c.g2d.p, 0, 3 * N * 16, c.stream));
@@ -1017,6 +1379,7 @@ ts_status ts_view_stats(ts_ctx* x, int64_t out[4]) {
     Context& c = x->c;
     if (!out) return validation(c, "NULL output");
     CK(cudaSetDevice(c.device));
+    TS_SETTLE(c);
     uint32_t cnt[3];
     CK(cudaMemcpyAsync(cnt, c.counters.p, sizeof(cnt), cudaMemcpyDeviceToHost, c.stream));
     CK(cudaStreamSynchronize(c.stream));
@@ -1029,6 +1392,7 @@ ts_status ts_view_stats(ts_ctx* x, int64_t out[4]) {
 
 ts_status ts_set_profiling(ts_ctx* x, int32_t on) {
     TS_CHECK_CTX(x);
+    TS_SETTLE(x->c);
     Context& c = x->c;
     if (c.profiling || on) cudaStreamSynchronize(c.stream);
     c.profiling = on != 0;

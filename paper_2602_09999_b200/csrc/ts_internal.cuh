@@ -42,6 +42,28 @@ struct DevBuf {
     size_t cap = 0;  // elements
 };
 
+// CUDA-graph mode of ts_train_step: one instantiated graph per (view, config, target, mode)
+struct GraphEntry {
+    ts_camera cam;
+    ts_render_config cfg;
+    const float* target;  // host target (pinned, fixed address) or nullptr (slot)
+    int32_t slot, want_loss, mode;
+    int64_t N;
+    uint64_t gen;
+    cudaGraphExec_t exec;
+    int64_t kernels;     // kernel nodes of the graph (launch-count evidence)
+    uint32_t cls[7];     // size-class tile counts of the view's host-path step (sort grid hints)
+    int64_t I;           // its instance count (list capacity of the capture)
+};
+// a graph step launched but not yet known to have passed its capacity check
+struct GraphStep {
+    ts_camera cam;
+    ts_render_config cfg;
+    const float* target;
+    int32_t slot;
+    ts_adam_config adam;
+};
+
 struct Context {
     int device = 0;
     cudaStream_t stream = nullptr;
@@ -131,7 +153,17 @@ struct Context {
     cudaEvent_t loss_ev = nullptr;
     int binning_mode = 0;        // 0 auto (bucket + per-tile sort), 1 force the two-stage radix path
     // CUDA-graph mode of ts_train_step (ts_capi.cu graph_step)
+    bool graph_on = false;       // ts_set_graph
     bool gmode = false;          // the step being captured: no host reads, device-side counts and checks
+    bool capturing = false;      // stream capture active: ensure() must not allocate
+    uint64_t gen = 1;            // bumped by every device (re)allocation / buffer swap (graphs embed pointers)
+    std::vector<GraphEntry> graphs;
+    std::vector<GraphEntry> graph_seen;  // views run once on the host path (buffers sized), exec unused
+    std::vector<GraphStep> glog;         // launched graph steps not yet verified
+    cudaEvent_t gstep_ev = nullptr;      // recorded after each graph launch
+    uint32_t* gflag_host = nullptr;      // pinned copy of the sticky flag (written inside each graph)
+    bool I_on_device = false;            // the last view ran in a graph: c.I is read back lazily
+    int64_t graph_launches = 0, graph_captures = 0, graph_replays = 0;
     int cur_tn = 0;              // tiles of the view being binned
     void* adam_dev = nullptr;    // device copy of the per-step Adam arguments (graph mode)
     unsigned char adam_dev_bytes[128] = {};  // host staging of those arguments (size bound)

@@ -87,6 +87,8 @@ _SIGS = {
     "ts_debug_loss_grad": [_vp, _vp],
     "ts_binning_path": [_vp, _vp],
     "ts_launch_count": [_vp, ctypes.POINTER(_i64)],
+    "ts_set_graph": [_vp, _i32],
+    "ts_graph_stats": [_vp, _vp],
     "ts_host_alloc": [ctypes.c_size_t, ctypes.POINTER(_vp)],
     "ts_host_free": [_vp],
 }
@@ -247,6 +249,16 @@ class Engine:
                                           ctypes.byref(adam), ctypes.byref(out) if want_loss else None),
                     "ts_train_step")
         return float(out.value) if want_loss else None
+
+    def set_graph(self, on: bool):
+        """CUDA-graph mode of train_step (ts_set_graph): the step of each view is captured once and
+        relaunched; results equal the host-driven path (voided steps are replayed)."""
+        self._check(self._L.ts_set_graph(self._h, 1 if on else 0), "ts_set_graph")
+
+    def graph_stats(self):
+        out = np.zeros(4, np.int64)
+        self._check(self._L.ts_graph_stats(self._h, _ptr(out)), "ts_graph_stats")
+        return dict(launches=int(out[0]), captures=int(out[1]), replays=int(out[2]), graphs=int(out[3]))
 
     def densify_and_prune(self, grad_thresh: float, extent: float, seed: int, it: int):
         na = ctypes.c_int64()

@@ -20,6 +20,7 @@ _, _, pc, _ = O.render(p, n, cam, cfg)
 rng = np.random.default_rng(0)
 tiles = rng.choice(cam.n_tiles, 400, replace=False)
 tot = dict(all=0, rowcull=0, kept=0, kept_active=0, half_kept_active=0, px_ka=0, thr_ka=0, pair_work=0)
+hist = np.zeros(33, np.int64)
 for t in tiles:
     tx, ty = t % cam.tiles_x, t // cam.tiles_x
     b, e = ranges[t]
@@ -61,12 +62,15 @@ for t in tiles:
         # thread = 1 column x 4 rows: threads with >= 1 kept active pixel
         thr = ka[sel].reshape(-1, 2, 4, 16).any(axis=2)
         tot["thr_ka"] += thr.sum()
+        if thr.shape[0]: hist += np.bincount(thr.reshape(thr.shape[0], -1).sum(axis=1), minlength=33)[:33]
         kk = ka[sel]
         p0 = kk[:, [0, 1, 4, 5], :].any(axis=(1, 2))
         p1 = kk[:, [2, 3, 6, 7], :].any(axis=(1, 2))
         tot["pair_work"] += p0.sum() + p1.sum()
 print(wname, {k: int(v) for k, v in tot.items()})
 print({k: round(v / tot["rowcull"], 3) for k, v in tot.items()})
+c = np.cumsum(hist) / hist.sum()
+print("active lanes per worked warp-fragment, CDF at 1,2,4,8,16,24,31,32:", [round(float(c[k]), 3) for k in (1, 2, 4, 8, 16, 24, 31, 32)])
 print("pixel utilisation in worked warp-fragments:", tot["px_ka"] / (tot["kept_active"] * 128),
       " thread utilisation:", tot["thr_ka"] / (tot["kept_active"] * 32),
       " pairs needed (of 2 per worked warp-fragment):", tot["pair_work"] / (2 * tot["kept_active"]))

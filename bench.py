@@ -266,7 +266,7 @@ def run_reference(args):
     return 0
 
 
-def compute_roofline(avg_ms, vstats, clocks, n_tiles):
+def compute_roofline(avg_ms, vstats, clocks, n_tiles, workload):
     """Blend kernels (K6 / K8): fragment evaluations per second (256 pixels x processed list
     positions Ip per pass) and the issue-slot fraction = warp instructions per launch (ncu,
     profiles/inst.json, same workload) / (duration x 148 SMs x 4 schedulers x SM clock)."""
@@ -275,7 +275,7 @@ def compute_roofline(avg_ms, vstats, clocks, n_tiles):
     if os.path.exists(f):
         try:
             with open(f) as fh:
-                inst = json.load(fh)
+                inst = json.load(fh).get(workload, {})
         except Exception:
             inst = {}
     mhz = clocks.get("sm_mhz") or 1965.0
@@ -569,7 +569,7 @@ def run_ours(args):
                         else "profiled loop (stage CUDA events)", "mpix_s": P / (fwd_bwd_ms * 1e-3) / 1e6,
                         "algorithmic_bytes": int(R), "achieved_gbs": R / (fwd_bwd_ms * 1e-3) / 1e9,
                         "roofline_frac": R / (fwd_bwd_ms * 1e-3) / 1e9 / peak},
-            "compute": compute_roofline(avg, vstats, clocks, cams[0].n_tiles),
+            "compute": compute_roofline(avg, vstats, clocks, cams[0].n_tiles, w.name),
             "binning_counters": bcnt,
             "stage_ms": {k: round(v, 4) for k, v in avg.items()},
             "densify": [{"step": d[0], "n_after": d[1], "clones": d[2][0], "splits": d[2][1], "pruned": d[2][2]}

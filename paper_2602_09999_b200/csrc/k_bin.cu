@@ -351,15 +351,20 @@ __device__ __forceinline__ void tile_sort_one(uint32_t t, int seg, const uint32_
 // units u = blockIdx.x, blockIdx.x + gridDim.x, ... of the class.  meta == nullptr: the host
 // passes the class's tile list and count; otherwise (graph-captured step) both come from the
 // device-side class counts, so the grid is a fixed resident-size grid.
-template <int CAP, int NT, bool SEG = false>
+template <int CAP, int NT, bool SEG = false, bool DEV = false>
 __global__ void __launch_bounds__(NT) tile_sort_kernel(const uint32_t* __restrict__ starts,
                                                        const uint32_t* __restrict__ in,
                                                        const uint32_t* __restrict__ dkey, uint32_t* __restrict__ out,
                                                        const uint32_t* __restrict__ tiles, uint32_t n_host,
                                                        const uint32_t* __restrict__ meta, int cls) {
     extern __shared__ uint32_t sm[];
+    if (!DEV) {  // host path: exactly one unit per CTA
+        tile_sort_one<CAP, NT, SEG>(tiles[SEG ? blockIdx.x >> 2 : blockIdx.x], SEG ? int(blockIdx.x & 3u) : 0, starts,
+                                    in, dkey, out, sm);
+        return;
+    }
     uint32_t off = 0, n = n_host;
-    if (meta) class_range(meta, cls, &off, &n);
+    class_range(meta, cls, &off, &n);
     const uint32_t units = SEG ? 4u * n : n;
     for (uint32_t u = blockIdx.x; u < units; u += gridDim.x) {
         const uint32_t t = tiles[off + (SEG ? u >> 2 : u)];
@@ -524,6 +529,7 @@ bool launch_bin_count(Context& c, const DevCam& cam, const ts_render_config& cfg
     launch_exclusive_scan(c, c.bintot.p, nullptr, c.starts.p, Tn);
     // I, the class counts and the longest list to pinned host memory; the host waits on this
     // event only, so the scatter launched next overlaps the read-back
+    if (c.gmode) return true;  // a captured step never reads the counts back
     cudaMemcpyAsync(c.bin_host, c.starts.p + Tn, 4, cudaMemcpyDeviceToHost, c.stream);
     cudaMemcpyAsync(c.bin_host + 1, meta, 8 * 4, cudaMemcpyDeviceToHost, c.stream);
     cudaEventRecord(c.bin_ev, c.stream);
@@ -570,7 +576,9 @@ void launch_bin_scatter(Context& c, const DevCam& cam, const ts_render_config& c
 template <int CAP, int NT, bool SEG = false>
 static void sort_variant(Context& c, const uint32_t* tiles, uint32_t n, cudaStream_t st, int cls) {
     if (!c.gmode && !n) return;
-    set_func_attr(c, reinterpret_cast<const void*>(tile_sort_kernel<CAP, NT, SEG>),
+    set_func_attr(c, reinterpret_cast<const void*>(tile_sort_kernel<CAP, NT, SEG, false>),
+                  cudaFuncAttributeMaxDynamicSharedMemorySize, int(tile_sort_smem(CAP)));
+    set_func_attr(c, reinterpret_cast<const void*>(tile_sort_kernel<CAP, NT, SEG, true>),
                   cudaFuncAttributeMaxDynamicSharedMemorySize, int(tile_sort_smem(CAP)));
     const size_t smem = tile_sort_smem(CAP);
     unsigned grid = SEG ? 4 * n : n;
@@ -581,9 +589,14 @@ static void sort_variant(Context& c, const uint32_t* tiles, uint32_t n, cudaStre
         grid = SEG ? 4 * hint : hint;
     }
     // segments sort in place in the scatter output; whole lists go to the final list buffer
-    tile_sort_kernel<CAP, NT, SEG><<<grid, NT, smem, st>>>(c.starts.p, c.ival[1].p, c.dkey[0].p,
-                                                           SEG ? c.ival[1].p : c.ival[0].p, tiles, n,
-                                                           c.gmode ? c.bintot.p + c.cur_tn : nullptr, cls);
+    if (c.gmode)
+        tile_sort_kernel<CAP, NT, SEG, true><<<grid, NT, smem, st>>>(c.starts.p, c.ival[1].p, c.dkey[0].p,
+                                                                     SEG ? c.ival[1].p : c.ival[0].p, tiles, n,
+                                                                     c.bintot.p + c.cur_tn, cls);
+    else
+        tile_sort_kernel<CAP, NT, SEG, false><<<grid, NT, smem, st>>>(c.starts.p, c.ival[1].p, c.dkey[0].p,
+                                                                      SEG ? c.ival[1].p : c.ival[0].p, tiles, n,
+                                                                      nullptr, cls);
     TS_LAUNCHED(c);
 }
 

@@ -42,7 +42,10 @@ __device__ __forceinline__ bool visible_of(uint32_t i, const Bounds& b, const ui
 
 // One float4 (4 consecutive elements) per thread; elements outside [begin, end)
 // are written back unchanged.  Buffers are padded to a multiple of 4 floats.
-template <int MODE, bool ZERO>
+// DEV (graph-captured step): the per-step arguments come from device memory (written before each
+// launch) and a voided step (capacity check) does nothing; the host path keeps them in the
+// kernel's parameter bank
+template <int MODE, bool ZERO, bool DEV>
 __global__ void __launch_bounds__(256) adam_kernel(float4* __restrict__ th, float4* __restrict__ g,
                                                    float4* __restrict__ m, float4* __restrict__ v, uint32_t q0,
                                                    uint32_t q1, uint32_t begin, uint32_t end, Bounds bd, AdamArgs a_host,
@@ -51,10 +54,8 @@ __global__ void __launch_bounds__(256) adam_kernel(float4* __restrict__ th, floa
                                                    const uint32_t* __restrict__ gflag) {
     const uint32_t q = q0 + blockIdx.x * 256u + threadIdx.x;
     if (q >= q1) return;
-    // graph-captured step: per-step arguments from device memory (written before each launch),
-    // and nothing at all when the step was voided by its capacity check
-    if (gflag && *gflag) return;
-    const AdamArgs a = a_dev ? *a_dev : a_host;
+    if (DEV && *gflag) return;
+    const AdamArgs& a = DEV ? *a_dev : a_host;
     float4 t4 = th[q], g4 = g[q], m4 = m[q], v4 = v[q];
     float* tp = &t4.x;
     float* gp = &g4.x;
@@ -184,8 +185,11 @@ void launch_adam(Context& c, const ts_adam_config& a, int64_t begin, int64_t end
         xd = reinterpret_cast<const AdamArgs*>(c.adam_dev);
     }
     const uint32_t* gf = c.gmode ? c.counters.p + kGraphFlag : nullptr;
-#define TS_ADAM(MODE, Z) \
-    adam_kernel<MODE, Z><<<blocks, 256, 0, c.stream>>>(th, g, m, v, q0, q1, b, e, bd, x, c.vis.p, xd, gf)
+#define TS_ADAM(MODE, Z)                                                                                      \
+    if (c.gmode)                                                                                              \
+        adam_kernel<MODE, Z, true><<<blocks, 256, 0, c.stream>>>(th, g, m, v, q0, q1, b, e, bd, x, c.vis.p, xd, gf); \
+    else                                                                                                      \
+        adam_kernel<MODE, Z, false><<<blocks, 256, 0, c.stream>>>(th, g, m, v, q0, q1, b, e, bd, x, c.vis.p, xd, gf)
     if (a.mode == 2) {
         if (a.zero_grads) TS_ADAM(2, true);
         else TS_ADAM(2, false);

@@ -627,6 +627,15 @@ ts_status graph_capture(Context& c, const ts_camera& cam, const ts_render_config
     if (target_hwc && !ensure(c, c.tgt_stage, 3 * P)) return TS_ERR_OOM;
     CK(cudaStreamSynchronize(c.stream));
     const int64_t launches0 = c.launches;  // captured launches are counted when the graph runs
+    auto swap_events = [&c] {
+        std::swap(c.fork_ev, c.cap_fork);
+        std::swap(c.join_ev[0], c.cap_join[0]);
+        std::swap(c.join_ev[1], c.cap_join[1]);
+        std::swap(c.copy_fork, c.cap_copy_fork);
+        std::swap(c.copy_join, c.cap_copy_join);
+        std::swap(c.loss_ev, c.cap_loss);
+    };
+    swap_events();  // the capture records its own events (see Context::cap_fork)
     c.capturing = c.gmode = true;
     cudaError_t e = cudaStreamBeginCapture(c.stream, cudaStreamCaptureModeThreadLocal);
     if (e != cudaSuccess) {
@@ -674,6 +683,7 @@ ts_status graph_capture(Context& c, const ts_camera& cam, const ts_render_config
     cudaGraph_t g = nullptr;
     const cudaError_t e2 = cudaStreamEndCapture(c.stream, &g);
     c.capturing = c.gmode = false;
+    swap_events();
     *kernels = c.launches - launches0;
     c.launches = launches0;
     if (st == TS_OK && e != cudaSuccess) st = cuda_fail(c, e, "graph capture");
@@ -753,7 +763,7 @@ ts_status graph_step(Context& c, const ts_camera& cam, const ts_render_config& c
     c.loss_valid = false;
     c.I_on_device = true;
     if (out_loss) {
-        CK(cudaEventSynchronize(c.loss_ev));
+        CK(cudaEventSynchronize(c.cap_loss));  // the graph's external loss event node
         if (*c.gflag_host) {  // voided: replay now and report the replayed loss
             CK(cudaEventSynchronize(c.gstep_ev));
             c.glog.pop_back();
@@ -819,6 +829,17 @@ ts_status ts_create(int32_t device, void* stream, ts_ctx** out) {
         cudaEventCreateWithFlags(&c.copy_join, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&c.loss_ev, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&c.gstep_ev, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c.fork_ev, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c.join_ev[0], cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c.join_ev[1], cudaEventDisableTiming) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&c.side[0], cudaStreamNonBlocking) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&c.side[1], cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c.cap_fork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c.cap_join[0], cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c.cap_join[1], cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c.cap_copy_fork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c.cap_copy_join, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c.cap_loss, cudaEventDisableTiming) != cudaSuccess ||
         cudaMallocHost(reinterpret_cast<void**>(&c.loss_host), 2 * sizeof(double)) != cudaSuccess ||
         cudaMallocHost(reinterpret_cast<void**>(&c.gflag_host), sizeof(uint32_t)) != cudaSuccess ||
         cudaMalloc(&c.adam_dev, sizeof(c.adam_dev_bytes)) != cudaSuccess) {
@@ -846,6 +867,8 @@ ts_status ts_destroy(ts_ctx* x) {
     cudaStreamSynchronize(c.stream);
     drop_graphs(c);
     if (c.gstep_ev) cudaEventDestroy(c.gstep_ev);
+    for (cudaEvent_t ev : {c.cap_fork, c.cap_join[0], c.cap_join[1], c.cap_copy_fork, c.cap_copy_join, c.cap_loss})
+        if (ev) cudaEventDestroy(ev);
     if (c.gflag_host) cudaFreeHost(c.gflag_host);
     if (c.adam_dev) cudaFree(c.adam_dev);
     release(c.params), release(c.grads), release(c.m), release(c.v), release(c.accum), release(c.vcount);

@@ -161,6 +161,11 @@ struct Context {
     std::vector<GraphEntry> graph_seen;  // views run once on the host path (buffers sized), exec unused
     std::vector<GraphStep> glog;         // launched graph steps not yet verified
     cudaEvent_t gstep_ev = nullptr;      // recorded after each graph launch
+    // events used inside captures (fork / join dependencies, the loss read-back node): an event
+    // recorded in a capturing stream may not be waited on outside the graph, so the host path
+    // keeps its own set (swapped in and out around each capture)
+    cudaEvent_t cap_fork = nullptr, cap_join[2] = {nullptr, nullptr}, cap_copy_fork = nullptr,
+                cap_copy_join = nullptr, cap_loss = nullptr;
     uint32_t* gflag_host = nullptr;      // pinned copy of the sticky flag (written inside each graph)
     bool I_on_device = false;            // the last view ran in a graph: c.I is read back lazily
     int64_t graph_launches = 0, graph_captures = 0, graph_replays = 0;

@@ -1,6 +1,6 @@
 """Regenerate profiles/<round>_step_ncu.md, <round>_launches.md, traffic.json and <round>_bench.json
 from a full-step ncu report, a launch-list csv and a bench JSON line.
-usage: refresh_profiles.py ROUND STEP.ncu-rep LAUNCHES.csv BENCH.json"""
+usage: refresh_profiles.py ROUND STEP.ncu-rep LAUNCHES.csv BENCH.json [OTHER_BENCH.json ...]"""
 import json, os, subprocess, sys
 
 rnd, rep, csvf, benchf = sys.argv[1:5]
@@ -16,6 +16,22 @@ launch = run("scripts/launch_table.py", csvf)
 b = json.loads(open(benchf).read().strip().splitlines()[-1])
 with open(os.path.join(prof, f"{rnd}_bench.json"), "w") as f:
     f.write(json.dumps(b) + "\n")
+others = []
+for of in sys.argv[5:]:
+    try:
+        o = json.loads(open(of).read().strip().splitlines()[-1])
+    except Exception:
+        continue
+    fb = o.get("fwd_bwd") or {}
+    others.append(f"| {o['config']['workload']}{' + densify' if o.get('densify') else ''} | "
+                  f"{o['config'].get('views_per_step', 1)} | {o['value']:.1f} | {o['ms_per_step']:.3f} | "
+                  f"{o['e2e']['value']:.1f} | {fb.get('ms', 0):.3f} | {fb.get('roofline_frac', 0):.3f} | "
+                  f"{o['view']['V']} | {o['view']['I']} | {o['view']['Ip']} |")
+    with open(os.path.join(prof, f"{rnd}_bench_{o['config']['workload']}{'_densify' if o.get('densify') else ''}.json"), "w") as f:
+        f.write(json.dumps(o) + "\n")
+other_md = ("\n## Other workloads (`bench.py --workload ...`, same box)\n\n| workload | views/step | steps/s | ms/step | "
+            "e2e steps/s | fwd+bwd ms | fwd+bwd HBM frac | V | I | Ip |\n|---|---|---|---|---|---|---|---|---|---|\n"
+            + "\n".join(others) + "\n") if others else ""
 md = f"""# Round {rnd[1:]} (final kernels) — workload H: 3M Gaussians, SH3, 1920x1080, 1 view per step
 
 Bench (`python bench.py`, 200 timed steps, 8-camera view ring, z-ordered store): **{b['value']:.1f} steps/s**
@@ -40,14 +56,14 @@ SM / memory throughput %, achieved occupancy, registers, issue-active % (`script
 ```
 
 Reading it:
-* `adam_kernel` and `project_bwd_kernel` stream at ~7.0 and ~6.1 TB/s: HBM-bound at the roof (Adam's
+* `adam_kernel` and `project_bwd_kernel` stream at ~6.9 and ~6.4 TB/s: HBM-bound at the roof (Adam's
   4:3 read:write mix runs above the 6.56 TB/s 1:1 copy test of MEASURED_PEAKS.json).
-* `blend_fwd` / `blend_bwd` / `loss_fused` / `preprocess` are issue-bound (issue-active 65-77 %, DRAM < 3.2 TB/s):
-  their roofline fraction is limited by FP32/MUFU instruction count, not bytes.
-* `bin_scatter` (~51 % issue, 1.1 TB/s) is latency-bound on shared atomics and scattered 4-byte slot writes.
+* `blend_fwd` / `blend_bwd` / `loss_fused` / `preprocess` are issue-bound (issue-active 65-78 %, DRAM < 3.5 TB/s):
+  their roofline fraction is limited by instruction issue (ALU / FMA / MUFU pipes, `{rnd}_counters.md`), not bytes.
+* `bin_scatter` (~48 % issue, 1.3 TB/s) is latency-bound on shared atomics and scattered 4-byte slot writes.
 * `tile_sort` classes run on fork streams (the 6144/8192 classes overlap the 4096/1024 ones in the live step).
 """
-open(os.path.join(prof, f"{rnd}_step_ncu.md"), "w").write(md)
+open(os.path.join(prof, f"{rnd}_step_ncu.md"), "w").write(md + other_md)
 open(os.path.join(prof, f"{rnd}_launches.md"), "w").write(
     f"# Round {rnd[1:]} (final kernels) — ncu launch list, workload H\n\n"
     "`ncu --metrics gpu__time_duration.sum --clock-control none -s 200 -c 30 --csv python bench.py --steps 4 --warmup 3 --no-cpu-baseline`\n"

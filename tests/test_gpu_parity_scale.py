@@ -113,3 +113,52 @@ def test_scale_loss_and_gradients(big):
 def test_scale_densify_stats(big):
     assert np.array_equal(big["vc"], big["ovc"])
     _grad_check(big["acc"], big["oacc"], "densify accum")
+
+
+@pytest.fixture(scope="module")
+def headline_store():
+    w = scene.WORKLOADS["H"]
+    gt = scene.random_params(w.n, w.s0, w.m_o, w.seed)
+    return w, scene.perturb(gt, w.n, w.seed)
+
+
+def test_scale_morton_reorder_matches_oracle(engine, headline_store):
+    """morton_reorder of the 3M-Gaussian store: the permutation and the
+    permuted parameters equal the oracle's bit for bit."""
+    w, p = headline_store
+    n = w.n
+    engine.set_params(p, n)
+    perm = engine.morton_reorder()
+    gp = engine.get_params()
+    q = p.copy()
+    operm = O.morton_reorder(q, n)
+    assert np.array_equal(perm, operm)
+    assert np.array_equal(gp.view(np.uint32), q.view(np.uint32))
+
+
+def test_scale_densify_matches_oracle(engine, headline_store):
+    """One densify_and_prune event on the 3M-Gaussian store with the densify
+    statistics of a real backward (view 0 of the ring, the bench's loss): masks, compaction,
+    split children and moments bit for bit."""
+    w, p = headline_store
+    n = w.n
+    cam = scene.ring_camera(w, 0)
+    cfg = T.RenderConfig.make(sh_degree=w.sh_degree)
+    engine.set_params(p, n)
+    rgb, _, _ = engine.render(cam, cfg)
+    target = np.clip(rgb + np.random.default_rng(7).normal(0, 0.05, rgb.shape), 0, 1).astype(np.float32)
+    engine.training_loss(target)
+    engine.backward(None)
+    G, _, _, acc, vc = engine.get_state()
+    rng = np.random.default_rng(8)
+    m = rng.normal(0, 1e-3, 59 * n).astype(np.float32)
+    v = np.abs(rng.normal(0, 1e-4, 59 * n)).astype(np.float32)
+    engine.set_state(m=m, v=v, accum=acc, vcount=vc)
+    thresh = float(np.quantile((acc / np.maximum(vc, 1))[vc > 0], 0.99))   # ~1% selected
+    na, st = engine.densify_and_prune(thresh, 2.0, 1234, 700)
+    gp = engine.get_params()
+    _, gm, gv, _, _ = engine.get_state()
+    op, om, ov, ona, ost = O.densify(p, m, v, acc, vc, n, thresh, 2.0, 1234, 700)
+    assert na == ona and tuple(st) == tuple(ost) and st[0] + st[1] > 1000
+    assert np.array_equal(gp.view(np.uint32), op.view(np.uint32))
+    assert np.array_equal(gm.view(np.uint32), om.view(np.uint32)) and np.array_equal(gv.view(np.uint32), ov.view(np.uint32))

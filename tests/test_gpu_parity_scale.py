@@ -162,3 +162,35 @@ def test_scale_densify_matches_oracle(engine, headline_store):
     assert na == ona and tuple(st) == tuple(ost) and st[0] + st[1] > 1000
     assert np.array_equal(gp.view(np.uint32), op.view(np.uint32))
     assert np.array_equal(gm.view(np.uint32), om.view(np.uint32)) and np.array_equal(gv.view(np.uint32), ov.view(np.uint32))
+
+
+def test_scale_c4_two_view_accumulation(engine):
+    """Config 4's batch semantics (gradients summed over the views of a step) at
+    6M Gaussians, 1080p: two ring views accumulated in the device gradient buffer against the
+    sum of the oracle's per-view gradients; densify visible counts summed bitwise."""
+    w = scene.WORKLOADS["c4"]
+    n = w.n
+    O.set_workers(os.cpu_count() or 1)
+    p = scene.perturb(scene.random_params(n, w.s0, w.m_o, w.seed), n, w.seed)
+    cfg = T.RenderConfig.make(sh_degree=w.sh_degree)
+    cams = [scene.ring_camera(w, j) for j in (0, 5)]
+    rng = np.random.default_rng(44)
+    dls = [rng.normal(0, 1e-7, (w.height, w.width, 3)).astype(np.float32) for _ in cams]
+    engine.set_params(p, n)
+    for cam, dl in zip(cams, dls):
+        engine.render(cam, cfg, outputs=False)
+        engine.backward(dl)
+    G, _, _, acc, vc = engine.get_state()
+    oG = np.zeros(59 * n, np.float32)
+    ovc = np.zeros(n, np.float32)
+    oacc = np.zeros(n, np.float32)
+    for cam, dl in zip(cams, dls):
+        g_, _, a_, c_ = O.backward(p, n, cam, cfg, dl)
+        oG += g_
+        oacc += a_
+        ovc += c_
+        del g_
+    for (a, b), nm in zip(T.group_slices(n), T.GROUPS):
+        _grad_check(G[a:b], oG[a:b], f"c4/{nm}")
+    assert np.array_equal(vc, ovc)
+    _grad_check(acc, oacc, "c4 densify accum")

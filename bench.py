@@ -88,41 +88,94 @@ def stage_bytes(st, n, deg, n_tiles):
 
 
 class ClockSampler:
+    """SM clock and clock-event reasons sampled DURING the timed region.
+
+    An NVML thread (5 ms period) that is confirmed sampling before start() returns, so even a
+    short timed region (tens of ms) carries samples; nvidia-smi -lms is the fallback."""
+
     def __init__(self, gpu: int):
         self.gpu = gpu
         self.proc = None
         self.path = None
+        self.thread = None
+        self.rows = []
+        self.stop_flag = None
+
+    def _nvml_handle(self):
+        import pynvml
+        import torch
+        pynvml.nvmlInit()
+        try:
+            p = torch.cuda.get_device_properties(self.gpu)
+            bus = "%08X:%02X:%02X.0" % (p.pci_domain_id, p.pci_bus_id, p.pci_device_id)
+            return pynvml.nvmlDeviceGetHandleByPciBusId(bus)
+        except Exception:
+            return pynvml.nvmlDeviceGetHandleByIndex(self.gpu)
 
     def start(self):
+        import threading
+        try:
+            import pynvml
+            h = self._nvml_handle()
+            mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+            self.stop_flag = threading.Event()
+            first = threading.Event()
+
+            def run():
+                while True:
+                    try:
+                        sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+                        rs = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                        self.rows.append((float(sm), float(mx), int(rs)))
+                    except Exception:
+                        pass
+                    first.set()
+                    if self.stop_flag.wait(0.005):
+                        return
+
+            self.thread = threading.Thread(target=run, daemon=True)
+            self.thread.start()
+            first.wait(2.0)
+            return
+        except Exception:
+            self.thread = None
         fd, self.path = tempfile.mkstemp(prefix="clk", suffix=".csv")
         os.close(fd)
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.gpu), "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "20"],
                 stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+            t0 = time.time()  # wait for the first sample line so the timed region is covered
+            while time.time() - t0 < 5 and os.path.getsize(self.path) == 0:
+                time.sleep(0.01)
         except Exception:
             self.proc = None
 
     def stop(self):
-        if self.proc is None:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
-        self.proc.terminate()
-        try:
-            self.proc.wait(timeout=5)
-        except Exception:
-            self.proc.kill()
-        rows = []
-        with open(self.path) as f:
-            for line in f:
-                parts = [x.strip() for x in line.split(",")]
-                if len(parts) != 3:
-                    continue
-                try:
-                    rows.append((float(parts[0]), float(parts[1]), int(parts[2], 16)))
-                except ValueError:
-                    continue
-        os.unlink(self.path)
+        if self.thread is not None:
+            self.stop_flag.set()
+            self.thread.join(timeout=2)
+            rows = self.rows
+        elif self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no clock sampler (nvml / nvidia-smi)"], "samples": 0}
+        else:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+            rows = []
+            with open(self.path) as f:
+                for line in f:
+                    parts = [x.strip() for x in line.split(",")]
+                    if len(parts) != 3:
+                        continue
+                    try:
+                        rows.append((float(parts[0]), float(parts[1]), int(parts[2], 16)))
+                    except ValueError:
+                        continue
+            os.unlink(self.path)
         load = [r for r in rows if not (r[2] & 0x1)] or rows
         reasons = set()
         for r in load:
@@ -576,7 +629,7 @@ def run_ours(args):
                         for d in densify_log] if args.densify else None,
             "stage_calls": calls,
             "view": vstats,
-            "clocks": {k: clocks[k] for k in ("sm_mhz", "sm_max_mhz", "reasons")},
+            "clocks": {k: clocks[k] for k in ("sm_mhz", "sm_max_mhz", "reasons", "samples")},
         }
         if cpu is not None:
             line["cpu_baseline"] = {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")}

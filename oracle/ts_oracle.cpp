@@ -450,11 +450,12 @@ GFwd<T> gaussian_forward(const T* P, int64_t N, int64_t g, const Cam<T>& cam, co
     return F;
 }
 
-// Conic quadratic form, fixed evaluation order shared with the kernels:
-//   Q = dx*(A*dx + (2B)*dy) + dy*(C*dy)
+// Conic quadratic form, fixed evaluation order shared with the kernels
+// (ts_math.cuh tsx::conic_q; two correctly rounded products, two fused multiply-adds):
+//   Q = fma(dy, fma(C, dy, (2B)*dx), (A*dx)*dx)
 template <class T>
 inline T conic_q(T A, T B2, T C, T dx, T dy) {
-    return dx * (A * dx + B2 * dy) + dy * (C * dy);
+    return std::fma(dy, std::fma(C, dy, B2 * dx), (A * dx) * dx);
 }
 
 struct Rect {

@@ -104,17 +104,16 @@ __global__ void __launch_bounds__(kT, TS_FWD_MINB) blend_fwd_kernel(const uint32
                 const float4 a = sA[j];
                 if (a.y + q.w < wy0 || a.y - q.w > wy1) continue;  // splat misses this warp's 8 rows
                 const float dx = tsx::sub(fpx, a.x);
-                const float adx = tsx::mul(q.x, dx);
+                const float bdx = tsx::mul(q.y, dx), adxdx = tsx::mul(tsx::mul(q.x, dx), dx);
                 const float4 col = sC[j];
                 // keep mask of the 4 pixels first (exact Q, branch-free), heavy path only on set bits
                 float Qv[kPPT];
                 uint32_t km = 0;
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
-                    // Q = dx*(A*dx + 2B*dy) + dy*(C*dy), exact order (tsx::conic_q), two rows per op
+                    // Q = fma(dy, fma(C, dy, 2B*dx), (A*dx)*dx) (tsx::conic_q), two rows per op
                     const float2 dy = tsx::sub2(pyp[h], tsx::dup2(a.y));
-                    const float2 Q = tsx::add2(tsx::mul2(tsx::dup2(dx), tsx::add2(tsx::dup2(adx), tsx::mul2(tsx::dup2(q.y), dy))),
-                                               tsx::mul2(dy, tsx::mul2(tsx::dup2(q.z), dy)));
+                    const float2 Q = tsx::fma2(dy, tsx::fma2(tsx::dup2(q.z), dy, tsx::dup2(bdx)), tsx::dup2(adxdx));
                     Qv[2 * h] = Q.x;
                     Qv[2 * h + 1] = Q.y;
                     km |= (Q.x <= a.z) ? (1u << (2 * h)) : 0u;
@@ -314,6 +313,8 @@ __global__ void __launch_bounds__(kT, TS_BWD_MINB) blend_bwd_kernel(const uint32
     __syncthreads();
     const uint32_t b = starts[t];
     const uint32_t e = min(starts[t + 1], b + s_max);
+    // this warp's pixels have no contributor beyond list position wm: its fragment loop stops
+    // there (the CTA keeps staging up to the tile's maximum for the other warp)
     const int slot = red9_slot(lane);
     for (uint32_t base = b; base < e; base += kBatch) {
 #pragma unroll
@@ -336,58 +337,71 @@ __global__ void __launch_bounds__(kT, TS_BWD_MINB) blend_bwd_kernel(const uint32
         __syncthreads();
         const int n = int(tmin<uint32_t>(kBatch, e - base));
         const uint32_t local0 = base - b;
-        for (int j = 0; j < n; ++j) {
+        const int nw = wm > local0 ? int(tmin<uint32_t>(uint32_t(n), wm - local0)) : 0;
+        for (int j = 0; j < nw; ++j) {
             const float4 q = sB[j];
             const float4 a = sA[j];
             if (a.y + q.w < wy0 || a.y - q.w > wy1) continue;  // warp-uniform row cull
             const float dx = tsx::sub(fpx, a.x);
             const float adx = tsx::mul(q.x, dx);
+            const float bdx = tsx::mul(q.y, dx), adxdx = tsx::mul(adx, dx);
             const uint32_t li = local0 + uint32_t(j);
-            // keep mask of the 4 pixels first (exact Q); the warp skips the fragment if no lane keeps it
+            // keep mask of the 4 pixels first (exact Q, tsx::conic_q); the warp skips the fragment if no lane keeps it
             float2 Qp[2], dyp[2];
             uint32_t km = 0;
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
                 dyp[h] = tsx::sub2(pyp[h], tsx::dup2(a.y));
-                Qp[h] = tsx::add2(tsx::mul2(tsx::dup2(dx), tsx::add2(tsx::dup2(adx), tsx::mul2(tsx::dup2(q.y), dyp[h]))),
-                                  tsx::mul2(dyp[h], tsx::mul2(tsx::dup2(q.z), dyp[h])));
+                Qp[h] = tsx::fma2(dyp[h], tsx::fma2(tsx::dup2(q.z), dyp[h], tsx::dup2(bdx)), tsx::dup2(adxdx));
                 km |= (li < cnt[2 * h] && Qp[h].x <= a.z) ? (1u << (2 * h)) : 0u;
                 km |= (li < cnt[2 * h + 1] && Qp[h].y <= a.z) ? (2u << (2 * h)) : 0u;
             }
             if (!__any_sync(0xffffffffu, km)) continue;
             const float4 col = sC[j];
+            const float hoa = 0.5f * a.w;
             const float2 ncx = tsx::dup2(-col.x), ncy = tsx::dup2(-col.y), ncz = tsx::dup2(-col.z);
             // per-thread sums over its pixels (pairs, folded at the end): colour / opacity
             // grads and the three moments of dL/dQ that give the mean2d and conic grads
             // (dx is shared).  Branch-free: a dropped pixel has alpha 0 (w = 0, T and g.U
             // unchanged) and a zero dL/dalpha mask.  ng* = negated quantities (ngc = -g.c,
             // ndal = -dL/dalpha) so every update is one FFMA2.
-            float2 vr2 = make_float2(0.f, 0.f), vg2 = vr2, vb2 = vr2, nvo2 = vr2, sq2 = vr2, sqy2 = vr2, sqyy2 = vr2;
+            float2 vr2, vg2, vb2, nvo2, sq2, sqy2, sqyy2;
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
                 const bool k0 = km & (1u << (2 * h)), k1 = km & (2u << (2 * h));
                 const float2 e = tsx::mul2(Qp[h], tsx::dup2(kNegHalfLog2e));
-                const float2 G = make_float2(tsx::ex2_approx(e.x), tsx::ex2_approx(e.y));
+                // G of a dropped pixel is 0: alpha, w, the opacity and conic terms vanish with it
+                const float2 G = make_float2(k0 ? tsx::ex2_approx(e.x) : 0.f, k1 ? tsx::ex2_approx(e.y) : 0.f);
                 const float2 og = tsx::mul2(tsx::dup2(a.w), G);
-                const bool l0 = k0 && og.x <= 0.99f, l1 = k1 && og.y <= 0.99f;  // alpha not clamped: gradient flows
-                const float2 al = make_float2(k0 ? fminf(og.x, 0.99f) : 0.f, k1 ? fminf(og.y, 0.99f) : 0.f);
+                const float2 al = make_float2(fminf(og.x, 0.99f), fminf(og.y, 0.99f));
+                // alpha not clamped: gradient flows through G (SPEC.md clamp rule, App. A.8)
+                const float2 Gl = make_float2(og.x <= 0.99f ? G.x : 0.f, og.y <= 0.99f ? G.y : 0.f);
                 const float2 w = tsx::mul2(al, Tp[h]);
                 const float2 om = tsx::sub2(tsx::dup2(1.f), al);
                 const float2 ngc = tsx::fma2(g2p[h], ncz, tsx::fma2(g1p[h], ncy, tsx::mul2(g0p[h], ncx)));
                 const float2 after = tsx::fma2(w, ngc, gUp[h]);  // g . (colour after this fragment, incl. bg)
                 const float2 r = make_float2(rcp_approx(om.x), rcp_approx(om.y));
-                float2 ndal = tsx::fma2(Tp[h], ngc, tsx::mul2(after, r));
-                ndal.x = l0 ? ndal.x : 0.f;
-                ndal.y = l1 ? ndal.y : 0.f;
-                vr2 = tsx::fma2(w, g0p[h], vr2);
-                vg2 = tsx::fma2(w, g1p[h], vg2);
-                vb2 = tsx::fma2(w, g2p[h], vb2);
-                nvo2 = tsx::fma2(G, ndal, nvo2);
-                const float2 dQ = tsx::mul2(tsx::mul2(tsx::dup2(0.5f), og), ndal);
+                const float2 ndal = tsx::fma2(Tp[h], ngc, tsx::mul2(after, r));
+                const float2 nvo = tsx::mul2(Gl, ndal);              // -dL/do contribution
+                const float2 dQ = tsx::mul2(nvo, tsx::dup2(hoa));  // dL/dQ = -0.5 o G dL/dalpha
                 const float2 dQy = tsx::mul2(dQ, dyp[h]);
-                sq2 = tsx::add2(sq2, dQ);
-                sqy2 = tsx::add2(sqy2, dQy);
-                sqyy2 = tsx::fma2(dQy, dyp[h], sqyy2);
+                if (h == 0) {
+                    vr2 = tsx::mul2(w, g0p[h]);
+                    vg2 = tsx::mul2(w, g1p[h]);
+                    vb2 = tsx::mul2(w, g2p[h]);
+                    nvo2 = nvo;
+                    sq2 = dQ;
+                    sqy2 = dQy;
+                    sqyy2 = tsx::mul2(dQy, dyp[h]);
+                } else {
+                    vr2 = tsx::fma2(w, g0p[h], vr2);
+                    vg2 = tsx::fma2(w, g1p[h], vg2);
+                    vb2 = tsx::fma2(w, g2p[h], vb2);
+                    nvo2 = tsx::add2(nvo2, nvo);
+                    sq2 = tsx::add2(sq2, dQ);
+                    sqy2 = tsx::add2(sqy2, dQy);
+                    sqyy2 = tsx::fma2(dQy, dyp[h], sqyy2);
+                }
                 gUp[h] = after;
                 Tp[h] = tsx::mul2(Tp[h], om);
             }

@@ -75,16 +75,28 @@ __global__ void __launch_bounds__(kT, TS_FWD_MINB) blend_fwd_kernel(const uint32
 #pragma unroll
     for (int k = 0; k < kPPT; ++k) {
         last[k] = 0;
-        if (px >= cam.w || py0 + k >= cam.h) done |= 1u << k;
+        if (px >= cam.w || py0 + k >= cam.h) {
+            done |= 1u << k;
+            if (!kCompat) {  // fast path: a pixel is live while T >= 1e-4 (outside the image: never)
+                if (k & 1) Tp[k >> 1].y = 0.f;
+                else Tp[k >> 1].x = 0.f;
+            }
+        }
     }
     // scalar views of the pair state (constant k after unrolling: stays in registers)
 #define T(k) (((k) & 1) ? Tp[(k) >> 1].y : Tp[(k) >> 1].x)
 #define C0(k) (((k) & 1) ? C0p[(k) >> 1].y : C0p[(k) >> 1].x)
 #define C1(k) (((k) & 1) ? C1p[(k) >> 1].y : C1p[(k) >> 1].x)
 #define C2(k) (((k) & 1) ? C2p[(k) >> 1].y : C2p[(k) >> 1].x)
+    // "blend then stop": the fast path keeps no done mask, a pixel with T < 1e-4 is simply never
+    // kept again (T only decreases); the compat path ("stop before blending") keeps the mask
+    auto all_done = [&]() -> bool {
+        if (kCompat) return done == 0xFu;
+        return fmaxf(fmaxf(Tp[0].x, Tp[0].y), fmaxf(Tp[1].x, Tp[1].y)) < 1e-4f;
+    };
     if (threadIdx.x == 0) s_max = 0;
     for (uint32_t base = b; base < e; base += kBatch) {
-        if (__syncthreads_count(done == 0xFu) == kT) break;
+        if (__syncthreads_count(all_done()) == kT) break;
 #pragma unroll
         for (int u = 0; u < kBatch / kT; ++u) {
             const uint32_t i = base + threadIdx.x + u * kT;
@@ -98,7 +110,7 @@ __global__ void __launch_bounds__(kT, TS_FWD_MINB) blend_fwd_kernel(const uint32
         }
         __syncthreads();
         const int n = int(tmin<uint32_t>(kBatch, e - base));
-        if (done != 0xFu) {
+        if (!all_done()) {
             for (int j = 0; j < n; ++j) {
                 const float4 q = sB[j];
                 const float4 a = sA[j];
@@ -106,27 +118,29 @@ __global__ void __launch_bounds__(kT, TS_FWD_MINB) blend_fwd_kernel(const uint32
                 const float dx = tsx::sub(fpx, a.x);
                 const float bdx = tsx::mul(q.y, dx), adxdx = tsx::mul(tsx::mul(q.x, dx), dx);
                 const float4 col = sC[j];
-                // keep mask of the 4 pixels first (exact Q, branch-free), heavy path only on set bits
-                float Qv[kPPT];
-                uint32_t km = 0;
+                // keep decisions of the 4 pixels first (exact Q, branch-free), heavy path only if any is set
+                float2 Qp[2];
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
                     // Q = fma(dy, fma(C, dy, 2B*dx), (A*dx)*dx) (tsx::conic_q), two rows per op
                     const float2 dy = tsx::sub2(pyp[h], tsx::dup2(a.y));
-                    const float2 Q = tsx::fma2(dy, tsx::fma2(tsx::dup2(q.z), dy, tsx::dup2(bdx)), tsx::dup2(adxdx));
-                    Qv[2 * h] = Q.x;
-                    Qv[2 * h + 1] = Q.y;
-                    km |= (Q.x <= a.z) ? (1u << (2 * h)) : 0u;
-                    km |= (Q.y <= a.z) ? (2u << (2 * h)) : 0u;
+                    Qp[h] = tsx::fma2(dy, tsx::fma2(tsx::dup2(q.z), dy, tsx::dup2(bdx)), tsx::dup2(adxdx));
                 }
-                km &= ~done;
-                if (!km) continue;
                 const uint32_t idx1 = base - b + uint32_t(j) + 1u;
-                if (kCompat) {
+                if constexpr (kCompat) {
+                    uint32_t km = 0;
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        km |= (Qp[h].x <= a.z) ? (1u << (2 * h)) : 0u;
+                        km |= (Qp[h].y <= a.z) ? (2u << (2 * h)) : 0u;
+                    }
+                    km &= ~done;
+                    if (!km) continue;
 #pragma unroll
                     for (int k = 0; k < kPPT; ++k) {
                         if (!(km & (1u << k))) continue;
-                        const float G = tsx::ex2_approx(Qv[k] * kNegHalfLog2e);
+                        const float Qk = (k & 1) ? Qp[k >> 1].y : Qp[k >> 1].x;
+                        const float G = tsx::ex2_approx(Qk * kNegHalfLog2e);
                         const float al = fminf(0.99f, a.w * G);
                         const float om = 1.f - al;
                         if (T(k) * om < 1e-4f) {
@@ -140,16 +154,23 @@ __global__ void __launch_bounds__(kT, TS_FWD_MINB) blend_fwd_kernel(const uint32
                         T(k) = T(k) * om;
                         last[k] = idx1;
                     }
+                    if (done == 0xFu) break;
                 } else {
+                    bool kp[kPPT];
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        kp[2 * h] = Qp[h].x <= a.z && Tp[h].x >= 1e-4f;
+                        kp[2 * h + 1] = Qp[h].y <= a.z && Tp[h].y >= 1e-4f;
+                    }
+                    if (!(kp[0] | kp[1] | kp[2] | kp[3])) continue;
                     // branch-free over the 4 pixels, two pixel pairs in packed fp32x2 ops
                     // (per lane the same IEEE ops as the scalar form): a dropped pixel
                     // blends alpha 0, which leaves C and T bit-identical (fma(0, c, C) = C, T * 1 = T)
                     const float2 cx = tsx::dup2(col.x), cy = tsx::dup2(col.y), cz = tsx::dup2(col.z);
 #pragma unroll
                     for (int h = 0; h < 2; ++h) {
-                        const bool k0 = km & (1u << (2 * h)), k1 = km & (2u << (2 * h));
-                        const float2 Qh = make_float2(Qv[2 * h], Qv[2 * h + 1]);
-                        const float2 e = tsx::mul2(Qh, tsx::dup2(kNegHalfLog2e));
+                        const bool k0 = kp[2 * h], k1 = kp[2 * h + 1];
+                        const float2 e = tsx::mul2(Qp[h], tsx::dup2(kNegHalfLog2e));
                         const float2 G = make_float2(tsx::ex2_approx(e.x), tsx::ex2_approx(e.y));
                         const float2 og = tsx::mul2(tsx::dup2(a.w), G);
                         const float2 al = make_float2(k0 ? fminf(0.99f, og.x) : 0.f, k1 ? fminf(0.99f, og.y) : 0.f);
@@ -160,11 +181,9 @@ __global__ void __launch_bounds__(kT, TS_FWD_MINB) blend_fwd_kernel(const uint32
                         Tp[h] = tsx::mul2(Tp[h], tsx::sub2(tsx::dup2(1.f), al));
                         last[2 * h] = k0 ? idx1 : last[2 * h];
                         last[2 * h + 1] = k1 ? idx1 : last[2 * h + 1];
-                        done |= (Tp[h].x < 1e-4f) ? (1u << (2 * h)) : 0u;
-                        done |= (Tp[h].y < 1e-4f) ? (2u << (2 * h)) : 0u;
                     }
+                    if (all_done()) break;
                 }
-                if (done == 0xFu) break;
             }
         }
     }

@@ -34,13 +34,15 @@ constexpr float kNegHalfLog2e = -0.72134752044448170368f;  // -0.5 * log2(e)
 __device__ __forceinline__ int tile_row0(int tid) { return (tid >> 5) * 8 + ((tid >> 4) & 1) * 4; }
 
 template <bool kCompat>
-// an explicit minimum of 1 resident CTA lets ptxas spend registers (64 / 90) instead of
-// rematerialising for occupancy: measured 2% (K6) and 1% (K8) faster than the default
+// resident-CTA minimums that cap the registers at 72 (K6: 14 CTAs = 28 warps per SM) and 80 (K8: 12
+// CTAs, which also fills the shared memory): measured 0.239 -> 0.217 ms (K6, with the per-warp
+// staging below) and 0.441 -> 0.438 ms (K8) against uncapped 78 / 93 registers; 15-16 CTAs for
+// K6 were slower again (0.237 ms)
 #ifndef TS_FWD_MINB
-#define TS_FWD_MINB 1
+#define TS_FWD_MINB 14
 #endif
 #ifndef TS_BWD_MINB
-#define TS_BWD_MINB 1
+#define TS_BWD_MINB 12
 #endif
 __global__ void __launch_bounds__(kT, TS_FWD_MINB) blend_fwd_kernel(const uint32_t* __restrict__ starts,
                                                       const uint32_t* __restrict__ ival,
@@ -51,15 +53,18 @@ __global__ void __launch_bounds__(kT, TS_FWD_MINB) blend_fwd_kernel(const uint32
                                                       const uint32_t* __restrict__ order,
                                                       uint32_t* __restrict__ tile_proc,
                                                       const float* __restrict__ ryv) {
-    __shared__ float4 sA[kBatch];  // mx, my, k2, o
-    __shared__ float4 sB[kBatch];  // A, 2B, C, ry
-    __shared__ float4 sC[kBatch];  // r, g, b
+    // per-warp staged batches: only the splats whose keep ellipse reaches the warp's 8 rows,
+    // compacted in list order (the warps of a tile run independently: no CTA barrier in the loop)
+    __shared__ float4 sA[2][kBatch];  // mx, my, k2, o
+    __shared__ float4 sB[2][kBatch];  // A, 2B, C, -
+    __shared__ float4 sC[2][kBatch];  // r, g, b, list position + 1 (uint bits)
     __shared__ uint32_t s_max;
     const int t = order ? int(order[blockIdx.x]) : int(blockIdx.x);
     const int tx = t % cam.tiles_x, ty = t / cam.tiles_x;
     const int px = tx * 16 + (threadIdx.x & 15);
     const int py0 = ty * 16 + tile_row0(threadIdx.x);
-    const float wy0 = float(ty * 16 + (threadIdx.x >> 5) * 8), wy1 = wy0 + 7.f;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const float wy0 = float(ty * 16 + warp * 8), wy1 = wy0 + 7.f;
     const uint32_t b = starts[t], e = starts[t + 1];
     const float fpx = float(px);
     // per-pixel state as pixel pairs (rows py0+2h, py0+2h+1) for the packed ops
@@ -96,28 +101,39 @@ __global__ void __launch_bounds__(kT, TS_FWD_MINB) blend_fwd_kernel(const uint32
     };
     if (threadIdx.x == 0) s_max = 0;
     for (uint32_t base = b; base < e; base += kBatch) {
-        if (__syncthreads_count(all_done()) == kT) break;
+        __syncwarp();  // every lane is done reading the previous batch
+        if (__all_sync(0xffffffffu, all_done())) break;
+        int n = 0;
 #pragma unroll
-        for (int u = 0; u < kBatch / kT; ++u) {
-            const uint32_t i = base + threadIdx.x + u * kT;
+        for (int u = 0; u < kBatch / 32; ++u) {
+            const uint32_t i = base + uint32_t(lane + 32 * u);
+            float4 s0, s1, s2;
+            bool hit = false;
             if (i < e) {
                 const uint32_t g = __ldg(ival + i);
-                const float4 s0 = __ldg(splat + 3 * g), s1 = __ldg(splat + 3 * g + 1), s2 = __ldg(splat + 3 * g + 2);
-                sA[threadIdx.x + u * kT] = s0;
-                sB[threadIdx.x + u * kT] = make_float4(s1.x, tsx::add(s1.y, s1.y), s1.z, __ldg(ryv + g));
-                sC[threadIdx.x + u * kT] = s2;
+                s0 = __ldg(splat + 3 * g);
+                s1 = __ldg(splat + 3 * g + 1);
+                s2 = __ldg(splat + 3 * g + 2);
+                const float ry = __ldg(ryv + g);
+                hit = !(s0.y + ry < wy0 || s0.y - ry > wy1);  // keep ellipse reaches this warp's rows
             }
+            const uint32_t m = __ballot_sync(0xffffffffu, hit);
+            if (hit) {
+                const int pos = n + __popc(m & ((1u << lane) - 1u));
+                sA[warp][pos] = s0;
+                sB[warp][pos] = make_float4(s1.x, tsx::add(s1.y, s1.y), s1.z, 0.f);
+                sC[warp][pos] = make_float4(s2.x, s2.y, s2.z, __uint_as_float(i - b + 1u));
+            }
+            n += __popc(m);
         }
-        __syncthreads();
-        const int n = int(tmin<uint32_t>(kBatch, e - base));
+        __syncwarp();
         if (!all_done()) {
             for (int j = 0; j < n; ++j) {
-                const float4 q = sB[j];
-                const float4 a = sA[j];
-                if (a.y + q.w < wy0 || a.y - q.w > wy1) continue;  // splat misses this warp's 8 rows
+                const float4 q = sB[warp][j];
+                const float4 a = sA[warp][j];
                 const float dx = tsx::sub(fpx, a.x);
                 const float bdx = tsx::mul(q.y, dx), adxdx = tsx::mul(tsx::mul(q.x, dx), dx);
-                const float4 col = sC[j];
+                const float4 col = sC[warp][j];
                 // keep decisions of the 4 pixels first (exact Q, branch-free), heavy path only if any is set
                 float2 Qp[2];
 #pragma unroll
@@ -126,7 +142,7 @@ __global__ void __launch_bounds__(kT, TS_FWD_MINB) blend_fwd_kernel(const uint32
                     const float2 dy = tsx::sub2(pyp[h], tsx::dup2(a.y));
                     Qp[h] = tsx::fma2(dy, tsx::fma2(tsx::dup2(q.z), dy, tsx::dup2(bdx)), tsx::dup2(adxdx));
                 }
-                const uint32_t idx1 = base - b + uint32_t(j) + 1u;
+                const uint32_t idx1 = __float_as_uint(col.w);
                 if constexpr (kCompat) {
                     uint32_t km = 0;
 #pragma unroll

@@ -1,21 +1,20 @@
-// K6 blend_fwd and K8 blend_bwd: one CTA per 16x16 tile, one thread per pixel.
+// K6 blend_fwd and K8 blend_bwd: one CTA of two warps per 16x16 tile, each thread a 1x4 pixel
+// column; the two warps (8 rows each) run independently.
 //
-// Forward (fragment_alpha SPEC.md:316-324, blend_tile :326-334): the tile's
-// depth-ordered instance list is staged 128 splats at a time into shared memory
-// (gathered by Gaussian index, 48 B rows); each of 64 threads blends a 1x4 pixel
-// column front to back, "blend then stop" at T < 1e-4, and the CTA leaves as
-// soon as all 256 pixels are done (__syncthreads_count).  The keep decision Q <= k2 uses the exact-op
-// quadratic form (bit-identical to the oracle); alpha uses MUFU.EX2.
+// Forward (fragment_alpha SPEC.md:316-324, blend_tile :326-334): each warp stages the tile's
+// depth-ordered instance list 128 entries at a time into its own shared batch, keeping only the
+// splats whose keep ellipse reaches its 8 rows (compacted in list order, 48 B rows gathered by
+// Gaussian index); each thread blends its 4 pixels front to back, "blend then stop" at
+// T < 1e-4, and the warp leaves as soon as its 128 pixels are done.  The keep decision Q <= k2
+// uses the exact-op quadratic form (bit-identical to the oracle); alpha uses MUFU.EX2.
 //
-// Backward (backward_per_pixel SPEC.md:382-390): front-to-back replay with the
-// suffix-colour recurrence (no division by (1 - alpha) of T).
-// Each thread owns a 1x4 pixel column (64 threads per tile): per fragment it
-// sums its 4 pixels' 9 partial gradients, the warp (128 pixels) reduces them
-// with a transposed shuffle reduction (12 SHFL instead of 45), the 2 warps merge
-// in shared memory, and each (Gaussian, tile) pair issues ONE set of vector
-// atomics (RED.F32x4) into the per-Gaussian 2D-gradient accumulator.  A
-// conservative per-warp row cull skips splats whose alpha >= tau ellipse misses
-// the warp's 8 rows before any per-pixel work.
+// Backward (backward_per_pixel SPEC.md:382-390): front-to-back replay of each pixel up to its
+// contributor count, dL/dalpha from the colour still to come (g . U, kept as one scalar) and
+// rcp.approx(1 - alpha).  Per fragment a thread sums its 4 pixels' 9 partial
+// gradients, the warp (128 pixels) reduces them with a transposed shuffle reduction (12 SHFL
+// instead of 45), and the 9 slot lanes send the sums to the per-Gaussian 2D-gradient
+// accumulator (scalar REDs).  Staging as in the forward (per warp, row-culled, up to the warp's
+// last contributor).
 #include "ts_internal.cuh"
 #include "ts_math.cuh"
 
@@ -284,14 +283,18 @@ __device__ __forceinline__ float red9(const float (&v)[9], int lane) {
     return y;
 }
 
-constexpr int kGS = 12;  // smem gradient row stride (floats)
-
 __device__ __forceinline__ float rcp_approx(float x) {
     float y;
     asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
     return y;
 }
 
+// The two warps of a tile run independently: each stages only the splats whose keep ellipse
+// reaches its 8 rows (compacted in list order, up to the warp's last contributor), reduces every
+// fragment over its 128 pixels and sends the 9 sums straight to the accumulator (one scalar RED
+// per slot lane): no shared partial rows, no merge pass and no CTA barrier (round 1 merged the
+// two warps' partials in shared memory and sent one vector RED set per (Gaussian, tile):
+// 0.436 vs 0.420 ms at H).
 __global__ void __launch_bounds__(kT, TS_BWD_MINB) blend_bwd_kernel(const uint32_t* __restrict__ starts,
                                                       const uint32_t* __restrict__ ival,
                                                       const float4* __restrict__ splat, DevCam cam,
@@ -299,24 +302,17 @@ __global__ void __launch_bounds__(kT, TS_BWD_MINB) blend_bwd_kernel(const uint32
                                                       const float* __restrict__ dLdC, float4* __restrict__ g2d,
                                                       const uint32_t* __restrict__ order,
                                                       const float* __restrict__ ryv) {
-    __shared__ float4 sA[kBatch];  // mx, my, k2, o
-    __shared__ float4 sB[kBatch];  // A, 2B, C, ry
-    __shared__ float4 sC[kBatch];  // r, g, b
-    __shared__ uint32_t sIdx[kBatch];
-    __shared__ __align__(16) float sG[2 * kBatch * kGS];  // per-warp partial gradients
-    __shared__ uint32_t s_max;
+    __shared__ float4 sA[2][kBatch];  // mx, my, k2, o
+    __shared__ float4 sB[2][kBatch];  // A, 2B, C, Gaussian index (uint bits)
+    __shared__ float4 sC[2][kBatch];  // r, g, b, list position (uint bits)
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int t = order ? int(order[blockIdx.x]) : int(blockIdx.x);
     const int tx = t % cam.tiles_x, ty = t / cam.tiles_x;
     const int px = tx * 16 + (threadIdx.x & 15);
     const int py0 = ty * 16 + tile_row0(threadIdx.x);
-    const float wy0 = float(ty * 16 + (threadIdx.x >> 5) * 8), wy1 = wy0 + 7.f;
+    const float wy0 = float(ty * 16 + warp * 8), wy1 = wy0 + 7.f;
     const int P = cam.w * cam.h;
     const float fpx = float(px);
-    // per pixel: upstream gradient g, T, count, and gU = g . U where U = C_final - prefix
-    // (the colour still to come after the current fragment, incl. background).  Only
-    // g . U enters the gradient and it updates as gU -= w (g . c), so one scalar suffices.
-    // per-pixel state as pixel pairs (rows py0+2h, py0+2h+1) for the packed fp32x2 ops
     float2 g0p[2], g1p[2], g2p[2], gUp[2], Tp[2];
     const float2 pyp[2] = {make_float2(float(py0), float(py0 + 1)), make_float2(float(py0 + 2), float(py0 + 3))};
     uint32_t cnt[kPPT];
@@ -341,47 +337,46 @@ __global__ void __launch_bounds__(kT, TS_BWD_MINB) blend_bwd_kernel(const uint32
         }
         mymax = max(mymax, cnt[k]);
     }
-    if (threadIdx.x == 0) s_max = 0;
-    __syncthreads();
     const uint32_t wm = __reduce_max_sync(0xffffffffu, mymax);
-    if (lane == 0) atomicMax(&s_max, wm);
-    __syncthreads();
     const uint32_t b = starts[t];
-    const uint32_t e = min(starts[t + 1], b + s_max);
-    // this warp's pixels have no contributor beyond list position wm: its fragment loop stops
-    // there (the CTA keeps staging up to the tile's maximum for the other warp)
+    const uint32_t e = min(starts[t + 1], b + wm);
     const int slot = red9_slot(lane);
+    float* const gacc = reinterpret_cast<float*>(g2d);
     for (uint32_t base = b; base < e; base += kBatch) {
+        __syncwarp();  // every lane is done reading the previous batch
+        int n = 0;
 #pragma unroll
-        for (int u = 0; u < kBatch / kT; ++u) {
-            const int r = threadIdx.x + u * kT;
-            const uint32_t i = base + r;
+        for (int u = 0; u < kBatch / 32; ++u) {
+            const uint32_t i = base + uint32_t(lane + 32 * u);
+            float4 s0, s1, s2;
+            uint32_t g = 0;
+            bool hit = false;
             if (i < e) {
-                const uint32_t g = __ldg(ival + i);
-                const float4 s0 = __ldg(splat + 3 * g), s1 = __ldg(splat + 3 * g + 1), s2 = __ldg(splat + 3 * g + 2);
-                sA[r] = s0;
-                sB[r] = make_float4(s1.x, tsx::add(s1.y, s1.y), s1.z, __ldg(ryv + g));
-                sC[r] = s2;
-                sIdx[r] = g;
+                g = __ldg(ival + i);
+                s0 = __ldg(splat + 3 * g);
+                s1 = __ldg(splat + 3 * g + 1);
+                s2 = __ldg(splat + 3 * g + 2);
+                const float ry = __ldg(ryv + g);
+                hit = !(s0.y + ry < wy0 || s0.y - ry > wy1);
             }
-            float4* z0 = reinterpret_cast<float4*>(sG + r * kGS);
-            float4* z1 = reinterpret_cast<float4*>(sG + (kBatch + r) * kGS);
-#pragma unroll
-            for (int k = 0; k < kGS / 4; ++k) z0[k] = z1[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+            const uint32_t m = __ballot_sync(0xffffffffu, hit);
+            if (hit) {
+                const int pos = n + __popc(m & ((1u << lane) - 1u));
+                sA[warp][pos] = s0;
+                sB[warp][pos] = make_float4(s1.x, tsx::add(s1.y, s1.y), s1.z, __uint_as_float(g));
+                sC[warp][pos] = make_float4(s2.x, s2.y, s2.z, __uint_as_float(i - b));
+            }
+            n += __popc(m);
         }
-        __syncthreads();
-        const int n = int(tmin<uint32_t>(kBatch, e - base));
-        const uint32_t local0 = base - b;
-        const int nw = wm > local0 ? int(tmin<uint32_t>(uint32_t(n), wm - local0)) : 0;
-        for (int j = 0; j < nw; ++j) {
-            const float4 q = sB[j];
-            const float4 a = sA[j];
-            if (a.y + q.w < wy0 || a.y - q.w > wy1) continue;  // warp-uniform row cull
+        __syncwarp();
+        for (int j = 0; j < n; ++j) {
+            const float4 q = sB[warp][j];
+            const float4 a = sA[warp][j];
             const float dx = tsx::sub(fpx, a.x);
             const float adx = tsx::mul(q.x, dx);
             const float bdx = tsx::mul(q.y, dx), adxdx = tsx::mul(adx, dx);
-            const uint32_t li = local0 + uint32_t(j);
-            // keep mask of the 4 pixels first (exact Q, tsx::conic_q); the warp skips the fragment if no lane keeps it
+            const float4 colw = sC[warp][j];
+            const uint32_t li = __float_as_uint(colw.w);
             float2 Qp[2], dyp[2];
             uint32_t km = 0;
 #pragma unroll
@@ -392,7 +387,7 @@ __global__ void __launch_bounds__(kT, TS_BWD_MINB) blend_bwd_kernel(const uint32
                 km |= (li < cnt[2 * h + 1] && Qp[h].y <= a.z) ? (2u << (2 * h)) : 0u;
             }
             if (!__any_sync(0xffffffffu, km)) continue;
-            const float4 col = sC[j];
+            const float4 col = colw;
             const float hoa = 0.5f * a.w;
             const float2 ncx = tsx::dup2(-col.x), ncy = tsx::dup2(-col.y), ncz = tsx::dup2(-col.z);
             // per-thread sums over its pixels (pairs, folded at the end): colour / opacity
@@ -454,30 +449,8 @@ __global__ void __launch_bounds__(kT, TS_BWD_MINB) blend_bwd_kernel(const uint32
             v[7] = vg;
             v[8] = vb;
             const float r = red9(v, lane);
-            if (slot >= 0) sG[(warp * kBatch + j) * kGS + slot] = r;  // per-warp partials: plain stores
+            if (slot >= 0 && r != 0.f) atomicAdd(gacc + 12 * size_t(__float_as_uint(q.w)) + slot, r);
         }
-        __syncthreads();
-#pragma unroll
-        for (int u = 0; u < kBatch / kT; ++u) {
-            const int r = threadIdx.x + u * kT;
-            if (r < n) {
-                const float4* g0s = reinterpret_cast<const float4*>(sG + r * kGS);
-                const float4* g1s = reinterpret_cast<const float4*>(sG + (kBatch + r) * kGS);
-                const float4 x0 = g0s[0], x1 = g0s[1], x2 = g0s[2], y0 = g1s[0], y1 = g1s[1], y2 = g1s[2];
-                const float4 a0 = make_float4(x0.x + y0.x, x0.y + y0.y, x0.z + y0.z, x0.w + y0.w);
-                const float4 a1 = make_float4(x1.x + y1.x, x1.y + y1.y, x1.z + y1.z, x1.w + y1.w);
-                const float a2 = x2.x + y2.x;
-                const bool nz = (a0.x != 0.f) | (a0.y != 0.f) | (a0.z != 0.f) | (a0.w != 0.f) | (a1.x != 0.f) |
-                                (a1.y != 0.f) | (a1.z != 0.f) | (a1.w != 0.f) | (a2 != 0.f);
-                if (nz) {
-                    const uint32_t g = sIdx[r];
-                    atomicAdd(g2d + 3 * g, a0);
-                    atomicAdd(g2d + 3 * g + 1, a1);
-                    atomicAdd(reinterpret_cast<float*>(g2d + 3 * g + 2), a2);
-                }
-            }
-        }
-        __syncthreads();
     }
 }
 

@@ -61,19 +61,31 @@ __global__ void __launch_bounds__(256) adam_kernel(float4* __restrict__ th, floa
     float* gp = &g4.x;
     float* mp = &m4.x;
     float* vp = &v4.x;
+    const tsx::RcpConst c1 = tsx::rcp_const(a.bc1), c2 = tsx::rcp_const(a.bc2);
+    const float b1 = a.b1, b2 = a.b2, omb1 = a.omb1, omb2 = a.omb2, eps = a.eps;
+    auto lr_of = [&](uint32_t i) {
+        return i < bd.b1 ? a.lr[0] : i < bd.b2 ? a.lr[1] : i < bd.b3 ? a.lr[2] : i < bd.b4 ? a.lr[3] : i < bd.b5 ? a.lr[4] : a.lr[5];
+    };
+    const uint32_t i0 = 4u * q;
+    // the quad inside [begin, end) and inside one parameter group (all but a handful of quads
+    // when N % 4 != 0): one learning rate, no per-element range tests
+    const bool uniform = i0 >= begin && i0 + 3u < end && lr_of(i0) == lr_of(i0 + 3u);
+    if (uniform && MODE != 2) {
+        const float lr = lr_of(i0);
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-        const uint32_t i = 4u * q + k;
-        if (i < begin || i >= end) continue;
-        const float lr = i < bd.b1 ? a.lr[0]
-                         : i < bd.b2 ? a.lr[1]
-                         : i < bd.b3 ? a.lr[2]
-                         : i < bd.b4 ? a.lr[3]
-                         : i < bd.b5 ? a.lr[4]
-                                     : a.lr[5];
-        if (visible_of<MODE>(i, bd, vis))
-            tsx::adam_elem(tp[k], gp[k], mp[k], vp[k], lr, a.b1, a.b2, a.omb1, a.omb2, a.eps, a.bc1, a.bc2);
-        if (ZERO) gp[k] = 0.f;
+        for (int k = 0; k < 4; ++k) {
+            tsx::adam_elem(tp[k], gp[k], mp[k], vp[k], lr, b1, b2, omb1, omb2, eps, c1, c2);
+            if (ZERO) gp[k] = 0.f;
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const uint32_t i = i0 + k;
+            if (i < begin || i >= end) continue;
+            if (visible_of<MODE>(i, bd, vis))
+                tsx::adam_elem(tp[k], gp[k], mp[k], vp[k], lr_of(i), b1, b2, omb1, omb2, eps, c1, c2);
+            if (ZERO) gp[k] = 0.f;
+        }
     }
     th[q] = t4;
     m[q] = m4;

@@ -452,6 +452,9 @@ __global__ void __launch_bounds__(kBlock, TS_PB_MINB) project_bwd_kernel(const f
 // fused backward + Adam kernel
 // ---------------------------------------------------------------------------
 constexpr int kFB = 128;  // Gaussians (= threads) per CTA
+#ifndef TS_FB_UNROLL
+#define TS_FB_UNROLL 4
+#endif
 
 struct FusedAdam {
     float lr[6];  // per group
@@ -459,8 +462,9 @@ struct FusedAdam {
 };
 
 // Adam element: the reference op sequence (ts_math.cuh adam_elem)
-__device__ __forceinline__ void adam_fused_elem(float& th, float g, float& m, float& v, float lr, const FusedAdam& a) {
-    tsx::adam_elem(th, g, m, v, lr, a.b1, a.b2, a.omb1, a.omb2, a.eps, a.bc1, a.bc2);
+__device__ __forceinline__ void adam_fused_elem(float& th, float g, float& m, float& v, float lr, const FusedAdam& a,
+                                                tsx::RcpConst c1, tsx::RcpConst c2) {
+    tsx::adam_elem(th, g, m, v, lr, a.b1, a.b2, a.omb1, a.omb2, a.eps, c1, c2);
 }
 
 // shared layout (floats): staged parameters (6 attribute segments of the CTA's
@@ -556,9 +560,12 @@ __global__ void __launch_bounds__(kFB, 4) project_bwd_adam_kernel(float* __restr
             for (int j = 0; j < width[s]; ++j, ++k) pr[s][j] = gs[k];
     }
     __syncthreads();
-#pragma unroll
+    const tsx::RcpConst c1 = tsx::rcp_const(fa.bc1), c2 = tsx::rcp_const(fa.bc2);
+    // a rolled segment loop and 4 element groups in flight keep the sweep's code small (the
+    // unrolled 6 x 12 sweep thrashed the instruction cache: 38% "no instruction" stalls)
+#pragma unroll 1
     for (int s = 0; s < 6; ++s) {
-        constexpr int kU = 12;
+        constexpr int kU = TS_FB_UNROLL;
         const int n = width[s] * rows;
         const float* gr_s = smem + L::kP + segoff[s] + sh[s];
         float* Pg = P + goff[s] + width[s] * g0;
@@ -580,7 +587,7 @@ __global__ void __launch_bounds__(kFB, 4) project_bwd_adam_kernel(float* __restr
             for (int u = 0; u < kU; ++u) {
                 const int i = i0 + u * kFB;
                 if (i < n && (!kSkipInvisible || act[i / width[s]] != 0.f)) {
-                    adam_fused_elem(tr[u], gr_s[i], mr[u], vr[u], lr, fa);
+                    adam_fused_elem(tr[u], gr_s[i], mr[u], vr[u], lr, fa, c1, c2);
                     Pg[i] = tr[u];
                     Mg[i] = mr[u];
                     Vg[i] = vr[u];

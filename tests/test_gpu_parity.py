@@ -183,6 +183,47 @@ def test_adam_bitwise(engine, mode):
     assert np.all(gg == 0)
 
 
+@pytest.mark.parametrize("step", [1, 2, 7, 100, 3000, 30000])
+def test_adam_bitwise_extreme_moments(engine, step):
+    """The device Adam divides by the per-launch bias corrections with the reciprocal hoisted
+    (ts_math.cuh div_const: div.rn's own fast path where it is exact, div.rn elsewhere).  Moments
+    spanning the whole float range -- zeros of both signs, subnormals, values near the overflow
+    threshold, infinities -- must still update bit for bit as the oracle's IEEE divisions do."""
+    n = 4001
+    rng = np.random.default_rng(step)
+    L = 59 * n
+
+    def wide(size, signed):
+        e = rng.integers(-149, 128, size)
+        x = np.ldexp(rng.uniform(1.0, 2.0, size), e).astype(np.float32)
+        if signed:
+            x *= rng.choice([-1.0, 1.0], size).astype(np.float32)
+        k = rng.integers(0, 40, size)
+        x[k == 0] = 0.0
+        x[k == 1] = -0.0 if signed else 0.0
+        x[k == 2] = np.inf
+        return x
+
+    p = scene.random_params(n, 0.02, 0.0, 9)
+    g = np.where(rng.uniform(size=L) < 0.5, 0.0, rng.normal(0, 1e-2, L)).astype(np.float32)
+    m = wide(L, True)
+    v = wide(L, False)
+    m[np.isinf(m)] = 1e30  # inf - inf in m updates would give NaN (payload bits are not compared)
+    engine.set_params(p, n)
+    engine.set_state(grads=g, m=m, v=v)
+    cfg = T.AdamConfig.make(step=step, extent=2.5, zero_grads=1, mode=T.ADAM_FUSED)
+    engine.adam_step(cfg)
+    gp = engine.get_params()
+    _, gm, gv, _, _ = engine.get_state()
+    op, om, ov = p.copy(), m.copy(), v.copy()
+    O.adam_step(op, g.copy(), om, ov, n, np.array(cfg.lr[:], np.float32), cfg.beta1, cfg.beta2, cfg.eps,
+                cfg.bc1, cfg.bc2, mode=T.ADAM_FUSED)
+    for dev, ref in ((gp, op), (gm, om), (gv, ov)):
+        nan = np.isnan(ref)
+        assert np.array_equal(np.isnan(dev), nan)
+        assert np.array_equal(dev[~nan].view(np.uint32), ref[~nan].view(np.uint32))
+
+
 def test_adam_range_and_skip_invisible(engine):
     w = scene.WORKLOADS["c1"]
     p = scene.random_params(w.n, w.s0, w.m_o, w.seed)

@@ -574,3 +574,4 @@ def test_fused_backward_update_against_oracle(engine, mode):
             for x, x0 in ((gp, p0), (gm, m0), (gv, v0)):
                 A, B = x[s0:s1].reshape(n, wd), x0[s0:s1].reshape(n, wd)
                 assert np.array_equal(A[inv], B[inv])
+

@@ -127,6 +127,11 @@ ts_status ts_adam_step(ts_ctx* ctx, const ts_adam_config* cfg);
 /* Adam over [begin, end) of the flat buffer only (sharded optimizer for data parallel). */
 ts_status ts_adam_step_range(ts_ctx* ctx, const ts_adam_config* cfg, int64_t begin, int64_t end);
 
+/* Blend backward: 0 = backward_per_pixel (default, K8), 1 = backward_per_gaussian
+ * (buckets of 32 list entries, one Gaussian per lane, state restored from the BlendCheckpoint the
+ * forward then records).  Not with early_stop_compat or in graph mode. */
+ts_status ts_set_backward_mode(ts_ctx* ctx, int32_t mode);
+
 /* fused_backward_update: backward of the last forward with the Adam
  * update applied to each Gaussian's gradient row in place (modes 3/4); the end state
  * equals ts_backward + ts_adam_step(mode 1/2) bitwise.  Only for single-view steps

@@ -32,7 +32,6 @@ constexpr float kNegHalfLog2e = -0.72134752044448170368f;  // -0.5 * log2(e)
 // lanes 0-15 rows 8w..8w+3, lanes 16-31 rows 8w+4..8w+7; column = tid % 16.
 __device__ __forceinline__ int tile_row0(int tid) { return (tid >> 5) * 8 + ((tid >> 4) & 1) * 4; }
 
-template <bool kCompat>
 // resident-CTA minimums that cap the registers at 72 (K6: 14 CTAs = 28 warps per SM) and 80 (K8: 12
 // CTAs, which also fills the shared memory): measured 0.239 -> 0.217 ms (K6, with the per-warp
 // staging below) and 0.441 -> 0.438 ms (K8) against uncapped 78 / 93 registers; 15-16 CTAs for
@@ -43,6 +42,11 @@ template <bool kCompat>
 #ifndef TS_BWD_MINB
 #define TS_BWD_MINB 12
 #endif
+// kCkpt (per-Gaussian backward): the blend state (T, C) of each pixel before list
+// positions 32, 64, ... (BlendCheckpoint) goes to ckpt[(starts[t] / 32 + t + k) * 256
+// + pixel], written when the warp first reaches a position at or past the boundary (its pixels' state
+// cannot change over entries it skips)
+template <bool kCompat, bool kCkpt>
 __global__ void __launch_bounds__(kT, TS_FWD_MINB) blend_fwd_kernel(const uint32_t* __restrict__ starts,
                                                       const uint32_t* __restrict__ ival,
                                                       const float4* __restrict__ splat, DevCam cam,
@@ -51,7 +55,7 @@ __global__ void __launch_bounds__(kT, TS_FWD_MINB) blend_fwd_kernel(const uint32
                                                       uint32_t* __restrict__ ip_counter,
                                                       const uint32_t* __restrict__ order,
                                                       uint32_t* __restrict__ tile_proc,
-                                                      const float* __restrict__ ryv) {
+                                                      const float* __restrict__ ryv, float4* __restrict__ ckpt) {
     // per-warp staged batches: only the splats whose keep ellipse reaches the warp's 8 rows,
     // compacted in list order (the warps of a tile run independently: no CTA barrier in the loop)
     __shared__ float4 sA[2][kBatch];  // mx, my, k2, o
@@ -98,6 +102,7 @@ __global__ void __launch_bounds__(kT, TS_FWD_MINB) blend_fwd_kernel(const uint32
         if (kCompat) return done == 0xFu;
         return fmaxf(fmaxf(Tp[0].x, Tp[0].y), fmaxf(Tp[1].x, Tp[1].y)) < 1e-4f;
     };
+    uint32_t ckb = 1;  // next checkpoint boundary (kCkpt)
     if (threadIdx.x == 0) s_max = 0;
     for (uint32_t base = b; base < e; base += kBatch) {
         __syncwarp();  // every lane is done reading the previous batch
@@ -142,6 +147,15 @@ __global__ void __launch_bounds__(kT, TS_FWD_MINB) blend_fwd_kernel(const uint32
                     Qp[h] = tsx::fma2(dy, tsx::fma2(tsx::dup2(q.z), dy, tsx::dup2(bdx)), tsx::dup2(adxdx));
                 }
                 const uint32_t idx1 = __float_as_uint(col.w);
+                if constexpr (kCkpt) {
+                    while (32u * ckb < idx1) {  // entry idx1 - 1 is at or past boundary ckb
+                        float4* dst = ckpt + size_t(b / 32u + uint32_t(t) + ckb) * 256u;
+                        const int pr = tile_row0(threadIdx.x), pc = threadIdx.x & 15;
+#pragma unroll
+                        for (int k = 0; k < kPPT; ++k) dst[(pr + k) * 16 + pc] = make_float4(T(k), C0(k), C1(k), C2(k));
+                        ++ckb;
+                    }
+                }
                 if constexpr (kCompat) {
                     uint32_t km = 0;
 #pragma unroll
@@ -454,28 +468,173 @@ __global__ void __launch_bounds__(kT, TS_BWD_MINB) blend_bwd_kernel(const uint32
     }
 }
 
+// ---------------------------------------------------------------------------
+// Per-Gaussian bucket backward (backward_per_gaussian SPEC.md:392-400; option,
+// ts_set_backward_mode(1)).  A CTA of kGW warps per tile; a warp takes a bucket of 32 list
+// entries, one Gaussian per lane.  The tile's per-pixel data (dL/dC, g . C_final, contributor
+// count) sit in shared memory; the pixels still active in the bucket (count past its start) form a
+// compacted list.  Pixel q flows lane 0 -> 31 (step s, lane i handles pixel s - i): lane 0 restores
+// (T, g . U) from the forward's checkpoint at the bucket start, every lane blends its Gaussian into
+// the pixel and hands (T, g . U) to the next lane by shuffle; each lane accumulates its Gaussian's
+// 9 partial gradients over the tile in registers and sends them with one RED set per bucket.
+// Same per-fragment arithmetic as K8 (dL/dalpha from g . U and rcp(1 - alpha)).
+// ---------------------------------------------------------------------------
+constexpr int kGW = 4;
+
+__global__ void __launch_bounds__(kGW * 32) blend_bwd_gauss_kernel(const uint32_t* __restrict__ starts,
+                                                                  const uint32_t* __restrict__ ival,
+                                                                  const float4* __restrict__ splat, DevCam cam,
+                                                                  const float* __restrict__ rgb,
+                                                                  const uint32_t* __restrict__ pcount,
+                                                                  const float* __restrict__ dLdC,
+                                                                  float4* __restrict__ g2d,
+                                                                  const uint32_t* __restrict__ order,
+                                                                  const uint32_t* __restrict__ tile_proc,
+                                                                  const float4* __restrict__ ckpt) {
+    __shared__ float4 sPix[256];  // dL/dC (3), u = g . C_final (incl. background)
+    __shared__ uint32_t sCnt[256];
+    __shared__ uint8_t sList[kGW][256];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int t = order ? int(order[blockIdx.x]) : int(blockIdx.x);
+    const int tx = t % cam.tiles_x, ty = t / cam.tiles_x;
+    const uint32_t b = starts[t];
+    const uint32_t L = min(starts[t + 1] - b, tile_proc[t]);
+    if (L == 0) return;
+    const int P = cam.w * cam.h;
+    for (int pix = threadIdx.x; pix < 256; pix += kGW * 32) {
+        const int px = tx * 16 + (pix & 15), py = ty * 16 + (pix >> 4);
+        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+        uint32_t cn = 0;
+        if (px < cam.w && py < cam.h) {
+            const int p = py * cam.w + px;
+            v.x = dLdC[p];
+            v.y = dLdC[P + p];
+            v.z = dLdC[2 * P + p];
+            v.w = v.x * rgb[p] + v.y * rgb[P + p] + v.z * rgb[2 * P + p];
+            cn = pcount[p];
+        }
+        sPix[pix] = v;
+        sCnt[pix] = cn;
+    }
+    __syncthreads();
+    const uint32_t bbase = b / 32u + uint32_t(t);
+    const uint32_t nbk = (L + 31u) / 32u;
+    const float fx0 = float(tx * 16), fy0 = float(ty * 16);
+    for (uint32_t k = uint32_t(warp); k < nbk; k += kGW) {
+        const uint32_t pos = 32u * k + uint32_t(lane);
+        const bool has = pos < L;
+        float mx = 0.f, my = 0.f, k2 = -1.f, o = 0.f, A = 0.f, B2 = 0.f, C = 0.f, cr = 0.f, cg = 0.f, cb = 0.f;
+        uint32_t g = 0;
+        if (has) {
+            g = __ldg(ival + b + pos);
+            const float4 s0 = __ldg(splat + 3 * g), s1 = __ldg(splat + 3 * g + 1), s2 = __ldg(splat + 3 * g + 2);
+            mx = s0.x, my = s0.y, k2 = s0.z, o = s0.w;
+            A = s1.x, B2 = tsx::add(s1.y, s1.y), C = s1.z;
+            cr = s2.x, cg = s2.y, cb = s2.z;
+        }
+        // pixels with a contributor past the bucket start, compacted
+        int npix = 0;
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+            const int pix = 32 * r + lane;
+            const bool act = sCnt[pix] > 32u * k;
+            const uint32_t m = __ballot_sync(0xffffffffu, act);
+            if (act) sList[warp][npix + __popc(m & ((1u << lane) - 1u))] = uint8_t(pix);
+            npix += __popc(m);
+        }
+        __syncwarp();
+        float a_mx = 0.f, a_my = 0.f, a_A = 0.f, a_B = 0.f, a_C = 0.f, a_o = 0.f, a_r = 0.f, a_g = 0.f, a_b = 0.f;
+        float T = 1.f, gU = 0.f;
+        const float4* ck = ckpt + size_t(bbase + k) * 256u;
+        const float hoa = 0.5f * o;
+        for (int s = 0; s < npix + 31; ++s) {
+            float Tin = __shfl_up_sync(0xffffffffu, T, 1);
+            float gUin = __shfl_up_sync(0xffffffffu, gU, 1);
+            const int q = s - lane;
+            if (q >= 0 && q < npix) {
+                const int pix = sList[warp][q];
+                const float4 pv = sPix[pix];
+                if (lane == 0) {
+                    if (k == 0) {
+                        Tin = 1.f;
+                        gUin = pv.w;
+                    } else {
+                        const float4 c4 = ck[pix];
+                        Tin = c4.x;
+                        gUin = pv.w - (pv.x * c4.y + pv.y * c4.z + pv.z * c4.w);
+                    }
+                }
+                T = Tin;
+                gU = gUin;
+                if (has && pos < sCnt[pix]) {
+                    const float dx = tsx::sub(fx0 + float(pix & 15), mx), dy = tsx::sub(fy0 + float(pix >> 4), my);
+                    const float Q = tsx::conic_q(A, B2, C, dx, dy);
+                    if (Q <= k2) {
+                        const float G = tsx::ex2_approx(Q * kNegHalfLog2e);
+                        const float og = o * G;
+                        const float al = fminf(og, 0.99f);
+                        const float w = al * T;
+                        const float om = 1.f - al;
+                        const float ngc = fmaf(pv.z, -cb, fmaf(pv.y, -cg, pv.x * -cr));
+                        const float after = fmaf(w, ngc, gU);
+                        const float ndal = fmaf(T, ngc, after * rcp_approx(om));
+                        const float nvo = (og <= 0.99f ? G : 0.f) * ndal;
+                        const float dQ = nvo * hoa;
+                        a_mx -= dQ * (2.f * A * dx + B2 * dy);
+                        a_my -= dQ * (B2 * dx + 2.f * C * dy);
+                        a_A += dQ * dx * dx;
+                        a_B += 2.f * dQ * dx * dy;
+                        a_C += dQ * dy * dy;
+                        a_o -= nvo;
+                        a_r += w * pv.x;
+                        a_g += w * pv.y;
+                        a_b += w * pv.z;
+                        T = T * om;
+                        gU = after;
+                    }
+                }
+            }
+        }
+        if (has) {
+            atomicAdd(g2d + 3 * g, make_float4(a_mx, a_my, a_A, a_B));
+            atomicAdd(g2d + 3 * g + 1, make_float4(a_C, a_o, a_r, a_g));
+            atomicAdd(reinterpret_cast<float*>(g2d + 3 * g + 2), a_b);
+        }
+        __syncwarp();  // sList is rebuilt for the next bucket
+    }
+}
+
 }  // namespace
 
 void launch_blend_fwd(Context& c, const DevCam& cam, const ts_render_config& cfg) {
     const int Tn = cam.tiles_x * cam.tiles_y;
     ensure(c, c.tile_proc, size_t(Tn));
-    if (cfg.early_stop_compat)
-        blend_fwd_kernel<true><<<Tn, kT, 0, c.stream>>>(c.starts.p, c.ival[0].p, c.splat.p, cam, cfg, c.rgb.p,
-                                                        c.Tfin.p, c.pcount.p, c.counters.p + 2, c.order_ok ? c.tile_order.p : nullptr,
-                                                        c.tile_proc.p, c.ryv.p);
-    else
-        blend_fwd_kernel<false><<<Tn, kT, 0, c.stream>>>(c.starts.p, c.ival[0].p, c.splat.p, cam, cfg, c.rgb.p,
-                                                         c.Tfin.p, c.pcount.p, c.counters.p + 2, c.order_ok ? c.tile_order.p : nullptr,
-                                                         c.tile_proc.p, c.ryv.p);
+    const uint32_t* ord = c.order_ok ? c.tile_order.p : nullptr;
+    const bool ck = c.backward_mode == 1 && !cfg.early_stop_compat && !c.gmode &&
+                    ensure_grow(c, c.ckpt, (size_t(c.I) / 32 + size_t(Tn) + 1) * 256);
+    c.ckpt_valid = ck;
+#define TS_FWD(C, K)                                                                                          \
+    blend_fwd_kernel<C, K><<<Tn, kT, 0, c.stream>>>(c.starts.p, c.ival[0].p, c.splat.p, cam, cfg, c.rgb.p, c.Tfin.p, \
+                                                    c.pcount.p, c.counters.p + 2, ord, c.tile_proc.p, c.ryv.p,   \
+                                                    c.ckpt.p)
+    if (cfg.early_stop_compat) TS_FWD(true, false);
+    else if (ck) TS_FWD(false, true);
+    else TS_FWD(false, false);
+#undef TS_FWD
     TS_LAUNCHED(c);
 }
 
 void launch_blend_bwd(Context& c, const DevCam& cam, const ts_render_config& cfg) {
     (void)cfg;
     const int Tn = cam.tiles_x * cam.tiles_y;
-    blend_bwd_kernel<<<Tn, kT, 0, c.stream>>>(c.starts.p, c.ival[0].p, c.splat.p, cam, c.rgb.p, c.pcount.p,
-                                              c.dLdC.p, c.g2d.p, c.bwd_order_ok ? c.bwd_order.p : (c.order_ok ? c.tile_order.p : nullptr),
-                                              c.ryv.p);
+    const uint32_t* ord = c.bwd_order_ok ? c.bwd_order.p : (c.order_ok ? c.tile_order.p : nullptr);
+    if (c.backward_mode == 1 && c.ckpt_valid)
+        blend_bwd_gauss_kernel<<<Tn, kGW * 32, 0, c.stream>>>(c.starts.p, c.ival[0].p, c.splat.p, cam, c.rgb.p,
+                                                               c.pcount.p, c.dLdC.p, c.g2d.p, ord, c.tile_proc.p,
+                                                               c.ckpt.p);
+    else
+        blend_bwd_kernel<<<Tn, kT, 0, c.stream>>>(c.starts.p, c.ival[0].p, c.splat.p, cam, c.rgb.p, c.pcount.p,
+                                                  c.dLdC.p, c.g2d.p, ord, c.ryv.p);
     TS_LAUNCHED(c);
 }
 

@@ -563,7 +563,7 @@ bool graph_eligible(const Context& c, const ts_camera& cam, const ts_render_conf
     const int Tn = ((cam.width + 15) / 16) * ((cam.height + 15) / 16);
     // (a live gradient buffer would be accumulated into by the host path; the graph overwrites)
     return c.graph_on && !c.profiling && c.binning_mode == 0 && bin_supported(Tn) && a.mode >= 0 && a.mode <= 2 &&
-           cfg.aa_mode != 1 && c.N > 0 && c.grad_state != Context::kGradLive;
+           cfg.aa_mode != 1 && c.N > 0 && c.grad_state != Context::kGradLive && c.backward_mode == 0;
 }
 
 // every launched graph step verified; voided steps replayed on the host path.  block: wait for the
@@ -1133,6 +1133,16 @@ ts_status ts_set_graph(ts_ctx* x, int32_t on) {
     TS_SETTLE(c);
     c.graph_on = on != 0;
     if (!c.graph_on) drop_graphs(c);
+    return TS_OK;
+}
+
+ts_status ts_set_backward_mode(ts_ctx* x, int32_t mode) {
+    TS_CHECK_CTX(x);
+    Context& c = x->c;
+    if (mode != 0 && mode != 1) return validation(c, "backward mode must be 0 (per-pixel) or 1 (per-Gaussian)");
+    TS_SETTLE(c);
+    c.backward_mode = mode;
+    c.view_valid = false;  // the checkpoints of the per-Gaussian mode come from its own forward
     return TS_OK;
 }
 

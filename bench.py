@@ -331,6 +331,14 @@ def compute_roofline(avg_ms, vstats, clocks, n_tiles, workload):
                 inst = json.load(fh).get(workload, {})
         except Exception:
             inst = {}
+    ceil = {}
+    fc = os.path.join(ROOT, "profiles", "issue_ceiling.json")
+    if os.path.exists(fc):
+        try:
+            with open(fc) as fh:
+                ceil = json.load(fh).get("dense_inst_per_sm_cycle", {})
+        except Exception:
+            ceil = {}
     mhz = clocks.get("sm_mhz") or 1965.0
     out = {"fragment_evals_per_pass": 256 * vstats["Ip"], "sm_mhz": mhz,
            "issue_peak_winst_per_s": 148 * 4 * mhz * 1e6}
@@ -345,6 +353,13 @@ def compute_roofline(avg_ms, vstats, clocks, n_tiles, workload):
         if wi:
             row["warp_inst_per_launch"] = wi
             row["issue_frac"] = wi / (t * out["issue_peak_winst_per_s"])
+            # fraction of the kernel's measured issue ceiling: live warp instructions per SM cycle
+            # over the rate the same kernel sustains on the dense scene (profiles/issue_ceiling.json)
+            dense = ceil.get(k)
+            if dense:
+                row["inst_per_sm_cycle"] = wi / (t * 148 * mhz * 1e6)
+                row["issue_ceiling_inst_per_sm_cycle"] = dense
+                row["frac_of_issue_ceiling"] = row["inst_per_sm_cycle"] / dense
         out[k] = row
     return out
 

@@ -11,10 +11,11 @@
 // Backward (backward_per_pixel SPEC.md:382-390): front-to-back replay of each pixel up to its
 // contributor count, dL/dalpha from the colour still to come (g . U, kept as one scalar) and
 // rcp.approx(1 - alpha).  Per fragment a thread sums its 4 pixels' 9 partial
-// gradients, the warp (128 pixels) reduces them with a transposed shuffle reduction (12 SHFL
-// instead of 45), and the 9 slot lanes send the sums to the per-Gaussian 2D-gradient
-// accumulator (scalar REDs).  Staging as in the forward (per warp, row-culled, up to the warp's
-// last contributor).
+// gradients and parks them in shared memory; every kRF = 3 worked fragments 27 lanes each sum one
+// (fragment, value) row of 32 lane partials (16-byte reads) and send it to the per-Gaussian
+// 2D-gradient accumulator (scalar REDs) -- ~22 instead of ~60 instructions per worked fragment for
+// the transposed shuffle reduction (red9, TS_BWD_SMEMRED=0).  Staging as in the forward (per warp,
+// row-culled, up to the warp's last contributor).
 #include "ts_internal.cuh"
 #include "ts_math.cuh"
 
@@ -22,6 +23,15 @@ namespace ts {
 namespace {
 
 constexpr int kT = 64;       // threads per tile CTA (2 warps)
+#ifndef TS_BWD_SMEMRED
+#define TS_BWD_SMEMRED 1
+#endif
+#ifndef TS_BWD_RF
+#define TS_BWD_RF 3
+#endif
+constexpr int kRF = TS_BWD_RF;  // K8: worked fragments per deferred-reduction flush (<= 9)
+static_assert(kRF >= 1 && kRF <= 9, "flush sums 9 kRF rows, sid / 9 via (sid * 57) >> 9");
+constexpr int kRS = 36;      // K8: shared row stride (floats) of the 32 lane partials of one (fragment, value)
 constexpr int kPPT = 4;      // pixels per thread (a 1x4 column)
 constexpr int kBatch = 128;  // splats staged per round
 constexpr float kNegHalfLog2e = -0.72134752044448170368f;  // -0.5 * log2(e)
@@ -32,15 +42,15 @@ constexpr float kNegHalfLog2e = -0.72134752044448170368f;  // -0.5 * log2(e)
 // lanes 0-15 rows 8w..8w+3, lanes 16-31 rows 8w+4..8w+7; column = tid % 16.
 __device__ __forceinline__ int tile_row0(int tid) { return (tid >> 5) * 8 + ((tid >> 4) & 1) * 4; }
 
-// resident-CTA minimums that cap the registers at 72 (K6: 14 CTAs = 28 warps per SM) and 80 (K8: 12
-// CTAs, which also fills the shared memory): measured 0.239 -> 0.217 ms (K6, with the per-warp
-// staging below) and 0.441 -> 0.438 ms (K8) against uncapped 78 / 93 registers; 15-16 CTAs for
-// K6 were slower again (0.237 ms)
+// resident-CTA minimums that cap the registers at 72 (K6: 14 CTAs = 28 warps per SM) and 96 (K8: 10
+// CTAs, with 20 KB of shared memory each): K6 0.239 -> 0.217 ms (with the per-warp staging below)
+// against 78 uncapped registers, 15-16 CTAs slower again (0.237 ms); K8 (deferred reduction) 0.387 /
+// 0.378 / 0.377 ms at 12 / 11 / 10 CTAs
 #ifndef TS_FWD_MINB
 #define TS_FWD_MINB 14
 #endif
 #ifndef TS_BWD_MINB
-#define TS_BWD_MINB 12
+#define TS_BWD_MINB 10
 #endif
 // kCkpt (per-Gaussian backward): the blend state (T, C) of each pixel before list
 // positions 32, 64, ... (BlendCheckpoint) goes to ckpt[(starts[t] / 32 + t + k) * 256
@@ -354,8 +364,35 @@ __global__ void __launch_bounds__(kT, TS_BWD_MINB) blend_bwd_kernel(const uint32
     const uint32_t wm = __reduce_max_sync(0xffffffffu, mymax);
     const uint32_t b = starts[t];
     const uint32_t e = min(starts[t + 1], b + wm);
-    const int slot = red9_slot(lane);
     float* const gacc = reinterpret_cast<float*>(g2d);
+#if TS_BWD_SMEMRED
+    // deferred reduction: the 9 lane partials of kRF worked fragments are parked in shared memory
+    // (row (fragment, value) of 32 lanes, stride kRS: conflict-free 16-byte reads) and summed by
+    // 9 kRF lanes at once, each reading its row and sending one RED
+    __shared__ __align__(16) float sR[2][kRF * 9 * kRS];
+    __shared__ uint32_t sRg[2][kRF];
+    int nbuf = 0;
+    auto flush = [&]() {
+        __syncwarp();
+        for (int sid = lane; sid < 9 * nbuf; sid += 32) {
+            const float4* row = reinterpret_cast<const float4*>(&sR[warp][sid * kRS]);
+            float2 acc = make_float2(0.f, 0.f);
+#pragma unroll
+            for (int q4 = 0; q4 < 8; ++q4) {
+                const float4 x = row[q4];
+                acc = tsx::add2(acc, make_float2(x.x, x.y));
+                acc = tsx::add2(acc, make_float2(x.z, x.w));
+            }
+            const float r = acc.x + acc.y;
+            const int f = (sid * 57) >> 9;  // sid / 9 (exact for sid < 81)
+            if (r != 0.f) atomicAdd(gacc + 12 * size_t(sRg[warp][f]) + (sid - 9 * f), r);
+        }
+        __syncwarp();
+        nbuf = 0;
+    };
+#else
+    const int slot = red9_slot(lane);
+#endif
     for (uint32_t base = b; base < e; base += kBatch) {
         __syncwarp();  // every lane is done reading the previous batch
         int n = 0;
@@ -462,9 +499,19 @@ __global__ void __launch_bounds__(kT, TS_BWD_MINB) blend_bwd_kernel(const uint32
             v[6] = vr;
             v[7] = vg;
             v[8] = vb;
+#if TS_BWD_SMEMRED
+#pragma unroll
+            for (int k = 0; k < 9; ++k) sR[warp][(nbuf * 9 + k) * kRS + lane] = v[k];
+            if (lane == 0) sRg[warp][nbuf] = __float_as_uint(q.w);
+            if (++nbuf == kRF) flush();
+#else
             const float r = red9(v, lane);
             if (slot >= 0 && r != 0.f) atomicAdd(gacc + 12 * size_t(__float_as_uint(q.w)) + slot, r);
+#endif
         }
+#if TS_BWD_SMEMRED
+        if (nbuf) flush();
+#endif
     }
 }
 

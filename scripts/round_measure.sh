@@ -13,3 +13,9 @@ python bench.py --workload c4 --steps 10 --warmup 3 --no-cpu-baseline > gpurun_o
 python bench.py --graph --steps 200 --no-cpu-baseline > gpurun_out/${P}_bench_graph.json 2> gpurun_out/${P}_bench_graph.err
 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/${P}_ref.json 2> gpurun_out/${P}_ref.err; echo "ref rc=$?"
 bash scripts/prof_round.sh ${P}
+# blend issue ceiling (dense scene vs H) -> scripts/ic_json.py
+M=smsp__inst_executed.sum,smsp__issue_active.avg.pct_of_peak_sustained_active,sm__cycles_elapsed.avg,gpu__time_duration.sum,sm__warps_active.avg.pct_of_peak_sustained_active
+for wl in dense H; do
+  ncu --metrics $M --clock-control none -k regex:blend -c 3 --csv --log-file gpurun_out/${P}_ic_$wl.csv python scripts/issue_ceiling.py $wl 600 > /dev/null 2>&1
+done
+echo "issue ceiling rc=$?"

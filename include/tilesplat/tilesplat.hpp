@@ -185,6 +185,8 @@ class Engine {
         return n;
     }
     void opacity_reset() { check(ts_opacity_reset(ctx_), "ts_opacity_reset"); }
+    // blend backward: 0 per-pixel (default), 1 per-Gaussian buckets
+    void set_backward_mode(int mode) { check(ts_set_backward_mode(ctx_, mode), "ts_set_backward_mode"); }
     // antialias: sampling rates over the training views, post-step 3D-filter clip
     void compute_sampling_rates(const std::vector<Camera>& cams, float extent) {
         std::vector<ts_camera> c;

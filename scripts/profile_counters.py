@@ -27,7 +27,7 @@ lines = ["| kernel | us | warp inst (M) | issue-active % | ALU % | FMA % | XU (M
          "L2 RED req (M) | L2 RED sectors (M) | L2 RED req/s (G) | smem atomic wavefronts (M) |",
          "|---|---|---|---|---|---|---|---|---|---|---|---|---|"]
 inst = {}
-stage = {"preprocess_kernel<3>": "preprocess", "blend_fwd_kernel<0>": "blend", "blend_bwd_kernel": "blend_bwd",
+stage = {"preprocess_kernel<3>": "preprocess", "blend_fwd_kernel<0>": "blend", "blend_fwd_kernel<0, 0>": "blend", "blend_bwd_kernel": "blend_bwd",
          "loss_fused_kernel": "loss", "project_bwd_kernel<3, 0>": "project_bwd", "adam_kernel<1, 0, 0>": "adam",
          "adam_kernel<1, 0>": "adam", "bin_scatter_kernel": "duplicate"}
 for k, m in first.items():

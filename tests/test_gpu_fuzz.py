@@ -55,6 +55,33 @@ def test_fuzz_render_and_gradients(engine, seed):
         assert frac >= 0.99, f"seed {seed} {nm}: {frac:.4f}"
 
 
+@pytest.mark.parametrize("seed", range(12))
+def test_fuzz_per_gaussian_backward(engine, seed):
+    """The per-Gaussian bucket backward (ts_set_backward_mode(1)) over the same
+    configuration space (early-stop compat cases excluded: the option requires the standard stop)."""
+    p, n, cam, cfg = _case(seed)
+    cfg.early_stop_compat = 0
+    engine.set_params(p, n)
+    engine.set_backward_mode(1)
+    try:
+        engine.render(cam, cfg, outputs=False)
+        dl = np.random.default_rng(seed).normal(0, 1e-2, (cam.height, cam.width, 3)).astype(np.float32)
+        engine.zero_grads()
+        engine.backward(dl)
+        G, _, _, _, _ = engine.get_state()
+    finally:
+        engine.set_backward_mode(0)
+    oG, _, _, _ = O.backward(p, n, cam, cfg, dl)
+    for (a, b), nm in zip(T.group_slices(n), T.GROUPS):
+        g, o = G[a:b].astype(np.float64), oG[a:b].astype(np.float64)
+        if not o.any():
+            assert not g.any(), nm
+            continue
+        rms = np.sqrt(np.mean(o * o))
+        frac = np.mean(np.abs(g - o) <= 1e-3 * np.maximum(np.abs(o), rms))
+        assert frac >= 0.99, f"seed {seed} {nm}: {frac:.4f}"
+
+
 @pytest.mark.parametrize("dilation", [0.3, 0.0])
 def test_needles_row_cull_conservative(engine, dilation):
     """High-aspect needles (2D variance up to ~1e5 px^2 along the long axis, sub-pixel across):

@@ -455,6 +455,12 @@ constexpr int kFB = 128;  // Gaussians (= threads) per CTA
 #ifndef TS_FB_UNROLL
 #define TS_FB_UNROLL 4
 #endif
+#ifndef TS_FB_MINB
+#define TS_FB_MINB 4
+#endif
+#ifndef TS_FB_QUADS
+#define TS_FB_QUADS 2
+#endif
 
 struct FusedAdam {
     float lr[6];  // per group
@@ -490,7 +496,7 @@ struct FbLayout {
 //     -- applying the fused Adam element update and writing theta, m, v back.
 //     The gradient never touches HBM.
 template <int DEG, bool kSkipInvisible>
-__global__ void __launch_bounds__(kFB, 4) project_bwd_adam_kernel(float* __restrict__ P, float* __restrict__ Mo,
+__global__ void __launch_bounds__(kFB, TS_FB_MINB) project_bwd_adam_kernel(float* __restrict__ P, float* __restrict__ Mo,
                                                                   float* __restrict__ Vo, float4* __restrict__ g2d,
                                                                   const uint32_t* __restrict__ tcount,
                                                                   float* __restrict__ accum,
@@ -572,7 +578,48 @@ __global__ void __launch_bounds__(kFB, 4) project_bwd_adam_kernel(float* __restr
         float* Mg = Mo + goff[s] + width[s] * g0;
         float* Vg = Vo + goff[s] + width[s] * g0;
         const float lr = fa.lr[s];
-        for (int i0 = tid; i0 < n; i0 += kU * kFB) {
+        int done = 0;
+        if (((goff[s] + width[s] * g0) & 3) == 0) {
+            // segment on a 16-byte boundary (N % 4 == 0): float4 sweep, kQ quads per array in flight
+            const int n4 = n >> 2;
+            const float4* g4 = reinterpret_cast<const float4*>(gr_s);
+            float4* P4 = reinterpret_cast<float4*>(Pg);
+            float4* M4 = reinterpret_cast<float4*>(Mg);
+            float4* V4 = reinterpret_cast<float4*>(Vg);
+            constexpr int kQ = TS_FB_QUADS;
+            for (int q0 = tid; q0 < n4; q0 += kQ * kFB) {
+                float4 tq[kQ], mq[kQ], vq[kQ];
+#pragma unroll
+                for (int u = 0; u < kQ; ++u) {
+                    const int q = q0 + u * kFB;
+                    if (q < n4) {
+                        tq[u] = P4[q];
+                        mq[u] = M4[q];
+                        vq[u] = V4[q];
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < kQ; ++u) {
+                    const int q = q0 + u * kFB;
+                    if (q < n4) {
+                        const float4 gq = g4[q];
+                        float* tp = &tq[u].x;
+                        float* mp = &mq[u].x;
+                        float* vp = &vq[u].x;
+                        const float* gp = &gq.x;
+#pragma unroll
+                        for (int k = 0; k < 4; ++k)
+                            if (!kSkipInvisible || act[(4 * q + k) / width[s]] != 0.f)
+                                adam_fused_elem(tp[k], gp[k], mp[k], vp[k], lr, fa, c1, c2);
+                        P4[q] = tq[u];
+                        M4[q] = mq[u];
+                        V4[q] = vq[u];
+                    }
+                }
+            }
+            done = n4 << 2;
+        }
+        for (int i0 = done + tid; i0 < n; i0 += kU * kFB) {
             float tr[kU], mr[kU], vr[kU];
 #pragma unroll
             for (int u = 0; u < kU; ++u) {

@@ -11,7 +11,8 @@ Contract (north_star; SPEC.md:244-262 sort + ranges, :423 gradients):
   * rgb and final T within 1e-4 max abs; contributor counts equal on >= 99.9% of pixels;
   * training loss within 1e-5 relative;
   * parameter gradients: >= 99% of coordinates per class within 1e-3 relative
-    (absolute floor 1e-3 x class RMS); densify visible counts bitwise, accumulators 1e-3.
+    (absolute floor 1e-3 x class RMS), through the per-pixel backward (default) and the
+    per-Gaussian bucket backward; densify visible counts bitwise, accumulators 1e-3.
 The oracle runs on all host cores (about 10-20 s per configuration and view).
 """
 import os
@@ -67,6 +68,16 @@ def big(request, engine):
     engine.backward(None)
     G, _, _, acc, vc = engine.get_state()
     out.update(G=G, acc=acc, vc=vc)
+    # the same view through the per-Gaussian bucket backward (ts_set_backward_mode(1))
+    engine.set_backward_mode(1)
+    try:
+        engine.zero_grads()
+        engine.render(cam, cfg, outputs=False)
+        engine.training_loss(target, want_value=False)
+        engine.backward(None)
+        out["G_pg"] = engine.get_state()[0]
+    finally:
+        engine.set_backward_mode(0)
     out["oloss"], od = O.training_loss(orgb, target)
     oG, _, oacc, ovc = O.backward(p, n, cam, cfg, od)
     out.update(oG=oG, oacc=oacc, ovc=ovc)
@@ -108,6 +119,13 @@ def test_scale_loss_and_gradients(big):
     n = big["n"]
     for (a, b), nm in zip(T.group_slices(n), T.GROUPS):
         _grad_check(big["G"][a:b], big["oG"][a:b], f"{big['name']}/{nm}")
+
+
+def test_scale_per_gaussian_backward_gradients(big):
+    """backward_per_gaussian at the bench configurations, same contract."""
+    n = big["n"]
+    for (a, b), nm in zip(T.group_slices(n), T.GROUPS):
+        _grad_check(big["G_pg"][a:b], big["oG"][a:b], f"{big['name']}/per-Gaussian/{nm}")
 
 
 def test_scale_densify_stats(big):

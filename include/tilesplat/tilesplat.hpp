@@ -80,6 +80,9 @@ struct RenderConfig {
     int32_t bound_mode = 2;  // rect_opacity
     int32_t cull_mode = 1;   // exact
     int32_t early_stop_compat = 0;
+    int32_t truncation = 0;     // 0 classic, 1 response (keep iff the Mahalanobis distance <= sigma_cut)
+    float sigma_cut = 3.33f;
+    int32_t backward_mode = 0;  // 0 per-pixel, 1 per-Gaussian buckets
     float tau_alpha = 1.0f / 255.0f;
     float dilation = 0.3f;   // classic 0.3; the Mip 2D filter variance 0.1 with AntiAlias::full
     Vec3<float> background{0.f, 0.f, 0.f};
@@ -89,8 +92,8 @@ struct RenderConfig {
     ts_render_config abi() const {
         ts_render_config c{};
         c.sh_degree = sh_degree, c.bound_mode = bound_mode, c.cull_mode = cull_mode;
-        c.truncation = 0, c.early_stop_compat = early_stop_compat, c.backward_mode = 0;
-        c.tau_alpha = tau_alpha, c.dilation = dilation, c.sigma_cut = 3.33f;
+        c.truncation = truncation, c.early_stop_compat = early_stop_compat, c.backward_mode = backward_mode;
+        c.tau_alpha = tau_alpha, c.dilation = dilation, c.sigma_cut = sigma_cut;
         c.bg[0] = background.x, c.bg[1] = background.y, c.bg[2] = background.z;
         c.aa_mode = static_cast<int32_t>(aa), c.kappa3d = kappa3d;
         return c;
@@ -185,8 +188,6 @@ class Engine {
         return n;
     }
     void opacity_reset() { check(ts_opacity_reset(ctx_), "ts_opacity_reset"); }
-    // blend backward: 0 per-pixel (default), 1 per-Gaussian buckets
-    void set_backward_mode(int mode) { check(ts_set_backward_mode(ctx_, mode), "ts_set_backward_mode"); }
     // antialias: sampling rates over the training views, post-step 3D-filter clip
     void compute_sampling_rates(const std::vector<Camera>& cams, float extent) {
         std::vector<ts_camera> c;

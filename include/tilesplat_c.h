@@ -61,12 +61,15 @@ typedef struct {
     int32_t sh_degree;         /* active degree 0..3                    */
     int32_t bound_mode;        /* 0 square, 1 rect, 2 rect_opacity     */
     int32_t cull_mode;         /* 0 none, 1 exact tile culling         */
-    int32_t truncation;        /* 0 classic; others rejected              */
+    int32_t truncation;        /* 0 classic, 1 response: keep iff Q <= sigma_cut^2       */
+                               /*                                       */
     int32_t early_stop_compat; /* 0 blend-then-stop, 1 skip-before-blend   */
-    int32_t backward_mode;     /* 0 per-pixel replay + warp reduction */
+    int32_t backward_mode;     /* 0 per-pixel replay + reduction,     */
+                               /* 1 per-Gaussian buckets; the forward then records the  */
+                               /* BlendCheckpoint            */
     float tau_alpha;           /* 1/255                                                  */
     float dilation;            /* 0.3 with AA off (DESIGN.md App. A.1)                   */
-    float sigma_cut;           /* reserved (response truncation)                         */
+    float sigma_cut;           /* response truncation cutoff in sigmas (3.33)            */
     float bg[3];               /* background colour c_bg                                 */
     int32_t aa_mode;           /* 0 off, 1 filter3d_original, 2 filter3d_clip, 3 full    */
                                /* (clip + Mip 2D filter, dilation 0.1) */
@@ -126,11 +129,6 @@ ts_status ts_reserve_flat(ts_ctx* ctx, int64_t min_len);
 ts_status ts_adam_step(ts_ctx* ctx, const ts_adam_config* cfg);
 /* Adam over [begin, end) of the flat buffer only (sharded optimizer for data parallel). */
 ts_status ts_adam_step_range(ts_ctx* ctx, const ts_adam_config* cfg, int64_t begin, int64_t end);
-
-/* Blend backward: 0 = backward_per_pixel (default, K8), 1 = backward_per_gaussian
- * (buckets of 32 list entries, one Gaussian per lane, state restored from the BlendCheckpoint the
- * forward then records).  Not with early_stop_compat or in graph mode. */
-ts_status ts_set_backward_mode(ts_ctx* ctx, int32_t mode);
 
 /* fused_backward_update: backward of the last forward with the Adam
  * update applied to each Gaussian's gradient row in place (modes 3/4); the end state

@@ -426,8 +426,15 @@ GFwd<T> gaussian_forward(const T* P, int64_t N, int64_t g, const Cam<T>& cam, co
     if (cfg.aa_mode == 3) F.ofac = det_pre > T(0) ? std::sqrt(det_pre / det) : T(0);
     F.o = (cfg.aa_mode == 1 || cfg.aa_mode == 3) ? F.o_raw * F.ofac : F.o_raw;
     T tau = T(cfg.tau_alpha);
-    F.has_bound = F.o > tau;
-    F.k2 = F.has_bound ? T(-2) * M<T>::log_(tau / F.o) : T(0);
+    if (cfg.truncation == 1) {
+        // fragment_alpha response mode: keep iff G >= exp(-sigma_cut^2 / 2), i.e. the
+        // Mahalanobis distance Q <= sigma_cut^2, whatever the opacity
+        F.has_bound = F.o > T(0);
+        F.k2 = F.has_bound ? T(cfg.sigma_cut) * T(cfg.sigma_cut) : T(0);
+    } else {
+        F.has_bound = F.o > tau;
+        F.k2 = F.has_bound ? T(-2) * M<T>::log_(tau / F.o) : T(0);
+    }
     // eval_sh (view dir = mu - campos)
     T d0 = mu[0] - cam.pos[0], d1 = mu[1] - cam.pos[1], d2 = mu[2] - cam.pos[2];
     F.dlen = std::sqrt((d0 * d0 + d1 * d1) + d2 * d2);
@@ -534,6 +541,7 @@ bool tile_keep(T mx, T my, T A, T B, T C, T k2, int tx, int ty, const Cam<T>& ca
 
 template <class T>
 T plain_k2(const tso_render_config& cfg) {
+    if (cfg.truncation == 1) return T(cfg.sigma_cut) * T(cfg.sigma_cut);  // response mode: one cutoff for all
     return T(-2) * M<T>::log_(T(cfg.tau_alpha));
 }
 
@@ -708,7 +716,7 @@ void blend_all(const View<T>& V, const Cam<T>& cam, const tso_render_config& cfg
                     const GFwd<T>& F = V.F[V.vals[i]];
                     T dx = T(px) - F.mx, dy = T(py) - F.my;
                     T Q = conic_q(F.A, F.B + F.B, F.C, dx, dy);
-                    if (!(Q <= F.k2)) continue;  // o*G < tau  (classic truncation)
+                    if (!(Q <= F.k2)) continue;  // classic: o*G < tau; response: G < exp(-sigma_cut^2 / 2)
                     T G = M<T>::exp_blend(T(-0.5) * Q);
                     T al = F.o * G;
                     al = al > T(0.99) ? T(0.99) : al;

@@ -39,12 +39,12 @@ typedef struct {
     int32_t sh_degree;        /* active SH degree 0..3 */
     int32_t bound_mode;       /* 0 square, 1 rect, 2 rect_opacity */
     int32_t cull_mode;        /* 0 none, 1 exact */
-    int32_t truncation;       /* 0 classic */
+    int32_t truncation;       /* 0 classic, 1 response */
     int32_t early_stop_compat;/* 0 blend-then-stop, 1 skip-before-blend */
     int32_t backward_mode;    /* 0 per-pixel, 1 per-gaussian buckets */
     float tau_alpha;          /* 1/255 */
     float dilation;           /* 0.3 when AA off */
-    float sigma_cut;          /* response truncation (unused in classic) */
+    float sigma_cut;          /* response truncation cutoff (sigmas) */
     float bg[3];
     int32_t aa_mode;          /* 0 off, 1 filter3d_original, 2 filter3d_clip, 3 full = clip + mip */
     float kappa3d;            /* 3D filter variance kappa_3D = 0.2 */

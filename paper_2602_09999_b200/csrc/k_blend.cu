@@ -517,7 +517,7 @@ __global__ void __launch_bounds__(kT, TS_BWD_MINB) blend_bwd_kernel(const uint32
 
 // ---------------------------------------------------------------------------
 // Per-Gaussian bucket backward (backward_per_gaussian SPEC.md:392-400; option,
-// ts_set_backward_mode(1)).  A CTA of kGW warps per tile; a warp takes a bucket of 32 list
+// ts_render_config.backward_mode = 1).  A CTA of kGW warps per tile; a warp takes a bucket of 32 list
 // entries, one Gaussian per lane.  The tile's per-pixel data (dL/dC, g . C_final, contributor
 // count) sit in shared memory; the pixels still active in the bucket (count past its start) form a
 // compacted list.  Pixel q flows lane 0 -> 31 (step s, lane i handles pixel s - i): lane 0 restores
@@ -657,7 +657,7 @@ void launch_blend_fwd(Context& c, const DevCam& cam, const ts_render_config& cfg
     const int Tn = cam.tiles_x * cam.tiles_y;
     ensure(c, c.tile_proc, size_t(Tn));
     const uint32_t* ord = c.order_ok ? c.tile_order.p : nullptr;
-    const bool ck = c.backward_mode == 1 && !cfg.early_stop_compat && !c.gmode &&
+    const bool ck = cfg.backward_mode == 1 && !cfg.early_stop_compat && !c.gmode &&
                     ensure_grow(c, c.ckpt, (size_t(c.I) / 32 + size_t(Tn) + 1) * 256);
     c.ckpt_valid = ck;
 #define TS_FWD(C, K)                                                                                          \
@@ -675,7 +675,7 @@ void launch_blend_bwd(Context& c, const DevCam& cam, const ts_render_config& cfg
     (void)cfg;
     const int Tn = cam.tiles_x * cam.tiles_y;
     const uint32_t* ord = c.bwd_order_ok ? c.bwd_order.p : (c.order_ok ? c.tile_order.p : nullptr);
-    if (c.backward_mode == 1 && c.ckpt_valid)
+    if (cfg.backward_mode == 1 && c.ckpt_valid)
         blend_bwd_gauss_kernel<<<Tn, kGW * 32, 0, c.stream>>>(c.starts.p, c.ival[0].p, c.splat.p, cam, c.rgb.p,
                                                                c.pcount.p, c.dLdC.p, c.g2d.p, ord, c.tile_proc.p,
                                                                c.ckpt.p);

@@ -160,15 +160,17 @@ __global__ void __launch_bounds__(kBlock) preprocess_kernel(
         const float rdet = div(1.f, det);
         const float A = mul(c, rdet), B = mul(-b, rdet), C = mul(a, rdet);
         const float mx = fma_(cam.fx, txz, cam.cx), my = fma_(cam.fy, tyz, cam.cy);
-        // activate_opacity; alpha level set Q <= k2  <=>  o exp(-Q/2) >= tau
+        // activate_opacity; keep level set Q <= k2  (classic: o exp(-Q/2) >= tau)
         const float logit = sm[kOp + sh[3] + tid];
         const float o_raw = div(1.f, add(1.f, expf_det(-logit)));
         // Mip compensation: sqrt(det_pre / det_post), detached in the backward
         if (cfg.aa_mode == 3) ofac = det_pre > 0.f ? sqrt_(div(det_pre, det)) : 0.f;
         const float o = (cfg.aa_mode == 1 || cfg.aa_mode == 3) ? mul(o_raw, ofac) : o_raw;
         const float tau = cfg.tau_alpha;
-        const bool has_bound = o > tau;
-        const float k2 = has_bound ? mul(-2.f, logf_det(div(tau, o))) : 0.f;
+        // classic truncation: o G >= tau; response truncation: G >= exp(-sigma_cut^2 / 2)
+        const bool resp = cfg.truncation == 1;
+        const bool has_bound = resp ? o > 0.f : o > tau;
+        const float k2 = !has_bound ? 0.f : resp ? mul(cfg.sigma_cut, cfg.sigma_cut) : mul(-2.f, logf_det(div(tau, o)));
         ok = true;
 
         // ---- eval_sh (colour tolerance path: contraction allowed) ----
@@ -228,7 +230,7 @@ __global__ void __launch_bounds__(kBlock) preprocess_kernel(
             const float lam = add(mid, sqrt_(disc > 0.f ? disc : 0.f));
             rx = ry = mul(3.f, sqrt_(lam));
         } else {
-            const float kk = sqrt_(cfg.bound_mode == 1 ? mul(-2.f, logf_det(tau)) : k2);
+            const float kk = sqrt_(cfg.bound_mode == 1 && !resp ? mul(-2.f, logf_det(tau)) : k2);
             rx = mul(kk, sqrt_(a));
             ry = mul(kk, sqrt_(c));
         }

@@ -166,8 +166,12 @@ bool valid_config(const ts_render_config* cfg, std::string* why) {
     if (cfg->sh_degree < 0 || cfg->sh_degree > 3) return *why = "sh_degree must be 0..3", false;
     if (cfg->bound_mode < 0 || cfg->bound_mode > 2) return *why = "bound_mode must be 0..2", false;
     if (cfg->cull_mode < 0 || cfg->cull_mode > 1) return *why = "cull_mode must be 0..1", false;
-    if (cfg->truncation != 0) return *why = "only classic truncation (0) is supported", false;
-    if (cfg->backward_mode != 0) return *why = "only the per-pixel backward (0) is implemented on device", false;
+    if (cfg->truncation < 0 || cfg->truncation > 1) return *why = "truncation must be 0 (classic) or 1 (response)", false;
+    if (cfg->truncation == 1 && !(cfg->sigma_cut > 0.f && cfg->sigma_cut < 1e3f))
+        return *why = "response truncation needs sigma_cut in (0, 1000)", false;
+    if (cfg->backward_mode < 0 || cfg->backward_mode > 1) return *why = "backward_mode must be 0 (per-pixel) or 1 (per-Gaussian)", false;
+    if (cfg->backward_mode == 1 && cfg->early_stop_compat)
+        return *why = "the per-Gaussian backward needs the standard early stop (early_stop_compat = 0)", false;
     if (!(cfg->tau_alpha > 0.f && cfg->tau_alpha < 1.f)) return *why = "tau_alpha must be in (0,1)", false;
     if (!(cfg->dilation >= 0.f)) return *why = "dilation must be >= 0", false;
     if (cfg->aa_mode < 0 || cfg->aa_mode > 3) return *why = "aa_mode must be 0..3", false;
@@ -563,7 +567,7 @@ bool graph_eligible(const Context& c, const ts_camera& cam, const ts_render_conf
     const int Tn = ((cam.width + 15) / 16) * ((cam.height + 15) / 16);
     // (a live gradient buffer would be accumulated into by the host path; the graph overwrites)
     return c.graph_on && !c.profiling && c.binning_mode == 0 && bin_supported(Tn) && a.mode >= 0 && a.mode <= 2 &&
-           cfg.aa_mode != 1 && c.N > 0 && c.grad_state != Context::kGradLive && c.backward_mode == 0;
+           cfg.aa_mode != 1 && c.N > 0 && c.grad_state != Context::kGradLive && cfg.backward_mode == 0;
 }
 
 // every launched graph step verified; voided steps replayed on the host path.  block: wait for the
@@ -1133,16 +1137,6 @@ ts_status ts_set_graph(ts_ctx* x, int32_t on) {
     TS_SETTLE(c);
     c.graph_on = on != 0;
     if (!c.graph_on) drop_graphs(c);
-    return TS_OK;
-}
-
-ts_status ts_set_backward_mode(ts_ctx* x, int32_t mode) {
-    TS_CHECK_CTX(x);
-    Context& c = x->c;
-    if (mode != 0 && mode != 1) return validation(c, "backward mode must be 0 (per-pixel) or 1 (per-Gaussian)");
-    TS_SETTLE(c);
-    c.backward_mode = mode;
-    c.view_valid = false;  // the checkpoints of the per-Gaussian mode come from its own forward
     return TS_OK;
 }
 

@@ -136,7 +136,6 @@ struct Context {
     bool order_ok = false;         // tile_order is valid for the current view
     DevBuf<uint32_t> tile_proc;    // per tile: list positions the forward processed (its max contributor count)
     DevBuf<uint32_t> bwd_order;    // blend-backward order: tiles by descending processed length
-    int backward_mode = 0;         // 0 per-pixel (K8), 1 per-Gaussian buckets (ts_set_backward_mode)
     DevBuf<float4> ckpt;           // BlendCheckpoint: (T, C) per pixel at every 32-entry bucket start
     bool ckpt_valid = false;       // the last forward wrote checkpoints
     bool bwd_order_ok = false;

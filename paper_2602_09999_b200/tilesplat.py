@@ -88,7 +88,6 @@ _SIGS = {
     "ts_binning_path": [_vp, _vp],
     "ts_launch_count": [_vp, ctypes.POINTER(_i64)],
     "ts_set_graph": [_vp, _i32],
-    "ts_set_backward_mode": [_vp, _i32],
     "ts_graph_stats": [_vp, _vp],
     "ts_host_alloc": [ctypes.c_size_t, ctypes.POINTER(_vp)],
     "ts_host_free": [_vp],
@@ -255,11 +254,6 @@ class Engine:
         """CUDA-graph mode of train_step (ts_set_graph): the step of each view is captured once and
         relaunched; results equal the host-driven path (voided steps are replayed)."""
         self._check(self._L.ts_set_graph(self._h, 1 if on else 0), "ts_set_graph")
-
-    def set_backward_mode(self, mode: int):
-        """Blend backward (ts_set_backward_mode): 0 per-pixel (default), 1 per-Gaussian buckets with
-        forward checkpoints."""
-        self._check(self._L.ts_set_backward_mode(self._h, int(mode)), "ts_set_backward_mode")
 
     def graph_stats(self):
         out = np.zeros(4, np.int64)

@@ -22,6 +22,7 @@ GROUP_WIDTH = (3, 3, 4, 1, 3, 45)
 BOUND_SQUARE, BOUND_RECT, BOUND_RECT_OPACITY = 0, 1, 2
 CULL_NONE, CULL_EXACT = 0, 1
 BACKWARD_PER_PIXEL, BACKWARD_PER_GAUSSIAN = 0, 1
+TRUNC_CLASSIC, TRUNC_RESPONSE = 0, 1  # fragment_alpha modes
 ADAM_REFERENCE, ADAM_FUSED, ADAM_SKIP_INVISIBLE, ADAM_FUSED_BACKWARD, ADAM_FUSED_BACKWARD_SKIP = 0, 1, 2, 3, 4
 AA_OFF, AA_FILTER3D_ORIGINAL, AA_FILTER3D_CLIP, AA_FULL = 0, 1, 2, 3
 AA_MODES = {"off": AA_OFF, "filter3d_original": AA_FILTER3D_ORIGINAL, "filter3d_clip": AA_FILTER3D_CLIP,
@@ -91,7 +92,7 @@ class RenderConfig(ctypes.Structure):
     @classmethod
     def make(cls, sh_degree=3, bound_mode=BOUND_RECT_OPACITY, cull_mode=CULL_EXACT, early_stop_compat=0,
              backward_mode=BACKWARD_PER_PIXEL, tau_alpha=1.0 / 255.0, dilation=None, sigma_cut=3.33,
-             bg=(0.0, 0.0, 0.0), aa="off", kappa3d=0.2) -> "RenderConfig":
+             bg=(0.0, 0.0, 0.0), aa="off", kappa3d=0.2, truncation=TRUNC_CLASSIC) -> "RenderConfig":
         """aa: off | filter3d_original | filter3d_clip | full; the 2D dilation defaults to
         0.3 (classic) unless aa == "full", which uses the Mip filter variance 0.1 with compensation."""
         c = cls()
@@ -100,7 +101,7 @@ class RenderConfig(ctypes.Structure):
         if dilation is None:
             dilation = 0.1 if c.aa_mode == AA_FULL else 0.3
         c.sh_degree, c.bound_mode, c.cull_mode = sh_degree, bound_mode, cull_mode
-        c.truncation, c.early_stop_compat, c.backward_mode = 0, early_stop_compat, backward_mode
+        c.truncation, c.early_stop_compat, c.backward_mode = truncation, early_stop_compat, backward_mode
         c.tau_alpha, c.dilation, c.sigma_cut = tau_alpha, dilation, sigma_cut
         for i in range(3):
             c.bg[i] = bg[i]

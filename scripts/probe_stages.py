@@ -19,7 +19,7 @@ e.set_params(scene.perturb(gt, w.n, w.seed), w.n)
 if os.environ.get("PROBE_MORTON"):
     e.morton_reorder()
 if os.environ.get("PROBE_BWD"):
-    e.set_backward_mode(int(os.environ["PROBE_BWD"]))
+    cfg.backward_mode = int(os.environ["PROBE_BWD"])
 for i in range(5):
     e.train_step(cam, cfg, T.AdamConfig.make(step=i + 1, mode=mode), want_loss=False)
 e.synchronize()

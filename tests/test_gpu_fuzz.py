@@ -57,20 +57,47 @@ def test_fuzz_render_and_gradients(engine, seed):
 
 @pytest.mark.parametrize("seed", range(12))
 def test_fuzz_per_gaussian_backward(engine, seed):
-    """The per-Gaussian bucket backward (ts_set_backward_mode(1)) over the same
-    configuration space (early-stop compat cases excluded: the option requires the standard stop)."""
+    """The per-Gaussian bucket backward (render config backward_mode = 1) over the
+    same configuration space (early-stop compat cases excluded: the option requires the standard stop)."""
     p, n, cam, cfg = _case(seed)
     cfg.early_stop_compat = 0
+    cfg.backward_mode = T.BACKWARD_PER_GAUSSIAN
     engine.set_params(p, n)
-    engine.set_backward_mode(1)
-    try:
-        engine.render(cam, cfg, outputs=False)
-        dl = np.random.default_rng(seed).normal(0, 1e-2, (cam.height, cam.width, 3)).astype(np.float32)
-        engine.zero_grads()
-        engine.backward(dl)
-        G, _, _, _, _ = engine.get_state()
-    finally:
-        engine.set_backward_mode(0)
+    engine.render(cam, cfg, outputs=False)
+    dl = np.random.default_rng(seed).normal(0, 1e-2, (cam.height, cam.width, 3)).astype(np.float32)
+    engine.zero_grads()
+    engine.backward(dl)
+    G, _, _, _, _ = engine.get_state()
+    oG, _, _, _ = O.backward(p, n, cam, cfg, dl)
+    for (a, b), nm in zip(T.group_slices(n), T.GROUPS):
+        g, o = G[a:b].astype(np.float64), oG[a:b].astype(np.float64)
+        if not o.any():
+            assert not g.any(), nm
+            continue
+        rms = np.sqrt(np.mean(o * o))
+        frac = np.mean(np.abs(g - o) <= 1e-3 * np.maximum(np.abs(o), rms))
+        assert frac >= 0.99, f"seed {seed} {nm}: {frac:.4f}"
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_fuzz_response_truncation(engine, seed):
+    """fragment_alpha's response mode (truncation = 1: keep iff G >= exp(-sigma_cut^2/2),
+    whatever the opacity) through the whole path: tile lists bit-exact, images, gradients."""
+    p, n, cam, cfg = _case(seed)
+    cfg.truncation = T.TRUNC_RESPONSE
+    cfg.sigma_cut = float(np.random.default_rng(77 + seed).choice([3.33, 2.5, 3.0]))
+    engine.set_params(p, n)
+    rgb, Tf, cnt = engine.render(cam, cfg)
+    gk, gv, gr = engine.debug_instances()
+    ok, ov, orr, _ = O.instances(p, n, cam, cfg, sort="combined")
+    assert np.array_equal(gk, ok) and np.array_equal(gv, ov) and np.array_equal(gr, orr)
+    orgb, oT, ocnt, _ = O.render(p, n, cam, cfg)
+    assert np.abs(rgb - orgb).max() <= 1e-4 and np.abs(Tf - oT).max() <= 1e-4
+    assert np.mean(cnt == ocnt) >= 0.999
+    dl = np.random.default_rng(seed).normal(0, 1e-2, rgb.shape).astype(np.float32)
+    engine.zero_grads()
+    engine.backward(dl)
+    G, _, _, _, _ = engine.get_state()
     oG, _, _, _ = O.backward(p, n, cam, cfg, dl)
     for (a, b), nm in zip(T.group_slices(n), T.GROUPS):
         g, o = G[a:b].astype(np.float64), oG[a:b].astype(np.float64)

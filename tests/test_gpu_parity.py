@@ -586,21 +586,19 @@ def test_per_gaussian_backward_against_oracle(sc, engine):
     H, W = sc["cam"].height, sc["cam"].width
     dl = rng.normal(0, 1e-3, (H, W, 3)).astype(np.float32)
     engine.set_params(sc["p"], sc["n"])
-    engine.set_backward_mode(1)
-    try:
-        engine.render(sc["cam"], sc["cfg"], outputs=False)
-        g2 = engine.debug_grad2d(dl)
-        og, o2, _, ovc = O.backward(sc["p"], sc["n"], sc["cam"], sc["cfg"], dl)
-        for k, nm in enumerate(["dmx", "dmy", "dA", "dB", "dC", "do", "dr", "dg", "db"]):
-            _grad_check(g2[:, k], o2[:, k], nm)
-        engine.render(sc["cam"], sc["cfg"], outputs=False)
-        engine.backward(dl)
-        G, _, _, _, vc = engine.get_state()
-        n = sc["n"]
-        for (a, b), nm in zip(T.group_slices(n), T.GROUPS):
-            if nm == "sh_rest" and sc["cfg"].sh_degree == 0:
-                continue
-            _grad_check(G[a:b], og[a:b], nm)
-        assert np.array_equal(vc, ovc)
-    finally:
-        engine.set_backward_mode(0)
+    cfg = T.RenderConfig.from_buffer_copy(sc["cfg"])
+    cfg.backward_mode = T.BACKWARD_PER_GAUSSIAN
+    engine.render(sc["cam"], cfg, outputs=False)
+    g2 = engine.debug_grad2d(dl)
+    og, o2, _, ovc = O.backward(sc["p"], sc["n"], sc["cam"], sc["cfg"], dl)
+    for k, nm in enumerate(["dmx", "dmy", "dA", "dB", "dC", "do", "dr", "dg", "db"]):
+        _grad_check(g2[:, k], o2[:, k], nm)
+    engine.render(sc["cam"], cfg, outputs=False)
+    engine.backward(dl)
+    G, _, _, _, vc = engine.get_state()
+    n = sc["n"]
+    for (a, b), nm in zip(T.group_slices(n), T.GROUPS):
+        if nm == "sh_rest" and sc["cfg"].sh_degree == 0:
+            continue
+        _grad_check(G[a:b], og[a:b], nm)
+    assert np.array_equal(vc, ovc)

@@ -68,16 +68,13 @@ def big(request, engine):
     engine.backward(None)
     G, _, _, acc, vc = engine.get_state()
     out.update(G=G, acc=acc, vc=vc)
-    # the same view through the per-Gaussian bucket backward (ts_set_backward_mode(1))
-    engine.set_backward_mode(1)
-    try:
-        engine.zero_grads()
-        engine.render(cam, cfg, outputs=False)
-        engine.training_loss(target, want_value=False)
-        engine.backward(None)
-        out["G_pg"] = engine.get_state()[0]
-    finally:
-        engine.set_backward_mode(0)
+    # the same view through the per-Gaussian bucket backward (render config backward_mode = 1)
+    cfg_pg = T.RenderConfig.make(sh_degree=w.sh_degree, backward_mode=T.BACKWARD_PER_GAUSSIAN)
+    engine.zero_grads()
+    engine.render(cam, cfg_pg, outputs=False)
+    engine.training_loss(target, want_value=False)
+    engine.backward(None)
+    out["G_pg"] = engine.get_state()[0]
     out["oloss"], od = O.training_loss(orgb, target)
     oG, _, oacc, ovc = O.backward(p, n, cam, cfg, od)
     out.update(oG=oG, oacc=oacc, ovc=ovc)

@@ -23,7 +23,7 @@ def _bad_cfg(**kw):
 
 
 @pytest.mark.parametrize("field,value", [("sh_degree", 4), ("sh_degree", -1), ("bound_mode", 3), ("cull_mode", 2),
-                                         ("truncation", 1), ("backward_mode", 1), ("tau_alpha", 0.0),
+                                         ("truncation", 2), ("backward_mode", 2), ("tau_alpha", 0.0),
                                          ("tau_alpha", 1.0), ("dilation", -0.1), ("aa_mode", 4)])
 def test_bad_render_config(engine, field, value):
     p, n, cam, cfg = _small()
@@ -35,6 +35,14 @@ def test_bad_render_config(engine, field, value):
     assert engine.launch_count() == l0
     again, _, _ = engine.render(cam, cfg)
     assert np.array_equal(ref, again)
+
+
+@pytest.mark.parametrize("kw", [dict(truncation=1, sigma_cut=0.0), dict(backward_mode=1, early_stop_compat=1)])
+def test_bad_render_config_combinations(engine, kw):
+    p, n, cam, cfg = _small()
+    engine.set_params(p, n)
+    with pytest.raises(ValidationError):
+        engine.render(cam, _bad_cfg(**kw))
 
 
 def test_bad_camera(engine):

@@ -359,14 +359,14 @@ def test_backward_per_gaussian_equals_per_pixel():  # SPEC.md:398-400, :874 (bit
         assert np.array_equal(x, y)
 
 
-@pytest.mark.parametrize("seed", [0, 1])
-def test_finite_difference_gradients_f64(seed):
+@pytest.mark.parametrize("seed,trunc", [(0, 0), (1, 0), (0, 1), (2, 1)])
+def test_finite_difference_gradients_f64(seed, trunc):  # SPEC.md:390, :423, :873 (incl. truncation modes)
     rng = np.random.default_rng(seed)
     n, W, H = 16, 32, 32
     p = scene.random_params(n, 0.15, 1.0, 40 + seed).astype(np.float64)
     p[0:3 * n] *= 0.6
     cam = scene.make_camera(W, H, eye=(0.2, -0.3, -3.0))
-    cfg = T.RenderConfig.make(sh_degree=3, bg=(0.1, 0.2, 0.3))
+    cfg = T.RenderConfig.make(sh_degree=3, bg=(0.1, 0.2, 0.3), truncation=trunc)
     tgt = rng.uniform(0, 1, (H, W, 3))
 
     def loss(pp):
@@ -391,6 +391,31 @@ def test_finite_difference_gradients_f64(seed):
             scale = max(abs(fd), abs(G[i]), 1e-7)
             ok += abs(fd - G[i]) / scale < 1e-3
         assert ok / len(idx) >= 0.95, f"{name}: {ok}/{len(idx)}"
+
+
+def test_response_truncation_keep_rule():  # SPEC.md:316-324 (response mode), :426
+    o = 0.002  # below tau = 1/255: classic truncation renders nothing of it
+    p, n, cam = _two_splats([math.log(o / (1 - o))], [(0.8, 0.4, 0.2)], W=96, H=96)
+    classic = T.RenderConfig.make(sh_degree=0)
+    resp = T.RenderConfig.make(sh_degree=0, truncation=T.TRUNC_RESPONSE, sigma_cut=3.33)
+    _, Tc, _, Ic = O.render(p, n, cam, classic)
+    assert Ic == 0 and np.all(Tc == 1)
+    splat, _, cnt, _ = O.preprocess(p, n, cam, resp)
+    assert splat[0, 2] == np.float32(3.33) * np.float32(3.33)  # k2 = sigma_cut^2, independent of o
+    _, Tr, cr, Ir = O.render(p, n, cam, resp)
+    assert Ir > 0 and cnt[0] > 0
+    assert abs((1 - Tr[48, 48]) - o) < 1e-6  # alpha = o G, G = 1 at the mean
+    # kept pixels are exactly those within sigma_cut (Mahalanobis): compare with sigma_cut 2
+    _, _, c2, _ = O.render(p, n, cam, T.RenderConfig.make(sh_degree=0, truncation=T.TRUNC_RESPONSE, sigma_cut=2.0))
+    k33, k2 = (cr > 0).sum(), (c2 > 0).sum()
+    assert 2.0 < k33 / k2 < 3.3  # disc areas scale with sigma_cut^2 (3.33^2 / 2^2 = 2.77)
+    # the opacity gradient flows although o G < tau: dL/do = G (c_r - bg_r) at the mean
+    d = np.zeros((96, 96, 3), np.float64)
+    d[48, 48, 0] = 1.0
+    _, g2, _, _ = O.backward(p.astype(np.float64), n, cam, resp, d, f64=True)
+    assert abs(g2[0, 5] - 0.8) < 1e-6
+    _, g2c, _, _ = O.backward(p.astype(np.float64), n, cam, classic, d, f64=True)
+    assert g2c[0, 5] == 0.0
 
 
 def test_densify_stats_examples():

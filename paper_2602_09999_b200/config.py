@@ -47,7 +47,8 @@ class TrainConfig:
     aa_mode: str = "off"          # off | filter3d_original | filter3d_clip | full
     kappa3d: float = 0.2          # 3D filter variance
     rate_interval: int = 100      # sampling-rate recompute interval
-    truncation: str = "classic"
+    truncation: str = "classic"   # classic | response
+    sigma_cut: float = 3.33        # response truncation cutoff (sigmas)
     dynamic_4d: bool = False
     batch_size: int = 1
     seed: int = 0
@@ -66,8 +67,12 @@ class TrainConfig:
             raise ConfigError(f"aa_mode {self.aa_mode!r}: one of {sorted(T.AA_MODES)} (SPEC.md:675)")
         if not self.kappa3d > 0 or self.rate_interval < 1:
             raise ConfigError("kappa3d > 0 and rate_interval >= 1 required")
-        if self.truncation != "classic" or self.dynamic_4d:
-            raise ConfigError("truncation/dynamic_4d: only classic/false are on the B200 path")
+        if self.truncation not in ("classic", "response") or not self.sigma_cut > 0:
+            raise ConfigError("truncation: classic | response, sigma_cut > 0 (SPEC.md:319)")
+        if self.dynamic_4d:
+            raise ConfigError("dynamic_4d: the 4D extension is not on the B200 path")
+        if self.backward_mode not in (T.BACKWARD_PER_PIXEL, T.BACKWARD_PER_GAUSSIAN):
+            raise ConfigError(f"backward_mode {self.backward_mode}")
         if self.optimizer_mode not in range(5):
             raise ConfigError(f"optimizer_mode {self.optimizer_mode}")
         self.densify.validate(self.total_iterations)

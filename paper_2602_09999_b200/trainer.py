@@ -41,8 +41,10 @@ class Trainer:
             from .scene import scene_extent
             extent = scene_extent(self.cams)
         self.extent = float(extent)
-        self.rcfg = render_cfg or T.RenderConfig.make(bound_mode=cfg.bound_mode, cull_mode=cfg.cull_mode,
-                                                      aa=cfg.aa_mode, kappa3d=cfg.kappa3d)
+        self.rcfg = render_cfg or T.RenderConfig.make(
+            bound_mode=cfg.bound_mode, cull_mode=cfg.cull_mode, aa=cfg.aa_mode, kappa3d=cfg.kappa3d,
+            backward_mode=cfg.backward_mode, sigma_cut=cfg.sigma_cut,
+            truncation=T.TRUNC_RESPONSE if cfg.truncation == "response" else T.TRUNC_CLASSIC)
         self.aa = T.AA_MODES[cfg.aa_mode]
         self._rates_stale = True
         self.n_views = len(self.cams)

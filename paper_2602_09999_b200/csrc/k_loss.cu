@@ -29,17 +29,26 @@ __device__ __forceinline__ int refl(int i, int n) { return i < 0 ? -i : (i >= n 
 //                               onto p (per axis; separable)
 //   output   32x32  [0, 32)
 // The transposed filter is the same symmetric window.  Shared memory (floats):
-// A = 5 x 52 x 42 horizontal moments, later hb 3 x 42 x 47;
-// B = 3 x 42 x 58 (input 2 x 52 x 52, then (a, b, c) column-padded to [-10, 48),
-// then vb 3 x 47 x 32).
+// A = 5 x 52 x 42 horizontal moments (row stride 43), later hb 3 x 42 x 47;
+// B = 3 x 42 x 58 (row stride 59) (input 2 x 52 x 52 (row stride 53), then (a, b, c)
+// column-padded to [-10, 48), then vb 3 x 47 x 32).
 // ---------------------------------------------------------------------------
 constexpr int kFT = 32;                   // output tile edge
 constexpr int kFI = kFT + 20;             // input region edge (52)
 constexpr int kFM = kFT + 10;             // moment region edge (42)
 constexpr int kFV = kFT + 15;             // virtual transposed-filter positions (47)
 constexpr int kFP = kFV + 11;             // padded (a, b, c) columns / hf rows (58)
-constexpr int kFA = 5 * kFI * kFM;        // 10920
-constexpr int kFB = 3 * kFM * kFP;        // 7308
+// shared row strides padded to odd word counts: the row-parallel passes (lanes on consecutive
+// rows) then hit 32 distinct banks (round 1's even strides: ~40% of the shared wavefronts were
+// bank conflicts)
+constexpr int kXS = kFI + 1;              // input rows (53)
+constexpr int kAS = kFM + 1;              // horizontal-moment rows (43)
+constexpr int kAP = kFI * kAS;            // one moment plane
+constexpr int kBS = kFP + 1;              // (a, b, c) rows (59)
+constexpr int kBP = kFM * kBS;            // one (a, b, c) plane
+constexpr int kFA = 5 * kAP;              // 11180
+constexpr int kFB = 3 * kBP;              // 7434 (also holds the input 2 x 52 x 53 and vb 3 x 47 x 32)
+static_assert(kFB >= 2 * kFI * kXS && kFB >= 3 * kFV * kFT && kFA >= 3 * kFM * kFV, "shared layout");
 #ifndef TS_LOSS_THREADS
 #define TS_LOSS_THREADS 320  // 10 warps: the 312 horizontal-moment items of a tile in one round
 #endif
@@ -64,7 +73,7 @@ __global__ void __launch_bounds__(kFThreads, 3) loss_fused_kernel(const float* _
     for (int k = 0; k < 11; ++k) wk[k] = c_gw[k];
     // 1. input region (reflect; clamped first so far-outside positions of small images stay in range)
     float* xs = B;
-    float* ys = B + kFI * kFI;
+    float* ys = B + kFI * kXS;
     {
         // kFRowGroups rows x 64 columns per pass (52 active): the column's reflected index
         // once per thread; all rows' loads issued before any store (latency overlapped)
@@ -83,8 +92,8 @@ __global__ void __launch_bounds__(kFThreads, 3) loss_fused_kernel(const float* _
             for (int k = 0; k < kFRowIters; ++k) {
                 const int r = (tid >> 6) + kFRowGroups * k;
                 if (r < kFI) {
-                    xs[r * kFI + c] = xv[k];
-                    ys[r * kFI + c] = yv[k];
+                    xs[r * kXS + c] = xv[k];
+                    ys[r * kXS + c] = yv[k];
                 }
             }
         }
@@ -95,11 +104,11 @@ __global__ void __launch_bounds__(kFThreads, 3) loss_fused_kernel(const float* _
     {
         constexpr int S = 7, NS = kFM / S;
         for (int it = tid; it < kFI * NS; it += kFThreads) {
-            const int r = it / NS, c0 = (it - r * NS) * S;
+            const int r = it % kFI, c0 = (it / kFI) * S;  // lanes on consecutive rows
             // (x, y) pairs: {mu_x, mu_y} and {x^2, y^2} moments in packed fp32x2 ops
             float2 ab[S + 10];
 #pragma unroll
-            for (int k = 0; k < S + 10; ++k) ab[k] = make_float2(xs[r * kFI + c0 + k], ys[r * kFI + c0 + k]);
+            for (int k = 0; k < S + 10; ++k) ab[k] = make_float2(xs[r * kXS + c0 + k], ys[r * kXS + c0 + k]);
 #pragma unroll
             for (int j = 0; j < S; ++j) {
                 float2 m01 = make_float2(0.f, 0.f), m23 = m01;
@@ -112,12 +121,12 @@ __global__ void __launch_bounds__(kFThreads, 3) loss_fused_kernel(const float* _
                     m23 = tsx::fma2(wv, v, m23);
                     m4 = fmaf(wv.x, v.y, m4);
                 }
-                const int o = r * kFM + c0 + j;
+                const int o = r * kAS + c0 + j;
                 A[o] = m01.x;
-                A[kFI * kFM + o] = m01.y;
-                A[2 * kFI * kFM + o] = m23.x;
-                A[3 * kFI * kFM + o] = m23.y;
-                A[4 * kFI * kFM + o] = m4;
+                A[kAP + o] = m01.y;
+                A[2 * kAP + o] = m23.x;
+                A[3 * kAP + o] = m23.y;
+                A[4 * kAP + o] = m4;
             }
         }
     }
@@ -134,7 +143,7 @@ __global__ void __launch_bounds__(kFThreads, 3) loss_fused_kernel(const float* _
                 float2 win[S + 10];
 #pragma unroll
                 for (int k = 0; k < S + 10; ++k)
-                    win[k] = make_float2(A[q * kFI * kFM + (r0 + k) * kFM + c], A[(q + 1) * kFI * kFM + (r0 + k) * kFM + c]);
+                    win[k] = make_float2(A[q * kAP + (r0 + k) * kAS + c], A[(q + 1) * kAP + (r0 + k) * kAS + c]);
 #pragma unroll
                 for (int j = 0; j < S; ++j) {
                     float2 sacc = make_float2(0.f, 0.f);
@@ -147,7 +156,7 @@ __global__ void __launch_bounds__(kFThreads, 3) loss_fused_kernel(const float* _
             {
                 float win[S + 10];
 #pragma unroll
-                for (int k = 0; k < S + 10; ++k) win[k] = A[4 * kFI * kFM + (r0 + k) * kFM + c];
+                for (int k = 0; k < S + 10; ++k) win[k] = A[4 * kAP + (r0 + k) * kAS + c];
 #pragma unroll
                 for (int j = 0; j < S; ++j) {
                     float sacc = 0.f;
@@ -177,14 +186,14 @@ __global__ void __launch_bounds__(kFThreads, 3) loss_fused_kernel(const float* _
                     tc = dS_dcxy;
                     if (r >= 5 && r < 5 + kFT && c >= 5 && c < 5 + kFT) ss += Sv;
                 }
-                B[0 * kFM * kFP + r * kFP + c + 5] = ta;
-                B[1 * kFM * kFP + r * kFP + c + 5] = tb;
-                B[2 * kFM * kFP + r * kFP + c + 5] = tc;
+                B[0 * kBP + r * kBS + c + 5] = ta;
+                B[1 * kBP + r * kBS + c + 5] = tb;
+                B[2 * kBP + r * kBS + c + 5] = tc;
             }
         }
         // zero the padding columns [0, 5) and [47, 58) of every (a, b, c) row (3 x 42 rows)
         if (tid < 3 * kFM) {
-            float* row = B + tid * kFP;
+            float* row = B + (tid / kFM) * kBP + (tid % kFM) * kBS;
 #pragma unroll
             for (int k = 0; k < 5; ++k) row[k] = 0.f;
 #pragma unroll
@@ -197,14 +206,14 @@ __global__ void __launch_bounds__(kFThreads, 3) loss_fused_kernel(const float* _
     {
         constexpr int S = 8, NS = (kFV + S - 1) / S;  // 6 segments (48 columns, last partly unused)
         for (int it = tid; it < kFM * NS; it += kFThreads) {
-            const int r = it / NS, c0 = (it - r * NS) * S;
+            const int r = it % kFM, c0 = (it / kFM) * S;  // lanes on consecutive rows
             float2 ab[S + 10];
             float cc[S + 10];
 #pragma unroll
             for (int k = 0; k < S + 10; ++k) {
                 const bool in = c0 + k < kFP;
-                ab[k] = in ? make_float2(B[r * kFP + c0 + k], B[kFM * kFP + r * kFP + c0 + k]) : make_float2(0.f, 0.f);
-                cc[k] = in ? B[2 * kFM * kFP + r * kFP + c0 + k] : 0.f;
+                ab[k] = in ? make_float2(B[r * kBS + c0 + k], B[kBP + r * kBS + c0 + k]) : make_float2(0.f, 0.f);
+                cc[k] = in ? B[2 * kBP + r * kBS + c0 + k] : 0.f;
             }
 #pragma unroll
             for (int j = 0; j < S; ++j) {

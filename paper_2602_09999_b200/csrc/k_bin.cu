@@ -208,7 +208,13 @@ __global__ void __launch_bounds__(kBinThreads, TS_SC_MINB) bin_scatter_kernel(co
 #ifndef TS_SORT_BDIV
 #define TS_SORT_BDIV 1  // list elements per bucket (on average): fewer rank comparisons
 #endif
-constexpr size_t tile_sort_smem(int cap) { return size_t(cap) * 8 + (size_t(cap) / TS_SORT_BDIV + 1) * 4; }
+// bucket counter i lives at cpad(i) = i + i / 32 (one pad word per 32): the threads' contiguous scan
+// segments (per = ceil(L / NT) counters each) then start on distinct banks, so the segment-parallel
+// scan is (nearly) bank-conflict free (round 1: up to 8-way conflicts at per = 8)
+__device__ __forceinline__ int cpad(int i) { return i + (i >> 5); }
+constexpr size_t tile_sort_smem(int cap) {
+    return size_t(cap) * 8 + (size_t(cap) / TS_SORT_BDIV + 1 + (size_t(cap) / TS_SORT_BDIV + 1) / 32 + 1) * 4;
+}
 
 // SEG: CTA blockIdx.x sorts segment (blockIdx.x & 3) of length <= CAP of long tile
 // tiles[blockIdx.x >> 2], in place (every element is loaded before any is written)
@@ -246,7 +252,7 @@ __device__ __forceinline__ void tile_sort_one(uint32_t t, int seg, const uint32_
         s_max = 0u;
     }
     const int nbk = max(1, min(NB, L / TS_SORT_BDIV));
-    for (int i = tid; i <= nbk; i += NT) cnt[i] = 0;
+    for (int i = tid; i <= nbk; i += NT) cnt[cpad(i)] = 0;
     uint32_t gg[R], kk[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) {
@@ -279,7 +285,7 @@ __device__ __forceinline__ void tile_sort_one(uint32_t t, int seg, const uint32_
     for (int r = 0; r < R; ++r) {
         const int i = tid + r * NT;
         bk[r] = min(uint32_t(nbk - 1), uint32_t(float(kk[r] - kmin) * scale));
-        if (i < L) atomicAdd(&cnt[bk[r]], 1u);
+        if (i < L) atomicAdd(&cnt[cpad(int(bk[r]))], 1u);
     }
     __syncthreads();
     // exclusive scan of the bucket counts: every thread a contiguous segment, block scan of the sums
@@ -287,7 +293,7 @@ __device__ __forceinline__ void tile_sort_one(uint32_t t, int seg, const uint32_
         const int per = (nbk + NT - 1) / NT;
         const int s0 = min(nbk, tid * per), s1 = min(nbk, s0 + per);
         uint32_t run = 0;
-        for (int i = s0; i < s1; ++i) run += cnt[i];
+        for (int i = s0; i < s1; ++i) run += cnt[cpad(i)];
         const int lane = tid & 31, wid = tid >> 5;
         uint32_t inc = run;
 #pragma unroll
@@ -310,8 +316,8 @@ __device__ __forceinline__ void tile_sort_one(uint32_t t, int seg, const uint32_
         __syncthreads();
         uint32_t acc = inc - run + s_wsum[wid];
         for (int i = s0; i < s1; ++i) {
-            const uint32_t c = cnt[i];
-            cnt[i] = acc;
+            const uint32_t c = cnt[cpad(i)];
+            cnt[cpad(i)] = acc;
             acc += c;
         }
     }
@@ -321,7 +327,7 @@ __device__ __forceinline__ void tile_sort_one(uint32_t t, int seg, const uint32_
     for (int r = 0; r < R; ++r) {
         const int i = tid + r * NT;
         if (i < L) {
-            const uint32_t p = atomicAdd(&cnt[bk[r]], 1u);
+            const uint32_t p = atomicAdd(&cnt[cpad(int(bk[r]))], 1u);
             skey[p] = kk[r];
             sgid[p] = gg[r];
         }
@@ -334,8 +340,8 @@ __device__ __forceinline__ void tile_sort_one(uint32_t t, int seg, const uint32_
         const int i = tid + r * NT;
         if (i < L) {
             const uint32_t bb = bk[r];
-            const int e = int(cnt[bb]);
-            const int s = bb == 0 ? 0 : int(cnt[bb - 1]);
+            const int e = int(cnt[cpad(int(bb))]);
+            const int s = bb == 0 ? 0 : int(cnt[cpad(int(bb) - 1)]);
             const uint32_t k = kk[r], g = gg[r];
             int rank = s;
             for (int j = s; j < e; ++j) {

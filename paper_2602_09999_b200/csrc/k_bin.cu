@@ -542,19 +542,19 @@ bool launch_bin_count(Context& c, const DevCam& cam, const ts_render_config& cfg
     return true;
 }
 
-void launch_tile_order(Context& c, int Tn) {
+void launch_tile_order(Context& c, int Tn, cudaStream_t st) {
     if (!ensure(c, c.tile_order, size_t(Tn))) return;
     // graph-captured step: the capacity check of the step runs here (see tile_order_kernel)
     const uint32_t capI = uint32_t(std::min<size_t>(c.ival[1].cap, c.ival[0].cap));
-    tile_order_kernel<<<1, 1024, 0, c.stream>>>(c.starts.p, nullptr, Tn, c.tile_order.p,
+    tile_order_kernel<<<1, 1024, 0, st ? st : c.stream>>>(c.starts.p, nullptr, Tn, c.tile_order.p,
                                                 c.gmode ? c.counters.p + kGraphFlag : nullptr, capI,
                                                 c.bintot.p + Tn);
     TS_LAUNCHED(c);
 }
 
-void launch_bwd_tile_order(Context& c, int Tn) {
+void launch_bwd_tile_order(Context& c, int Tn, cudaStream_t st) {
     if (!c.tile_proc.p || !ensure(c, c.bwd_order, size_t(Tn))) return;
-    tile_order_kernel<<<1, 1024, 0, c.stream>>>(c.starts.p, c.tile_proc.p, Tn, c.bwd_order.p, nullptr, 0u, nullptr);
+    tile_order_kernel<<<1, 1024, 0, st ? st : c.stream>>>(c.starts.p, c.tile_proc.p, Tn, c.bwd_order.p, nullptr, 0u, nullptr);
     TS_LAUNCHED(c);
 }
 

@@ -241,6 +241,14 @@ int tile_bits_for(int tn) {
 }
 
 // the forward pipeline of one view
+bool ensure_order_events(Context& c) {
+    if (c.ord_fork) return true;
+    return cudaEventCreateWithFlags(&c.ord_fork, cudaEventDisableTiming) == cudaSuccess &&
+           cudaEventCreateWithFlags(&c.ord_join, cudaEventDisableTiming) == cudaSuccess &&
+           cudaEventCreateWithFlags(&c.bwd_fork, cudaEventDisableTiming) == cudaSuccess &&
+           cudaEventCreateWithFlags(&c.bwd_join, cudaEventDisableTiming) == cudaSuccess;
+}
+
 ts_status run_forward(Context& c, const ts_camera& cam, const ts_render_config& cfg) {
     if (cfg.aa_mode == 1 && !c.nu_valid)
         return validation(c, "aa_mode filter3d_original needs ts_compute_sampling_rates (or ts_set_sampling_rates)");
@@ -262,6 +270,8 @@ ts_status run_forward(Context& c, const ts_camera& cam, const ts_render_config& 
         stage_begin(c, 1);
         if (!launch_bin_count(c, dc, cfg)) return c.err.empty() ? TS_ERR_OOM : TS_ERR_CUDA;
         stage_end(c, 1);
+        if (!ensure_order_events(c)) return cuda_fail(c, cudaGetLastError(), "order events");
+        CK(cudaEventRecord(c.ord_fork, c.stream));  // the tile order needs only the ranges
         // the scatter does not need I on the host: launch it into the current list buffer
         // (bounds-checked) while the host waits for I; relaunched below if the buffer was short
         if (c.ival[1].p && c.ival[1].cap > 0) {
@@ -321,8 +331,13 @@ ts_status run_forward(Context& c, const ts_camera& cam, const ts_render_config& 
             launch_bin_scatter(c, dc, cfg);
             stage_end(c, 3);
         }
-        launch_tile_order(c, Tn);  // also the per-class tile lists of the sorts (longest first)
+        // the tile order (also the per-class tile lists of the sorts, longest first) runs on a side
+        // stream beside the scatter
+        CK(cudaStreamWaitEvent(c.side[1], c.ord_fork, 0));
+        launch_tile_order(c, Tn, c.side[1]);
         if (!c.tile_order.p) return TS_ERR_OOM;
+        CK(cudaEventRecord(c.ord_join, c.side[1]));
+        CK(cudaStreamWaitEvent(c.stream, c.ord_join, 0));
         stage_begin(c, 4);
         launch_tile_depth_sort(c, Tn, max_len);
         stage_end(c, 4);
@@ -332,6 +347,14 @@ ts_status run_forward(Context& c, const ts_camera& cam, const ts_render_config& 
     stage_begin(c, 6);
     launch_blend_fwd(c, dc, cfg);
     stage_end(c, 6);
+    // the backward's tile order (by this view's processed lengths) beside the loss
+    if (ensure_order_events(c)) {
+        CK(cudaEventRecord(c.bwd_fork, c.stream));
+        CK(cudaStreamWaitEvent(c.side[1], c.bwd_fork, 0));
+        launch_bwd_tile_order(c, Tn, c.side[1]);
+        CK(cudaEventRecord(c.bwd_join, c.side[1]));
+        c.bwd_order_pending = c.bwd_order.p != nullptr;
+    }
     if (ts_status s = last_launch(c, "forward"); s != TS_OK) return s;
     c.cam = cam;
     c.cfg = cfg;
@@ -344,6 +367,7 @@ ts_status run_forward(Context& c, const ts_camera& cam, const ts_render_config& 
 // runs before the scatter and performs the step's capacity check (tile_order_kernel); the size
 // classes are launched on resident grids that read the device-side class counts.
 ts_status run_forward_graph(Context& c, const ts_camera& cam, const ts_render_config& cfg) {
+    c.bwd_order_pending = false;  // the captured backward builds its order in-line
     DevCam dc = make_devcam(cam);
     const int Tn = dc.tiles_x * dc.tiles_y;
     if (ensure_frame(c, cam.width, cam.height) != TS_OK) return TS_ERR_OOM;
@@ -427,8 +451,10 @@ ts_status run_backward(Context& c, const float* dLdC_hwc) {
     if (c.grad_state != Context::kGradLive)
         CK(cudaMemsetAsync(c.vis.p, 0, size_t(std::max<int64_t>(c.N, 1)), c.stream));
     stage_begin(c, 8);
-    // backward order: tiles by the forward's processed length (the backward's per-tile work)
-    launch_bwd_tile_order(c, dc.tiles_x * dc.tiles_y);
+    // backward order: tiles by the forward's processed length (the backward's per-tile work),
+    // built beside the loss by the host-path forward
+    if (c.bwd_order_pending) CK(cudaStreamWaitEvent(c.stream, c.bwd_join, 0));
+    else launch_bwd_tile_order(c, dc.tiles_x * dc.tiles_y);
     c.bwd_order_ok = c.bwd_order.p != nullptr && c.tile_proc.p != nullptr;
     launch_blend_bwd(c, dc, c.cfg);
     stage_end(c, 8);
@@ -894,6 +920,8 @@ ts_status ts_destroy(ts_ctx* x) {
         if (c.join_ev[k]) cudaEventDestroy(c.join_ev[k]);
     }
     if (c.fork_ev) cudaEventDestroy(c.fork_ev);
+    for (cudaEvent_t e : {c.ord_fork, c.ord_join, c.bwd_fork, c.bwd_join})
+        if (e) cudaEventDestroy(e);
     if (c.copy_stream) cudaStreamDestroy(c.copy_stream);
     if (c.bin_host) cudaFreeHost(c.bin_host);
     if (c.bin_ev) cudaEventDestroy(c.bin_ev);

@@ -147,6 +147,10 @@ struct Context {
     DevBuf<uint32_t> sortmp;     // merge scratch of the long-list class (I entries)
     cudaStream_t side[2] = {nullptr, nullptr};  // fork streams for independent launches
     cudaEvent_t fork_ev = nullptr, join_ev[2] = {nullptr, nullptr};
+    // host path: the two tile-order kernels run on side[1] (the forward order beside the scatter,
+    // the backward order beside the loss), joined before their consumers
+    cudaEvent_t ord_fork = nullptr, ord_join = nullptr, bwd_fork = nullptr, bwd_join = nullptr;
+    bool bwd_order_pending = false;
     // ts_train_step's host-target upload, overlapped with the forward
     cudaStream_t copy_stream = nullptr;
     cudaEvent_t copy_fork = nullptr, copy_join = nullptr;
@@ -205,9 +209,9 @@ bool launch_bin_count(Context& c, const DevCam& cam, const ts_render_config& cfg
 // wait for that read-back; returns I (-1 on error)
 int64_t finish_bin_count(Context& c, uint32_t* max_len);
 // c.tile_order = tiles by descending list length (from the tile ranges; both binning paths)
-void launch_tile_order(Context& c, int Tn);
+void launch_tile_order(Context& c, int Tn, cudaStream_t st = nullptr);
 // c.bwd_order from the forward's processed lengths (the backward's per-tile work)
-void launch_bwd_tile_order(Context& c, int Tn);
+void launch_bwd_tile_order(Context& c, int Tn, cudaStream_t st = nullptr);
 void launch_bin_scatter(Context& c, const DevCam& cam, const ts_render_config& cfg);
 void launch_tile_depth_sort(Context& c, int Tn, uint32_t max_len);
 void launch_blend_fwd(Context& c, const DevCam& cam, const ts_render_config& cfg);

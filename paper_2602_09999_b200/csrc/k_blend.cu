@@ -65,7 +65,8 @@ __global__ void __launch_bounds__(kT, TS_FWD_MINB) blend_fwd_kernel(const uint32
                                                       uint32_t* __restrict__ ip_counter,
                                                       const uint32_t* __restrict__ order,
                                                       uint32_t* __restrict__ tile_proc,
-                                                      const float* __restrict__ ryv, float4* __restrict__ ckpt) {
+                                                      const float* __restrict__ ryv, float4* __restrict__ ckpt,
+                                                      float4* __restrict__ gz, uint32_t nz) {
     // per-warp staged batches: only the splats whose keep ellipse reaches the warp's 8 rows,
     // compacted in list order (the warps of a tile run independently: no CTA barrier in the loop)
     __shared__ float4 sA[2][kBatch];  // mx, my, k2, o
@@ -248,6 +249,9 @@ __global__ void __launch_bounds__(kT, TS_FWD_MINB) blend_fwd_kernel(const uint32
     __syncthreads();
     if (threadIdx.x == 0 && s_max) atomicAdd(ip_counter, s_max);
     if (threadIdx.x == 0 && tile_proc) tile_proc[t] = s_max;
+    // clear the per-Gaussian 2D-gradient accumulator for this view's backward (grid-stride, 16-byte
+    // stores): this issue-bound kernel leaves the DRAM idle, the HBM-bound K9 used to do it
+    for (uint32_t i = blockIdx.x * kT + threadIdx.x; i < nz; i += gridDim.x * kT) gz[i] = make_float4(0.f, 0.f, 0.f, 0.f);
 }
 #undef T
 #undef C0
@@ -663,11 +667,12 @@ void launch_blend_fwd(Context& c, const DevCam& cam, const ts_render_config& cfg
 #define TS_FWD(C, K)                                                                                          \
     blend_fwd_kernel<C, K><<<Tn, kT, 0, c.stream>>>(c.starts.p, c.ival[0].p, c.splat.p, cam, cfg, c.rgb.p, c.Tfin.p, \
                                                     c.pcount.p, c.counters.p + 2, ord, c.tile_proc.p, c.ryv.p,   \
-                                                    c.ckpt.p)
+                                                    c.ckpt.p, c.g2d.p, uint32_t(3 * c.N))
     if (cfg.early_stop_compat) TS_FWD(true, false);
     else if (ck) TS_FWD(false, true);
     else TS_FWD(false, false);
 #undef TS_FWD
+    c.g2d_clean = true;
     TS_LAUNCHED(c);
 }
 
@@ -682,6 +687,7 @@ void launch_blend_bwd(Context& c, const DevCam& cam, const ts_render_config& cfg
     else
         blend_bwd_kernel<<<Tn, kT, 0, c.stream>>>(c.starts.p, c.ival[0].p, c.splat.p, cam, c.rgb.p, c.pcount.p,
                                                   c.dLdC.p, c.g2d.p, ord, c.ryv.p);
+    c.g2d_clean = false;  // K9 consumes it without clearing; the next forward's K6 clears it
     TS_LAUNCHED(c);
 }
 

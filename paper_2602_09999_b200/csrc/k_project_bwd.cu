@@ -414,9 +414,6 @@ __global__ void __launch_bounds__(kBlock, TS_PB_MINB) project_bwd_kernel(const f
             if constexpr (ACCUM) G[idx[k]] += gs[k];
             else G[idx[k]] = gs[k];
         }
-        reinterpret_cast<float4*>(g2d)[3 * g] = make_float4(0.f, 0.f, 0.f, 0.f);
-        reinterpret_cast<float4*>(g2d)[3 * g + 1] = make_float4(0.f, 0.f, 0.f, 0.f);
-        reinterpret_cast<float4*>(g2d)[3 * g + 2] = make_float4(0.f, 0.f, 0.f, 0.f);
         accum[g] = smem[L::kAc + sh[6] + tid] + nrm;
         vcount[g] = smem[L::kVc + sh[7] + tid] + 1.f;
         vis[g] = 1;
@@ -548,9 +545,6 @@ __global__ void __launch_bounds__(kFB, TS_FB_MINB) project_bwd_adam_kernel(float
             const Rows rw{pr[0], pr[1], pr[2], pr[3][0], pr[4], pr[5], smem + L::kG2 + sh[6] + 12 * tid};
             // in place: every SH-rest element is read before its gradient is written
             const float nrm = pb_grads<DEG>(rw, RowSink{pr[5]}, cam, cfg, nu_hat ? nu_hat[g] : 1.f, gs);
-            reinterpret_cast<float4*>(g2d)[3 * g] = make_float4(0.f, 0.f, 0.f, 0.f);
-            reinterpret_cast<float4*>(g2d)[3 * g + 1] = make_float4(0.f, 0.f, 0.f, 0.f);
-            reinterpret_cast<float4*>(g2d)[3 * g + 2] = make_float4(0.f, 0.f, 0.f, 0.f);
             accum[g] = smem[L::kAc + sh[7] + tid] + nrm;
             vcount[g] = smem[L::kVc + sh[8] + tid] + 1.f;
             vis[g] = 1;

@@ -221,6 +221,7 @@ ts_status zero_state(Context& c) {
     CK(cudaMemsetAsync(c.accum.p, 0, N * 4, c.stream));
     CK(cudaMemsetAsync(c.vcount.p, 0, N * 4, c.stream));
     CK(cudaMemsetAsync(c.g2d.p, 0, 3 * N * 16, c.stream));
+    c.g2d_clean = true;
     CK(cudaMemsetAsync(c.vis.p, 0, N, c.stream));
     return TS_OK;
 }
@@ -450,6 +451,7 @@ ts_status run_backward(Context& c, const float* dLdC_hwc) {
     // (cleared here rather than after Adam, so a range-chunked optimizer sweep sees it whole)
     if (c.grad_state != Context::kGradLive)
         CK(cudaMemsetAsync(c.vis.p, 0, size_t(std::max<int64_t>(c.N, 1)), c.stream));
+    if (!c.g2d_clean) CK(cudaMemsetAsync(c.g2d.p, 0, size_t(c.N) * 48, c.stream));  // a second backward of a view
     stage_begin(c, 8);
     // backward order: tiles by the forward's processed length (the backward's per-tile work),
     // built beside the loss by the host-path forward
@@ -478,6 +480,7 @@ ts_status run_backward_adam(Context& c, const float* dLdC_hwc, const ts_adam_con
     }
     DevCam dc = make_devcam(c.cam);
     CK(cudaMemsetAsync(c.vis.p, 0, size_t(std::max<int64_t>(c.N, 1)), c.stream));  // new accumulation
+    if (!c.g2d_clean) CK(cudaMemsetAsync(c.g2d.p, 0, size_t(c.N) * 48, c.stream));
     stage_begin(c, 8);
     launch_blend_bwd(c, dc, c.cfg);
     stage_end(c, 8);
@@ -1421,6 +1424,7 @@ ts_status ts_debug_grad2d(ts_ctx* x, const float* dLdC_hwc, float* g2d9) {
     std::vector<float4> g(3 * N);
     if (N) CK(cudaMemcpyAsync(g.data(), c.g2d.p, 3 * N * 16, cudaMemcpyDeviceToHost, c.stream));
     CK(cudaMemsetAsync(c.g2d.p, 0, 3 * N * 16, c.stream));
+    c.g2d_clean = true;
     CK(cudaStreamSynchronize(c.stream));
     for (size_t k = 0; k < N; ++k) {
         const float* s = reinterpret_cast<const float*>(&g[3 * k]);

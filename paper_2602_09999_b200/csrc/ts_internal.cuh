@@ -151,6 +151,9 @@ struct Context {
     // the backward order beside the loss), joined before their consumers
     cudaEvent_t ord_fork = nullptr, ord_join = nullptr, bwd_fork = nullptr, bwd_join = nullptr;
     bool bwd_order_pending = false;
+    // the 2D-gradient accumulator is all zero (cleared by each forward's K6; a backward accumulates
+    // into it and K9 consumes it without clearing)
+    bool g2d_clean = true;
     // ts_train_step's host-target upload, overlapped with the forward
     cudaStream_t copy_stream = nullptr;
     cudaEvent_t copy_fork = nullptr, copy_join = nullptr;

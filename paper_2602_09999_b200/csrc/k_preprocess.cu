@@ -26,7 +26,7 @@ __global__ void __launch_bounds__(kBlock) preprocess_kernel(
     constexpr int deg = DEG;
     constexpr int nb = (deg + 1) * (deg + 1);
     constexpr int nrest = 3 * (nb - 1);
-    __shared__ __align__(16) float sm[kRest + (nrest > 0 ? 45 * kBlock + 4 : 0)];
+    __shared__ __align__(16) float sm[kRest + (nrest > 0 ? 45 * kBlock + 4 : 12 * kBlock + 4)];
     const Off off(N);
     const int64_t g0 = int64_t(blockIdx.x) * kBlock;
     const int64_t g = g0 + threadIdx.x;
@@ -62,7 +62,7 @@ __global__ void __launch_bounds__(kBlock) preprocess_kernel(
     float zh = 0.f;
     float ry_cull = 0.f;  // blend row-cull half-height (0: no tiles)
     // exact-cull inputs of the warp-cooperative pass (ntl = 0: nothing to test)
-    uint32_t ntl_c = 0, rect0 = 0;
+    uint32_t ntl_c = 0, rect0 = 0, magic_c = 0;
     int tw_c = 1;
     float mx_c = 0.f, my_c = 0.f, A_c = 0.f, B_c = 0.f, C_c = 0.f, k2_c = 0.f, nBA_c = 0.f, nBC_c = 0.f;
     bool big_c = false;
@@ -262,6 +262,7 @@ __global__ void __launch_bounds__(kBlock) preprocess_kernel(
             ntl_c = uint32_t(ntl);
             rect0 = uint32_t(tx0) | (uint32_t(ty0) << 16);
             tw_c = tx1 - tx0 + 1;
+            magic_c = 0xFFFFFFFFu / uint32_t(tw_c);
             mx_c = mx, my_c = my, A_c = A, B_c = B, C_c = C, k2_c = k2;
             nBA_c = div(-B, A), nBC_c = div(-B, C);
             big_c = big;
@@ -277,10 +278,14 @@ __global__ void __launch_bounds__(kBlock) preprocess_kernel(
         // tile_cull_exact, warp-cooperative: the warp's (Gaussian, rect tile) pairs are
         // enumerated as one list (exclusive scan of the rect sizes) and tested 32 at a
         // time, so lanes with small rects do not idle behind the warp's largest one.
-        // Pair e belongs to the last lane whose scan offset is <= e; each owner
-        // gathers its keep bits (row-major rect order) from the ballots.
+        // The nonempty rects are ranked and their cull inputs tabled in shared memory (in
+        // the warp's own, fully consumed SH staging rows); pair e belongs to the rect of
+        // rank (owner of the window's first pair) + (segment starts in the window at or
+        // before e), one OR-reduction per window.  Each Gaussian gathers its keep bits
+        // (row-major rect order) from the window ballots.
         const unsigned kFull = 0xffffffffu;
         const int lane = threadIdx.x & 31;
+        const int warp = threadIdx.x >> 5;
         uint32_t incl = ntl_c;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -289,45 +294,61 @@ __global__ void __launch_bounds__(kBlock) preprocess_kernel(
         }
         const uint32_t excl = incl - ntl_c;
         const uint32_t total = __shfl_sync(kFull, incl, 31);
-        const float rcp_tw = 1.f / float(tw_c);
+        const uint32_t ne = __ballot_sync(kFull, ntl_c != 0);
+        const int rank = __popc(ne & ((1u << lane) - 1u));
+        const int tb = nrest > 0 ? ((kRest + sh[5] + 45 * 32 * warp + 3) & ~3) : ((kRest + 3) & ~3) + 384 * warp;
+        float4* tab = reinterpret_cast<float4*>(sm + tb);
+        __syncwarp();  // the warp's lanes are done with their staged SH rows
+        if (ntl_c) {
+            tab[rank] = make_float4(mx_c, my_c, A_c, B_c);
+            tab[32 + rank] = make_float4(C_c, k2_c, nBA_c, nBC_c);
+            tab[64 + rank] = make_float4(__uint_as_float(rect0), __int_as_float(tw_c), __uint_as_float(magic_c),
+                                         __uint_as_float(excl));
+        }
+        __syncwarp();
         uint32_t* hrow = binH ? binH + size_t(g0 / bin_chunk) * size_t(cam.tiles_x * cam.tiles_y) : nullptr;
         uint64_t mask = 0;
+        uint32_t bcnt = 0;
+        int carry = -1;  // rank of the owner of pair base - 1
         for (uint32_t base = 0; base < total; base += 32) {
             const uint32_t e = base + uint32_t(lane);
-            int own = 0;
-#pragma unroll
-            for (int step = 16; step >= 1; step >>= 1) {
-                const uint32_t ex = __shfl_sync(kFull, excl, own + step);
-                if (ex <= e) own += step;
-            }
-            const float omx = __shfl_sync(kFull, mx_c, own), omy = __shfl_sync(kFull, my_c, own);
-            const float oA = __shfl_sync(kFull, A_c, own), oB = __shfl_sync(kFull, B_c, own);
-            const float oC = __shfl_sync(kFull, C_c, own), ok2 = __shfl_sync(kFull, k2_c, own);
-            const float onBA = __shfl_sync(kFull, nBA_c, own), onBC = __shfl_sync(kFull, nBC_c, own);
-            const uint32_t orect = __shfl_sync(kFull, rect0, own), oex = __shfl_sync(kFull, excl, own);
-            const int otw = __shfl_sync(kFull, tw_c, own);
-            const float orcp = __shfl_sync(kFull, rcp_tw, own);
+            const uint32_t rel = excl - base;  // < 32 iff this lane's segment starts in the window
+            const uint32_t sb = __reduce_or_sync(kFull, (ntl_c != 0 && rel < 32u) ? (1u << rel) : 0u);
+            const int own = carry + __popc(sb & ((2u << lane) - 1u));
+            carry += __popc(sb);
             bool keep = false;
             if (e < total) {
-                const int li = int(e - oex);
-                int q = int(float(li) * orcp);
-                int r = li - q * otw;
-                if (r < 0) r += otw, --q;
+                const float4 p0 = tab[own], p1 = tab[32 + own], p2 = tab[64 + own];
+                const uint32_t li = e - __float_as_uint(p2.w);
+                const uint32_t otw = __float_as_uint(p2.y);
+                // li / otw by a multiply-high (magic = floor((2^32-1)/otw) is at most one short)
+                uint32_t q = __umulhi(li, __float_as_uint(p2.z));
+                uint32_t r = li - q * otw;
                 if (r >= otw) r -= otw, ++q;
-                const int txx = int(orect & 0xffffu) + r, tyy = int(orect >> 16) + q;
-                keep = tile_keep(omx, omy, oA, oB, oC, ok2, onBA, onBC, txx, tyy, cam.w, cam.h);
+                const uint32_t orect = __float_as_uint(p2.x);
+                const int txx = int(orect & 0xffffu) + int(r), tyy = int(orect >> 16) + int(q);
+                keep = tile_keep(p0.x, p0.y, p0.z, p0.w, p1.x, p1.y, p1.z, p1.w, txx, tyy, cam.w, cam.h);
                 if (keep && hrow) atomicAdd(hrow + tyy * cam.tiles_x + txx, 1u);
             }
             const uint32_t K = __ballot_sync(kFull, keep);
-            if (ntl_c) {
+            // this lane's pairs [excl, excl + ntl) -> mask bit (pair - excl); bits of other
+            // lanes' pairs beyond the segment are cleared after the loop
+            const int shf = int(base) - int(excl);
+            if (shf > -32 && shf < 64) mask |= shf >= 0 ? (uint64_t(K) << shf) : uint64_t(K >> -shf);
+            if (big_c) {  // rects of more than 64 tiles: count only
                 const uint32_t lo = excl > base ? excl : base, hi = incl < base + 32 ? incl : base + 32;
                 if (lo < hi) {
                     const uint32_t len = hi - lo;
-                    const uint32_t bits = (K >> (lo - base)) & (len == 32 ? kFull : ((1u << len) - 1u));
-                    cnt += __popc(bits);
-                    if (!big_c) mask |= uint64_t(bits) << (lo - excl);
+                    bcnt += __popc((K >> (lo - base)) & (len == 32 ? kFull : ((1u << len) - 1u)));
                 }
             }
+        }
+        if (big_c) {
+            cnt = bcnt;
+            mask = 0;
+        } else {
+            mask &= ntl_c >= 64 ? ~0ull : ((1ull << ntl_c) - 1ull);
+            cnt = uint32_t(__popcll(mask));
         }
         rc.z = uint32_t(mask);
         rc.w = uint32_t(mask >> 32);

@@ -46,6 +46,10 @@ __device__ __forceinline__ int tile_row0(int tid) { return (tid >> 5) * 8 + ((ti
 // CTAs, with 20 KB of shared memory each): K6 0.239 -> 0.217 ms (with the per-warp staging below)
 // against 78 uncapped registers, 15-16 CTAs slower again (0.237 ms); K8 (deferred reduction) 0.387 /
 // 0.378 / 0.377 ms at 12 / 11 / 10 CTAs
+#ifndef TS_FWD_CHK
+#define TS_FWD_CHK 128  // = kBatch: once per staged batch (16: 0.1985, 32: 0.198, 128: 0.196 ms)
+#endif
+constexpr int kFwdChk = TS_FWD_CHK;
 #ifndef TS_FWD_MINB
 #define TS_FWD_MINB 14
 #endif
@@ -142,8 +146,14 @@ __global__ void __launch_bounds__(kT, TS_FWD_MINB) blend_fwd_kernel(const uint32
             n += __popc(m);
         }
         __syncwarp();
-        if (!all_done()) {
-            for (int j = 0; j < n; ++j) {
+        // the fast path tests for saturation once per kFwdChk entries (a lane leaving the loop
+        // early saves issue slots only once its whole warp has left; a saturated pixel keeps
+        // nothing, so the test placement does not change results)
+        constexpr int kChk = kCompat ? 1 : kFwdChk;
+        for (int j0 = 0; j0 < n; j0 += kChk) {
+            if (all_done()) break;
+            const int j1 = min(n, j0 + kChk);
+            for (int j = j0; j < j1; ++j) {
                 const float4 q = sB[warp][j];
                 const float4 a = sA[warp][j];
                 const float dx = tsx::sub(fpx, a.x);
@@ -222,7 +232,6 @@ __global__ void __launch_bounds__(kT, TS_FWD_MINB) blend_fwd_kernel(const uint32
                         last[2 * h] = k0 ? idx1 : last[2 * h];
                         last[2 * h + 1] = k1 ? idx1 : last[2 * h + 1];
                     }
-                    if (all_done()) break;
                 }
             }
         }

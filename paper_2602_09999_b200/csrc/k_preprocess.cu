@@ -307,6 +307,7 @@ __global__ void __launch_bounds__(kBlock) preprocess_kernel(
         }
         __syncwarp();
         uint32_t* hrow = binH ? binH + size_t(g0 / bin_chunk) * size_t(cam.tiles_x * cam.tiles_y) : nullptr;
+        const bool hist = hrow != nullptr;
         uint64_t mask = 0;
         uint32_t bcnt = 0;
         int carry = -1;  // rank of the owner of pair base - 1
@@ -328,7 +329,7 @@ __global__ void __launch_bounds__(kBlock) preprocess_kernel(
                 const uint32_t orect = __float_as_uint(p2.x);
                 const int txx = int(orect & 0xffffu) + int(r), tyy = int(orect >> 16) + int(q);
                 keep = tile_keep(p0.x, p0.y, p0.z, p0.w, p1.x, p1.y, p1.z, p1.w, txx, tyy, cam.w, cam.h);
-                if (keep && hrow) atomicAdd(hrow + tyy * cam.tiles_x + txx, 1u);
+                if (keep & hist) atomicAdd(hrow + (uint32_t(tyy) * uint32_t(cam.tiles_x) + uint32_t(txx)), 1u);
             }
             const uint32_t K = __ballot_sync(kFull, keep);
             // this lane's pairs [excl, excl + ntl) -> mask bit (pair - excl); bits of other

@@ -30,6 +30,9 @@
 #ifndef TS_NT_1
 #define TS_NT_1 512
 #endif
+#ifndef TS_SC_FLAT
+#define TS_SC_FLAT 1  // warp-flattened (Gaussian, tile) expansion in the scatter
+#endif
 #ifndef TS_SC_MINB
 #define TS_SC_MINB 2  // 2 resident chunk CTAs (64 registers, rects held in registers): 0.136 -> 0.128 ms
 #endif
@@ -189,6 +192,69 @@ __global__ void __launch_bounds__(kBinThreads, TS_SC_MINB) bin_scatter_kernel(co
         rc[u] = u < npre && g < N ? __ldg(rect + g) : make_uint4(1u, 1u, 0u, 0u);
     }
     __syncthreads();
+#if TS_SC_FLAT
+    // warp-flattened expansion: the (Gaussian, rect tile) pairs of the warp's 32 rects (of at
+    // most 64 tiles) are enumerated as one list and handled 32 per round (lanes do not idle
+    // behind the warp's largest rect); pair e belongs to the rect of rank (owner of the round's
+    // first pair) + (segment starts in the round at or before e), its rect and mask read from
+    // the warp's table; a pair whose mask bit is set claims a slot of its tile's list.  Rects
+    // of more than 64 tiles (exact cull per tile) follow per lane.
+    __shared__ uint4 tabA[kBinThreads / 32][32];  // rect x, rect y, mask lo, mask hi
+    __shared__ uint4 tabB[kBinThreads / 32][32];  // Gaussian, rect width, div magic, first pair
+    const unsigned kFull = 0xffffffffu;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll 1
+    for (int u = 0; u < npre; ++u) {
+        const int64_t g = g0 + threadIdx.x + u * kBinThreads;
+        const uint4 r = rc[u];
+        const int tx0 = r.x & 0xFFFF, tx1 = (r.x >> 16) & 0x7FFF, ty0 = r.y & 0xFFFF, ty1 = (r.y >> 16) & 0x7FFF;
+        const bool nonempty = g < N && tx0 <= tx1 && ty0 <= ty1;
+        const bool big = (r.y & 0x80000000u) != 0;
+        const int wdt = tx1 - tx0 + 1;
+        const uint32_t np = nonempty && !big ? uint32_t(wdt * (ty1 - ty0 + 1)) : 0u;
+        uint32_t incl = np;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t t = __shfl_up_sync(kFull, incl, o);
+            if (lane >= o) incl += t;
+        }
+        const uint32_t excl = incl - np;
+        const uint32_t total = __shfl_sync(kFull, incl, 31);
+        const int rank = __popc(__ballot_sync(kFull, np != 0) & ((1u << lane) - 1u));
+        __syncwarp();
+        if (np) {
+            tabA[warp][rank] = make_uint4(uint32_t(tx0) | (uint32_t(ty0) << 16), 0u, r.z, r.w);
+            tabB[warp][rank] = make_uint4(uint32_t(g), uint32_t(wdt), 0xFFFFFFFFu / uint32_t(wdt), excl);
+        }
+        __syncwarp();
+        int carry = -1;  // rank of the owner of pair base - 1
+        for (uint32_t base = 0; base < total; base += 32) {
+            const uint32_t e = base + uint32_t(lane);
+            const uint32_t rel = excl - base;
+            const uint32_t sb = __reduce_or_sync(kFull, (np != 0 && rel < 32u) ? (1u << rel) : 0u);
+            const int own = carry + __popc(sb & ((2u << lane) - 1u));
+            carry += __popc(sb);
+            if (e < total) {
+                const uint4 A = tabA[warp][own], B = tabB[warp][own];
+                const uint32_t li = e - B.w;
+                const uint32_t word = li < 32u ? A.z : A.w;
+                if ((word >> (li & 31u)) & 1u) {
+                    uint32_t q = __umulhi(li, B.z);
+                    uint32_t rr = li - q * B.y;
+                    if (rr >= B.y) rr -= B.y, ++q;
+                    const uint32_t t = ((A.x >> 16) + q) * uint32_t(tiles_x) + (A.x & 0xFFFFu) + rr;
+                    const uint32_t slot = atomicAdd(&cur[t], 1u);
+                    if (slot < cap) out[slot] = B.x;  // launched before I is known: stay in bounds
+                }
+            }
+        }
+        if (nonempty && big)
+            for (int t = -1; (t = big_rect_next(splat, uint32_t(g), tx0, tx1, ty0, ty1, W, H, tiles_x, cull_mode, t)) >= 0;) {
+                const uint32_t slot = atomicAdd(&cur[t], 1u);
+                if (slot < cap) out[slot] = uint32_t(g);
+            }
+    }
+#else
 #pragma unroll 1
     for (int u = 0; u < npre; ++u) {
         const int64_t g = g0 + threadIdx.x + u * kBinThreads;
@@ -198,6 +264,7 @@ __global__ void __launch_bounds__(kBinThreads, TS_SC_MINB) bin_scatter_kernel(co
                         if (slot < cap) out[slot] = gg;  // launched before I is known: stay in bounds
                     });
     }
+#endif
 }
 
 // ---------------------------------------------------------------------------

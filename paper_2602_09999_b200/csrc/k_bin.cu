@@ -272,6 +272,10 @@ __global__ void __launch_bounds__(kBinThreads, TS_SC_MINB) bin_scatter_kernel(co
 // ---------------------------------------------------------------------------
 // shared layout: bucketed keys/indices (CAP each) + bucket counters (CAP/2 + 1);
 // the list itself stays in registers (CAP / NT per thread)
+#ifndef TS_SORT_RU
+#define TS_SORT_RU 1
+#endif
+constexpr int kSortRU = TS_SORT_RU;  // unroll of the rank loop
 #ifndef TS_SORT_BDIV
 #define TS_SORT_BDIV 1  // list elements per bucket (on average): fewer rank comparisons
 #endif
@@ -305,8 +309,9 @@ __device__ __forceinline__ void tile_sort_one(uint32_t t, int seg, const uint32_
                                               uint32_t* __restrict__ out, uint32_t* sm) {
     constexpr int R = CAP / NT;
     constexpr int NB = CAP / TS_SORT_BDIV;  // bucket counters (buckets = L / TS_SORT_BDIV)
-    uint32_t* skey = sm;
-    uint32_t* sgid = sm + CAP;
+    // bucketed (depth key, Gaussian) pairs as one 64-bit word each: key in the high half, so
+    // the rank test on (key, index) is a single unsigned 64-bit comparison
+    unsigned long long* skv = reinterpret_cast<unsigned long long*>(sm);
     uint32_t* cnt = sm + 2 * CAP;
     __shared__ uint32_t s_min, s_max;
     __shared__ uint32_t s_wsum[32];
@@ -395,8 +400,7 @@ __device__ __forceinline__ void tile_sort_one(uint32_t t, int seg, const uint32_
         const int i = tid + r * NT;
         if (i < L) {
             const uint32_t p = atomicAdd(&cnt[cpad(int(bk[r]))], 1u);
-            skey[p] = kk[r];
-            sgid[p] = gg[r];
+            skv[p] = (static_cast<unsigned long long>(kk[r]) << 32) | gg[r];
         }
     }
     __syncthreads();
@@ -409,13 +413,13 @@ __device__ __forceinline__ void tile_sort_one(uint32_t t, int seg, const uint32_
             const uint32_t bb = bk[r];
             const int e = int(cnt[cpad(int(bb))]);
             const int s = bb == 0 ? 0 : int(cnt[cpad(int(bb) - 1)]);
-            const uint32_t k = kk[r], g = gg[r];
+            const unsigned long long mine = (static_cast<unsigned long long>(kk[r]) << 32) | gg[r];
             int rank = s;
-            for (int j = s; j < e; ++j) {
-                const uint32_t kj = skey[j], gj = sgid[j];
-                rank += (kj < k || (kj == k && gj < g)) ? 1 : 0;
-            }
-            out[b + rank] = g;
+            // buckets hold ~2 members on average: a short rolled loop (the compiler's 8-way
+            // unrolling with remainder paths cost more than the loop itself)
+#pragma unroll kSortRU
+            for (int j = s; j < e; ++j) rank += skv[j] < mine ? 1 : 0;
+            out[b + rank] = gg[r];
         }
     }
 }

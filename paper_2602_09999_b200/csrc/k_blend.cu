@@ -46,6 +46,14 @@ __device__ __forceinline__ int tile_row0(int tid) { return (tid >> 5) * 8 + ((ti
 // CTAs, with 20 KB of shared memory each): K6 0.239 -> 0.217 ms (with the per-warp staging below)
 // against 78 uncapped registers, 15-16 CTAs slower again (0.237 ms); K8 (deferred reduction) 0.387 /
 // 0.378 / 0.377 ms at 12 / 11 / 10 CTAs
+#ifndef TS_FWD_JU
+#define TS_FWD_JU 4  // unroll of K6's fragment loop (0: the compiler's choice; 1: +7 us, 2: +0, 4: -2.5 us)
+#endif
+constexpr int kFwdJU = TS_FWD_JU > 0 ? TS_FWD_JU : 1;
+#ifndef TS_BWD_JU
+#define TS_BWD_JU 2  // unroll of K8's fragment loop (0: the compiler's choice; 1: +0, 2: -3 us)
+#endif
+constexpr int kBwdJU = TS_BWD_JU > 0 ? TS_BWD_JU : 1;
 #ifndef TS_FWD_CHK
 #define TS_FWD_CHK 128  // = kBatch: once per staged batch (16: 0.1985, 32: 0.198, 128: 0.196 ms)
 #endif
@@ -153,6 +161,9 @@ __global__ void __launch_bounds__(kT, TS_FWD_MINB) blend_fwd_kernel(const uint32
         for (int j0 = 0; j0 < n; j0 += kChk) {
             if (all_done()) break;
             const int j1 = min(n, j0 + kChk);
+#if TS_FWD_JU > 0
+#pragma unroll kFwdJU
+#endif
             for (int j = j0; j < j1; ++j) {
                 const float4 q = sB[warp][j];
                 const float4 a = sA[warp][j];
@@ -433,6 +444,9 @@ __global__ void __launch_bounds__(kT, TS_BWD_MINB) blend_bwd_kernel(const uint32
             n += __popc(m);
         }
         __syncwarp();
+#if TS_BWD_JU > 0
+#pragma unroll kBwdJU
+#endif
         for (int j = 0; j < n; ++j) {
             const float4 q = sB[warp][j];
             const float4 a = sA[warp][j];

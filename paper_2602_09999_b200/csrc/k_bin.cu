@@ -124,9 +124,13 @@ constexpr int kCapL = 4 * kCap3;
 // 64 tiles x kCS chunk segments per CTA: each thread sums its segment of its tile's
 // column, the segment offsets come from shared memory, then each thread rewrites its
 // segment as the exclusive prefix (second read hits L2)
-constexpr int kCS = 4;
+#ifndef TS_CS
+#define TS_CS 8  // chunk segments per tile column (4: 34 us stage, 8: 28 us, 16: 32 us)
+#endif
+constexpr int kCS = TS_CS;
 __global__ void __launch_bounds__(64 * kCS) bin_colscan_kernel(uint32_t* __restrict__ Hm, int nchunks, int Tn,
-                                                              uint32_t* __restrict__ tot, uint32_t* __restrict__ meta) {
+                                                              uint32_t* __restrict__ tot, uint32_t* __restrict__ meta,
+                                                              uint32_t* __restrict__ starts) {
     __shared__ uint32_t part[kCS][64];
     const int lt = threadIdx.x & 63, sg = threadIdx.x >> 6;
     const int t = blockIdx.x * 64 + lt;
@@ -160,18 +164,55 @@ __global__ void __launch_bounds__(64 * kCS) bin_colscan_kernel(uint32_t* __restr
                 }
         }
     }
-    if (sg != kCS - 1) return;  // the last segment's thread holds the tile total
-    if (t < Tn) {
-        tot[t] = run;
-        const int k = run == 1 ? 0 : run <= uint32_t(kCap0) ? 1 : run <= uint32_t(kCap1) ? 2 : run <= uint32_t(kCapM) ? 5
-                    : run <= uint32_t(kCap2) ? 3 : run <= uint32_t(kCap3) ? 4 : 6;
-        // class counts only: the per-class tile lists are ranges of the tile order (KO)
-        if (run > 0 && run <= uint32_t(kCapL)) atomicAdd(&meta[k], 1u);
-    } else {
-        run = 0;
+    if (sg == kCS - 1) {  // the last segment's thread holds the tile total
+        if (t < Tn) {
+            tot[t] = run;
+            const int k = run == 1 ? 0 : run <= uint32_t(kCap0) ? 1 : run <= uint32_t(kCap1) ? 2 : run <= uint32_t(kCapM) ? 5
+                        : run <= uint32_t(kCap2) ? 3 : run <= uint32_t(kCap3) ? 4 : 6;
+            // class counts only: the per-class tile lists are ranges of the tile order (KO)
+            if (run > 0 && run <= uint32_t(kCapL)) atomicAdd(&meta[k], 1u);
+        } else {
+            run = 0;
+        }
+        const uint32_t wm = __reduce_max_sync(0xffffffffu, run);
+        if ((threadIdx.x & 31) == 0 && wm) atomicMax(&meta[7], wm);
     }
-    const uint32_t wm = __reduce_max_sync(0xffffffffu, run);
-    if ((threadIdx.x & 31) == 0 && wm) atomicMax(&meta[7], wm);
+    // the last CTA to finish scans the tile totals into the tile ranges (starts[Tn] = I):
+    // no separate scan launch
+    __shared__ uint32_t s_last, s_wsum[64 * kCS / 32];
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) s_last = atomicAdd(&meta[8], 1u) == gridDim.x - 1u;
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    // rounds of NT coalesced totals: block scan of the round, carried across rounds
+    constexpr int NT = 64 * kCS;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    uint32_t carry = 0;
+    for (int r0 = 0; r0 < Tn; r0 += NT) {
+        const int i = r0 + int(threadIdx.x);
+        const uint32_t x = i < Tn ? __ldcg(tot + i) : 0u;
+        uint32_t inc = x;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t v = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += v;
+        }
+        if (lane == 31) s_wsum[wid] = inc;
+        __syncthreads();
+        uint32_t woff = 0, rsum = 0;
+#pragma unroll
+        for (int w = 0; w < NT / 32; ++w) {
+            const uint32_t y = s_wsum[w];
+            woff += w < wid ? y : 0u;
+            rsum += y;
+        }
+        if (i < Tn) starts[i] = carry + woff + inc - x;
+        carry += rsum;
+        __syncthreads();  // s_wsum is rewritten by the next round
+    }
+    if (threadIdx.x == 0) starts[Tn] = carry;
 }
 
 __global__ void __launch_bounds__(kBinThreads, TS_SC_MINB) bin_scatter_kernel(const uint4* __restrict__ rect,
@@ -591,25 +632,30 @@ bool launch_bin_count(Context& c, const DevCam& cam, const ts_render_config& cfg
                   200 * 1024);
     if (!c.bin_host) {
         if (cudaMallocHost(reinterpret_cast<void**>(&c.bin_host), 16 * sizeof(uint32_t)) != cudaSuccess ||
-            cudaEventCreateWithFlags(&c.bin_ev, cudaEventDisableTiming) != cudaSuccess)
+            cudaEventCreateWithFlags(&c.bin_ev, cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&c.bin_fork, cudaEventDisableTiming) != cudaSuccess)
             return false;
     }
     uint32_t* meta = c.bintot.p + Tn;
     cudaMemsetAsync(meta, 0, 16 * 4, c.stream);
     if (c.N > 0) {
         // H[chunk][tile] was accumulated by K1 (launch_preprocess)
-        bin_colscan_kernel<<<(Tn + 63) / 64, 64 * kCS, 0, c.stream>>>(c.binH.p, nch, Tn, c.bintot.p, meta);
+        // column prefixes, tile totals, class counts and (last CTA) the tile ranges
+        bin_colscan_kernel<<<(Tn + 63) / 64, 64 * kCS, 0, c.stream>>>(c.binH.p, nch, Tn, c.bintot.p, meta,
+                                                                        c.starts.p);
         TS_LAUNCHED(c);
     } else {
         cudaMemsetAsync(c.bintot.p, 0, size_t(Tn) * 4, c.stream);
+        launch_exclusive_scan(c, c.bintot.p, nullptr, c.starts.p, Tn);
     }
-    launch_exclusive_scan(c, c.bintot.p, nullptr, c.starts.p, Tn);
-    // I, the class counts and the longest list to pinned host memory; the host waits on this
-    // event only, so the scatter launched next overlaps the read-back
+    // I, the class counts and the longest list to pinned host memory, on a side stream (off the
+    // engine stream, where the copies delayed the scatter); the host waits on this event only
     if (c.gmode) return true;  // a captured step never reads the counts back
-    cudaMemcpyAsync(c.bin_host, c.starts.p + Tn, 4, cudaMemcpyDeviceToHost, c.stream);
-    cudaMemcpyAsync(c.bin_host + 1, meta, 8 * 4, cudaMemcpyDeviceToHost, c.stream);
-    cudaEventRecord(c.bin_ev, c.stream);
+    cudaEventRecord(c.bin_fork, c.stream);
+    cudaStreamWaitEvent(c.side[1], c.bin_fork, 0);
+    cudaMemcpyAsync(c.bin_host, c.starts.p + Tn, 4, cudaMemcpyDeviceToHost, c.side[1]);
+    cudaMemcpyAsync(c.bin_host + 1, meta, 8 * 4, cudaMemcpyDeviceToHost, c.side[1]);
+    cudaEventRecord(c.bin_ev, c.side[1]);
     return true;
 }
 

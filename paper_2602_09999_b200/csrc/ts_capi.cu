@@ -928,6 +928,7 @@ ts_status ts_destroy(ts_ctx* x) {
     if (c.copy_stream) cudaStreamDestroy(c.copy_stream);
     if (c.bin_host) cudaFreeHost(c.bin_host);
     if (c.bin_ev) cudaEventDestroy(c.bin_ev);
+    if (c.bin_fork) cudaEventDestroy(c.bin_fork);
     if (c.loss_host) cudaFreeHost(c.loss_host);
     if (c.loss_ev) cudaEventDestroy(c.loss_ev);
     if (c.copy_fork) cudaEventDestroy(c.copy_fork);

@@ -141,6 +141,7 @@ struct Context {
     bool bwd_order_ok = false;
     uint32_t* bin_host = nullptr;  // pinned read-back of (I, class counts, longest list)
     cudaEvent_t bin_ev = nullptr;
+    cudaEvent_t bin_fork = nullptr;  // counts ready on the engine stream (read back on side[1])
     DevBuf<float> nu_hat;        // sampling rates (antialias), N floats
     bool nu_valid = false;       // computed for the current ParameterStore rows
     uint32_t bin_class[7] = {0, 0, 0, 0, 0, 0, 0};  // tiles per per-tile sort size class (last view)

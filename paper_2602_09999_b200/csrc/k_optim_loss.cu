@@ -234,8 +234,8 @@ void launch_filter3d_clip(Context& c, float kappa3d) {
     TS_LAUNCHED(c);
 }
 
-void launch_hwc_to_chw(Context& c, const float* hwc, float* chw, int P) {
-    hwc_to_chw_kernel<<<(P + 255) / 256, 256, 0, c.stream>>>(hwc, chw, P);
+void launch_hwc_to_chw(Context& c, const float* hwc, float* chw, int P, cudaStream_t st) {
+    hwc_to_chw_kernel<<<(P + 255) / 256, 256, 0, st ? st : c.stream>>>(hwc, chw, P);
     TS_LAUNCHED(c);
 }
 

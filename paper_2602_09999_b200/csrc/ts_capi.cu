@@ -521,19 +521,20 @@ ts_status run_train_step(Context& c, const ts_camera& camr, const ts_render_conf
             CK(cudaEventCreateWithFlags(&c.copy_fork, cudaEventDisableTiming));
             CK(cudaEventCreateWithFlags(&c.copy_join, cudaEventDisableTiming));
         }
-        // copy_fork marks the previous step's last read of tgt_stage (its layout conversion,
-        // early in that step), so this upload starts at once instead of behind the previous
-        // step's backward and Adam (never recorded yet: the wait is a no-op)
-        CK(cudaStreamWaitEvent(c.copy_stream, c.copy_fork, 0));
+        // upload and layout conversion both on the copy stream, off the engine stream: the upload
+        // at once (tgt_stage was last read by the previous conversion, earlier on this stream),
+        // the conversion once the previous step's loss has consumed tgt (copy_fork; never
+        // recorded yet: the wait is a no-op)
         CK(cudaMemcpyAsync(c.tgt_stage.p, target_hwc, 3 * P * 4, cudaMemcpyHostToDevice, c.copy_stream));
+        CK(cudaStreamWaitEvent(c.copy_stream, c.copy_fork, 0));
+        launch_hwc_to_chw(c, c.tgt_stage.p, c.tgt.p, int(P), c.copy_stream);
         CK(cudaEventRecord(c.copy_join, c.copy_stream));
     }
     if (ts_status s = run_forward(c, *cam, *cfg); s != TS_OK) return s;
     if (target_hwc) {
         CK(cudaStreamWaitEvent(c.stream, c.copy_join, 0));
-        launch_hwc_to_chw(c, c.tgt_stage.p, c.tgt.p, int(P));
-        CK(cudaEventRecord(c.copy_fork, c.stream));  // tgt_stage free for the next upload
         if (ts_status s = run_loss(c, nullptr, slot, nullptr, c.tgt.p); s != TS_OK) return s;
+        CK(cudaEventRecord(c.copy_fork, c.stream));  // tgt consumed: the next conversion may overwrite it
     } else {
         if (ts_status s = run_loss(c, nullptr, slot, nullptr); s != TS_OK) return s;
     }

@@ -226,7 +226,7 @@ void launch_project_bwd(Context& c, const DevCam& cam, const ts_render_config& c
 void launch_project_bwd_adam(Context& c, const DevCam& cam, const ts_render_config& cfg, const ts_adam_config& a);
 void launch_adam(Context& c, const ts_adam_config& a, int64_t begin, int64_t end);
 size_t adam_args_bytes(const ts_adam_config& a, void* out);  // the kernel's argument block of a (<= 128 B)
-void launch_hwc_to_chw(Context& c, const float* hwc, float* chw, int P);
+void launch_hwc_to_chw(Context& c, const float* hwc, float* chw, int P, cudaStream_t st = nullptr);
 void launch_chw_to_hwc(Context& c, const float* chw, float* hwc, int P);
 void launch_opacity_reset(Context& c, float logit_max);
 bool launch_sampling_rates(Context& c, const DevCam* cams_host, int ncams, float extent);

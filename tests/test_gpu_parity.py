@@ -624,3 +624,29 @@ def test_per_gaussian_backward_matches_per_pixel_on_device(sc, engine):
         if nm == "sh_rest" and sc["cfg"].sh_degree == 0:
             continue
         _grad_check(grads[1][a:b], grads[0][a:b], nm, rtol=1e-4, frac=0.999)
+
+
+def test_host_target_steps_match_device_targets(engine):
+    """ts_train_step with a host target (upload and layout conversion on the copy stream, the
+    conversion gated by the previous step's loss) gives the losses of the same steps on
+    device-resident slot targets.  Learning rates 0 keep the parameters fixed, so every step's
+    loss depends only on its view and target; alternating views with different targets would
+    expose a conversion that overwrote the target under the previous step's loss."""
+    n = 20_000
+    gt = scene.random_params(n, 0.004, 0.0, 43)
+    cams = scene.fibonacci_cameras(2, 240, 160)
+    cfg = T.RenderConfig.make(sh_degree=3)
+    engine.set_params(gt, n)
+    tgts = [engine.render(c, cfg)[0] for c in cams]
+    p0 = scene.perturb(gt, n, 43)
+    seq = [0, 1, 0, 1, 1, 0, 1]
+    a0 = T.AdamConfig.make(step=1, lrs=[0.0] * 6)
+    engine.set_params(p0, n)
+    for s in range(2):
+        engine.set_target(s, tgts[s])
+    dev = [engine.train_step(cams[s], cfg, a0, slot=s) for s in seq]
+    engine.set_params(p0, n)
+    host = [engine.train_step(cams[s], cfg, a0, target=tgts[s]) for s in seq]
+    assert np.array_equal(engine.get_params(), p0)
+    np.testing.assert_allclose(host, dev, rtol=1e-9, atol=0)
+    assert abs(dev[0] - dev[1]) > 1e-6   # the two views' losses differ
